@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""bench.py -- ELLPACK X^2 multiply on B200 (BASELINE.json metric), one JSON line.
+
+Default workload (BASELINE.json configs[4], the largest single-GPU multiply, on
+which the north star's ">= 50% of HBM peak" target is stated):
+    cfg5: X^2 of a random banded symmetric X, N=262144, M=256, tau=1e-5, FP64.
+A "step" = one ellpack_multiply_x2 call (fused row kernel: window pre-pass,
+gather-accumulate, drop/compact/write, trace partials; canonical trace
+reduction; status read-back) -- SURVEY §8a rows a0..a4. With N>1 ranks a step
+is the NCCL all-gather of X's row blocks (BJ north_star (3)) followed by the
+multiply of the rank's own rows (strong scaling: total work fixed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload x2|spgemm|sp2] [--n N --m M]
+
+--impl reference times the CPU oracle (oracle/, the reference arm of this tier)
+on the host cores, on a bounded row sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+HBM_FALLBACK_GBS = 6650.0
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload: str):
+    """dram bytes per launch of the row kernel from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get(workload)
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 3 + k and r[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def live_entries(e) -> int:
+    return int(e.nnz.sum())
+
+
+def x2_bytes(nnz_x: int, nnz_c: int, n: int) -> int:
+    """Compulsory HBM bytes of one X^2: 12 B per stored input entry read once,
+    12 B per kept output entry written once, 4 B per row_nnz read and written."""
+    return 12 * (nnz_x + nnz_c) + 8 * n
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------- oracle arm
+
+def oracle_sample_rate(X, tau: float, budget_s: float):
+    """Time the oracle (as it stands) on a bounded row sample of the X^2 workload.
+    Returns (products/s, sample description, cores, seconds)."""
+    import oracle
+    from synth import Ell
+    n = X.n
+    rows = 256
+    rng = np.random.default_rng(0)
+    while True:
+        idx = np.sort(rng.choice(n, size=min(rows, n), replace=False))
+        A = Ell.empty(n, X.w)
+        A.val[idx] = X.val[idx]
+        A.col[idx] = X.col[idx]
+        A.nnz[idx] = X.nnz[idx]
+        P = synth.products(A, X)
+        Y = Ell.empty(n, 8 * X.w if n > 8 * X.w else n + (n & 1))
+        t0 = time.perf_counter()
+        oracle.multiply(A, X, Y, 1.0, 0.0, tau)
+        dt = time.perf_counter() - t0
+        if dt > budget_s / 4 or rows >= n:
+            return P / dt, f"{len(idx)} uniformly sampled rows of the same X^2 ({P} products)", oracle.num_threads(), dt
+        rows = min(n, int(rows * max(2.0, (budget_s / 2) / max(dt, 1e-3))))
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    X = synth.cfg5(args.n, args.m)
+    P = synth.products(X, X)
+    times = []
+    rate = None
+    desc = ""
+    cores = 0
+    for _ in range(args.warmup + args.steps):
+        rate, desc, cores, dt = oracle_sample_rate(X, 1e-5, args.ref_budget)
+        times.append(dt)
+    gflops = 2.0 * rate / 1e9
+    line = {
+        "impl": "reference", "metric": "ELLPACK X^2 multiply GFLOP/s", "value": gflops, "unit": "GFLOP/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * 2.0 * P / (gflops * 1e9), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth.cfg5, seed 5)",
+        "config": {"workload": f"cfg5 X^2 N={args.n} M={args.m} tau=1e-5", "products": P},
+        "cpu_baseline": {"value": gflops, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": gflops, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2102_08505_b200 as eb
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    eb.build()
+    ctx = eb.Context(dev)
+    if args.window:
+        ctx.set_option(eb.OPT_WINDOW, args.window)
+    if args.warps:
+        ctx.set_option(eb.OPT_WARPS, args.warps)
+    if ws > 1:
+        uid = [eb.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        r0, r1 = eb.row_partition(args.n, ws)[rank]
+        ctx.attach_nccl(ws, rank, uid[0], r0, r1)
+    tau = 1e-5
+    X = synth.cfg5(args.n, args.m)
+    n = X.n
+    P = synth.products(X, X)
+    x = eb.Mat.from_host(X)
+    # reading R2: the literal width M overflows; the first call reports the required width
+    y = eb.Mat.empty(n, args.m)
+    st, _, _ = ctx.multiply_x2(x, y, tau)
+    assert st == eb.ERR_OVERFLOW
+    _, req = ctx.overflow_info()
+    w_out = ((req + 31) // 32) * 32
+    del y
+    y = eb.Mat.empty(n, w_out)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if ws > 1:
+            ctx.allgather_rows(x)
+        s, tx, tx2 = ctx.multiply_x2(x, y, tau)
+        return s, tx, tx2
+
+    for _ in range(max(3, args.warmup)):
+        s, tx, tx2 = step()
+        assert s == eb.OK
+    nnz_c = int(y.nnz.sum().item())
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.kernel_launches()
+    ctx.set_option(eb.OPT_PROFILE, 1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms_total = e0.elapsed_time(e1)
+    kern_ms, kern_n = ctx.kernel_time()
+    ctx.set_option(eb.OPT_PROFILE, 0)
+    launches = ctx.kernel_launches() - launches0
+    if ws > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        dist.barrier()
+    ms_step = ms_total / args.steps
+    gflops = 2.0 * P / (ms_step * 1e-3) / 1e9
+    Bc = x2_bytes(live_entries(X), nnz_c, n)
+    hbm_peak, peak_src = peaks()
+    kern_avg = kern_ms / max(kern_n, 1)
+    rows_local = (n // ws)
+    bytes_launch = Bc * rows_local / n if ws > 1 else Bc
+    achieved = bytes_launch / (kern_avg * 1e-3) / 1e9
+    traffic = ncu_traffic(f"x2_n{n}_m{args.m}")
+
+    # ---- end to end through the host-buffer ABI call (H2D of X + kernels + D2H of X^2)
+    e2e = None
+    if not args.no_e2e and ws == 1:
+        hx = {k: torch.from_numpy(getattr(X, k)).pin_memory() for k in ("val", "col", "nnz")}
+        hy = {"val": torch.empty((n, w_out), dtype=torch.float64).pin_memory(),
+              "col": torch.empty((n, w_out), dtype=torch.int32).pin_memory(),
+              "nnz": torch.empty((n,), dtype=torch.int32).pin_memory()}
+
+        class _H:
+            pass
+        hxo, hyo = _H(), _H()
+        for k in hx:
+            setattr(hxo, k, hx[k])
+            setattr(hyo, k, hy[k])
+        del y
+        torch.cuda.empty_cache()
+        ctx.multiply_x2_host(hxo, hyo, tau)  # warm (allocates the device scratch)
+        torch.cuda.synchronize()
+        k_e2e = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            ctx.multiply_x2_host(hxo, hyo, tau)
+        dt = (time.perf_counter() - t0) / k_e2e
+        h2d = sum(t.numel() * t.element_size() for t in hx.values())
+        d2h = sum(t.numel() * t.element_size() for t in hy.values())
+        e2e = {"value": 2.0 * P / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3}
+
+    # ---- CPU oracle beside it (rank 0, N=1 only, bounded sample)
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1 and rank == 0:
+        rate, desc, cores, _ = oracle_sample_rate(X, tau, args.ref_budget)
+        cpu = {"value": 2.0 * rate / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": "ELLPACK X^2 multiply GFLOP/s", "value": gflops, "unit": "GFLOP/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (synth.cfg5, seed 5; BASELINE configs[4] recipe, SURVEY §8d)",
+            "config": {"workload": f"cfg5 X^2 N={n} M={args.m} tau={tau}", "products": P,
+                       "out_width": w_out, "nnz_x": live_entries(X), "nnz_x2": nnz_c,
+                       "l2": "inputs larger than L2 (X 0.8 GB padded, X^2 16 GB)",
+                       "parallelism": f"row-blocks x{ws}" if ws > 1 else "1 GPU"},
+            "hbm_gbs_algorithmic": Bc / (ms_step * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "ell::row_op_kernel", "kernel_ms_avg": kern_avg,
+                         "algorithmic_bytes_per_launch": bytes_launch},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=262144)
+    ap.add_argument("--m", type=int, default=256)
+    ap.add_argument("--window", type=int, default=0, help="dense-window doubles per row (0 = auto)")
+    ap.add_argument("--warps", type=int, default=0, help="warps per CTA (0 = auto)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=20.0, help="seconds of oracle work per sample")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

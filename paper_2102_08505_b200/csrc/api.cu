@@ -1,0 +1,949 @@
+// api.cu — the C ABI of libellpack (include/ellpack.h): context, validation, the
+// ELLPACK ops, the SP2-Basic driver and the NCCL row-block exchange.
+//
+// Every op is one launch of the fused row kernel (spgemm.cu) plus, where traces
+// are returned, the canonical block-sum kernels (reduce.cu):
+//   multiply            A x B,  Old = C (beta != 0), C in place
+//   multiply_x2         X x X,  diag_a/diag_s -> tr(X), tr(X^2)
+//   add                 A x I,  Old = B (old_mode 1), C = A in place   -> fma(alpha, a, beta*b)
+//   (scale_)add_identity A x I, Old = I                                -> fma(alpha, a_ii, beta)
+//   sp2 step            X x X,  Old = X, C = X_{n+1}                   (BJ north_star (2))
+// A x I reproduces a exactly (fma(a, 1, +0) = a), so add/identity share the
+// kernel's single-rounding combine instead of a second code path.
+#include "internal.cuh"
+#include "../../include/ellpack.h"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+using namespace ell;
+
+namespace {
+
+struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+// NCCL entry points resolved at attach time (torch's libnccl.so.2), so the
+// library loads on machines without NCCL.
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+};
+
+NcclApi g_nccl;
+
+bool load_nccl() {
+    if (g_nccl.ok) return true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        const char* envp = getenv("ELLPACK_NCCL_LIB");
+        if (envp) h = dlopen(envp, RTLD_NOW | RTLD_GLOBAL);
+    }
+    if (!h) return false;
+#define LOADSYM(field, name) g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name)); \
+    if (!g_nccl.field) return false;
+    LOADSYM(GetUniqueId, "ncclGetUniqueId");
+    LOADSYM(CommInitRank, "ncclCommInitRank");
+    LOADSYM(CommDestroy, "ncclCommDestroy");
+    LOADSYM(AllGather, "ncclAllGather");
+    LOADSYM(AllReduce, "ncclAllReduce");
+    LOADSYM(GroupStart, "ncclGroupStart");
+    LOADSYM(GroupEnd, "ncclGroupEnd");
+#undef LOADSYM
+    g_nccl.ok = true;
+    return true;
+}
+
+}  // namespace
+
+struct ellpack_ctx_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    int window_opt = 0, warps_opt = 0, sp2_width0 = 0;
+    int64_t launches = 0;
+    // small device/pinned blocks
+    int32_t* d_status = nullptr;              // [0] ovf rows, [1] max kept
+    unsigned long long* d_keys = nullptr;     // gershgorin min/max keys
+    double* d_sums = nullptr;                 // final sums (<= 8)
+    struct Host {
+        int32_t status[2];
+        unsigned long long keys[2];
+        double sums[8];
+        int32_t imax;
+    }* h = nullptr;
+    // workspace
+    Buf rows[4];      // per-row double arrays
+    Buf partials;     // canonical block partials
+    Buf cursors, stash_val, stash_col;
+    Buf ident_val, ident_col, ident_nnz;
+    int64_t ident_n = 0;
+    Buf hx_val, hx_col, hx_nnz, hy_val, hy_col, hy_nnz;  // host-path device copies
+    // overflow info of the last OVERFLOW
+    int64_t last_ovf_rows = 0;
+    int32_t last_req = 0;
+    // row partition
+    int64_t row_begin = 0, row_end = -1;
+    int nranks = 1, rank = 0;
+    ncclComm_t comm = nullptr;
+    cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    // row-kernel profiling (ELLPACK_OPT_PROFILE)
+    bool profile = false, prof_pending = false;
+    double prof_ms = 0.0;
+    int64_t prof_launches = 0;
+};
+
+namespace {
+
+int from_cuda(cudaError_t e) {
+    if (e == cudaSuccess) return ELLPACK_OK;
+    if (e == cudaErrorMemoryAllocation) return ELLPACK_ERR_NOMEM;
+    return ELLPACK_ERR_CUDA;
+}
+
+#define CK(x)                                  \
+    do {                                       \
+        cudaError_t e_ = (x);                  \
+        if (e_ != cudaSuccess) return from_cuda(e_); \
+    } while (0)
+#define RK(x)                                  \
+    do {                                       \
+        int r_ = (x);                          \
+        if (r_ != ELLPACK_OK) return r_;       \
+    } while (0)
+#define NK(x)                                  \
+    do {                                       \
+        if ((x) != ncclSuccess) return ELLPACK_ERR_NCCL; \
+    } while (0)
+
+int grow(ellpack_ctx c, Buf& b, size_t bytes) {
+    if (b.bytes >= bytes) return ELLPACK_OK;
+    if (b.p) CK(cudaFreeAsync(b.p, c->stream));
+    b.p = nullptr;
+    b.bytes = 0;
+    size_t want = bytes + bytes / 8 + 256;
+    CK(cudaMallocAsync(&b.p, want, c->stream));
+    b.bytes = want;
+    return ELLPACK_OK;
+}
+
+void release(ellpack_ctx c, Buf& b) {
+    if (b.p) cudaFreeAsync(b.p, c->stream);
+    b.p = nullptr;
+    b.bytes = 0;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int check_desc(const ellpack_desc* d) {
+    if (!d || d->n <= 0 || d->w <= 0 || (d->w & 1) || !d->val || !d->col || !d->nnz)
+        return ELLPACK_ERR_ARG;
+    if (d->n > INT32_MAX) return ELLPACK_ERR_ARG;
+    if (!aligned16(d->val) || !aligned16(d->col) || (reinterpret_cast<uintptr_t>(d->nnz) & 3))
+        return ELLPACK_ERR_ARG;
+    return ELLPACK_OK;
+}
+
+bool valid_tau(double t) { return t >= 0.0 && std::isfinite(t); }
+
+KMat kmat(const ellpack_desc* d) { return KMat{d->val, d->col, d->nnz, d->w}; }
+KOut kout(const ellpack_desc* d) { return KOut{d->val, d->col, d->nnz, d->w}; }
+
+bool same(const ellpack_desc* a, const ellpack_desc* b) {
+    return a->val == b->val || a->col == b->col || a->nnz == b->nnz;
+}
+
+void rows_of(ellpack_ctx c, int64_t n, int64_t* r0, int64_t* r1) {
+    if (c->row_end < 0) { *r0 = 0; *r1 = n; }
+    else { *r0 = c->row_begin < n ? c->row_begin : n; *r1 = c->row_end < n ? c->row_end : n; }
+}
+
+int ensure_identity(ellpack_ctx c, int64_t n) {
+    if (c->ident_n >= n) return ELLPACK_OK;
+    RK(grow(c, c->ident_val, sizeof(double) * 2 * n));
+    RK(grow(c, c->ident_col, sizeof(int32_t) * 2 * n));
+    RK(grow(c, c->ident_nnz, sizeof(int32_t) * n));
+    CK(launch_identity(n, KOut{(double*)c->ident_val.p, (int32_t*)c->ident_col.p,
+                               (int32_t*)c->ident_nnz.p, 2}, c->stream));
+    c->launches++;
+    c->ident_n = n;
+    return ELLPACK_OK;
+}
+
+KMat identity(ellpack_ctx c) {
+    return KMat{(const double*)c->ident_val.p, (const int32_t*)c->ident_col.p,
+                (const int32_t*)c->ident_nnz.p, 2};
+}
+
+// all-reduce of the status block (sum overflow rows, max kept) over the comm
+int reduce_status(ellpack_ctx c) {
+    if (!c->comm) return ELLPACK_OK;
+    NK(g_nccl.GroupStart());
+    NK(g_nccl.AllReduce(c->d_status, c->d_status, 1, ncclInt32, ncclSum, c->comm, c->stream));
+    NK(g_nccl.AllReduce(c->d_status + 1, c->d_status + 1, 1, ncclInt32, ncclMax, c->comm, c->stream));
+    NK(g_nccl.GroupEnd());
+    return ELLPACK_OK;
+}
+
+// Enqueue one row op (kernel + scratch management). Status is left in d_status.
+int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
+    LaunchCfg cfg;
+    int window = c->window_opt;
+    if (window <= 0) {
+        window = 4096;
+        int64_t nr = (n + 31) & ~int64_t(31);
+        if (nr < window) window = (int)nr;
+    }
+    CK(plan_row_op(p, window, c->warps_opt, c->num_sms, &cfg));
+    p.S = cfg.S;
+    const int64_t total_warps = (int64_t)cfg.grid * cfg.warps_per_cta;
+    const bool may_multi = n > cfg.S;
+    if (may_multi) {
+        p.cur_stride = p.A.w;
+        RK(grow(c, c->cursors, sizeof(int32_t) * (size_t)total_warps * p.cur_stride));
+        p.cursors = (int32_t*)c->cursors.p;
+        if (p.stash_a || p.stash_old) {
+            p.st_stride = (p.stash_a ? p.A.w : 0) + (p.stash_old ? p.Old.w : 0);
+            RK(grow(c, c->stash_val, sizeof(double) * (size_t)total_warps * p.st_stride));
+            RK(grow(c, c->stash_col, sizeof(int32_t) * (size_t)total_warps * p.st_stride));
+            p.st_val = (double*)c->stash_val.p;
+            p.st_col = (int32_t*)c->stash_col.p;
+        }
+    }
+    p.status = c->d_status;
+    CK(cudaMemsetAsync(c->d_status, 0, 2 * sizeof(int32_t), c->stream));
+    if (c->profile) CK(cudaEventRecord(c->ev[4], c->stream));
+    CK(launch_row_op(p, cfg, c->stream));
+    if (c->profile) {
+        CK(cudaEventRecord(c->ev[5], c->stream));
+        c->prof_pending = true;
+    }
+    c->launches++;
+    return ELLPACK_OK;
+}
+
+// called after a stream sync: fold the pending row-kernel event pair into the profile
+void prof_collect(ellpack_ctx c) {
+    if (!c->prof_pending) return;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]) == cudaSuccess) {
+        c->prof_ms += ms;
+        c->prof_launches++;
+    }
+    c->prof_pending = false;
+}
+
+// Canonical sums of `narr` per-row arrays over all n rows (partials exchanged over ranks).
+int enqueue_canonical(ellpack_ctx c, const double* const* arrays, int narr, int64_t n) {
+    int64_t r0, r1;
+    rows_of(c, n, &r0, &r1);
+    const int64_t nb = (n + kTraceBlock - 1) / kTraceBlock;
+    RK(grow(c, c->partials, sizeof(double) * (size_t)nb * narr));
+    double* part = (double*)c->partials.p;
+    CK(launch_block_partials(arrays, narr, r0, r1, n, part, c->stream));
+    c->launches++;
+    if (c->comm) {
+        const int64_t per = (r1 - r0) / kTraceBlock;  // equal 256-aligned blocks (checked at attach)
+        NK(g_nccl.GroupStart());
+        for (int a = 0; a < narr; ++a) {
+            double* base = part + (size_t)a * nb;
+            NK(g_nccl.AllGather(base + (size_t)c->rank * per, base, (size_t)per, ncclFloat64, c->comm,
+                                c->stream));
+        }
+        NK(g_nccl.GroupEnd());
+    }
+    CK(launch_final_sums(part, narr, nb, c->d_sums, c->stream));
+    c->launches++;
+    return ELLPACK_OK;
+}
+
+int fetch(ellpack_ctx c, int nsums) {
+    CK(cudaMemcpyAsync(c->h->status, c->d_status, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    if (nsums > 0)
+        CK(cudaMemcpyAsync(c->h->sums, c->d_sums, nsums * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    prof_collect(c);
+    return ELLPACK_OK;
+}
+
+int finish_status(ellpack_ctx c) {
+    if (c->h->status[0] > 0) {
+        c->last_ovf_rows = c->h->status[0];
+        c->last_req = c->h->status[1];
+        return ELLPACK_ERR_OVERFLOW;
+    }
+    return ELLPACK_OK;
+}
+
+RowOpParams base_params(ellpack_ctx c, int64_t n) {
+    RowOpParams p;
+    memset(&p, 0, sizeof p);
+    rows_of(c, n, &p.row_begin, &p.row_end);
+    return p;
+}
+
+int allgather_desc(ellpack_ctx c, const ellpack_desc* m) {
+    if (!c->comm) return ELLPACK_OK;
+    int64_t r0, r1;
+    rows_of(c, m->n, &r0, &r1);
+    const size_t per = (size_t)(r1 - r0);
+    const size_t w = (size_t)m->w;
+    NK(g_nccl.GroupStart());
+    NK(g_nccl.AllGather(m->val + (size_t)r0 * w, m->val, per * w, ncclFloat64, c->comm, c->stream));
+    NK(g_nccl.AllGather(m->col + (size_t)r0 * w, m->col, per * w, ncclInt32, c->comm, c->stream));
+    NK(g_nccl.AllGather(m->nnz + r0, m->nnz, per, ncclInt32, c->comm, c->stream));
+    NK(g_nccl.GroupEnd());
+    return ELLPACK_OK;
+}
+
+}  // namespace
+
+// =========================================================================== ABI
+
+extern "C" {
+
+const char* ellpack_strerror(int s) {
+    switch (s) {
+        case ELLPACK_OK: return "ok";
+        case ELLPACK_ERR_ARG: return "invalid argument";
+        case ELLPACK_ERR_DIM: return "dimension mismatch";
+        case ELLPACK_ERR_OVERFLOW: return "output row exceeds ELLPACK width";
+        case ELLPACK_ERR_BOUNDS: return "degenerate spectral bounds";
+        case ELLPACK_ERR_NOCONV: return "SP2 did not converge within max_iter";
+        case ELLPACK_ERR_NOMEM: return "device allocation failed";
+        case ELLPACK_ERR_CUDA: return "CUDA error";
+        case ELLPACK_ERR_NCCL: return "NCCL error";
+        case ELLPACK_ERR_STATE: return "invalid context state";
+        default: return "unknown status";
+    }
+}
+
+int ellpack_ctx_create(int device, void* stream, ellpack_ctx* out) {
+    if (!out) return ELLPACK_ERR_ARG;
+    *out = nullptr;
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return ELLPACK_ERR_ARG;
+    CK(cudaSetDevice(device));
+    ellpack_ctx c = new (std::nothrow) ellpack_ctx_s();
+    if (!c) return ELLPACK_ERR_NOMEM;
+    c->device = device;
+    c->stream = (cudaStream_t)stream;
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    cudaError_t e = cudaMalloc(&c->d_status, 64);
+    if (!e) e = cudaMalloc(&c->d_keys, 64);
+    if (!e) e = cudaMalloc(&c->d_sums, 64);
+    if (!e) e = cudaMallocHost(&c->h, sizeof(ellpack_ctx_s::Host));
+    for (int k = 0; k < 6 && !e; ++k) e = cudaEventCreate(&c->ev[k]);
+    if (e) { ellpack_ctx_destroy(c); return from_cuda(e); }
+    *out = c;
+    return ELLPACK_OK;
+}
+
+int ellpack_ctx_destroy(ellpack_ctx c) {
+    if (!c) return ELLPACK_ERR_ARG;
+    cudaSetDevice(c->device);
+    Buf* bufs[] = {&c->rows[0], &c->rows[1], &c->rows[2], &c->rows[3], &c->partials, &c->cursors,
+                   &c->stash_val, &c->stash_col, &c->ident_val, &c->ident_col, &c->ident_nnz,
+                   &c->hx_val, &c->hx_col, &c->hx_nnz, &c->hy_val, &c->hy_col, &c->hy_nnz};
+    for (Buf* b : bufs) release(c, *b);
+    cudaStreamSynchronize(c->stream);
+    if (c->comm && g_nccl.ok) g_nccl.CommDestroy(c->comm);
+    cudaFree(c->d_status);
+    cudaFree(c->d_keys);
+    cudaFree(c->d_sums);
+    if (c->h) cudaFreeHost(c->h);
+    for (int k = 0; k < 6; ++k) if (c->ev[k]) cudaEventDestroy(c->ev[k]);
+    delete c;
+    return ELLPACK_OK;
+}
+
+int ellpack_ctx_set_stream(ellpack_ctx c, void* stream) {
+    if (!c) return ELLPACK_ERR_ARG;
+    c->stream = (cudaStream_t)stream;
+    return ELLPACK_OK;
+}
+
+int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
+    if (!c || v < 0) return ELLPACK_ERR_ARG;
+    switch (key) {
+        case ELLPACK_OPT_WINDOW: c->window_opt = (int)v; return ELLPACK_OK;
+        case ELLPACK_OPT_WARPS: c->warps_opt = (int)v; return ELLPACK_OK;
+        case ELLPACK_OPT_SP2_WIDTH0: c->sp2_width0 = (int)v; return ELLPACK_OK;
+        case ELLPACK_OPT_PROFILE:
+            c->profile = v != 0;
+            c->prof_ms = 0.0;
+            c->prof_launches = 0;
+            c->prof_pending = false;
+            return ELLPACK_OK;
+        default: return ELLPACK_ERR_ARG;
+    }
+}
+
+int64_t ellpack_ctx_kernel_launches(ellpack_ctx c) { return c ? c->launches : -1; }
+
+int ellpack_ctx_kernel_time(ellpack_ctx c, double* ms, int64_t* launches) {
+    if (!c) return ELLPACK_ERR_ARG;
+    if (ms) *ms = c->prof_ms;
+    if (launches) *launches = c->prof_launches;
+    return ELLPACK_OK;
+}
+
+int ellpack_ctx_set_rows(ellpack_ctx c, int64_t r0, int64_t r1) {
+    if (!c || r0 < 0 || (r1 >= 0 && r1 < r0)) return ELLPACK_ERR_ARG;
+    if (c->comm) return ELLPACK_ERR_STATE;
+    c->row_begin = r0;
+    c->row_end = r1;
+    return ELLPACK_OK;
+}
+
+int ellpack_create(ellpack_ctx c, int64_t n, int32_t m, ellpack_desc* out) {
+    if (!c || !out || n <= 0 || n > INT32_MAX || m <= 0 || (m & 1)) return ELLPACK_ERR_ARG;
+    CK(cudaSetDevice(c->device));
+    ellpack_desc d{};
+    d.n = n;
+    d.w = m;
+    const size_t cells = (size_t)n * (size_t)m;
+    cudaError_t e = cudaMallocAsync((void**)&d.val, cells * sizeof(double), c->stream);
+    if (!e) e = cudaMallocAsync((void**)&d.col, cells * sizeof(int32_t), c->stream);
+    if (!e) e = cudaMallocAsync((void**)&d.nnz, (size_t)n * sizeof(int32_t), c->stream);
+    if (!e) e = cudaMemsetAsync(d.nnz, 0, (size_t)n * sizeof(int32_t), c->stream);
+    if (!e) e = cudaMemsetAsync(d.val, 0, cells * sizeof(double), c->stream);
+    if (!e) e = cudaMemsetAsync(d.col, 0, cells * sizeof(int32_t), c->stream);
+    if (e) {
+        if (d.val) cudaFreeAsync(d.val, c->stream);
+        if (d.col) cudaFreeAsync(d.col, c->stream);
+        if (d.nnz) cudaFreeAsync(d.nnz, c->stream);
+        return from_cuda(e);
+    }
+    *out = d;
+    return ELLPACK_OK;
+}
+
+int ellpack_destroy(ellpack_ctx c, ellpack_desc* d) {
+    if (!c || !d) return ELLPACK_ERR_ARG;
+    if (d->val) cudaFreeAsync(d->val, c->stream);
+    if (d->col) cudaFreeAsync(d->col, c->stream);
+    if (d->nnz) cudaFreeAsync(d->nnz, c->stream);
+    memset(d, 0, sizeof *d);
+    return ELLPACK_OK;
+}
+
+int ellpack_overflow_info(ellpack_ctx c, int64_t* rows, int32_t* req) {
+    if (!c) return ELLPACK_ERR_ARG;
+    if (rows) *rows = c->last_ovf_rows;
+    if (req) *req = c->last_req;
+    return ELLPACK_OK;
+}
+
+int ellpack_multiply(ellpack_ctx c, const ellpack_desc* a, const ellpack_desc* b, ellpack_desc* cm,
+                     double alpha, double beta, double tau) {
+    if (!c) return ELLPACK_ERR_ARG;
+    RK(check_desc(a));
+    RK(check_desc(b));
+    RK(check_desc(cm));
+    if (a->n != b->n || a->n != cm->n) return ELLPACK_ERR_DIM;
+    if (!valid_tau(tau) || !std::isfinite(alpha) || !std::isfinite(beta)) return ELLPACK_ERR_ARG;
+    if (same(cm, a) || same(cm, b)) return ELLPACK_ERR_ARG;
+    CK(cudaSetDevice(c->device));
+    RowOpParams p = base_params(c, a->n);
+    p.A = kmat(a);
+    p.B = kmat(b);
+    p.C = kout(cm);
+    p.alpha = alpha;
+    p.beta = beta;
+    p.tau = tau;
+    if (beta != 0.0) {
+        p.old_mode = 1;
+        p.Old = kmat(cm);
+        p.stash_old = 1;
+    }
+    RK(enqueue_row_op(c, p, a->n));
+    RK(reduce_status(c));
+    RK(fetch(c, 0));
+    return finish_status(c);
+}
+
+int ellpack_multiply_x2(ellpack_ctx c, const ellpack_desc* x, ellpack_desc* x2, double tau,
+                        double* trace_x, double* trace_x2) {
+    if (!c) return ELLPACK_ERR_ARG;
+    RK(check_desc(x));
+    RK(check_desc(x2));
+    if (x->n != x2->n) return ELLPACK_ERR_DIM;
+    if (!valid_tau(tau)) return ELLPACK_ERR_ARG;
+    if (same(x, x2)) return ELLPACK_ERR_ARG;
+    CK(cudaSetDevice(c->device));
+    const int64_t n = x->n;
+    RK(grow(c, c->rows[0], sizeof(double) * n));
+    RK(grow(c, c->rows[1], sizeof(double) * n));
+    RowOpParams p = base_params(c, n);
+    p.A = kmat(x);
+    p.B = kmat(x);
+    p.C = kout(x2);
+    p.alpha = 1.0;
+    p.beta = 0.0;
+    p.tau = tau;
+    p.diag_a = (double*)c->rows[0].p;
+    p.diag_s = (double*)c->rows[1].p;
+    RK(enqueue_row_op(c, p, n));
+    const double* arrs[2] = {p.diag_a, p.diag_s};
+    RK(enqueue_canonical(c, arrs, 2, n));
+    RK(reduce_status(c));
+    RK(fetch(c, 2));
+    RK(finish_status(c));
+    if (trace_x) *trace_x = c->h->sums[0];
+    if (trace_x2) *trace_x2 = c->h->sums[1];
+    return ELLPACK_OK;
+}
+
+static int add_via_identity(ellpack_ctx c, ellpack_desc* a, const KMat& old, bool old_is_a,
+                            double alpha, double beta, double tau) {
+    CK(cudaSetDevice(c->device));
+    RK(ensure_identity(c, a->n));
+    RowOpParams p = base_params(c, a->n);
+    p.A = kmat(a);
+    p.B = identity(c);
+    p.Old = old;
+    p.old_mode = 1;
+    p.C = kout(a);
+    p.alpha = alpha;
+    p.beta = beta;
+    p.tau = tau;
+    p.stash_a = 1;
+    p.stash_old = old_is_a ? 1 : 0;
+    RK(enqueue_row_op(c, p, a->n));
+    RK(reduce_status(c));
+    RK(fetch(c, 0));
+    return finish_status(c);
+}
+
+int ellpack_add(ellpack_ctx c, ellpack_desc* a, const ellpack_desc* b, double alpha, double beta,
+                double tau) {
+    if (!c) return ELLPACK_ERR_ARG;
+    RK(check_desc(a));
+    RK(check_desc(b));
+    if (a->n != b->n) return ELLPACK_ERR_DIM;
+    if (!valid_tau(tau) || !std::isfinite(alpha) || !std::isfinite(beta)) return ELLPACK_ERR_ARG;
+    const bool ident = a->val == b->val && a->col == b->col && a->nnz == b->nnz && a->w == b->w;
+    if (!ident && same(a, b)) return ELLPACK_ERR_ARG;  // partial aliasing
+    return add_via_identity(c, a, kmat(b), ident, alpha, beta, tau);
+}
+
+int ellpack_scale_add_identity(ellpack_ctx c, ellpack_desc* a, double alpha, double beta, double tau) {
+    if (!c) return ELLPACK_ERR_ARG;
+    RK(check_desc(a));
+    if (!valid_tau(tau) || !std::isfinite(alpha) || !std::isfinite(beta)) return ELLPACK_ERR_ARG;
+    CK(cudaSetDevice(c->device));
+    RK(ensure_identity(c, a->n));
+    return add_via_identity(c, a, identity(c), false, alpha, beta, tau);
+}
+
+int ellpack_add_identity(ellpack_ctx c, ellpack_desc* a, double beta, double tau) {
+    return ellpack_scale_add_identity(c, a, 1.0, beta, tau);
+}
+
+int ellpack_trace(ellpack_ctx c, const ellpack_desc* a, double* out) {
+    if (!c || !out) return ELLPACK_ERR_ARG;
+    RK(check_desc(a));
+    CK(cudaSetDevice(c->device));
+    const int64_t n = a->n;
+    RK(grow(c, c->rows[0], sizeof(double) * n));
+    int64_t r0, r1;
+    rows_of(c, n, &r0, &r1);
+    CK(launch_stored_diag(kmat(a), r0, r1, (double*)c->rows[0].p, c->stream));
+    c->launches++;
+    const double* arrs[1] = {(const double*)c->rows[0].p};
+    RK(enqueue_canonical(c, arrs, 1, n));
+    CK(cudaMemsetAsync(c->d_status, 0, 8, c->stream));
+    RK(fetch(c, 1));
+    *out = c->h->sums[0];
+    return ELLPACK_OK;
+}
+
+int ellpack_fnorm_diff(ellpack_ctx c, const ellpack_desc* a, const ellpack_desc* b, double* out) {
+    if (!c || !out) return ELLPACK_ERR_ARG;
+    RK(check_desc(a));
+    RK(check_desc(b));
+    if (a->n != b->n) return ELLPACK_ERR_DIM;
+    CK(cudaSetDevice(c->device));
+    const int64_t n = a->n;
+    RK(grow(c, c->rows[0], sizeof(double) * n));
+    int64_t r0, r1;
+    rows_of(c, n, &r0, &r1);
+    CK(launch_fnorm_rows(kmat(a), kmat(b), r0, r1, (double*)c->rows[0].p, c->stream));
+    c->launches++;
+    const double* arrs[1] = {(const double*)c->rows[0].p};
+    RK(enqueue_canonical(c, arrs, 1, n));
+    CK(cudaMemsetAsync(c->d_status, 0, 8, c->stream));
+    RK(fetch(c, 1));
+    *out = std::sqrt(c->h->sums[0]);
+    return ELLPACK_OK;
+}
+
+static int gershgorin_impl(ellpack_ctx c, const ellpack_desc* h, double* emin, double* emax) {
+    const int64_t n = h->n;
+    int64_t r0, r1;
+    rows_of(c, n, &r0, &r1);
+    const unsigned long long init[2] = {~0ull, 0ull};
+    c->h->keys[0] = init[0];
+    c->h->keys[1] = init[1];
+    CK(cudaMemcpyAsync(c->d_keys, c->h->keys, 16, cudaMemcpyHostToDevice, c->stream));
+    CK(launch_gershgorin(kmat(h), r0, r1, c->d_keys, c->stream));
+    c->launches++;
+    if (c->comm) {
+        NK(g_nccl.GroupStart());
+        NK(g_nccl.AllReduce(c->d_keys, c->d_keys, 1, ncclUint64, ncclMin, c->comm, c->stream));
+        NK(g_nccl.AllReduce(c->d_keys + 1, c->d_keys + 1, 1, ncclUint64, ncclMax, c->comm, c->stream));
+        NK(g_nccl.GroupEnd());
+    }
+    CK(cudaMemcpyAsync(c->h->keys, c->d_keys, 16, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *emin = dkey_inv(c->h->keys[0]);
+    *emax = dkey_inv(c->h->keys[1]);
+    return ELLPACK_OK;
+}
+
+int ellpack_gershgorin(ellpack_ctx c, const ellpack_desc* h, double* emin, double* emax) {
+    if (!c || !emin || !emax) return ELLPACK_ERR_ARG;
+    RK(check_desc(h));
+    CK(cudaSetDevice(c->device));
+    return gershgorin_impl(c, h, emin, emax);
+}
+
+int ellpack_allgather_rows(ellpack_ctx c, ellpack_desc* m) {
+    if (!c) return ELLPACK_ERR_ARG;
+    RK(check_desc(m));
+    return allgather_desc(c, m);
+}
+
+int ellpack_nccl_unique_id(uint8_t id[128]) {
+    if (!id) return ELLPACK_ERR_ARG;
+    if (!load_nccl()) return ELLPACK_ERR_NCCL;
+    ncclUniqueId u;
+    NK(g_nccl.GetUniqueId(&u));
+    memcpy(id, &u, 128);
+    return ELLPACK_OK;
+}
+
+int ellpack_ctx_attach_nccl(ellpack_ctx c, int nranks, int rank, const uint8_t id[128],
+                            int64_t row_begin, int64_t row_end) {
+    if (!c || !id || nranks < 1 || rank < 0 || rank >= nranks || row_begin < 0 || row_end < row_begin)
+        return ELLPACK_ERR_ARG;
+    if (row_begin % kTraceBlock) return ELLPACK_ERR_ARG;
+    if (c->comm) return ELLPACK_ERR_STATE;
+    if (!load_nccl()) return ELLPACK_ERR_NCCL;
+    CK(cudaSetDevice(c->device));
+    ncclUniqueId u;
+    memcpy(&u, id, 128);
+    NK(g_nccl.CommInitRank(&c->comm, nranks, u, rank));
+    c->nranks = nranks;
+    c->rank = rank;
+    c->row_begin = row_begin;
+    c->row_end = row_end;
+    return ELLPACK_OK;
+}
+
+void sp2_opts_default(sp2_opts* o) {
+    if (!o) return;
+    memset(o, 0, sizeof *o);
+    o->threshold = 0.0;
+    o->max_iter = 100;
+    o->min_iter = 20;
+    o->stag_gate = 1e-3;
+    o->emin = NAN;
+    o->emax = NAN;
+    o->on_overflow = SP2_GROW;
+    o->max_width = 0;
+    o->initial_width = 0;
+}
+
+// ------------------------------------------------------------------------- SP2
+
+namespace {
+
+struct DevMatrix {
+    ellpack_desc d{};
+    bool owned = false;
+};
+
+int dm_alloc(ellpack_ctx c, DevMatrix& m, int64_t n, int32_t w) {
+    if (m.owned) ellpack_destroy(c, &m.d);
+    m.owned = false;
+    RK(ellpack_create(c, n, w, &m.d));
+    m.owned = true;
+    return ELLPACK_OK;
+}
+
+void dm_free(ellpack_ctx c, DevMatrix& m) {
+    if (m.owned) ellpack_destroy(c, &m.d);
+    m.owned = false;
+}
+
+int32_t round_up32(int64_t x) { return (int32_t)((x + 31) & ~int64_t(31)); }
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// X (width w) <- drop(alpha*H + beta*I) computed at a safe width first (H.w + 1),
+// then copied at width w; returns required width in *req.
+int sp2_make_x0(ellpack_ctx c, const ellpack_desc* h, double alpha, double beta, double tau,
+                DevMatrix& tmp, int32_t* req) {
+    const int64_t n = h->n;
+    const int32_t wt = (h->w + 2) & ~1;
+    RK(dm_alloc(c, tmp, n, wt));
+    int64_t r0, r1;
+    rows_of(c, n, &r0, &r1);
+    // tmp <- H (own rows), then tmp <- alpha*tmp + beta*I in place
+    CK(cudaMemsetAsync(c->d_status, 0, 8, c->stream));
+    CK(launch_copy_rows(kmat(h), kout(&tmp.d), r0, r1, c->d_status, c->stream));
+    c->launches++;
+    RK(ensure_identity(c, n));
+    RowOpParams p = base_params(c, n);
+    p.A = kmat(&tmp.d);
+    p.B = identity(c);
+    p.Old = identity(c);
+    p.old_mode = 1;
+    p.C = kout(&tmp.d);
+    p.alpha = alpha;
+    p.beta = beta;
+    p.tau = tau;
+    p.stash_a = 1;
+    RK(enqueue_row_op(c, p, n));
+    RK(reduce_status(c));
+    RK(fetch(c, 0));
+    *req = c->h->status[1];
+    return ELLPACK_OK;
+}
+
+}  // namespace
+
+int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, const sp2_opts* opts_in,
+            ellpack_desc* dout, sp2_report* rep) {
+    if (!c) return ELLPACK_ERR_ARG;
+    RK(check_desc(h));
+    RK(check_desc(dout));
+    const int64_t n = h->n;
+    if (dout->n != n) return ELLPACK_ERR_DIM;
+    if (nocc < 0 || nocc > n || !(tol >= 0.0)) return ELLPACK_ERR_ARG;
+    sp2_opts o;
+    if (opts_in) o = *opts_in; else sp2_opts_default(&o);
+    if (!valid_tau(o.threshold) || o.max_iter < 1) return ELLPACK_ERR_ARG;
+    CK(cudaSetDevice(c->device));
+    sp2_iter_rec* iters = rep ? rep->iters : nullptr;
+    sp2_report R;
+    memset(&R, 0, sizeof R);
+    R.iters = iters;
+    R.fail_iter = 0;
+    const double t_start = now_s();
+
+    // ---- Init Misc: bounds, X0, tr(X0)
+    double emin = o.emin, emax = o.emax;
+    if (std::isnan(emin) || std::isnan(emax)) RK(gershgorin_impl(c, h, &emin, &emax));
+    R.emin = emin;
+    R.emax = emax;
+    const double dl = emax - emin;
+    if (!(dl > 0.0) || !std::isfinite(dl)) {
+        if (rep) *rep = R;
+        return ELLPACK_ERR_BOUNDS;
+    }
+    const double alpha0 = -1.0 / dl, beta0 = emax / dl;
+    const int32_t maxw = o.max_width > 0 ? ((o.max_width + 1) & ~1) : (int32_t)((n + 1) & ~int64_t(1));
+    int32_t w = c->sp2_width0 > 0 ? c->sp2_width0 : (o.initial_width > 0 ? o.initial_width : h->w);
+    w = (w + 1) & ~1;
+    const double t_read_end = now_s();
+    DevMatrix X, Y, T;
+    int status = ELLPACK_OK;
+    int32_t req = 0;
+    auto cleanup = [&]() { dm_free(c, X); dm_free(c, Y); dm_free(c, T); };
+    int rc = sp2_make_x0(c, h, alpha0, beta0, o.threshold, T, &req);
+    if (rc) { cleanup(); return rc; }
+    if (req > w) {
+        if (o.on_overflow == SP2_FAIL || req > maxw) {
+            R.stop_reason = SP2_OVERFLOWED; R.required_width = req; R.fail_iter = -1;
+            R.overflow_rows = -1;
+            c->last_req = req;
+            cleanup();
+            if (rep) *rep = R;
+            return ELLPACK_ERR_OVERFLOW;
+        }
+        w = round_up32(req) < maxw ? round_up32(req) : maxw;
+        R.regrows++;
+    }
+    int64_t r0, r1;
+    rows_of(c, n, &r0, &r1);
+    if ((rc = dm_alloc(c, X, n, w))) { cleanup(); return rc; }
+    CK(cudaMemsetAsync(c->d_status, 0, 8, c->stream));
+    CK(launch_copy_rows(kmat(&T.d), kout(&X.d), r0, r1, c->d_status, c->stream));
+    c->launches++;
+    dm_free(c, T);
+    if ((rc = allgather_desc(c, &X.d))) { cleanup(); return rc; }
+    double trX;
+    if ((rc = ellpack_trace(c, &X.d, &trX))) { cleanup(); return rc; }
+    const double t_init_end = now_s();
+
+    // ---- SP2 loop
+    RK(grow(c, c->rows[0], sizeof(double) * n));
+    RK(grow(c, c->rows[1], sizeof(double) * n));
+    RK(grow(c, c->rows[2], sizeof(double) * n));
+    double t_x2 = 0.0, t_norm = 0.0;
+    double e_hist[2] = {NAN, NAN};
+    int32_t wy = w;
+    int stop = -1;
+    int it;
+    for (it = 0; it < o.max_iter; ++it) {
+        const int branch = (trX > (double)nocc) ? SP2_SQUARE : SP2_EXPAND;
+        if (!Y.owned || Y.d.w != wy) {
+            if ((rc = dm_alloc(c, Y, n, wy))) { status = rc; break; }
+        }
+        bool redo;
+        int32_t kept_max = 0;
+        do {
+            redo = false;
+            RowOpParams p = base_params(c, n);
+            p.A = kmat(&X.d);
+            p.B = kmat(&X.d);
+            p.Old = kmat(&X.d);
+            p.C = kout(&Y.d);
+            p.tau = o.threshold;
+            if (branch == SP2_SQUARE) { p.alpha = 1.0; p.beta = 0.0; p.old_mode = 2; }
+            else { p.alpha = -1.0; p.beta = 2.0; p.old_mode = 1; }
+            p.diag_s = (double*)c->rows[0].p;
+            p.diag_c = (double*)c->rows[1].p;
+            p.normsq = (double*)c->rows[2].p;
+            cudaEventRecord(c->ev[0], c->stream);
+            if ((rc = enqueue_row_op(c, p, n))) { status = rc; break; }
+            cudaEventRecord(c->ev[1], c->stream);
+            if ((rc = reduce_status(c))) { status = rc; break; }
+            const double* arrs[3] = {p.diag_s, p.diag_c, p.normsq};
+            if ((rc = enqueue_canonical(c, arrs, 3, n))) { status = rc; break; }
+            cudaEventRecord(c->ev[2], c->stream);
+            if ((rc = fetch(c, 3))) { status = rc; break; }
+            float ms1 = 0.f, ms2 = 0.f;
+            cudaEventElapsedTime(&ms1, c->ev[0], c->ev[1]);
+            cudaEventElapsedTime(&ms2, c->ev[1], c->ev[2]);
+            t_x2 += ms1 * 1e-3;
+            t_norm += ms2 * 1e-3;
+            kept_max = c->h->status[1];
+            if (c->h->status[0] > 0) {
+                if (o.on_overflow == SP2_FAIL || kept_max > maxw) {
+                    R.stop_reason = SP2_OVERFLOWED;
+                    R.overflow_rows = c->h->status[0];
+                    R.required_width = kept_max;
+                    R.fail_iter = it;
+                    c->last_ovf_rows = c->h->status[0];
+                    c->last_req = kept_max;
+                    status = ELLPACK_ERR_OVERFLOW;
+                    break;
+                }
+                wy = round_up32(kept_max) < maxw ? round_up32(kept_max) : maxw;
+                if ((rc = dm_alloc(c, Y, n, wy))) { status = rc; break; }
+                R.regrows++;
+                redo = true;
+            }
+        } while (redo);
+        if (status != ELLPACK_OK) break;
+        const double trS = c->h->sums[0];
+        const double trY = c->h->sums[1];
+        const double fn = std::sqrt(c->h->sums[2]);
+        const double e = trX - trS;
+        if (iters) {
+            iters[it].trX = trX;
+            iters[it].trS = trS;
+            iters[it].e = e;
+            iters[it].fnorm = fn;
+            iters[it].branch = branch;
+            iters[it].width = wy;
+            iters[it].required = kept_max;
+            iters[it].reserved = 0;
+            iters[it].products = -1;
+        }
+        if ((rc = allgather_desc(c, &Y.d))) { status = rc; break; }
+        std::swap(X, Y);
+        trX = trY;
+        if (std::fabs(e) <= tol) stop = SP2_CONVERGED;
+        else if (it + 1 >= o.min_iter && e <= o.stag_gate && !std::isnan(e_hist[0]) && e >= e_hist[0])
+            stop = SP2_STAGNATED;
+        else if (it + 1 == o.max_iter) stop = SP2_MAXITER;
+        e_hist[0] = e_hist[1];
+        e_hist[1] = e;
+        if (stop >= 0) { ++it; break; }
+    }
+    const double t_loop_end = now_s();
+    R.iterations = it;
+    R.final_width = X.owned ? X.d.w : 0;
+    R.trD = trX;
+    if (status == ELLPACK_OK) {
+        R.stop_reason = stop;
+        CK(cudaMemsetAsync(c->d_status, 0, 8, c->stream));
+        CK(launch_copy_rows(kmat(&X.d), kout(dout), 0, n, c->d_status, c->stream));
+        c->launches++;
+        RK(fetch(c, 0));
+        if (c->h->status[0] > 0) {
+            R.required_width = c->h->status[1];
+            c->last_req = c->h->status[1];
+            c->last_ovf_rows = c->h->status[0];
+            status = ELLPACK_ERR_OVERFLOW;
+        } else if (stop == SP2_MAXITER) {
+            status = ELLPACK_ERR_NOCONV;
+        }
+    }
+    cleanup();
+    cudaStreamSynchronize(c->stream);
+    R.t_read_hamiltonian = t_read_end - t_start;
+    R.t_init_misc = t_init_end - t_read_end;
+    R.t_sp2_loop_x2 = t_x2;
+    R.t_sp2_loop_norm = t_norm;
+    R.t_sp2_loop_misc = (t_loop_end - t_init_end) - t_x2 - t_norm;
+    if (rep) *rep = R;
+    return status;
+}
+
+int ellpack_multiply_x2_host(ellpack_ctx c, int64_t n, int32_t wx, const double* xv, const int32_t* xc,
+                             const int32_t* xn, int32_t wx2, double* yv, int32_t* yc, int32_t* yn,
+                             double tau, double* trace_x, double* trace_x2) {
+    if (!c || n <= 0 || wx <= 0 || wx2 <= 0 || (wx & 1) || (wx2 & 1) || !xv || !xc || !xn || !yv || !yc || !yn)
+        return ELLPACK_ERR_ARG;
+    CK(cudaSetDevice(c->device));
+    const size_t cx = (size_t)n * wx, cy = (size_t)n * wx2;
+    RK(grow(c, c->hx_val, cx * 8));
+    RK(grow(c, c->hx_col, cx * 4));
+    RK(grow(c, c->hx_nnz, n * 4));
+    RK(grow(c, c->hy_val, cy * 8));
+    RK(grow(c, c->hy_col, cy * 4));
+    RK(grow(c, c->hy_nnz, n * 4));
+    ellpack_desc X{n, wx, 0, (double*)c->hx_val.p, (int32_t*)c->hx_col.p, (int32_t*)c->hx_nnz.p};
+    ellpack_desc Y{n, wx2, 0, (double*)c->hy_val.p, (int32_t*)c->hy_col.p, (int32_t*)c->hy_nnz.p};
+    CK(cudaMemcpyAsync(X.val, xv, cx * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(X.col, xc, cx * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(X.nnz, xn, n * 4, cudaMemcpyHostToDevice, c->stream));
+    double tx = 0, tx2 = 0;
+    int rc = ellpack_multiply_x2(c, &X, &Y, tau, &tx, &tx2);
+    if (rc != ELLPACK_OK && rc != ELLPACK_ERR_OVERFLOW) return rc;
+    CK(cudaMemcpyAsync(yv, Y.val, cy * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(yc, Y.col, cy * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(yn, Y.nnz, n * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (rc == ELLPACK_OK) {
+        if (trace_x) *trace_x = tx;
+        if (trace_x2) *trace_x2 = tx2;
+    }
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+// internal.cuh — device-side types and launcher prototypes of libellpack
+// (the B200 hot path of arXiv 2102.08505; public ABI in include/ellpack.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ell {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kTraceBlock = 256;  // canonical-sum block
+
+// Read-only view of an ELLPACK matrix (D1: row-major val/col [n][w], nnz [n]).
+struct KMat {
+    const double* val;
+    const int32_t* col;
+    const int32_t* nnz;
+    int32_t w;
+};
+
+// Writable view.
+struct KOut {
+    double* val;
+    int32_t* col;
+    int32_t* nnz;
+    int32_t w;
+};
+
+// One launch of the fused row kernel computes, for rows i in [row_begin, row_end):
+//   s_j   = fma chain over k ascending in A_i of a_ik * b_kj
+//   c_j   = fma(alpha, s_j, old_mode == 1 ? beta*old_ij : +0)        (§8a-a3)
+//   keep iff |c_j| > tau, write ascending into C row i (<= C.w)       (§8a-a3)
+// over the union of the product pattern and (old_mode != 0 ? Old_i : {}).
+// old_mode: 0 = no Old operand; 1 = Old enters the value (beta*old);
+//           2 = Old enters only the union and the norm (SP2 SQUARE step).
+struct RowOpParams {
+    KMat A, B, Old;
+    KOut C;
+    int64_t row_begin, row_end;
+    double alpha, beta, tau;
+    int32_t old_mode;
+    int32_t stash_a;    // C aliases A -> stash A row when the row needs > 1 pass
+    int32_t stash_old;  // C aliases Old -> stash Old row when the row needs > 1 pass
+    int32_t S;          // dense-window capacity (doubles) per warp
+    // optional per-row outputs, indexed by global row (nullable)
+    double* diag_a;   // stored a_ii
+    double* diag_s;   // pre-combine s_ii  (tr(X^2) pre-drop, R5)
+    double* diag_c;   // stored output c_ii (tr of the new iterate)
+    double* normsq;   // sum over the union of (s_ij - old_ij)^2   (old_mode != 0)
+    int32_t* status;  // [0] overflow rows, [1] max kept count
+    // per-warp global scratch (only touched by multi-pass rows)
+    int32_t* cursors;
+    int64_t cur_stride;
+    double* st_val;
+    int32_t* st_col;
+    int64_t st_stride;
+};
+
+struct LaunchCfg {
+    int S;               // window doubles per warp
+    int warps_per_cta;
+    int grid;
+    size_t smem;
+    int R;               // B slots per lane per prefetched step
+};
+
+// spgemm.cu
+cudaError_t plan_row_op(const RowOpParams& p, int window_opt, int warps_opt, int num_sms,
+                        LaunchCfg* cfg);
+cudaError_t launch_row_op(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s);
+
+// reduce.cu
+cudaError_t launch_block_partials(const double* const* arrays, int narr, int64_t row_begin,
+                                  int64_t row_end, int64_t n, double* partials, cudaStream_t s);
+cudaError_t launch_final_sums(const double* partials, int narr, int64_t nblocks, double* out,
+                              cudaStream_t s);
+cudaError_t launch_stored_diag(KMat a, int64_t row_begin, int64_t row_end, double* out,
+                               cudaStream_t s);
+cudaError_t launch_gershgorin(KMat h, int64_t row_begin, int64_t row_end,
+                              unsigned long long* minmax_keys, cudaStream_t s);
+cudaError_t launch_fnorm_rows(KMat a, KMat b, int64_t row_begin, int64_t row_end, double* out,
+                              cudaStream_t s);
+cudaError_t launch_identity(int64_t n, KOut id, cudaStream_t s);
+cudaError_t launch_copy_rows(KMat src, KOut dst, int64_t row_begin, int64_t row_end,
+                             int32_t* status, cudaStream_t s);
+cudaError_t launch_max_nnz(const int32_t* nnz, int64_t row_begin, int64_t row_end,
+                           int32_t* out, cudaStream_t s);
+
+// order-preserving double <-> u64 keys for exact atomic min/max
+__host__ __device__ inline unsigned long long dkey(double x) {
+    unsigned long long b;
+#ifdef __CUDA_ARCH__
+    b = (unsigned long long)__double_as_longlong(x);
+#else
+    __builtin_memcpy(&b, &x, 8);
+#endif
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ inline double dkey_inv(unsigned long long k) {
+    unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+    double x;
+#ifdef __CUDA_ARCH__
+    x = __longlong_as_double((long long)b);
+#else
+    __builtin_memcpy(&x, &b, 8);
+#endif
+    return x;
+}
+
+}  // namespace ell

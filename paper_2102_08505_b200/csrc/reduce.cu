@@ -1,0 +1,222 @@
+// reduce.cu — canonical reductions and small per-row kernels of libellpack.
+//
+//  * canonical sums (reading R12): the per-row inputs d_i (stored
+//    diagonals, pre-drop diagonals, row norms) are summed sequentially inside
+//    256-row blocks (one thread per block), then sequentially over blocks (one
+//    thread). This fixed tree makes every trace bitwise reproducible, equal to the
+//    oracle's, and identical for any row partition over ranks whose blocks start
+//    on multiples of 256 (§8c-c12): the block partials are exchanged, never
+//    re-associated.
+//  * Gershgorin bounds (§8c-c8): thread per row, sequential in slot
+//    order; min/max are exact, so any combine order gives the same bits.
+//  * fnorm_diff rows: warp per row, binary search of the partner row.
+#include "internal.cuh"
+
+namespace ell {
+
+__global__ void final_sums_kernel(const double* partials, int narr, int64_t nblocks, double* out) {
+    const int a = threadIdx.x;
+    if (a >= narr) return;
+    double s = 0.0;
+    for (int64_t b = 0; b < nblocks; ++b) s = __dadd_rn(s, partials[(size_t)a * nblocks + b]);
+    out[a] = s;
+}
+
+struct PtrPack { const double* p[8]; };
+
+__global__ void block_partials_pack_kernel(PtrPack arrays, int narr, int64_t b0, int64_t b1,
+                                           int64_t row_end, double* partials, int64_t nblocks_total) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nb = b1 - b0;
+    if (t >= nb * narr) return;
+    const int a = (int)(t / nb);
+    const int64_t b = b0 + t % nb;
+    const double* d = arrays.p[a];
+    const int64_t r0 = b * kTraceBlock;
+    const int64_t r1 = min(r0 + kTraceBlock, row_end);
+    double s = 0.0;
+    for (int64_t r = r0; r < r1; ++r) s = __dadd_rn(s, d[r]);
+    partials[(size_t)a * nblocks_total + b] = s;
+}
+
+// partials layout: [narr][nblocks(n)], only blocks of [row_begin,row_end) written.
+cudaError_t launch_block_partials(const double* const* arrays, int narr, int64_t row_begin,
+                                  int64_t row_end, int64_t n, double* partials, cudaStream_t s) {
+    if (narr < 1 || narr > 8) return cudaErrorInvalidValue;
+    PtrPack pk{};
+    for (int a = 0; a < narr; ++a) pk.p[a] = arrays[a];
+    const int64_t nbt = (n + kTraceBlock - 1) / kTraceBlock;
+    const int64_t b0 = row_begin / kTraceBlock;
+    const int64_t b1 = (row_end + kTraceBlock - 1) / kTraceBlock;
+    const int64_t work = (b1 - b0) * narr;
+    if (work <= 0) return cudaSuccess;
+    const int threads = 128;
+    block_partials_pack_kernel<<<(unsigned)((work + threads - 1) / threads), threads, 0, s>>>(
+        pk, narr, b0, b1, row_end, partials, nbt);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_final_sums(const double* partials, int narr, int64_t nblocks, double* out,
+                              cudaStream_t s) {
+    final_sums_kernel<<<1, 32, 0, s>>>(partials, narr, nblocks, out);
+    return cudaGetLastError();
+}
+
+// stored diagonal a_ii (0 if absent): warp per row, lanes scan the sorted row.
+__global__ void stored_diag_kernel(KMat a, int64_t r0, int64_t r1, double* out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = r0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (i >= r1) return;
+    const int32_t* c = a.col + (size_t)i * a.w;
+    const double* v = a.val + (size_t)i * a.w;
+    const int n = a.nnz[i];
+    double d = 0.0;
+    for (int q = lane; q < n; q += 32)
+        if (c[q] == (int)i) d = v[q];
+    const unsigned m = __ballot_sync(FULL, d != 0.0);
+    d = m ? __shfl_sync(FULL, d, __ffs(m) - 1) : 0.0;
+    if (lane == 0) out[i] = d;
+}
+
+cudaError_t launch_stored_diag(KMat a, int64_t r0, int64_t r1, double* out, cudaStream_t s) {
+    const int64_t rows = r1 - r0;
+    if (rows <= 0) return cudaSuccess;
+    stored_diag_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(a, r0, r1, out);
+    return cudaGetLastError();
+}
+
+// Gershgorin: keys[0] = min key of lo_i, keys[1] = max key of hi_i (dkey order).
+__global__ void gershgorin_kernel(KMat h, int64_t r0, int64_t r1, unsigned long long* keys) {
+    const int64_t i = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long kmin = ~0ull, kmax = 0ull;
+    if (i < r1) {
+        const int32_t* c = h.col + (size_t)i * h.w;
+        const double* v = h.val + (size_t)i * h.w;
+        const int n = h.nnz[i];
+        double r = 0.0, d = 0.0;
+        for (int q = 0; q < n; ++q) {
+            if (c[q] == (int)i) d = v[q];
+            else r = __dadd_rn(r, fabs(v[q]));
+        }
+        kmin = dkey(__dsub_rn(d, r));
+        kmax = dkey(__dadd_rn(d, r));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(FULL, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(FULL, kmax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(keys + 0, kmin);
+        atomicMax(keys + 1, kmax);
+    }
+}
+
+cudaError_t launch_gershgorin(KMat h, int64_t r0, int64_t r1, unsigned long long* keys,
+                              cudaStream_t s) {
+    const int64_t rows = r1 - r0;
+    if (rows <= 0) return cudaSuccess;
+    gershgorin_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(h, r0, r1, keys);
+    return cudaGetLastError();
+}
+
+__device__ __forceinline__ int lower_bound(const int32_t* c, int n, int key) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (c[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// out[i] = sum over the union of (a_ij - b_ij)^2 (order: lanes then butterfly; deterministic)
+__global__ void fnorm_rows_kernel(KMat a, KMat b, int64_t r0, int64_t r1, double* out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = r0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (i >= r1) return;
+    const int32_t* ca = a.col + (size_t)i * a.w;
+    const double* va = a.val + (size_t)i * a.w;
+    const int32_t* cb = b.col + (size_t)i * b.w;
+    const double* vb = b.val + (size_t)i * b.w;
+    const int na = a.nnz[i], nb = b.nnz[i];
+    double s = 0.0;
+    for (int q = lane; q < na; q += 32) {
+        const int j = ca[q];
+        const int pb = lower_bound(cb, nb, j);
+        const double bj = (pb < nb && cb[pb] == j) ? vb[pb] : 0.0;
+        const double d = __dsub_rn(va[q], bj);
+        s = __fma_rn(d, d, s);
+    }
+    for (int q = lane; q < nb; q += 32) {
+        const int j = cb[q];
+        const int pa = lower_bound(ca, na, j);
+        if (!(pa < na && ca[pa] == j)) s = __fma_rn(vb[q], vb[q], s);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(FULL, s, o));
+    if (lane == 0) out[i] = s;
+}
+
+cudaError_t launch_fnorm_rows(KMat a, KMat b, int64_t r0, int64_t r1, double* out, cudaStream_t s) {
+    const int64_t rows = r1 - r0;
+    if (rows <= 0) return cudaSuccess;
+    fnorm_rows_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(a, b, r0, r1, out);
+    return cudaGetLastError();
+}
+
+__global__ void identity_kernel(int64_t n, KOut id) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    id.val[(size_t)i * id.w] = 1.0;
+    id.col[(size_t)i * id.w] = (int32_t)i;
+    id.nnz[i] = 1;
+}
+
+cudaError_t launch_identity(int64_t n, KOut id, cudaStream_t s) {
+    identity_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, id);
+    return cudaGetLastError();
+}
+
+// dst row i <- src row i (truncated to dst.w; status[0] += overflow rows, status[1] max nnz)
+__global__ void copy_rows_kernel(KMat src, KOut dst, int64_t r0, int64_t r1, int32_t* status) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = r0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (i >= r1) return;
+    const int n = src.nnz[i];
+    const int m = n < dst.w ? n : dst.w;
+    const size_t so = (size_t)i * src.w, d_o = (size_t)i * dst.w;
+    for (int q = lane; q < m; q += 32) {
+        dst.val[d_o + q] = src.val[so + q];
+        dst.col[d_o + q] = src.col[so + q];
+    }
+    if (lane == 0) {
+        dst.nnz[i] = m;
+        if (n > dst.w) atomicAdd(status, 1);
+        atomicMax(status + 1, n);
+    }
+}
+
+cudaError_t launch_copy_rows(KMat src, KOut dst, int64_t r0, int64_t r1, int32_t* status,
+                             cudaStream_t s) {
+    const int64_t rows = r1 - r0;
+    if (rows <= 0) return cudaSuccess;
+    copy_rows_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(src, dst, r0, r1, status);
+    return cudaGetLastError();
+}
+
+__global__ void max_nnz_kernel(const int32_t* nnz, int64_t r0, int64_t r1, int32_t* out) {
+    const int64_t i = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int v = (i < r1) ? nnz[i] : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+    if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
+}
+
+cudaError_t launch_max_nnz(const int32_t* nnz, int64_t r0, int64_t r1, int32_t* out, cudaStream_t s) {
+    const int64_t rows = r1 - r0;
+    if (rows <= 0) return cudaSuccess;
+    max_nnz_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(nnz, r0, r1, out);
+    return cudaGetLastError();
+}
+
+}  // namespace ell
