@@ -24,6 +24,11 @@
 
 using namespace ell;
 
+// Dense-window limits (doubles per row): rows whose centred window needs more than
+// kFastWindowMax use the multi-pass general path with kGeneralWindow.
+constexpr int64_t kFastWindowMax = 12288;  // 96 KB + stage per warp
+constexpr int64_t kGeneralWindow = 4096;
+
 namespace {
 
 struct Buf {
@@ -81,7 +86,10 @@ struct ellpack_ctx_s {
     int32_t* d_status = nullptr;              // [0] ovf rows, [1] max kept
     unsigned long long* d_keys = nullptr;     // gershgorin min/max keys
     double* d_sums = nullptr;                 // final sums (<= 8)
+    int32_t* d_bw = nullptr;                  // bandwidth probe
+    LaunchCfg last_cfg{};
     struct Host {
+        int32_t bw[4];
         int32_t status[2];
         unsigned long long keys[2];
         double sums[8];
@@ -201,18 +209,46 @@ int reduce_status(ellpack_ctx c) {
 }
 
 // Enqueue one row op (kernel + scratch management). Status is left in d_status.
+// The launch geometry comes from a bandwidth probe (one tiny kernel + a 12-byte read-back):
+// with half-bandwidths hA, hB, hOld every row's products and Old entries lie within
+// i +- h, h = max(hA + hB, hOld), so a row-centred window of S >= 2h + 1 doubles holds the
+// whole row ("fast path", no span pre-pass). Wider rows use the multi-pass general path.
 int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
-    LaunchCfg cfg;
-    int window = c->window_opt;
-    if (window <= 0) {
-        window = 4096;
-        int64_t nr = (n + 31) & ~int64_t(31);
-        if (nr < window) window = (int)nr;
+    p.ncols = n;
+    const bool has_old = p.old_mode != 0;
+    CK(cudaMemsetAsync(c->d_bw, 0, 4 * sizeof(int32_t), c->stream));
+    const KMat none{nullptr, nullptr, nullptr, 0};
+    CK(launch_bandwidth(p.alpha != 0.0 ? p.A : none, p.B, has_old ? p.Old : none,
+                        has_old ? 3 : 2, p.row_begin, p.row_end, n, c->d_bw, c->stream));
+    c->launches++;
+    CK(cudaMemcpyAsync(c->h->bw, c->d_bw, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const int64_t hprod = p.alpha != 0.0 ? (int64_t)c->h->bw[0] + c->h->bw[1] : 0;
+    const int64_t h = has_old ? (hprod > c->h->bw[2] ? hprod : c->h->bw[2]) : hprod;
+    const int64_t need = 2 * h + 1;
+    const int64_t nr = (n + 31) & ~int64_t(31);
+    int64_t S;
+    if (c->window_opt > 0) {
+        S = c->window_opt;
+        p.fast = need <= S ? 1 : 0;
+    } else if (need <= kFastWindowMax) {
+        S = (need + 31) & ~int64_t(31);
+        p.fast = 1;
+    } else {
+        S = kGeneralWindow;
+        p.fast = 0;
     }
-    CK(plan_row_op(p, window, c->warps_opt, c->num_sms, &cfg));
+    if (S > nr) { S = nr; p.fast = 1; }
+    if (S < 32) S = 32;
+    LaunchCfg cfg;
+    CK(plan_row_op(p, (int)S, c->warps_opt, c->num_sms, &cfg));
     p.S = cfg.S;
+    c->last_cfg = cfg;
     const int64_t total_warps = (int64_t)cfg.grid * cfg.warps_per_cta;
     const bool may_multi = n > cfg.S;
+    p.cursors = nullptr;
+    p.st_val = nullptr;
+    p.st_col = nullptr;
     if (may_multi) {
         p.cur_stride = p.A.w;
         RK(grow(c, c->cursors, sizeof(int32_t) * (size_t)total_warps * p.cur_stride));
@@ -348,6 +384,7 @@ int ellpack_ctx_create(int device, void* stream, ellpack_ctx* out) {
     cudaError_t e = cudaMalloc(&c->d_status, 64);
     if (!e) e = cudaMalloc(&c->d_keys, 64);
     if (!e) e = cudaMalloc(&c->d_sums, 64);
+    if (!e) e = cudaMalloc(&c->d_bw, 64);
     if (!e) e = cudaMallocHost(&c->h, sizeof(ellpack_ctx_s::Host));
     for (int k = 0; k < 6 && !e; ++k) e = cudaEventCreate(&c->ev[k]);
     if (e) { ellpack_ctx_destroy(c); return from_cuda(e); }
@@ -367,6 +404,7 @@ int ellpack_ctx_destroy(ellpack_ctx c) {
     cudaFree(c->d_status);
     cudaFree(c->d_keys);
     cudaFree(c->d_sums);
+    cudaFree(c->d_bw);
     if (c->h) cudaFreeHost(c->h);
     for (int k = 0; k < 6; ++k) if (c->ev[k]) cudaEventDestroy(c->ev[k]);
     delete c;

@@ -41,6 +41,8 @@ struct RowOpParams {
     int32_t stash_a;    // C aliases A -> stash A row when the row needs > 1 pass
     int32_t stash_old;  // C aliases Old -> stash Old row when the row needs > 1 pass
     int32_t S;          // dense-window capacity (doubles) per warp
+    int32_t fast;       // 1: every row fits the row-centred window of S (bandwidth-probed)
+    int64_t ncols;      // matrix dimension N (columns >= N never exist)
     // optional per-row outputs, indexed by global row (nullable)
     double* diag_a;   // stored a_ii
     double* diag_s;   // pre-combine s_ii  (tr(X^2) pre-drop, R5)
@@ -64,9 +66,12 @@ struct LaunchCfg {
 };
 
 // spgemm.cu
-cudaError_t plan_row_op(const RowOpParams& p, int window_opt, int warps_opt, int num_sms,
-                        LaunchCfg* cfg);
+cudaError_t plan_row_op(const RowOpParams& p, int S, int warps_opt, int num_sms, LaunchCfg* cfg);
 cudaError_t launch_row_op(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s);
+size_t row_op_warp_smem(int S, bool has_old);
+// out[0..2] = max half-bandwidth of a (rows r0..r1), b (all rows), c (rows r0..r1)
+cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64_t r1, int64_t n,
+                             int32_t* out, cudaStream_t s);
 
 // reduce.cu
 cudaError_t launch_block_partials(const double* const* arrays, int narr, int64_t row_begin,

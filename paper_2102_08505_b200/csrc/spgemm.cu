@@ -3,21 +3,27 @@
 // One warp owns one output row i (BJ north_star (1): "a warp or small CTA owns each
 // output row"); a persistent grid strides over rows [row_begin, row_end).
 // Per row:
-//   a1  span pre-pass: lo = min over k in A_i of col_B[k][0], hi = max of the last
-//       column (plus Old_i's extent); the row's column window [lo, hi] is processed
-//       in ceil(span / S) passes of an S-double dense-window accumulator in shared
-//       memory (single pass whenever the span fits).
-//   a2  gather + accumulate: for k in A_i ascending, the warp's lanes take the
-//       entries of B row k (distinct columns, so no two lanes collide inside one k)
-//       and do acc[j] = fma(a_ik, b_kj, acc[j]); a __syncwarp between consecutive
-//       k orders the read-modify-writes, so every output entry is the fma chain in
-//       ascending k (reading R12 -> bitwise equal to the oracle). B rows are
-//       prefetched D steps ahead into registers (R slots of 32 entries per step)
-//       with read-only (ld.global.nc) loads, hiding the L2 latency of the gather.
+//   a1  window: the host probes the bandwidths of A, B (and Old) once per launch, so
+//       every row's products fall in the row-centred window [i - h, i + h]; the
+//       window (S doubles, S >= 2h+1) is a dense accumulator in shared memory and
+//       the row needs no span pre-pass ("fast path"). Rows whose span does not fit
+//       (S capped by shared memory, e.g. dense SP2 iterates) take the general path:
+//       a span pre-pass and ceil(span/S) passes with per-k cursors.
+//   a2  gather + accumulate: A's row is staged in shared memory (k, a_ik, nnz_B(k));
+//       for k ascending the warp's lanes take the entries of B row k (distinct
+//       columns, so no two lanes collide inside one k) and do
+//       acc[j] = fma(a_ik, b_kj, acc[j]); a __syncwarp between consecutive k orders
+//       the read-modify-writes, so every output entry is the fma chain in ascending
+//       k (reading R12 -> bitwise equal to the oracle). B rows are prefetched D
+//       steps ahead into registers (up to R groups of 32 entries per step, groups
+//       beyond nnz_B(k) skipped warp-uniformly) with read-only loads, hiding the L2
+//       latency of the gather; the R loads / fmas / stores of a step are issued as
+//       three batches on 32-bit shared addresses.
 //   a3  combine + drop + compact: Old_i entries (C_old / the SP2 iterate) are merged
-//       into the window with c = fma(alpha, s, beta*old); a window scan keeps
-//       |c| > tau, compacts with ballot/popc and writes the row contiguously in
-//       ascending column order (coalesced stores), counting overflow past C.w.
+//       into the window with c = fma(alpha, s, beta*old); a window scan (two slots
+//       per lane, 16-byte shared loads) keeps |c| > tau, compacts with ballot/popc
+//       and writes the row contiguously in ascending column order, counting
+//       overflow past C.w.
 //   a4  per-row trace / norm inputs (stored a_ii, pre-drop s_ii, stored c_ii,
 //       ||S - Old||^2), reduced later in canonical order (reduce.cu).
 // With A = B = Old = X this single kernel is the fused SP2 step (BJ north_star (2)):
@@ -27,6 +33,8 @@
 #include <climits>
 
 namespace ell {
+
+constexpr int kStage = 128;  // A-row entries staged in shared memory per piece
 
 __device__ __forceinline__ int warp_min(int v) {
 #pragma unroll
@@ -44,24 +52,293 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// 32-bit shared-window accesses (no generic->shared conversion per access)
+__device__ __forceinline__ double lds64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void lds128(uint32_t a, double& x, double& y) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t a, double x, double y) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x), "d"(y) : "memory");
+}
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lds16u(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts16u(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// Per-warp shared layout: acc[S] f64 | stage: ak[kStage] i32, anb[kStage] i32, ast[kStage] i32,
+// aa[kStage] f64 | flags[S] u8 (only when old_mode != 0)
+struct WarpSmem {
+    uint32_t acc;   // shared address of acc[0]
+    uint32_t flg;   // shared address of flags[0]
+    int* ak;
+    int* anb;
+    int* ast;
+    double* aa;
+};
+
+__host__ __device__ inline size_t warp_smem_bytes(int S, bool has_old) {
+    return (size_t)S * 8 + (size_t)kStage * 20 + (has_old ? (size_t)S : 0);
+}
+
+struct RowCtx {
+    const RowOpParams* p;
+    WarpSmem w;
+    int lane;
+};
+
+// Load one prefetched step (R groups of 32 entries of B row k starting at st) into the ring slot.
+template <int R>
+__device__ __forceinline__ void load_step(const RowOpParams& p, const WarpSmem& w, int lane, int t,
+                                          int (&rj)[R], double (&rv)[R]) {
+    const int k = w.ak[t];
+    const int nb = w.anb[t];
+    const int st = w.ast[t];
+    const int32_t* bc = p.B.col + (size_t)k * p.B.w;
+    const double* bv = p.B.val + (size_t)k * p.B.w;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        rj[r] = INT_MAX;
+        if (32 * r < nb - st) {
+            const int q = st + 32 * r + lane;
+            if (q < nb) {
+                rj[r] = __ldg(bc + q);
+                rv[r] = __ldg(bv + q);
+            }
+        }
+    }
+}
+
+// Accumulate steps [0, cnt) of the staged piece into the window [c0, c0 + width).
+// MULTI: entries at or beyond c0 + width are left for later passes (cursor advanced by the
+// in-range count); otherwise they are violations (reported through *viol).
+template <int R, int D, bool MULTI>
+__device__ __forceinline__ void accumulate_piece(const RowOpParams& p, const WarpSmem& w, int lane, int cnt,
+                                                 int c0, int width, unsigned* viol) {
+    int rj[D][R];
+    double rv[D][R];
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+        if (d < cnt) load_step<R>(p, w, lane, d, rj[d], rv[d]);
+    unsigned bad = 0;
+    for (int t0 = 0; t0 < cnt; t0 += D) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            const int t = t0 + d;
+            if (t < cnt) {
+                const double a = w.aa[t];
+                const int nb = w.anb[t];
+                const int st = w.ast[t];
+                const int rem = nb - st;
+                // batch 1: in-range test + shared loads
+                uint32_t ad[R];
+                double old[R];
+                bool inr[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const unsigned off = (unsigned)(rj[d][r] - c0);
+                    inr[r] = (32 * r < rem) && off < (unsigned)width;
+                    ad[r] = w.acc + off * 8u;
+                    if (!MULTI && (32 * r < rem) && rj[d][r] != INT_MAX && !inr[r]) bad = 1;
+                    if (inr[r]) old[r] = lds64(ad[r]);
+                }
+                // batch 2: fma + shared stores
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    if (inr[r]) sts64(ad[r], __fma_rn(a, rv[d][r], old[r]));
+                int n_in = 0;
+                if (MULTI) {
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (32 * r < rem) n_in += __popc(__ballot_sync(FULL, inr[r]));
+                }
+                if (rem > 32 * R && (!MULTI || n_in == 32 * R)) {
+                    // B row longer than the prefetched groups: finish it here (rare).
+                    const int k = w.ak[t];
+                    const int32_t* bc = p.B.col + (size_t)k * p.B.w;
+                    const double* bv = p.B.val + (size_t)k * p.B.w;
+                    for (int q0 = st + 32 * R; q0 < nb; q0 += 64) {
+                        const int qa = q0 + lane, qb = q0 + 32 + lane;
+                        const int ja = qa < nb ? __ldg(bc + qa) : INT_MAX;
+                        const int jb = qb < nb ? __ldg(bc + qb) : INT_MAX;
+                        const double va = qa < nb ? __ldg(bv + qa) : 0.0;
+                        const double vb = qb < nb ? __ldg(bv + qb) : 0.0;
+                        const unsigned oa = (unsigned)(ja - c0), ob = (unsigned)(jb - c0);
+                        const bool ia = oa < (unsigned)width, ib = ob < (unsigned)width;
+                        if (!MULTI && ((ja != INT_MAX && !ia) || (jb != INT_MAX && !ib))) bad = 1;
+                        double xa = 0.0, xb = 0.0;
+                        if (ia) xa = lds64(w.acc + oa * 8u);
+                        if (ib) xb = lds64(w.acc + ob * 8u);
+                        if (ia) sts64(w.acc + oa * 8u, __fma_rn(a, va, xa));
+                        if (ib) sts64(w.acc + ob * 8u, __fma_rn(a, vb, xb));
+                        if (MULTI) {
+                            const int na = __popc(__ballot_sync(FULL, ia));
+                            const int nbb = __popc(__ballot_sync(FULL, ib));
+                            n_in += na + nbb;
+                            if (na + nbb < 64) break;
+                        }
+                    }
+                }
+                if (MULTI && lane == 0) w.ast[t] = st + n_in;
+                if (t + D < cnt) load_step<R>(p, w, lane, t + D, rj[d], rv[d]);
+                __syncwarp();
+            }
+        }
+    }
+    if (!MULTI) *viol |= __ballot_sync(FULL, bad);
+}
+
+// Stage A-row entries [p0, p0 + cnt) into shared memory (k, a, nnz_B(k), cursor).
+__device__ __forceinline__ void stage_piece(const RowOpParams& p, const WarpSmem& w, int lane,
+                                            const int32_t* a_col, const double* a_val, int p0, int cnt,
+                                            const int32_t* cur) {
+    for (int q = lane; q < cnt; q += 32) {
+        const int k = a_col[p0 + q];
+        w.ak[q] = k;
+        w.aa[q] = a_val[p0 + q];
+        w.anb[q] = __ldg(p.B.nnz + k);
+        w.ast[q] = cur ? cur[p0 + q] : 0;
+    }
+    __syncwarp();
+}
+
+// Combine Old entries with columns in [c0, c0 + width): acc <- fma(alpha, s, beta*old), flag.
+// Returns false (fast path) if an Old entry lies outside the window.
+__device__ __forceinline__ bool combine_old(const RowOpParams& p, const WarpSmem& w, int lane,
+                                            const int32_t* o_col, const double* o_val, int nOld,
+                                            int& old_cur, int c0, int width, bool multi, double& nrm) {
+    bool ok = true;
+    while (old_cur < nOld) {
+        const int q = old_cur + lane;
+        const bool v = q < nOld;
+        const int j = v ? o_col[q] : INT_MAX;
+        const unsigned off = (unsigned)(j - c0);
+        const bool inr = v && off < (unsigned)width;
+        if (v && !inr && !multi) ok = false;
+        if (inr) {
+            const double x = o_val[q];
+            const double s = lds64(w.acc + off * 8u);
+            if (p.normsq) {
+                const double df = __dsub_rn(s, x);
+                nrm = __fma_rn(df, df, nrm);
+            }
+            const double tt = (p.old_mode == 1) ? __dmul_rn(p.beta, x) : 0.0;
+            sts64(w.acc + off * 8u, __fma_rn(p.alpha, s, tt));
+            sts8(w.flg + off, 1u);
+        }
+        const int n = __popc(__ballot_sync(FULL, inr));
+        old_cur += n;
+        if (n < 32) break;
+    }
+    __syncwarp();
+    return __all_sync(FULL, ok);
+}
+
+// Emit window [0, width) (columns c0 + jj): drop, compact, write at C row offset; clears the window.
+__device__ __forceinline__ void emit_window(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
+                                            size_t c_off, int c0, int width, int64_t ncols, int& kept,
+                                            double& dc, double& nrm) {
+    const bool has_old = p.old_mode != 0;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    // two slots per lane: columns c0 + b + 2*lane, +1 (width is a multiple of 2)
+    for (int b = 0; b < width; b += 64) {
+        const int jj = b + 2 * lane;
+        const bool in = jj < width;
+        double v0 = 0.0, v1 = 0.0;
+        uint32_t f = 0;
+        if (in) {
+            lds128(w.acc + (uint32_t)jj * 8u, v0, v1);
+            sts128(w.acc + (uint32_t)jj * 8u, 0.0, 0.0);
+            if (has_old) {
+                f = lds16u(w.flg + jj);
+                sts16u(w.flg + jj, 0u);
+            }
+        }
+        double c0v, c1v;
+        if (f & 0xffu) c0v = v0;
+        else {
+            c0v = __fma_rn(p.alpha, v0, 0.0);
+            if (p.normsq) nrm = __fma_rn(v0, v0, nrm);
+        }
+        if (f & 0xff00u) c1v = v1;
+        else {
+            c1v = __fma_rn(p.alpha, v1, 0.0);
+            if (p.normsq) nrm = __fma_rn(v1, v1, nrm);
+        }
+        const int64_t col0 = (int64_t)c0 + jj;
+        const bool k0 = in && col0 < ncols && fabs(c0v) > p.tau;
+        const bool k1 = in && col0 + 1 < ncols && fabs(c1v) > p.tau;
+        const unsigned m0 = __ballot_sync(FULL, k0);
+        const unsigned m1 = __ballot_sync(FULL, k1);
+        const int before = __popc(m0 & lt_mask) + __popc(m1 & lt_mask);
+        int pos = kept + before;
+        if (k0) {
+            if (pos < p.C.w) {
+                p.C.val[c_off + pos] = c0v;
+                p.C.col[c_off + pos] = (int32_t)col0;
+            }
+            if (col0 == i) dc = c0v;
+            ++pos;
+        }
+        if (k1) {
+            if (pos < p.C.w) {
+                p.C.val[c_off + pos] = c1v;
+                p.C.col[c_off + pos] = (int32_t)(col0 + 1);
+            }
+            if (col0 + 1 == i) dc = c1v;
+        }
+        kept += __popc(m0) + __popc(m1);
+    }
+    __syncwarp();
+}
+
+// Zero the window (after an abandoned fast-path attempt).
+__device__ __forceinline__ void clear_window(const WarpSmem& w, int lane, int S, bool has_old) {
+    for (int jj = 2 * lane; jj < S; jj += 64) {
+        sts128(w.acc + (uint32_t)jj * 8u, 0.0, 0.0);
+        if (has_old) sts16u(w.flg + jj, 0u);
+    }
+    __syncwarp();
+}
+
 template <int R, int D>
 __global__ void __launch_bounds__(128) row_op_kernel(const RowOpParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    const int wpc = blockDim.x >> 5;
     const int S = p.S;
-    double* acc = reinterpret_cast<double*>(smem_raw) + (size_t)wid * S;
-    unsigned char* flg = smem_raw + (size_t)wpc * S * sizeof(double) + (size_t)wid * S;
     const bool has_old = p.old_mode != 0;
-    for (int j = lane; j < S; j += 32) acc[j] = 0.0;
-    if (has_old)
-        for (int j = lane; j < S; j += 32) flg[j] = 0;
-    __syncwarp();
+    unsigned char* base = smem_raw + (size_t)wid * warp_smem_bytes(S, has_old);
+    WarpSmem w;
+    w.acc = (uint32_t)__cvta_generic_to_shared(base);
+    w.ak = reinterpret_cast<int*>(base + (size_t)S * 8);
+    w.anb = w.ak + kStage;
+    w.ast = w.anb + kStage;
+    w.aa = reinterpret_cast<double*>(w.ast + kStage);
+    w.flg = w.acc + (uint32_t)(S * 8 + kStage * 20);
+    clear_window(w, lane, S, has_old);
 
-    const unsigned lt_mask = (1u << lane) - 1u;
-    const int64_t gw = (int64_t)blockIdx.x * wpc + wid;
-    const int64_t nwarps = (int64_t)gridDim.x * wpc;
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t ncols = p.ncols;
     int32_t my_max_kept = 0, my_ovf = 0;
 
     for (int64_t i = p.row_begin + gw; i < p.row_end; i += nwarps) {
@@ -76,217 +353,114 @@ __global__ void __launch_bounds__(128) row_op_kernel(const RowOpParams p) {
             o_col = p.Old.col + (size_t)i * p.Old.w;
             nOld = p.Old.nnz[i];
         }
-
-        // ---- a1: span pre-pass (+ stored diagonal of A)
-        int lo = INT_MAX, hi = -1;
+        // stored diagonal of A (x2 traces)
         double dA = 0.0;
-        bool hasdA = false;
-        for (int q = lane; q < nA; q += 32) {
-            const int k = a_col[q];
-            if (k == (int)i) { dA = a_val[q]; hasdA = true; }
-            const int nb = __ldg(p.B.nnz + k);
-            if (nb > 0) {
-                const int32_t* bc = p.B.col + (size_t)k * p.B.w;
-                lo = min(lo, __ldg(bc));
-                hi = max(hi, __ldg(bc + nb - 1));
-            }
-        }
-        if (nOld > 0 && lane == 0) {
-            lo = min(lo, o_col[0]);
-            hi = max(hi, o_col[nOld - 1]);
-        }
-        lo = warp_min(lo);
-        hi = warp_max(hi);
         if (p.diag_a) {
-            const unsigned m = __ballot_sync(FULL, hasdA);
+            bool has = false;
+            for (int q = lane; q < nA; q += 32)
+                if (a_col[q] == (int)i) { dA = a_val[q]; has = true; }
+            const unsigned m = __ballot_sync(FULL, has);
             dA = m ? __shfl_sync(FULL, dA, __ffs(m) - 1) : 0.0;
         }
 
         int32_t kept = 0;
         double ds = 0.0, dc = 0.0, nrm = 0.0;
         const size_t c_off = (size_t)i * p.C.w;
-        if (hi >= lo) {
-            const int span = hi - lo + 1;
-            const int npass = (span + S - 1) / S;
-            const bool multi = npass > 1;
-            int32_t* cur = p.cursors + gw * p.cur_stride;
-            if (multi && (p.stash_a || p.stash_old)) {
-                // C aliases an input: copy the input rows aside before pass 0 writes.
-                double* sv = p.st_val + gw * p.st_stride;
-                int32_t* sc = p.st_col + gw * p.st_stride;
-                if (p.stash_a) {
-                    for (int q = lane; q < nA; q += 32) { sv[q] = a_val[q]; sc[q] = a_col[q]; }
-                    a_val = sv; a_col = sc;
-                    sv += p.A.w; sc += p.A.w;
-                }
-                if (p.stash_old) {
-                    for (int q = lane; q < nOld; q += 32) { sv[q] = o_val[q]; sc[q] = o_col[q]; }
-                    o_val = sv; o_col = sc;
-                }
-                __syncwarp();
+        bool done = false;
+
+        if (p.fast) {
+            // ---- fast path: one pass over the row-centred window
+            int c0 = 0;
+            if ((int64_t)S < ncols) {
+                int64_t c = i - (S >> 1);
+                if (c < 0) c = 0;
+                if (c > ncols - S) c = ncols - S;
+                c0 = (int)c;
             }
-            int old_cur = 0;
-            for (int pass = 0; pass < npass; ++pass) {
-                const int c0 = lo + pass * S;
-                const int c1 = min(c0 + S, hi + 1);
+            unsigned viol = 0;
+            for (int p0 = 0; p0 < nA; p0 += kStage) {
+                const int cnt = min(kStage, nA - p0);
+                stage_piece(p, w, lane, a_col, a_val, p0, cnt, nullptr);
+                accumulate_piece<R, D, false>(p, w, lane, cnt, c0, S, &viol);
+            }
+            __syncwarp();
+            bool ok = viol == 0;
+            if (ok) {
+                if ((int64_t)c0 <= i && i < (int64_t)c0 + S) ds = lds64(w.acc + (uint32_t)(i - c0) * 8u);
+                int old_cur = 0;
+                if (has_old) ok = combine_old(p, w, lane, o_col, o_val, nOld, old_cur, c0, S, false, nrm);
+            }
+            if (ok) {
+                emit_window(p, w, lane, i, c_off, c0, S, ncols, kept, dc, nrm);
+                done = true;
+            } else {
+                clear_window(w, lane, S, has_old);
+                nrm = 0.0;
+                ds = 0.0;
+            }
+        }
 
-                // ---- a2: gather + accumulate, k ascending
-                for (int p0 = 0; p0 < nA; p0 += 32) {
-                    const int cnt = min(32, nA - p0);
-                    int mk = 0, mnb = 0, mst = 0;
-                    double ma = 0.0;
-                    if (lane < cnt) {
-                        mk = a_col[p0 + lane];
-                        ma = a_val[p0 + lane];
-                        mnb = __ldg(p.B.nnz + mk);
-                        if (multi && pass > 0) mst = cur[p0 + lane];
-                    }
-                    int rj[D][R];
-                    double rv[D][R];
-                    // prologue: steps 0..D-1
-#pragma unroll
-                    for (int d = 0; d < D; ++d) {
-                        if (d < cnt) {
-                            const int k = __shfl_sync(FULL, mk, d);
-                            const int nb = __shfl_sync(FULL, mnb, d);
-                            const int st = __shfl_sync(FULL, mst, d);
-                            const int32_t* bc = p.B.col + (size_t)k * p.B.w;
-                            const double* bv = p.B.val + (size_t)k * p.B.w;
-#pragma unroll
-                            for (int r = 0; r < R; ++r) {
-                                const int q = st + lane + 32 * r;
-                                rj[d][r] = INT_MAX;
-                                rv[d][r] = 0.0;
-                                if (q < nb) { rj[d][r] = __ldg(bc + q); rv[d][r] = __ldg(bv + q); }
-                            }
-                        }
-                    }
-                    for (int t0 = 0; t0 < cnt; t0 += D) {
-#pragma unroll
-                        for (int d = 0; d < D; ++d) {
-                            const int t = t0 + d;
-                            if (t < cnt) {
-                                const double a = __shfl_sync(FULL, ma, t);
-                                int n_in = 0;
-#pragma unroll
-                                for (int r = 0; r < R; ++r) {
-                                    const int j = rj[d][r];
-                                    const bool inr = j < c1;
-                                    if (inr) {
-                                        double* ap = acc + (j - c0);
-                                        *ap = __fma_rn(a, rv[d][r], *ap);
-                                    }
-                                    n_in += __popc(__ballot_sync(FULL, inr));
-                                }
-                                if (n_in == 32 * R) {
-                                    // B row longer than the prefetched slots: finish it directly.
-                                    const int k = __shfl_sync(FULL, mk, t);
-                                    const int nb = __shfl_sync(FULL, mnb, t);
-                                    const int st = __shfl_sync(FULL, mst, t);
-                                    const int32_t* bc = p.B.col + (size_t)k * p.B.w;
-                                    const double* bv = p.B.val + (size_t)k * p.B.w;
-                                    int q = st + 32 * R + lane;
-                                    while (true) {
-                                        const bool v = q < nb;
-                                        const int j = v ? __ldg(bc + q) : INT_MAX;
-                                        const bool inr = j < c1;
-                                        if (inr) {
-                                            double* ap = acc + (j - c0);
-                                            *ap = __fma_rn(a, __ldg(bv + q), *ap);
-                                        }
-                                        const int n = __popc(__ballot_sync(FULL, inr));
-                                        n_in += n;
-                                        if (n < 32) break;
-                                        q += 32;
-                                    }
-                                }
-                                if (multi && lane == t) mst += n_in;
-                                // refill this slot with step t + D
-                                if (t + D < cnt) {
-                                    const int k = __shfl_sync(FULL, mk, t + D);
-                                    const int nb = __shfl_sync(FULL, mnb, t + D);
-                                    const int st = __shfl_sync(FULL, mst, t + D);
-                                    const int32_t* bc = p.B.col + (size_t)k * p.B.w;
-                                    const double* bv = p.B.val + (size_t)k * p.B.w;
-#pragma unroll
-                                    for (int r = 0; r < R; ++r) {
-                                        const int q = st + lane + 32 * r;
-                                        rj[d][r] = INT_MAX;
-                                        rv[d][r] = 0.0;
-                                        if (q < nb) { rj[d][r] = __ldg(bc + q); rv[d][r] = __ldg(bv + q); }
-                                    }
-                                }
-                                __syncwarp();
-                            }
-                        }
-                    }
-                    if (multi && lane < cnt) cur[p0 + lane] = mst;
+        if (!done) {
+            // ---- general path: span pre-pass + ceil(span / S) passes with cursors
+            int lo = INT_MAX, hi = -1;
+            for (int q = lane; q < nA; q += 32) {
+                const int k = a_col[q];
+                const int nb = __ldg(p.B.nnz + k);
+                if (nb > 0) {
+                    const int32_t* bc = p.B.col + (size_t)k * p.B.w;
+                    lo = min(lo, __ldg(bc));
+                    hi = max(hi, __ldg(bc + nb - 1));
                 }
-                __syncwarp();
-
-                // ---- a4: pre-combine diagonal s_ii
-                if ((int64_t)c0 <= i && i < (int64_t)c1) ds = acc[i - c0];
-
-                // ---- a3: combine with Old entries in [c0, c1)
-                if (has_old) {
-                    while (old_cur < nOld) {
-                        const int q = old_cur + lane;
-                        const bool v = q < nOld;
-                        const int j = v ? o_col[q] : INT_MAX;
-                        const bool inr = j < c1;
-                        if (inr) {
-                            const double x = o_val[q];
-                            double* ap = acc + (j - c0);
-                            const double s = *ap;
-                            if (p.normsq) {
-                                const double df = __dsub_rn(s, x);
-                                nrm = __fma_rn(df, df, nrm);
-                            }
-                            const double tt = (p.old_mode == 1) ? __dmul_rn(p.beta, x) : 0.0;
-                            *ap = __fma_rn(p.alpha, s, tt);
-                            flg[j - c0] = 1;
-                        }
-                        const int n = __popc(__ballot_sync(FULL, inr));
-                        old_cur += n;
-                        if (n < 32) break;
+            }
+            if (nOld > 0 && lane == 0) {
+                lo = min(lo, o_col[0]);
+                hi = max(hi, o_col[nOld - 1]);
+            }
+            lo = warp_min(lo) & ~1;  // even start: 16-byte aligned window slots
+            hi = warp_max(hi);
+            if (hi >= lo) {
+                const int span = hi - lo + 1;
+                const int npass = (span + S - 1) / S;
+                const bool multi = npass > 1;
+                int32_t* cur = p.cursors ? p.cursors + gw * p.cur_stride : nullptr;
+                if (multi && (p.stash_a || p.stash_old)) {
+                    double* sv = p.st_val + gw * p.st_stride;
+                    int32_t* sc = p.st_col + gw * p.st_stride;
+                    if (p.stash_a) {
+                        for (int q = lane; q < nA; q += 32) { sv[q] = a_val[q]; sc[q] = a_col[q]; }
+                        a_val = sv; a_col = sc;
+                        sv += p.A.w; sc += p.A.w;
+                    }
+                    if (p.stash_old) {
+                        for (int q = lane; q < nOld; q += 32) { sv[q] = o_val[q]; sc[q] = o_col[q]; }
+                        o_val = sv; o_col = sc;
                     }
                     __syncwarp();
                 }
-
-                // ---- a3: drop + compact + write (ascending columns)
-                const int width = c1 - c0;
-                for (int b = 0; b < width; b += 32) {
-                    const int jj = b + lane;
-                    const bool in = jj < width;
-                    double v = 0.0;
-                    bool f = false;
-                    if (in) {
-                        v = acc[jj];
-                        acc[jj] = 0.0;
-                        if (has_old) { f = flg[jj] != 0; flg[jj] = 0; }
-                    }
-                    double c;
-                    if (f) {
-                        c = v;
-                    } else {
-                        c = __fma_rn(p.alpha, v, 0.0);
-                        if (p.normsq) nrm = __fma_rn(v, v, nrm);
-                    }
-                    const bool keep = in && fabs(c) > p.tau;
-                    const unsigned m = __ballot_sync(FULL, keep);
-                    if (keep) {
-                        const int pos = kept + __popc(m & lt_mask);
-                        if (pos < p.C.w) {
-                            p.C.val[c_off + pos] = c;
-                            p.C.col[c_off + pos] = c0 + jj;
-                        }
-                        if ((int64_t)(c0 + jj) == i) dc = c;
-                    }
-                    kept += __popc(m);
-                }
+                if (multi)
+                    for (int q = lane; q < nA; q += 32) cur[q] = 0;
                 __syncwarp();
+                int old_cur = 0;
+                for (int pass = 0; pass < npass; ++pass) {
+                    const int c0 = lo + pass * S;
+                    const int width = min(S, hi + 1 - c0 + 1) & ~1;  // even, covers [c0, hi]
+                    for (int p0 = 0; p0 < nA; p0 += kStage) {
+                        const int cnt = min(kStage, nA - p0);
+                        stage_piece(p, w, lane, a_col, a_val, p0, cnt, multi ? cur : nullptr);
+                        accumulate_piece<R, D, true>(p, w, lane, cnt, c0, width, nullptr);
+                        if (multi) {
+                            for (int q = lane; q < cnt; q += 32) cur[p0 + q] = w.ast[q];
+                            __syncwarp();
+                        }
+                    }
+                    __syncwarp();
+                    if ((int64_t)c0 <= i && i < (int64_t)c0 + width) ds = lds64(w.acc + (uint32_t)(i - c0) * 8u);
+                    if (has_old) combine_old(p, w, lane, o_col, o_val, nOld, old_cur, c0, width, true, nrm);
+                    emit_window(p, w, lane, i, c_off, c0, width, ncols, kept, dc, nrm);
+                }
             }
         }
+
         // ---- row epilogue
         if (lane == 0) p.C.nnz[i] = kept < p.C.w ? kept : p.C.w;
         my_max_kept = max(my_max_kept, kept);
@@ -308,49 +482,86 @@ __global__ void __launch_bounds__(128) row_op_kernel(const RowOpParams p) {
     }
 }
 
-template <int R, int D>
-static cudaError_t config_kernel(size_t smem) {
-    return cudaFuncSetAttribute(row_op_kernel<R, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem);
+// Half-bandwidth probe: out[m] = max over rows of max(i - col[i][0], col[i][nnz-1] - i).
+__global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64_t r1,
+                                 int64_t n, int32_t* out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int bw[3] = {0, 0, 0};
+    const KMat* ms[3] = {&a, &b, &c};
+    if (i < n) {
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+            if (m >= nmat) break;
+            // A and Old only matter on the computed rows; B on every row
+            if (m != 1 && (i < r0 || i >= r1)) continue;
+            const KMat& x = *ms[m];
+            if (x.nnz == nullptr) continue;
+            const int nz = x.nnz[i];
+            if (nz > 0) {
+                const int f = x.col[(size_t)i * x.w], l = x.col[(size_t)i * x.w + nz - 1];
+                bw[m] = max((int)(i - f), (int)(l - i));
+                bw[m] = max(bw[m], 0);
+            }
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+        int v = bw[m];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+        if ((threadIdx.x & 31) == 0 && v > 0) atomicMax(out + m, v);
+    }
 }
 
-static int pick_R(int wb) { return wb <= 32 ? 1 : (wb <= 64 ? 2 : 4); }
+cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64_t r1, int64_t n,
+                             int32_t* out, cudaStream_t s) {
+    bandwidth_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, c, nmat, r0, r1, n, out);
+    return cudaGetLastError();
+}
 
-cudaError_t plan_row_op(const RowOpParams& p, int window_opt, int warps_opt, int num_sms,
-                        LaunchCfg* cfg) {
-    int S = window_opt > 0 ? window_opt : 4096;
+template <int R, int D>
+static cudaError_t prep(const LaunchCfg& cfg, int* blocks_per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(row_op_kernel<R, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)cfg.smem);
+    if (e) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, row_op_kernel<R, D>,
+                                                         cfg.warps_per_cta * 32, cfg.smem);
+}
+
+static int pick_R(int wb) {
+    if (wb <= 32) return 1;
+    if (wb <= 64) return 2;
+    if (wb <= 128) return 4;
+    return 8;
+}
+
+size_t row_op_warp_smem(int S, bool has_old) { return warp_smem_bytes(S, has_old); }
+
+cudaError_t plan_row_op(const RowOpParams& p, int S, int warps_opt, int num_sms, LaunchCfg* cfg) {
     S = (S + 31) & ~31;
+    const size_t per_warp = warp_smem_bytes(S, p.old_mode != 0);
+    const size_t cap = 227 * 1024;
+    if (per_warp > cap) return cudaErrorInvalidConfiguration;
     int wpc = warps_opt > 0 ? warps_opt : 4;
-    if (wpc > 4) wpc = 4;  // __launch_bounds__(128)
+    if (wpc > 4) wpc = 4;
+    while (wpc > 1 && (size_t)wpc * per_warp > cap) --wpc;
     cfg->S = S;
     cfg->warps_per_cta = wpc;
     cfg->R = pick_R(p.B.w);
-    cfg->smem = (size_t)wpc * S * (sizeof(double) + (p.old_mode ? 1 : 0));
-    if (cfg->smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    cfg->smem = (size_t)wpc * per_warp;
     cudaError_t e;
-    int blocks_per_sm = 0;
+    int bps = 0;
     switch (cfg->R) {
-        case 1:
-            if ((e = config_kernel<1, 8>(cfg->smem))) return e;
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, row_op_kernel<1, 8>,
-                                                              wpc * 32, cfg->smem);
-            break;
-        case 2:
-            if ((e = config_kernel<2, 8>(cfg->smem))) return e;
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, row_op_kernel<2, 8>,
-                                                              wpc * 32, cfg->smem);
-            break;
-        default:
-            if ((e = config_kernel<4, 4>(cfg->smem))) return e;
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, row_op_kernel<4, 4>,
-                                                              wpc * 32, cfg->smem);
-            break;
+        case 1: e = prep<1, 8>(*cfg, &bps); break;
+        case 2: e = prep<2, 6>(*cfg, &bps); break;
+        case 4: e = prep<4, 4>(*cfg, &bps); break;
+        default: e = prep<8, 3>(*cfg, &bps); break;
     }
     if (e) return e;
-    if (blocks_per_sm < 1) return cudaErrorInvalidConfiguration;
+    if (bps < 1) return cudaErrorInvalidConfiguration;
     const int64_t rows = p.row_end - p.row_begin;
-    int64_t need = (rows + wpc - 1) / wpc;
-    int64_t full = (int64_t)blocks_per_sm * num_sms;
+    const int64_t need = (rows + wpc - 1) / wpc;
+    const int64_t full = (int64_t)bps * num_sms;
     cfg->grid = (int)(need < full ? (need > 0 ? need : 1) : full);
     return cudaSuccess;
 }
@@ -359,8 +570,9 @@ cudaError_t launch_row_op(const RowOpParams& p, const LaunchCfg& cfg, cudaStream
     dim3 block(cfg.warps_per_cta * 32), grid(cfg.grid);
     switch (cfg.R) {
         case 1: row_op_kernel<1, 8><<<grid, block, cfg.smem, s>>>(p); break;
-        case 2: row_op_kernel<2, 8><<<grid, block, cfg.smem, s>>>(p); break;
-        default: row_op_kernel<4, 4><<<grid, block, cfg.smem, s>>>(p); break;
+        case 2: row_op_kernel<2, 6><<<grid, block, cfg.smem, s>>>(p); break;
+        case 4: row_op_kernel<4, 4><<<grid, block, cfg.smem, s>>>(p); break;
+        default: row_op_kernel<8, 3><<<grid, block, cfg.smem, s>>>(p); break;
     }
     return cudaGetLastError();
 }

@@ -81,7 +81,7 @@ def test_cfg2_multiply_bitwise_in_place(ctx):
 @pytest.mark.parametrize("m", [64, 128, 256])
 def test_cfg5_small_n_x2_bitwise(ctx, m):
     X = synth.cfg5(32768, m)
-    r, Y = ora_x2(X, 8 * m, 1e-5)
+    r, Y = ora_x2(X, 32 * m, 1e-5)
     assert r.status == oracle.OK
     w = ((r.required_width + 31) // 32) * 32
     st, G, tx, tx2 = gpu_x2(ctx, X, w, 1e-5)
@@ -106,12 +106,16 @@ def test_cfg5_full_size_sampled_rows_bitwise(ctx):
     """BASELINE cfg5 largest (N=262144, M=256) in the bench's launch configuration."""
     X = synth.cfg5(262144, 256)
     x = up(X)
-    y = eb().Mat.empty(X.n, 5184)
+    y = eb().Mat.empty(X.n, 256)
+    st, _, _ = ctx.multiply_x2(x, y, 1e-5)  # literal width -> required width (reading R2)
+    assert st == eb().ERR_OVERFLOW
+    w = ((ctx.overflow_info()[1] + 31) // 32) * 32
+    y = eb().Mat.empty(X.n, w)
     st, tx, tx2 = ctx.multiply_x2(x, y, 1e-5)
     assert st == eb().OK
     rng = np.random.default_rng(0)
     rows = sorted(set(rng.integers(0, X.n, 384).tolist()) | {0, 1, X.n - 1, X.n // 2})
-    r, Y = _sample_rows_oracle(X, rows, 5184, 1e-5)
+    r, Y = _sample_rows_oracle(X, rows, w, 1e-5)
     assert r.status == oracle.OK
     idx = torch_index(rows)
     gv, gc, gn = y.val[idx].cpu().numpy(), y.col[idx].cpu().numpy(), y.nnz[idx].cpu().numpy()
@@ -135,7 +139,7 @@ def torch_index(rows):
 def test_x2_of_symmetric_is_bitwise_symmetric_gpu(ctx):
     """P4 on the GPU alone (no oracle needed): cfg5 N=32768, M=64."""
     X = synth.cfg5(32768, 64)
-    st, G, _, _ = gpu_x2(ctx, X, 832, 1e-5)
+    st, G, _, _ = gpu_x2(ctx, X, 1024, 1e-5)
     assert st == eb().OK
     import scipy.sparse as sp
     rows = np.repeat(np.arange(G.n), G.nnz)
@@ -195,8 +199,8 @@ def test_multipass_window_and_stash_bitwise(ellpack_lib, window, beta):
     assert same_bits(g.to_host(), Co)
     # x2 + traces under multi-pass
     X = synth.cfg5(4096, 64)
-    rr, Y = ora_x2(X, 832, 1e-5)
-    st, G, tx, tx2 = gpu_x2(ctx, X, 832, 1e-5)
+    rr, Y = ora_x2(X, 1024, 1e-5)
+    st, G, tx, tx2 = gpu_x2(ctx, X, 1024, 1e-5)
     assert same_bits(G, Y) and (tx, tx2) == (rr.trace_x, rr.trace_x2)
     # add family in place with multi-pass stash
     A2 = A.widened(64)
@@ -383,9 +387,9 @@ def test_row_block_partition_is_bitwise_invariant(ellpack_lib, nranks):
     the blocks equals the single-rank product bit for bit (§8c-c12, row independence)."""
     X = synth.cfg5(32768, 64)
     full = ellpack_lib.Context(0)
-    y1 = ellpack_lib.Mat.empty(X.n, 832)
-    full.multiply_x2(up(X), y1, 1e-5)
-    yp = ellpack_lib.Mat.empty(X.n, 832)
+    y1 = ellpack_lib.Mat.empty(X.n, 1024)
+    assert full.multiply_x2(up(X), y1, 1e-5)[0] == ellpack_lib.OK
+    yp = ellpack_lib.Mat.empty(X.n, 1024)
     x = up(X)
     for (r0, r1) in ellpack_lib.row_partition(X.n, nranks):
         c = ellpack_lib.Context(0)
