@@ -9,26 +9,31 @@
 //       the row needs no span pre-pass ("fast path"). Rows whose span does not fit
 //       (S capped by shared memory, e.g. dense SP2 iterates) take the general path:
 //       a span pre-pass and ceil(span/S) passes with per-k cursors.
-//   a2  gather + accumulate: A's row is staged in shared memory (k, a_ik, nnz_B(k));
-//       for k ascending the warp's lanes take the entries of B row k (distinct
-//       columns, so no two lanes collide inside one k) and do
+//   a2  gather + accumulate: A's row is staged in shared memory (B-row offset,
+//       a_ik, nnz_B(k)); for k ascending the warp's lanes take the entries of B row k
+//       (distinct columns, so no two lanes collide inside one k) and do
 //       acc[j] = fma(a_ik, b_kj, acc[j]); a __syncwarp between consecutive k orders
 //       the read-modify-writes, so every output entry is the fma chain in ascending
 //       k (reading R12 -> bitwise equal to the oracle). B rows are prefetched D
-//       steps ahead into registers (up to R groups of 32 entries per step, groups
-//       beyond nnz_B(k) skipped warp-uniformly) with read-only loads, hiding the L2
-//       latency of the gather; the R loads / fmas / stores of a step are issued as
-//       three batches on 32-bit shared addresses.
+//       steps ahead into registers (up to R groups of 32 entries per step; groups
+//       beyond nnz_B(k) are skipped warp-uniformly) with read-only loads, hiding the
+//       L2 latency of the gather; a step's R shared loads, fmas and shared stores
+//       are issued as batches on 32-bit shared addresses.
 //   a3  combine + drop + compact: Old_i entries (C_old / the SP2 iterate) are merged
 //       into the window with c = fma(alpha, s, beta*old); a window scan (two slots
 //       per lane, 16-byte shared loads) keeps |c| > tau, compacts with ballot/popc
-//       and writes the row contiguously in ascending column order, counting
-//       overflow past C.w.
+//       and writes the row contiguously in ascending column order with predicated
+//       stores, counting overflow past C.w.
 //   a4  per-row trace / norm inputs (stored a_ii, pre-drop s_ii, stored c_ii,
 //       ||S - Old||^2), reduced later in canonical order (reduce.cu).
 // With A = B = Old = X this single kernel is the fused SP2 step (BJ north_star (2)):
 // SQUARE = (alpha 1, old_mode 2), EXPAND = (alpha -1, beta 2, old_mode 1) since
 // fma(-1, s, 2x) = round(2x - s) exactly (2x is exact).
+//
+// Template parameters: R (B groups of 32 per prefetched step), D (prefetch depth),
+// MODE (0: no Old operand; 1: Old operand; 2: Old operand + ||S - Old||^2 norm). Whether
+// Old enters the value (beta*old, p.old_mode == 1) or only the union (p.old_mode == 2)
+// is a runtime, warp-uniform choice.
 #include "internal.cuh"
 #include <climits>
 
@@ -67,11 +72,6 @@ __device__ __forceinline__ void lds128(uint32_t a, double& x, double& y) {
 __device__ __forceinline__ void sts128(uint32_t a, double x, double y) {
     asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x), "d"(y) : "memory");
 }
-__device__ __forceinline__ uint32_t lds8(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-    return v;
-}
 __device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
@@ -84,135 +84,28 @@ __device__ __forceinline__ void sts16u(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
-// Per-warp shared layout: acc[S] f64 | stage: ak[kStage] i32, anb[kStage] i32, ast[kStage] i32,
-// aa[kStage] f64 | flags[S] u8 (only when old_mode != 0)
+// Per-warp shared layout: acc[S] f64 | stage: boff[kStage] i64, aa[kStage] f64,
+// anb[kStage] i32, ast[kStage] i32 | flags[S] u8 (MODE != 0 only)
 struct WarpSmem {
-    uint32_t acc;   // shared address of acc[0]
-    uint32_t flg;   // shared address of flags[0]
-    int* ak;
+    uint32_t acc;  // shared address of acc[0]
+    uint32_t flg;  // shared address of flags[0]
+    long long* boff;
+    double* aa;
     int* anb;
     int* ast;
-    double* aa;
 };
 
 __host__ __device__ inline size_t warp_smem_bytes(int S, bool has_old) {
-    return (size_t)S * 8 + (size_t)kStage * 20 + (has_old ? (size_t)S : 0);
+    return (size_t)S * 8 + (size_t)kStage * 24 + (has_old ? (size_t)S : 0);
 }
 
-struct RowCtx {
-    const RowOpParams* p;
-    WarpSmem w;
-    int lane;
-};
-
-// Load one prefetched step (R groups of 32 entries of B row k starting at st) into the ring slot.
-template <int R>
-__device__ __forceinline__ void load_step(const RowOpParams& p, const WarpSmem& w, int lane, int t,
-                                          int (&rj)[R], double (&rv)[R]) {
-    const int k = w.ak[t];
-    const int nb = w.anb[t];
-    const int st = w.ast[t];
-    const int32_t* bc = p.B.col + (size_t)k * p.B.w;
-    const double* bv = p.B.val + (size_t)k * p.B.w;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        rj[r] = INT_MAX;
-        if (32 * r < nb - st) {
-            const int q = st + 32 * r + lane;
-            if (q < nb) {
-                rj[r] = __ldg(bc + q);
-                rv[r] = __ldg(bv + q);
-            }
-        }
-    }
-}
-
-// Accumulate steps [0, cnt) of the staged piece into the window [c0, c0 + width).
-// MULTI: entries at or beyond c0 + width are left for later passes (cursor advanced by the
-// in-range count); otherwise they are violations (reported through *viol).
-template <int R, int D, bool MULTI>
-__device__ __forceinline__ void accumulate_piece(const RowOpParams& p, const WarpSmem& w, int lane, int cnt,
-                                                 int c0, int width, unsigned* viol) {
-    int rj[D][R];
-    double rv[D][R];
-#pragma unroll
-    for (int d = 0; d < D; ++d)
-        if (d < cnt) load_step<R>(p, w, lane, d, rj[d], rv[d]);
-    unsigned bad = 0;
-    for (int t0 = 0; t0 < cnt; t0 += D) {
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-            const int t = t0 + d;
-            if (t < cnt) {
-                const double a = w.aa[t];
-                const int nb = w.anb[t];
-                const int st = w.ast[t];
-                const int rem = nb - st;
-                // batch 1: in-range test + shared loads
-                uint32_t ad[R];
-                double old[R];
-                bool inr[R];
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const unsigned off = (unsigned)(rj[d][r] - c0);
-                    inr[r] = (32 * r < rem) && off < (unsigned)width;
-                    ad[r] = w.acc + off * 8u;
-                    if (!MULTI && (32 * r < rem) && rj[d][r] != INT_MAX && !inr[r]) bad = 1;
-                    if (inr[r]) old[r] = lds64(ad[r]);
-                }
-                // batch 2: fma + shared stores
-#pragma unroll
-                for (int r = 0; r < R; ++r)
-                    if (inr[r]) sts64(ad[r], __fma_rn(a, rv[d][r], old[r]));
-                int n_in = 0;
-                if (MULTI) {
-#pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if (32 * r < rem) n_in += __popc(__ballot_sync(FULL, inr[r]));
-                }
-                if (rem > 32 * R && (!MULTI || n_in == 32 * R)) {
-                    // B row longer than the prefetched groups: finish it here (rare).
-                    const int k = w.ak[t];
-                    const int32_t* bc = p.B.col + (size_t)k * p.B.w;
-                    const double* bv = p.B.val + (size_t)k * p.B.w;
-                    for (int q0 = st + 32 * R; q0 < nb; q0 += 64) {
-                        const int qa = q0 + lane, qb = q0 + 32 + lane;
-                        const int ja = qa < nb ? __ldg(bc + qa) : INT_MAX;
-                        const int jb = qb < nb ? __ldg(bc + qb) : INT_MAX;
-                        const double va = qa < nb ? __ldg(bv + qa) : 0.0;
-                        const double vb = qb < nb ? __ldg(bv + qb) : 0.0;
-                        const unsigned oa = (unsigned)(ja - c0), ob = (unsigned)(jb - c0);
-                        const bool ia = oa < (unsigned)width, ib = ob < (unsigned)width;
-                        if (!MULTI && ((ja != INT_MAX && !ia) || (jb != INT_MAX && !ib))) bad = 1;
-                        double xa = 0.0, xb = 0.0;
-                        if (ia) xa = lds64(w.acc + oa * 8u);
-                        if (ib) xb = lds64(w.acc + ob * 8u);
-                        if (ia) sts64(w.acc + oa * 8u, __fma_rn(a, va, xa));
-                        if (ib) sts64(w.acc + ob * 8u, __fma_rn(a, vb, xb));
-                        if (MULTI) {
-                            const int na = __popc(__ballot_sync(FULL, ia));
-                            const int nbb = __popc(__ballot_sync(FULL, ib));
-                            n_in += na + nbb;
-                            if (na + nbb < 64) break;
-                        }
-                    }
-                }
-                if (MULTI && lane == 0) w.ast[t] = st + n_in;
-                if (t + D < cnt) load_step<R>(p, w, lane, t + D, rj[d], rv[d]);
-                __syncwarp();
-            }
-        }
-    }
-    if (!MULTI) *viol |= __ballot_sync(FULL, bad);
-}
-
-// Stage A-row entries [p0, p0 + cnt) into shared memory (k, a, nnz_B(k), cursor).
+// Stage A-row entries [p0, p0 + cnt): B-row offset k*B.w, a_ik, nnz_B(k), cursor.
 __device__ __forceinline__ void stage_piece(const RowOpParams& p, const WarpSmem& w, int lane,
                                             const int32_t* a_col, const double* a_val, int p0, int cnt,
                                             const int32_t* cur) {
     for (int q = lane; q < cnt; q += 32) {
         const int k = a_col[p0 + q];
-        w.ak[q] = k;
+        w.boff[q] = (long long)k * p.B.w;
         w.aa[q] = a_val[p0 + q];
         w.anb[q] = __ldg(p.B.nnz + k);
         w.ast[q] = cur ? cur[p0 + q] : 0;
@@ -220,8 +113,132 @@ __device__ __forceinline__ void stage_piece(const RowOpParams& p, const WarpSmem
     __syncwarp();
 }
 
+// ---------------------------------------------------------------------------- fast path
+
+// Accumulate the staged steps [0, cnt) into the window [c0, c0 + width); every entry is
+// expected inside it (a miss sets `bad`, the row then reruns on the general path).
+template <int R, int D>
+__device__ __forceinline__ void accumulate_fast(const RowOpParams& p, const WarpSmem& w, int lane, int cnt,
+                                                int c0, int width, unsigned& bad) {
+    int rj[D][R];
+    double rv[D][R];
+    double ra[D];
+    int rnb[D];
+    const int32_t* __restrict__ bcol = p.B.col;
+    const double* __restrict__ bval = p.B.val;
+    auto load = [&](int d, int t) {
+        const long long bo = w.boff[t];
+        const int nb = w.anb[t];
+        ra[d] = w.aa[t];
+        rnb[d] = nb;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            rj[d][r] = INT_MAX;
+            if (32 * r < nb) {
+                const int q = 32 * r + lane;
+                if (q < nb) {
+                    rj[d][r] = __ldg(bcol + bo + q);
+                    rv[d][r] = __ldg(bval + bo + q);
+                }
+            }
+        }
+    };
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+        if (d < cnt) load(d, d);
+    for (int t0 = 0; t0 < cnt; t0 += D) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            const int t = t0 + d;
+            if (t < cnt) {
+                const double a = ra[d];
+                const int nb = rnb[d];
+                uint32_t ad[R];
+                double old[R];
+                bool inr[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    inr[r] = false;
+                    if (32 * r < nb) {
+                        const unsigned off = (unsigned)(rj[d][r] - c0);
+                        inr[r] = off < (unsigned)width;
+                        bad |= (unsigned)((rj[d][r] != INT_MAX) & !inr[r]);
+                        ad[r] = w.acc + off * 8u;
+                        if (inr[r]) old[r] = lds64(ad[r]);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    if (inr[r]) sts64(ad[r], __fma_rn(a, rv[d][r], old[r]));
+                if (nb > 32 * R) {
+                    // B row longer than the prefetched groups: finish it here.
+                    const long long bo = w.boff[t];
+                    for (int q0 = 32 * R; q0 < nb; q0 += 64) {
+                        const int qa = q0 + lane, qb = q0 + 32 + lane;
+                        const int ja = qa < nb ? __ldg(bcol + bo + qa) : INT_MAX;
+                        const int jb = qb < nb ? __ldg(bcol + bo + qb) : INT_MAX;
+                        const double va = qa < nb ? __ldg(bval + bo + qa) : 0.0;
+                        const double vb = qb < nb ? __ldg(bval + bo + qb) : 0.0;
+                        const unsigned oa = (unsigned)(ja - c0), ob = (unsigned)(jb - c0);
+                        const bool ia = oa < (unsigned)width, ib = ob < (unsigned)width;
+                        bad |= (unsigned)(((ja != INT_MAX) & !ia) | ((jb != INT_MAX) & !ib));
+                        double xa = 0.0, xb = 0.0;
+                        if (ia) xa = lds64(w.acc + oa * 8u);
+                        if (ib) xb = lds64(w.acc + ob * 8u);
+                        if (ia) sts64(w.acc + oa * 8u, __fma_rn(a, va, xa));
+                        if (ib) sts64(w.acc + ob * 8u, __fma_rn(a, vb, xb));
+                    }
+                }
+                if (t + D < cnt) load(d, t + D);
+                __syncwarp();
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------- general path
+
+// Multi-pass accumulate: entries at or beyond c0 + width are left for later passes; the
+// staged cursor ast[t] advances by the in-range count.
+template <int R, int D>
+__device__ __forceinline__ void accumulate_multi(const RowOpParams& p, const WarpSmem& w, int lane, int cnt,
+                                                 int c0, int width) {
+    const int32_t* __restrict__ bcol = p.B.col;
+    const double* __restrict__ bval = p.B.val;
+    for (int t = 0; t < cnt; ++t) {
+        const long long bo = w.boff[t];
+        const int nb = w.anb[t];
+        const int st = w.ast[t];
+        const double a = w.aa[t];
+        int q0 = st, n_in = 0;
+        while (q0 < nb) {
+            const int qa = q0 + lane, qb = q0 + 32 + lane;
+            const int ja = qa < nb ? __ldg(bcol + bo + qa) : INT_MAX;
+            const int jb = qb < nb ? __ldg(bcol + bo + qb) : INT_MAX;
+            const unsigned oa = (unsigned)(ja - c0), ob = (unsigned)(jb - c0);
+            const bool ia = oa < (unsigned)width, ib = ob < (unsigned)width;
+            const double va = ia ? __ldg(bval + bo + qa) : 0.0;
+            const double vb = ib ? __ldg(bval + bo + qb) : 0.0;
+            double xa = 0.0, xb = 0.0;
+            if (ia) xa = lds64(w.acc + oa * 8u);
+            if (ib) xb = lds64(w.acc + ob * 8u);
+            if (ia) sts64(w.acc + oa * 8u, __fma_rn(a, va, xa));
+            if (ib) sts64(w.acc + ob * 8u, __fma_rn(a, vb, xb));
+            const int n = __popc(__ballot_sync(FULL, ia)) + __popc(__ballot_sync(FULL, ib));
+            n_in += n;
+            if (n < 64) break;
+            q0 += 64;
+        }
+        if (lane == 0) w.ast[t] = st + n_in;
+        __syncwarp();
+    }
+}
+
+// --------------------------------------------------------------------- combine and emit
+
 // Combine Old entries with columns in [c0, c0 + width): acc <- fma(alpha, s, beta*old), flag.
 // Returns false (fast path) if an Old entry lies outside the window.
+template <int MODE>
 __device__ __forceinline__ bool combine_old(const RowOpParams& p, const WarpSmem& w, int lane,
                                             const int32_t* o_col, const double* o_val, int nOld,
                                             int& old_cur, int c0, int width, bool multi, double& nrm) {
@@ -236,7 +253,7 @@ __device__ __forceinline__ bool combine_old(const RowOpParams& p, const WarpSmem
         if (inr) {
             const double x = o_val[q];
             const double s = lds64(w.acc + off * 8u);
-            if (p.normsq) {
+            if (MODE == 2) {
                 const double df = __dsub_rn(s, x);
                 nrm = __fma_rn(df, df, nrm);
             }
@@ -252,13 +269,19 @@ __device__ __forceinline__ bool combine_old(const RowOpParams& p, const WarpSmem
     return __all_sync(FULL, ok);
 }
 
-// Emit window [0, width) (columns c0 + jj): drop, compact, write at C row offset; clears the window.
+// Emit window slots [0, width) (columns c0 + jj, width even): drop, compact, write into the
+// C row at `kept`; clears the window (and flags).
+template <int MODE>
 __device__ __forceinline__ void emit_window(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
-                                            size_t c_off, int c0, int width, int64_t ncols, int& kept,
-                                            double& dc, double& nrm) {
-    const bool has_old = p.old_mode != 0;
+                                            double* __restrict__ crow_v, int32_t* __restrict__ crow_c,
+                                            int c0, int width, int64_t ncols, int& kept, double& dc,
+                                            double& nrm) {
     const unsigned lt_mask = (1u << lane) - 1u;
-    // two slots per lane: columns c0 + b + 2*lane, +1 (width is a multiple of 2)
+    const int cw = p.C.w;
+    const double tau = p.tau, alpha = p.alpha;
+    const bool a1 = alpha == 1.0;
+    const int jdiag = (int)(i - c0);
+    const int jmax = (int)((ncols - c0) < (int64_t)width ? (ncols - c0) : (int64_t)width);
     for (int b = 0; b < width; b += 64) {
         const int jj = b + 2 * lane;
         const bool in = jj < width;
@@ -267,74 +290,68 @@ __device__ __forceinline__ void emit_window(const RowOpParams& p, const WarpSmem
         if (in) {
             lds128(w.acc + (uint32_t)jj * 8u, v0, v1);
             sts128(w.acc + (uint32_t)jj * 8u, 0.0, 0.0);
-            if (has_old) {
+            if (MODE != 0) {
                 f = lds16u(w.flg + jj);
                 sts16u(w.flg + jj, 0u);
             }
         }
-        double c0v, c1v;
-        if (f & 0xffu) c0v = v0;
-        else {
-            c0v = __fma_rn(p.alpha, v0, 0.0);
-            if (p.normsq) nrm = __fma_rn(v0, v0, nrm);
+        double x0 = v0, x1 = v1;
+        if (!(f & 0xffu)) {
+            if (!a1) x0 = __dmul_rn(alpha, v0);
+            if (MODE == 2) nrm = __fma_rn(v0, v0, nrm);
         }
-        if (f & 0xff00u) c1v = v1;
-        else {
-            c1v = __fma_rn(p.alpha, v1, 0.0);
-            if (p.normsq) nrm = __fma_rn(v1, v1, nrm);
+        if (!(f & 0xff00u)) {
+            if (!a1) x1 = __dmul_rn(alpha, v1);
+            if (MODE == 2) nrm = __fma_rn(v1, v1, nrm);
         }
-        const int64_t col0 = (int64_t)c0 + jj;
-        const bool k0 = in && col0 < ncols && fabs(c0v) > p.tau;
-        const bool k1 = in && col0 + 1 < ncols && fabs(c1v) > p.tau;
+        const bool k0 = (jj < jmax) && fabs(x0) > tau;
+        const bool k1 = (jj + 1 < jmax) && fabs(x1) > tau;
         const unsigned m0 = __ballot_sync(FULL, k0);
         const unsigned m1 = __ballot_sync(FULL, k1);
-        const int before = __popc(m0 & lt_mask) + __popc(m1 & lt_mask);
-        int pos = kept + before;
-        if (k0) {
-            if (pos < p.C.w) {
-                p.C.val[c_off + pos] = c0v;
-                p.C.col[c_off + pos] = (int32_t)col0;
-            }
-            if (col0 == i) dc = c0v;
-            ++pos;
+        const int pos0 = kept + __popc(m0 & lt_mask) + __popc(m1 & lt_mask);
+        const int pos1 = pos0 + (k0 ? 1 : 0);
+        if (k0 && pos0 < cw) {
+            crow_v[pos0] = x0;
+            crow_c[pos0] = c0 + jj;
         }
-        if (k1) {
-            if (pos < p.C.w) {
-                p.C.val[c_off + pos] = c1v;
-                p.C.col[c_off + pos] = (int32_t)(col0 + 1);
-            }
-            if (col0 + 1 == i) dc = c1v;
+        if (k1 && pos1 < cw) {
+            crow_v[pos1] = x1;
+            crow_c[pos1] = c0 + jj + 1;
         }
+        if (k0 && jj == jdiag) dc = x0;
+        if (k1 && jj + 1 == jdiag) dc = x1;
         kept += __popc(m0) + __popc(m1);
     }
     __syncwarp();
 }
 
-// Zero the window (after an abandoned fast-path attempt).
-__device__ __forceinline__ void clear_window(const WarpSmem& w, int lane, int S, bool has_old) {
+// Zero the window (after an abandoned fast-path attempt / at start).
+template <int MODE>
+__device__ __forceinline__ void clear_window(const WarpSmem& w, int lane, int S) {
     for (int jj = 2 * lane; jj < S; jj += 64) {
         sts128(w.acc + (uint32_t)jj * 8u, 0.0, 0.0);
-        if (has_old) sts16u(w.flg + jj, 0u);
+        if (MODE != 0) sts16u(w.flg + jj, 0u);
     }
     __syncwarp();
 }
 
-template <int R, int D>
-__global__ void __launch_bounds__(128) row_op_kernel(const RowOpParams p) {
+// -------------------------------------------------------------------------------- kernel
+
+template <int R, int D, int MODE>
+__global__ void __launch_bounds__(128, 1) row_op_kernel(const RowOpParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int S = p.S;
-    const bool has_old = p.old_mode != 0;
-    unsigned char* base = smem_raw + (size_t)wid * warp_smem_bytes(S, has_old);
+    unsigned char* base = smem_raw + (size_t)wid * warp_smem_bytes(S, MODE != 0);
     WarpSmem w;
     w.acc = (uint32_t)__cvta_generic_to_shared(base);
-    w.ak = reinterpret_cast<int*>(base + (size_t)S * 8);
-    w.anb = w.ak + kStage;
+    w.boff = reinterpret_cast<long long*>(base + (size_t)S * 8);
+    w.aa = reinterpret_cast<double*>(w.boff + kStage);
+    w.anb = reinterpret_cast<int*>(w.aa + kStage);
     w.ast = w.anb + kStage;
-    w.aa = reinterpret_cast<double*>(w.ast + kStage);
-    w.flg = w.acc + (uint32_t)(S * 8 + kStage * 20);
-    clear_window(w, lane, S, has_old);
+    w.flg = w.acc + (uint32_t)(S * 8 + kStage * 24);
+    clear_window<MODE>(w, lane, S);
 
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -348,11 +365,13 @@ __global__ void __launch_bounds__(128) row_op_kernel(const RowOpParams p) {
         const double* o_val = nullptr;
         const int32_t* o_col = nullptr;
         int32_t nOld = 0;
-        if (has_old) {
+        if (MODE != 0) {
             o_val = p.Old.val + (size_t)i * p.Old.w;
             o_col = p.Old.col + (size_t)i * p.Old.w;
             nOld = p.Old.nnz[i];
         }
+        double* crow_v = p.C.val + (size_t)i * p.C.w;
+        int32_t* crow_c = p.C.col + (size_t)i * p.C.w;
         // stored diagonal of A (x2 traces)
         double dA = 0.0;
         if (p.diag_a) {
@@ -365,36 +384,34 @@ __global__ void __launch_bounds__(128) row_op_kernel(const RowOpParams p) {
 
         int32_t kept = 0;
         double ds = 0.0, dc = 0.0, nrm = 0.0;
-        const size_t c_off = (size_t)i * p.C.w;
         bool done = false;
 
         if (p.fast) {
-            // ---- fast path: one pass over the row-centred window
+            // ---- fast path: one pass over the row-centred window (c0 even)
             int c0 = 0;
             if ((int64_t)S < ncols) {
                 int64_t c = i - (S >> 1);
                 if (c < 0) c = 0;
                 if (c > ncols - S) c = ncols - S;
-                c0 = (int)c;
+                c0 = (int)(c & ~int64_t(1));
             }
-            unsigned viol = 0;
+            unsigned bad = 0;
             for (int p0 = 0; p0 < nA; p0 += kStage) {
                 const int cnt = min(kStage, nA - p0);
                 stage_piece(p, w, lane, a_col, a_val, p0, cnt, nullptr);
-                accumulate_piece<R, D, false>(p, w, lane, cnt, c0, S, &viol);
+                accumulate_fast<R, D>(p, w, lane, cnt, c0, S, bad);
             }
-            __syncwarp();
-            bool ok = viol == 0;
+            bool ok = __ballot_sync(FULL, bad) == 0;
             if (ok) {
                 if ((int64_t)c0 <= i && i < (int64_t)c0 + S) ds = lds64(w.acc + (uint32_t)(i - c0) * 8u);
                 int old_cur = 0;
-                if (has_old) ok = combine_old(p, w, lane, o_col, o_val, nOld, old_cur, c0, S, false, nrm);
+                if (MODE != 0) ok = combine_old<MODE>(p, w, lane, o_col, o_val, nOld, old_cur, c0, S, false, nrm);
             }
             if (ok) {
-                emit_window(p, w, lane, i, c_off, c0, S, ncols, kept, dc, nrm);
+                emit_window<MODE>(p, w, lane, i, crow_v, crow_c, c0, S, ncols, kept, dc, nrm);
                 done = true;
             } else {
-                clear_window(w, lane, S, has_old);
+                clear_window<MODE>(w, lane, S);
                 nrm = 0.0;
                 ds = 0.0;
             }
@@ -412,11 +429,11 @@ __global__ void __launch_bounds__(128) row_op_kernel(const RowOpParams p) {
                     hi = max(hi, __ldg(bc + nb - 1));
                 }
             }
-            if (nOld > 0 && lane == 0) {
+            if (MODE != 0 && nOld > 0 && lane == 0) {
                 lo = min(lo, o_col[0]);
                 hi = max(hi, o_col[nOld - 1]);
             }
-            lo = warp_min(lo) & ~1;  // even start: 16-byte aligned window slots
+            lo = warp_min(lo) & ~1;  // even window start (16-byte slot pairs)
             hi = warp_max(hi);
             if (hi >= lo) {
                 const int span = hi - lo + 1;
@@ -431,7 +448,7 @@ __global__ void __launch_bounds__(128) row_op_kernel(const RowOpParams p) {
                         a_val = sv; a_col = sc;
                         sv += p.A.w; sc += p.A.w;
                     }
-                    if (p.stash_old) {
+                    if (MODE != 0 && p.stash_old) {
                         for (int q = lane; q < nOld; q += 32) { sv[q] = o_val[q]; sc[q] = o_col[q]; }
                         o_val = sv; o_col = sc;
                     }
@@ -443,11 +460,11 @@ __global__ void __launch_bounds__(128) row_op_kernel(const RowOpParams p) {
                 int old_cur = 0;
                 for (int pass = 0; pass < npass; ++pass) {
                     const int c0 = lo + pass * S;
-                    const int width = min(S, hi + 1 - c0 + 1) & ~1;  // even, covers [c0, hi]
+                    const int width = min(S, hi + 2 - c0) & ~1;  // even, covers [c0, hi]
                     for (int p0 = 0; p0 < nA; p0 += kStage) {
                         const int cnt = min(kStage, nA - p0);
                         stage_piece(p, w, lane, a_col, a_val, p0, cnt, multi ? cur : nullptr);
-                        accumulate_piece<R, D, true>(p, w, lane, cnt, c0, width, nullptr);
+                        accumulate_multi<R, D>(p, w, lane, cnt, c0, width);
                         if (multi) {
                             for (int q = lane; q < cnt; q += 32) cur[p0 + q] = w.ast[q];
                             __syncwarp();
@@ -455,8 +472,8 @@ __global__ void __launch_bounds__(128) row_op_kernel(const RowOpParams p) {
                     }
                     __syncwarp();
                     if ((int64_t)c0 <= i && i < (int64_t)c0 + width) ds = lds64(w.acc + (uint32_t)(i - c0) * 8u);
-                    if (has_old) combine_old(p, w, lane, o_col, o_val, nOld, old_cur, c0, width, true, nrm);
-                    emit_window(p, w, lane, i, c_off, c0, width, ncols, kept, dc, nrm);
+                    if (MODE != 0) combine_old<MODE>(p, w, lane, o_col, o_val, nOld, old_cur, c0, width, true, nrm);
+                    emit_window<MODE>(p, w, lane, i, crow_v, crow_c, c0, width, ncols, kept, dc, nrm);
                 }
             }
         }
@@ -471,7 +488,7 @@ __global__ void __launch_bounds__(128) row_op_kernel(const RowOpParams p) {
         }
         if (p.diag_s && lane == 0) p.diag_s[i] = ds;
         if (p.diag_a && lane == 0) p.diag_a[i] = dA;
-        if (p.normsq) {
+        if (MODE == 2 && p.normsq) {
             nrm = warp_sum(nrm);
             if (lane == 0) p.normsq[i] = nrm;
         }
@@ -483,15 +500,13 @@ __global__ void __launch_bounds__(128) row_op_kernel(const RowOpParams p) {
 }
 
 // Half-bandwidth probe: out[m] = max over rows of max(i - col[i][0], col[i][nnz-1] - i).
-__global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64_t r1,
-                                 int64_t n, int32_t* out) {
+__global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int64_t r0, int64_t r1, int64_t n, int32_t* out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int bw[3] = {0, 0, 0};
     const KMat* ms[3] = {&a, &b, &c};
     if (i < n) {
 #pragma unroll
         for (int m = 0; m < 3; ++m) {
-            if (m >= nmat) break;
             // A and Old only matter on the computed rows; B on every row
             if (m != 1 && (i < r0 || i >= r1)) continue;
             const KMat& x = *ms[m];
@@ -499,8 +514,7 @@ __global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int nmat, int64_t r0, i
             const int nz = x.nnz[i];
             if (nz > 0) {
                 const int f = x.col[(size_t)i * x.w], l = x.col[(size_t)i * x.w + nz - 1];
-                bw[m] = max((int)(i - f), (int)(l - i));
-                bw[m] = max(bw[m], 0);
+                bw[m] = max(max((int)(i - f), (int)(l - i)), 0);
             }
         }
     }
@@ -515,18 +529,44 @@ __global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int nmat, int64_t r0, i
 
 cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64_t r1, int64_t n,
                              int32_t* out, cudaStream_t s) {
-    bandwidth_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, c, nmat, r0, r1, n, out);
+    (void)nmat;
+    bandwidth_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, c, r0, r1, n, out);
     return cudaGetLastError();
 }
 
-template <int R, int D>
-static cudaError_t prep(const LaunchCfg& cfg, int* blocks_per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(row_op_kernel<R, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)cfg.smem);
+// ----------------------------------------------------------------------------- dispatch
+
+template <int R, int D, int MODE>
+static cudaError_t prep_one(const LaunchCfg& cfg, int* bps) {
+    cudaError_t e = cudaFuncSetAttribute(row_op_kernel<R, D, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
     if (e) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, row_op_kernel<R, D>,
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, row_op_kernel<R, D, MODE>,
                                                          cfg.warps_per_cta * 32, cfg.smem);
 }
+
+template <int MODE>
+static cudaError_t prep_mode(const LaunchCfg& cfg, int* bps) {
+    switch (cfg.R) {
+        case 1: return prep_one<1, 8, MODE>(cfg, bps);
+        case 2: return prep_one<2, 6, MODE>(cfg, bps);
+        case 4: return prep_one<4, 4, MODE>(cfg, bps);
+        default: return prep_one<8, 3, MODE>(cfg, bps);
+    }
+}
+
+template <int MODE>
+static void launch_mode(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s) {
+    dim3 block(cfg.warps_per_cta * 32), grid(cfg.grid);
+    switch (cfg.R) {
+        case 1: row_op_kernel<1, 8, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 2: row_op_kernel<2, 6, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 4: row_op_kernel<4, 4, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        default: row_op_kernel<8, 3, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+    }
+}
+
+static int mode_of(const RowOpParams& p) { return p.old_mode == 0 ? 0 : (p.normsq ? 2 : 1); }
 
 static int pick_R(int wb) {
     if (wb <= 32) return 1;
@@ -549,14 +589,10 @@ cudaError_t plan_row_op(const RowOpParams& p, int S, int warps_opt, int num_sms,
     cfg->warps_per_cta = wpc;
     cfg->R = pick_R(p.B.w);
     cfg->smem = (size_t)wpc * per_warp;
-    cudaError_t e;
     int bps = 0;
-    switch (cfg->R) {
-        case 1: e = prep<1, 8>(*cfg, &bps); break;
-        case 2: e = prep<2, 6>(*cfg, &bps); break;
-        case 4: e = prep<4, 4>(*cfg, &bps); break;
-        default: e = prep<8, 3>(*cfg, &bps); break;
-    }
+    const int mode = mode_of(p);
+    cudaError_t e = mode == 0 ? prep_mode<0>(*cfg, &bps) : mode == 1 ? prep_mode<1>(*cfg, &bps)
+                                                                      : prep_mode<2>(*cfg, &bps);
     if (e) return e;
     if (bps < 1) return cudaErrorInvalidConfiguration;
     const int64_t rows = p.row_end - p.row_begin;
@@ -567,13 +603,10 @@ cudaError_t plan_row_op(const RowOpParams& p, int S, int warps_opt, int num_sms,
 }
 
 cudaError_t launch_row_op(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s) {
-    dim3 block(cfg.warps_per_cta * 32), grid(cfg.grid);
-    switch (cfg.R) {
-        case 1: row_op_kernel<1, 8><<<grid, block, cfg.smem, s>>>(p); break;
-        case 2: row_op_kernel<2, 6><<<grid, block, cfg.smem, s>>>(p); break;
-        case 4: row_op_kernel<4, 4><<<grid, block, cfg.smem, s>>>(p); break;
-        default: row_op_kernel<8, 3><<<grid, block, cfg.smem, s>>>(p); break;
-    }
+    const int mode = mode_of(p);
+    if (mode == 0) launch_mode<0>(p, cfg, s);
+    else if (mode == 1) launch_mode<1>(p, cfg, s);
+    else launch_mode<2>(p, cfg, s);
     return cudaGetLastError();
 }
 
