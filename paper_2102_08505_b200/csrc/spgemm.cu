@@ -72,6 +72,11 @@ __device__ __forceinline__ void lds128(uint32_t a, double& x, double& y) {
 __device__ __forceinline__ void sts128(uint32_t a, double x, double y) {
     asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x), "d"(y) : "memory");
 }
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
 __device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
@@ -281,60 +286,72 @@ __device__ __forceinline__ bool combine_old(const RowOpParams& p, const WarpSmem
     return __all_sync(FULL, ok);
 }
 
-// Emit window slots [0, width) (columns c0 + jj, width even): drop, compact, write into the
-// C row at `kept`; clears the window (and flags).
-template <int MODE>
-__device__ __forceinline__ void emit_window(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
-                                            double* __restrict__ crow_v, int32_t* __restrict__ crow_c,
-                                            int c0, int width, int64_t ncols, int& kept, double& dc,
-                                            double& nrm) {
+// Emit window slots [0, width) (columns c0 + jj): drop, compact, write into the C row at
+// `kept`; clears the window (and flags). One slot per lane per sub-step (four sub-steps per
+// iteration), so every ballot-compacted run is a contiguous, coalesced store. Slots for
+// columns >= N hold +0 and are never kept (tau >= 0). The stored diagonal c_ii is read by
+// the caller before the emit (window_diag).
+template <int MODE, bool A1>
+__device__ __forceinline__ void emit_window_t(const RowOpParams& p, const WarpSmem& w, int lane,
+                                              double* __restrict__ crow_v, int32_t* __restrict__ crow_c,
+                                              int c0, int width, int& kept, double& nrm) {
     const unsigned lt_mask = (1u << lane) - 1u;
     const int cw = p.C.w;
     const double tau = p.tau, alpha = p.alpha;
-    const bool a1 = alpha == 1.0;
-    const int jdiag = (int)(i - c0);
-    const int jmax = (int)((ncols - c0) < (int64_t)width ? (ncols - c0) : (int64_t)width);
-    for (int b = 0; b < width; b += 64) {
-        const int jj = b + 2 * lane;
-        const bool in = jj < width;
-        double v0 = 0.0, v1 = 0.0;
-        uint32_t f = 0;
-        if (in) {
-            lds128(w.acc + (uint32_t)jj * 8u, v0, v1);
-            sts128(w.acc + (uint32_t)jj * 8u, 0.0, 0.0);
-            if (MODE != 0) {
-                f = lds16u(w.flg + jj);
-                sts16u(w.flg + jj, 0u);
+    for (int b = 0; b < width; b += 128) {
+        double v[4];
+        uint32_t f[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const int jj = b + 32 * s + lane;
+            v[s] = 0.0;
+            f[s] = 0;
+            if (jj < width) {
+                const uint32_t ad = w.acc + (uint32_t)jj * 8u;
+                v[s] = lds64(ad);
+                sts64(ad, 0.0);
+                if (MODE != 0) {
+                    f[s] = lds8(w.flg + jj);
+                    sts8(w.flg + jj, 0u);
+                }
             }
         }
-        double x0 = v0, x1 = v1;
-        if (!(f & 0xffu)) {
-            if (!a1) x0 = __dmul_rn(alpha, v0);
-            if (MODE == 2) nrm = __fma_rn(v0, v0, nrm);
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            double x = v[s];
+            if (MODE == 0 || !f[s]) {
+                if (!A1) x = __dmul_rn(alpha, x);
+                if (MODE == 2) nrm = __fma_rn(v[s], v[s], nrm);
+            }
+            const bool keep = fabs(x) > tau;
+            const unsigned m = __ballot_sync(FULL, keep);
+            const int pos = kept + __popc(m & lt_mask);
+            if (keep && pos < cw) {
+                crow_v[pos] = x;
+                crow_c[pos] = c0 + b + 32 * s + lane;
+            }
+            kept += __popc(m);
         }
-        if (!(f & 0xff00u)) {
-            if (!a1) x1 = __dmul_rn(alpha, v1);
-            if (MODE == 2) nrm = __fma_rn(v1, v1, nrm);
-        }
-        const bool k0 = (jj < jmax) && fabs(x0) > tau;
-        const bool k1 = (jj + 1 < jmax) && fabs(x1) > tau;
-        const unsigned m0 = __ballot_sync(FULL, k0);
-        const unsigned m1 = __ballot_sync(FULL, k1);
-        const int pos0 = kept + __popc(m0 & lt_mask) + __popc(m1 & lt_mask);
-        const int pos1 = pos0 + (k0 ? 1 : 0);
-        if (k0 && pos0 < cw) {
-            crow_v[pos0] = x0;
-            crow_c[pos0] = c0 + jj;
-        }
-        if (k1 && pos1 < cw) {
-            crow_v[pos1] = x1;
-            crow_c[pos1] = c0 + jj + 1;
-        }
-        if (k0 && jj == jdiag) dc = x0;
-        if (k1 && jj + 1 == jdiag) dc = x1;
-        kept += __popc(m0) + __popc(m1);
     }
     __syncwarp();
+}
+
+template <int MODE>
+__device__ __forceinline__ void emit_window(const RowOpParams& p, const WarpSmem& w, int lane,
+                                            double* __restrict__ crow_v, int32_t* __restrict__ crow_c,
+                                            int c0, int width, int& kept, double& nrm) {
+    if (p.alpha == 1.0) emit_window_t<MODE, true>(p, w, lane, crow_v, crow_c, c0, width, kept, nrm);
+    else emit_window_t<MODE, false>(p, w, lane, crow_v, crow_c, c0, width, kept, nrm);
+}
+
+// Stored (post-combine, post-drop) value of window slot jd, or 0 (read before the emit).
+template <int MODE>
+__device__ __forceinline__ double window_diag(const RowOpParams& p, const WarpSmem& w, int jd, int width) {
+    if (jd < 0 || jd >= width) return 0.0;
+    double x = lds64(w.acc + (uint32_t)jd * 8u);
+    const bool flagged = MODE != 0 && lds8(w.flg + jd) != 0;
+    if (!flagged && p.alpha != 1.0) x = __dmul_rn(p.alpha, x);
+    return fabs(x) > p.tau ? x : 0.0;
 }
 
 // Zero the window (after an abandoned fast-path attempt / at start).
@@ -406,7 +423,7 @@ __global__ void __launch_bounds__(128, 1) row_op_kernel(const RowOpParams p) {
                 int64_t c = i - (S >> 1);
                 if (c < 0) c = 0;
                 if (c > ncols - S) c = ncols - S;
-                c0 = (int)(c & ~int64_t(1));
+                c0 = (int)c;
             }
             for (int p0 = 0; p0 < nA; p0 += kStage) {
                 const int cnt = min(kStage, nA - p0);
@@ -421,7 +438,8 @@ __global__ void __launch_bounds__(128, 1) row_op_kernel(const RowOpParams p) {
                 if (MODE != 0) ok = combine_old<MODE>(p, w, lane, o_col, o_val, nOld, old_cur, c0, S, false, nrm);
             }
             if (ok) {
-                emit_window<MODE>(p, w, lane, i, crow_v, crow_c, c0, S, ncols, kept, dc, nrm);
+                if (p.diag_c) dc = window_diag<MODE>(p, w, (int)(i - c0), S);
+                emit_window<MODE>(p, w, lane, crow_v, crow_c, c0, S, kept, nrm);
                 done = true;
             } else {
                 clear_window<MODE>(w, lane, S);
@@ -486,7 +504,9 @@ __global__ void __launch_bounds__(128, 1) row_op_kernel(const RowOpParams p) {
                     __syncwarp();
                     if ((int64_t)c0 <= i && i < (int64_t)c0 + width) ds = lds64(w.acc + (uint32_t)(i - c0) * 8u);
                     if (MODE != 0) combine_old<MODE>(p, w, lane, o_col, o_val, nOld, old_cur, c0, width, true, nrm);
-                    emit_window<MODE>(p, w, lane, i, crow_v, crow_c, c0, width, ncols, kept, dc, nrm);
+                    if (p.diag_c && (int64_t)c0 <= i && i < (int64_t)c0 + width)
+                        dc = window_diag<MODE>(p, w, (int)(i - c0), width);
+                    emit_window<MODE>(p, w, lane, crow_v, crow_c, c0, width, kept, nrm);
                 }
             }
         }
@@ -495,10 +515,7 @@ __global__ void __launch_bounds__(128, 1) row_op_kernel(const RowOpParams p) {
         if (lane == 0) p.C.nnz[i] = kept < p.C.w ? kept : p.C.w;
         my_max_kept = max(my_max_kept, kept);
         if (kept > p.C.w) ++my_ovf;
-        if (p.diag_c) {
-            dc = warp_sum(dc);  // at most one lane holds c_ii != 0; x + 0 = x exactly
-            if (lane == 0) p.diag_c[i] = dc;
-        }
+        if (p.diag_c && lane == 0) p.diag_c[i] = dc;
         if (p.diag_s && lane == 0) p.diag_s[i] = ds;
         if (p.diag_a && lane == 0) p.diag_a[i] = dA;
         if (MODE == 2 && p.normsq) {
@@ -550,7 +567,7 @@ cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64
 // ----------------------------------------------------------------------------- dispatch
 
 // (G groups x V entries per lane, prefetch depth D) by B width: <=32: 1x1 (D 8),
-// <=64: 1x2 (D 8), <=128: 2x2 (D 6), wider: 4x2 (D 4)
+// <=64: 1x2 (D 8), <=128: 2x2 (D 6), wider: 3x2 (D 4; rows past 192 entries finish inline)
 template <int G, int V, int D, int MODE>
 static cudaError_t prep_one(const LaunchCfg& cfg, int* bps) {
     cudaError_t e = cudaFuncSetAttribute(row_op_kernel<G, V, D, MODE>,
@@ -566,7 +583,7 @@ static cudaError_t prep_mode(const LaunchCfg& cfg, int* bps) {
         case 1: return prep_one<1, 1, 8, MODE>(cfg, bps);
         case 2: return prep_one<1, 2, 8, MODE>(cfg, bps);
         case 4: return prep_one<2, 2, 6, MODE>(cfg, bps);
-        default: return prep_one<4, 2, 4, MODE>(cfg, bps);
+        default: return prep_one<3, 2, 4, MODE>(cfg, bps);
     }
 }
 
@@ -577,7 +594,7 @@ static void launch_mode(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t
         case 1: row_op_kernel<1, 1, 8, MODE><<<grid, block, cfg.smem, s>>>(p); break;
         case 2: row_op_kernel<1, 2, 8, MODE><<<grid, block, cfg.smem, s>>>(p); break;
         case 4: row_op_kernel<2, 2, 6, MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        default: row_op_kernel<4, 2, 4, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        default: row_op_kernel<3, 2, 4, MODE><<<grid, block, cfg.smem, s>>>(p); break;
     }
 }
 
