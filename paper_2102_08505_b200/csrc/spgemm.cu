@@ -316,22 +316,29 @@ __device__ __forceinline__ void emit_window_t(const RowOpParams& p, const WarpSm
                 }
             }
         }
+        double x[4];
+        unsigned m[4];
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
-            double x = v[s];
+            x[s] = v[s];
             if (MODE == 0 || !f[s]) {
-                if (!A1) x = __dmul_rn(alpha, x);
+                if (!A1) x[s] = __dmul_rn(alpha, v[s]);
                 if (MODE == 2) nrm = __fma_rn(v[s], v[s], nrm);
             }
-            const bool keep = fabs(x) > tau;
-            const unsigned m = __ballot_sync(FULL, keep);
-            const int pos = kept + __popc(m & lt_mask);
-            if (keep && pos < cw) {
-                crow_v[pos] = x;
+            m[s] = __ballot_sync(FULL, fabs(x[s]) > tau);
+        }
+        // positions of the four runs are independent: no serial dependence on `kept`
+        int before = kept;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const int pos = before + __popc(m[s] & lt_mask);
+            if (((m[s] >> lane) & 1u) && pos < cw) {
+                crow_v[pos] = x[s];
                 crow_c[pos] = c0 + b + 32 * s + lane;
             }
-            kept += __popc(m);
+            before += __popc(m[s]);
         }
+        kept = before;
     }
     __syncwarp();
 }
@@ -567,7 +574,7 @@ cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64
 // ----------------------------------------------------------------------------- dispatch
 
 // (G groups x V entries per lane, prefetch depth D) by B width: <=32: 1x1 (D 8),
-// <=64: 1x2 (D 8), <=128: 2x2 (D 6), wider: 3x2 (D 4; rows past 192 entries finish inline)
+// <=64: 1x2 (D 8), <=128: 2x2 (D 6), wider: 3x2 (D 8; rows past 192 entries finish inline)
 template <int G, int V, int D, int MODE>
 static cudaError_t prep_one(const LaunchCfg& cfg, int* bps) {
     cudaError_t e = cudaFuncSetAttribute(row_op_kernel<G, V, D, MODE>,
@@ -583,7 +590,7 @@ static cudaError_t prep_mode(const LaunchCfg& cfg, int* bps) {
         case 1: return prep_one<1, 1, 8, MODE>(cfg, bps);
         case 2: return prep_one<1, 2, 8, MODE>(cfg, bps);
         case 4: return prep_one<2, 2, 6, MODE>(cfg, bps);
-        default: return prep_one<3, 2, 4, MODE>(cfg, bps);
+        default: return prep_one<3, 2, 8, MODE>(cfg, bps);
     }
 }
 
@@ -594,7 +601,7 @@ static void launch_mode(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t
         case 1: row_op_kernel<1, 1, 8, MODE><<<grid, block, cfg.smem, s>>>(p); break;
         case 2: row_op_kernel<1, 2, 8, MODE><<<grid, block, cfg.smem, s>>>(p); break;
         case 4: row_op_kernel<2, 2, 6, MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        default: row_op_kernel<3, 2, 4, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        default: row_op_kernel<3, 2, 8, MODE><<<grid, block, cfg.smem, s>>>(p); break;
     }
 }
 
