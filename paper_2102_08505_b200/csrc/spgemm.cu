@@ -131,13 +131,16 @@ template <int G, int V, int D>
 __device__ __forceinline__ void accumulate_fast(const RowOpParams& p, const WarpSmem& w, int lane, int cnt,
                                                 int c0, int S) {
     constexpr int GE = 32 * V;  // entries per group
+    // Ring slots hold the raw loaded registers; nothing reads them until the step is
+    // consumed D steps later (validity is re-derived from nnz at consume time), so the
+    // gathers stay in flight across D steps.
     int rj[D][G][V];
     double rv[D][G][V];
     double ra[D];
     int rnb[D];
     const int32_t* __restrict__ bcol = p.B.col;
     const double* __restrict__ bval = p.B.val;
-    const int trash = c0 + S;                        // column that maps to acc[S]
+    const int trash = c0 + S;                          // column that maps to acc[S]
     const uint32_t abase = w.acc - 8u * (uint32_t)c0;  // acc + 8*(j - c0) = abase + 8*j (mod 2^32)
     auto load = [&](int d, int t) {
         const long long bo = w.boff[t];
@@ -146,8 +149,6 @@ __device__ __forceinline__ void accumulate_fast(const RowOpParams& p, const Warp
         rnb[d] = nb;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-#pragma unroll
-            for (int v = 0; v < V; ++v) rj[d][g][v] = trash;
             if (GE * g < nb) {
                 const int q = GE * g + V * lane;
                 if (q < nb) {
@@ -155,8 +156,8 @@ __device__ __forceinline__ void accumulate_fast(const RowOpParams& p, const Warp
                         const int2 c2 = __ldg(reinterpret_cast<const int2*>(bcol + bo + q));
                         const double2 v2 = __ldg(reinterpret_cast<const double2*>(bval + bo + q));
                         rj[d][g][0] = c2.x;
+                        rj[d][g][V - 1] = c2.y;
                         rv[d][g][0] = v2.x;
-                        rj[d][g][V - 1] = (q + 1 < nb) ? c2.y : trash;
                         rv[d][g][V - 1] = v2.y;
                     } else {
                         rj[d][g][0] = __ldg(bcol + bo + q);
@@ -183,7 +184,8 @@ __device__ __forceinline__ void accumulate_fast(const RowOpParams& p, const Warp
                         double old[V];
 #pragma unroll
                         for (int v = 0; v < V; ++v) {
-                            ad[v] = abase + 8u * (uint32_t)rj[d][g][v];
+                            const int j = (GE * g + V * lane + v < nb) ? rj[d][g][v] : trash;
+                            ad[v] = abase + 8u * (uint32_t)j;
                             old[v] = lds64(ad[v]);
                         }
 #pragma unroll
@@ -195,10 +197,10 @@ __device__ __forceinline__ void accumulate_fast(const RowOpParams& p, const Warp
                     const long long bo = w.boff[t];
                     for (int q0 = GE * G; q0 < nb; q0 += 64) {
                         const int qa = q0 + lane, qb = q0 + 32 + lane;
-                        const int ja = qa < nb ? __ldg(bcol + bo + qa) : trash;
-                        const int jb = qb < nb ? __ldg(bcol + bo + qb) : trash;
-                        const double va = qa < nb ? __ldg(bval + bo + qa) : 0.0;
-                        const double vb = qb < nb ? __ldg(bval + bo + qb) : 0.0;
+                        int ja = trash, jb = trash;
+                        double va = 0.0, vb = 0.0;
+                        if (qa < nb) { ja = __ldg(bcol + bo + qa); va = __ldg(bval + bo + qa); }
+                        if (qb < nb) { jb = __ldg(bcol + bo + qb); vb = __ldg(bval + bo + qb); }
                         const uint32_t aa_ = abase + 8u * (uint32_t)ja, ab_ = abase + 8u * (uint32_t)jb;
                         const double xa = lds64(aa_);
                         const double xb = lds64(ab_);
