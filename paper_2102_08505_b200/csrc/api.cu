@@ -227,6 +227,8 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
     const int64_t h = has_old ? (hprod > c->h->bw[2] ? hprod : c->h->bw[2]) : hprod;
     const int64_t need = 2 * h + 1;
     const int64_t nr = (n + 31) & ~int64_t(31);
+    const int maxnb = p.alpha != 0.0 ? c->h->bw[3] : 0;
+    const int groups = maxnb <= 64 ? 1 : (maxnb + 63) / 64;
     int64_t S;
     if (c->window_opt > 0) {
         S = c->window_opt;
@@ -238,10 +240,11 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
         S = kGeneralWindow;
         p.fast = 0;
     }
-    if (S > nr) { S = nr; p.fast = 1; }
+    if (S > nr) { S = nr; if (c->window_opt <= 0) p.fast = 1; }
     if (S < 32) S = 32;
+    if (groups > 4) p.fast = 0;  // B rows wider than 256 entries: general path
     LaunchCfg cfg;
-    CK(plan_row_op(p, (int)S, c->warps_opt, c->num_sms, &cfg));
+    CK(plan_row_op(p, (int)S, groups, c->warps_opt, c->num_sms, &cfg));
     p.S = cfg.S;
     c->last_cfg = cfg;
     const int64_t total_warps = (int64_t)cfg.grid * cfg.warps_per_cta;

@@ -62,14 +62,15 @@ struct LaunchCfg {
     int warps_per_cta;
     int grid;
     size_t smem;
-    int R;               // B slots per lane per prefetched step
+    int R;               // fast path: 64-entry B groups per step (1..4)
 };
 
 // spgemm.cu
-cudaError_t plan_row_op(const RowOpParams& p, int S, int warps_opt, int num_sms, LaunchCfg* cfg);
+// groups = ceil(max nnz_B / 64): the fast path processes every B row as `groups` 64-entry groups
+cudaError_t plan_row_op(const RowOpParams& p, int S, int groups, int warps_opt, int num_sms, LaunchCfg* cfg);
 cudaError_t launch_row_op(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s);
 size_t row_op_warp_smem(int S, bool has_old);
-// out[0..2] = max half-bandwidth of a (rows r0..r1), b (all rows), c (rows r0..r1)
+// out[0..2] = max half-bandwidth of a (rows r0..r1), b (all rows), c (rows r0..r1); out[3] = max nnz of b
 cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64_t r1, int64_t n,
                              int32_t* out, cudaStream_t s);
 

@@ -89,6 +89,15 @@ __device__ __forceinline__ void sts16u(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
+// Branch-free predicated store of one output entry (value + column).
+__device__ __forceinline__ void st_entry(bool pred, double* pv, int32_t* pc, double x, int32_t c) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t"
+        "@q st.global.f64 [%1], %2;\n\t@q st.global.b32 [%3], %4;\n\t}" ::"r"((int)pred),
+        "l"(pv), "d"(x), "l"(pc), "r"(c)
+        : "memory");
+}
+
 // Per-warp shared layout: acc[S] f64 | stage: boff[kStage] i64, aa[kStage] f64,
 // anb[kStage] i32, ast[kStage] i32 | flags[S] u8 (MODE != 0 only)
 struct WarpSmem {
@@ -121,21 +130,19 @@ __device__ __forceinline__ void stage_piece(const RowOpParams& p, const WarpSmem
 
 // ---------------------------------------------------------------------------- fast path
 
-// Accumulate the staged steps [0, cnt) into the window [c0, c0 + S). The host's bandwidth
-// probe guarantees every product column lies inside the window, so a step is pure
-// gather + RMW: each lane takes V consecutive entries of a 32*V-entry group (8/16-byte
-// vector loads), and the shared address acc + 8*(j - c0) is formed with one IMAD from a
-// per-row base; entries past nnz_B(k) point at a per-warp trash slot (acc[S]) instead of
-// being predicated, so a product costs IMAD + LDS + DFMA + STS.
-template <int G, int V, int D>
+// Accumulate the staged steps [0, cnt) into the window [c0, c0 + S). The host's probe
+// guarantees (i) every product column lies inside the window and (ii) every B row has at
+// most 64*G entries, so a step is a fixed, branch-free block: each lane takes entries
+// 2*lane, 2*lane+1 of each 64-entry group (8/16-byte vector loads), forms the shared
+// address acc + 8*(j - c0) with one IMAD from a per-row base (entries past nnz_B(k) are
+// sent to a per-warp trash slot acc[S] instead of being predicated), then issues all 2G
+// shared loads, all 2G FMAs and all 2G shared stores of the step. Ring slots hold raw
+// loaded registers and are not read until the step is consumed D steps later.
+template <int G, int D>
 __device__ __forceinline__ void accumulate_fast(const RowOpParams& p, const WarpSmem& w, int lane, int cnt,
                                                 int c0, int S) {
-    constexpr int GE = 32 * V;  // entries per group
-    // Ring slots hold the raw loaded registers; nothing reads them until the step is
-    // consumed D steps later (validity is re-derived from nnz at consume time), so the
-    // gathers stay in flight across D steps.
-    int rj[D][G][V];
-    double rv[D][G][V];
+    int2 rc[D][G];
+    double2 rv[D][G];
     double ra[D];
     int rnb[D];
     const int32_t* __restrict__ bcol = p.B.col;
@@ -149,21 +156,10 @@ __device__ __forceinline__ void accumulate_fast(const RowOpParams& p, const Warp
         rnb[d] = nb;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            if (GE * g < nb) {
-                const int q = GE * g + V * lane;
-                if (q < nb) {
-                    if (V == 2) {
-                        const int2 c2 = __ldg(reinterpret_cast<const int2*>(bcol + bo + q));
-                        const double2 v2 = __ldg(reinterpret_cast<const double2*>(bval + bo + q));
-                        rj[d][g][0] = c2.x;
-                        rj[d][g][V - 1] = c2.y;
-                        rv[d][g][0] = v2.x;
-                        rv[d][g][V - 1] = v2.y;
-                    } else {
-                        rj[d][g][0] = __ldg(bcol + bo + q);
-                        rv[d][g][0] = __ldg(bval + bo + q);
-                    }
-                }
+            const int q = 64 * g + 2 * lane;
+            if (q < nb) {
+                rc[d][g] = __ldg(reinterpret_cast<const int2*>(bcol + bo + q));
+                rv[d][g] = __ldg(reinterpret_cast<const double2*>(bval + bo + q));
             }
         }
     };
@@ -177,36 +173,25 @@ __device__ __forceinline__ void accumulate_fast(const RowOpParams& p, const Warp
             if (t < cnt) {
                 const double a = ra[d];
                 const int nb = rnb[d];
+                uint32_t ad[G][2];
+                double old[G][2];
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
-                    if (GE * g < nb) {
-                        uint32_t ad[V];
-                        double old[V];
-#pragma unroll
-                        for (int v = 0; v < V; ++v) {
-                            const int j = (GE * g + V * lane + v < nb) ? rj[d][g][v] : trash;
-                            ad[v] = abase + 8u * (uint32_t)j;
-                            old[v] = lds64(ad[v]);
-                        }
-#pragma unroll
-                        for (int v = 0; v < V; ++v) sts64(ad[v], __fma_rn(a, rv[d][g][v], old[v]));
-                    }
+                    const int q = 64 * g + 2 * lane;
+                    const int j0 = q < nb ? rc[d][g].x : trash;
+                    const int j1 = q + 1 < nb ? rc[d][g].y : trash;
+                    ad[g][0] = abase + 8u * (uint32_t)j0;
+                    ad[g][1] = abase + 8u * (uint32_t)j1;
                 }
-                if (nb > GE * G) {
-                    // B row longer than the prefetched groups: finish it here.
-                    const long long bo = w.boff[t];
-                    for (int q0 = GE * G; q0 < nb; q0 += 64) {
-                        const int qa = q0 + lane, qb = q0 + 32 + lane;
-                        int ja = trash, jb = trash;
-                        double va = 0.0, vb = 0.0;
-                        if (qa < nb) { ja = __ldg(bcol + bo + qa); va = __ldg(bval + bo + qa); }
-                        if (qb < nb) { jb = __ldg(bcol + bo + qb); vb = __ldg(bval + bo + qb); }
-                        const uint32_t aa_ = abase + 8u * (uint32_t)ja, ab_ = abase + 8u * (uint32_t)jb;
-                        const double xa = lds64(aa_);
-                        const double xb = lds64(ab_);
-                        sts64(aa_, __fma_rn(a, va, xa));
-                        sts64(ab_, __fma_rn(a, vb, xb));
-                    }
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    old[g][0] = lds64(ad[g][0]);
+                    old[g][1] = lds64(ad[g][1]);
+                }
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    sts64(ad[g][0], __fma_rn(a, rv[d][g].x, old[g][0]));
+                    sts64(ad[g][1], __fma_rn(a, rv[d][g].y, old[g][1]));
                 }
                 if (t + D < cnt) load(d, t + D);
                 __syncwarp();
@@ -219,7 +204,6 @@ __device__ __forceinline__ void accumulate_fast(const RowOpParams& p, const Warp
 
 // Multi-pass accumulate: entries at or beyond c0 + width are left for later passes; the
 // staged cursor ast[t] advances by the in-range count.
-template <int R, int D>
 __device__ __forceinline__ void accumulate_multi(const RowOpParams& p, const WarpSmem& w, int lane, int cnt,
                                                  int c0, int width) {
     const int32_t* __restrict__ bcol = p.B.col;
@@ -334,10 +318,7 @@ __device__ __forceinline__ void emit_window_t(const RowOpParams& p, const WarpSm
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
             const int pos = before + __popc(m[s] & lt_mask);
-            if (((m[s] >> lane) & 1u) && pos < cw) {
-                crow_v[pos] = x[s];
-                crow_c[pos] = c0 + b + 32 * s + lane;
-            }
+            st_entry(((m[s] >> lane) & 1u) && pos < cw, crow_v + pos, crow_c + pos, x[s], c0 + b + 32 * s + lane);
             before += __popc(m[s]);
         }
         kept = before;
@@ -375,9 +356,8 @@ __device__ __forceinline__ void clear_window(const WarpSmem& w, int lane, int S)
 
 // -------------------------------------------------------------------------------- kernel
 
-template <int G, int V, int D, int MODE>
+template <int G, int D, int MODE>
 __global__ void __launch_bounds__(128, 1) row_op_kernel(const RowOpParams p) {
-    constexpr int R = G * V;  // 32-entry groups covered by the prefetch (general path)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
@@ -437,7 +417,7 @@ __global__ void __launch_bounds__(128, 1) row_op_kernel(const RowOpParams p) {
             for (int p0 = 0; p0 < nA; p0 += kStage) {
                 const int cnt = min(kStage, nA - p0);
                 stage_piece(p, w, lane, a_col, a_val, p0, cnt, nullptr);
-                accumulate_fast<G, V, D>(p, w, lane, cnt, c0, S);
+                accumulate_fast<G, D>(p, w, lane, cnt, c0, S);
             }
             __syncwarp();
             bool ok = true;
@@ -504,7 +484,7 @@ __global__ void __launch_bounds__(128, 1) row_op_kernel(const RowOpParams p) {
                     for (int p0 = 0; p0 < nA; p0 += kStage) {
                         const int cnt = min(kStage, nA - p0);
                         stage_piece(p, w, lane, a_col, a_val, p0, cnt, multi ? cur : nullptr);
-                        accumulate_multi<R, D>(p, w, lane, cnt, c0, width);
+                        accumulate_multi(p, w, lane, cnt, c0, width);
                         if (multi) {
                             for (int q = lane; q < cnt; q += 32) cur[p0 + q] = w.ast[q];
                             __syncwarp();
@@ -557,9 +537,10 @@ __global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int64_t r0, int64_t r1,
             }
         }
     }
+    int nzb = (i < n) ? b.nnz[i] : 0;
 #pragma unroll
-    for (int m = 0; m < 3; ++m) {
-        int v = bw[m];
+    for (int m = 0; m < 4; ++m) {
+        int v = m < 3 ? bw[m] : nzb;
 #pragma unroll
         for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
         if ((threadIdx.x & 31) == 0 && v > 0) atomicMax(out + m, v);
@@ -575,24 +556,24 @@ cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64
 
 // ----------------------------------------------------------------------------- dispatch
 
-// (G groups x V entries per lane, prefetch depth D) by B width: <=32: 1x1 (D 8),
-// <=64: 1x2 (D 8), <=128: 2x2 (D 6), wider: 3x2 (D 8; rows past 192 entries finish inline)
-template <int G, int V, int D, int MODE>
+// Variants by G = ceil(max nnz_B / 64) (64-entry groups per step; prefetch depth D):
+// G1: D 10, G2: D 8, G3: D 6, G4: D 5. cfg.R carries G.
+template <int G, int D, int MODE>
 static cudaError_t prep_one(const LaunchCfg& cfg, int* bps) {
-    cudaError_t e = cudaFuncSetAttribute(row_op_kernel<G, V, D, MODE>,
+    cudaError_t e = cudaFuncSetAttribute(row_op_kernel<G, D, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
     if (e) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, row_op_kernel<G, V, D, MODE>,
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, row_op_kernel<G, D, MODE>,
                                                          cfg.warps_per_cta * 32, cfg.smem);
 }
 
 template <int MODE>
 static cudaError_t prep_mode(const LaunchCfg& cfg, int* bps) {
     switch (cfg.R) {
-        case 1: return prep_one<1, 1, 8, MODE>(cfg, bps);
-        case 2: return prep_one<1, 2, 8, MODE>(cfg, bps);
-        case 4: return prep_one<2, 2, 6, MODE>(cfg, bps);
-        default: return prep_one<3, 2, 8, MODE>(cfg, bps);
+        case 1: return prep_one<1, 10, MODE>(cfg, bps);
+        case 2: return prep_one<2, 8, MODE>(cfg, bps);
+        case 3: return prep_one<3, 6, MODE>(cfg, bps);
+        default: return prep_one<4, 5, MODE>(cfg, bps);
     }
 }
 
@@ -600,25 +581,18 @@ template <int MODE>
 static void launch_mode(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s) {
     dim3 block(cfg.warps_per_cta * 32), grid(cfg.grid);
     switch (cfg.R) {
-        case 1: row_op_kernel<1, 1, 8, MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        case 2: row_op_kernel<1, 2, 8, MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        case 4: row_op_kernel<2, 2, 6, MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        default: row_op_kernel<3, 2, 8, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 1: row_op_kernel<1, 10, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 2: row_op_kernel<2, 8, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 3: row_op_kernel<3, 6, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        default: row_op_kernel<4, 5, MODE><<<grid, block, cfg.smem, s>>>(p); break;
     }
 }
 
 static int mode_of(const RowOpParams& p) { return p.old_mode == 0 ? 0 : (p.normsq ? 2 : 1); }
 
-static int pick_R(int wb) {
-    if (wb <= 32) return 1;
-    if (wb <= 64) return 2;
-    if (wb <= 128) return 4;
-    return 8;
-}
-
 size_t row_op_warp_smem(int S, bool has_old) { return warp_smem_bytes(S, has_old); }
 
-cudaError_t plan_row_op(const RowOpParams& p, int S, int warps_opt, int num_sms, LaunchCfg* cfg) {
+cudaError_t plan_row_op(const RowOpParams& p, int S, int groups, int warps_opt, int num_sms, LaunchCfg* cfg) {
     S = (S + 31) & ~31;
     const size_t per_warp = warp_smem_bytes(S, p.old_mode != 0);
     const size_t cap = 227 * 1024;
@@ -628,7 +602,7 @@ cudaError_t plan_row_op(const RowOpParams& p, int S, int warps_opt, int num_sms,
     while (wpc > 1 && (size_t)wpc * per_warp > cap) --wpc;
     cfg->S = S;
     cfg->warps_per_cta = wpc;
-    cfg->R = pick_R(p.B.w);
+    cfg->R = groups < 1 ? 1 : (groups > 4 ? 4 : groups);
     cfg->smem = (size_t)wpc * per_warp;
     int bps = 0;
     const int mode = mode_of(p);
