@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _REPO = os.path.dirname(_HERE)
-_LIB = os.path.join(_HERE, "libellpack.so")
+_LIB = os.environ.get("ELLPACK_LIB") or os.path.join(_HERE, "libellpack.so")
 _SRCS = [os.path.join(_HERE, "csrc", f) for f in ("spgemm.cu", "reduce.cu", "api.cu")]
 _HDRS = [os.path.join(_HERE, "csrc", "internal.cuh"), os.path.join(_REPO, "include", "ellpack.h")]
 

@@ -17,6 +17,8 @@
 #include <nccl.h>
 
 #include <chrono>
+#include <cstdio>
+#include <vector>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -102,6 +104,7 @@ struct ellpack_ctx_s {
     Buf ident_val, ident_col, ident_nnz;
     int64_t ident_n = 0;
     Buf hx_val, hx_col, hx_nnz, hy_val, hy_col, hy_nnz;  // host-path device copies
+    Buf timing;                                          // ELL_TIMING debug builds only
     // overflow info of the last OVERFLOW
     int64_t last_ovf_rows = 0;
     int32_t last_req = 0;
@@ -266,8 +269,31 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
     }
     p.status = c->d_status;
     CK(cudaMemsetAsync(c->d_status, 0, 2 * sizeof(int32_t), c->stream));
+#ifdef ELL_TIMING
+    // debug build only: per-warp phase cycle counters, summarised on stderr after each launch
+    const size_t tbytes = sizeof(unsigned long long) * 8 * (size_t)total_warps;
+    RK(grow(c, c->timing, tbytes));
+    CK(cudaMemsetAsync(c->timing.p, 0, tbytes, c->stream));
+    p.timing = (unsigned long long*)c->timing.p;
+#else
+    p.timing = nullptr;
+#endif
     if (c->profile) CK(cudaEventRecord(c->ev[4], c->stream));
     CK(launch_row_op(p, cfg, c->stream));
+#ifdef ELL_TIMING
+    {
+        std::vector<unsigned long long> T(8 * (size_t)total_warps);
+        CK(cudaMemcpyAsync(T.data(), c->timing.p, tbytes, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        double st = 0, ac = 0, em = 0, rows = 0, nz = 0;
+        for (int64_t k = 0; k < total_warps; ++k) {
+            st += T[8 * k]; ac += T[8 * k + 1]; em += T[8 * k + 2]; rows += T[8 * k + 3]; nz += T[8 * k + 4];
+        }
+        if (rows > 0)
+            fprintf(stderr, "[ell-timing] S=%d G=%d wpc=%d grid=%d rows=%.0f  cycles/row: stage %.0f acc %.0f emit %.0f  | acc cycles/step %.1f\n",
+                    cfg.S, cfg.R, cfg.warps_per_cta, cfg.grid, rows, st / rows, ac / rows, em / rows, ac / (nz > 0 ? nz : 1));
+    }
+#endif
     if (c->profile) {
         CK(cudaEventRecord(c->ev[5], c->stream));
         c->prof_pending = true;

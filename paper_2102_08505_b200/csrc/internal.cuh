@@ -55,6 +55,7 @@ struct RowOpParams {
     double* st_val;
     int32_t* st_col;
     int64_t st_stride;
+    unsigned long long* timing;  // ELL_TIMING builds only: per-warp phase cycle counters
 };
 
 struct LaunchCfg {

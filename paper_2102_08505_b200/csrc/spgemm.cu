@@ -414,10 +414,23 @@ __global__ void __launch_bounds__(128, 1) row_op_kernel(const RowOpParams p) {
                 if (c > ncols - S) c = ncols - S;
                 c0 = (int)c;
             }
+#ifdef ELL_TIMING
+            long long t_a = clock64(), t_stage = 0, t_acc = 0;
+#endif
             for (int p0 = 0; p0 < nA; p0 += kStage) {
                 const int cnt = min(kStage, nA - p0);
                 stage_piece(p, w, lane, a_col, a_val, p0, cnt, nullptr);
+#ifdef ELL_TIMING
+                __syncwarp();
+                long long t_b = clock64();
+                t_stage += t_b - t_a;
+#endif
                 accumulate_fast<G, D>(p, w, lane, cnt, c0, S);
+#ifdef ELL_TIMING
+                __syncwarp();
+                t_a = clock64();
+                t_acc += t_a - t_b;
+#endif
             }
             __syncwarp();
             bool ok = true;
@@ -428,7 +441,21 @@ __global__ void __launch_bounds__(128, 1) row_op_kernel(const RowOpParams p) {
             }
             if (ok) {
                 if (p.diag_c) dc = window_diag<MODE>(p, w, (int)(i - c0), S);
+#ifdef ELL_TIMING
+                long long t_e0 = clock64();
+#endif
                 emit_window<MODE>(p, w, lane, crow_v, crow_c, c0, S, kept, nrm);
+#ifdef ELL_TIMING
+                long long t_e1 = clock64();
+                if (lane == 0 && p.timing) {
+                    unsigned long long* T = p.timing + 8 * (blockIdx.x * (blockDim.x >> 5) + wid);
+                    atomicAdd(T + 0, (unsigned long long)t_stage);
+                    atomicAdd(T + 1, (unsigned long long)t_acc);
+                    atomicAdd(T + 2, (unsigned long long)(t_e1 - t_e0));
+                    atomicAdd(T + 3, 1ull);
+                    atomicAdd(T + 4, (unsigned long long)nA);
+                }
+#endif
                 done = true;
             } else {
                 clear_window<MODE>(w, lane, S);
