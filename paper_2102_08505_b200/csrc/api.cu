@@ -226,26 +226,31 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
     c->launches++;
     CK(cudaMemcpyAsync(c->h->bw, c->d_bw, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    const int64_t hprod = p.alpha != 0.0 ? (int64_t)c->h->bw[0] + c->h->bw[1] : 0;
+    const int64_t hB = c->h->bw[1];
+    const int64_t hprod = p.alpha != 0.0 ? (int64_t)c->h->bw[0] + hB : 0;
     const int64_t h = has_old ? (hprod > c->h->bw[2] ? hprod : c->h->bw[2]) : hprod;
-    const int64_t need = 2 * h + 1;
     const int64_t nr = (n + 31) & ~int64_t(31);
     const int maxnb = p.alpha != 0.0 ? c->h->bw[3] : 0;
     const int groups = maxnb <= 64 ? 1 : (maxnb + 63) / 64;
+    p.hB = (int32_t)hB;
+    // ring fast path: S >= 2 hB + 33 slots (progressive emission), B rows <= 256 entries
+    int64_t ring = (2 * hB + 33 + 31) & ~int64_t(31);
+    if (ring > nr) ring = nr < 32 ? 32 : nr;
     int64_t S;
     if (c->window_opt > 0) {
+        // forced general path (tests): multi-pass windows of window_opt doubles
         S = c->window_opt;
-        p.fast = need <= S ? 1 : 0;
-    } else if (need <= kFastWindowMax) {
-        S = (need + 31) & ~int64_t(31);
+        p.fast = 0;
+    } else if (ring <= kFastWindowMax && groups <= 4) {
+        S = ring;
         p.fast = 1;
     } else {
         S = kGeneralWindow;
         p.fast = 0;
     }
-    if (S > nr) { S = nr; if (c->window_opt <= 0) p.fast = 1; }
+    (void)h;
+    if (S > nr) S = nr;
     if (S < 32) S = 32;
-    if (groups > 4) p.fast = 0;  // B rows wider than 256 entries: general path
     LaunchCfg cfg;
     CK(plan_row_op(p, (int)S, groups, c->warps_opt, c->num_sms, &cfg));
     p.S = cfg.S;

@@ -41,7 +41,8 @@ struct RowOpParams {
     int32_t stash_a;    // C aliases A -> stash A row when the row needs > 1 pass
     int32_t stash_old;  // C aliases Old -> stash Old row when the row needs > 1 pass
     int32_t S;          // dense-window capacity (doubles) per warp
-    int32_t fast;       // 1: every row fits the row-centred window of S (bandwidth-probed)
+    int32_t fast;       // 1: ring fast path (S = ring slots >= 2 hB + 33, B rows <= 256 entries)
+    int32_t hB;         // max half-bandwidth of B (probe)
     int64_t ncols;      // matrix dimension N (columns >= N never exist)
     // optional per-row outputs, indexed by global row (nullable)
     double* diag_a;   // stored a_ii

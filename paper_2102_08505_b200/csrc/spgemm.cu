@@ -98,8 +98,8 @@ __device__ __forceinline__ void st_entry(bool pred, double* pv, int32_t* pc, dou
         : "memory");
 }
 
-// Per-warp shared layout: acc[S] f64 | stage: boff[kStage] i64, aa[kStage] f64,
-// anb[kStage] i32, ast[kStage] i32 | flags[S] u8 (MODE != 0 only)
+// Per-warp shared layout: acc[S + 2] f64 | stage: boff[kStage] i64, aa[kStage] f64,
+// anb[kStage] i32, ast[kStage] i32, ak[kStage] i32 | flags[S] u8 (MODE != 0 only)
 struct WarpSmem {
     uint32_t acc;  // shared address of acc[0]
     uint32_t flg;  // shared address of flags[0]
@@ -107,11 +107,12 @@ struct WarpSmem {
     double* aa;
     int* anb;
     int* ast;
+    int* ak;
 };
 
 // acc has S + 2 slots: acc[S] is the trash slot of padded lanes (16-byte aligned pair).
 __host__ __device__ inline size_t warp_smem_bytes(int S, bool has_old) {
-    return (size_t)(S + 2) * 8 + (size_t)kStage * 24 + (has_old ? (size_t)S : 0);
+    return (size_t)(S + 2) * 8 + (size_t)kStage * 28 + (has_old ? (size_t)S : 0);
 }
 
 // Stage A-row entries [p0, p0 + cnt): B-row offset k*B.w, a_ik, nnz_B(k), cursor.
@@ -121,6 +122,7 @@ __device__ __forceinline__ void stage_piece(const RowOpParams& p, const WarpSmem
     for (int q = lane; q < cnt; q += 32) {
         const int k = a_col[p0 + q];
         w.boff[q] = (long long)k * p.B.w;
+        w.ak[q] = k;
         w.aa[q] = a_val[p0 + q];
         w.anb[q] = __ldg(p.B.nnz + k);
         w.ast[q] = cur ? cur[p0 + q] : 0;
@@ -354,6 +356,189 @@ __device__ __forceinline__ void clear_window(const WarpSmem& w, int lane, int S)
     __syncwarp();
 }
 
+// ------------------------------------------------------------------- ring fast path
+//
+// Row-centred windows need 2(hA + hB) + 1 doubles per row. The k-sweep is ascending, and
+// step k touches only columns [k - hB, k + hB], so once step k starts every column below
+// k - hB is final. The fast path therefore keeps a RING of S >= 2 hB + 33 slots (column j
+// lives in slot j mod S, S a multiple of 32) and emits finished 32-column chunks as the
+// sweep advances ("progressive emission"): before step k, chunks below floor32(k - hB) are
+// combined with Old, dropped, compacted and written, and their slots cleared, so the live
+// span never exceeds S. Half the shared memory of a full window for X^2 (hA = hB), hence
+// twice the rows in flight per SM. Each step is software-pipelined over a (D+1)-slot
+// register ring: the gathers for step t + D are issued before step t's FMAs.
+
+// Emit the 32-column chunk [F, F + 32) living in ring slots [F - baseF, F - baseF + 32).
+template <int MODE>
+__device__ __forceinline__ void ring_emit_chunk(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
+                                                int F, int baseF, const int32_t* o_col, const double* o_val,
+                                                int nOld, int& old_cur, double* __restrict__ crow_v,
+                                                int32_t* __restrict__ crow_c, int& kept, double& ds, double& dc,
+                                                double& nrm) {
+    const uint32_t pa = w.acc + 8u * (uint32_t)(F - baseF + lane);
+    if ((int64_t)F <= i && i < (int64_t)F + 32) ds = lds64(w.acc + 8u * (uint32_t)(i - baseF));
+    if (MODE != 0 && old_cur < nOld) {
+        // at most 32 Old entries (distinct columns) fall in a 32-column chunk
+        const int q = old_cur + lane;
+        const bool v = q < nOld;
+        const int jo = v ? o_col[q] : INT_MAX;
+        const bool inr = jo < F + 32;
+        if (inr) {
+            const double x = o_val[q];
+            const uint32_t sa = w.acc + 8u * (uint32_t)(jo - baseF);
+            const double sv = lds64(sa);
+            if (MODE == 2) {
+                const double df = __dsub_rn(sv, x);
+                nrm = __fma_rn(df, df, nrm);
+            }
+            const double tt = (p.old_mode == 1) ? __dmul_rn(p.beta, x) : 0.0;
+            sts64(sa, __fma_rn(p.alpha, sv, tt));
+            sts8(w.flg + (uint32_t)(jo - baseF), 1u);
+        }
+        old_cur += __popc(__ballot_sync(FULL, inr));
+        __syncwarp();
+    }
+    double v = lds64(pa);
+    sts64(pa, 0.0);
+    bool flagged = false;
+    if (MODE != 0) {
+        const uint32_t fa = w.flg + (uint32_t)(F - baseF + lane);
+        flagged = lds8(fa) != 0;
+        sts8(fa, 0u);
+    }
+    double x = v;
+    if (!flagged) {
+        if (p.alpha != 1.0) x = __dmul_rn(p.alpha, v);
+        if (MODE == 2) nrm = __fma_rn(v, v, nrm);
+    }
+    const bool keep = fabs(x) > p.tau;
+    const unsigned m = __ballot_sync(FULL, keep);
+    const int pos = kept + __popc(m & ((1u << lane) - 1u));
+    st_entry(keep && pos < p.C.w, crow_v + pos, crow_c + pos, x, F + lane);
+    if ((int64_t)F + lane == i) dc = keep ? x : 0.0;
+    kept += __popc(m);
+}
+
+template <int G, int D, int MODE>
+__device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
+                                         const int32_t* a_col, const double* a_val, int nA,
+                                         const int32_t* o_col, const double* o_val, int nOld,
+                                         double* __restrict__ crow_v, int32_t* __restrict__ crow_c,
+                                         int& kept, double& ds, double& dc, double& nrm) {
+    constexpr int NS = D + 1;  // register ring slots
+    const int S = p.S;
+    const int hB = p.hB;
+    const int ncols = (int)p.ncols;
+    (void)ncols;
+    // column extent of the row: products in [k_first - hB, k_last + hB], plus Old entries
+    int lo_col = INT_MAX, hi_col = -1;
+    if (nA > 0) {
+        lo_col = max(0, a_col[0] - hB);
+        hi_col = min(ncols - 1, a_col[nA - 1] + hB);
+    }
+    if (MODE != 0 && nOld > 0) {
+        lo_col = min(lo_col, o_col[0]);
+        hi_col = max(hi_col, o_col[nOld - 1]);
+    }
+    if (hi_col < lo_col) return;
+    int F = lo_col & ~31;
+    const int Fend = (hi_col + 32) & ~31;
+    int baseF = F - F % S;  // multiple of S with baseF <= F < baseF + S
+    int baseS = baseF;
+    int old_cur = 0;
+    const uint32_t trash = w.acc + 8u * (uint32_t)S;
+    const int32_t* __restrict__ bcol = p.B.col;
+    const double* __restrict__ bval = p.B.val;
+
+    int2 rc[NS][G];
+    double2 rv[NS][G];
+    double ra[NS];
+    int rnb[NS], rk[NS];
+    for (int p0 = 0; p0 < nA; p0 += kStage) {
+        const int cnt = min(kStage, nA - p0);
+        stage_piece(p, w, lane, a_col, a_val, p0, cnt, nullptr);
+        auto load = [&](int slot, int t) {
+            const long long bo = w.boff[t];
+            const int nb = w.anb[t];
+            ra[slot] = w.aa[t];
+            rnb[slot] = nb;
+            rk[slot] = w.ak[t];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int q = 64 * g + 2 * lane;
+                if (q < nb) {
+                    rc[slot][g] = __ldg(reinterpret_cast<const int2*>(bcol + bo + q));
+                    rv[slot][g] = __ldg(reinterpret_cast<const double2*>(bval + bo + q));
+                }
+            }
+        };
+#pragma unroll
+        for (int d = 0; d < D; ++d)
+            if (d < cnt) load(d, d);
+        for (int t0 = 0; t0 < cnt; t0 += NS) {
+#pragma unroll
+            for (int d = 0; d < NS; ++d) {
+                const int t = t0 + d;
+                if (t < cnt) {
+                    const int kt = rk[d];
+                    // 1. columns below floor32(k - hB) are final: emit them (frees their slots)
+                    const int target = (kt - hB) & ~31;
+                    while (F < target) {
+                        if (F - baseF >= S) baseF += S;
+                        ring_emit_chunk<MODE>(p, w, lane, i, F, baseF, o_col, o_val, nOld, old_cur, crow_v,
+                                                  crow_c, kept, ds, dc, nrm);
+                        F += 32;
+                    }
+                    __syncwarp();
+                    // 2. ring slot mapping for this step: columns [lo, k + hB], lo >= baseS
+                    const int lo = max(0, kt - hB);
+                    while (lo - baseS >= S) baseS += S;
+                    const uint32_t abase = w.acc - 8u * (uint32_t)baseS;
+                    const int jw = baseS + S;
+                    const int nb = rnb[d];
+                    const double a = ra[d];
+                    uint32_t ad[G][2];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        const int q = 64 * g + 2 * lane;
+                        const int j0 = rc[d][g].x, j1 = rc[d][g].y;
+                        uint32_t a0 = abase + 8u * (uint32_t)j0 - (j0 >= jw ? 8u * (uint32_t)S : 0u);
+                        uint32_t a1 = abase + 8u * (uint32_t)j1 - (j1 >= jw ? 8u * (uint32_t)S : 0u);
+                        ad[g][0] = q < nb ? a0 : trash;
+                        ad[g][1] = q + 1 < nb ? a1 : trash;
+                    }
+                    // 3. shared loads of the step
+                    double old[G][2];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        old[g][0] = lds64(ad[g][0]);
+                        old[g][1] = lds64(ad[g][1]);
+                    }
+                    // 4. gathers for step t + D into the slot freed by step t - 1
+                    if (t + D < cnt) load((d + D) % NS, t + D);
+                    // 5. fma + shared stores
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        sts64(ad[g][0], __fma_rn(a, rv[d][g].x, old[g][0]));
+                        sts64(ad[g][1], __fma_rn(a, rv[d][g].y, old[g][1]));
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    }
+    // final chunks
+    while (F < Fend) {
+        if (F - baseF >= S) baseF += S;
+        ring_emit_chunk<MODE>(p, w, lane, i, F, baseF, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept,
+                                  ds, dc, nrm);
+        F += 32;
+    }
+    __syncwarp();
+    dc = warp_sum(dc);  // only the diagonal's lane holds a nonzero value (x + 0 = x exactly)
+    ds = ds;            // ds is warp-uniform (broadcast shared load)
+}
+
 // -------------------------------------------------------------------------------- kernel
 
 template <int G, int D, int MODE>
@@ -369,7 +554,8 @@ __global__ void __launch_bounds__(128, 1) row_op_kernel(const RowOpParams p) {
     w.aa = reinterpret_cast<double*>(w.boff + kStage);
     w.anb = reinterpret_cast<int*>(w.aa + kStage);
     w.ast = w.anb + kStage;
-    w.flg = w.acc + (uint32_t)((S + 2) * 8 + kStage * 24);
+    w.ak = w.ast + kStage;
+    w.flg = w.acc + (uint32_t)((S + 2) * 8 + kStage * 28);
     clear_window<MODE>(w, lane, S);
 
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
@@ -406,62 +592,10 @@ __global__ void __launch_bounds__(128, 1) row_op_kernel(const RowOpParams p) {
         bool done = false;
 
         if (p.fast) {
-            // ---- fast path: one pass over the row-centred window (c0 even)
-            int c0 = 0;
-            if ((int64_t)S < ncols) {
-                int64_t c = i - (S >> 1);
-                if (c < 0) c = 0;
-                if (c > ncols - S) c = ncols - S;
-                c0 = (int)c;
-            }
-#ifdef ELL_TIMING
-            long long t_a = clock64(), t_stage = 0, t_acc = 0;
-#endif
-            for (int p0 = 0; p0 < nA; p0 += kStage) {
-                const int cnt = min(kStage, nA - p0);
-                stage_piece(p, w, lane, a_col, a_val, p0, cnt, nullptr);
-#ifdef ELL_TIMING
-                __syncwarp();
-                long long t_b = clock64();
-                t_stage += t_b - t_a;
-#endif
-                accumulate_fast<G, D>(p, w, lane, cnt, c0, S);
-#ifdef ELL_TIMING
-                __syncwarp();
-                t_a = clock64();
-                t_acc += t_a - t_b;
-#endif
-            }
-            __syncwarp();
-            bool ok = true;
-            if (ok) {
-                if ((int64_t)c0 <= i && i < (int64_t)c0 + S) ds = lds64(w.acc + (uint32_t)(i - c0) * 8u);
-                int old_cur = 0;
-                if (MODE != 0) ok = combine_old<MODE>(p, w, lane, o_col, o_val, nOld, old_cur, c0, S, false, nrm);
-            }
-            if (ok) {
-                if (p.diag_c) dc = window_diag<MODE>(p, w, (int)(i - c0), S);
-#ifdef ELL_TIMING
-                long long t_e0 = clock64();
-#endif
-                emit_window<MODE>(p, w, lane, crow_v, crow_c, c0, S, kept, nrm);
-#ifdef ELL_TIMING
-                long long t_e1 = clock64();
-                if (lane == 0 && p.timing) {
-                    unsigned long long* T = p.timing + 8 * (blockIdx.x * (blockDim.x >> 5) + wid);
-                    atomicAdd(T + 0, (unsigned long long)t_stage);
-                    atomicAdd(T + 1, (unsigned long long)t_acc);
-                    atomicAdd(T + 2, (unsigned long long)(t_e1 - t_e0));
-                    atomicAdd(T + 3, 1ull);
-                    atomicAdd(T + 4, (unsigned long long)nA);
-                }
-#endif
-                done = true;
-            } else {
-                clear_window<MODE>(w, lane, S);
-                nrm = 0.0;
-                ds = 0.0;
-            }
+            // ---- fast path: ring window with progressive emission (single pass)
+            row_ring<G, D, MODE>(p, w, lane, i, a_col, a_val, nA, o_col, o_val, nOld, crow_v, crow_c, kept, ds,
+                                 dc, nrm);
+            done = true;
         }
 
         if (!done) {
@@ -584,7 +718,7 @@ cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64
 // ----------------------------------------------------------------------------- dispatch
 
 // Variants by G = ceil(max nnz_B / 64) (64-entry groups per step; prefetch depth D):
-// G1: D 10, G2: D 8, G3: D 6, G4: D 5. cfg.R carries G.
+// G1: D 8, G2: D 6, G3: D 4, G4: D 3 (the ring holds D + 1 slots). cfg.R carries G.
 template <int G, int D, int MODE>
 static cudaError_t prep_one(const LaunchCfg& cfg, int* bps) {
     cudaError_t e = cudaFuncSetAttribute(row_op_kernel<G, D, MODE>,
@@ -597,10 +731,10 @@ static cudaError_t prep_one(const LaunchCfg& cfg, int* bps) {
 template <int MODE>
 static cudaError_t prep_mode(const LaunchCfg& cfg, int* bps) {
     switch (cfg.R) {
-        case 1: return prep_one<1, 10, MODE>(cfg, bps);
-        case 2: return prep_one<2, 8, MODE>(cfg, bps);
-        case 3: return prep_one<3, 6, MODE>(cfg, bps);
-        default: return prep_one<4, 5, MODE>(cfg, bps);
+        case 1: return prep_one<1, 8, MODE>(cfg, bps);
+        case 2: return prep_one<2, 6, MODE>(cfg, bps);
+        case 3: return prep_one<3, 4, MODE>(cfg, bps);
+        default: return prep_one<4, 3, MODE>(cfg, bps);
     }
 }
 
@@ -608,10 +742,10 @@ template <int MODE>
 static void launch_mode(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s) {
     dim3 block(cfg.warps_per_cta * 32), grid(cfg.grid);
     switch (cfg.R) {
-        case 1: row_op_kernel<1, 10, MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        case 2: row_op_kernel<2, 8, MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        case 3: row_op_kernel<3, 6, MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        default: row_op_kernel<4, 5, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 1: row_op_kernel<1, 8, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 2: row_op_kernel<2, 6, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 3: row_op_kernel<3, 4, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        default: row_op_kernel<4, 3, MODE><<<grid, block, cfg.smem, s>>>(p); break;
     }
 }
 
