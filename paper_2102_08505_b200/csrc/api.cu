@@ -242,7 +242,15 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
         S = c->window_opt;
         p.fast = 0;
     } else if (ring <= kFastWindowMax && groups <= 4) {
-        S = ring;
+        // grow the ring while the resident rows per SM stay the same (slack batches the emission)
+        const size_t cap = 227 * 1024;
+        const size_t per0 = row_op_warp_smem((int)ring, has_old);
+        const size_t rows_sm = cap / per0;
+        int64_t grown = ring;
+        while (grown + 32 <= ring + 512 && grown + 32 <= kFastWindowMax &&
+               cap / row_op_warp_smem((int)(grown + 32), has_old) >= rows_sm)
+            grown += 32;
+        S = grown;
         p.fast = 1;
     } else {
         S = kGeneralWindow;
@@ -264,6 +272,9 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
         p.cur_stride = p.A.w;
         RK(grow(c, c->cursors, sizeof(int32_t) * (size_t)total_warps * p.cur_stride));
         p.cursors = (int32_t*)c->cursors.p;
+    }
+    if (may_multi || p.fast) {
+        // in-place rows are stashed on the ring path (progressive emission) and on multi-pass rows
         if (p.stash_a || p.stash_old) {
             p.st_stride = (p.stash_a ? p.A.w : 0) + (p.stash_old ? p.Old.w : 0);
             RK(grow(c, c->stash_val, sizeof(double) * (size_t)total_warps * p.st_stride));

@@ -368,55 +368,103 @@ __device__ __forceinline__ void clear_window(const WarpSmem& w, int lane, int S)
 // twice the rows in flight per SM. Each step is software-pipelined over a (D+1)-slot
 // register ring: the gathers for step t + D are issued before step t's FMAs.
 
-// Emit the 32-column chunk [F, F + 32) living in ring slots [F - baseF, F - baseF + 32).
-template <int MODE>
-__device__ __forceinline__ void ring_emit_chunk(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
+// Emit NCH consecutive 32-column chunks [F, F + 32 NCH) (column j lives in ring slot
+// j - baseF, minus S past the wrap): pre-combine diagonal, combine with Old, drop, compact
+// (NCH independent ballots) and write; the slots (and flags) are cleared.
+template <int MODE, int NCH>
+__device__ __forceinline__ void ring_emit_block(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
                                                 int F, int baseF, const int32_t* o_col, const double* o_val,
                                                 int nOld, int& old_cur, double* __restrict__ crow_v,
                                                 int32_t* __restrict__ crow_c, int& kept, double& ds, double& dc,
                                                 double& nrm) {
-    const uint32_t pa = w.acc + 8u * (uint32_t)(F - baseF + lane);
-    if ((int64_t)F <= i && i < (int64_t)F + 32) ds = lds64(w.acc + 8u * (uint32_t)(i - baseF));
-    if (MODE != 0 && old_cur < nOld) {
-        // at most 32 Old entries (distinct columns) fall in a 32-column chunk
-        const int q = old_cur + lane;
-        const bool v = q < nOld;
-        const int jo = v ? o_col[q] : INT_MAX;
-        const bool inr = jo < F + 32;
-        if (inr) {
-            const double x = o_val[q];
-            const uint32_t sa = w.acc + 8u * (uint32_t)(jo - baseF);
-            const double sv = lds64(sa);
-            if (MODE == 2) {
-                const double df = __dsub_rn(sv, x);
-                nrm = __fma_rn(df, df, nrm);
+    const int S = p.S;
+    const int Fe = F + 32 * NCH;
+    if ((int64_t)F <= i && i < (int64_t)Fe) {
+        int pi = (int)(i - baseF);
+        if (pi >= S) pi -= S;
+        ds = lds64(w.acc + 8u * (uint32_t)pi);
+    }
+    if (MODE != 0) {
+        while (old_cur < nOld) {
+            const int q = old_cur + lane;
+            const bool v = q < nOld;
+            const int jo = v ? o_col[q] : INT_MAX;
+            const bool inr = jo < Fe;
+            if (inr) {
+                const double x = o_val[q];
+                int po = jo - baseF;
+                if (po >= S) po -= S;
+                const uint32_t sa = w.acc + 8u * (uint32_t)po;
+                const double sv = lds64(sa);
+                if (MODE == 2) {
+                    const double df = __dsub_rn(sv, x);
+                    nrm = __fma_rn(df, df, nrm);
+                }
+                const double tt = (p.old_mode == 1) ? __dmul_rn(p.beta, x) : 0.0;
+                sts64(sa, __fma_rn(p.alpha, sv, tt));
+                sts8(w.flg + (uint32_t)po, 1u);
             }
-            const double tt = (p.old_mode == 1) ? __dmul_rn(p.beta, x) : 0.0;
-            sts64(sa, __fma_rn(p.alpha, sv, tt));
-            sts8(w.flg + (uint32_t)(jo - baseF), 1u);
+            const int n = __popc(__ballot_sync(FULL, inr));
+            old_cur += n;
+            if (n < 32) break;
         }
-        old_cur += __popc(__ballot_sync(FULL, inr));
         __syncwarp();
     }
-    double v = lds64(pa);
-    sts64(pa, 0.0);
-    bool flagged = false;
-    if (MODE != 0) {
-        const uint32_t fa = w.flg + (uint32_t)(F - baseF + lane);
-        flagged = lds8(fa) != 0;
-        sts8(fa, 0u);
+    double x[NCH];
+    unsigned m[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+        int pc = F + 32 * c - baseF;
+        if (pc >= S) pc -= S;
+        const uint32_t pa = w.acc + 8u * (uint32_t)(pc + lane);
+        const double v = lds64(pa);
+        sts64(pa, 0.0);
+        bool flagged = false;
+        if (MODE != 0) {
+            const uint32_t fa = w.flg + (uint32_t)(pc + lane);
+            flagged = lds8(fa) != 0;
+            sts8(fa, 0u);
+        }
+        x[c] = v;
+        if (!flagged) {
+            if (p.alpha != 1.0) x[c] = __dmul_rn(p.alpha, v);
+            if (MODE == 2) nrm = __fma_rn(v, v, nrm);
+        }
+        m[c] = __ballot_sync(FULL, fabs(x[c]) > p.tau);
     }
-    double x = v;
-    if (!flagged) {
-        if (p.alpha != 1.0) x = __dmul_rn(p.alpha, v);
-        if (MODE == 2) nrm = __fma_rn(v, v, nrm);
+    const unsigned lt = (1u << lane) - 1u;
+    int before = kept;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+        const bool keep = (m[c] >> lane) & 1u;
+        const int pos = before + __popc(m[c] & lt);
+        st_entry(keep && pos < p.C.w, crow_v + pos, crow_c + pos, x[c], F + 32 * c + lane);
+        if ((int64_t)F + 32 * c + lane == i) dc = keep ? x[c] : 0.0;
+        before += __popc(m[c]);
     }
-    const bool keep = fabs(x) > p.tau;
-    const unsigned m = __ballot_sync(FULL, keep);
-    const int pos = kept + __popc(m & ((1u << lane) - 1u));
-    st_entry(keep && pos < p.C.w, crow_v + pos, crow_c + pos, x, F + lane);
-    if ((int64_t)F + lane == i) dc = keep ? x : 0.0;
-    kept += __popc(m);
+    kept = before;
+}
+
+// Emit [F, Fto) (multiples of 32), four chunks at a time where possible; advances F, baseF.
+template <int MODE>
+__device__ __forceinline__ void ring_emit_range(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
+                                                int& F, int& baseF, int Fto, const int32_t* o_col,
+                                                const double* o_val, int nOld, int& old_cur,
+                                                double* __restrict__ crow_v, int32_t* __restrict__ crow_c,
+                                                int& kept, double& ds, double& dc, double& nrm) {
+    while (F + 128 <= Fto) {
+        ring_emit_block<MODE, 4>(p, w, lane, i, F, baseF, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept, ds,
+                                 dc, nrm);
+        F += 128;
+        while (F - baseF >= p.S) baseF += p.S;
+    }
+    while (F < Fto) {
+        ring_emit_block<MODE, 1>(p, w, lane, i, F, baseF, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept, ds,
+                                 dc, nrm);
+        F += 32;
+        if (F - baseF >= p.S) baseF += p.S;
+    }
+    __syncwarp();
 }
 
 template <int G, int D, int MODE>
@@ -481,15 +529,14 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
                 const int t = t0 + d;
                 if (t < cnt) {
                     const int kt = rk[d];
-                    // 1. columns below floor32(k - hB) are final: emit them (frees their slots)
-                    const int target = (kt - hB) & ~31;
-                    while (F < target) {
-                        if (F - baseF >= S) baseF += S;
-                        ring_emit_chunk<MODE>(p, w, lane, i, F, baseF, o_col, o_val, nOld, old_cur, crow_v,
-                                                  crow_c, kept, ds, dc, nrm);
-                        F += 32;
+                    // 1. lazy emission: only when step k would reach a slot still holding an
+                    //    unemitted column (k + hB >= F + S); then emit everything final
+                    //    (< floor32(k - hB)), which batches the emission when the ring has slack.
+                    if (kt + hB >= F + S) {
+                        const int target = (kt - hB) & ~31;
+                        ring_emit_range<MODE>(p, w, lane, i, F, baseF, target, o_col, o_val, nOld, old_cur,
+                                              crow_v, crow_c, kept, ds, dc, nrm);
                     }
-                    __syncwarp();
                     // 2. ring slot mapping for this step: columns [lo, k + hB], lo >= baseS
                     const int lo = max(0, kt - hB);
                     while (lo - baseS >= S) baseS += S;
@@ -528,13 +575,8 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
         }
     }
     // final chunks
-    while (F < Fend) {
-        if (F - baseF >= S) baseF += S;
-        ring_emit_chunk<MODE>(p, w, lane, i, F, baseF, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept,
-                                  ds, dc, nrm);
-        F += 32;
-    }
-    __syncwarp();
+    ring_emit_range<MODE>(p, w, lane, i, F, baseF, Fend, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept, ds,
+                          dc, nrm);
     dc = warp_sum(dc);  // only the diagonal's lane holds a nonzero value (x + 0 = x exactly)
     ds = ds;            // ds is warp-uniform (broadcast shared load)
 }
@@ -591,6 +633,21 @@ __global__ void __launch_bounds__(128, 1) row_op_kernel(const RowOpParams p) {
         double ds = 0.0, dc = 0.0, nrm = 0.0;
         bool done = false;
 
+        if (p.fast && (p.stash_a || p.stash_old)) {
+            // C aliases an input and rows are emitted progressively: copy the input rows aside first
+            double* sv = p.st_val + gw * p.st_stride;
+            int32_t* sc = p.st_col + gw * p.st_stride;
+            if (p.stash_a) {
+                for (int q = lane; q < nA; q += 32) { sv[q] = a_val[q]; sc[q] = a_col[q]; }
+                a_val = sv; a_col = sc;
+                sv += p.A.w; sc += p.A.w;
+            }
+            if (MODE != 0 && p.stash_old) {
+                for (int q = lane; q < nOld; q += 32) { sv[q] = o_val[q]; sc[q] = o_col[q]; }
+                o_val = sv; o_col = sc;
+            }
+            __syncwarp();
+        }
         if (p.fast) {
             // ---- fast path: ring window with progressive emission (single pass)
             row_ring<G, D, MODE>(p, w, lane, i, a_col, a_val, nA, o_col, o_val, nOld, crow_v, crow_c, kept, ds,
