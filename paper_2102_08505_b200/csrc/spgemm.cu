@@ -452,7 +452,7 @@ __device__ __forceinline__ void ring_emit_range(const RowOpParams& p, const Warp
                                                 const double* o_val, int nOld, int& old_cur,
                                                 double* __restrict__ crow_v, int32_t* __restrict__ crow_c,
                                                 int& kept, double& ds, double& dc, double& nrm) {
-    while (F + 128 <= Fto) {
+    while (p.S >= 256 && F + 128 <= Fto) {  // a 128-column block wraps at most once
         ring_emit_block<MODE, 4>(p, w, lane, i, F, baseF, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept, ds,
                                  dc, nrm);
         F += 128;
@@ -502,6 +502,9 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
     double2 rv[NS][G];
     double ra[NS];
     int rnb[NS], rk[NS];
+#ifdef ELL_TIMING
+    long long t_row0 = clock64(), t_em = 0;
+#endif
     for (int p0 = 0; p0 < nA; p0 += kStage) {
         const int cnt = min(kStage, nA - p0);
         stage_piece(p, w, lane, a_col, a_val, p0, cnt, nullptr);
@@ -534,8 +537,14 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
                     //    (< floor32(k - hB)), which batches the emission when the ring has slack.
                     if (kt + hB >= F + S) {
                         const int target = (kt - hB) & ~31;
+#ifdef ELL_TIMING
+                        long long te0 = clock64();
+#endif
                         ring_emit_range<MODE>(p, w, lane, i, F, baseF, target, o_col, o_val, nOld, old_cur,
                                               crow_v, crow_c, kept, ds, dc, nrm);
+#ifdef ELL_TIMING
+                        t_em += clock64() - te0;
+#endif
                     }
                     // 2. ring slot mapping for this step: columns [lo, k + hB], lo >= baseS
                     const int lo = max(0, kt - hB);
@@ -575,8 +584,23 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
         }
     }
     // final chunks
+#ifdef ELL_TIMING
+    long long te1 = clock64();
+#endif
     ring_emit_range<MODE>(p, w, lane, i, F, baseF, Fend, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept, ds,
                           dc, nrm);
+#ifdef ELL_TIMING
+    long long te2 = clock64();
+    t_em += te2 - te1;
+    if (lane == 0 && p.timing) {
+        unsigned long long* T = p.timing + 8 * (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+        atomicAdd(T + 0, 0ull);
+        atomicAdd(T + 1, (unsigned long long)(te2 - t_row0 - t_em));
+        atomicAdd(T + 2, (unsigned long long)t_em);
+        atomicAdd(T + 3, 1ull);
+        atomicAdd(T + 4, (unsigned long long)nA);
+    }
+#endif
     dc = warp_sum(dc);  // only the diagonal's lane holds a nonzero value (x + 0 = x exactly)
     ds = ds;            // ds is warp-uniform (broadcast shared load)
 }
@@ -815,19 +839,33 @@ cudaError_t plan_row_op(const RowOpParams& p, int S, int groups, int warps_opt, 
     const size_t per_warp = warp_smem_bytes(S, p.old_mode != 0);
     const size_t cap = 227 * 1024;
     if (per_warp > cap) return cudaErrorInvalidConfiguration;
-    int wpc = warps_opt > 0 ? warps_opt : 4;
-    if (wpc > 4) wpc = 4;
-    while (wpc > 1 && (size_t)wpc * per_warp > cap) --wpc;
     cfg->S = S;
-    cfg->warps_per_cta = wpc;
     cfg->R = groups < 1 ? 1 : (groups > 4 ? 4 : groups);
-    cfg->smem = (size_t)wpc * per_warp;
-    int bps = 0;
     const int mode = mode_of(p);
-    cudaError_t e = mode == 0 ? prep_mode<0>(*cfg, &bps) : mode == 1 ? prep_mode<1>(*cfg, &bps)
-                                                                      : prep_mode<2>(*cfg, &bps);
-    if (e) return e;
-    if (bps < 1) return cudaErrorInvalidConfiguration;
+    // warps per CTA: maximise resident warps (rows in flight) per SM under the shared-memory
+    // and register limits; ties go to the larger CTA
+    int best_w = 0, best_wpc = 1, best_bps = 0;
+    const int lo_w = warps_opt > 0 ? warps_opt : 1, hi_w = warps_opt > 0 ? warps_opt : 4;
+    for (int wpc = hi_w; wpc >= lo_w; --wpc) {
+        if ((size_t)wpc * per_warp > cap) continue;
+        cfg->warps_per_cta = wpc;
+        cfg->smem = (size_t)wpc * per_warp;
+        int bps = 0;
+        cudaError_t e = mode == 0 ? prep_mode<0>(*cfg, &bps) : mode == 1 ? prep_mode<1>(*cfg, &bps)
+                                                                          : prep_mode<2>(*cfg, &bps);
+        if (e) return e;
+        if (bps * wpc > best_w) { best_w = bps * wpc; best_wpc = wpc; best_bps = bps; }
+    }
+    if (best_w < 1) return cudaErrorInvalidConfiguration;
+    const int wpc = best_wpc, bps = best_bps;
+    cfg->warps_per_cta = wpc;
+    cfg->smem = (size_t)wpc * per_warp;
+    {
+        int dummy = 0;
+        cudaError_t e = mode == 0 ? prep_mode<0>(*cfg, &dummy) : mode == 1 ? prep_mode<1>(*cfg, &dummy)
+                                                                            : prep_mode<2>(*cfg, &dummy);
+        if (e) return e;
+    }
     const int64_t rows = p.row_end - p.row_begin;
     const int64_t need = (rows + wpc - 1) / wpc;
     const int64_t full = (int64_t)bps * num_sms;
