@@ -467,6 +467,23 @@ __device__ __forceinline__ void ring_emit_range(const RowOpParams& p, const Warp
     __syncwarp();
 }
 
+// Emission state of a ring row (kept in registers; copied by value through the rare
+// out-of-line fallback so the unrolled step loop stays small).
+struct EmitState {
+    int F, baseF, old_cur, kept;
+    double ds, dc, nrm;
+};
+
+template <int MODE>
+__device__ __noinline__ EmitState ring_emit_fallback(const RowOpParams& p, WarpSmem w, int lane, int64_t i,
+                                                      EmitState st, int target, const int32_t* o_col,
+                                                      const double* o_val, int nOld, double* crow_v,
+                                                      int32_t* crow_c) {
+    ring_emit_range<MODE>(p, w, lane, i, st.F, st.baseF, target, o_col, o_val, nOld, st.old_cur, crow_v, crow_c,
+                          st.kept, st.ds, st.dc, st.nrm);
+    return st;
+}
+
 template <int G, int D, int MODE>
 __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
                                          const int32_t* a_col, const double* a_val, int nA,
@@ -527,24 +544,33 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
         for (int d = 0; d < D; ++d)
             if (d < cnt) load(d, d);
         for (int t0 = 0; t0 < cnt; t0 += NS) {
+            {
+                // 1. once per block of NS steps: emit every final column (< floor32(k_t0 - hB));
+                //    the ring's slack normally covers the block's k advance
+                const int target = (rk[0] - hB) & ~31;
+                if (target > F) {
+#ifdef ELL_TIMING
+                    long long te0 = clock64();
+#endif
+                    ring_emit_range<MODE>(p, w, lane, i, F, baseF, target, o_col, o_val, nOld, old_cur, crow_v,
+                                          crow_c, kept, ds, dc, nrm);
+#ifdef ELL_TIMING
+                    t_em += clock64() - te0;
+#endif
+                }
+            }
 #pragma unroll
             for (int d = 0; d < NS; ++d) {
                 const int t = t0 + d;
                 if (t < cnt) {
                     const int kt = rk[d];
-                    // 1. lazy emission: only when step k would reach a slot still holding an
-                    //    unemitted column (k + hB >= F + S); then emit everything final
-                    //    (< floor32(k - hB)), which batches the emission when the ring has slack.
+                    // 1b. rare: step k would reach a slot still holding an unemitted column
                     if (kt + hB >= F + S) {
-                        const int target = (kt - hB) & ~31;
-#ifdef ELL_TIMING
-                        long long te0 = clock64();
-#endif
-                        ring_emit_range<MODE>(p, w, lane, i, F, baseF, target, o_col, o_val, nOld, old_cur,
-                                              crow_v, crow_c, kept, ds, dc, nrm);
-#ifdef ELL_TIMING
-                        t_em += clock64() - te0;
-#endif
+                        EmitState st{F, baseF, old_cur, kept, ds, dc, nrm};
+                        st = ring_emit_fallback<MODE>(p, w, lane, i, st, (kt - hB) & ~31, o_col, o_val, nOld,
+                                                      crow_v, crow_c);
+                        F = st.F; baseF = st.baseF; old_cur = st.old_cur; kept = st.kept;
+                        ds = st.ds; dc = st.dc; nrm = st.nrm;
                     }
                     // 2. ring slot mapping for this step: columns [lo, k + hB], lo >= baseS
                     const int lo = max(0, kt - hB);
@@ -607,12 +633,9 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
 
 // -------------------------------------------------------------------------------- kernel
 
-template <int G, int D, int MODE>
-__global__ void __launch_bounds__(128, 1) row_op_kernel(const RowOpParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31;
-    const int wid = threadIdx.x >> 5;
-    const int S = p.S;
+// Per-warp shared layout setup (window/ring + stage + flags).
+template <int MODE>
+__device__ __forceinline__ WarpSmem warp_smem(unsigned char* smem_raw, int wid, int S) {
     unsigned char* base = smem_raw + (size_t)wid * warp_smem_bytes(S, MODE != 0);
     WarpSmem w;
     w.acc = (uint32_t)__cvta_generic_to_shared(base);
@@ -622,64 +645,137 @@ __global__ void __launch_bounds__(128, 1) row_op_kernel(const RowOpParams p) {
     w.ast = w.anb + kStage;
     w.ak = w.ast + kStage;
     w.flg = w.acc + (uint32_t)((S + 2) * 8 + kStage * 28);
-    clear_window<MODE>(w, lane, S);
+    return w;
+}
 
+struct RowIO {
+    const double* a_val;
+    const int32_t* a_col;
+    int32_t nA;
+    const double* o_val;
+    const int32_t* o_col;
+    int32_t nOld;
+    double* crow_v;
+    int32_t* crow_c;
+};
+
+template <int MODE>
+__device__ __forceinline__ RowIO row_io(const RowOpParams& p, int64_t i) {
+    RowIO r;
+    r.a_val = p.A.val + (size_t)i * p.A.w;
+    r.a_col = p.A.col + (size_t)i * p.A.w;
+    r.nA = (p.alpha != 0.0) ? p.A.nnz[i] : 0;
+    r.o_val = nullptr;
+    r.o_col = nullptr;
+    r.nOld = 0;
+    if (MODE != 0) {
+        r.o_val = p.Old.val + (size_t)i * p.Old.w;
+        r.o_col = p.Old.col + (size_t)i * p.Old.w;
+        r.nOld = p.Old.nnz[i];
+    }
+    r.crow_v = p.C.val + (size_t)i * p.C.w;
+    r.crow_c = p.C.col + (size_t)i * p.C.w;
+    return r;
+}
+
+// stored diagonal of A (x2 traces), warp-uniform result
+__device__ __forceinline__ double stored_diag_a(const RowIO& r, int lane, int64_t i) {
+    double dA = 0.0;
+    bool has = false;
+    for (int q = lane; q < r.nA; q += 32)
+        if (r.a_col[q] == (int)i) { dA = r.a_val[q]; has = true; }
+    const unsigned m = __ballot_sync(FULL, has);
+    return m ? __shfl_sync(FULL, dA, __ffs(m) - 1) : 0.0;
+}
+
+template <int MODE>
+__device__ __forceinline__ void row_epilogue(const RowOpParams& p, int lane, int64_t i, int32_t kept, double dA,
+                                             double ds, double dc, double nrm, int32_t& my_max_kept,
+                                             int32_t& my_ovf) {
+    if (lane == 0) p.C.nnz[i] = kept < p.C.w ? kept : p.C.w;
+    my_max_kept = max(my_max_kept, kept);
+    if (kept > p.C.w) ++my_ovf;
+    if (p.diag_c && lane == 0) p.diag_c[i] = dc;
+    if (p.diag_s && lane == 0) p.diag_s[i] = ds;
+    if (p.diag_a && lane == 0) p.diag_a[i] = dA;
+    if (MODE == 2 && p.normsq) {
+        nrm = warp_sum(nrm);
+        if (lane == 0) p.normsq[i] = nrm;
+    }
+}
+
+__device__ __forceinline__ void flush_status(const RowOpParams& p, int lane, int32_t my_max_kept, int32_t my_ovf) {
+    if (lane == 0) {
+        if (my_ovf) atomicAdd(p.status + 0, my_ovf);
+        if (my_max_kept) atomicMax(p.status + 1, my_max_kept);
+    }
+}
+
+// Fast kernel: ring window, every row single-pass (host-verified: ring >= 2 hB + 33,
+// B rows <= 64 G entries).
+template <int G, int D, int MODE>
+__global__ void __launch_bounds__(128, 1) row_fast_kernel(const RowOpParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const WarpSmem w = warp_smem<MODE>(smem_raw, wid, p.S);
+    clear_window<MODE>(w, lane, p.S);
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    const int64_t ncols = p.ncols;
     int32_t my_max_kept = 0, my_ovf = 0;
-
     for (int64_t i = p.row_begin + gw; i < p.row_end; i += nwarps) {
-        const double* a_val = p.A.val + (size_t)i * p.A.w;
-        const int32_t* a_col = p.A.col + (size_t)i * p.A.w;
-        const int32_t nA = (p.alpha != 0.0) ? p.A.nnz[i] : 0;
-        const double* o_val = nullptr;
-        const int32_t* o_col = nullptr;
-        int32_t nOld = 0;
-        if (MODE != 0) {
-            o_val = p.Old.val + (size_t)i * p.Old.w;
-            o_col = p.Old.col + (size_t)i * p.Old.w;
-            nOld = p.Old.nnz[i];
-        }
-        double* crow_v = p.C.val + (size_t)i * p.C.w;
-        int32_t* crow_c = p.C.col + (size_t)i * p.C.w;
-        // stored diagonal of A (x2 traces)
-        double dA = 0.0;
-        if (p.diag_a) {
-            bool has = false;
-            for (int q = lane; q < nA; q += 32)
-                if (a_col[q] == (int)i) { dA = a_val[q]; has = true; }
-            const unsigned m = __ballot_sync(FULL, has);
-            dA = m ? __shfl_sync(FULL, dA, __ffs(m) - 1) : 0.0;
-        }
-
-        int32_t kept = 0;
-        double ds = 0.0, dc = 0.0, nrm = 0.0;
-        bool done = false;
-
-        if (p.fast && (p.stash_a || p.stash_old)) {
+        RowIO r = row_io<MODE>(p, i);
+        const double dA = p.diag_a ? stored_diag_a(r, lane, i) : 0.0;
+        if (p.stash_a || p.stash_old) {
             // C aliases an input and rows are emitted progressively: copy the input rows aside first
             double* sv = p.st_val + gw * p.st_stride;
             int32_t* sc = p.st_col + gw * p.st_stride;
             if (p.stash_a) {
-                for (int q = lane; q < nA; q += 32) { sv[q] = a_val[q]; sc[q] = a_col[q]; }
-                a_val = sv; a_col = sc;
+                for (int q = lane; q < r.nA; q += 32) { sv[q] = r.a_val[q]; sc[q] = r.a_col[q]; }
+                r.a_val = sv; r.a_col = sc;
                 sv += p.A.w; sc += p.A.w;
             }
             if (MODE != 0 && p.stash_old) {
-                for (int q = lane; q < nOld; q += 32) { sv[q] = o_val[q]; sc[q] = o_col[q]; }
-                o_val = sv; o_col = sc;
+                for (int q = lane; q < r.nOld; q += 32) { sv[q] = r.o_val[q]; sc[q] = r.o_col[q]; }
+                r.o_val = sv; r.o_col = sc;
             }
             __syncwarp();
         }
-        if (p.fast) {
-            // ---- fast path: ring window with progressive emission (single pass)
-            row_ring<G, D, MODE>(p, w, lane, i, a_col, a_val, nA, o_col, o_val, nOld, crow_v, crow_c, kept, ds,
-                                 dc, nrm);
-            done = true;
-        }
+        int32_t kept = 0;
+        double ds = 0.0, dc = 0.0, nrm = 0.0;
+        row_ring<G, D, MODE>(p, w, lane, i, r.a_col, r.a_val, r.nA, r.o_col, r.o_val, r.nOld, r.crow_v, r.crow_c,
+                             kept, ds, dc, nrm);
+        row_epilogue<MODE>(p, lane, i, kept, dA, ds, dc, nrm, my_max_kept, my_ovf);
+    }
+    flush_status(p, lane, my_max_kept, my_ovf);
+}
 
-        if (!done) {
+// General kernel: span pre-pass + ceil(span / S) passes of an S-double window with per-k
+// cursors (rows wider than any ring that fits shared memory, B rows > 256 entries).
+template <int MODE>
+__global__ void __launch_bounds__(128, 1) row_general_kernel(const RowOpParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const int S = p.S;
+    const WarpSmem w = warp_smem<MODE>(smem_raw, wid, S);
+    clear_window<MODE>(w, lane, S);
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    int32_t my_max_kept = 0, my_ovf = 0;
+    for (int64_t i = p.row_begin + gw; i < p.row_end; i += nwarps) {
+        RowIO r = row_io<MODE>(p, i);
+        const double* a_val = r.a_val;
+        const int32_t* a_col = r.a_col;
+        const double* o_val = r.o_val;
+        const int32_t* o_col = r.o_col;
+        const int32_t nA = r.nA, nOld = r.nOld;
+        double* crow_v = r.crow_v;
+        int32_t* crow_c = r.crow_c;
+        const double dA = p.diag_a ? stored_diag_a(r, lane, i) : 0.0;
+        int32_t kept = 0;
+        double ds = 0.0, dc = 0.0, nrm = 0.0;
+        {
             // ---- general path: span pre-pass + ceil(span / S) passes with cursors
             int lo = INT_MAX, hi = -1;
             for (int q = lane; q < nA; q += 32) {
@@ -742,22 +838,9 @@ __global__ void __launch_bounds__(128, 1) row_op_kernel(const RowOpParams p) {
             }
         }
 
-        // ---- row epilogue
-        if (lane == 0) p.C.nnz[i] = kept < p.C.w ? kept : p.C.w;
-        my_max_kept = max(my_max_kept, kept);
-        if (kept > p.C.w) ++my_ovf;
-        if (p.diag_c && lane == 0) p.diag_c[i] = dc;
-        if (p.diag_s && lane == 0) p.diag_s[i] = ds;
-        if (p.diag_a && lane == 0) p.diag_a[i] = dA;
-        if (MODE == 2 && p.normsq) {
-            nrm = warp_sum(nrm);
-            if (lane == 0) p.normsq[i] = nrm;
-        }
+        row_epilogue<MODE>(p, lane, i, kept, dA, ds, dc, nrm, my_max_kept, my_ovf);
     }
-    if (lane == 0) {
-        if (my_ovf) atomicAdd(p.status + 0, my_ovf);
-        if (my_max_kept) atomicMax(p.status + 1, my_max_kept);
-    }
+    flush_status(p, lane, my_max_kept, my_ovf);
 }
 
 // Half-bandwidth probe: out[m] = max over rows of max(i - col[i][0], col[i][nnz-1] - i).
@@ -798,24 +881,24 @@ cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64
 
 // ----------------------------------------------------------------------------- dispatch
 
-// Variants by G = ceil(max nnz_B / 64) (64-entry groups per step; prefetch depth D):
-// G1: D 8, G2: D 6, G3: D 4, G4: D 3 (the ring holds D + 1 slots). cfg.R carries G.
-template <int G, int D, int MODE>
-static cudaError_t prep_one(const LaunchCfg& cfg, int* bps) {
-    cudaError_t e = cudaFuncSetAttribute(row_op_kernel<G, D, MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
+// Fast-kernel variants by G = ceil(max nnz_B / 64) (64-entry groups per step; prefetch
+// depth D, the register ring holds D + 1 slots): G1: D 8, G2: D 6, G3: D 4, G4: D 3.
+// cfg.R carries G; cfg.R == 0 selects the general kernel.
+template <typename K>
+static cudaError_t prep_kernel(K kern, const LaunchCfg& cfg, int* bps) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
     if (e) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, row_op_kernel<G, D, MODE>,
-                                                         cfg.warps_per_cta * 32, cfg.smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, kern, cfg.warps_per_cta * 32, cfg.smem);
 }
 
 template <int MODE>
 static cudaError_t prep_mode(const LaunchCfg& cfg, int* bps) {
     switch (cfg.R) {
-        case 1: return prep_one<1, 8, MODE>(cfg, bps);
-        case 2: return prep_one<2, 6, MODE>(cfg, bps);
-        case 3: return prep_one<3, 4, MODE>(cfg, bps);
-        default: return prep_one<4, 3, MODE>(cfg, bps);
+        case 0: return prep_kernel(row_general_kernel<MODE>, cfg, bps);
+        case 1: return prep_kernel(row_fast_kernel<1, 8, MODE>, cfg, bps);
+        case 2: return prep_kernel(row_fast_kernel<2, 6, MODE>, cfg, bps);
+        case 3: return prep_kernel(row_fast_kernel<3, 4, MODE>, cfg, bps);
+        default: return prep_kernel(row_fast_kernel<4, 3, MODE>, cfg, bps);
     }
 }
 
@@ -823,10 +906,11 @@ template <int MODE>
 static void launch_mode(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s) {
     dim3 block(cfg.warps_per_cta * 32), grid(cfg.grid);
     switch (cfg.R) {
-        case 1: row_op_kernel<1, 8, MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        case 2: row_op_kernel<2, 6, MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        case 3: row_op_kernel<3, 4, MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        default: row_op_kernel<4, 3, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 0: row_general_kernel<MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 1: row_fast_kernel<1, 8, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 2: row_fast_kernel<2, 6, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 3: row_fast_kernel<3, 4, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        default: row_fast_kernel<4, 3, MODE><<<grid, block, cfg.smem, s>>>(p); break;
     }
 }
 
@@ -840,7 +924,7 @@ cudaError_t plan_row_op(const RowOpParams& p, int S, int groups, int warps_opt, 
     const size_t cap = 227 * 1024;
     if (per_warp > cap) return cudaErrorInvalidConfiguration;
     cfg->S = S;
-    cfg->R = groups < 1 ? 1 : (groups > 4 ? 4 : groups);
+    cfg->R = !p.fast ? 0 : (groups < 1 ? 1 : (groups > 4 ? 4 : groups));
     const int mode = mode_of(p);
     // warps per CTA: maximise resident warps (rows in flight) per SM under the shared-memory
     // and register limits; ties go to the larger CTA
