@@ -103,12 +103,31 @@ __device__ __forceinline__ void st_entry(bool pred, double* pv, int32_t* pc, dou
 struct WarpSmem {
     uint32_t acc;  // shared address of acc[0]
     uint32_t flg;  // shared address of flags[0]
-    long long* boff;
-    double* aa;
-    int* anb;
-    int* ast;
-    int* ak;
+    uint32_t stg;  // shared address of the stage (explicit 32-bit shared accesses: the
+                   // generic path would route these through L1TEX with long-scoreboard waits)
 };
+
+// stage field accessors (boff | aa | anb | ast | ak, kStage entries each)
+__device__ __forceinline__ long long stg_boff(const WarpSmem& w, int t) {
+    long long v;
+    asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(w.stg + 8u * t) : "memory");
+    return v;
+}
+__device__ __forceinline__ double stg_aa(const WarpSmem& w, int t) { return lds64(w.stg + 8u * (kStage + t)); }
+__device__ __forceinline__ int lds32i(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts32i(uint32_t a, int v) {
+    asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t stg_anb_a(const WarpSmem& w, int t) { return w.stg + 16u * kStage + 4u * t; }
+__device__ __forceinline__ uint32_t stg_ast_a(const WarpSmem& w, int t) { return w.stg + 20u * kStage + 4u * t; }
+__device__ __forceinline__ uint32_t stg_ak_a(const WarpSmem& w, int t) { return w.stg + 24u * kStage + 4u * t; }
+__device__ __forceinline__ int stg_anb(const WarpSmem& w, int t) { return lds32i(stg_anb_a(w, t)); }
+__device__ __forceinline__ int stg_ast(const WarpSmem& w, int t) { return lds32i(stg_ast_a(w, t)); }
+__device__ __forceinline__ int stg_ak(const WarpSmem& w, int t) { return lds32i(stg_ak_a(w, t)); }
 
 // acc has S + 2 slots: acc[S] is the trash slot of padded lanes (16-byte aligned pair).
 __host__ __device__ inline size_t warp_smem_bytes(int S, bool has_old) {
@@ -121,11 +140,12 @@ __device__ __forceinline__ void stage_piece(const RowOpParams& p, const WarpSmem
                                             const int32_t* cur) {
     for (int q = lane; q < cnt; q += 32) {
         const int k = a_col[p0 + q];
-        w.boff[q] = (long long)k * p.B.w;
-        w.ak[q] = k;
-        w.aa[q] = a_val[p0 + q];
-        w.anb[q] = __ldg(p.B.nnz + k);
-        w.ast[q] = cur ? cur[p0 + q] : 0;
+        const long long bo = (long long)k * p.B.w;
+        asm volatile("st.shared.s64 [%0], %1;" ::"r"(w.stg + 8u * q), "l"(bo) : "memory");
+        sts64(w.stg + 8u * (kStage + q), a_val[p0 + q]);
+        sts32i(stg_anb_a(w, q), __ldg(p.B.nnz + k));
+        sts32i(stg_ast_a(w, q), cur ? cur[p0 + q] : 0);
+        sts32i(stg_ak_a(w, q), k);
     }
     __syncwarp();
 }
@@ -152,9 +172,9 @@ __device__ __forceinline__ void accumulate_fast(const RowOpParams& p, const Warp
     const int trash = c0 + S;                          // column that maps to acc[S]
     const uint32_t abase = w.acc - 8u * (uint32_t)c0;  // acc + 8*(j - c0) = abase + 8*j (mod 2^32)
     auto load = [&](int d, int t) {
-        const long long bo = w.boff[t];
-        const int nb = w.anb[t];
-        ra[d] = w.aa[t];
+        const long long bo = stg_boff(w, t);
+        const int nb = stg_anb(w, t);
+        ra[d] = stg_aa(w, t);
         rnb[d] = nb;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
@@ -211,10 +231,10 @@ __device__ __forceinline__ void accumulate_multi(const RowOpParams& p, const War
     const int32_t* __restrict__ bcol = p.B.col;
     const double* __restrict__ bval = p.B.val;
     for (int t = 0; t < cnt; ++t) {
-        const long long bo = w.boff[t];
-        const int nb = w.anb[t];
-        const int st = w.ast[t];
-        const double a = w.aa[t];
+        const long long bo = stg_boff(w, t);
+        const int nb = stg_anb(w, t);
+        const int st = stg_ast(w, t);
+        const double a = stg_aa(w, t);
         int q0 = st, n_in = 0;
         while (q0 < nb) {
             const int qa = q0 + lane, qb = q0 + 32 + lane;
@@ -234,7 +254,7 @@ __device__ __forceinline__ void accumulate_multi(const RowOpParams& p, const War
             if (n < 64) break;
             q0 += 64;
         }
-        if (lane == 0) w.ast[t] = st + n_in;
+        if (lane == 0) sts32i(stg_ast_a(w, t), st + n_in);
         __syncwarp();
     }
 }
@@ -526,11 +546,11 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
         const int cnt = min(kStage, nA - p0);
         stage_piece(p, w, lane, a_col, a_val, p0, cnt, nullptr);
         auto load = [&](int slot, int t) {
-            const long long bo = w.boff[t];
-            const int nb = w.anb[t];
-            ra[slot] = w.aa[t];
+            const long long bo = stg_boff(w, t);
+            const int nb = stg_anb(w, t);
+            ra[slot] = stg_aa(w, t);
             rnb[slot] = nb;
-            rk[slot] = w.ak[t];
+            rk[slot] = stg_ak(w, t);
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 const int q = 64 * g + 2 * lane;
@@ -639,11 +659,7 @@ __device__ __forceinline__ WarpSmem warp_smem(unsigned char* smem_raw, int wid, 
     unsigned char* base = smem_raw + (size_t)wid * warp_smem_bytes(S, MODE != 0);
     WarpSmem w;
     w.acc = (uint32_t)__cvta_generic_to_shared(base);
-    w.boff = reinterpret_cast<long long*>(base + (size_t)(S + 2) * 8);
-    w.aa = reinterpret_cast<double*>(w.boff + kStage);
-    w.anb = reinterpret_cast<int*>(w.aa + kStage);
-    w.ast = w.anb + kStage;
-    w.ak = w.ast + kStage;
+    w.stg = w.acc + (uint32_t)((S + 2) * 8);
     w.flg = w.acc + (uint32_t)((S + 2) * 8 + kStage * 28);
     return w;
 }
@@ -824,7 +840,7 @@ __global__ void __launch_bounds__(128, 1) row_general_kernel(const RowOpParams p
                         stage_piece(p, w, lane, a_col, a_val, p0, cnt, multi ? cur : nullptr);
                         accumulate_multi(p, w, lane, cnt, c0, width);
                         if (multi) {
-                            for (int q = lane; q < cnt; q += 32) cur[p0 + q] = w.ast[q];
+                            for (int q = lane; q < cnt; q += 32) cur[p0 + q] = stg_ast(w, q);
                             __syncwarp();
                         }
                     }
