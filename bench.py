@@ -298,7 +298,7 @@ def run_ours(args):
             "hbm_gbs_algorithmic": Bc / (ms_step * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "ell::row_op_kernel", "kernel_ms_avg": kern_avg,
+                         "kernel": "ell::row_fast_kernel", "kernel_ms_avg": kern_avg,
                          "algorithmic_bytes_per_launch": bytes_launch},
             "cpu_baseline": cpu,
             "e2e": e2e,
