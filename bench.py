@@ -176,11 +176,12 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2102_08505_b200 as eb
+    from paper_2102_08505_b200 import multirank as mr
 
-    ws, rank, local = dist_env()
+    ws, rank, local = mr.dist_env()
     if ws > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        mr.init_process_group("nccl", device=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
@@ -191,10 +192,9 @@ def run_ours(args):
     if args.warps:
         ctx.set_option(eb.OPT_WARPS, args.warps)
     if ws > 1:
-        uid = [eb.Context.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        r0, r1 = eb.row_partition(args.n, ws)[rank]
-        ctx.attach_nccl(ws, rank, uid[0], r0, r1)
+        uid = mr.broadcast_bytes(eb.Context.nccl_unique_id() if rank == 0 else None)
+        r0, r1 = mr.rank_rows(args.n, ws, rank)
+        ctx.attach_nccl(ws, rank, uid, r0, r1)
     tau = 1e-5
     X = synth.cfg5(args.n, args.m)
     n = X.n
@@ -237,9 +237,7 @@ def run_ours(args):
     ctx.set_option(eb.OPT_PROFILE, 0)
     launches = ctx.kernel_launches() - launches0
     if ws > 1:
-        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+        ms_total = mr.max_over_ranks(ms_total, device="cuda")
         dist.barrier()
     ms_step = ms_total / args.steps
     gflops = 2.0 * P / (ms_step * 1e-3) / 1e9

@@ -105,6 +105,10 @@ struct ellpack_ctx_s {
     int64_t ident_n = 0;
     Buf hx_val, hx_col, hx_nnz, hy_val, hy_col, hy_nnz;  // host-path device copies
     Buf timing;                                          // ELL_TIMING debug builds only
+    Buf bt, bt_nbin;                         // bank-balanced copy of B (fast path)
+    // ring sizing cache: (hB, G, mode) -> (S, rows resident per SM)
+    int64_t ring_key = -1;
+    int ring_S = 0;
     // overflow info of the last OVERFLOW
     int64_t last_ovf_rows = 0;
     int32_t last_req = 0;
@@ -242,16 +246,35 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
         S = c->window_opt;
         p.fast = 0;
     } else if (ring <= kFastWindowMax && groups <= 4) {
-        // grow the ring while the resident rows per SM stay the same (slack batches the emission)
-        const size_t cap = 227 * 1024;
-        const size_t per0 = row_op_warp_smem((int)ring, has_old);
-        const size_t rows_sm = cap / per0;
-        int64_t grown = ring;
-        while (grown + 32 <= ring + 512 && grown + 32 <= kFastWindowMax &&
-               cap / row_op_warp_smem((int)(grown + 32), has_old) >= rows_sm)
-            grown += 32;
-        S = grown;
+        // Grow the ring by slack while the rows resident per SM stay the same: slack lets the
+        // emission run in 4-chunk blocks every few steps instead of one chunk per step.
         p.fast = 1;
+        const int mode = !has_old ? 0 : (p.normsq ? 2 : 1);
+        const int64_t key = ((ring * 8 + groups) * 4 + mode) * 64 + c->warps_opt;
+        if (key != c->ring_key) {
+            LaunchCfg t;
+            CK(plan_row_op(p, (int)ring, groups, c->warps_opt, c->num_sms, &t));
+            const int64_t rows0 = (int64_t)t.grid * t.warps_per_cta;  // resident rows (full grid)
+            int64_t grown = ring;
+            for (int64_t s2 = ring + 32; s2 <= ring + 512 && s2 <= kFastWindowMax && s2 <= nr; s2 += 32) {
+                LaunchCfg u;
+                if (plan_row_op(p, (int)s2, groups, c->warps_opt, c->num_sms, &u) != cudaSuccess) break;
+                if ((int64_t)u.grid * u.warps_per_cta < rows0) break;
+                grown = s2;
+            }
+            c->ring_key = key;
+            c->ring_S = (int)grown;
+        }
+        S = c->ring_S;
+        // bank-balanced copy of B (all N rows: B is the full operand on every rank)
+        const int wt = 64 * (groups < 1 ? 1 : groups);
+        RK(grow(c, c->bt, (size_t)12 * n * wt));
+        RK(grow(c, c->bt_nbin, sizeof(int32_t) * (size_t)n));
+        CK(launch_balance(p.B, n, wt, (unsigned char*)c->bt.p, (int32_t*)c->bt_nbin.p, c->num_sms, c->stream));
+        c->launches++;
+        p.bt = (const unsigned char*)c->bt.p;
+        p.bt_nbin = (const int32_t*)c->bt_nbin.p;
+        p.bt_w = wt;
     } else {
         S = kGeneralWindow;
         p.fast = 0;
@@ -442,7 +465,8 @@ int ellpack_ctx_destroy(ellpack_ctx c) {
     cudaSetDevice(c->device);
     Buf* bufs[] = {&c->rows[0], &c->rows[1], &c->rows[2], &c->rows[3], &c->partials, &c->cursors,
                    &c->stash_val, &c->stash_col, &c->ident_val, &c->ident_col, &c->ident_nnz,
-                   &c->hx_val, &c->hx_col, &c->hx_nnz, &c->hy_val, &c->hy_col, &c->hy_nnz};
+                   &c->hx_val, &c->hx_col, &c->hx_nnz, &c->hy_val, &c->hy_col, &c->hy_nnz,
+                   &c->bt, &c->bt_nbin, &c->timing};
     for (Buf* b : bufs) release(c, *b);
     cudaStreamSynchronize(c->stream);
     if (c->comm && g_nccl.ok) g_nccl.CommDestroy(c->comm);

@@ -130,8 +130,9 @@ __device__ __forceinline__ int stg_ast(const WarpSmem& w, int t) { return lds32i
 __device__ __forceinline__ int stg_ak(const WarpSmem& w, int t) { return lds32i(stg_ak_a(w, t)); }
 
 // acc has S + 2 slots: acc[S] is the trash slot of padded lanes (16-byte aligned pair).
-__host__ __device__ inline size_t warp_smem_bytes(int S, bool has_old) {
-    return (size_t)(S + 2) * 8 + (size_t)kStage * 28 + (has_old ? (size_t)S : 0);
+// The fast path's stage holds 16 B per entry (a_ik, k, NB(k)); the general path's 28 B.
+__host__ __device__ inline size_t warp_smem_bytes(int S, bool has_old, bool fast) {
+    return (size_t)(S + 2) * 8 + (size_t)kStage * (fast ? 16 : 28) + (has_old ? (size_t)S : 0);
 }
 
 // Stage A-row entries [p0, p0 + cnt): B-row offset k*B.w, a_ik, nnz_B(k), cursor.
@@ -150,76 +151,122 @@ __device__ __forceinline__ void stage_piece(const RowOpParams& p, const WarpSmem
     __syncwarp();
 }
 
-// ---------------------------------------------------------------------------- fast path
+// ------------------------------------------------------------- bank-balanced B (fast path)
+//
+// The accumulator is a dense ring of doubles: entry (k, j) of a B row updates ring slot
+// (j - base) mod S, i.e. shared-memory bank pair j mod 16 (S and base are multiples of 32).
+// Measured on B200 (tools/bank_bench.cu): a warp-wide 64-bit shared access is served as two
+// 16-lane halves; each half costs as many wavefronts as its most-repeated bank pair (loads
+// retire two wavefronts per clock, stores one). Column indices of a sorted B row are
+// random modulo 16, so taking consecutive entries costs 3-6 wavefronts per instruction
+// (r01 profile). The entries of ONE B row have distinct columns, so the order in which the
+// lanes apply them within a step is free: the fma chain of every output entry stays
+// ascending in k (R12). The balance pass stores each B row permuted so that every 16-lane
+// half sees (nearly) distinct bank pairs:
+//   1. rank the row's entries by residue r = j mod 16 (stable counting sort): e in [0, n);
+//   2. deal the ranks round-robin over NB = ceil(n / 16) half-instruction bins:
+//      bin b = e mod NB, position m = e / NB (a residue with c_r <= NB entries lands in
+//      c_r distinct bins);
+//   3. bin b is half h = (b >> 1) & 1 of instruction (group g = b >> 2, parity b & 1):
+//      slot 64 g + 2 (16 h + m) + (b & 1), so a lane's two slots of a group are adjacent
+//      (one 8-byte offset load, one 16-byte value load).
+// Row record (12 * 64 G bytes): int32 off[64 G] then f64 val[64 G]; off = 8 (j - k) (the
+// kernel adds the warp-uniform 8 (k - base)); unused slots of used groups hold INT_MIN.
+// bt_nbin[k] = NB: group g is loaded iff NB > 4 g.
+constexpr int32_t kPad = INT_MIN;
 
-// Accumulate the staged steps [0, cnt) into the window [c0, c0 + S). The host's probe
-// guarantees (i) every product column lies inside the window and (ii) every B row has at
-// most 64*G entries, so a step is a fixed, branch-free block: each lane takes entries
-// 2*lane, 2*lane+1 of each 64-entry group (8/16-byte vector loads), forms the shared
-// address acc + 8*(j - c0) with one IMAD from a per-row base (entries past nnz_B(k) are
-// sent to a per-warp trash slot acc[S] instead of being predicated), then issues all 2G
-// shared loads, all 2G FMAs and all 2G shared stores of the step. Ring slots hold raw
-// loaded registers and are not read until the step is consumed D steps later.
-template <int G, int D>
-__device__ __forceinline__ void accumulate_fast(const RowOpParams& p, const WarpSmem& w, int lane, int cnt,
-                                                int c0, int S) {
-    int2 rc[D][G];
-    double2 rv[D][G];
-    double ra[D];
-    int rnb[D];
-    const int32_t* __restrict__ bcol = p.B.col;
-    const double* __restrict__ bval = p.B.val;
-    const int trash = c0 + S;                          // column that maps to acc[S]
-    const uint32_t abase = w.acc - 8u * (uint32_t)c0;  // acc + 8*(j - c0) = abase + 8*j (mod 2^32)
-    auto load = [&](int d, int t) {
-        const long long bo = stg_boff(w, t);
-        const int nb = stg_anb(w, t);
-        ra[d] = stg_aa(w, t);
-        rnb[d] = nb;
+__global__ void balance_kernel(KMat b, int64_t n, int wt, unsigned char* __restrict__ bt,
+                               int32_t* __restrict__ bt_nbin) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = w0; k < n; k += nw) {
+        const int nb = b.nnz[k];
+        const int NB = (nb + 15) >> 4;
+        const int32_t* __restrict__ bc = b.col + (size_t)k * b.w;
+        const double* __restrict__ bv = b.val + (size_t)k * b.w;
+        int32_t* __restrict__ oo = reinterpret_cast<int32_t*>(bt + (size_t)k * 12 * wt);
+        double* __restrict__ ov = reinterpret_cast<double*>(bt + (size_t)k * 12 * wt + 4 * (size_t)wt);
+        if (lane == 0) bt_nbin[k] = NB;
+        const int used = 64 * ((NB + 3) >> 2);
+        for (int s = lane; s < used; s += 32) oo[s] = kPad;
+        // pass 1: per-residue counts (warp-uniform)
+        int cnt[16];
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const int q = 64 * g + 2 * lane;
-            if (q < nb) {
-                rc[d][g] = __ldg(reinterpret_cast<const int2*>(bcol + bo + q));
-                rv[d][g] = __ldg(reinterpret_cast<const double2*>(bval + bo + q));
-            }
+        for (int r = 0; r < 16; ++r) cnt[r] = 0;
+        for (int c = 0; c < nb; c += 32) {
+            const int q = c + lane;
+            const int res = q < nb ? (__ldg(bc + q) & 15) : 16;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) cnt[r] += __popc(__ballot_sync(FULL, res == r));
         }
-    };
+        int run[16];
+        int acc = 0;
 #pragma unroll
-    for (int d = 0; d < D; ++d)
-        if (d < cnt) load(d, d);
-    for (int t0 = 0; t0 < cnt; t0 += D) {
+        for (int r = 0; r < 16; ++r) { run[r] = acc; acc += cnt[r]; }
+        __syncwarp();  // padding fill ordered before the scatter
+        // pass 2: rank e within the residue-sorted order, dealt round-robin over the bins
+        for (int c = 0; c < nb; c += 32) {
+            const int q = c + lane;
+            const bool v = q < nb;
+            const int j = v ? __ldg(bc + q) : 0;
+            const int res = v ? (j & 15) : 16;
+            int e = 0;
 #pragma unroll
-        for (int d = 0; d < D; ++d) {
-            const int t = t0 + d;
-            if (t < cnt) {
-                const double a = ra[d];
-                const int nb = rnb[d];
-                uint32_t ad[G][2];
-                double old[G][2];
-#pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const int q = 64 * g + 2 * lane;
-                    const int j0 = q < nb ? rc[d][g].x : trash;
-                    const int j1 = q + 1 < nb ? rc[d][g].y : trash;
-                    ad[g][0] = abase + 8u * (uint32_t)j0;
-                    ad[g][1] = abase + 8u * (uint32_t)j1;
-                }
-#pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    old[g][0] = lds64(ad[g][0]);
-                    old[g][1] = lds64(ad[g][1]);
-                }
-#pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    sts64(ad[g][0], __fma_rn(a, rv[d][g].x, old[g][0]));
-                    sts64(ad[g][1], __fma_rn(a, rv[d][g].y, old[g][1]));
-                }
-                if (t + D < cnt) load(d, t + D);
-                __syncwarp();
+            for (int r = 0; r < 16; ++r) {
+                const unsigned m = __ballot_sync(FULL, res == r);
+                if (res == r) e = run[r] + __popc(m & lt);
+                run[r] += __popc(m);
+            }
+            if (v) {
+                const int bin = e % NB, pos = e / NB;
+                const int sl = 64 * (bin >> 2) + 2 * (16 * ((bin >> 1) & 1) + pos) + (bin & 1);
+                oo[sl] = 8 * (j - (int)k);
+                ov[sl] = __ldg(bv + q);
             }
         }
     }
+}
+
+cudaError_t launch_balance(KMat b, int64_t n, int wt, unsigned char* bt, int32_t* bt_nbin, int num_sms,
+                           cudaStream_t s) {
+    const int64_t blocks_needed = (n + 7) / 8;
+    const int64_t cap = (int64_t)num_sms * 8;
+    balance_kernel<<<(unsigned)(blocks_needed < cap ? blocks_needed : cap), 256, 0, s>>>(b, n, wt, bt, bt_nbin);
+    return cudaGetLastError();
+}
+
+// Fast-path stage: 16 B per A entry {a_ik f64, k i32, NB(k) i32} (one 16-byte shared load per step)
+__device__ __forceinline__ void stage_fast(const RowOpParams& p, const WarpSmem& w, int lane,
+                                           const int32_t* a_col, const double* a_val, int p0, int cnt) {
+    for (int q = lane; q < cnt; q += 32) {
+        const int k = a_col[p0 + q];
+        const int nb = __ldg(p.bt_nbin + k);
+        const unsigned long long knb = (unsigned long long)(uint32_t)k | ((unsigned long long)(uint32_t)nb << 32);
+        asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(w.stg + 16u * q),
+                     "l"(__double_as_longlong(a_val[p0 + q])), "l"(knb) : "memory");
+    }
+    __syncwarp();
+}
+__device__ __forceinline__ void stage_fast_get(const WarpSmem& w, int t, double& a, int& k, int& nb) {
+    unsigned long long x, y;
+    asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(w.stg + 16u * t) : "memory");
+    a = __longlong_as_double((long long)x);
+    k = (int)(uint32_t)y;
+    nb = (int)(y >> 32);
+}
+
+// predicated shared accesses (padding lanes issue no request and cost no wavefront)
+__device__ __forceinline__ double lds64_if(bool pr, uint32_t a) {
+    double v;  // undefined when !pr (the predicated store discards the result)
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t@q ld.shared.f64 %0, [%2];\n\t}"
+                 : "=d"(v) : "r"((int)pr), "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts64_if(bool pr, uint32_t a, double v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.shared.f64 [%1], %2;\n\t}"
+                 ::"r"((int)pr), "r"(a), "d"(v) : "memory");
 }
 
 // ------------------------------------------------------------------------- general path
@@ -388,6 +435,112 @@ __device__ __forceinline__ void clear_window(const WarpSmem& w, int lane, int S)
 // twice the rows in flight per SM. Each step is software-pipelined over a (D+1)-slot
 // register ring: the gathers for step t + D are issued before step t's FMAs.
 
+// Combine the Old entries with columns < Fe (ascending, from old_cur) into the ring:
+// s <- fma(alpha, s, beta*old) (old_mode 1) or fma(alpha, s, +0) (old_mode 2, with the
+// ||S - Old||^2 term), and flag the slot so the emit does not scale it again.
+template <int MODE>
+__device__ __forceinline__ void ring_merge_old(const RowOpParams& p, const WarpSmem& w, int lane, int Fe,
+                                               int baseF, const int32_t* o_col, const double* o_val, int nOld,
+                                               int& old_cur, double& nrm) {
+    const int S = p.S;
+    while (old_cur < nOld) {
+        const int q = old_cur + lane;
+        const bool v = q < nOld;
+        const int jo = v ? o_col[q] : INT_MAX;
+        const bool inr = jo < Fe;
+        if (inr) {
+            const double x = o_val[q];
+            int po = jo - baseF;
+            if (po >= S) po -= S;
+            const uint32_t sa = w.acc + 8u * (uint32_t)po;
+            const double sv = lds64(sa);
+            if (MODE == 2) {
+                const double df = __dsub_rn(sv, x);
+                nrm = __fma_rn(df, df, nrm);
+            }
+            const double tt = (p.old_mode == 1) ? __dmul_rn(p.beta, x) : 0.0;
+            sts64(sa, __fma_rn(p.alpha, sv, tt));
+            sts8(w.flg + (uint32_t)po, 1u);
+        }
+        const int n = __popc(__ballot_sync(FULL, inr));
+        old_cur += n;
+        if (n < 32) break;
+    }
+    __syncwarp();
+}
+
+// Emit NP consecutive 64-column pairs of chunks [F, F + 64 NP): each lane owns two adjacent
+// columns (one 16-byte shared load and one 16-byte zeroing store per lane), two ballots per
+// pair compact the kept entries in ascending column order:
+//   rank(F + 64c + 2l) = popc(m0 & lt) + popc(m1 & lt),  rank(+1) = rank + keep0.
+// A 32-column chunk never straddles the ring wrap (S, F - baseF multiples of 32), so each
+// lane's pair is contiguous in the ring.
+template <int MODE, int NP>
+__device__ __forceinline__ void ring_emit_pairs(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
+                                                int F, int baseF, const int32_t* o_col, const double* o_val,
+                                                int nOld, int& old_cur, double* __restrict__ crow_v,
+                                                int32_t* __restrict__ crow_c, int& kept, double& ds, double& dc,
+                                                double& nrm) {
+    const int S = p.S;
+    const int Fe = F + 64 * NP;
+    if ((int64_t)F <= i && i < (int64_t)Fe) {
+        int pi = (int)(i - baseF);
+        if (pi >= S) pi -= S;
+        ds = lds64(w.acc + 8u * (uint32_t)pi);
+    }
+    if (MODE != 0) ring_merge_old<MODE>(p, w, lane, Fe, baseF, o_col, o_val, nOld, old_cur, nrm);
+    const bool a1 = p.alpha == 1.0;
+    double x[NP][2];
+    unsigned m[NP][2];
+#pragma unroll
+    for (int c = 0; c < NP; ++c) {
+        int sl = F + 64 * c + 2 * lane - baseF;
+        if (sl >= S) sl -= S;
+        const uint32_t pa = w.acc + 8u * (uint32_t)sl;
+        double v0, v1;
+        lds128(pa, v0, v1);
+        sts128(pa, 0.0, 0.0);
+        bool f0 = false, f1 = false;
+        if (MODE != 0) {
+            const uint32_t fa = w.flg + (uint32_t)sl;
+            const uint32_t fl = lds16u(fa);
+            f0 = (fl & 0xffu) != 0;
+            f1 = (fl >> 8) != 0;
+            sts16u(fa, 0u);
+        }
+        x[c][0] = v0;
+        x[c][1] = v1;
+        if (!f0) {
+            if (!a1) x[c][0] = __dmul_rn(p.alpha, v0);
+            if (MODE == 2) nrm = __fma_rn(v0, v0, nrm);
+        }
+        if (!f1) {
+            if (!a1) x[c][1] = __dmul_rn(p.alpha, v1);
+            if (MODE == 2) nrm = __fma_rn(v1, v1, nrm);
+        }
+        m[c][0] = __ballot_sync(FULL, fabs(x[c][0]) > p.tau);
+        m[c][1] = __ballot_sync(FULL, fabs(x[c][1]) > p.tau);
+    }
+    const unsigned lt = (1u << lane) - 1u;
+    const bool want_dc = p.diag_c != nullptr;
+    int before = kept;
+#pragma unroll
+    for (int c = 0; c < NP; ++c) {
+        const bool k0 = (m[c][0] >> lane) & 1u, k1 = (m[c][1] >> lane) & 1u;
+        const int pos0 = before + __popc(m[c][0] & lt) + __popc(m[c][1] & lt);
+        const int pos1 = pos0 + (int)k0;
+        const int col0 = F + 64 * c + 2 * lane;
+        st_entry(k0 && pos0 < p.C.w, crow_v + pos0, crow_c + pos0, x[c][0], col0);
+        st_entry(k1 && pos1 < p.C.w, crow_v + pos1, crow_c + pos1, x[c][1], col0 + 1);
+        if (want_dc) {
+            if ((int64_t)col0 == i) dc = k0 ? x[c][0] : 0.0;
+            if ((int64_t)col0 + 1 == i) dc = k1 ? x[c][1] : 0.0;
+        }
+        before += __popc(m[c][0]) + __popc(m[c][1]);
+    }
+    kept = before;
+}
+
 // Emit NCH consecutive 32-column chunks [F, F + 32 NCH) (column j lives in ring slot
 // j - baseF, minus S past the wrap): pre-combine diagonal, combine with Old, drop, compact
 // (NCH independent ballots) and write; the slots (and flags) are cleared.
@@ -404,32 +557,7 @@ __device__ __forceinline__ void ring_emit_block(const RowOpParams& p, const Warp
         if (pi >= S) pi -= S;
         ds = lds64(w.acc + 8u * (uint32_t)pi);
     }
-    if (MODE != 0) {
-        while (old_cur < nOld) {
-            const int q = old_cur + lane;
-            const bool v = q < nOld;
-            const int jo = v ? o_col[q] : INT_MAX;
-            const bool inr = jo < Fe;
-            if (inr) {
-                const double x = o_val[q];
-                int po = jo - baseF;
-                if (po >= S) po -= S;
-                const uint32_t sa = w.acc + 8u * (uint32_t)po;
-                const double sv = lds64(sa);
-                if (MODE == 2) {
-                    const double df = __dsub_rn(sv, x);
-                    nrm = __fma_rn(df, df, nrm);
-                }
-                const double tt = (p.old_mode == 1) ? __dmul_rn(p.beta, x) : 0.0;
-                sts64(sa, __fma_rn(p.alpha, sv, tt));
-                sts8(w.flg + (uint32_t)po, 1u);
-            }
-            const int n = __popc(__ballot_sync(FULL, inr));
-            old_cur += n;
-            if (n < 32) break;
-        }
-        __syncwarp();
-    }
+    if (MODE != 0) ring_merge_old<MODE>(p, w, lane, Fe, baseF, o_col, o_val, nOld, old_cur, nrm);
     double x[NCH];
     unsigned m[NCH];
 #pragma unroll
@@ -473,7 +601,7 @@ __device__ __forceinline__ void ring_emit_range(const RowOpParams& p, const Warp
                                                 double* __restrict__ crow_v, int32_t* __restrict__ crow_c,
                                                 int& kept, double& ds, double& dc, double& nrm) {
     while (p.S >= 256 && F + 128 <= Fto) {  // a 128-column block wraps at most once
-        ring_emit_block<MODE, 4>(p, w, lane, i, F, baseF, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept, ds,
+        ring_emit_pairs<MODE, 2>(p, w, lane, i, F, baseF, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept, ds,
                                  dc, nrm);
         F += 128;
         while (F - baseF >= p.S) baseF += p.S;
@@ -487,34 +615,27 @@ __device__ __forceinline__ void ring_emit_range(const RowOpParams& p, const Warp
     __syncwarp();
 }
 
-// Emission state of a ring row (kept in registers; copied by value through the rare
-// out-of-line fallback so the unrolled step loop stays small).
-struct EmitState {
-    int F, baseF, old_cur, kept;
-    double ds, dc, nrm;
-};
-
-template <int MODE>
-__device__ __noinline__ EmitState ring_emit_fallback(const RowOpParams& p, WarpSmem w, int lane, int64_t i,
-                                                      EmitState st, int target, const int32_t* o_col,
-                                                      const double* o_val, int nOld, double* crow_v,
-                                                      int32_t* crow_c) {
-    ring_emit_range<MODE>(p, w, lane, i, st.F, st.baseF, target, o_col, o_val, nOld, st.old_cur, crow_v, crow_c,
-                          st.kept, st.ds, st.dc, st.nrm);
-    return st;
-}
-
-template <int G, int D, int MODE>
+// One output row on the ring fast path. B is the bank-balanced copy (p.bt, 64 G slots per
+// row); A's row is staged in pieces of kStage entries; a (D+1)-slot register ring holds the
+// gathered B rows of the next D steps. Before step k, if the step's columns [k - hB, k + hB]
+// would reach a ring slot still holding an unemitted column, every column below
+// floor32(k - hB) (final: later steps only touch columns >= k' - hB >= k - hB) is emitted in
+// 4-chunk blocks; with S >= 2 hB + 33 + slack that happens every few steps.
+//
+// Per entry the step costs one IADD (ring offset = uniform 8 (k - base) + stored 8 (j - k)),
+// one IADD + one unsigned min (wrap: min(o, o - 8 S) as unsigned picks o - 8 S exactly when
+// o >= 8 S), a padding test, and the LDS / DFMA / STS of the update.
+template <int G, int B, int MODE>
 __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
                                          const int32_t* a_col, const double* a_val, int nA,
                                          const int32_t* o_col, const double* o_val, int nOld,
                                          double* __restrict__ crow_v, int32_t* __restrict__ crow_c,
                                          int& kept, double& ds, double& dc, double& nrm) {
-    constexpr int NS = D + 1;  // register ring slots
+    constexpr int NS = 2 * B;  // register ring slots: two halves of B steps
     const int S = p.S;
+    const uint32_t S8 = 8u * (uint32_t)S;
     const int hB = p.hB;
     const int ncols = (int)p.ncols;
-    (void)ncols;
     // column extent of the row: products in [k_first - hB, k_last + hB], plus Old entries
     int lo_col = INT_MAX, hi_col = -1;
     if (nA > 0) {
@@ -531,98 +652,84 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
     int baseF = F - F % S;  // multiple of S with baseF <= F < baseF + S
     int baseS = baseF;
     int old_cur = 0;
-    const uint32_t trash = w.acc + 8u * (uint32_t)S;
-    const int32_t* __restrict__ bcol = p.B.col;
-    const double* __restrict__ bval = p.B.val;
+    const uint32_t acc = w.acc;
+    const size_t rs = (size_t)12 * p.bt_w;  // balanced row record bytes
+    const unsigned char* __restrict__ bto = p.bt + 8 * lane;                   // offsets, lane pair
+    const unsigned char* __restrict__ btv = p.bt + 4 * (size_t)p.bt_w + 16 * lane;  // values, lane pair
 
-    int2 rc[NS][G];
+    int2 ro[NS][G];
     double2 rv[NS][G];
     double ra[NS];
     int rnb[NS], rk[NS];
-#ifdef ELL_TIMING
-    long long t_row0 = clock64(), t_em = 0;
-#endif
     for (int p0 = 0; p0 < nA; p0 += kStage) {
         const int cnt = min(kStage, nA - p0);
-        stage_piece(p, w, lane, a_col, a_val, p0, cnt, nullptr);
+        stage_fast(p, w, lane, a_col, a_val, p0, cnt);
         auto load = [&](int slot, int t) {
-            const long long bo = stg_boff(w, t);
-            const int nb = stg_anb(w, t);
-            ra[slot] = stg_aa(w, t);
+            int k, nb;
+            stage_fast_get(w, t, ra[slot], k, nb);
             rnb[slot] = nb;
-            rk[slot] = stg_ak(w, t);
+            rk[slot] = k;
+            const size_t rb = (size_t)k * rs;
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                const int q = 64 * g + 2 * lane;
-                if (q < nb) {
-                    rc[slot][g] = __ldg(reinterpret_cast<const int2*>(bcol + bo + q));
-                    rv[slot][g] = __ldg(reinterpret_cast<const double2*>(bval + bo + q));
+                if (nb > 4 * g) {
+                    ro[slot][g] = __ldg(reinterpret_cast<const int2*>(bto + rb + 256 * g));
+                    rv[slot][g] = __ldg(reinterpret_cast<const double2*>(btv + rb + 512 * g));
                 }
             }
         };
+        // Gathers are issued a half-ring (B steps) at a time, right after the first step of the
+        // other half has consumed its data: a variable-latency scoreboard slot drains as a whole,
+        // so waiting for step t's registers also waits for every gather issued before it -- one
+        // batch per B steps keeps the youngest outstanding gather B steps (not one step) away.
 #pragma unroll
-        for (int d = 0; d < D; ++d)
-            if (d < cnt) load(d, d);
+        for (int d = 0; d < B; ++d) load(d, min(d, cnt - 1));
         for (int t0 = 0; t0 < cnt; t0 += NS) {
-            {
-                // 1. once per block of NS steps: emit every final column (< floor32(k_t0 - hB));
-                //    the ring's slack normally covers the block's k advance
-                const int target = (rk[0] - hB) & ~31;
-                if (target > F) {
-#ifdef ELL_TIMING
-                    long long te0 = clock64();
-#endif
-                    ring_emit_range<MODE>(p, w, lane, i, F, baseF, target, o_col, o_val, nOld, old_cur, crow_v,
-                                          crow_c, kept, ds, dc, nrm);
-#ifdef ELL_TIMING
-                    t_em += clock64() - te0;
-#endif
-                }
-            }
 #pragma unroll
             for (int d = 0; d < NS; ++d) {
                 const int t = t0 + d;
                 if (t < cnt) {
                     const int kt = rk[d];
-                    // 1b. rare: step k would reach a slot still holding an unemitted column
-                    if (kt + hB >= F + S) {
-                        EmitState st{F, baseF, old_cur, kept, ds, dc, nrm};
-                        st = ring_emit_fallback<MODE>(p, w, lane, i, st, (kt - hB) & ~31, o_col, o_val, nOld,
-                                                      crow_v, crow_c);
-                        F = st.F; baseF = st.baseF; old_cur = st.old_cur; kept = st.kept;
-                        ds = st.ds; dc = st.dc; nrm = st.nrm;
-                    }
-                    // 2. ring slot mapping for this step: columns [lo, k + hB], lo >= baseS
+                    // 1. emit the final columns when step k would wrap onto them
+                    if (kt + hB >= F + S)
+                        ring_emit_range<MODE>(p, w, lane, i, F, baseF, (kt - hB) & ~31, o_col, o_val, nOld,
+                                              old_cur, crow_v, crow_c, kept, ds, dc, nrm);
+                    // 2. ring base for this step: columns [lo, k + hB], lo >= baseS
                     const int lo = max(0, kt - hB);
                     while (lo - baseS >= S) baseS += S;
-                    const uint32_t abase = w.acc - 8u * (uint32_t)baseS;
-                    const int jw = baseS + S;
+                    const uint32_t kb8 = 8u * (uint32_t)(kt - baseS);
                     const int nb = rnb[d];
                     const double a = ra[d];
                     uint32_t ad[G][2];
+                    bool pv[G][2];
 #pragma unroll
                     for (int g = 0; g < G; ++g) {
-                        const int q = 64 * g + 2 * lane;
-                        const int j0 = rc[d][g].x, j1 = rc[d][g].y;
-                        uint32_t a0 = abase + 8u * (uint32_t)j0 - (j0 >= jw ? 8u * (uint32_t)S : 0u);
-                        uint32_t a1 = abase + 8u * (uint32_t)j1 - (j1 >= jw ? 8u * (uint32_t)S : 0u);
-                        ad[g][0] = q < nb ? a0 : trash;
-                        ad[g][1] = q + 1 < nb ? a1 : trash;
+                        const bool gl = nb > 4 * g;  // warp-uniform: group loaded
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int o = h ? ro[d][g].y : ro[d][g].x;
+                            const uint32_t r = kb8 + (uint32_t)o;
+                            ad[g][h] = acc + min(r, r - S8);
+                            pv[g][h] = gl && o != kPad;
+                        }
                     }
-                    // 3. shared loads of the step
+                    // 3. shared loads, fma, shared stores of the step
                     double old[G][2];
 #pragma unroll
                     for (int g = 0; g < G; ++g) {
-                        old[g][0] = lds64(ad[g][0]);
-                        old[g][1] = lds64(ad[g][1]);
+                        old[g][0] = lds64_if(pv[g][0], ad[g][0]);
+                        old[g][1] = lds64_if(pv[g][1], ad[g][1]);
                     }
-                    // 4. gathers for step t + D into the slot freed by step t - 1
-                    if (t + D < cnt) load((d + D) % NS, t + D);
-                    // 5. fma + shared stores
 #pragma unroll
                     for (int g = 0; g < G; ++g) {
-                        sts64(ad[g][0], __fma_rn(a, rv[d][g].x, old[g][0]));
-                        sts64(ad[g][1], __fma_rn(a, rv[d][g].y, old[g][1]));
+                        sts64_if(pv[g][0], ad[g][0], __fma_rn(a, rv[d][g].x, old[g][0]));
+                        sts64_if(pv[g][1], ad[g][1], __fma_rn(a, rv[d][g].y, old[g][1]));
+                    }
+                    // 4. first step of a half: gathers of the next B steps into the other half
+                    //    (after this step's stores: the asm memory clobbers keep them here)
+                    if (d == 0 || d == B) {
+#pragma unroll
+                        for (int e = 0; e < B; ++e) load((d == 0 ? B : 0) + e, min(t + B + e, cnt - 1));
                     }
                     __syncwarp();
                 }
@@ -630,37 +737,21 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
         }
     }
     // final chunks
-#ifdef ELL_TIMING
-    long long te1 = clock64();
-#endif
     ring_emit_range<MODE>(p, w, lane, i, F, baseF, Fend, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept, ds,
                           dc, nrm);
-#ifdef ELL_TIMING
-    long long te2 = clock64();
-    t_em += te2 - te1;
-    if (lane == 0 && p.timing) {
-        unsigned long long* T = p.timing + 8 * (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
-        atomicAdd(T + 0, 0ull);
-        atomicAdd(T + 1, (unsigned long long)(te2 - t_row0 - t_em));
-        atomicAdd(T + 2, (unsigned long long)t_em);
-        atomicAdd(T + 3, 1ull);
-        atomicAdd(T + 4, (unsigned long long)nA);
-    }
-#endif
     dc = warp_sum(dc);  // only the diagonal's lane holds a nonzero value (x + 0 = x exactly)
-    ds = ds;            // ds is warp-uniform (broadcast shared load)
 }
 
 // -------------------------------------------------------------------------------- kernel
 
 // Per-warp shared layout setup (window/ring + stage + flags).
 template <int MODE>
-__device__ __forceinline__ WarpSmem warp_smem(unsigned char* smem_raw, int wid, int S) {
-    unsigned char* base = smem_raw + (size_t)wid * warp_smem_bytes(S, MODE != 0);
+__device__ __forceinline__ WarpSmem warp_smem(unsigned char* smem_raw, int wid, int S, bool fast) {
+    unsigned char* base = smem_raw + (size_t)wid * warp_smem_bytes(S, MODE != 0, fast);
     WarpSmem w;
     w.acc = (uint32_t)__cvta_generic_to_shared(base);
     w.stg = w.acc + (uint32_t)((S + 2) * 8);
-    w.flg = w.acc + (uint32_t)((S + 2) * 8 + kStage * 28);
+    w.flg = w.acc + (uint32_t)((S + 2) * 8 + kStage * (fast ? 16 : 28));
     return w;
 }
 
@@ -728,16 +819,16 @@ __device__ __forceinline__ void flush_status(const RowOpParams& p, int lane, int
 }
 
 // Fast kernel: ring window, every row single-pass (host-verified: ring >= 2 hB + 33,
-// B rows <= 64 G entries).
-template <int G, int D, int MODE>
-__global__ void __launch_bounds__(128, 1) row_fast_kernel(const RowOpParams p) {
+// B rows <= 64 G entries). One warp per CTA: the ring base is then a compile-time constant
+// and folds into the shared-memory address of every accumulator access.
+template <int G, int B, int MODE>
+__global__ void __launch_bounds__(32, 8) row_fast_kernel(const RowOpParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31;
-    const int wid = threadIdx.x >> 5;
-    const WarpSmem w = warp_smem<MODE>(smem_raw, wid, p.S);
+    const int lane = threadIdx.x;
+    const WarpSmem w = warp_smem<MODE>(smem_raw, 0, p.S, true);
     clear_window<MODE>(w, lane, p.S);
-    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
-    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t gw = blockIdx.x;
+    const int64_t nwarps = gridDim.x;
     int32_t my_max_kept = 0, my_ovf = 0;
     for (int64_t i = p.row_begin + gw; i < p.row_end; i += nwarps) {
         RowIO r = row_io<MODE>(p, i);
@@ -759,7 +850,7 @@ __global__ void __launch_bounds__(128, 1) row_fast_kernel(const RowOpParams p) {
         }
         int32_t kept = 0;
         double ds = 0.0, dc = 0.0, nrm = 0.0;
-        row_ring<G, D, MODE>(p, w, lane, i, r.a_col, r.a_val, r.nA, r.o_col, r.o_val, r.nOld, r.crow_v, r.crow_c,
+        row_ring<G, B, MODE>(p, w, lane, i, r.a_col, r.a_val, r.nA, r.o_col, r.o_val, r.nOld, r.crow_v, r.crow_c,
                              kept, ds, dc, nrm);
         row_epilogue<MODE>(p, lane, i, kept, dA, ds, dc, nrm, my_max_kept, my_ovf);
     }
@@ -774,7 +865,7 @@ __global__ void __launch_bounds__(128, 1) row_general_kernel(const RowOpParams p
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int S = p.S;
-    const WarpSmem w = warp_smem<MODE>(smem_raw, wid, S);
+    const WarpSmem w = warp_smem<MODE>(smem_raw, wid, S, false);
     clear_window<MODE>(w, lane, S);
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -898,7 +989,7 @@ cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64
 // ----------------------------------------------------------------------------- dispatch
 
 // Fast-kernel variants by G = ceil(max nnz_B / 64) (64-entry groups per step; prefetch
-// depth D, the register ring holds D + 1 slots): G1: D 8, G2: D 6, G3: D 4, G4: D 3.
+// half-ring B, the register ring holds 2 B slots): G1: B 4, G2: B 3, G3: B 3, G4: B 2.
 // cfg.R carries G; cfg.R == 0 selects the general kernel.
 template <typename K>
 static cudaError_t prep_kernel(K kern, const LaunchCfg& cfg, int* bps) {
@@ -911,10 +1002,10 @@ template <int MODE>
 static cudaError_t prep_mode(const LaunchCfg& cfg, int* bps) {
     switch (cfg.R) {
         case 0: return prep_kernel(row_general_kernel<MODE>, cfg, bps);
-        case 1: return prep_kernel(row_fast_kernel<1, 8, MODE>, cfg, bps);
-        case 2: return prep_kernel(row_fast_kernel<2, 6, MODE>, cfg, bps);
-        case 3: return prep_kernel(row_fast_kernel<3, 4, MODE>, cfg, bps);
-        default: return prep_kernel(row_fast_kernel<4, 3, MODE>, cfg, bps);
+        case 1: return prep_kernel(row_fast_kernel<1, 4, MODE>, cfg, bps);
+        case 2: return prep_kernel(row_fast_kernel<2, 3, MODE>, cfg, bps);
+        case 3: return prep_kernel(row_fast_kernel<3, 3, MODE>, cfg, bps);
+        default: return prep_kernel(row_fast_kernel<4, 2, MODE>, cfg, bps);
     }
 }
 
@@ -923,20 +1014,20 @@ static void launch_mode(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t
     dim3 block(cfg.warps_per_cta * 32), grid(cfg.grid);
     switch (cfg.R) {
         case 0: row_general_kernel<MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        case 1: row_fast_kernel<1, 8, MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        case 2: row_fast_kernel<2, 6, MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        case 3: row_fast_kernel<3, 4, MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        default: row_fast_kernel<4, 3, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 1: row_fast_kernel<1, 4, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 2: row_fast_kernel<2, 3, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 3: row_fast_kernel<3, 3, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        default: row_fast_kernel<4, 2, MODE><<<grid, block, cfg.smem, s>>>(p); break;
     }
 }
 
 static int mode_of(const RowOpParams& p) { return p.old_mode == 0 ? 0 : (p.normsq ? 2 : 1); }
 
-size_t row_op_warp_smem(int S, bool has_old) { return warp_smem_bytes(S, has_old); }
+size_t row_op_warp_smem(int S, bool has_old, bool fast) { return warp_smem_bytes(S, has_old, fast); }
 
 cudaError_t plan_row_op(const RowOpParams& p, int S, int groups, int warps_opt, int num_sms, LaunchCfg* cfg) {
     S = (S + 31) & ~31;
-    const size_t per_warp = warp_smem_bytes(S, p.old_mode != 0);
+    const size_t per_warp = warp_smem_bytes(S, p.old_mode != 0, p.fast != 0);
     const size_t cap = 227 * 1024;
     if (per_warp > cap) return cudaErrorInvalidConfiguration;
     cfg->S = S;
@@ -945,7 +1036,8 @@ cudaError_t plan_row_op(const RowOpParams& p, int S, int groups, int warps_opt, 
     // warps per CTA: maximise resident warps (rows in flight) per SM under the shared-memory
     // and register limits; ties go to the larger CTA
     int best_w = 0, best_wpc = 1, best_bps = 0;
-    const int lo_w = warps_opt > 0 ? warps_opt : 1, hi_w = warps_opt > 0 ? warps_opt : 4;
+    int lo_w = warps_opt > 0 ? warps_opt : 1, hi_w = warps_opt > 0 ? warps_opt : 4;
+    if (p.fast) lo_w = hi_w = 1;  // the fast kernel is one warp per CTA
     for (int wpc = hi_w; wpc >= lo_w; --wpc) {
         if ((size_t)wpc * per_warp > cap) continue;
         cfg->warps_per_cta = wpc;

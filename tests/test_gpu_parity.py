@@ -412,4 +412,4 @@ def test_kernel_launch_counter(ctx):
     before = ctx.kernel_launches()
     X = synth.cfg1()
     gpu_x2(ctx, X, 256, 1e-5)
-    assert ctx.kernel_launches() - before == 4  # bandwidth probe + row kernel + block partials + final sums
+    assert ctx.kernel_launches() - before == 5  # bandwidth probe + balance pass + row kernel + block partials + final sums

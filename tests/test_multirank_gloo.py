@@ -1,0 +1,121 @@
+"""World-size-2 `gloo` tests of the multi-GPU row partition, on CPU.
+
+The GPU path exchanges X's row blocks and the canonical trace-block partials with
+NCCL inside libellpack; the pool has one GPU, so here the same protocol runs over
+gloo with the CPU oracle as the per-rank compute: each rank computes only its
+256-aligned row block, the blocks and partials are all-gathered, and the
+assembled result must be bitwise the single-process result (c12). The
+bootstrap helpers bench.py uses (unique-id broadcast, max over ranks) run here
+unchanged.
+"""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as tmp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _x2_rows(X, r0, r1, width, tau):
+    """Oracle X^2 of rows [r0, r1) only (the rank's share): rows outside the block are empty in A."""
+    import oracle
+    from synth import Ell
+    A = Ell.empty(X.n, X.w)
+    A.val[r0:r1], A.col[r0:r1], A.nnz[r0:r1] = X.val[r0:r1], X.col[r0:r1], X.nnz[r0:r1]
+    Y = Ell.empty(X.n, width)
+    r = oracle.multiply(A, X, Y, 1.0, 0.0, tau, want_diag=True)
+    return r, Y
+
+
+def _worker(rank, ws, port, n, m, tau):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(ws),
+                      LOCAL_RANK=str(rank))
+    sys.path.insert(0, ROOT)
+    import oracle
+    import synth
+    from paper_2102_08505_b200 import multirank as mr
+
+    oracle.set_threads(1)
+    dist = mr.init_process_group("gloo")
+    assert mr.dist_env() == (ws, rank, rank)
+
+    # (1) NCCL unique-id bootstrap: rank 0's 128 bytes reach every rank unchanged
+    uid = mr.broadcast_bytes(os.urandom(128) if rank == 0 else None)
+    seen = [None] * ws
+    dist.all_gather_object(seen, uid)
+    assert len(uid) == 128 and all(s == uid for s in seen)
+
+    # (2) the rank's 256-aligned block
+    r0, r1 = mr.rank_rows(n, ws, rank)
+    assert r0 % 256 == 0 and (r1 - r0) == n // ws
+
+    X = synth.cfg5(n, m)
+    ref_lit = oracle.x2(X, synth.Ell.empty(n, m), tau)  # literal width -> OVERFLOW report (R2)
+    assert ref_lit.status == oracle.OVERFLOW
+    w = ((ref_lit.required_width + 31) // 32) * 32
+    ref_Y = synth.Ell.empty(n, w)
+    ref = oracle.x2(X, ref_Y, tau)
+    assert ref.status == oracle.OK
+
+    # (3) overflow decision: per-rank counts all-reduced (sum rows, max width) = the P = 1 report
+    r_lit, _ = _x2_rows(X, r0, r1, m, tau)
+    assert r_lit.status == oracle.OVERFLOW
+    assert int(mr.sum_over_ranks(r_lit.overflow_rows)) == ref_lit.overflow_rows
+    assert int(mr.max_over_ranks(r_lit.required_width)) == ref_lit.required_width
+
+    # (4) the rank's rows at the agreed width, then the all-gather of row blocks
+    r, Y = _x2_rows(X, r0, r1, w, tau)
+    assert r.status == oracle.OK
+    blocks = {}
+    for name in ("val", "col", "nnz"):
+        mine = torch.from_numpy(np.ascontiguousarray(getattr(Y, name)[r0:r1]))
+        parts = [torch.empty_like(mine) for _ in range(ws)]
+        dist.all_gather(parts, mine)
+        blocks[name] = torch.cat(parts).numpy()
+    assert np.array_equal(blocks["nnz"], ref_Y.nnz)
+    for i in range(n):
+        k = int(ref_Y.nnz[i])
+        assert np.array_equal(blocks["col"][i, :k], ref_Y.col[i, :k])
+        assert np.array_equal(blocks["val"][i, :k].view(np.uint64), ref_Y.val[i, :k].view(np.uint64))
+
+    # (5) canonical traces: own block partials all-gathered (never all-reduced), summed in block order
+    diag_x = np.zeros(n)
+    for i in range(r0, r1):
+        hit = X.col[i, :X.nnz[i]] == i
+        diag_x[i] = X.val[i, :X.nnz[i]][hit][0] if hit.any() else 0.0
+    for d, expect in ((diag_x, ref.trace_x), (r.diag_s, ref.trace_x2)):
+        own = torch.from_numpy(oracle.block_partials(d)[r0 // 256:r1 // 256].copy())
+        parts = [torch.empty_like(own) for _ in range(ws)]
+        dist.all_gather(parts, own)
+        total = 0.0
+        for t in torch.cat(parts).tolist():
+            total = total + t
+        assert np.float64(total).view(np.uint64) == np.float64(expect).view(np.uint64)
+
+    # (6) bench.py timing: the slowest rank decides
+    assert mr.max_over_ranks(1.5 + rank) == 1.5 + (ws - 1)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,m", [(2048, 64), (4096, 32)])
+def test_row_partition_protocol_gloo_ws2(n, m):
+    tmp.spawn(_worker, args=(2, _free_port(), n, m, 1e-5), nprocs=2, join=True)
+
+
+def test_partition_rejects_unaligned_blocks():
+    sys.path.insert(0, ROOT)
+    from paper_2102_08505_b200 import multirank as mr
+    assert mr.rank_rows(4096, 2, 1) == (2048, 4096)
+    with pytest.raises(ValueError):
+        mr.rank_rows(512 + 256, 2, 0)
