@@ -97,8 +97,12 @@ int ellpack_ctx_set_stream(ellpack_ctx ctx, void* stream);
  *  ELLPACK_OPT_PROFILE     1 = bracket every launch of the fused row kernel with
  *                          CUDA events on the context stream and accumulate its
  *                          device time (ellpack_ctx_kernel_time); setting it
- *                          resets the accumulators. 0 = off (default). */
-enum { ELLPACK_OPT_WINDOW = 1, ELLPACK_OPT_WARPS = 2, ELLPACK_OPT_SP2_WIDTH0 = 3, ELLPACK_OPT_PROFILE = 4 };
+ *                          resets the accumulators. 0 = off (default).
+ *  ELLPACK_OPT_ABLATE      timing experiments only, results are WRONG when set:
+ *                          1 = the fast kernel skips its output-row stores,
+ *                          2 = it skips the accumulator updates. 0 = off (default). */
+enum { ELLPACK_OPT_WINDOW = 1, ELLPACK_OPT_WARPS = 2, ELLPACK_OPT_SP2_WIDTH0 = 3, ELLPACK_OPT_PROFILE = 4,
+       ELLPACK_OPT_ABLATE = 5 };
 int ellpack_ctx_set_option(ellpack_ctx ctx, int key, int64_t value);
 
 /* Accumulated device time (ms, CUDA events on the ctx stream) and launch count of

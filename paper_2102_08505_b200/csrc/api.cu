@@ -82,7 +82,7 @@ struct ellpack_ctx_s {
     int device = 0;
     cudaStream_t stream = nullptr;
     int num_sms = 148;
-    int window_opt = 0, warps_opt = 0, sp2_width0 = 0;
+    int window_opt = 0, warps_opt = 0, sp2_width0 = 0, ablate = 0;
     int64_t launches = 0;
     // small device/pinned blocks
     int32_t* d_status = nullptr;              // [0] ovf rows, [1] max kept
@@ -237,6 +237,7 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
     const int maxnb = p.alpha != 0.0 ? c->h->bw[3] : 0;
     const int groups = maxnb <= 64 ? 1 : (maxnb + 63) / 64;
     p.hB = (int32_t)hB;
+    p.ablate = c->ablate;
     // ring fast path: S >= 2 hB + 33 slots (progressive emission), B rows <= 256 entries
     int64_t ring = (2 * hB + 33 + 31) & ~int64_t(31);
     if (ring > nr) ring = nr < 32 ? 32 : nr;
@@ -266,15 +267,6 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
             c->ring_S = (int)grown;
         }
         S = c->ring_S;
-        // bank-balanced copy of B (all N rows: B is the full operand on every rank)
-        const int wt = 64 * (groups < 1 ? 1 : groups);
-        RK(grow(c, c->bt, (size_t)12 * n * wt));
-        RK(grow(c, c->bt_nbin, sizeof(int32_t) * (size_t)n));
-        CK(launch_balance(p.B, n, wt, (unsigned char*)c->bt.p, (int32_t*)c->bt_nbin.p, c->num_sms, c->stream));
-        c->launches++;
-        p.bt = (const unsigned char*)c->bt.p;
-        p.bt_nbin = (const int32_t*)c->bt_nbin.p;
-        p.bt_w = wt;
     } else {
         S = kGeneralWindow;
         p.fast = 0;
@@ -285,6 +277,19 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
     LaunchCfg cfg;
     CK(plan_row_op(p, (int)S, groups, c->warps_opt, c->num_sms, &cfg));
     p.S = cfg.S;
+    if (p.fast) {
+        // bank-balanced copy of B with ring slots precomputed for this S (all N rows: B is the
+        // full operand on every rank)
+        const int wt = 64 * (groups < 1 ? 1 : groups);
+        RK(grow(c, c->bt, (size_t)12 * n * wt));
+        RK(grow(c, c->bt_nbin, sizeof(int32_t) * (size_t)n));
+        CK(launch_balance(p.B, n, wt, p.S, (unsigned char*)c->bt.p, (int32_t*)c->bt_nbin.p, c->num_sms,
+                          c->stream));
+        c->launches++;
+        p.bt = (const unsigned char*)c->bt.p;
+        p.bt_nbin = (const int32_t*)c->bt_nbin.p;
+        p.bt_w = wt;
+    }
     c->last_cfg = cfg;
     const int64_t total_warps = (int64_t)cfg.grid * cfg.warps_per_cta;
     const bool may_multi = n > cfg.S;
@@ -492,6 +497,7 @@ int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
         case ELLPACK_OPT_WINDOW: c->window_opt = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_WARPS: c->warps_opt = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_SP2_WIDTH0: c->sp2_width0 = (int)v; return ELLPACK_OK;
+        case ELLPACK_OPT_ABLATE: c->ablate = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_PROFILE:
             c->profile = v != 0;
             c->prof_ms = 0.0;

@@ -46,9 +46,10 @@ struct RowOpParams {
     int64_t ncols;      // matrix dimension N (columns >= N never exist)
     // fast path: bank-balanced copy of B (balance_kernel): [N][bt_w] values / columns
     // (column -1 = padding) and NB(k) = ceil(nnz_B(k) / 16) used half-instruction bins
-    const unsigned char* bt;  // row k: int32 off[bt_w] (8 (j - k), INT_MIN = padding), f64 val[bt_w]
+    const unsigned char* bt;  // row k: int32 slot8[bt_w] (8 (j mod S), padding: 8 (S + r)), f64 val[bt_w]
     const int32_t* bt_nbin;
     int32_t bt_w;             // 64 G
+    int32_t ablate;           // timing experiments only (ELLPACK_OPT_ABLATE): 1 no row stores, 2 no accumulate
     // optional per-row outputs, indexed by global row (nullable)
     double* diag_a;   // stored a_ii
     double* diag_s;   // pre-combine s_ii  (tr(X^2) pre-drop, R5)
@@ -78,7 +79,8 @@ cudaError_t plan_row_op(const RowOpParams& p, int S, int groups, int warps_opt, 
 cudaError_t launch_row_op(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s);
 size_t row_op_warp_smem(int S, bool has_old, bool fast);
 // bank-balanced copy of B for the fast path (wt = 64 G >= 16 ceil(nnz/16) for every row)
-cudaError_t launch_balance(KMat b, int64_t n, int wt, unsigned char* bt, int32_t* bt_nbin, int num_sms,
+// (S: the ring size of the launch that consumes it; slots are precomputed as 8 (j mod S))
+cudaError_t launch_balance(KMat b, int64_t n, int wt, int S, unsigned char* bt, int32_t* bt_nbin, int num_sms,
                            cudaStream_t s);
 // out[0..2] = max half-bandwidth of a (rows r0..r1), b (all rows), c (rows r0..r1); out[3] = max nnz of b
 cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64_t r1, int64_t n,

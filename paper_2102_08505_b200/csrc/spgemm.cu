@@ -93,7 +93,7 @@ __device__ __forceinline__ void sts16u(uint32_t a, uint32_t v) {
 __device__ __forceinline__ void st_entry(bool pred, double* pv, int32_t* pc, double x, int32_t c) {
     asm volatile(
         "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t"
-        "@q st.global.f64 [%1], %2;\n\t@q st.global.b32 [%3], %4;\n\t}" ::"r"((int)pred),
+        "@q st.global.cs.f64 [%1], %2;\n\t@q st.global.cs.b32 [%3], %4;\n\t}" ::"r"((int)pred),
         "l"(pv), "d"(x), "l"(pc), "r"(c)
         : "memory");
 }
@@ -129,10 +129,11 @@ __device__ __forceinline__ int stg_anb(const WarpSmem& w, int t) { return lds32i
 __device__ __forceinline__ int stg_ast(const WarpSmem& w, int t) { return lds32i(stg_ast_a(w, t)); }
 __device__ __forceinline__ int stg_ak(const WarpSmem& w, int t) { return lds32i(stg_ak_a(w, t)); }
 
-// acc has S + 2 slots: acc[S] is the trash slot of padded lanes (16-byte aligned pair).
-// The fast path's stage holds 16 B per entry (a_ik, k, NB(k)); the general path's 28 B.
+// acc has S + kTrash slots: acc[S .. S + 15] are trash slots (one per bank pair) that padding
+// lanes of the fast path update; acc[S] is also the general path's trash slot.
+constexpr int kTrash = 16;
 __host__ __device__ inline size_t warp_smem_bytes(int S, bool has_old, bool fast) {
-    return (size_t)(S + 2) * 8 + (size_t)kStage * (fast ? 16 : 28) + (has_old ? (size_t)S : 0);
+    return (size_t)(S + kTrash) * 8 + (fast ? (size_t)64 * 16 : (size_t)kStage * 28) + (has_old ? (size_t)S : 0);
 }
 
 // Stage A-row entries [p0, p0 + cnt): B-row offset k*B.w, a_ik, nnz_B(k), cursor.
@@ -153,29 +154,31 @@ __device__ __forceinline__ void stage_piece(const RowOpParams& p, const WarpSmem
 
 // ------------------------------------------------------------- bank-balanced B (fast path)
 //
-// The accumulator is a dense ring of doubles: entry (k, j) of a B row updates ring slot
-// (j - base) mod S, i.e. shared-memory bank pair j mod 16 (S and base are multiples of 32).
-// Measured on B200 (tools/bank_bench.cu): a warp-wide 64-bit shared access is served as two
-// 16-lane halves; each half costs as many wavefronts as its most-repeated bank pair (loads
-// retire two wavefronts per clock, stores one). Column indices of a sorted B row are
-// random modulo 16, so taking consecutive entries costs 3-6 wavefronts per instruction
-// (r01 profile). The entries of ONE B row have distinct columns, so the order in which the
-// lanes apply them within a step is free: the fma chain of every output entry stays
-// ascending in k (R12). The balance pass stores each B row permuted so that every 16-lane
-// half sees (nearly) distinct bank pairs:
+// The accumulator of an output row is a ring of S doubles (S a multiple of 32): column j lives
+// in slot j mod S for every row (the ring base is always a multiple of S), so the slot of a B
+// entry does not depend on the output row and is precomputed here: the accumulate step is
+// then LDS / DFMA / STS per entry, with no address arithmetic.
+//
+// Bank conflicts. Slot j mod S is bank pair j mod 16. Measured on B200 (tools/bank_bench.cu):
+// a warp-wide 64-bit shared access is served as two 16-lane halves; each half costs as many
+// wavefronts as its most-repeated bank pair (loads retire two wavefronts per clock, stores
+// one). Column indices of a sorted B row are random modulo 16, so consecutive entries cost
+// 3-6 wavefronts per instruction (r01 profile). The entries of ONE B row have distinct
+// columns, so the order in which the lanes apply them within a step is free: the fma chain of
+// every output entry stays ascending in k (R12). Each B row is stored permuted:
 //   1. rank the row's entries by residue r = j mod 16 (stable counting sort): e in [0, n);
 //   2. deal the ranks round-robin over NB = ceil(n / 16) half-instruction bins:
 //      bin b = e mod NB, position m = e / NB (a residue with c_r <= NB entries lands in
 //      c_r distinct bins);
 //   3. bin b is half h = (b >> 1) & 1 of instruction (group g = b >> 2, parity b & 1):
 //      slot 64 g + 2 (16 h + m) + (b & 1), so a lane's two slots of a group are adjacent
-//      (one 8-byte offset load, one 16-byte value load).
-// Row record (12 * 64 G bytes): int32 off[64 G] then f64 val[64 G]; off = 8 (j - k) (the
-// kernel adds the warp-uniform 8 (k - base)); unused slots of used groups hold INT_MIN.
-// bt_nbin[k] = NB: group g is loaded iff NB > 4 g.
-constexpr int32_t kPad = INT_MIN;
-
-__global__ void balance_kernel(KMat b, int64_t n, int wt, unsigned char* __restrict__ bt,
+//      (one 8-byte index load, one 16-byte value load);
+//   4. unused positions of a used group are padding: value 0 and a trash slot S + r with a
+//      residue r not used in the position's bin (distinct per padding lane while possible),
+//      so padding lanes run the same LDS / DFMA / STS without adding bank conflicts.
+// Record of row k (12 * 64 G bytes): int32 slot8[64 G] (= 8 * slot) then f64 val[64 G].
+// bt_nbin[k] = NB: group g holds entries iff NB > 4 g.
+__global__ void balance_kernel(KMat b, int64_t n, int wt, int S, unsigned char* __restrict__ bt,
                                int32_t* __restrict__ bt_nbin) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -189,8 +192,6 @@ __global__ void balance_kernel(KMat b, int64_t n, int wt, unsigned char* __restr
         int32_t* __restrict__ oo = reinterpret_cast<int32_t*>(bt + (size_t)k * 12 * wt);
         double* __restrict__ ov = reinterpret_cast<double*>(bt + (size_t)k * 12 * wt + 4 * (size_t)wt);
         if (lane == 0) bt_nbin[k] = NB;
-        const int used = 64 * ((NB + 3) >> 2);
-        for (int s = lane; s < used; s += 32) oo[s] = kPad;
         // pass 1: per-residue counts (warp-uniform)
         int cnt[16];
 #pragma unroll
@@ -205,8 +206,9 @@ __global__ void balance_kernel(KMat b, int64_t n, int wt, unsigned char* __restr
         int acc = 0;
 #pragma unroll
         for (int r = 0; r < 16; ++r) { run[r] = acc; acc += cnt[r]; }
-        __syncwarp();  // padding fill ordered before the scatter
-        // pass 2: rank e within the residue-sorted order, dealt round-robin over the bins
+        // pass 2: rank e within the residue-sorted order, dealt round-robin over the bins;
+        // bin_mask (lane b < NB): residues used in bin b
+        unsigned bin_mask = 0;
         for (int c = 0; c < nb; c += 32) {
             const int q = c + lane;
             const bool v = q < nb;
@@ -219,21 +221,46 @@ __global__ void balance_kernel(KMat b, int64_t n, int wt, unsigned char* __restr
                 if (res == r) e = run[r] + __popc(m & lt);
                 run[r] += __popc(m);
             }
+            const int bin = v ? e % NB : 32, pos = v ? e / NB : 0;
             if (v) {
-                const int bin = e % NB, pos = e / NB;
                 const int sl = 64 * (bin >> 2) + 2 * (16 * ((bin >> 1) & 1) + pos) + (bin & 1);
-                oo[sl] = 8 * (j - (int)k);
+                oo[sl] = 8 * (j % S);
                 ov[sl] = __ldg(bv + q);
+            }
+            for (int bb = 0; bb < NB; ++bb) {
+                const unsigned rm = __reduce_or_sync(FULL, bin == bb ? (1u << res) : 0u);
+                if (lane == bb) bin_mask |= rm;
+            }
+        }
+        // padding: bin b holds fill_b = ceil((nb - b) / NB) entries at positions 0..fill_b-1;
+        // positions fill_b..15 of bins < 4 ceil(NB / 4) get distinct unused residues' trash slots
+        const int nbins = 4 * ((NB + 3) >> 2);
+        for (int bb = 0; bb < nbins; ++bb) {
+            const int fill = bb < NB ? (nb - bb + NB - 1) / NB : 0;
+            const unsigned used = __shfl_sync(FULL, bin_mask, bb & 31) & (bb < NB ? 0xffffu : 0u);
+            const int m = lane;  // position handled by this lane (lanes 0..15)
+            if (m < 16 && m >= fill) {
+                // the (m - fill)-th residue not used in the bin (wrapping if the bin uses > 16 - ...)
+                const unsigned freem = ~used & 0xffffu;
+                const int nfree = __popc(freem);
+                int want = nfree ? (m - fill) % nfree : 0;
+                int r = 0;
+                unsigned f = nfree ? freem : 0xffffu;
+                for (; want > 0; --want) f &= f - 1;
+                r = __ffs(f) - 1;
+                const int sl = 64 * (bb >> 2) + 2 * (16 * ((bb >> 1) & 1) + m) + (bb & 1);
+                oo[sl] = 8 * (S + r);
+                ov[sl] = 0.0;
             }
         }
     }
 }
 
-cudaError_t launch_balance(KMat b, int64_t n, int wt, unsigned char* bt, int32_t* bt_nbin, int num_sms,
+cudaError_t launch_balance(KMat b, int64_t n, int wt, int S, unsigned char* bt, int32_t* bt_nbin, int num_sms,
                            cudaStream_t s) {
     const int64_t blocks_needed = (n + 7) / 8;
     const int64_t cap = (int64_t)num_sms * 8;
-    balance_kernel<<<(unsigned)(blocks_needed < cap ? blocks_needed : cap), 256, 0, s>>>(b, n, wt, bt, bt_nbin);
+    balance_kernel<<<(unsigned)(blocks_needed < cap ? blocks_needed : cap), 256, 0, s>>>(b, n, wt, S, bt, bt_nbin);
     return cudaGetLastError();
 }
 
@@ -255,6 +282,27 @@ __device__ __forceinline__ void stage_fast_get(const WarpSmem& w, int t, double&
     a = __longlong_as_double((long long)x);
     k = (int)(uint32_t)y;
     nb = (int)(y >> 32);
+}
+
+// Gathers of the balanced B copy: read-only, no L1 allocation (each is used once per SM), L2
+// evict_last (every record is re-read by the ~2 hB rows around it while the output stream,
+// written with .cs, passes through L2).
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ int2 ldg_keep_i2(const void* p, uint64_t pol) {
+    int2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double2 ldg_keep_d2(const void* p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
 }
 
 // predicated shared accesses (padding lanes issue no request and cost no wavefront)
@@ -530,8 +578,9 @@ __device__ __forceinline__ void ring_emit_pairs(const RowOpParams& p, const Warp
         const int pos0 = before + __popc(m[c][0] & lt) + __popc(m[c][1] & lt);
         const int pos1 = pos0 + (int)k0;
         const int col0 = F + 64 * c + 2 * lane;
-        st_entry(k0 && pos0 < p.C.w, crow_v + pos0, crow_c + pos0, x[c][0], col0);
-        st_entry(k1 && pos1 < p.C.w, crow_v + pos1, crow_c + pos1, x[c][1], col0 + 1);
+        const bool stw = !(p.ablate & 1);
+        st_entry(stw && k0 && pos0 < p.C.w, crow_v + (uint32_t)pos0, crow_c + (uint32_t)pos0, x[c][0], col0);
+        st_entry(stw && k1 && pos1 < p.C.w, crow_v + (uint32_t)pos1, crow_c + (uint32_t)pos1, x[c][1], col0 + 1);
         if (want_dc) {
             if ((int64_t)col0 == i) dc = k0 ? x[c][0] : 0.0;
             if ((int64_t)col0 + 1 == i) dc = k1 ? x[c][1] : 0.0;
@@ -586,7 +635,7 @@ __device__ __forceinline__ void ring_emit_block(const RowOpParams& p, const Warp
     for (int c = 0; c < NCH; ++c) {
         const bool keep = (m[c] >> lane) & 1u;
         const int pos = before + __popc(m[c] & lt);
-        st_entry(keep && pos < p.C.w, crow_v + pos, crow_c + pos, x[c], F + 32 * c + lane);
+        st_entry(keep && pos < p.C.w, crow_v + (uint32_t)pos, crow_c + (uint32_t)pos, x[c], F + 32 * c + lane);
         if ((int64_t)F + 32 * c + lane == i) dc = keep ? x[c] : 0.0;
         before += __popc(m[c]);
     }
@@ -600,6 +649,13 @@ __device__ __forceinline__ void ring_emit_range(const RowOpParams& p, const Warp
                                                 const double* o_val, int nOld, int& old_cur,
                                                 double* __restrict__ crow_v, int32_t* __restrict__ crow_c,
                                                 int& kept, double& ds, double& dc, double& nrm) {
+    if (p.ablate & 8) {  // timing experiment: no emission work at all
+        while (F < Fto) {
+            F += 32;
+            if (F - baseF >= p.S) baseF += p.S;
+        }
+        return;
+    }
     while (p.S >= 256 && F + 128 <= Fto) {  // a 128-column block wraps at most once
         ring_emit_pairs<MODE, 2>(p, w, lane, i, F, baseF, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept, ds,
                                  dc, nrm);
@@ -616,27 +672,36 @@ __device__ __forceinline__ void ring_emit_range(const RowOpParams& p, const Warp
 }
 
 // One output row on the ring fast path. B is the bank-balanced copy (p.bt, 64 G slots per
-// row); A's row is staged in pieces of kStage entries; a (D+1)-slot register ring holds the
-// gathered B rows of the next D steps. Before step k, if the step's columns [k - hB, k + hB]
-// would reach a ring slot still holding an unemitted column, every column below
-// floor32(k - hB) (final: later steps only touch columns >= k' - hB >= k - hB) is emitted in
-// 4-chunk blocks; with S >= 2 hB + 33 + slack that happens every few steps.
+// row, precomputed ring slots); A's row is staged in pieces of at most kPieceF entries,
+// padded with null steps (nb = 0: no loads, no accumulator access) to whole halves of HB
+// steps.
 //
-// Per entry the step costs one IADD (ring offset = uniform 8 (k - base) + stored 8 (j - k)),
-// one IADD + one unsigned min (wrap: min(o, o - 8 S) as unsigned picks o - 8 S exactly when
-// o >= 8 S), a padding test, and the LDS / DFMA / STS of the update.
-template <int G, int B, int MODE>
+// Gathers go straight to registers in bursts of one half (HB steps) into a two-half register
+// ring. ptxas gives every gather the same variable-latency scoreboard and a consumer waits
+// for the whole scoreboard (i.e. for the youngest gather), and it drains the scoreboard at
+// loop heads and control-flow joins. So a half runs: touch its own registers (waits for its
+// burst, issued one half earlier, while nothing younger is outstanding) -> emit if needed
+// (branchy; nothing young to drain) -> issue the next half's burst -> HB branch-free steps
+// whose operands are all ready. A step is, per entry, LDS -> DFMA -> STS on the precomputed
+// slot (padding lanes hit trash slots).
+//
+// Before a half, every column below floor32(k_first - hB) is final and is emitted when the
+// half's first step would otherwise wrap onto it; if the whole half then fits the ring
+// (k_last + hB < F + S) its steps need no checks, else (rare: k jumps > slack) the half runs
+// step by step with per-step emission checks.
+constexpr int kStageF = 64;  // fast-path stage entries (16 B each)
+
+template <int G, int HB, int MODE>
 __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
                                          const int32_t* a_col, const double* a_val, int nA,
                                          const int32_t* o_col, const double* o_val, int nOld,
                                          double* __restrict__ crow_v, int32_t* __restrict__ crow_c,
                                          int& kept, double& ds, double& dc, double& nrm) {
-    constexpr int NS = 2 * B;  // register ring slots: two halves of B steps
+    constexpr int kPieceF = kStageF - 2 * HB + 1;  // real steps per piece (room for padding + a null half)
+    constexpr int RS = 12 * 64 * G;                // balanced row record bytes (p.bt_w == 64 G)
     const int S = p.S;
-    const uint32_t S8 = 8u * (uint32_t)S;
     const int hB = p.hB;
     const int ncols = (int)p.ncols;
-    // column extent of the row: products in [k_first - hB, k_last + hB], plus Old entries
     int lo_col = INT_MAX, hi_col = -1;
     if (nA > 0) {
         lo_col = max(0, a_col[0] - hB);
@@ -650,90 +715,100 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
     int F = lo_col & ~31;
     const int Fend = (hi_col + 32) & ~31;
     int baseF = F - F % S;  // multiple of S with baseF <= F < baseF + S
-    int baseS = baseF;
     int old_cur = 0;
     const uint32_t acc = w.acc;
-    const size_t rs = (size_t)12 * p.bt_w;  // balanced row record bytes
-    const unsigned char* __restrict__ bto = p.bt + 8 * lane;                   // offsets, lane pair
-    const unsigned char* __restrict__ btv = p.bt + 4 * (size_t)p.bt_w + 16 * lane;  // values, lane pair
+    const unsigned char* __restrict__ btl = p.bt + 8 * lane;  // this lane's slot pair of a record
+    const uint64_t pol = l2_evict_last_policy();
 
-    int2 ro[NS][G];
-    double2 rv[NS][G];
-    double ra[NS];
-    int rnb[NS], rk[NS];
-    for (int p0 = 0; p0 < nA; p0 += kStage) {
-        const int cnt = min(kStage, nA - p0);
-        stage_fast(p, w, lane, a_col, a_val, p0, cnt);
-        auto load = [&](int slot, int t) {
+    int2 ro[2][HB][G];
+    double2 rv[2][HB][G];
+    // burst: the gathers of half h into register half X (stage metadata k, nb)
+    auto burst = [&](int X, int h) {
+#pragma unroll
+        for (int e = 0; e < HB; ++e) {
+            double a_unused;
             int k, nb;
-            stage_fast_get(w, t, ra[slot], k, nb);
-            rnb[slot] = nb;
-            rk[slot] = k;
-            const size_t rb = (size_t)k * rs;
+            stage_fast_get(w, h * HB + e, a_unused, k, nb);
+            const unsigned char* __restrict__ rp = btl + (size_t)(uint32_t)k * RS;
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                if (nb > 4 * g) {
-                    ro[slot][g] = __ldg(reinterpret_cast<const int2*>(bto + rb + 256 * g));
-                    rv[slot][g] = __ldg(reinterpret_cast<const double2*>(btv + rb + 512 * g));
+                if (nb > 4 * g && !(p.ablate & 4)) {
+                    ro[X][e][g] = ldg_keep_i2(rp + 256 * g, pol);
+                    rv[X][e][g] = ldg_keep_d2(rp + 256 * G + 8 * lane + 512 * g, pol);
                 }
             }
-        };
-        // Gathers are issued a half-ring (B steps) at a time, right after the first step of the
-        // other half has consumed its data: a variable-latency scoreboard slot drains as a whole,
-        // so waiting for step t's registers also waits for every gather issued before it -- one
-        // batch per B steps keeps the youngest outstanding gather B steps (not one step) away.
+        }
+    };
+    // accumulate one step from register half X, slot e
+    auto step = [&](int X, int e, double a, int nb) {
+        double old[G][2];
+        bool gl[G];
 #pragma unroll
-        for (int d = 0; d < B; ++d) load(d, min(d, cnt - 1));
-        for (int t0 = 0; t0 < cnt; t0 += NS) {
+        for (int g = 0; g < G; ++g) {
+            gl[g] = nb > 4 * g && !(p.ablate & 2);  // warp-uniform: group holds entries
+            old[g][0] = lds64_if(gl[g], acc + (uint32_t)ro[X][e][g].x);
+            old[g][1] = lds64_if(gl[g], acc + (uint32_t)ro[X][e][g].y);
+        }
 #pragma unroll
-            for (int d = 0; d < NS; ++d) {
-                const int t = t0 + d;
-                if (t < cnt) {
-                    const int kt = rk[d];
-                    // 1. emit the final columns when step k would wrap onto them
-                    if (kt + hB >= F + S)
-                        ring_emit_range<MODE>(p, w, lane, i, F, baseF, (kt - hB) & ~31, o_col, o_val, nOld,
-                                              old_cur, crow_v, crow_c, kept, ds, dc, nrm);
-                    // 2. ring base for this step: columns [lo, k + hB], lo >= baseS
-                    const int lo = max(0, kt - hB);
-                    while (lo - baseS >= S) baseS += S;
-                    const uint32_t kb8 = 8u * (uint32_t)(kt - baseS);
-                    const int nb = rnb[d];
-                    const double a = ra[d];
-                    uint32_t ad[G][2];
-                    bool pv[G][2];
+        for (int g = 0; g < G; ++g) {
+            sts64_if(gl[g], acc + (uint32_t)ro[X][e][g].x, __fma_rn(a, rv[X][e][g].x, old[g][0]));
+            sts64_if(gl[g], acc + (uint32_t)ro[X][e][g].y, __fma_rn(a, rv[X][e][g].y, old[g][1]));
+        }
+        __syncwarp();
+    };
+    // one half of HB steps from register half X
+    auto half = [&](int X, int h) {
+        double a_[HB];
+        int k_[HB], nb_[HB];
 #pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        const bool gl = nb > 4 * g;  // warp-uniform: group loaded
+        for (int e = 0; e < HB; ++e) stage_fast_get(w, h * HB + e, a_[e], k_[e], nb_[e]);
+        // touch this half's burst: the store waits for it (and for nothing younger)
+        if (nb_[0] > 0) sts32i(acc + 8u * (uint32_t)S, ro[X][0][0].x);
+        const int kf = k_[0], kl = k_[HB - 1];
+        if (kf + hB >= F + S)
+            ring_emit_range<MODE>(p, w, lane, i, F, baseF, (kf - hB) & ~31, o_col, o_val, nOld, old_cur,
+                                  crow_v, crow_c, kept, ds, dc, nrm);
+        __syncwarp();
+        burst(X ^ 1, h + 1);  // the next half (a null half past the piece end: no loads)
+        if (kl + hB < F + S) {
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int o = h ? ro[d][g].y : ro[d][g].x;
-                            const uint32_t r = kb8 + (uint32_t)o;
-                            ad[g][h] = acc + min(r, r - S8);
-                            pv[g][h] = gl && o != kPad;
-                        }
-                    }
-                    // 3. shared loads, fma, shared stores of the step
-                    double old[G][2];
+            for (int e = 0; e < HB; ++e) step(X, e, a_[e], nb_[e]);
+        } else {
 #pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        old[g][0] = lds64_if(pv[g][0], ad[g][0]);
-                        old[g][1] = lds64_if(pv[g][1], ad[g][1]);
-                    }
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        sts64_if(pv[g][0], ad[g][0], __fma_rn(a, rv[d][g].x, old[g][0]));
-                        sts64_if(pv[g][1], ad[g][1], __fma_rn(a, rv[d][g].y, old[g][1]));
-                    }
-                    // 4. first step of a half: gathers of the next B steps into the other half
-                    //    (after this step's stores: the asm memory clobbers keep them here)
-                    if (d == 0 || d == B) {
-#pragma unroll
-                        for (int e = 0; e < B; ++e) load((d == 0 ? B : 0) + e, min(t + B + e, cnt - 1));
-                    }
-                    __syncwarp();
-                }
+            for (int e = 0; e < HB; ++e) {
+                const int kt = k_[e];
+                if (kt + hB >= F + S)
+                    ring_emit_range<MODE>(p, w, lane, i, F, baseF, (kt - hB) & ~31, o_col, o_val, nOld, old_cur,
+                                          crow_v, crow_c, kept, ds, dc, nrm);
+                step(X, e, a_[e], nb_[e]);
             }
+        }
+    };
+    for (int p0 = 0; p0 < nA; p0 += kPieceF) {
+        const int cnt = min(kPieceF, nA - p0);
+        const int nh = (cnt + HB - 1) / HB;  // halves, the last padded with null steps
+        // stage: real steps, then null steps (k = last real k, nb = 0, a = 0) through half nh
+        for (int q = lane; q < (nh + 1) * HB; q += 32) {
+            int k, nb;
+            double a;
+            if (q < cnt) {
+                k = a_col[p0 + q];
+                nb = __ldg(p.bt_nbin + k);
+                a = a_val[p0 + q];
+            } else {
+                k = a_col[p0 + cnt - 1];
+                nb = 0;
+                a = 0.0;
+            }
+            const unsigned long long knb = (unsigned long long)(uint32_t)k | ((unsigned long long)(uint32_t)nb << 32);
+            asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(w.stg + 16u * q),
+                         "l"(__double_as_longlong(a)), "l"(knb) : "memory");
+        }
+        __syncwarp();
+        burst(0, 0);
+        for (int h = 0; h < nh; h += 2) {
+            half(0, h);
+            if (h + 1 < nh) half(1, h + 1);
         }
     }
     // final chunks
@@ -750,8 +825,8 @@ __device__ __forceinline__ WarpSmem warp_smem(unsigned char* smem_raw, int wid, 
     unsigned char* base = smem_raw + (size_t)wid * warp_smem_bytes(S, MODE != 0, fast);
     WarpSmem w;
     w.acc = (uint32_t)__cvta_generic_to_shared(base);
-    w.stg = w.acc + (uint32_t)((S + 2) * 8);
-    w.flg = w.acc + (uint32_t)((S + 2) * 8 + kStage * (fast ? 16 : 28));
+    w.stg = w.acc + (uint32_t)((S + kTrash) * 8);
+    w.flg = w.acc + (uint32_t)((S + kTrash) * 8 + (fast ? 64 * 16 : kStage * 28));
     return w;
 }
 
@@ -1004,7 +1079,7 @@ static cudaError_t prep_mode(const LaunchCfg& cfg, int* bps) {
         case 0: return prep_kernel(row_general_kernel<MODE>, cfg, bps);
         case 1: return prep_kernel(row_fast_kernel<1, 4, MODE>, cfg, bps);
         case 2: return prep_kernel(row_fast_kernel<2, 3, MODE>, cfg, bps);
-        case 3: return prep_kernel(row_fast_kernel<3, 3, MODE>, cfg, bps);
+        case 3: return prep_kernel(row_fast_kernel<3, 2, MODE>, cfg, bps);
         default: return prep_kernel(row_fast_kernel<4, 2, MODE>, cfg, bps);
     }
 }
@@ -1016,7 +1091,7 @@ static void launch_mode(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t
         case 0: row_general_kernel<MODE><<<grid, block, cfg.smem, s>>>(p); break;
         case 1: row_fast_kernel<1, 4, MODE><<<grid, block, cfg.smem, s>>>(p); break;
         case 2: row_fast_kernel<2, 3, MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        case 3: row_fast_kernel<3, 3, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 3: row_fast_kernel<3, 2, MODE><<<grid, block, cfg.smem, s>>>(p); break;
         default: row_fast_kernel<4, 2, MODE><<<grid, block, cfg.smem, s>>>(p); break;
     }
 }

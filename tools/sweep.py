@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--windows", nargs="+", type=int, default=[0])
     ap.add_argument("--warps", nargs="+", type=int, default=[0])
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--ablate", nargs="+", type=int, default=[0],
+                    help="timing-only ablations (results wrong): 1 no row stores, 2 no accumulate")
     args = ap.parse_args()
     eb.build()
     for sz in args.sizes:
@@ -40,9 +42,11 @@ def main():
         del y
         y = eb.Mat.empty(n, w)
         ctx.close()
-        for win in args.windows:
-            for wp in args.warps:
+        for win, wp, ab in [(a, b, c) for a in args.windows for b in args.warps for c in args.ablate]:
+            if True:
                 ctx = eb.Context(0)
+                if ab:
+                    ctx.set_option(eb.OPT_ABLATE, ab)
                 if win:
                     ctx.set_option(eb.OPT_WINDOW, win)
                 if wp:
@@ -55,7 +59,7 @@ def main():
                 ms /= max(k, 1)
                 nnz_c = int(y.nnz.sum().item())
                 Bc = 12 * (int(X.nnz.sum()) + nnz_c) + 8 * n
-                print(json.dumps({"n": n, "m": m, "window": win, "warps": wp, "status": s, "ms": ms,
+                print(json.dumps({"n": n, "m": m, "window": win, "warps": wp, "ablate": ab, "status": s, "ms": ms,
                                   "gflops": 2 * P / ms / 1e6, "alg_GBps": Bc / ms / 1e6,
                                   "products": P, "out_w": w}), flush=True)
                 ctx.close()
