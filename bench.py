@@ -314,6 +314,90 @@ def run_ours(args):
     return 0
 
 
+# ------------------------------------------------------------------------- SP2 window
+
+def run_sp2(args):
+    """SP2 iterations/sec (BASELINE metric, second half) on cfg3 or cfg4 over a fixed window of K
+    iterations (GROW policy; the configs are gapless, SURVEY §8d "SP2 protocol"): one step = one
+    sp2_run call of K iterations, timed with CUDA events on the context stream; the CPU oracle
+    runs the same window beside it (rank 0, N = 1)."""
+    import torch
+
+    import paper_2102_08505_b200 as eb
+    from paper_2102_08505_b200 import multirank as mr
+
+    ws, rank, local = mr.dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        mr.init_process_group("nccl", device=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    eb.build()
+    ctx = eb.Context(dev)
+    if args.sp2_cfg == 3:
+        H, cf = synth.cfg3(), synth.CFG3
+    else:
+        H, cf = synth.cfg4(), synth.CFG4
+    n = H.n
+    if ws > 1:
+        uid = mr.broadcast_bytes(eb.Context.nccl_unique_id() if rank == 0 else None)
+        r0, r1 = mr.rank_rows(n, ws, rank)
+        ctx.attach_nccl(ws, rank, uid, r0, r1)
+    K = args.sp2_iters
+    h = eb.Mat.from_host(H)
+    d = eb.Mat.empty(n, min(n + (n & 1), 8192))
+    stream = torch.cuda.current_stream()
+
+    def step():
+        return ctx.sp2_run(h, cf["nocc"], cf["tol"], d, threshold=cf["threshold"], max_iter=K)
+
+    for _ in range(max(1, args.warmup)):
+        r = step()
+    prods = sum(it.get("products", 0) for it in r.iters) if r.iters and "products" in r.iters[0] else None
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            r = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if ws > 1:
+        ms = mr.max_over_ranks(ms, device="cuda")
+    its = r.iterations
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        import oracle
+        t0 = time.perf_counter()
+        o = oracle.sp2(H, cf["nocc"], cf["tol"], oracle.SP2Opts(threshold=cf["threshold"], max_iter=K),
+                       d_width=min(n + (n & 1), 8192))
+        dt = time.perf_counter() - t0
+        cpu = {"value": o.iterations / dt, "unit": "iterations/s", "cores": oracle.num_threads(), "kind": "oracle",
+               "sample": f"the same {K}-iteration window (stop {o.stop}, width {o.final_width})"}
+    if rank == 0:
+        line = {
+            "metric": "SP2 iterations/sec", "value": its / (ms * 1e-3), "unit": "iterations/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic (synth.cfg{args.sp2_cfg}, SURVEY §8d)",
+            "config": {"workload": f"cfg{args.sp2_cfg} SP2 N={n} tau={cf['threshold']} window K={K} GROW",
+                       "iterations": its, "stop": r.stop, "final_width": r.final_width, "regrows": r.regrows,
+                       "products": prods, "gflops": (2.0 * prods / (ms * 1e-3) / 1e9) if prods else None,
+                       "phases_s": r.phases},
+            "cpu_baseline": cpu, "gpu_launches": ctx.kernel_launches() - launches0, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -327,7 +411,17 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=20.0, help="seconds of oracle work per sample")
+    ap.add_argument("--workload", default="x2", choices=["x2", "sp2"],
+                    help="x2: the headline cfg5 X^2 (default); sp2: SP2 iterations/sec on cfg3/cfg4")
+    ap.add_argument("--sp2-cfg", type=int, default=3, choices=[3, 4])
+    ap.add_argument("--sp2-iters", type=int, default=10)
     args = ap.parse_args()
+    if args.workload == "sp2":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "--workload sp2 reports the oracle inline "
+                              "(cpu_baseline); the reference arm is the x2 workload"}))
+            return 0
+        return run_sp2(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -316,7 +316,7 @@ class Context:
         n_rec = min(rep.iterations, max_iter)
         iters = [dict(trX=recs[k].trX, trS=recs[k].trS, e=recs[k].e, fnorm=recs[k].fnorm,
                       branch="SQUARE" if recs[k].branch == 0 else "EXPAND", width=recs[k].width,
-                      required=recs[k].required) for k in range(n_rec)]
+                      required=recs[k].required, products=recs[k].products) for k in range(n_rec)]
         phases = dict(read_hamiltonian=rep.t_read_hamiltonian, init_misc=rep.t_init_misc,
                       sp2_loop_x2=rep.t_sp2_loop_x2, sp2_loop_norm=rep.t_sp2_loop_norm,
                       sp2_loop_misc=rep.t_sp2_loop_misc)

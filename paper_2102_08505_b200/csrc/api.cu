@@ -86,7 +86,7 @@ struct ellpack_ctx_s {
     int64_t launches = 0;
     // small device/pinned blocks
     int32_t* d_status = nullptr;              // [0] ovf rows, [1] max kept
-    unsigned long long* d_keys = nullptr;     // gershgorin min/max keys
+    unsigned long long* d_keys = nullptr;     // gershgorin min/max keys; [2] SP2 product count
     double* d_sums = nullptr;                 // final sums (<= 8)
     int32_t* d_bw = nullptr;                  // bandwidth probe
     LaunchCfg last_cfg{};
@@ -454,6 +454,16 @@ int ellpack_ctx_create(int device, void* stream, ellpack_ctx* out) {
     c->device = device;
     c->stream = (cudaStream_t)stream;
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    {
+        // keep freed stream-ordered allocations in the device pool: SP2 re-creates iterates of
+        // growing width every few iterations, and returning them to the driver at each sync
+        // costs milliseconds per GB
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     cudaError_t e = cudaMalloc(&c->d_status, 64);
     if (!e) e = cudaMalloc(&c->d_keys, 64);
     if (!e) e = cudaMalloc(&c->d_sums, 64);
@@ -916,13 +926,29 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     RK(grow(c, c->rows[2], sizeof(double) * n));
     double t_x2 = 0.0, t_norm = 0.0;
     double e_hist[2] = {NAN, NAN};
-    int32_t wy = w;
+    // Widths. The GROW reading (§8c-c10 iv) fixes the LOGICAL width sequence (round_up32 of the
+    // required width whenever it is exceeded) that the report records, exactly as the oracle.
+    // The PHYSICAL width of the iterate buffer may be larger: it is allocated with headroom
+    // (x 1.5 of the required width, the fill of gapless systems grows every iteration), so an
+    // iteration whose logical width grows is recomputed only when the physical one overflows.
+    // Values and patterns do not depend on the storage width.
+    int32_t wy = w;       // logical width of X_{n+1}
+    int32_t wx = w;       // logical width of X_n
+    int32_t wcap = w;     // physical width of the Y buffer
     int stop = -1;
     int it;
     for (it = 0; it < o.max_iter; ++it) {
         const int branch = (trX > (double)nocc) ? SP2_SQUARE : SP2_EXPAND;
-        if (!Y.owned || Y.d.w != wy) {
-            if ((rc = dm_alloc(c, Y, n, wy))) { status = rc; break; }
+        if (!Y.owned || Y.d.w < wy) {
+            if ((rc = dm_alloc(c, Y, n, wcap > wy ? wcap : wy))) { status = rc; break; }
+        }
+        // scalar products of this X^2 (this rank's rows; summed over ranks below)
+        CK(cudaMemsetAsync(c->d_keys + 2, 0, 8, c->stream));
+        {
+            int64_t pr0, pr1;
+            rows_of(c, n, &pr0, &pr1);
+            CK(launch_products(kmat(&X.d), X.d.nnz, pr0, pr1, c->d_keys + 2, c->stream));
+            c->launches++;
         }
         bool redo;
         int32_t kept_max = 0;
@@ -953,20 +979,31 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             t_x2 += ms1 * 1e-3;
             t_norm += ms2 * 1e-3;
             kept_max = c->h->status[1];
-            if (c->h->status[0] > 0) {
+            if (kept_max > wy) {
+                // the logical width grows (the oracle's regrow)
                 if (o.on_overflow == SP2_FAIL || kept_max > maxw) {
                     R.stop_reason = SP2_OVERFLOWED;
-                    R.overflow_rows = c->h->status[0];
+                    R.overflow_rows = 0;
+                    // rows over the logical width: exact count needs the full output when the
+                    // physical buffer overflowed too; the status word counts rows over Y.d.w
+                    R.overflow_rows = c->h->status[0] > 0 ? c->h->status[0] : -1;
                     R.required_width = kept_max;
                     R.fail_iter = it;
-                    c->last_ovf_rows = c->h->status[0];
+                    c->last_ovf_rows = R.overflow_rows;
                     c->last_req = kept_max;
                     status = ELLPACK_ERR_OVERFLOW;
                     break;
                 }
                 wy = round_up32(kept_max) < maxw ? round_up32(kept_max) : maxw;
-                if ((rc = dm_alloc(c, Y, n, wy))) { status = rc; break; }
                 R.regrows++;
+            }
+            if (c->h->status[0] > 0) {
+                // the physical buffer overflowed: re-create it with headroom and redo step n
+                // (deterministic: the same values)
+                const int64_t want = round_up32((int64_t)kept_max + kept_max / 2);
+                wcap = (int32_t)(want < maxw ? want : maxw);
+                if (wcap < wy) wcap = wy;
+                if ((rc = dm_alloc(c, Y, n, wcap))) { status = rc; break; }
                 redo = true;
             }
         } while (redo);
@@ -984,10 +1021,18 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             iters[it].width = wy;
             iters[it].required = kept_max;
             iters[it].reserved = 0;
-            iters[it].products = -1;
+            unsigned long long pr = 0;
+            if (c->comm) {
+                NK(g_nccl.AllReduce(c->d_keys + 2, c->d_keys + 2, 1, ncclUint64, ncclSum, c->comm, c->stream));
+            }
+            CK(cudaMemcpyAsync(&c->h->keys[0], c->d_keys + 2, 8, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            pr = c->h->keys[0];
+            iters[it].products = (int64_t)pr;
         }
         if ((rc = allgather_desc(c, &Y.d))) { status = rc; break; }
         std::swap(X, Y);
+        wx = wy;
         trX = trY;
         if (std::fabs(e) <= tol) stop = SP2_CONVERGED;
         else if (it + 1 >= o.min_iter && e <= o.stag_gate && !std::isnan(e_hist[0]) && e >= e_hist[0])
@@ -999,7 +1044,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     }
     const double t_loop_end = now_s();
     R.iterations = it;
-    R.final_width = X.owned ? X.d.w : 0;
+    R.final_width = X.owned ? wx : 0;
     R.trD = trX;
     if (status == ELLPACK_OK) {
         R.stop_reason = stop;

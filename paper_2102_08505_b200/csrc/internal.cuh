@@ -100,6 +100,8 @@ cudaError_t launch_fnorm_rows(KMat a, KMat b, int64_t row_begin, int64_t row_end
 cudaError_t launch_identity(int64_t n, KOut id, cudaStream_t s);
 cudaError_t launch_copy_rows(KMat src, KOut dst, int64_t row_begin, int64_t row_end,
                              int32_t* status, cudaStream_t s);
+cudaError_t launch_products(KMat a, const int32_t* nnz_b, int64_t r0, int64_t r1, unsigned long long* out,
+                            cudaStream_t s);
 cudaError_t launch_max_nnz(const int32_t* nnz, int64_t row_begin, int64_t row_end,
                            int32_t* out, cudaStream_t s);
 

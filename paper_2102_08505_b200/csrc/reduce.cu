@@ -220,3 +220,30 @@ cudaError_t launch_max_nnz(const int32_t* nnz, int64_t r0, int64_t r1, int32_t* 
 }
 
 }  // namespace ell
+
+namespace ell {
+// P = sum_i sum_{k in A_i} nnz_B(k), rows [r0, r1): the scalar-product count of A x B
+// (SURVEY §8d "P"), reported per SP2 iteration. Warp per row, exact int64 atomics.
+__global__ void products_kernel(KMat a, const int32_t* __restrict__ nnz_b, int64_t r0, int64_t r1,
+                                unsigned long long* out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = r0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    unsigned long long s = 0;
+    if (i < r1) {
+        const int na = a.nnz[i];
+        const int32_t* ac = a.col + (size_t)i * a.w;
+        for (int q = lane; q < na; q += 32) s += (unsigned long long)nnz_b[ac[q]];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    if (lane == 0 && s) atomicAdd(out, s);
+}
+
+cudaError_t launch_products(KMat a, const int32_t* nnz_b, int64_t r0, int64_t r1, unsigned long long* out,
+                            cudaStream_t s) {
+    const int64_t rows = r1 - r0;
+    if (rows <= 0) return cudaSuccess;
+    products_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(a, nnz_b, r0, r1, out);
+    return cudaGetLastError();
+}
+}  // namespace ell

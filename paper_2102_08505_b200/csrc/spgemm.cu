@@ -40,6 +40,9 @@
 namespace ell {
 
 constexpr int kStage = 128;  // A-row entries staged in shared memory per piece
+#ifndef ELL_G3_HB
+#define ELL_G3_HB 2  // fast path, 3 groups per step: steps per register half
+#endif
 
 __device__ __forceinline__ int warp_min(int v) {
 #pragma unroll
@@ -1079,7 +1082,7 @@ static cudaError_t prep_mode(const LaunchCfg& cfg, int* bps) {
         case 0: return prep_kernel(row_general_kernel<MODE>, cfg, bps);
         case 1: return prep_kernel(row_fast_kernel<1, 4, MODE>, cfg, bps);
         case 2: return prep_kernel(row_fast_kernel<2, 3, MODE>, cfg, bps);
-        case 3: return prep_kernel(row_fast_kernel<3, 2, MODE>, cfg, bps);
+        case 3: return prep_kernel(row_fast_kernel<3, ELL_G3_HB, MODE>, cfg, bps);
         default: return prep_kernel(row_fast_kernel<4, 2, MODE>, cfg, bps);
     }
 }
@@ -1091,7 +1094,7 @@ static void launch_mode(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t
         case 0: row_general_kernel<MODE><<<grid, block, cfg.smem, s>>>(p); break;
         case 1: row_fast_kernel<1, 4, MODE><<<grid, block, cfg.smem, s>>>(p); break;
         case 2: row_fast_kernel<2, 3, MODE><<<grid, block, cfg.smem, s>>>(p); break;
-        case 3: row_fast_kernel<3, 2, MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 3: row_fast_kernel<3, ELL_G3_HB, MODE><<<grid, block, cfg.smem, s>>>(p); break;
         default: row_fast_kernel<4, 2, MODE><<<grid, block, cfg.smem, s>>>(p); break;
     }
 }

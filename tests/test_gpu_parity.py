@@ -330,6 +330,7 @@ def _compare_sp2(g, o):
         assert a["branch"] == b["branch"]
         assert (a["trX"], a["trS"], a["e"]) == (b["trX"], b["trS"], b["e"])
         assert a["width"] == b["width"] and a["required"] == b["required"]
+        assert a["products"] == b["products"]  # scalar-product count of the X^2
         assert abs(a["fnorm"] - b["fnorm"]) <= 1e-10 * max(b["fnorm"], 1e-300)
     assert g.trD == o.trD
 
