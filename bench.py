@@ -335,6 +335,8 @@ def run_sp2(args):
     dev = torch.cuda.current_device()
     eb.build()
     ctx = eb.Context(dev)
+    if args.general_window:
+        ctx.set_option(eb.OPT_GENERAL_WINDOW, args.general_window)
     if args.sp2_cfg == 3:
         H, cf = synth.cfg3(), synth.CFG3
     else:
@@ -415,6 +417,7 @@ def main():
                     help="x2: the headline cfg5 X^2 (default); sp2: SP2 iterations/sec on cfg3/cfg4")
     ap.add_argument("--sp2-cfg", type=int, default=3, choices=[3, 4])
     ap.add_argument("--sp2-iters", type=int, default=10)
+    ap.add_argument("--general-window", type=int, default=0, help="general-path window (0 = auto)")
     args = ap.parse_args()
     if args.workload == "sp2":
         if args.impl == "reference":

@@ -100,9 +100,11 @@ int ellpack_ctx_set_stream(ellpack_ctx ctx, void* stream);
  *                          resets the accumulators. 0 = off (default).
  *  ELLPACK_OPT_ABLATE      timing experiments only, results are WRONG when set:
  *                          1 = the fast kernel skips its output-row stores,
- *                          2 = it skips the accumulator updates. 0 = off (default). */
+ *                          2 = it skips the accumulator updates. 0 = off (default).
+ *  ELLPACK_OPT_GENERAL_WINDOW  window (doubles, multiple of 32) of the general path that
+ *                          wide rows (dense SP2 iterates) use; 0 = automatic (1024). */
 enum { ELLPACK_OPT_WINDOW = 1, ELLPACK_OPT_WARPS = 2, ELLPACK_OPT_SP2_WIDTH0 = 3, ELLPACK_OPT_PROFILE = 4,
-       ELLPACK_OPT_ABLATE = 5 };
+       ELLPACK_OPT_ABLATE = 5, ELLPACK_OPT_GENERAL_WINDOW = 6 };
 int ellpack_ctx_set_option(ellpack_ctx ctx, int key, int64_t value);
 
 /* Accumulated device time (ms, CUDA events on the ctx stream) and launch count of

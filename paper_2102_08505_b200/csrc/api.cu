@@ -29,7 +29,7 @@ using namespace ell;
 // Dense-window limits (doubles per row): rows whose centred window needs more than
 // kFastWindowMax use the multi-pass general path with kGeneralWindow.
 constexpr int64_t kFastWindowMax = 12288;  // 96 KB + stage per warp
-constexpr int64_t kGeneralWindow = 4096;
+constexpr int64_t kGeneralWindow = 1024;  // measured best for cfg3/cfg4 SP2 (512..4096 swept)
 
 namespace {
 
@@ -82,7 +82,7 @@ struct ellpack_ctx_s {
     int device = 0;
     cudaStream_t stream = nullptr;
     int num_sms = 148;
-    int window_opt = 0, warps_opt = 0, sp2_width0 = 0, ablate = 0;
+    int window_opt = 0, warps_opt = 0, sp2_width0 = 0, ablate = 0, general_s = 0;
     int64_t launches = 0;
     // small device/pinned blocks
     int32_t* d_status = nullptr;              // [0] ovf rows, [1] max kept
@@ -105,7 +105,7 @@ struct ellpack_ctx_s {
     int64_t ident_n = 0;
     Buf hx_val, hx_col, hx_nnz, hy_val, hy_col, hy_nnz;  // host-path device copies
     Buf timing;                                          // ELL_TIMING debug builds only
-    Buf bt, bt_nbin;                         // bank-balanced copy of B (fast path)
+    Buf bt, bt_nbin, bp;                         // bank-balanced copy of B (fast path)
     // ring sizing cache: (hB, G, mode) -> (S, rows resident per SM)
     int64_t ring_key = -1;
     int ring_S = 0;
@@ -268,7 +268,7 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
         }
         S = c->ring_S;
     } else {
-        S = kGeneralWindow;
+        S = c->general_s > 0 ? c->general_s : kGeneralWindow;
         p.fast = 0;
     }
     (void)h;
@@ -289,6 +289,14 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
         p.bt = (const unsigned char*)c->bt.p;
         p.bt_nbin = (const int32_t*)c->bt_nbin.p;
         p.bt_w = wt;
+    } else {
+        // breakpoints of B at the aligned window starts (general path)
+        const int np = (int)((n + p.S - 1) / p.S) + 1;
+        RK(grow(c, c->bp, sizeof(int32_t) * (size_t)n * np));
+        CK(launch_breakpoints(p.B, n, p.S, np, (int32_t*)c->bp.p, c->num_sms, c->stream));
+        c->launches++;
+        p.bp = (const int32_t*)c->bp.p;
+        p.bp_np = np;
     }
     c->last_cfg = cfg;
     const int64_t total_warps = (int64_t)cfg.grid * cfg.warps_per_cta;
@@ -296,11 +304,6 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
     p.cursors = nullptr;
     p.st_val = nullptr;
     p.st_col = nullptr;
-    if (may_multi) {
-        p.cur_stride = p.A.w;
-        RK(grow(c, c->cursors, sizeof(int32_t) * (size_t)total_warps * p.cur_stride));
-        p.cursors = (int32_t*)c->cursors.p;
-    }
     if (may_multi || p.fast) {
         // in-place rows are stashed on the ring path (progressive emission) and on multi-pass rows
         if (p.stash_a || p.stash_old) {
@@ -481,7 +484,7 @@ int ellpack_ctx_destroy(ellpack_ctx c) {
     Buf* bufs[] = {&c->rows[0], &c->rows[1], &c->rows[2], &c->rows[3], &c->partials, &c->cursors,
                    &c->stash_val, &c->stash_col, &c->ident_val, &c->ident_col, &c->ident_nnz,
                    &c->hx_val, &c->hx_col, &c->hx_nnz, &c->hy_val, &c->hy_col, &c->hy_nnz,
-                   &c->bt, &c->bt_nbin, &c->timing};
+                   &c->bt, &c->bt_nbin, &c->bp, &c->timing};
     for (Buf* b : bufs) release(c, *b);
     cudaStreamSynchronize(c->stream);
     if (c->comm && g_nccl.ok) g_nccl.CommDestroy(c->comm);
@@ -508,6 +511,10 @@ int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
         case ELLPACK_OPT_WARPS: c->warps_opt = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_SP2_WIDTH0: c->sp2_width0 = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_ABLATE: c->ablate = (int)v; return ELLPACK_OK;
+        case ELLPACK_OPT_GENERAL_WINDOW:
+            if (v < 0 || v > kFastWindowMax || (v & 31)) return ELLPACK_ERR_ARG;
+            c->general_s = (int)v;
+            return ELLPACK_OK;
         case ELLPACK_OPT_PROFILE:
             c->profile = v != 0;
             c->prof_ms = 0.0;

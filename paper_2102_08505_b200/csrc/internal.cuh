@@ -49,6 +49,8 @@ struct RowOpParams {
     const unsigned char* bt;  // row k: int32 slot8[bt_w] (8 (j mod S), padding: 8 (S + r)), f64 val[bt_w]
     const int32_t* bt_nbin;
     int32_t bt_w;             // 64 G
+    const int32_t* bp;        // general path: breakpoints [N][bp_np] of B at multiples of S
+    int32_t bp_np;
     int32_t ablate;           // timing experiments only (ELLPACK_OPT_ABLATE): 1 no row stores, 2 no accumulate
     // optional per-row outputs, indexed by global row (nullable)
     double* diag_a;   // stored a_ii
@@ -100,6 +102,7 @@ cudaError_t launch_fnorm_rows(KMat a, KMat b, int64_t row_begin, int64_t row_end
 cudaError_t launch_identity(int64_t n, KOut id, cudaStream_t s);
 cudaError_t launch_copy_rows(KMat src, KOut dst, int64_t row_begin, int64_t row_end,
                              int32_t* status, cudaStream_t s);
+cudaError_t launch_breakpoints(KMat b, int64_t n, int S, int np, int32_t* bp, int num_sms, cudaStream_t s);
 cudaError_t launch_products(KMat a, const int32_t* nnz_b, int64_t r0, int64_t r1, unsigned long long* out,
                             cudaStream_t s);
 cudaError_t launch_max_nnz(const int32_t* nnz, int64_t row_begin, int64_t row_end,

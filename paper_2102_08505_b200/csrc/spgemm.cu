@@ -322,39 +322,67 @@ __device__ __forceinline__ void sts64_if(bool pr, uint32_t a, double v) {
 
 // ------------------------------------------------------------------------- general path
 
-// Multi-pass accumulate: entries at or beyond c0 + width are left for later passes; the
-// staged cursor ast[t] advances by the in-range count.
-__device__ __forceinline__ void accumulate_multi(const RowOpParams& p, const WarpSmem& w, int lane, int cnt,
-                                                 int c0, int width) {
+// Window accumulate of the general path: for staged step t, B row k's entries whose columns
+// fall in the window [c0, c0 + S) are exactly the slots [ast(t), anb(t)) (precomputed
+// breakpoints, windows aligned to multiples of S), so there is no range test and no cursor.
+// Each round issues U independent gathers per lane (U * 32 entries) before the updates.
+template <int U>
+__device__ __forceinline__ void accumulate_seg(const RowOpParams& p, const WarpSmem& w, int lane, int cnt, int c0) {
     const int32_t* __restrict__ bcol = p.B.col;
     const double* __restrict__ bval = p.B.val;
+    const uint32_t abase = w.acc - 8u * (uint32_t)c0;
     for (int t = 0; t < cnt; ++t) {
         const long long bo = stg_boff(w, t);
-        const int nb = stg_anb(w, t);
-        const int st = stg_ast(w, t);
+        const int e = stg_anb(w, t);
+        int q0 = stg_ast(w, t);
+        if (q0 >= e) continue;  // warp-uniform: no entry of row k in this window
         const double a = stg_aa(w, t);
-        int q0 = st, n_in = 0;
-        while (q0 < nb) {
-            const int qa = q0 + lane, qb = q0 + 32 + lane;
-            const int ja = qa < nb ? __ldg(bcol + bo + qa) : INT_MAX;
-            const int jb = qb < nb ? __ldg(bcol + bo + qb) : INT_MAX;
-            const unsigned oa = (unsigned)(ja - c0), ob = (unsigned)(jb - c0);
-            const bool ia = oa < (unsigned)width, ib = ob < (unsigned)width;
-            const double va = ia ? __ldg(bval + bo + qa) : 0.0;
-            const double vb = ib ? __ldg(bval + bo + qb) : 0.0;
-            double xa = 0.0, xb = 0.0;
-            if (ia) xa = lds64(w.acc + oa * 8u);
-            if (ib) xb = lds64(w.acc + ob * 8u);
-            if (ia) sts64(w.acc + oa * 8u, __fma_rn(a, va, xa));
-            if (ib) sts64(w.acc + ob * 8u, __fma_rn(a, vb, xb));
-            const int n = __popc(__ballot_sync(FULL, ia)) + __popc(__ballot_sync(FULL, ib));
-            n_in += n;
-            if (n < 64) break;
-            q0 += 64;
+        for (; q0 < e; q0 += 32 * U) {
+            int j[U];
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int q = q0 + 32 * u + lane;
+                j[u] = q < e ? __ldg(bcol + bo + q) : -1;
+                v[u] = q < e ? __ldg(bval + bo + q) : 0.0;
+            }
+            double x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) x[u] = lds64_if(j[u] >= 0, abase + 8u * (uint32_t)j[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) sts64_if(j[u] >= 0, abase + 8u * (uint32_t)j[u], __fma_rn(a, v[u], x[u]));
         }
-        if (lane == 0) sts32i(stg_ast_a(w, t), st + n_in);
         __syncwarp();
     }
+}
+
+// Breakpoints of B for windows aligned to multiples of S: bp[k * np + q] = number of entries of
+// row k with column < q * S (q = 0 .. np - 1, np = ceil(N / S) + 1). Warp per row, lanes
+// binary-search the window starts.
+__global__ void breakpoints_kernel(KMat b, int64_t n, int S, int np, int32_t* __restrict__ bp) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = w0; k < n; k += nw) {
+        const int nb = b.nnz[k];
+        const int32_t* __restrict__ bc = b.col + (size_t)k * b.w;
+        for (int q = lane; q < np; q += 32) {
+            const long long x = (long long)q * S;
+            int lo = 0, hi = nb;  // first index with col >= x
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if ((long long)__ldg(bc + mid) < x) lo = mid + 1; else hi = mid;
+            }
+            bp[k * np + q] = lo;
+        }
+    }
+}
+
+cudaError_t launch_breakpoints(KMat b, int64_t n, int S, int np, int32_t* bp, int num_sms, cudaStream_t s) {
+    const int64_t blocks_needed = (n + 7) / 8;
+    const int64_t cap = (int64_t)num_sms * 8;
+    breakpoints_kernel<<<(unsigned)(blocks_needed < cap ? blocks_needed : cap), 256, 0, s>>>(b, n, S, np, bp);
+    return cudaGetLastError();
 }
 
 // --------------------------------------------------------------------- combine and emit
@@ -935,8 +963,9 @@ __global__ void __launch_bounds__(32, 8) row_fast_kernel(const RowOpParams p) {
     flush_status(p, lane, my_max_kept, my_ovf);
 }
 
-// General kernel: span pre-pass + ceil(span / S) passes of an S-double window with per-k
-// cursors (rows wider than any ring that fits shared memory, B rows > 256 entries).
+// General kernel: span pre-pass + one pass per S-aligned window the row touches; B rows are
+// split at window boundaries by precomputed breakpoints (rows wider than any ring that fits
+// shared memory, B rows > 256 entries: the densifying SP2 iterates).
 template <int MODE>
 __global__ void __launch_bounds__(128, 1) row_general_kernel(const RowOpParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -961,7 +990,8 @@ __global__ void __launch_bounds__(128, 1) row_general_kernel(const RowOpParams p
         int32_t kept = 0;
         double ds = 0.0, dc = 0.0, nrm = 0.0;
         {
-            // ---- general path: span pre-pass + ceil(span / S) passes with cursors
+            // ---- general path: span pre-pass, then one pass per window [q S, (q + 1) S) that
+            //      the row's span touches (windows aligned so breakpoints are per B row)
             int lo = INT_MAX, hi = -1;
             for (int q = lane; q < nA; q += 32) {
                 const int k = a_col[q];
@@ -979,10 +1009,7 @@ __global__ void __launch_bounds__(128, 1) row_general_kernel(const RowOpParams p
             lo = warp_min(lo) & ~1;  // even window start (16-byte slot pairs)
             hi = warp_max(hi);
             if (hi >= lo) {
-                const int span = hi - lo + 1;
-                const int npass = (span + S - 1) / S;
-                const bool multi = npass > 1;
-                int32_t* cur = p.cursors ? p.cursors + gw * p.cur_stride : nullptr;
+                const bool multi = hi / S > lo / S;  // more than one aligned window
                 if (multi && (p.stash_a || p.stash_old)) {
                     double* sv = p.st_val + gw * p.st_stride;
                     int32_t* sc = p.st_col + gw * p.st_stride;
@@ -997,21 +1024,26 @@ __global__ void __launch_bounds__(128, 1) row_general_kernel(const RowOpParams p
                     }
                     __syncwarp();
                 }
-                if (multi)
-                    for (int q = lane; q < nA; q += 32) cur[q] = 0;
                 __syncwarp();
                 int old_cur = 0;
-                for (int pass = 0; pass < npass; ++pass) {
-                    const int c0 = lo + pass * S;
-                    const int width = min(S, hi + 2 - c0) & ~1;  // even, covers [c0, hi]
+                const int np = p.bp_np;
+                for (int pass = lo / S; pass <= hi / S; ++pass) {
+                    const int c0 = pass * S;
+                    const int width = min(S, (int)p.ncols - c0 + 1) & ~1;  // even, covers [c0, min(c0 + S, N))
                     for (int p0 = 0; p0 < nA; p0 += kStage) {
                         const int cnt = min(kStage, nA - p0);
-                        stage_piece(p, w, lane, a_col, a_val, p0, cnt, multi ? cur : nullptr);
-                        accumulate_multi(p, w, lane, cnt, c0, width);
-                        if (multi) {
-                            for (int q = lane; q < cnt; q += 32) cur[p0 + q] = stg_ast(w, q);
-                            __syncwarp();
+                        // stage: B-row offset, a_ik, and the window's slot range [bp(k, pass), bp(k, pass + 1))
+                        for (int q = lane; q < cnt; q += 32) {
+                            const int k = a_col[p0 + q];
+                            const long long bo = (long long)k * p.B.w;
+                            asm volatile("st.shared.s64 [%0], %1;" ::"r"(w.stg + 8u * q), "l"(bo) : "memory");
+                            sts64(w.stg + 8u * (kStage + q), a_val[p0 + q]);
+                            const int32_t* bpk = p.bp + (size_t)k * np + pass;
+                            sts32i(stg_ast_a(w, q), __ldg(bpk));
+                            sts32i(stg_anb_a(w, q), __ldg(bpk + 1));
                         }
+                        __syncwarp();
+                        accumulate_seg<4>(p, w, lane, cnt, c0);
                     }
                     __syncwarp();
                     if ((int64_t)c0 <= i && i < (int64_t)c0 + width) ds = lds64(w.acc + (uint32_t)(i - c0) * 8u);
