@@ -623,8 +623,15 @@ __device__ __forceinline__ void ring_emit_pairs(const RowOpParams& p, const Warp
 
 // Emit NCH consecutive 32-column chunks [F, F + 32 NCH) (column j lives in ring slot
 // j - baseF, minus S past the wrap): pre-combine diagonal, combine with Old, drop, compact
-// (NCH independent ballots) and write; the slots (and flags) are cleared.
-template <int MODE, int NCH>
+// (NCH independent ballots) and write; the slots (and flags) are cleared. One slot per lane
+// per chunk, so each chunk's kept entries are ONE contiguous run written by one store
+// instruction per array (fully coalesced). A1: alpha == 1 (no scaling of product-only slots).
+__device__ __forceinline__ uint64_t opaque_u64(uint64_t x) {
+    asm volatile("mov.b64 %0, %0;" : "+l"(x));  // keeps the row base a plain 64-bit register
+    return x;
+}
+
+template <int MODE, int NCH, bool A1>
 __device__ __forceinline__ void ring_emit_block(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
                                                 int F, int baseF, const int32_t* o_col, const double* o_val,
                                                 int nOld, int& old_cur, double* __restrict__ crow_v,
@@ -640,6 +647,7 @@ __device__ __forceinline__ void ring_emit_block(const RowOpParams& p, const Warp
     if (MODE != 0) ring_merge_old<MODE>(p, w, lane, Fe, baseF, o_col, o_val, nOld, old_cur, nrm);
     double x[NCH];
     unsigned m[NCH];
+    const double tau = p.tau;
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
         int pc = F + 32 * c - baseF;
@@ -655,25 +663,50 @@ __device__ __forceinline__ void ring_emit_block(const RowOpParams& p, const Warp
         }
         x[c] = v;
         if (!flagged) {
-            if (p.alpha != 1.0) x[c] = __dmul_rn(p.alpha, v);
+            if (!A1) x[c] = __dmul_rn(p.alpha, v);
             if (MODE == 2) nrm = __fma_rn(v, v, nrm);
         }
-        m[c] = __ballot_sync(FULL, fabs(x[c]) > p.tau);
+        m[c] = __ballot_sync(FULL, fabs(x[c]) > tau);
     }
     const unsigned lt = (1u << lane) - 1u;
+    const int cw = p.C.w;
+    const uint64_t bv = opaque_u64((uint64_t)crow_v), bc = opaque_u64((uint64_t)crow_c);
     int before = kept;
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
         const bool keep = (m[c] >> lane) & 1u;
-        const int pos = before + __popc(m[c] & lt);
-        st_entry(keep && pos < p.C.w, crow_v + (uint32_t)pos, crow_c + (uint32_t)pos, x[c], F + 32 * c + lane);
-        if ((int64_t)F + 32 * c + lane == i) dc = keep ? x[c] : 0.0;
+        const uint32_t pos = (uint32_t)before + (uint32_t)__popc(m[c] & lt);
+        const int col = F + 32 * c + lane;
+        st_entry(keep && pos < (uint32_t)cw && !(p.ablate & 1), reinterpret_cast<double*>(bv + 8ull * pos),
+                 reinterpret_cast<int32_t*>(bc + 4ull * pos), x[c], col);
+        if (MODE != 0 && (int64_t)col == i) dc = keep ? x[c] : 0.0;
         before += __popc(m[c]);
     }
     kept = before;
 }
 
 // Emit [F, Fto) (multiples of 32), four chunks at a time where possible; advances F, baseF.
+template <int MODE, bool A1>
+__device__ __forceinline__ void ring_emit_range_t(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
+                                                  int& F, int& baseF, int Fto, const int32_t* o_col,
+                                                  const double* o_val, int nOld, int& old_cur,
+                                                  double* __restrict__ crow_v, int32_t* __restrict__ crow_c,
+                                                  int& kept, double& ds, double& dc, double& nrm) {
+    while (p.S >= 256 && F + 128 <= Fto) {  // a 128-column block wraps at most once
+        ring_emit_block<MODE, 4, A1>(p, w, lane, i, F, baseF, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept,
+                                     ds, dc, nrm);
+        F += 128;
+        while (F - baseF >= p.S) baseF += p.S;
+    }
+    while (F < Fto) {
+        ring_emit_block<MODE, 1, A1>(p, w, lane, i, F, baseF, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept,
+                                     ds, dc, nrm);
+        F += 32;
+        if (F - baseF >= p.S) baseF += p.S;
+    }
+    __syncwarp();
+}
+
 template <int MODE>
 __device__ __forceinline__ void ring_emit_range(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
                                                 int& F, int& baseF, int Fto, const int32_t* o_col,
@@ -687,19 +720,12 @@ __device__ __forceinline__ void ring_emit_range(const RowOpParams& p, const Warp
         }
         return;
     }
-    while (p.S >= 256 && F + 128 <= Fto) {  // a 128-column block wraps at most once
-        ring_emit_pairs<MODE, 2>(p, w, lane, i, F, baseF, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept, ds,
-                                 dc, nrm);
-        F += 128;
-        while (F - baseF >= p.S) baseF += p.S;
-    }
-    while (F < Fto) {
-        ring_emit_block<MODE, 1>(p, w, lane, i, F, baseF, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept, ds,
-                                 dc, nrm);
-        F += 32;
-        if (F - baseF >= p.S) baseF += p.S;
-    }
-    __syncwarp();
+    if (p.alpha == 1.0)
+        ring_emit_range_t<MODE, true>(p, w, lane, i, F, baseF, Fto, o_col, o_val, nOld, old_cur, crow_v, crow_c,
+                                      kept, ds, dc, nrm);
+    else
+        ring_emit_range_t<MODE, false>(p, w, lane, i, F, baseF, Fto, o_col, o_val, nOld, old_cur, crow_v, crow_c,
+                                       kept, ds, dc, nrm);
 }
 
 // One output row on the ring fast path. B is the bank-balanced copy (p.bt, 64 G slots per
