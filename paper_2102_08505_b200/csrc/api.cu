@@ -316,6 +316,8 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
     }
     p.status = c->d_status;
     CK(cudaMemsetAsync(c->d_status, 0, 2 * sizeof(int32_t), c->stream));
+    p.row_ticket = c->d_keys + 3;  // d_keys[3]: the fast kernel's row counter
+    CK(cudaMemsetAsync(p.row_ticket, 0, 8, c->stream));
 #ifdef ELL_TIMING
     // debug build only: per-warp phase cycle counters, summarised on stderr after each launch
     const size_t tbytes = sizeof(unsigned long long) * 8 * (size_t)total_warps;

@@ -58,6 +58,7 @@ struct RowOpParams {
     double* diag_c;   // stored output c_ii (tr of the new iterate)
     double* normsq;   // sum over the union of (s_ij - old_ij)^2   (old_mode != 0)
     int32_t* status;  // [0] overflow rows, [1] max kept count
+    unsigned long long* row_ticket;  // fast kernel: dynamic row counter (zeroed before each launch)
     // per-warp global scratch (only touched by multi-pass rows)
     int32_t* cursors;
     int64_t cur_stride;

@@ -176,9 +176,9 @@ __device__ __forceinline__ void stage_piece(const RowOpParams& p, const WarpSmem
 //   3. bin b is half h = (b >> 1) & 1 of instruction (group g = b >> 2, parity b & 1):
 //      slot 64 g + 2 (16 h + m) + (b & 1), so a lane's two slots of a group are adjacent
 //      (one 8-byte index load, one 16-byte value load);
-//   4. unused positions of a used group are padding: value 0 and a trash slot S + r with a
-//      residue r not used in the position's bin (distinct per padding lane while possible),
-//      so padding lanes run the same LDS / DFMA / STS without adding bank conflicts.
+//   4. unused positions of a used group are padding: value 0 and a trash slot S + m (m the
+//      position in the bin: distinct bank pairs among a bin's padding lanes), so padding lanes
+//      run the same LDS / DFMA / STS.
 // Record of row k (12 * 64 G bytes): int32 slot8[64 G] (= 8 * slot) then f64 val[64 G].
 // bt_nbin[k] = NB: group g holds entries iff NB > 4 g.
 __global__ void balance_kernel(KMat b, int64_t n, int wt, int S, unsigned char* __restrict__ bt,
@@ -209,9 +209,7 @@ __global__ void balance_kernel(KMat b, int64_t n, int wt, int S, unsigned char* 
         int acc = 0;
 #pragma unroll
         for (int r = 0; r < 16; ++r) { run[r] = acc; acc += cnt[r]; }
-        // pass 2: rank e within the residue-sorted order, dealt round-robin over the bins;
-        // bin_mask (lane b < NB): residues used in bin b
-        unsigned bin_mask = 0;
+        // pass 2: rank e within the residue-sorted order, dealt round-robin over the bins
         for (int c = 0; c < nb; c += 32) {
             const int q = c + lane;
             const bool v = q < nb;
@@ -224,35 +222,24 @@ __global__ void balance_kernel(KMat b, int64_t n, int wt, int S, unsigned char* 
                 if (res == r) e = run[r] + __popc(m & lt);
                 run[r] += __popc(m);
             }
-            const int bin = v ? e % NB : 32, pos = v ? e / NB : 0;
             if (v) {
+                const int bin = e % NB, pos = e / NB;
                 const int sl = 64 * (bin >> 2) + 2 * (16 * ((bin >> 1) & 1) + pos) + (bin & 1);
                 oo[sl] = 8 * (j % S);
                 ov[sl] = __ldg(bv + q);
             }
-            for (int bb = 0; bb < NB; ++bb) {
-                const unsigned rm = __reduce_or_sync(FULL, bin == bb ? (1u << res) : 0u);
-                if (lane == bb) bin_mask |= rm;
-            }
         }
-        // padding: bin b holds fill_b = ceil((nb - b) / NB) entries at positions 0..fill_b-1;
-        // positions fill_b..15 of bins < 4 ceil(NB / 4) get distinct unused residues' trash slots
+        // padding: bin b holds fill_b = ceil((nb - b) / NB) entries at positions 0..fill_b-1; the
+        // positions fill_b..15 of the bins of used groups get trash slot S + m (distinct residues
+        // among the padding lanes of a bin; padding is rare: at most one position per bin of a
+        // used group, plus the unused bins of the last group)
         const int nbins = 4 * ((NB + 3) >> 2);
-        for (int bb = 0; bb < nbins; ++bb) {
+        for (int t = lane; t < nbins * 16; t += 32) {
+            const int bb = t >> 4, m = t & 15;
             const int fill = bb < NB ? (nb - bb + NB - 1) / NB : 0;
-            const unsigned used = __shfl_sync(FULL, bin_mask, bb & 31) & (bb < NB ? 0xffffu : 0u);
-            const int m = lane;  // position handled by this lane (lanes 0..15)
-            if (m < 16 && m >= fill) {
-                // the (m - fill)-th residue not used in the bin (wrapping if the bin uses > 16 - ...)
-                const unsigned freem = ~used & 0xffffu;
-                const int nfree = __popc(freem);
-                int want = nfree ? (m - fill) % nfree : 0;
-                int r = 0;
-                unsigned f = nfree ? freem : 0xffffu;
-                for (; want > 0; --want) f &= f - 1;
-                r = __ffs(f) - 1;
+            if (m >= fill) {
                 const int sl = 64 * (bb >> 2) + 2 * (16 * ((bb >> 1) & 1) + m) + (bb & 1);
-                oo[sl] = 8 * (S + r);
+                oo[sl] = 8 * (S + m);
                 ov[sl] = 0.0;
             }
         }
@@ -950,6 +937,13 @@ __device__ __forceinline__ void flush_status(const RowOpParams& p, int lane, int
     }
 }
 
+// Next row index (relative to row_begin) for this warp: lane 0 takes a ticket, all lanes get it.
+__device__ __forceinline__ int64_t next_row(const RowOpParams& p, int lane) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(p.row_ticket, 1ull);
+    return (int64_t)__shfl_sync(FULL, t, 0);
+}
+
 // Fast kernel: ring window, every row single-pass (host-verified: ring >= 2 hB + 33,
 // B rows <= 64 G entries). One warp per CTA: the ring base is then a compile-time constant
 // and folds into the shared-memory address of every accumulator access.
@@ -960,9 +954,10 @@ __global__ void __launch_bounds__(32, 8) row_fast_kernel(const RowOpParams p) {
     const WarpSmem w = warp_smem<MODE>(smem_raw, 0, p.S, true);
     clear_window<MODE>(w, lane, p.S);
     const int64_t gw = blockIdx.x;
-    const int64_t nwarps = gridDim.x;
     int32_t my_max_kept = 0, my_ovf = 0;
-    for (int64_t i = p.row_begin + gw; i < p.row_end; i += nwarps) {
+    // Rows are handed out dynamically (one atomic per row): 6 resident warps share 4 schedulers
+    // unevenly (2, 2, 1, 1), so a static stride would leave the lone warps idle at the tail.
+    for (int64_t i = p.row_begin + next_row(p, lane); i < p.row_end; i = p.row_begin + next_row(p, lane)) {
         RowIO r = row_io<MODE>(p, i);
         const double dA = p.diag_a ? stored_diag_a(r, lane, i) : 0.0;
         if (p.stash_a || p.stash_old) {
