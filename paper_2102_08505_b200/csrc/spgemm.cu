@@ -996,9 +996,8 @@ __global__ void __launch_bounds__(128, 1) row_general_kernel(const RowOpParams p
     const WarpSmem w = warp_smem<MODE>(smem_raw, wid, S, false);
     clear_window<MODE>(w, lane, S);
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
-    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
     int32_t my_max_kept = 0, my_ovf = 0;
-    for (int64_t i = p.row_begin + gw; i < p.row_end; i += nwarps) {
+    for (int64_t i = p.row_begin + next_row(p, lane); i < p.row_end; i = p.row_begin + next_row(p, lane)) {
         RowIO r = row_io<MODE>(p, i);
         const double* a_val = r.a_val;
         const int32_t* a_col = r.a_col;
