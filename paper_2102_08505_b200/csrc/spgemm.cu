@@ -36,6 +36,7 @@
 // is a runtime, warp-uniform choice.
 #include "internal.cuh"
 #include <climits>
+#include <type_traits>
 
 namespace ell {
 
@@ -281,6 +282,19 @@ __device__ __forceinline__ uint64_t l2_evict_last_policy() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
+}
+// predicated forms with an immediate byte offset: the address is formed once per B row
+template <int OFF>
+__device__ __forceinline__ void ldg_keep_i2_if(bool pr, const void* p, uint64_t pol, int2& v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+                 "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%3+%5], %4;\n\t}"
+                 : "+r"(v.x), "+r"(v.y) : "r"((int)pr), "l"(p), "l"(pol), "n"(OFF));
+}
+template <int OFF>
+__device__ __forceinline__ void ldg_keep_d2_if(bool pr, const void* p, uint64_t pol, double2& v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+                 "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%3+%5], %4;\n\t}"
+                 : "+d"(v.x), "+d"(v.y) : "r"((int)pr), "l"(p), "l"(pol), "n"(OFF));
 }
 __device__ __forceinline__ int2 ldg_keep_i2(const void* p, uint64_t pol) {
     int2 v;
@@ -766,20 +780,24 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
 
     int2 ro[2][HB][G];
     double2 rv[2][HB][G];
-    // burst: the gathers of half h into register half X (stage metadata k, nb)
-    auto burst = [&](int X, int h) {
+    double am[2][HB];  // per-step metadata of each register half (read once, by the burst)
+    int km[2][HB], nbm[2][HB];
+    // burst: the gathers of half h into register half X (stage metadata a, k, nb)
+    auto burst = [&](auto Xc, int h) {
+        constexpr int X = decltype(Xc)::value;
 #pragma unroll
         for (int e = 0; e < HB; ++e) {
-            double a_unused;
-            int k, nb;
-            stage_fast_get(w, h * HB + e, a_unused, k, nb);
-            const unsigned char* __restrict__ rp = btl + (size_t)(uint32_t)k * RS;
+            stage_fast_get(w, h * HB + e, am[X][e], km[X][e], nbm[X][e]);
+            const int nb = (p.ablate & 4) ? 0 : nbm[X][e];
+            const unsigned char* __restrict__ rp = btl + (size_t)(uint32_t)km[X][e] * RS;
+            const unsigned char* __restrict__ vp = rp + 8 * lane;
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                if (nb > 4 * g && !(p.ablate & 4)) {
-                    ro[X][e][g] = ldg_keep_i2(rp + 256 * g, pol);
-                    rv[X][e][g] = ldg_keep_d2(rp + 256 * G + 8 * lane + 512 * g, pol);
-                }
+                // immediate offsets: indices at 256 g, values at 256 G + 512 g (+ 8 lane via vp)
+                if (g == 0) { ldg_keep_i2_if<0>(nb > 0, rp, pol, ro[X][e][0]); ldg_keep_d2_if<256 * G>(nb > 0, vp, pol, rv[X][e][0]); }
+                if (g == 1) { ldg_keep_i2_if<256>(nb > 4, rp, pol, ro[X][e][1]); ldg_keep_d2_if<256 * G + 512>(nb > 4, vp, pol, rv[X][e][1]); }
+                if (g == 2) { ldg_keep_i2_if<512>(nb > 8, rp, pol, ro[X][e][2]); ldg_keep_d2_if<256 * G + 1024>(nb > 8, vp, pol, rv[X][e][2]); }
+                if (g == 3) { ldg_keep_i2_if<768>(nb > 12, rp, pol, ro[X][e][3]); ldg_keep_d2_if<256 * G + 1536>(nb > 12, vp, pol, rv[X][e][3]); }
             }
         }
     };
@@ -801,11 +819,11 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
         __syncwarp();
     };
     // one half of HB steps from register half X
-    auto half = [&](int X, int h) {
-        double a_[HB];
-        int k_[HB], nb_[HB];
-#pragma unroll
-        for (int e = 0; e < HB; ++e) stage_fast_get(w, h * HB + e, a_[e], k_[e], nb_[e]);
+    auto half = [&](auto Xc, int h) {
+        constexpr int X = decltype(Xc)::value;
+        const double* a_ = am[X];
+        const int* k_ = km[X];
+        const int* nb_ = nbm[X];
         // touch this half's burst: the store waits for it (and for nothing younger)
         if (nb_[0] > 0) sts32i(acc + 8u * (uint32_t)S, ro[X][0][0].x);
         const int kf = k_[0], kl = k_[HB - 1];
@@ -813,7 +831,7 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
             ring_emit_range<MODE>(p, w, lane, i, F, baseF, (kf - hB) & ~31, o_col, o_val, nOld, old_cur,
                                   crow_v, crow_c, kept, ds, dc, nrm);
         __syncwarp();
-        burst(X ^ 1, h + 1);  // the next half (a null half past the piece end: no loads)
+        burst(std::integral_constant<int, X ^ 1>{}, h + 1);  // the next half (a null half past the piece end: no loads)
         if (kl + hB < F + S) {
 #pragma unroll
             for (int e = 0; e < HB; ++e) step(X, e, a_[e], nb_[e]);
@@ -849,10 +867,10 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
                          "l"(__double_as_longlong(a)), "l"(knb) : "memory");
         }
         __syncwarp();
-        burst(0, 0);
+        burst(std::integral_constant<int, 0>{}, 0);
         for (int h = 0; h < nh; h += 2) {
-            half(0, h);
-            if (h + 1 < nh) half(1, h + 1);
+            half(std::integral_constant<int, 0>{}, h);
+            if (h + 1 < nh) half(std::integral_constant<int, 1>{}, h + 1);
         }
     }
     // final chunks
