@@ -336,8 +336,16 @@ __device__ __forceinline__ void accumulate_seg(const RowOpParams& p, const WarpS
         const long long bo = stg_boff(w, t);
         const int e = stg_anb(w, t);
         int q0 = stg_ast(w, t);
-        if (q0 >= e) continue;  // warp-uniform: no entry of row k in this window
         const double a = stg_aa(w, t);
+        if (e - q0 <= 32) {  // short segment (wide sparse rows): one entry per lane
+            const int q = q0 + lane;
+            const int j = q < e ? __ldg(bcol + bo + q) : -1;
+            const double v = q < e ? __ldg(bval + bo + q) : 0.0;
+            const double x = lds64_if(j >= 0, abase + 8u * (uint32_t)j);
+            sts64_if(j >= 0, abase + 8u * (uint32_t)j, __fma_rn(a, v, x));
+            __syncwarp();
+            continue;
+        }
         for (; q0 < e; q0 += 32 * U) {
             int j[U];
             double v[U];
@@ -1076,18 +1084,33 @@ __global__ void __launch_bounds__(128, 1) row_general_kernel(const RowOpParams p
                     const int width = min(S, (int)p.ncols - c0 + 1) & ~1;  // even, covers [c0, min(c0 + S, N))
                     for (int p0 = 0; p0 < nA; p0 += kStage) {
                         const int cnt = min(kStage, nA - p0);
-                        // stage: B-row offset, a_ik, and the window's slot range [bp(k, pass), bp(k, pass + 1))
-                        for (int q = lane; q < cnt; q += 32) {
-                            const int k = a_col[p0 + q];
-                            const long long bo = (long long)k * p.B.w;
-                            asm volatile("st.shared.s64 [%0], %1;" ::"r"(w.stg + 8u * q), "l"(bo) : "memory");
-                            sts64(w.stg + 8u * (kStage + q), a_val[p0 + q]);
-                            const int32_t* bpk = p.bp + (size_t)k * np + pass;
-                            sts32i(stg_ast_a(w, q), __ldg(bpk));
-                            sts32i(stg_anb_a(w, q), __ldg(bpk + 1));
+                        // stage (compacted, k ascending): B-row offset, a_ik and the window's slot
+                        // range [bp(k, pass), bp(k, pass + 1)) of the A entries whose B row has
+                        // entries in this window -- wide sparse rows touch few k per window
+                        int ns = 0;
+                        for (int q0 = 0; q0 < cnt; q0 += 32) {
+                            const int q = q0 + lane;
+                            int k = 0, sb = 0, se = 0;
+                            if (q < cnt) {
+                                k = a_col[p0 + q];
+                                const int32_t* bpk = p.bp + (size_t)k * np + pass;
+                                sb = __ldg(bpk);
+                                se = __ldg(bpk + 1);
+                            }
+                            const bool ne = se > sb;
+                            const unsigned m = __ballot_sync(FULL, ne);
+                            if (ne) {
+                                const int t = ns + __popc(m & ((1u << lane) - 1u));
+                                const long long bo = (long long)k * p.B.w;
+                                asm volatile("st.shared.s64 [%0], %1;" ::"r"(w.stg + 8u * t), "l"(bo) : "memory");
+                                sts64(w.stg + 8u * (kStage + t), a_val[p0 + q]);
+                                sts32i(stg_ast_a(w, t), sb);
+                                sts32i(stg_anb_a(w, t), se);
+                            }
+                            ns += __popc(m);
                         }
                         __syncwarp();
-                        accumulate_seg<4>(p, w, lane, cnt, c0);
+                        accumulate_seg<4>(p, w, lane, ns, c0);
                     }
                     __syncwarp();
                     if ((int64_t)c0 <= i && i < (int64_t)c0 + width) ds = lds64(w.acc + (uint32_t)(i - c0) * 8u);
