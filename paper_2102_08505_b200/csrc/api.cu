@@ -29,6 +29,7 @@ using namespace ell;
 // Dense-window limits (doubles per row): rows whose centred window needs more than
 // kFastWindowMax use the multi-pass general path with kGeneralWindow.
 constexpr int64_t kFastWindowMax = 12288;  // 96 KB + stage per warp
+constexpr int kFastMinRows = 4;            // ring path only with >= 4 rows resident per SM
 constexpr int64_t kGeneralWindow = 1024;  // measured best for cfg3/cfg4 SP2 (512..4096 swept)
 
 namespace {
@@ -109,6 +110,7 @@ struct ellpack_ctx_s {
     // ring sizing cache: (hB, G, mode) -> (S, rows resident per SM)
     int64_t ring_key = -1;
     int ring_S = 0;
+    bool ring_ok = true;
     // overflow info of the last OVERFLOW
     int64_t last_ovf_rows = 0;
     int32_t last_req = 0;
@@ -255,6 +257,10 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
         if (key != c->ring_key) {
             LaunchCfg t;
             CK(plan_row_op(p, (int)ring, groups, c->warps_opt, c->num_sms, &t));
+            // a ring too wide for kFastMinRows rows per SM leaves the SM latency-bound: the
+            // general path (1024-double windows, ~16 warps/SM) is faster there (SP2 cfg4 it 1:
+            // 2 rows/SM ring 29.7 ms)
+            c->ring_ok = t.bps * t.warps_per_cta >= kFastMinRows;
             const int64_t rows0 = (int64_t)t.grid * t.warps_per_cta;  // resident rows (full grid)
             int64_t grown = ring;
             for (int64_t s2 = ring + 32; s2 <= ring + 512 && s2 <= kFastWindowMax && s2 <= nr; s2 += 32) {
@@ -267,6 +273,10 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
             c->ring_S = (int)grown;
         }
         S = c->ring_S;
+        if (!c->ring_ok) {
+            S = c->general_s > 0 ? c->general_s : kGeneralWindow;
+            p.fast = 0;
+        }
     } else {
         S = c->general_s > 0 ? c->general_s : kGeneralWindow;
         p.fast = 0;
@@ -938,7 +948,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     // Widths. The GROW reading (§8c-c10 iv) fixes the LOGICAL width sequence (round_up32 of the
     // required width whenever it is exceeded) that the report records, exactly as the oracle.
     // The PHYSICAL width of the iterate buffer may be larger: it is allocated with headroom
-    // (x 1.5 of the required width, the fill of gapless systems grows every iteration), so an
+    // (x 3 of the required width, the fill of gapless systems grows every iteration), so an
     // iteration whose logical width grows is recomputed only when the physical one overflows.
     // Values and patterns do not depend on the storage width.
     int32_t wy = w;       // logical width of X_{n+1}
@@ -1009,7 +1019,8 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             if (c->h->status[0] > 0) {
                 // the physical buffer overflowed: re-create it with headroom and redo step n
                 // (deterministic: the same values)
-                const int64_t want = round_up32((int64_t)kept_max + kept_max / 2);
+                // headroom x3: the fill of gapless iterates grows 2.5-3x per early iteration
+                const int64_t want = round_up32((int64_t)kept_max * 3);
                 wcap = (int32_t)(want < maxw ? want : maxw);
                 if (wcap < wy) wcap = wy;
                 if ((rc = dm_alloc(c, Y, n, wcap))) { status = rc; break; }

@@ -74,6 +74,7 @@ struct LaunchCfg {
     int grid;
     size_t smem;
     int R;               // fast path: 64-entry B groups per step (1..4)
+    int bps;             // resident CTAs per SM at this configuration
 };
 
 // spgemm.cu

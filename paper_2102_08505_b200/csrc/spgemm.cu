@@ -1229,6 +1229,7 @@ cudaError_t plan_row_op(const RowOpParams& p, int S, int groups, int warps_opt, 
     const int wpc = best_wpc, bps = best_bps;
     cfg->warps_per_cta = wpc;
     cfg->smem = (size_t)wpc * per_warp;
+    cfg->bps = bps;
     {
         int dummy = 0;
         cudaError_t e = mode == 0 ? prep_mode<0>(*cfg, &dummy) : mode == 1 ? prep_mode<1>(*cfg, &dummy)
