@@ -309,6 +309,13 @@ __device__ __forceinline__ double2 ldg_keep_d2(const void* p, uint64_t pol) {
     return v;
 }
 
+// read-and-clear of an accumulator slot: shared 64-bit atomic exchange with +0.0
+__device__ __forceinline__ double lds64_clear(uint32_t a) {
+    unsigned long long v;
+    asm volatile("atom.shared.exch.b64 %0, [%1], 0;" : "=l"(v) : "r"(a) : "memory");
+    return __longlong_as_double((long long)v);
+}
+
 // predicated shared accesses (padding lanes issue no request and cost no wavefront)
 __device__ __forceinline__ double lds64_if(bool pr, uint32_t a) {
     double v;  // undefined when !pr (the predicated store discards the result)
@@ -662,8 +669,7 @@ __device__ __forceinline__ void ring_emit_block(const RowOpParams& p, const Warp
         int pc = F + 32 * c - baseF;
         if (pc >= S) pc -= S;
         const uint32_t pa = w.acc + 8u * (uint32_t)(pc + lane);
-        const double v = lds64(pa);
-        sts64(pa, 0.0);
+        const double v = lds64_clear(pa);  // read the slot and leave +0.0 behind (one instruction)
         bool flagged = false;
         if (MODE != 0) {
             const uint32_t fa = w.flg + (uint32_t)(pc + lane);
