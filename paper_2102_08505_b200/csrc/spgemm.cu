@@ -184,50 +184,67 @@ __device__ __forceinline__ void stage_piece(const RowOpParams& p, const WarpSmem
 // bt_nbin[k] = NB: group g holds entries iff NB > 4 g.
 __global__ void balance_kernel(KMat b, int64_t n, int wt, int S, unsigned char* __restrict__ bt,
                                int32_t* __restrict__ bt_nbin) {
+    __shared__ int hist_s[8][16];  // per warp: entries per residue (256-thread blocks)
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
+    int* hist = hist_s[threadIdx.x >> 5];
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const double invS = 1.0 / (double)S;
     for (int64_t k = w0; k < n; k += nw) {
-        const int nb = b.nnz[k];
+        const int nb = b.nnz[k];  // <= 256 on the fast path (8 chunks)
         const int NB = (nb + 15) >> 4;
         const int32_t* __restrict__ bc = b.col + (size_t)k * b.w;
         const double* __restrict__ bv = b.val + (size_t)k * b.w;
         int32_t* __restrict__ oo = reinterpret_cast<int32_t*>(bt + (size_t)k * 12 * wt);
         double* __restrict__ ov = reinterpret_cast<double*>(bt + (size_t)k * 12 * wt + 4 * (size_t)wt);
         if (lane == 0) bt_nbin[k] = NB;
-        // pass 1: per-residue counts (warp-uniform)
-        int cnt[16];
+        if (lane < 16) hist[lane] = 0;
+        __syncwarp();
+        // rank within residue (stable: chunk order, then lane order): one match per chunk
+        int jr[8], rk[8];
 #pragma unroll
-        for (int r = 0; r < 16; ++r) cnt[r] = 0;
-        for (int c = 0; c < nb; c += 32) {
-            const int q = c + lane;
-            const int res = q < nb ? (__ldg(bc + q) & 15) : 16;
-#pragma unroll
-            for (int r = 0; r < 16; ++r) cnt[r] += __popc(__ballot_sync(FULL, res == r));
-        }
-        int run[16];
-        int acc = 0;
-#pragma unroll
-        for (int r = 0; r < 16; ++r) { run[r] = acc; acc += cnt[r]; }
-        // pass 2: rank e within the residue-sorted order, dealt round-robin over the bins
-        for (int c = 0; c < nb; c += 32) {
-            const int q = c + lane;
-            const bool v = q < nb;
-            const int j = v ? __ldg(bc + q) : 0;
-            const int res = v ? (j & 15) : 16;
-            int e = 0;
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                const unsigned m = __ballot_sync(FULL, res == r);
-                if (res == r) e = run[r] + __popc(m & lt);
-                run[r] += __popc(m);
+        for (int c = 0; c < 8; ++c) {
+            const int q = 32 * c + lane;
+            jr[c] = q < nb ? __ldg(bc + q) : -1;
+            rk[c] = 0;
+            if (32 * c < nb) {  // warp-uniform
+                const int res = jr[c] >= 0 ? (jr[c] & 15) : 16 + lane;  // padding lanes: unique keys
+                const unsigned m = __match_any_sync(FULL, res);
+                const int leader = __ffs(m) - 1;
+                int base = 0;
+                if (lane == leader && jr[c] >= 0) base = atomicAdd(&hist[res], __popc(m));
+                base = __shfl_sync(FULL, base, leader);
+                rk[c] = base + __popc(m & lt);
             }
-            if (v) {
-                const int bin = e % NB, pos = e / NB;
-                const int sl = 64 * (bin >> 2) + 2 * (16 * ((bin >> 1) & 1) + pos) + (bin & 1);
-                oo[sl] = 8 * (j % S);
-                ov[sl] = __ldg(bv + q);
+        }
+        __syncwarp();
+        // exclusive prefix over the residues (lanes 0..15)
+        int h = lane < 16 ? hist[lane] : 0, pre = h;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, pre, o);
+            if (lane >= o) pre += y;
+        }
+        pre -= h;  // exclusive
+        // e / NB by multiply-high (exact for e < 2^16; NB == 1 has no 32-bit magic)
+        const unsigned magic = NB > 1 ? 0xffffffffu / (unsigned)NB + 1u : 0u;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            if (32 * c < nb) {
+                const int j = jr[c];
+                const int e = __shfl_sync(FULL, pre, j >= 0 ? (j & 15) : 0) + rk[c];
+                if (j >= 0) {
+                    const int pos = NB > 1 ? (int)__umulhi((unsigned)e, magic) : e;
+                    const int bin = e - pos * NB;
+                    const int sl = 64 * (bin >> 2) + 2 * (16 * ((bin >> 1) & 1) + pos) + (bin & 1);
+                    int qs = __double2int_rz((double)j * invS);
+                    int js = j - qs * S;
+                    js += js < 0 ? S : 0;
+                    js -= js >= S ? S : 0;
+                    oo[sl] = 8 * js;
+                    ov[sl] = __ldg(bv + 32 * c + lane);
+                }
             }
         }
         // padding: bin b holds fill_b = ceil((nb - b) / NB) entries at positions 0..fill_b-1; the
@@ -244,6 +261,7 @@ __global__ void balance_kernel(KMat b, int64_t n, int wt, int S, unsigned char* 
                 ov[sl] = 0.0;
             }
         }
+        __syncwarp();
     }
 }
 
