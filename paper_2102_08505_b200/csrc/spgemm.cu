@@ -682,15 +682,18 @@ __device__ __forceinline__ void ring_emit_block(const RowOpParams& p, const Warp
     double x[NCH];
     unsigned m[NCH];
     const double tau = p.tau;
+    // slot of chunk c: pc0 + 32 c, minus S from the chunk where the ring wraps (S, pc0 multiples
+    // of 32: a chunk never straddles the wrap)
+    const int pc0 = F - baseF;
+    const uint32_t sa0 = w.acc + 8u * (uint32_t)(pc0 + lane);
+    const uint32_t wrapb = 8u * (uint32_t)S;
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
-        int pc = F + 32 * c - baseF;
-        if (pc >= S) pc -= S;
-        const uint32_t pa = w.acc + 8u * (uint32_t)(pc + lane);
+        const uint32_t pa = sa0 + 256u * c - (pc0 + 32 * c >= S ? wrapb : 0u);
         const double v = lds64_clear(pa);  // read the slot and leave +0.0 behind (one instruction)
         bool flagged = false;
         if (MODE != 0) {
-            const uint32_t fa = w.flg + (uint32_t)(pc + lane);
+            const uint32_t fa = w.flg + (uint32_t)(pc0 + 32 * c - (pc0 + 32 * c >= S ? S : 0) + lane);
             flagged = lds8(fa) != 0;
             sts8(fa, 0u);
         }
@@ -704,13 +707,16 @@ __device__ __forceinline__ void ring_emit_block(const RowOpParams& p, const Warp
     const unsigned lt = (1u << lane) - 1u;
     const int cw = p.C.w;
     const uint64_t bv = opaque_u64((uint64_t)crow_v), bc = opaque_u64((uint64_t)crow_c);
+    // the width test is needed only when this block can reach the row's end (overflow rows)
+    const bool room = kept + 32 * NCH <= cw && !(p.ablate & 1);
     int before = kept;
+    const int col0 = F + lane;
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
         const bool keep = (m[c] >> lane) & 1u;
         const uint32_t pos = (uint32_t)before + (uint32_t)__popc(m[c] & lt);
-        const int col = F + 32 * c + lane;
-        st_entry(keep && pos < (uint32_t)cw && !(p.ablate & 1), reinterpret_cast<double*>(bv + 8ull * pos),
+        const int col = col0 + 32 * c;
+        st_entry(keep && (room || (pos < (uint32_t)cw && !(p.ablate & 1))), reinterpret_cast<double*>(bv + 8ull * pos),
                  reinterpret_cast<int32_t*>(bc + 4ull * pos), x[c], col);
         if (MODE != 0 && (int64_t)col == i) dc = keep ? x[c] : 0.0;
         before += __popc(m[c]);
