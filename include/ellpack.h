@@ -98,9 +98,10 @@ int ellpack_ctx_set_stream(ellpack_ctx ctx, void* stream);
  *                          CUDA events on the context stream and accumulate its
  *                          device time (ellpack_ctx_kernel_time); setting it
  *                          resets the accumulators. 0 = off (default).
- *  ELLPACK_OPT_ABLATE      timing experiments only, results are WRONG when set:
- *                          1 = the fast kernel skips its output-row stores,
- *                          2 = it skips the accumulator updates. 0 = off (default).
+ *  ELLPACK_OPT_ABLATE      timing experiments only, results are WRONG when set (bit mask):
+ *                          1 = the ring kernel skips its output-row stores, 2 = its
+ *                          accumulator updates, 4 = its B gathers, 8 = its emission.
+ *                          0 = off (default).
  *  ELLPACK_OPT_GENERAL_WINDOW  window (doubles, multiple of 32) of the general path that
  *                          wide rows (dense SP2 iterates) use; 0 = automatic (1024). */
 enum { ELLPACK_OPT_WINDOW = 1, ELLPACK_OPT_WARPS = 2, ELLPACK_OPT_SP2_WIDTH0 = 3, ELLPACK_OPT_PROFILE = 4,

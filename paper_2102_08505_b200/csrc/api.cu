@@ -101,11 +101,10 @@ struct ellpack_ctx_s {
     // workspace
     Buf rows[4];      // per-row double arrays
     Buf partials;     // canonical block partials
-    Buf cursors, stash_val, stash_col;
+    Buf stash_val, stash_col;
     Buf ident_val, ident_col, ident_nnz;
     int64_t ident_n = 0;
     Buf hx_val, hx_col, hx_nnz, hy_val, hy_col, hy_nnz;  // host-path device copies
-    Buf timing;                                          // ELL_TIMING debug builds only
     Buf bt, bt_nbin, bp;                         // bank-balanced copy of B (fast path)
     // ring sizing cache: (hB, G, mode) -> (S, rows resident per SM)
     int64_t ring_key = -1;
@@ -311,7 +310,6 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
     c->last_cfg = cfg;
     const int64_t total_warps = (int64_t)cfg.grid * cfg.warps_per_cta;
     const bool may_multi = n > cfg.S;
-    p.cursors = nullptr;
     p.st_val = nullptr;
     p.st_col = nullptr;
     if (may_multi || p.fast) {
@@ -328,31 +326,8 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
     CK(cudaMemsetAsync(c->d_status, 0, 2 * sizeof(int32_t), c->stream));
     p.row_ticket = c->d_keys + 3;  // d_keys[3]: the fast kernel's row counter
     CK(cudaMemsetAsync(p.row_ticket, 0, 8, c->stream));
-#ifdef ELL_TIMING
-    // debug build only: per-warp phase cycle counters, summarised on stderr after each launch
-    const size_t tbytes = sizeof(unsigned long long) * 8 * (size_t)total_warps;
-    RK(grow(c, c->timing, tbytes));
-    CK(cudaMemsetAsync(c->timing.p, 0, tbytes, c->stream));
-    p.timing = (unsigned long long*)c->timing.p;
-#else
-    p.timing = nullptr;
-#endif
     if (c->profile) CK(cudaEventRecord(c->ev[4], c->stream));
     CK(launch_row_op(p, cfg, c->stream));
-#ifdef ELL_TIMING
-    {
-        std::vector<unsigned long long> T(8 * (size_t)total_warps);
-        CK(cudaMemcpyAsync(T.data(), c->timing.p, tbytes, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        double st = 0, ac = 0, em = 0, rows = 0, nz = 0;
-        for (int64_t k = 0; k < total_warps; ++k) {
-            st += T[8 * k]; ac += T[8 * k + 1]; em += T[8 * k + 2]; rows += T[8 * k + 3]; nz += T[8 * k + 4];
-        }
-        if (rows > 0)
-            fprintf(stderr, "[ell-timing] S=%d G=%d wpc=%d grid=%d rows=%.0f  cycles/row: stage %.0f acc %.0f emit %.0f  | acc cycles/step %.1f\n",
-                    cfg.S, cfg.R, cfg.warps_per_cta, cfg.grid, rows, st / rows, ac / rows, em / rows, ac / (nz > 0 ? nz : 1));
-    }
-#endif
     if (c->profile) {
         CK(cudaEventRecord(c->ev[5], c->stream));
         c->prof_pending = true;
@@ -493,10 +468,10 @@ int ellpack_ctx_create(int device, void* stream, ellpack_ctx* out) {
 int ellpack_ctx_destroy(ellpack_ctx c) {
     if (!c) return ELLPACK_ERR_ARG;
     cudaSetDevice(c->device);
-    Buf* bufs[] = {&c->rows[0], &c->rows[1], &c->rows[2], &c->rows[3], &c->partials, &c->cursors,
+    Buf* bufs[] = {&c->rows[0], &c->rows[1], &c->rows[2], &c->rows[3], &c->partials,
                    &c->stash_val, &c->stash_col, &c->ident_val, &c->ident_col, &c->ident_nnz,
                    &c->hx_val, &c->hx_col, &c->hx_nnz, &c->hy_val, &c->hy_col, &c->hy_nnz,
-                   &c->bt, &c->bt_nbin, &c->bp, &c->timing};
+                   &c->bt, &c->bt_nbin, &c->bp};
     for (Buf* b : bufs) release(c, *b);
     cudaStreamSynchronize(c->stream);
     if (c->comm && g_nccl.ok) g_nccl.CommDestroy(c->comm);

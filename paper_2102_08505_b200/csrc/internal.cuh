@@ -51,7 +51,7 @@ struct RowOpParams {
     int32_t bt_w;             // 64 G
     const int32_t* bp;        // general path: breakpoints [N][bp_np] of B at multiples of S
     int32_t bp_np;
-    int32_t ablate;           // timing experiments only (ELLPACK_OPT_ABLATE): 1 no row stores, 2 no accumulate
+    int32_t ablate;           // timing experiments only (ELLPACK_OPT_ABLATE bit mask, include/ellpack.h)
     // optional per-row outputs, indexed by global row (nullable)
     double* diag_a;   // stored a_ii
     double* diag_s;   // pre-combine s_ii  (tr(X^2) pre-drop, R5)
@@ -59,13 +59,10 @@ struct RowOpParams {
     double* normsq;   // sum over the union of (s_ij - old_ij)^2   (old_mode != 0)
     int32_t* status;  // [0] overflow rows, [1] max kept count
     unsigned long long* row_ticket;  // fast kernel: dynamic row counter (zeroed before each launch)
-    // per-warp global scratch (only touched by multi-pass rows)
-    int32_t* cursors;
-    int64_t cur_stride;
+    // per-warp global scratch: in-place rows are copied aside (stash) before they are rewritten
     double* st_val;
     int32_t* st_col;
     int64_t st_stride;
-    unsigned long long* timing;  // ELL_TIMING builds only: per-warp phase cycle counters
 };
 
 struct LaunchCfg {

@@ -1,39 +1,33 @@
-// spgemm.cu — the fused ELLPACK row kernel of libellpack (sm_100a, FP64 CUDA cores).
+// spgemm.cu — the row kernels of libellpack (sm_100a, FP64 CUDA cores).
 //
-// One warp owns one output row i (BJ north_star (1): "a warp or small CTA owns each
-// output row"); a persistent grid strides over rows [row_begin, row_end).
-// Per row:
-//   a1  window: the host probes the bandwidths of A, B (and Old) once per launch, so
-//       every row's products fall in the row-centred window [i - h, i + h]; the
-//       window (S doubles, S >= 2h+1) is a dense accumulator in shared memory and
-//       the row needs no span pre-pass ("fast path"). Rows whose span does not fit
-//       (S capped by shared memory, e.g. dense SP2 iterates) take the general path:
-//       a span pre-pass and ceil(span/S) passes with per-k cursors.
-//   a2  gather + accumulate: A's row is staged in shared memory (B-row offset,
-//       a_ik, nnz_B(k)); for k ascending the warp's lanes take the entries of B row k
-//       (distinct columns, so no two lanes collide inside one k) and do
-//       acc[j] = fma(a_ik, b_kj, acc[j]); a __syncwarp between consecutive k orders
-//       the read-modify-writes, so every output entry is the fma chain in ascending
-//       k (reading R12 -> bitwise equal to the oracle). B rows are prefetched D
-//       steps ahead into registers (up to R groups of 32 entries per step; groups
-//       beyond nnz_B(k) are skipped warp-uniformly) with read-only loads, hiding the
-//       L2 latency of the gather; a step's R shared loads, fmas and shared stores
-//       are issued as batches on 32-bit shared addresses.
-//   a3  combine + drop + compact: Old_i entries (C_old / the SP2 iterate) are merged
-//       into the window with c = fma(alpha, s, beta*old); a window scan (two slots
-//       per lane, 16-byte shared loads) keeps |c| > tau, compacts with ballot/popc
-//       and writes the row contiguously in ascending column order with predicated
-//       stores, counting overflow past C.w.
+// One warp owns one output row at a time (BJ north_star (1): "a warp or small CTA owns each
+// output row"); rows are handed out dynamically. Per row:
+//   a1  window: the host probes the half-bandwidths of A, B (and Old) once per launch. If every
+//       B row has <= 256 entries and a ring of S >= 2 h_B + 33 doubles keeps >= 4 rows per SM,
+//       the ring path (row_fast_kernel) runs; otherwise the general path (row_general_kernel):
+//       S-aligned windows of 1024 doubles, one pass per window the row touches, B rows split
+//       at the window starts by precomputed breakpoints.
+//   a2  gather + accumulate: for k ascending in A's row, every entry (j, b_kj) of B row k does
+//       acc[j] = fma(a_ik, b_kj, acc[j]) in shared memory. The entries of one B row have
+//       distinct columns, so they are applied in any order by the lanes; a __syncwarp between
+//       consecutive k orders the read-modify-writes, so every output entry is the fma chain in
+//       ascending k (reading R12 -> bitwise equal to the oracle). The ring path reads B from a
+//       bank-balanced copy with the ring slots precomputed (balance_kernel) and gathers it in
+//       half-ring register bursts (see row_ring).
+//   a3  combine + drop + compact: Old entries (C_old / the SP2 iterate) are merged with
+//       c = fma(alpha, s, beta*old); chunks of 32 columns keep |c| > tau, compact with
+//       ballot/popc and write each chunk's kept run with one coalesced store per array,
+//       counting overflow past C.w.
 //   a4  per-row trace / norm inputs (stored a_ii, pre-drop s_ii, stored c_ii,
 //       ||S - Old||^2), reduced later in canonical order (reduce.cu).
-// With A = B = Old = X this single kernel is the fused SP2 step (BJ north_star (2)):
+// With A = B = Old = X one launch is the fused SP2 step (BJ north_star (2)):
 // SQUARE = (alpha 1, old_mode 2), EXPAND = (alpha -1, beta 2, old_mode 1) since
 // fma(-1, s, 2x) = round(2x - s) exactly (2x is exact).
 //
-// Template parameters: R (B groups of 32 per prefetched step), D (prefetch depth),
-// MODE (0: no Old operand; 1: Old operand; 2: Old operand + ||S - Old||^2 norm). Whether
-// Old enters the value (beta*old, p.old_mode == 1) or only the union (p.old_mode == 2)
-// is a runtime, warp-uniform choice.
+// Template parameters: G (64-entry groups per B row), HB (steps per register half), MODE
+// (0: no Old operand; 1: Old operand; 2: Old operand + ||S - Old||^2 norm). Whether Old enters
+// the value (beta*old, p.old_mode == 1) or only the union (p.old_mode == 2) is a runtime,
+// warp-uniform choice.
 #include "internal.cuh"
 #include <climits>
 #include <type_traits>
@@ -140,21 +134,6 @@ __host__ __device__ inline size_t warp_smem_bytes(int S, bool has_old, bool fast
     return (size_t)(S + kTrash) * 8 + (fast ? (size_t)64 * 16 : (size_t)kStage * 28) + (has_old ? (size_t)S : 0);
 }
 
-// Stage A-row entries [p0, p0 + cnt): B-row offset k*B.w, a_ik, nnz_B(k), cursor.
-__device__ __forceinline__ void stage_piece(const RowOpParams& p, const WarpSmem& w, int lane,
-                                            const int32_t* a_col, const double* a_val, int p0, int cnt,
-                                            const int32_t* cur) {
-    for (int q = lane; q < cnt; q += 32) {
-        const int k = a_col[p0 + q];
-        const long long bo = (long long)k * p.B.w;
-        asm volatile("st.shared.s64 [%0], %1;" ::"r"(w.stg + 8u * q), "l"(bo) : "memory");
-        sts64(w.stg + 8u * (kStage + q), a_val[p0 + q]);
-        sts32i(stg_anb_a(w, q), __ldg(p.B.nnz + k));
-        sts32i(stg_ast_a(w, q), cur ? cur[p0 + q] : 0);
-        sts32i(stg_ak_a(w, q), k);
-    }
-    __syncwarp();
-}
 
 // ------------------------------------------------------------- bank-balanced B (fast path)
 //
@@ -274,17 +253,6 @@ cudaError_t launch_balance(KMat b, int64_t n, int wt, int S, unsigned char* bt, 
 }
 
 // Fast-path stage: 16 B per A entry {a_ik f64, k i32, NB(k) i32} (one 16-byte shared load per step)
-__device__ __forceinline__ void stage_fast(const RowOpParams& p, const WarpSmem& w, int lane,
-                                           const int32_t* a_col, const double* a_val, int p0, int cnt) {
-    for (int q = lane; q < cnt; q += 32) {
-        const int k = a_col[p0 + q];
-        const int nb = __ldg(p.bt_nbin + k);
-        const unsigned long long knb = (unsigned long long)(uint32_t)k | ((unsigned long long)(uint32_t)nb << 32);
-        asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(w.stg + 16u * q),
-                     "l"(__double_as_longlong(a_val[p0 + q])), "l"(knb) : "memory");
-    }
-    __syncwarp();
-}
 __device__ __forceinline__ void stage_fast_get(const WarpSmem& w, int t, double& a, int& k, int& nb) {
     unsigned long long x, y;
     asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(w.stg + 16u * t) : "memory");
@@ -580,79 +548,6 @@ __device__ __forceinline__ void ring_merge_old(const RowOpParams& p, const WarpS
         if (n < 32) break;
     }
     __syncwarp();
-}
-
-// Emit NP consecutive 64-column pairs of chunks [F, F + 64 NP): each lane owns two adjacent
-// columns (one 16-byte shared load and one 16-byte zeroing store per lane), two ballots per
-// pair compact the kept entries in ascending column order:
-//   rank(F + 64c + 2l) = popc(m0 & lt) + popc(m1 & lt),  rank(+1) = rank + keep0.
-// A 32-column chunk never straddles the ring wrap (S, F - baseF multiples of 32), so each
-// lane's pair is contiguous in the ring.
-template <int MODE, int NP>
-__device__ __forceinline__ void ring_emit_pairs(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
-                                                int F, int baseF, const int32_t* o_col, const double* o_val,
-                                                int nOld, int& old_cur, double* __restrict__ crow_v,
-                                                int32_t* __restrict__ crow_c, int& kept, double& ds, double& dc,
-                                                double& nrm) {
-    const int S = p.S;
-    const int Fe = F + 64 * NP;
-    if ((int64_t)F <= i && i < (int64_t)Fe) {
-        int pi = (int)(i - baseF);
-        if (pi >= S) pi -= S;
-        ds = lds64(w.acc + 8u * (uint32_t)pi);
-    }
-    if (MODE != 0) ring_merge_old<MODE>(p, w, lane, Fe, baseF, o_col, o_val, nOld, old_cur, nrm);
-    const bool a1 = p.alpha == 1.0;
-    double x[NP][2];
-    unsigned m[NP][2];
-#pragma unroll
-    for (int c = 0; c < NP; ++c) {
-        int sl = F + 64 * c + 2 * lane - baseF;
-        if (sl >= S) sl -= S;
-        const uint32_t pa = w.acc + 8u * (uint32_t)sl;
-        double v0, v1;
-        lds128(pa, v0, v1);
-        sts128(pa, 0.0, 0.0);
-        bool f0 = false, f1 = false;
-        if (MODE != 0) {
-            const uint32_t fa = w.flg + (uint32_t)sl;
-            const uint32_t fl = lds16u(fa);
-            f0 = (fl & 0xffu) != 0;
-            f1 = (fl >> 8) != 0;
-            sts16u(fa, 0u);
-        }
-        x[c][0] = v0;
-        x[c][1] = v1;
-        if (!f0) {
-            if (!a1) x[c][0] = __dmul_rn(p.alpha, v0);
-            if (MODE == 2) nrm = __fma_rn(v0, v0, nrm);
-        }
-        if (!f1) {
-            if (!a1) x[c][1] = __dmul_rn(p.alpha, v1);
-            if (MODE == 2) nrm = __fma_rn(v1, v1, nrm);
-        }
-        m[c][0] = __ballot_sync(FULL, fabs(x[c][0]) > p.tau);
-        m[c][1] = __ballot_sync(FULL, fabs(x[c][1]) > p.tau);
-    }
-    const unsigned lt = (1u << lane) - 1u;
-    const bool want_dc = p.diag_c != nullptr;
-    int before = kept;
-#pragma unroll
-    for (int c = 0; c < NP; ++c) {
-        const bool k0 = (m[c][0] >> lane) & 1u, k1 = (m[c][1] >> lane) & 1u;
-        const int pos0 = before + __popc(m[c][0] & lt) + __popc(m[c][1] & lt);
-        const int pos1 = pos0 + (int)k0;
-        const int col0 = F + 64 * c + 2 * lane;
-        const bool stw = !(p.ablate & 1);
-        st_entry(stw && k0 && pos0 < p.C.w, crow_v + (uint32_t)pos0, crow_c + (uint32_t)pos0, x[c][0], col0);
-        st_entry(stw && k1 && pos1 < p.C.w, crow_v + (uint32_t)pos1, crow_c + (uint32_t)pos1, x[c][1], col0 + 1);
-        if (want_dc) {
-            if ((int64_t)col0 == i) dc = k0 ? x[c][0] : 0.0;
-            if ((int64_t)col0 + 1 == i) dc = k1 ? x[c][1] : 0.0;
-        }
-        before += __popc(m[c][0]) + __popc(m[c][1]);
-    }
-    kept = before;
 }
 
 // Emit NCH consecutive 32-column chunks [F, F + 32 NCH) (column j lives in ring slot
