@@ -35,6 +35,9 @@
 namespace ell {
 
 constexpr int kStage = 128;  // A-row entries staged in shared memory per piece
+#ifndef ELL_SEG_U
+#define ELL_SEG_U 4  // general path: gathers per lane per round
+#endif
 #ifndef ELL_G3_HB
 #define ELL_G3_HB 2  // fast path, 3 groups per step: steps per register half
 #endif
@@ -1035,7 +1038,7 @@ __global__ void __launch_bounds__(128, 1) row_general_kernel(const RowOpParams p
                             ns += __popc(m);
                         }
                         __syncwarp();
-                        accumulate_seg<4>(p, w, lane, ns, c0);
+                        accumulate_seg<ELL_SEG_U>(p, w, lane, ns, c0);
                     }
                     __syncwarp();
                     if ((int64_t)c0 <= i && i < (int64_t)c0 + width) ds = lds64(w.acc + (uint32_t)(i - c0) * 8u);
