@@ -337,7 +337,11 @@ def run_sp2(args):
     ctx = eb.Context(dev)
     if args.general_window:
         ctx.set_option(eb.OPT_GENERAL_WINDOW, args.general_window)
-    if args.sp2_cfg == 3:
+    if args.sp2_model:
+        # the paper's own gapped SP2 workloads, run to the stop rule
+        H = synth.model_hamiltonian(args.sp2_n, args.sp2_model, tau_store=1e-5)
+        cf = dict(nocc=args.sp2_n // 2, tol=1e-8, threshold=1e-5)
+    elif args.sp2_cfg == 3:
         H, cf = synth.cfg3(), synth.CFG3
     else:
         H, cf = synth.cfg4(), synth.CFG4
@@ -386,8 +390,11 @@ def run_sp2(args):
             "metric": "SP2 iterations/sec", "value": its / (ms * 1e-3), "unit": "iterations/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": f"synthetic (synth.cfg{args.sp2_cfg}, SURVEY §8d)",
-            "config": {"workload": f"cfg{args.sp2_cfg} SP2 N={n} tau={cf['threshold']} window K={K} GROW",
+            "data": (f"synthetic (synth.model_hamiltonian {args.sp2_model}, P:L419-433)" if args.sp2_model
+                     else f"synthetic (synth.cfg{args.sp2_cfg}, SURVEY §8d)"),
+            "config": {"workload": (f"{args.sp2_model} SP2 N={n} tau={cf['threshold']} max_iter={K} GROW"
+                                    if args.sp2_model else
+                                    f"cfg{args.sp2_cfg} SP2 N={n} tau={cf['threshold']} window K={K} GROW"),
                        "iterations": its, "stop": r.stop, "final_width": r.final_width, "regrows": r.regrows,
                        "products": prods, "gflops": (2.0 * prods / (ms * 1e-3) / 1e9) if prods else None,
                        "phases_s": r.phases},
@@ -416,7 +423,10 @@ def main():
     ap.add_argument("--workload", default="x2", choices=["x2", "sp2"],
                     help="x2: the headline cfg5 X^2 (default); sp2: SP2 iterations/sec on cfg3/cfg4")
     ap.add_argument("--sp2-cfg", type=int, default=3, choices=[3, 4])
-    ap.add_argument("--sp2-iters", type=int, default=10)
+    ap.add_argument("--sp2-iters", type=int, default=10, help="SP2 window (max_iter)")
+    ap.add_argument("--sp2-model", default=None, choices=["metal", "semiconductor", "soft_matter"],
+                    help="SP2 on the paper's model Hamiltonian instead of cfg3/cfg4")
+    ap.add_argument("--sp2-n", type=int, default=16384)
     ap.add_argument("--general-window", type=int, default=0, help="general-path window (0 = auto)")
     args = ap.parse_args()
     if args.workload == "sp2":

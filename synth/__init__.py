@@ -206,3 +206,34 @@ def cfg5(n: int, m: int, seed: int = 5) -> Ell:
 
 
 CFG5 = dict(ns=(32768, 131072, 262144), ms=(64, 128, 256), threshold=1e-5)
+
+
+# ------------------------------------------------------------ paper model Hamiltonian (f2)
+# The paper's two-level-system presets. Parameter
+# names follow SPEC's ModelParams; unset parameters are 0.0.
+MODEL_PRESETS = {
+    "metal": dict(d_aa=-1.0, d_bb=-1.0, k=-0.01),
+    "semiconductor": dict(d_bb=-1.0, d_ab_intra=-2.0, k=-0.01),
+    "soft_matter": dict(d_bb=-1.0, d_ab_intra=-1.0, eps_a=-10.0, k=-0.1, r=1.0),
+}
+
+
+def model_hamiltonian(n: int, kind: str = "soft_matter", tau_store: float = 1e-5, seed: int = 6, **over) -> Ell:
+    """Two-level model Hamiltonian (synth_model in gen.c), stored entries |h| > tau_store."""
+    prm = dict(eps_a=0.0, eps_b=0.0, d_aa=0.0, d_bb=0.0, d_ab_intra=0.0, d_ab_cross=0.0, k=0.0, r=0.0)
+    prm.update(MODEL_PRESETS[kind])
+    prm.update(over)
+    L = _L()
+    f = L.synth_model
+    f.restype = ctypes.c_int64
+    f.argtypes = [ctypes.c_int64, ctypes.c_int32] + [ctypes.c_double] * 9 + [ctypes.c_uint64] + [ctypes.c_void_p] * 3
+    args = (prm["eps_a"], prm["eps_b"], prm["d_aa"], prm["d_bb"], prm["d_ab_intra"], prm["d_ab_cross"], prm["k"],
+            prm["r"], tau_store)
+    wmax = f(n, 0, *args, seed, None, None, None)
+    if wmax < 0:
+        raise ValueError("synth_model: bad arguments")
+    w = max(2, int(wmax) + (int(wmax) & 1))
+    m = Ell.empty(n, w)
+    if f(n, w, *args, seed, _p(m.val), _p(m.col), _p(m.nnz)) != 0:
+        raise ValueError("synth_model: row wider than the sized width")
+    return m

@@ -273,3 +273,74 @@ int64_t synth_products(int64_t n, int32_t wa, const int32_t* ca, const int32_t* 
         for (int32_t q = 0; q < na[i]; ++q) p += nb[ca[(size_t)i * wa + q]];
     return p;
 }
+
+/* ------------------------------------------------------------------ model Hamiltonian
+ * The paper's two-level-system model Hamiltonian:
+ * n/2 dimers, orbitals interleaved [A0, B0, A1, B1, ...] (orbital o = 2 d + t, t = 0 A, 1 B).
+ *   diagonal            eps_t * (1 + r * RAND)
+ *   same dimer, A-B     dAB_intra * (1 + r * RAND)                       (distance 0)
+ *   dimers d1 != d2     delta(t1, t2) * exp(k * |d2 - d1|) * (1 + r * RAND)
+ *                       delta = dAA (A-A), dBB (B-B), dAB_cross (A-B, B-A)
+ * RAND in [-1, 1] is ONE draw per unordered pair (and per diagonal), from a counter-based
+ * hash of (seed, min(o1, o2), max(o1, o2)), so the matrix is exactly symmetric and independent
+ * of the enumeration order. An entry is stored iff |value| > tau_store; pairs whose largest
+ * possible magnitude |delta| (1 + r) exp(k d) is <= tau_store are never enumerated (the SPEC's
+ * cutoff, exact for the stored pattern). Input synthesis only. Returns the max row count when
+ * val == NULL (sizing pass), else 0; -1 on bad arguments or a row wider than w. */
+static uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+static double pair_rand(uint64_t seed, int64_t a, int64_t b) { /* uniform in [-1, 1) */
+    uint64_t h = mix64(seed ^ mix64(((uint64_t)a << 32) ^ (uint64_t)b ^ 0x9E3779B97F4A7C15ULL));
+    return 2.0 * ((double)(h >> 11) * 0x1.0p-53) - 1.0;
+}
+
+int64_t synth_model(int64_t n, int32_t w, double eps_a, double eps_b, double d_aa, double d_bb,
+                    double d_ab_intra, double d_ab_cross, double k, double r, double tau_store, uint64_t seed,
+                    double* val, int32_t* col, int32_t* nnz) {
+    if (n < 2 || (n & 1) || k > 0.0 || r < 0.0 || tau_store < 0.0) return -1;
+    const int64_t nd = n / 2;
+    double dmaxc = fabs(d_aa);
+    if (fabs(d_bb) > dmaxc) dmaxc = fabs(d_bb);
+    if (fabs(d_ab_cross) > dmaxc) dmaxc = fabs(d_ab_cross);
+    int64_t dcut = nd; /* largest dimer distance with |delta| (1 + r) e^{k d} > tau_store */
+    if (k < 0.0 && dmaxc > 0.0 && tau_store > 0.0) {
+        double dd = log(tau_store / (dmaxc * (1.0 + r))) / k;
+        dcut = dd < 0.0 ? 0 : (int64_t)dd + 1;
+        if (dcut > nd) dcut = nd;
+    } else if (dmaxc == 0.0) {
+        dcut = 0;
+    }
+    int64_t maxrow = 0;
+    for (int64_t o = 0; o < n; ++o) {
+        const int64_t d = o >> 1;
+        const int t = (int)(o & 1);
+        int32_t cnt = 0;
+        const int64_t dlo = d - dcut < 0 ? 0 : d - dcut, dhi = d + dcut > nd - 1 ? nd - 1 : d + dcut;
+        for (int64_t d2 = dlo; d2 <= dhi; ++d2) {
+            for (int t2 = 0; t2 < 2; ++t2) {
+                const int64_t o2 = 2 * d2 + t2;
+                double base;
+                if (o2 == o) base = t ? eps_b : eps_a;
+                else if (d2 == d) base = d_ab_intra;
+                else base = (t == 0 && t2 == 0) ? d_aa : (t == 1 && t2 == 1) ? d_bb : d_ab_cross;
+                if (base == 0.0) continue;
+                const int64_t lo = o < o2 ? o : o2, hi = o < o2 ? o2 : o;
+                const int64_t dist = d2 > d ? d2 - d : d - d2;
+                const double v = base * exp(k * (double)dist) * (1.0 + r * pair_rand(seed, lo, hi));
+                if (!(fabs(v) > tau_store)) continue;
+                if (val) {
+                    if (cnt >= w) return -1;
+                    val[(size_t)o * w + cnt] = v;
+                    col[(size_t)o * w + cnt] = (int32_t)o2;
+                }
+                ++cnt;
+            }
+        }
+        if (val) nnz[o] = cnt;
+        if (cnt > maxrow) maxrow = cnt;
+    }
+    return val ? 0 : maxrow;
+}
