@@ -34,7 +34,7 @@
 
 namespace ell {
 
-constexpr int kStage = 128;  // A-row entries staged in shared memory per piece
+constexpr int kStage = 64;  // general path: A-row entries staged per piece (64: 20 warps/SM at S = 1024)
 #ifndef ELL_SEG_U
 #define ELL_SEG_U 4  // general path: gathers per lane per round
 #endif
