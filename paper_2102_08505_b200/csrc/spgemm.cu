@@ -38,6 +38,13 @@ constexpr int kStage = 64;  // general path: A-row entries staged per piece (64:
 #ifndef ELL_SEG_U
 #define ELL_SEG_U 4  // general path: gathers per lane per round
 #endif
+#ifndef ELL_STAGE_F
+#define ELL_STAGE_F 128  // fast path: stage entries (16 B each); 128 measured best vs 64, 96
+#endif
+constexpr int kStageF = ELL_STAGE_F;
+#ifndef ELL_META_REGS
+#define ELL_META_REGS 1  // fast path: keep step metadata in registers from the burst
+#endif
 #ifndef ELL_G3_HB
 #define ELL_G3_HB 2  // fast path, 3 groups per step: steps per register half
 #endif
@@ -134,7 +141,7 @@ __device__ __forceinline__ int stg_ak(const WarpSmem& w, int t) { return lds32i(
 // lanes of the fast path update; acc[S] is also the general path's trash slot.
 constexpr int kTrash = 16;
 __host__ __device__ inline size_t warp_smem_bytes(int S, bool has_old, bool fast) {
-    return (size_t)(S + kTrash) * 8 + (fast ? (size_t)64 * 16 : (size_t)kStage * 28) + (has_old ? (size_t)S : 0);
+    return (size_t)(S + kTrash) * 8 + (fast ? (size_t)kStageF * 16 : (size_t)kStage * 28) + (has_old ? (size_t)S : 0);
 }
 
 
@@ -683,7 +690,6 @@ __device__ __forceinline__ void ring_emit_range(const RowOpParams& p, const Warp
 // half's first step would otherwise wrap onto it; if the whole half then fits the ring
 // (k_last + hB < F + S) its steps need no checks, else (rare: k jumps > slack) the half runs
 // step by step with per-step emission checks.
-constexpr int kStageF = 64;  // fast-path stage entries (16 B each)
 
 template <int G, int HB, int MODE>
 __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
@@ -716,16 +722,26 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
 
     int2 ro[2][HB][G];
     double2 rv[2][HB][G];
+#if ELL_META_REGS
     double am[2][HB];  // per-step metadata of each register half (read once, by the burst)
     int km[2][HB], nbm[2][HB];
+#endif
     // burst: the gathers of half h into register half X (stage metadata a, k, nb)
     auto burst = [&](auto Xc, int h) {
         constexpr int X = decltype(Xc)::value;
 #pragma unroll
         for (int e = 0; e < HB; ++e) {
+#if ELL_META_REGS
             stage_fast_get(w, h * HB + e, am[X][e], km[X][e], nbm[X][e]);
             const int nb = (p.ablate & 4) ? 0 : nbm[X][e];
             const unsigned char* __restrict__ rp = btl + (size_t)(uint32_t)km[X][e] * RS;
+#else
+            double a_u;
+            int k_u, nb_u;
+            stage_fast_get(w, h * HB + e, a_u, k_u, nb_u);
+            const int nb = (p.ablate & 4) ? 0 : nb_u;
+            const unsigned char* __restrict__ rp = btl + (size_t)(uint32_t)k_u * RS;
+#endif
             const unsigned char* __restrict__ vp = rp + 8 * lane;
 #pragma unroll
             for (int g = 0; g < G; ++g) {
@@ -757,9 +773,17 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
     // one half of HB steps from register half X
     auto half = [&](auto Xc, int h) {
         constexpr int X = decltype(Xc)::value;
+#if ELL_META_REGS
         const double* a_ = am[X];
         const int* k_ = km[X];
         const int* nb_ = nbm[X];
+#else
+        // step metadata re-read from the stage (fewer live registers across the half)
+        double a_[HB];
+        int k_[HB], nb_[HB];
+#pragma unroll
+        for (int e = 0; e < HB; ++e) stage_fast_get(w, h * HB + e, a_[e], k_[e], nb_[e]);
+#endif
         // touch this half's burst: the store waits for it (and for nothing younger)
         if (nb_[0] > 0) sts32i(acc + 8u * (uint32_t)S, ro[X][0][0].x);
         const int kf = k_[0], kl = k_[HB - 1];
@@ -824,7 +848,7 @@ __device__ __forceinline__ WarpSmem warp_smem(unsigned char* smem_raw, int wid, 
     WarpSmem w;
     w.acc = (uint32_t)__cvta_generic_to_shared(base);
     w.stg = w.acc + (uint32_t)((S + kTrash) * 8);
-    w.flg = w.acc + (uint32_t)((S + kTrash) * 8 + (fast ? 64 * 16 : kStage * 28));
+    w.flg = w.acc + (uint32_t)((S + kTrash) * 8 + (fast ? kStageF * 16 : kStage * 28));
     return w;
 }
 
