@@ -943,6 +943,11 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             rows_of(c, n, &pr0, &pr1);
             CK(launch_products(kmat(&X.d), X.d.nnz, pr0, pr1, c->d_keys + 2, c->stream));
             c->launches++;
+            if (c->comm) {
+                NK(g_nccl.AllReduce(c->d_keys + 2, c->d_keys + 2, 1, ncclUint64, ncclSum, c->comm, c->stream));
+            }
+            // read back with the step's status/sums (same stream, no extra synchronisation)
+            CK(cudaMemcpyAsync(&c->h->keys[0], c->d_keys + 2, 8, cudaMemcpyDeviceToHost, c->stream));
         }
         bool redo;
         int32_t kept_max = 0;
@@ -1016,14 +1021,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             iters[it].width = wy;
             iters[it].required = kept_max;
             iters[it].reserved = 0;
-            unsigned long long pr = 0;
-            if (c->comm) {
-                NK(g_nccl.AllReduce(c->d_keys + 2, c->d_keys + 2, 1, ncclUint64, ncclSum, c->comm, c->stream));
-            }
-            CK(cudaMemcpyAsync(&c->h->keys[0], c->d_keys + 2, 8, cudaMemcpyDeviceToHost, c->stream));
-            CK(cudaStreamSynchronize(c->stream));
-            pr = c->h->keys[0];
-            iters[it].products = (int64_t)pr;
+            iters[it].products = (int64_t)c->h->keys[0];  // landed with the status fetch
         }
         if ((rc = allgather_desc(c, &Y.d))) { status = rc; break; }
         std::swap(X, Y);
