@@ -915,7 +915,10 @@ __device__ __forceinline__ void flush_status(const RowOpParams& p, int lane, int
     }
 }
 
-constexpr int kRowChunk = 4;  // fast kernel: rows per ticket
+#ifndef ELL_ROW_CHUNK
+#define ELL_ROW_CHUNK 4
+#endif
+constexpr int kRowChunk = ELL_ROW_CHUNK;  // fast kernel: rows per ticket
 
 // Next ticket (relative to row_begin) for this warp: lane 0 takes it, all lanes get it.
 __device__ __forceinline__ int64_t next_row(const RowOpParams& p, int lane) {
