@@ -226,7 +226,9 @@ typedef struct sp2_report {
  *   OVERFLOW; GROW re-creates X_{n+1} at round_up32(required) and redoes step n.
  * D (caller-owned, width D->w) receives the final iterate; OVERFLOW if too
  * narrow. rep may be NULL. Errors: ARG (nocc not in [0,N], tol < 0), BOUNDS,
- * OVERFLOW, NOCONV (D and rep still valid), NOMEM, CUDA, NCCL. */
+ * OVERFLOW, NOCONV (D and rep still valid), NOMEM, CUDA, NCCL; STATE if the context's rows are
+ * restricted (ellpack_ctx_set_rows) without a communicator. Iterates live in context-owned
+ * buffers that are reused across calls. */
 int sp2_run(ellpack_ctx ctx, const ellpack_desc* h, int64_t nocc, double tol,
             const sp2_opts* opts, ellpack_desc* d, sp2_report* rep);
 

@@ -16,6 +16,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <vector>
@@ -105,7 +106,8 @@ struct ellpack_ctx_s {
     Buf ident_val, ident_col, ident_nnz;
     int64_t ident_n = 0;
     Buf hx_val, hx_col, hx_nnz, hy_val, hy_col, hy_nnz;  // host-path device copies
-    Buf bt, bt_nbin, bp;                         // bank-balanced copy of B (fast path)
+    Buf bt, bt_nbin, bp;
+    Buf it[3][3];  // SP2 iterate buffers (val, col, nnz) x 3 slots                         // bank-balanced copy of B (fast path)
     // ring sizing cache: (hB, G, mode) -> (S, rows resident per SM)
     int64_t ring_key = -1;
     int ring_S = 0;
@@ -472,6 +474,8 @@ int ellpack_ctx_destroy(ellpack_ctx c) {
                    &c->stash_val, &c->stash_col, &c->ident_val, &c->ident_col, &c->ident_nnz,
                    &c->hx_val, &c->hx_col, &c->hx_nnz, &c->hy_val, &c->hy_col, &c->hy_nnz,
                    &c->bt, &c->bt_nbin, &c->bp};
+    for (auto& sl : c->it)
+        for (Buf& b : sl) release(c, b);
     for (Buf* b : bufs) release(c, *b);
     cudaStreamSynchronize(c->stream);
     if (c->comm && g_nccl.ok) g_nccl.CommDestroy(c->comm);
@@ -793,23 +797,30 @@ void sp2_opts_default(sp2_opts* o) {
 
 namespace {
 
+// SP2 iterates live in context-owned buffers (c->it[slot]) that only grow: repeated runs and
+// regrows reuse them, no allocation or zero-fill in the loop (padding slots are never read).
 struct DevMatrix {
     ellpack_desc d{};
     bool owned = false;
+    int slot = 0;
 };
 
 int dm_alloc(ellpack_ctx c, DevMatrix& m, int64_t n, int32_t w) {
-    if (m.owned) ellpack_destroy(c, &m.d);
-    m.owned = false;
-    RK(ellpack_create(c, n, w, &m.d));
+    Buf* b = c->it[m.slot];
+    RK(grow(c, b[0], sizeof(double) * (size_t)n * w));
+    RK(grow(c, b[1], sizeof(int32_t) * (size_t)n * w));
+    RK(grow(c, b[2], sizeof(int32_t) * (size_t)n));
+    m.d.n = n;
+    m.d.w = w;
+    m.d.reserved = 0;
+    m.d.val = (double*)b[0].p;
+    m.d.col = (int32_t*)b[1].p;
+    m.d.nnz = (int32_t*)b[2].p;
     m.owned = true;
     return ELLPACK_OK;
 }
 
-void dm_free(ellpack_ctx c, DevMatrix& m) {
-    if (m.owned) ellpack_destroy(c, &m.d);
-    m.owned = false;
-}
+void dm_free(ellpack_ctx, DevMatrix& m) { m.owned = false; }
 
 int32_t round_up32(int64_t x) { return (int32_t)((x + 31) & ~int64_t(31)); }
 
@@ -858,6 +869,12 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     const int64_t n = h->n;
     if (dout->n != n) return ELLPACK_ERR_DIM;
     if (nocc < 0 || nocc > n || !(tol >= 0.0)) return ELLPACK_ERR_ARG;
+    {
+        // a row block without a communicator cannot see the other rows of X_{n+1}
+        int64_t q0, q1;
+        rows_of(c, n, &q0, &q1);
+        if (!c->comm && (q0 != 0 || q1 != n)) return ELLPACK_ERR_STATE;
+    }
     sp2_opts o;
     if (opts_in) o = *opts_in; else sp2_opts_default(&o);
     if (!valid_tau(o.threshold) || o.max_iter < 1) return ELLPACK_ERR_ARG;
@@ -885,6 +902,9 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     w = (w + 1) & ~1;
     const double t_read_end = now_s();
     DevMatrix X, Y, T;
+    X.slot = 0;
+    Y.slot = 1;
+    T.slot = 2;
     int status = ELLPACK_OK;
     int32_t req = 0;
     auto cleanup = [&]() { dm_free(c, X); dm_free(c, Y); dm_free(c, T); };
@@ -923,12 +943,14 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     // Widths. The GROW reading (§8c-c10 iv) fixes the LOGICAL width sequence (round_up32 of the
     // required width whenever it is exceeded) that the report records, exactly as the oracle.
     // The PHYSICAL width of the iterate buffer may be larger: it is allocated with headroom
-    // (x 3 of the required width, the fill of gapless systems grows every iteration), so an
+    // (x 8 of the initial width, x 4 of the required width on a physical overflow), so an
     // iteration whose logical width grows is recomputed only when the physical one overflows.
     // Values and patterns do not depend on the storage width.
     int32_t wy = w;       // logical width of X_{n+1}
     int32_t wx = w;       // logical width of X_n
-    int32_t wcap = w;     // physical width of the Y buffer
+    // physical width of the Y buffer: headroom from the start (gapless fills grow several-fold per
+    // early iteration; only FAIL keeps physical == logical so overflow counts stay exact)
+    int32_t wcap = o.on_overflow == SP2_FAIL ? w : (int32_t)std::min<int64_t>(maxw, round_up32((int64_t)w * 8));
     int stop = -1;
     int it;
     for (it = 0; it < o.max_iter; ++it) {
@@ -999,8 +1021,8 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             if (c->h->status[0] > 0) {
                 // the physical buffer overflowed: re-create it with headroom and redo step n
                 // (deterministic: the same values)
-                // headroom x3: the fill of gapless iterates grows 2.5-3x per early iteration
-                const int64_t want = round_up32((int64_t)kept_max * 3);
+                // headroom x4: the fill of gapless iterates grows 2.5-4x per early iteration
+                const int64_t want = round_up32((int64_t)kept_max * 4);
                 wcap = (int32_t)(want < maxw ? want : maxw);
                 if (wcap < wy) wcap = wy;
                 if ((rc = dm_alloc(c, Y, n, wcap))) { status = rc; break; }
