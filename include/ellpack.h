@@ -182,6 +182,15 @@ int ellpack_overflow_info(ellpack_ctx ctx, int64_t* overflow_rows, int32_t* requ
 enum { SP2_FAIL = 0, SP2_GROW = 1 };
 enum { SP2_CONVERGED = 0, SP2_STAGNATED = 1, SP2_MAXITER = 2, SP2_OVERFLOWED = 3 };
 enum { SP2_SQUARE = 0, SP2_EXPAND = 1 };
+/* Branch rules. TRACE_SIGN: SQUARE iff tr(X_n) > nocc (tie -> EXPAND).
+ * TRACE_CLOSEST (§8f-f4 (i); P:L52 cites Niklasson 2002; reading R19):
+ * SQUARE iff |T2 - nocc| < |(2 tr(X_n) - T2) - nocc| (tie -> EXPAND), where
+ * T2 = canonical sum over rows of q_i, q_i = fma chain q <- fma(x, x, q) over the
+ * stored slots of row i in ascending order from +0: for symmetric X_n (every
+ * iterate of a symmetric H) T2 = sum_ij x_ij^2 = tr(X_n^2) in exact arithmetic,
+ * so the rule is decided before the fused step. T2 of X_{n+1} is computed right
+ * after step n and fetched with that step's traces (no extra synchronisation). */
+enum { SP2_RULE_TRACE_SIGN = 0, SP2_RULE_TRACE_CLOSEST = 1 };
 
 typedef struct sp2_opts {
     double threshold;      /* tau, drop threshold of every iterate (default 0) */
@@ -192,7 +201,7 @@ typedef struct sp2_opts {
     int32_t on_overflow;   /* SP2_FAIL | SP2_GROW (default GROW) */
     int32_t max_width;     /* GROW ceiling (<= 0 -> N) */
     int32_t initial_width; /* width of X0 (<= 0 -> H.w) */
-    int32_t reserved;
+    int32_t branch_rule;   /* SP2_RULE_TRACE_SIGN (default) | SP2_RULE_TRACE_CLOSEST */
 } sp2_opts;
 
 typedef struct sp2_iter_rec {
@@ -202,6 +211,7 @@ typedef struct sp2_iter_rec {
     int32_t required;          /* max kept count of X_{n+1} */
     int32_t reserved;
     int64_t products;          /* scalar products of this X^2 (pattern count) */
+    double frob2;              /* TRACE_CLOSEST: T2 of X_n that decided the branch; else 0 */
 } sp2_iter_rec;
 
 typedef struct sp2_report {
@@ -218,7 +228,8 @@ typedef struct sp2_report {
  * P:L368-371; §8c-c9..c10):
  *   bounds (Gershgorin unless given), X0 = drop(alpha*H + beta*I) with
  *   alpha = -1/(emax-emin), beta = emax/(emax-emin); then per iteration n:
- *   branch = tr(X_n) > nocc ? SQUARE : EXPAND (tie -> EXPAND);
+ *   branch = tr(X_n) > nocc ? SQUARE : EXPAND (tie -> EXPAND), or the
+ *   trace-closest rule above when opts->branch_rule = SP2_RULE_TRACE_CLOSEST;
  *   ONE fused pass computes S = X_n^2 and writes X_{n+1} = drop(S) or
  *   drop(2X_n - S) with tr(S), tr(X_{n+1}) and ||S - X_n||_F^2 partials;
  *   stop when |tr(X_n) - tr(S)| <= tol (CONVERGED), on gated stagnation

@@ -49,13 +49,14 @@ class _Opts(ctypes.Structure):
     _fields_ = [("threshold", ctypes.c_double), ("max_iter", ctypes.c_int32), ("min_iter", ctypes.c_int32),
                 ("stag_gate", ctypes.c_double), ("emin", ctypes.c_double), ("emax", ctypes.c_double),
                 ("on_overflow", ctypes.c_int32), ("max_width", ctypes.c_int32),
-                ("initial_width", ctypes.c_int32)]
+                ("initial_width", ctypes.c_int32), ("branch_rule", ctypes.c_int32)]
 
 
 class _Iter(ctypes.Structure):
     _fields_ = [("trX", ctypes.c_double), ("trS", ctypes.c_double), ("e", ctypes.c_double),
                 ("fnorm", ctypes.c_double), ("branch", ctypes.c_int32), ("width", ctypes.c_int32),
-                ("required", ctypes.c_int32), ("pad", ctypes.c_int32), ("products", ctypes.c_int64)]
+                ("required", ctypes.c_int32), ("pad", ctypes.c_int32), ("products", ctypes.c_int64),
+                ("frob2", ctypes.c_double)]
 
 
 class _Report(ctypes.Structure):
@@ -218,6 +219,7 @@ class SP2Opts:
     on_overflow: int = 1  # 0 FAIL, 1 GROW
     max_width: int = 0
     initial_width: int = 0
+    branch_rule: int = 0  # 0 trace sign, 1 trace-closest (§8f-f4 i, reading R19)
 
 
 @dataclass
@@ -241,7 +243,7 @@ def sp2(H: Ell, nocc: int, tol: float, opts: SP2Opts | None = None, d_width: int
     """SP2-Basic (§8c-c9, c10). D is returned at width d_width (default n)."""
     o = opts or SP2Opts()
     co = _Opts(o.threshold, o.max_iter, o.min_iter, o.stag_gate, o.emin, o.emax, o.on_overflow,
-               o.max_width, o.initial_width)
+               o.max_width, o.initial_width, o.branch_rule)
     D = Ell.empty(H.n, d_width or H.n)
     rep = _Report()
     its = (_Iter * max(1, o.max_iter))()
@@ -250,7 +252,8 @@ def sp2(H: Ell, nocc: int, tol: float, opts: SP2Opts | None = None, d_width: int
                          ctypes.cast(its, ctypes.c_void_p))
     iters = [dict(trX=its[k].trX, trS=its[k].trS, e=its[k].e, fnorm=its[k].fnorm,
                   branch="SQUARE" if its[k].branch == 0 else "EXPAND", width=its[k].width,
-                  required=its[k].required, products=its[k].products)
+                  required=its[k].required, products=its[k].products,
+                  frob2=its[k].frob2)
              for k in range(min(rep.iterations, o.max_iter))]
     return SP2Result(rc, D, rep.iterations, STOP_NAMES.get(rep.stop_reason, "?"), rep.final_width,
                      rep.regrows, rep.emin, rep.emax, rep.trD, rep.overflow_rows, rep.required_width,

@@ -17,6 +17,7 @@
  *  - fnorm_diff                                              §8c-c11
  *  - gershgorin                                              §8c-c8
  *  - sp2 (init + loop + stop rule)                           §8c-c9,c10
+ *  - sp2 trace-closest branch rule (option)                  §8f-f4 (i); P:L52 (Niklasson 2002)
  *
  * Floating point: IEEE binary64, round-to-nearest-even. Every product-sum is
  * the explicit C99 fma() of the definition; the file is compiled with
@@ -402,6 +403,7 @@ typedef struct {
     int32_t on_overflow;/* 0 FAIL, 1 GROW */
     int32_t max_width;  /* <= 0 -> n */
     int32_t initial_width; /* <= 0 -> H.w */
+    int32_t branch_rule;   /* 0 trace sign (default), 1 trace-closest (§8f-f4 i) */
 } osp2_opts;
 
 typedef struct {
@@ -411,6 +413,7 @@ typedef struct {
     int32_t required; /* max kept count of X_{n+1} */
     int32_t pad;
     int64_t products;
+    double frob2;     /* branch_rule 1: T2_n (see sp2_frob2), else 0 */
 } osp2_iter;
 
 typedef struct {
@@ -486,6 +489,25 @@ static int sp2_step(const omat* X, omat* Y, int branch, double tau, double* ds, 
     return O_OK;
 }
 
+/*
+ * Trace-closest branch rule (§8f-f4 (i), Niklasson 2002 SP2; reading R19):
+ * SQUARE iff tr(X_n^2) is closer to nocc than tr(2X_n - X_n^2) = 2 tr(X_n) - tr(X_n^2).
+ * tr(X^2) must be known BEFORE the fused step, so it is taken from X_n itself:
+ * for symmetric X (every SP2 iterate of a symmetric H, P4) tr(X^2) = sum_ij x_ij x_ji
+ * = sum_ij x_ij^2. T2 = canonical sum (c7) of q_i, q_i = fma chain over the stored
+ * slots of row i in ascending order, q <- fma(x, x, q) from +0.
+ * Decision: |T2 - nocc| < |(2 trX - T2) - nocc| -> SQUARE, else EXPAND (tie -> EXPAND).
+ */
+static double sp2_frob2(const omat* X, double* q) {
+    for (int64_t i = 0; i < X->n; ++i) {
+        const double* v = X->val + (size_t)i * X->w;
+        double s = 0.0;
+        for (int32_t p = 0; p < X->nnz[i]; ++p) s = fma(v[p], v[p], s);
+        q[i] = s;
+    }
+    return oracle_canonical_sum(q, X->n);
+}
+
 static int mat_alloc(omat* M, int64_t n, int32_t w) {
     M->n = n; M->w = w;
     M->val = (double*)calloc((size_t)n * (size_t)w, sizeof(double));
@@ -500,7 +522,8 @@ static void mat_free(omat* M) { free(M->val); free(M->col); free(M->nnz); M->val
  *  init : (emin, emax) <- Gershgorin (or opts); D = emax - emin; D <= 0 or non-finite -> BOUNDS;
  *         alpha = -1/D, beta = emax/D; X0 = scale_add_identity(H, alpha, beta, tau); trX0 canonical.
  *  loop n = 0, 1, ...:
- *    (i)   b_n = SQUARE if trX_n > nocc else EXPAND (tie -> EXPAND)
+ *    (i)   b_n = SQUARE if trX_n > nocc else EXPAND (tie -> EXPAND); with branch_rule 1 the
+ *          trace-closest rule of sp2_frob2 instead
  *    (ii)  S_n = X_n X_n (pre-drop); trS_n canonical
  *    (iii) X_{n+1} = drop(S_n) | drop(fma(2, x, -s)) over the union
  *    (iv)  overflow -> FAIL: return OVERFLOW(n) | GROW: width <- round_up32(required) (<= max_width)
@@ -566,6 +589,11 @@ int oracle_sp2(const omat* H, int64_t nocc, double tol, const osp2_opts* o, omat
     int32_t it;
     for (it = 0; it < o->max_iter; ++it) {
         int branch = (trX > (double)nocc) ? 0 : 1;
+        double t2 = 0.0;
+        if (o->branch_rule == 1) {
+            t2 = sp2_frob2(&X, nr);
+            branch = (fabs(t2 - (double)nocc) < fabs((2.0 * trX - t2) - (double)nocc)) ? 0 : 1;
+        }
         if (mat_alloc(&Y, n, wy)) { status = O_NOMEM; break; }
         int64_t prod = 0;
         sp2_step(&X, &Y, branch, tau, ds, dy, nr, &ovf, &req, &prod);
@@ -589,6 +617,7 @@ int oracle_sp2(const omat* H, int64_t nocc, double tol, const osp2_opts* o, omat
             iters[it].trX = trX; iters[it].trS = trS; iters[it].e = e; iters[it].fnorm = fn;
             iters[it].branch = branch; iters[it].width = wy; iters[it].required = req;
             iters[it].products = prod;
+            iters[it].frob2 = t2;
         }
         mat_free(&X);
         X = Y;

@@ -28,6 +28,7 @@ _HDRS = [os.path.join(_HERE, "csrc", "internal.cuh"), os.path.join(_REPO, "inclu
 OK, ERR_ARG, ERR_DIM, ERR_OVERFLOW, ERR_BOUNDS, ERR_NOCONV, ERR_NOMEM, ERR_CUDA, ERR_NCCL, ERR_STATE = range(10)
 OPT_WINDOW, OPT_WARPS, OPT_SP2_WIDTH0, OPT_PROFILE, OPT_ABLATE, OPT_GENERAL_WINDOW = 1, 2, 3, 4, 5, 6
 SP2_FAIL, SP2_GROW = 0, 1
+SP2_RULE_TRACE_SIGN, SP2_RULE_TRACE_CLOSEST = 0, 1
 STOP_NAMES = {0: "CONVERGED", 1: "STAGNATED", 2: "NOCONV", 3: "OVERFLOW"}
 
 # Every symbol include/ellpack.h declares (checked by tests/test_abi.py).
@@ -77,13 +78,14 @@ class SP2Opts(ctypes.Structure):
     _fields_ = [("threshold", ctypes.c_double), ("max_iter", ctypes.c_int32), ("min_iter", ctypes.c_int32),
                 ("stag_gate", ctypes.c_double), ("emin", ctypes.c_double), ("emax", ctypes.c_double),
                 ("on_overflow", ctypes.c_int32), ("max_width", ctypes.c_int32),
-                ("initial_width", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("initial_width", ctypes.c_int32), ("branch_rule", ctypes.c_int32)]
 
 
 class SP2IterRec(ctypes.Structure):
     _fields_ = [("trX", ctypes.c_double), ("trS", ctypes.c_double), ("e", ctypes.c_double),
                 ("fnorm", ctypes.c_double), ("branch", ctypes.c_int32), ("width", ctypes.c_int32),
-                ("required", ctypes.c_int32), ("reserved", ctypes.c_int32), ("products", ctypes.c_int64)]
+                ("required", ctypes.c_int32), ("reserved", ctypes.c_int32), ("products", ctypes.c_int64),
+                ("frob2", ctypes.c_double)]
 
 
 class SP2Report(ctypes.Structure):
@@ -300,7 +302,7 @@ class Context:
 
     def sp2_run(self, h: Mat, nocc: int, tol: float, d: Mat, threshold: float = 0.0, max_iter: int = 100,
                 min_iter: int = 20, stag_gate: float = 1e-3, bounds=None, on_overflow: int = SP2_GROW,
-                max_width: int = 0, initial_width: int = 0,
+                max_width: int = 0, initial_width: int = 0, branch_rule: int = 0,
                 ok=(OK, ERR_NOCONV, ERR_OVERFLOW)) -> SP2Result:
         o = SP2Opts()
         lib().sp2_opts_default(ctypes.byref(o))
@@ -308,6 +310,7 @@ class Context:
         if bounds is not None:
             o.emin, o.emax = bounds
         o.on_overflow, o.max_width, o.initial_width = on_overflow, max_width, initial_width
+        o.branch_rule = branch_rule
         recs = (SP2IterRec * max(1, max_iter))()
         rep = SP2Report()
         rep.iters = ctypes.cast(recs, ctypes.POINTER(SP2IterRec))
@@ -316,7 +319,8 @@ class Context:
         n_rec = min(rep.iterations, max_iter)
         iters = [dict(trX=recs[k].trX, trS=recs[k].trS, e=recs[k].e, fnorm=recs[k].fnorm,
                       branch="SQUARE" if recs[k].branch == 0 else "EXPAND", width=recs[k].width,
-                      required=recs[k].required, products=recs[k].products) for k in range(n_rec)]
+                      required=recs[k].required, products=recs[k].products, frob2=recs[k].frob2)
+                 for k in range(n_rec)]
         phases = dict(read_hamiltonian=rep.t_read_hamiltonian, init_misc=rep.t_init_misc,
                       sp2_loop_x2=rep.t_sp2_loop_x2, sp2_loop_norm=rep.t_sp2_loop_norm,
                       sp2_loop_misc=rep.t_sp2_loop_misc)

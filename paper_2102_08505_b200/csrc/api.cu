@@ -878,6 +878,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     sp2_opts o;
     if (opts_in) o = *opts_in; else sp2_opts_default(&o);
     if (!valid_tau(o.threshold) || o.max_iter < 1) return ELLPACK_ERR_ARG;
+    if (o.branch_rule != SP2_RULE_TRACE_SIGN && o.branch_rule != SP2_RULE_TRACE_CLOSEST) return ELLPACK_ERR_ARG;
     CK(cudaSetDevice(c->device));
     sp2_iter_rec* iters = rep ? rep->iters : nullptr;
     sp2_report R;
@@ -932,6 +933,19 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     if ((rc = allgather_desc(c, &X.d))) { cleanup(); return rc; }
     double trX;
     if ((rc = ellpack_trace(c, &X.d, &trX))) { cleanup(); return rc; }
+    // trace-closest rule (SP2_RULE_TRACE_CLOSEST): T2 of X0 here, of X_{n+1} after step n
+    const bool closest = o.branch_rule == SP2_RULE_TRACE_CLOSEST;
+    double t2 = 0.0;
+    RK(grow(c, c->rows[3], sizeof(double) * n));
+    if (closest) {
+        CK(launch_sumsq_rows(kmat(&X.d), r0, r1, (double*)c->rows[3].p, c->stream));
+        c->launches++;
+        const double* arrs[1] = {(const double*)c->rows[3].p};
+        if ((rc = enqueue_canonical(c, arrs, 1, n))) { cleanup(); return rc; }
+        CK(cudaMemsetAsync(c->d_status, 0, 8, c->stream));
+        if ((rc = fetch(c, 1))) { cleanup(); return rc; }
+        t2 = c->h->sums[0];
+    }
     const double t_init_end = now_s();
 
     // ---- SP2 loop
@@ -954,7 +968,10 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     int stop = -1;
     int it;
     for (it = 0; it < o.max_iter; ++it) {
-        const int branch = (trX > (double)nocc) ? SP2_SQUARE : SP2_EXPAND;
+        int branch = (trX > (double)nocc) ? SP2_SQUARE : SP2_EXPAND;
+        if (closest)  // (same expression as the oracle: tie -> EXPAND)
+            branch = (std::fabs(t2 - (double)nocc) < std::fabs((2.0 * trX - t2) - (double)nocc)) ? SP2_SQUARE
+                                                                                                : SP2_EXPAND;
         if (!Y.owned || Y.d.w < wy) {
             if ((rc = dm_alloc(c, Y, n, wcap > wy ? wcap : wy))) { status = rc; break; }
         }
@@ -990,10 +1007,16 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             if ((rc = enqueue_row_op(c, p, n))) { status = rc; break; }
             cudaEventRecord(c->ev[1], c->stream);
             if ((rc = reduce_status(c))) { status = rc; break; }
-            const double* arrs[3] = {p.diag_s, p.diag_c, p.normsq};
-            if ((rc = enqueue_canonical(c, arrs, 3, n))) { status = rc; break; }
+            if (closest) {
+                // T2 of X_{n+1} (this rank's rows), summed with this step's traces
+                CK(launch_sumsq_rows(kmat(&Y.d), r0, r1, (double*)c->rows[3].p, c->stream));
+                c->launches++;
+            }
+            const double* arrs[4] = {p.diag_s, p.diag_c, p.normsq, (const double*)c->rows[3].p};
+            const int narr = closest ? 4 : 3;
+            if ((rc = enqueue_canonical(c, arrs, narr, n))) { status = rc; break; }
             cudaEventRecord(c->ev[2], c->stream);
-            if ((rc = fetch(c, 3))) { status = rc; break; }
+            if ((rc = fetch(c, narr))) { status = rc; break; }
             float ms1 = 0.f, ms2 = 0.f;
             cudaEventElapsedTime(&ms1, c->ev[0], c->ev[1]);
             cudaEventElapsedTime(&ms2, c->ev[1], c->ev[2]);
@@ -1044,7 +1067,9 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             iters[it].required = kept_max;
             iters[it].reserved = 0;
             iters[it].products = (int64_t)c->h->keys[0];  // landed with the status fetch
+            iters[it].frob2 = t2;
         }
+        if (closest) t2 = c->h->sums[3];
         if ((rc = allgather_desc(c, &Y.d))) { status = rc; break; }
         std::swap(X, Y);
         wx = wy;

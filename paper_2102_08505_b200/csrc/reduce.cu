@@ -164,6 +164,27 @@ cudaError_t launch_fnorm_rows(KMat a, KMat b, int64_t r0, int64_t r1, double* ou
     return cudaGetLastError();
 }
 
+// q_i = fma chain over the stored slots of row i, ascending, q <- fma(x, x, q) from +0
+// (the T2 of the trace-closest SP2 branch rule, include/ellpack.h SP2_RULE_TRACE_CLOSEST).
+// One thread per row: the chain order is the definition. Consecutive threads read consecutive
+// rows, so every 128-byte line a warp touches is reused by the next slots from L1.
+__global__ void sumsq_rows_kernel(KMat a, int64_t r0, int64_t r1, double* out) {
+    const int64_t i = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= r1) return;
+    const double* v = a.val + (size_t)i * a.w;
+    const int n = a.nnz[i];
+    double q = 0.0;
+    for (int p = 0; p < n; ++p) q = __fma_rn(v[p], v[p], q);
+    out[i] = q;
+}
+
+cudaError_t launch_sumsq_rows(KMat a, int64_t r0, int64_t r1, double* out, cudaStream_t s) {
+    const int64_t rows = r1 - r0;
+    if (rows <= 0) return cudaSuccess;
+    sumsq_rows_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(a, r0, r1, out);
+    return cudaGetLastError();
+}
+
 __global__ void identity_kernel(int64_t n, KOut id) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;

@@ -331,6 +331,7 @@ def _compare_sp2(g, o):
         assert (a["trX"], a["trS"], a["e"]) == (b["trX"], b["trS"], b["e"])
         assert a["width"] == b["width"] and a["required"] == b["required"]
         assert a["products"] == b["products"]  # scalar-product count of the X^2
+        assert same_bits_scalar(a["frob2"], b["frob2"])  # T2 of the trace-closest rule (0 otherwise)
         assert abs(a["fnorm"] - b["fnorm"]) <= 1e-10 * max(b["fnorm"], 1e-300)
     assert g.trD == o.trD
 
@@ -346,6 +347,35 @@ def test_sp2_iterate_parity(ctx, n, seed, tau):
     if tau == 0.0:
         D = o.D.to_dense()
         assert np.linalg.norm(D @ D - D) < 1e-8 and abs(np.trace(D) - n // 2) < 1e-8
+
+
+def same_bits_scalar(a, b):
+    return np.float64(a).view(np.uint64) == np.float64(b).view(np.uint64)
+
+
+@pytest.mark.parametrize("n,seed,tau,shrink", [(48, 0, 0.0, 0.05), (640, 7, 0.0, 0.05), (1024, 8, 1e-6, 0.03),
+                                               (512, 3, 1e-7, 0.0)])
+def test_sp2_trace_closest_rule_parity(ctx, n, seed, tau, shrink):
+    """§8f-f4 (i): the trace-closest branch rule (T2 from X_n, R19), bounds `shrink` inside the
+    spectrum so the rule departs from the trace-sign rule; bitwise against the oracle."""
+    if n == 48:
+        h = np.sort(np.random.default_rng(14).uniform(-2, 2, n))
+        H = synth.from_dense(np.diag(h), w=2)
+        nocc = 5
+    else:
+        H = synth.sym_banded(n, 32, 6, 12, 1, -1.0, 1.0, 0, 4.0, 0.0, seed)
+        nocc = n // 2 - 5
+    lo, hi = oracle.gershgorin(H)
+    if shrink:
+        lo, hi = lo + shrink * (hi - lo), hi - shrink * (hi - lo)
+    o = oracle.sp2(H, nocc, 1e-10, oracle.SP2Opts(threshold=tau, max_iter=100, emin=lo, emax=hi, branch_rule=1),
+                   d_width=n)
+    d = eb().Mat.empty(n, n)
+    g = ctx.sp2_run(up(H), nocc, 1e-10, d, threshold=tau, max_iter=100, bounds=(lo, hi),
+                    branch_rule=eb().SP2_RULE_TRACE_CLOSEST)
+    _compare_sp2(g, o)
+    assert all(it["frob2"] != 0.0 for it in g.iters)
+    assert same_bits(d.to_host(), o.D)
 
 
 def test_sp2_grow_fault_injection(ellpack_lib):

@@ -340,6 +340,80 @@ def test_p13_small_random_vs_eigh_projector(n, seed):
         assert it["e"] > -1e-12
 
 
+# ------------------------------------------- SP2 trace-closest rule (§8f-f4 i, R19)
+
+def test_p14_trace_closest_rule_diagonal_scalar_recursion():
+    """Diagonal H with spectral bounds 5% inside the spectrum, so X0 has levels outside [0, 1]:
+    every iterate is diagonal, T2 = sum x_i^2 = tr(X_n^2) exactly, and the rule is replayed in
+    60-digit arithmetic from the scalar maps alone. Here the trace-sign rule diverges while the
+    trace-closest rule recovers the projector (the point of the rule)."""
+    rng = np.random.default_rng(14)
+    n = 48
+    h = np.sort(rng.uniform(-2, 2, n))
+    H = from_dense(np.diag(h), w=2)
+    nocc = 5
+    lo, hi = h.min() + 0.05 * np.ptp(h), h.max() - 0.05 * np.ptp(h)
+    r = oracle.sp2(H, nocc, 1e-10, oracle.SP2Opts(max_iter=80, emin=lo, emax=hi, branch_rule=1))
+    assert r.stop == "CONVERGED"
+    decimal.getcontext().prec = 60
+    x = [(D_(hi) - D_(hv)) / (D_(hi) - D_(lo)) for hv in h]
+    assert min(x) < 0 and max(x) > 1
+    branches = [it["branch"] for it in r.iters]
+    differs = 0
+    for k, it in enumerate(r.iters):
+        tr1, tr2 = sum(x), sum(xi * xi for xi in x)
+        # T2 is tr(X_n^2) (binary64 rounding of the exact value)
+        assert abs(it["frob2"] - float(tr2)) <= 1e-12 * max(1.0, float(tr2))
+        sq, ex = abs(tr2 - nocc), abs(2 * tr1 - tr2 - nocc)
+        if abs(sq - ex) > D_("1e-9"):
+            assert (branches[k] == "SQUARE") == (sq < ex), k
+        differs += (branches[k] == "SQUARE") != (tr1 > nocc)
+        x = [xi * xi if branches[k] == "SQUARE" else 2 * xi - xi * xi for xi in x]
+    assert differs >= 1
+    got = r.D.to_dense().diagonal()
+    assert max(abs(float(e) - g) for e, g in zip(x, got)) <= 1e-10
+    assert np.max(np.abs(got - (np.arange(n) < nocc))) <= 1e-6
+    r0 = oracle.sp2(H, nocc, 1e-10, oracle.SP2Opts(max_iter=80, emin=lo, emax=hi))
+    assert r0.stop != "CONVERGED" or abs(r0.trD - nocc) > 1e-6
+
+
+def test_p14b_rules_coincide_inside_unit_interval():
+    """0 <= T2 <= T1 (levels in [0, 1], true bounds): |T2 - nocc| < |2 T1 - T2 - nocc| iff
+    T1 > nocc, so both rules take the same branches and give the same bits."""
+    for seed in (1, 2):
+        H = synth.sym_banded(128, 128, 6, 12, 1, -1.0, 1.0, 0, 4.0, 0.0, seed)
+        r0 = oracle.sp2(H, 61, 1e-10, oracle.SP2Opts(max_iter=100))
+        r1 = oracle.sp2(H, 61, 1e-10, oracle.SP2Opts(max_iter=100, branch_rule=1))
+        assert [it["branch"] for it in r0.iters] == [it["branch"] for it in r1.iters]
+        assert np.array_equal(r0.D.val.view(np.uint64), r1.D.val.view(np.uint64))
+
+
+@pytest.mark.parametrize("n,seed", [(64, 1), (192, 4)])
+def test_p15_trace_closest_rule_random_vs_eigh_projector(n, seed):
+    """Symmetric banded H: T2 (Frobenius of X_n) agrees with tr(X_n^2) taken from the product's
+    diagonal (an independent computation) to rounding, each branch is the trace-closest one, and
+    the limit is the eigh projector."""
+    H = synth.sym_banded(n, n, 6, 12, 1, -1.0, 1.0, 0, 4.0, 0.0, seed)
+    d = H.to_dense()
+    ev, Q = np.linalg.eigh(d)
+    nocc = n // 2 - 3
+    assert ev[nocc] - ev[nocc - 1] > 1e-3, "fixture must be gapped"
+    r = oracle.sp2(H, nocc, 1e-10, oracle.SP2Opts(max_iter=100, branch_rule=1))
+    assert r.status == oracle.OK and r.stop in ("CONVERGED", "STAGNATED")
+    for it in r.iters:
+        assert abs(it["frob2"] - it["trS"]) <= 1e-12 * max(1.0, abs(it["trS"]))
+        sq, ex = abs(it["trS"] - nocc), abs(2 * it["trX"] - it["trS"] - nocc)
+        if abs(sq - ex) > 1e-8:
+            assert (it["branch"] == "SQUARE") == (sq < ex)
+    D = r.D.to_dense()
+    Dx = Q[:, :nocc] @ Q[:, :nocc].T
+    assert np.linalg.norm(D @ D - D) < 1e-8 and abs(np.trace(D) - nocc) < 1e-8
+    assert np.linalg.norm(D - Dx) / np.linalg.norm(Dx) < 1e-6
+    # default rule: frob2 stays 0 (not computed)
+    r0 = oracle.sp2(H, nocc, 1e-10, oracle.SP2Opts(max_iter=100))
+    assert all(it["frob2"] == 0.0 for it in r0.iters)
+
+
 def test_sp2_overflow_fail_and_grow_widths():
     H = synth.cfg3(n=2048, m=64)
     opts = oracle.SP2Opts(threshold=1e-5, max_iter=3, on_overflow=0)
