@@ -173,22 +173,27 @@ __host__ __device__ inline size_t warp_smem_bytes(int S, bool has_old, bool fast
 // bt_nbin[k] = NB: group g holds entries iff NB > 4 g.
 __global__ void balance_kernel(KMat b, int64_t n, int wt, int S, unsigned char* __restrict__ bt,
                                int32_t* __restrict__ bt_nbin) {
-    __shared__ int hist_s[8][16];  // per warp: entries per residue (256-thread blocks)
+    __shared__ int hist_s[8][16];        // per warp: entries per residue (256-thread blocks)
+    __shared__ unsigned bmask_s[8][16];  // per warp and bin: residues of its real entries
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     int* hist = hist_s[threadIdx.x >> 5];
+    unsigned* bmask = bmask_s[threadIdx.x >> 5];
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const double invS = 1.0 / (double)S;
     for (int64_t k = w0; k < n; k += nw) {
         const int nb = b.nnz[k];  // <= 256 on the fast path (8 chunks)
-        const int NB = (nb + 15) >> 4;
+        // bins: every bin of the 64-entry groups a step loads anyway (4 ceil(nb / 64), not
+        // ceil(nb / 16)), so the entries of a residue class spread over more bins: fewer
+        // same-bank pairs in a half-instruction at no extra instruction or load
+        const int NB = 4 * ((nb + 63) >> 6);
         const int32_t* __restrict__ bc = b.col + (size_t)k * b.w;
         const double* __restrict__ bv = b.val + (size_t)k * b.w;
         int32_t* __restrict__ oo = reinterpret_cast<int32_t*>(bt + (size_t)k * 12 * wt);
         double* __restrict__ ov = reinterpret_cast<double*>(bt + (size_t)k * 12 * wt + 4 * (size_t)wt);
         if (lane == 0) bt_nbin[k] = NB;
-        if (lane < 16) hist[lane] = 0;
+        if (lane < 16) { hist[lane] = 0; bmask[lane] = 0u; }
         __syncwarp();
         // rank within residue (stable: chunk order, then lane order): one match per chunk
         int jr[8], rk[8];
@@ -233,20 +238,24 @@ __global__ void balance_kernel(KMat b, int64_t n, int wt, int S, unsigned char* 
                     js -= js >= S ? S : 0;
                     oo[sl] = 8 * js;
                     ov[sl] = __ldg(bv + 32 * c + lane);
+                    atomicOr(&bmask[bin], 1u << (js & 15));  // bank pair of the slot
                 }
             }
         }
-        // padding: bin b holds fill_b = ceil((nb - b) / NB) entries at positions 0..fill_b-1; the
-        // positions fill_b..15 of the bins of used groups get trash slot S + m (distinct residues
-        // among the padding lanes of a bin; padding is rare: at most one position per bin of a
-        // used group, plus the unused bins of the last group)
+        __syncwarp();
+        // padding: bin b holds fill_b = ceil((nb - b) / NB) entries at positions 0..fill_b-1;
+        // positions fill_b..15 get trash slots S + r, r distinct and unused by the bin's entries
         const int nbins = 4 * ((NB + 3) >> 2);
         for (int t = lane; t < nbins * 16; t += 32) {
             const int bb = t >> 4, m = t & 15;
             const int fill = bb < NB ? (nb - bb + NB - 1) / NB : 0;
             if (m >= fill) {
                 const int sl = 64 * (bb >> 2) + 2 * (16 * ((bb >> 1) & 1) + m) + (bb & 1);
-                oo[sl] = 8 * (S + m);
+                // the (m - fill)-th residue no real entry of the bin uses (16 - distinct residues
+                // >= the bin's padding positions), so padding lanes add no same-bank pair
+                unsigned f = ~bmask[bb] & 0xffffu;
+                for (int q = m - fill; q > 0; --q) f &= f - 1u;
+                oo[sl] = 8 * (S + ((__ffs(f) - 1 - S) & 15));
                 ov[sl] = 0.0;
             }
         }
