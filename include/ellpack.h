@@ -101,7 +101,8 @@ int ellpack_ctx_set_stream(ellpack_ctx ctx, void* stream);
  *  ELLPACK_OPT_ABLATE      timing experiments only, results are WRONG when set (bit mask):
  *                          1 = the ring kernel skips its output-row stores, 2 = its
  *                          accumulator updates, 4 = its B gathers, 8 = its emission.
- *                          0 = off (default).
+ *                          0 = off (default). Only builds with -DELL_ABLATE=1 accept a
+ *                          nonzero mask (ELLPACK_ERR_ARG otherwise).
  *  ELLPACK_OPT_GENERAL_WINDOW  window (doubles, multiple of 32) of the general path that
  *                          wide rows (dense SP2 iterates) use; 0 = automatic (1024). */
 enum { ELLPACK_OPT_WINDOW = 1, ELLPACK_OPT_WARPS = 2, ELLPACK_OPT_SP2_WIDTH0 = 3, ELLPACK_OPT_PROFILE = 4,

@@ -47,15 +47,16 @@ def _nccl_include() -> str:
     return os.path.join(list(nvidia.nccl.__path__)[0], "include")
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """nvcc -gencode arch=compute_100a,code=sm_100a -> libellpack.so (in-tree)."""
-    stale = force or not os.path.exists(_LIB) or any(
+def build(force: bool = False, verbose: bool = False, defines=()) -> str:
+    """nvcc -gencode arch=compute_100a,code=sm_100a -> libellpack.so (in-tree).
+    defines: extra -D tuning macros (tools/variants.py A/B builds only)."""
+    stale = force or defines or not os.path.exists(_LIB) or any(
         os.path.getmtime(s) > os.path.getmtime(_LIB) for s in _SRCS + _HDRS)
     if stale:
         tmp = _LIB + f".tmp{os.getpid()}"
         cmd = ["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
                "-Xcompiler", "-fPIC", "-shared", "-I" + os.path.join(_REPO, "include"),
-               "-I" + _nccl_include(), *_SRCS, "-o", tmp, "-ldl"]
+               "-I" + _nccl_include(), *[f"-D{d}" for d in defines], *_SRCS, "-o", tmp, "-ldl"]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.check_call(cmd, cwd=_HERE)

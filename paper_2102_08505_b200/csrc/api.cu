@@ -501,7 +501,13 @@ int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
         case ELLPACK_OPT_WINDOW: c->window_opt = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_WARPS: c->warps_opt = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_SP2_WIDTH0: c->sp2_width0 = (int)v; return ELLPACK_OK;
-        case ELLPACK_OPT_ABLATE: c->ablate = (int)v; return ELLPACK_OK;
+        case ELLPACK_OPT_ABLATE:
+#if defined(ELL_ABLATE) && ELL_ABLATE
+            c->ablate = (int)v;
+            return ELLPACK_OK;
+#else
+            return v == 0 ? ELLPACK_OK : ELLPACK_ERR_ARG;  // experiments not compiled in
+#endif
         case ELLPACK_OPT_GENERAL_WINDOW:
             if (v < 0 || v > kFastWindowMax || (v & 31)) return ELLPACK_ERR_ARG;
             c->general_s = (int)v;

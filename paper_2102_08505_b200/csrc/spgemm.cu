@@ -42,6 +42,11 @@ constexpr int kStage = 64;  // general path: A-row entries staged per piece (64:
 #define ELL_STAGE_F 128  // fast path: stage entries (16 B each); 128 measured best vs 64, 96
 #endif
 constexpr int kStageF = ELL_STAGE_F;
+#ifndef ELL_ABLATE
+#define ELL_ABLATE 0  // 1: compile the ELLPACK_OPT_ABLATE timing experiments into the ring kernel
+#endif
+// ablation bit b requested (always false in normal builds: no parameter read on the hot path)
+#define ABL(p, b) (ELL_ABLATE && ((p).ablate & (b)))
 #ifndef ELL_META_REGS
 #define ELL_META_REGS 1  // fast path: keep step metadata in registers from the burst
 #endif
@@ -622,7 +627,7 @@ __device__ __forceinline__ void ring_emit_block(const RowOpParams& p, const Warp
     const int cw = p.C.w;
     const uint64_t bv = opaque_u64((uint64_t)crow_v), bc = opaque_u64((uint64_t)crow_c);
     // the width test is needed only when this block can reach the row's end (overflow rows)
-    const bool room = kept + 32 * NCH <= cw && !(p.ablate & 1);
+    const bool room = kept + 32 * NCH <= cw && !ABL(p, 1);
     int before = kept;
     const int col0 = F + lane;
 #pragma unroll
@@ -630,7 +635,7 @@ __device__ __forceinline__ void ring_emit_block(const RowOpParams& p, const Warp
         const bool keep = (m[c] >> lane) & 1u;
         const uint32_t pos = (uint32_t)before + (uint32_t)__popc(m[c] & lt);
         const int col = col0 + 32 * c;
-        st_entry(keep && (room || (pos < (uint32_t)cw && !(p.ablate & 1))), reinterpret_cast<double*>(bv + 8ull * pos),
+        st_entry(keep && (room || (pos < (uint32_t)cw && !ABL(p, 1))), reinterpret_cast<double*>(bv + 8ull * pos),
                  reinterpret_cast<int32_t*>(bc + 4ull * pos), x[c], col);
         if (MODE != 0 && (int64_t)col == i) dc = keep ? x[c] : 0.0;
         before += __popc(m[c]);
@@ -666,7 +671,7 @@ __device__ __forceinline__ void ring_emit_range(const RowOpParams& p, const Warp
                                                 const double* o_val, int nOld, int& old_cur,
                                                 double* __restrict__ crow_v, int32_t* __restrict__ crow_c,
                                                 int& kept, double& ds, double& dc, double& nrm) {
-    if (p.ablate & 8) {  // timing experiment: no emission work at all
+    if (ABL(p, 8)) {  // timing experiment: no emission work at all
         while (F < Fto) {
             F += 32;
             if (F - baseF >= p.S) baseF += p.S;
@@ -735,20 +740,28 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
     double am[2][HB];  // per-step metadata of each register half (read once, by the burst)
     int km[2][HB], nbm[2][HB];
 #endif
-    // burst: the gathers of half h into register half X (stage metadata a, k, nb)
+#if ELL_META_REGS
+    // the stage metadata (a, k, nb) of half h into register half X: read at the top of the
+    // previous half so the shared-load latency overlaps its touch wait
+    auto meta = [&](auto Xc, int h) {
+        constexpr int X = decltype(Xc)::value;
+#pragma unroll
+        for (int e = 0; e < HB; ++e) stage_fast_get(w, h * HB + e, am[X][e], km[X][e], nbm[X][e]);
+    };
+#endif
+    // burst: the gathers of half h into register half X
     auto burst = [&](auto Xc, int h) {
         constexpr int X = decltype(Xc)::value;
 #pragma unroll
         for (int e = 0; e < HB; ++e) {
 #if ELL_META_REGS
-            stage_fast_get(w, h * HB + e, am[X][e], km[X][e], nbm[X][e]);
-            const int nb = (p.ablate & 4) ? 0 : nbm[X][e];
+            const int nb = ABL(p, 4) ? 0 : nbm[X][e];
             const unsigned char* __restrict__ rp = btl + (size_t)(uint32_t)km[X][e] * RS;
 #else
             double a_u;
             int k_u, nb_u;
             stage_fast_get(w, h * HB + e, a_u, k_u, nb_u);
-            const int nb = (p.ablate & 4) ? 0 : nb_u;
+            const int nb = ABL(p, 4) ? 0 : nb_u;
             const unsigned char* __restrict__ rp = btl + (size_t)(uint32_t)k_u * RS;
 #endif
             const unsigned char* __restrict__ vp = rp + 8 * lane;
@@ -768,7 +781,7 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
         bool gl[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            gl[g] = nb > 4 * g && !(p.ablate & 2);  // warp-uniform: group holds entries
+            gl[g] = nb > 4 * g && !ABL(p, 2);  // warp-uniform: group holds entries
             old[g][0] = lds64_if(gl[g], acc + (uint32_t)ro[X][e][g].x);
             old[g][1] = lds64_if(gl[g], acc + (uint32_t)ro[X][e][g].y);
         }
@@ -792,6 +805,9 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
         int k_[HB], nb_[HB];
 #pragma unroll
         for (int e = 0; e < HB; ++e) stage_fast_get(w, h * HB + e, a_[e], k_[e], nb_[e]);
+#endif
+#if ELL_META_REGS
+        meta(std::integral_constant<int, X ^ 1>{}, h + 1);
 #endif
         // touch this half's burst: the store waits for it (and for nothing younger)
         if (nb_[0] > 0) sts32i(acc + 8u * (uint32_t)S, ro[X][0][0].x);
@@ -836,6 +852,9 @@ __device__ __forceinline__ void row_ring(const RowOpParams& p, const WarpSmem& w
                          "l"(__double_as_longlong(a)), "l"(knb) : "memory");
         }
         __syncwarp();
+#if ELL_META_REGS
+        meta(std::integral_constant<int, 0>{}, 0);
+#endif
         burst(std::integral_constant<int, 0>{}, 0);
         for (int h = 0; h < nh; h += 2) {
             half(std::integral_constant<int, 0>{}, h);
