@@ -35,6 +35,9 @@
 namespace ell {
 
 constexpr int kStage = 64;  // general path: A-row entries staged per piece (64: 20 warps/SM at S = 1024)
+#ifndef ELL_SEG_PIPE
+#define ELL_SEG_PIPE 1  // general path: software-pipelined rounds (accumulate_pipe)
+#endif
 #ifndef ELL_SEG_U
 #define ELL_SEG_U 4  // general path: gathers per lane per round
 #endif
@@ -380,6 +383,67 @@ __device__ __forceinline__ void accumulate_seg(const RowOpParams& p, const WarpS
         }
         __syncwarp();
     }
+}
+
+// Software-pipelined variant: the segments' rounds (U * 32 entries of one B row each) form one
+// sequence; round r + 1's gathers are issued before round r's updates, into the other of two
+// register sets. ptxas gives every gather the same scoreboard and a consumer waits for the
+// youngest, so round r's registers are first touched (a store to the trash slot, issued while
+// nothing younger is in flight), then round r + 1 is issued, then round r's updates run on
+// ready registers. Rounds of consecutive segments stay in program order (the accumulator RAW).
+template <int U>
+__device__ __forceinline__ void accumulate_pipe(const RowOpParams& p, const WarpSmem& w, int lane, int cnt, int c0) {
+    if (cnt <= 0) return;
+    const int32_t* __restrict__ bcol = p.B.col;
+    const double* __restrict__ bval = p.B.val;
+    const uint32_t abase = w.acc - 8u * (uint32_t)c0;
+    const uint32_t trash = w.acc + 8u * (uint32_t)p.S;
+    int t = 0;
+    long long bo = stg_boff(w, 0);
+    int e = stg_anb(w, 0), q0 = stg_ast(w, 0);
+    double a = stg_aa(w, 0);
+    int j0[U], j1[U];
+    double v0[U], v1[U];
+    double a0 = a, a1 = 0.0;
+    auto load = [&](int (&j)[U], double (&v)[U]) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int q = q0 + 32 * u + lane;
+            j[u] = q < e ? __ldg(bcol + bo + q) : -1;
+            v[u] = q < e ? __ldg(bval + bo + q) : 0.0;
+        }
+    };
+    auto advance = [&]() -> bool {  // cursor to the next round; false past the last segment
+        q0 += 32 * U;
+        if (q0 < e) return true;
+        if (++t >= cnt) return false;
+        bo = stg_boff(w, t);
+        e = stg_anb(w, t);
+        q0 = stg_ast(w, t);
+        a = stg_aa(w, t);
+        return true;
+    };
+    auto update = [&](const int (&j)[U], const double (&v)[U], double aa) {
+        double x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = lds64_if(j[u] >= 0, abase + 8u * (uint32_t)j[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) sts64_if(j[u] >= 0, abase + 8u * (uint32_t)j[u], __fma_rn(aa, v[u], x[u]));
+    };
+    load(j0, v0);
+    for (;;) {
+        sts32i(trash, j0[0]);  // touch round r (set 0)
+        bool more = advance();
+        if (more) { load(j1, v1); a1 = a; }
+        update(j0, v0, a0);
+        if (!more) break;
+        sts32i(trash, j1[0]);  // touch round r + 1 (set 1)
+        more = advance();
+        if (more) { load(j0, v0); a0 = a; }
+        update(j1, v1, a1);
+        if (!more) break;
+    }
+    __syncwarp();
 }
 
 // Breakpoints of B for windows aligned to multiples of S: bp[k * np + q] = number of entries of
@@ -1093,7 +1157,11 @@ __global__ void __launch_bounds__(128, 1) row_general_kernel(const RowOpParams p
                             ns += __popc(m);
                         }
                         __syncwarp();
+#if ELL_SEG_PIPE
+                        accumulate_pipe<ELL_SEG_U>(p, w, lane, ns, c0);
+#else
                         accumulate_seg<ELL_SEG_U>(p, w, lane, ns, c0);
+#endif
                     }
                     __syncwarp();
                     if ((int64_t)c0 <= i && i < (int64_t)c0 + width) ds = lds64(w.acc + (uint32_t)(i - c0) * 8u);
