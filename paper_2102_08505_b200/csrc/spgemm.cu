@@ -183,10 +183,15 @@ __global__ void balance_kernel(KMat b, int64_t n, int wt, int S, unsigned char* 
                                int32_t* __restrict__ bt_nbin) {
     __shared__ int hist_s[8][16];        // per warp: entries per residue (256-thread blocks)
     __shared__ unsigned bmask_s[8][16];  // per warp and bin: residues of its real entries
+    // per warp: the record is assembled here (scattered slots) and leaves in coalesced 16-byte
+    // stores: int32 slots [256] then f64 values [256] (the used groups' prefixes are copied)
+    __shared__ __align__(16) unsigned char rec_s[8][12 * 256];
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     int* hist = hist_s[threadIdx.x >> 5];
     unsigned* bmask = bmask_s[threadIdx.x >> 5];
+    int32_t* so = reinterpret_cast<int32_t*>(rec_s[threadIdx.x >> 5]);
+    double* sv = reinterpret_cast<double*>(rec_s[threadIdx.x >> 5] + 4 * 256);
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const double invS = 1.0 / (double)S;
@@ -205,10 +210,15 @@ __global__ void balance_kernel(KMat b, int64_t n, int wt, int S, unsigned char* 
         __syncwarp();
         // rank within residue (stable: chunk order, then lane order): one match per chunk
         int jr[8], rk[8];
+        double vr[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             const int q = 32 * c + lane;
             jr[c] = q < nb ? __ldg(bc + q) : -1;
+            vr[c] = q < nb ? __ldg(bv + q) : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
             rk[c] = 0;
             if (32 * c < nb) {  // warp-uniform
                 const int res = jr[c] >= 0 ? (jr[c] & 15) : 16 + lane;  // padding lanes: unique keys
@@ -244,8 +254,8 @@ __global__ void balance_kernel(KMat b, int64_t n, int wt, int S, unsigned char* 
                     int js = j - qs * S;
                     js += js < 0 ? S : 0;
                     js -= js >= S ? S : 0;
-                    oo[sl] = 8 * js;
-                    ov[sl] = __ldg(bv + 32 * c + lane);
+                    so[sl] = 8 * js;
+                    sv[sl] = vr[c];
                     atomicOr(&bmask[bin], 1u << (js & 15));  // bank pair of the slot
                 }
             }
@@ -263,10 +273,16 @@ __global__ void balance_kernel(KMat b, int64_t n, int wt, int S, unsigned char* 
                 // >= the bin's padding positions), so padding lanes add no same-bank pair
                 unsigned f = ~bmask[bb] & 0xffffu;
                 for (int q = m - fill; q > 0; --q) f &= f - 1u;
-                oo[sl] = 8 * (S + ((__ffs(f) - 1 - S) & 15));
-                ov[sl] = 0.0;
+                so[sl] = 8 * (S + ((__ffs(f) - 1 - S) & 15));
+                sv[sl] = 0.0;
             }
         }
+        __syncwarp();
+        const int used = 16 * nbins;  // slots of the used groups (64 per group)
+        for (int t = lane; t < used / 4; t += 32)
+            reinterpret_cast<int4*>(oo)[t] = reinterpret_cast<const int4*>(so)[t];
+        for (int t = lane; t < used / 2; t += 32)
+            reinterpret_cast<int4*>(ov)[t] = reinterpret_cast<const int4*>(sv)[t];
         __syncwarp();
     }
 }
