@@ -182,6 +182,41 @@ def test_multiply_edge_cases_bitwise(ctx, case, alpha, beta, tau):
         assert ctx.overflow_info() == (r.overflow_rows, r.required_width)
 
 
+# Ring fast path with wide B rows: every group count G = 1..4 (B rows up to 256 entries),
+# row lengths straddling the 64-entry group and 16-entry bin boundaries, empty rows, and the
+# Old operand (beta != 0). The half-bandwidth keeps the ring within the fast path's limit.
+FAST = [
+    # (n, w, kmin, kmax, band, p_empty)
+    (2048, 64, 48, 64, 500, 0.02),    # G = 1
+    (2500, 128, 1, 128, 800, 0.05),   # G = 2, ragged
+    (3001, 192, 120, 192, 1200, 0.0),  # G = 3
+    (3000, 256, 180, 256, 1800, 0.01),  # G = 4, bins up to 16
+]
+
+
+@pytest.mark.parametrize("case", FAST, ids=lambda c: f"n{c[0]}w{c[1]}")
+@pytest.mark.parametrize("alpha,beta,tau", [(1.0, 0.0, 0.0), (0.75, -1.5, 1e-3)])
+def test_fast_path_wide_rows_bitwise(ctx, case, alpha, beta, tau):
+    n, w, kmin, kmax, band, pe = case
+    A = synth.random_sparse(n, w, kmin, kmax, band, pe, 1.0, seed=7 * n + 1)
+    B = synth.random_sparse(n, w, kmin, kmax, band, pe, 1.0, seed=7 * n + 2)
+    C0 = synth.random_sparse(n, w, kmin, kmax, band, pe, 1.0, seed=7 * n + 3)
+    lit = oracle.multiply(A, B, C0.widened(w).copy(), alpha, beta, tau)  # literal width -> required
+    wo = max(w, ((lit.required_width + 31) // 32) * 32)
+    Co = C0.widened(wo).copy()
+    r = oracle.multiply(A, B, Co, alpha, beta, tau)
+    assert r.status == oracle.OK
+    g = up(C0.widened(wo))
+    st = ctx.multiply(up(A), up(B), g, alpha, beta, tau)
+    assert st == eb().OK
+    assert same_bits(g.to_host(), Co)
+    # and the literal width reports the oracle's overflow exactly
+    if lit.status != oracle.OK:
+        g2 = up(C0.widened(w))
+        assert ctx.multiply(up(A), up(B), g2, alpha, beta, tau) == eb().ERR_OVERFLOW
+        assert ctx.overflow_info() == (lit.overflow_rows, lit.required_width)
+
+
 @pytest.mark.parametrize("window", [32, 64, 256])
 @pytest.mark.parametrize("beta", [0.0, 0.5])
 def test_multipass_window_and_stash_bitwise(ellpack_lib, window, beta):
