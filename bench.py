@@ -7,7 +7,8 @@ which the north star's ">= 50% of HBM peak" target is stated):
 A "step" = one ellpack_multiply_x2 call (fused row kernel: window pre-pass,
 gather-accumulate, drop/compact/write, trace partials; canonical trace
 reduction; status read-back) -- SURVEY §8a rows a0..a4. With N>1 ranks a step
-is the NCCL all-gather of X's row blocks (BJ north_star (3)) followed by the
+is the band-aware halo exchange of X's rows (NCCL send/recv of exactly the rows
+the rank's own rows reference, §8f-f1; BJ north_star (3)) followed by the
 multiply of the rank's own rows (strong scaling: total work fixed).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -215,7 +216,7 @@ def run_ours(args):
 
     def step():
         if ws > 1:
-            ctx.allgather_rows(x)
+            ctx.halo_rows(x)  # the rows of X this rank's rows reference (band-aware halo, §8f-f1)
         s, tx, tx2 = ctx.multiply_x2(x, y, tau)
         return s, tx, tx2
 

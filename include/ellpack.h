@@ -278,6 +278,26 @@ int ellpack_ctx_set_rows(ellpack_ctx ctx, int64_t row_begin, int64_t row_end);
  * communicator (the B-operand exchange of BJ north_star (3)). No-op without one. */
 int ellpack_allgather_rows(ellpack_ctx ctx, ellpack_desc* m);
 
+/* Band-aware halo exchange, the alternative to the full all-gather when the
+ * operands are banded: the rows [row_begin,row_end) of `a` on this rank reference only the B rows
+ * [lo, hi] (lo = min first column, hi = max last column of those rows), so each rank needs just
+ * those rows of `b`. In place over the attached communicator: every rank's [lo, hi] is
+ * all-gathered (16 bytes per rank), then the rows of the plan below travel by NCCL send/recv
+ * (val, col, nnz). a and b may be the same matrix (X^2, SP2). Rows of b outside this rank's
+ * block and its [lo, hi] are left untouched (not valid for this rank). No-op without a
+ * communicator. Errors: ARG, DIM, CUDA, NCCL. sp2_run uses it between iterations and all-gathers
+ * only the final iterate. */
+int ellpack_halo_rows(ellpack_ctx ctx, const ellpack_desc* a, ellpack_desc* b);
+
+/* The halo plan (host only, no context; the same function both sides of every pair evaluate):
+ * equal contiguous blocks of `per` rows (block q = [q per, min(n, (q+1) per))) and every rank's
+ * referenced rows need[2q] .. need[2q+1] (inclusive; need[2q] > need[2q+1] = none). This rank
+ * sends (peer, row_begin, row_end) = its block ∩ the peer's range, and receives the peer's block
+ * ∩ its own range, peers ascending, into send[3k..3k+2] (k < *n_send) and recv[3k..3k+2]
+ * (k < *n_recv); both arrays hold 3 nranks entries. Errors: ARG. */
+int ellpack_halo_plan(int64_t n, int nranks, int rank, int64_t per, const int64_t* need,
+                      int32_t* n_send, int64_t* send, int32_t* n_recv, int64_t* recv);
+
 const char* ellpack_strerror(int status);
 
 #ifdef __cplusplus

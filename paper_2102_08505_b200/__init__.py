@@ -38,7 +38,8 @@ ABI_SYMBOLS = (
     "ellpack_multiply_x2", "ellpack_add", "ellpack_add_identity", "ellpack_scale_add_identity",
     "ellpack_trace", "ellpack_fnorm_diff", "ellpack_gershgorin", "ellpack_overflow_info", "sp2_run",
     "sp2_opts_default", "ellpack_multiply_x2_host", "ellpack_nccl_unique_id", "ellpack_ctx_attach_nccl",
-    "ellpack_ctx_set_rows", "ellpack_allgather_rows", "ellpack_strerror",
+    "ellpack_ctx_set_rows", "ellpack_allgather_rows", "ellpack_halo_rows", "ellpack_halo_plan",
+    "ellpack_strerror",
 )
 
 
@@ -127,6 +128,7 @@ def lib() -> ctypes.CDLL:
             "ellpack_multiply_x2_host": [P, i64, i32, P, P, P, i32, P, P, P, d, P, P],
             "ellpack_nccl_unique_id": [P], "ellpack_ctx_attach_nccl": [P, i, i, P, i64, i64],
             "ellpack_ctx_set_rows": [P, i64, i64], "ellpack_allgather_rows": [P, D],
+            "ellpack_halo_rows": [P, D, D], "ellpack_halo_plan": [i64, i32, i32, i64, P, P, P, P, P],
             "ellpack_strerror": [i],
         }
         for name, args in sig.items():
@@ -356,6 +358,24 @@ class Context:
 
     def allgather_rows(self, m: Mat):
         _chk(lib().ellpack_allgather_rows(self._h, m.ref()), "ellpack_allgather_rows")
+
+    def halo_rows(self, a: Mat, b: Mat | None = None):
+        """Band-aware halo exchange (f1): the rows of b that this rank's rows of a reference."""
+        _chk(lib().ellpack_halo_rows(self._h, a.ref(), (b or a).ref()), "ellpack_halo_rows")
+
+
+def halo_plan(n: int, nranks: int, rank: int, per: int, need):
+    """ellpack_halo_plan (host only): need = [(lo_q, hi_q)] per rank (inclusive) ->
+    (sends, recvs), lists of (peer, row_begin, row_end)."""
+    import numpy as np
+    nd = np.ascontiguousarray(np.asarray(need, dtype=np.int64).reshape(-1))
+    snd = np.zeros(3 * nranks, np.int64)
+    rcv = np.zeros(3 * nranks, np.int64)
+    ns, nr = ctypes.c_int32(), ctypes.c_int32()
+    _chk(lib().ellpack_halo_plan(n, nranks, rank, per, nd.ctypes.data, ctypes.byref(ns), snd.ctypes.data,
+                                 ctypes.byref(nr), rcv.ctypes.data), "ellpack_halo_plan")
+    return ([tuple(int(x) for x in snd[3 * k:3 * k + 3]) for k in range(ns.value)],
+            [tuple(int(x) for x in rcv[3 * k:3 * k + 3]) for k in range(nr.value)])
 
 
 def row_partition(n: int, nranks: int, align: int = 256):

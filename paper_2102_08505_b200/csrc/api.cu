@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cstdio>
 #include <vector>
 #include <cmath>
@@ -52,6 +53,8 @@ struct NcclApi {
                               cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
 };
 
 NcclApi g_nccl;
@@ -73,6 +76,8 @@ bool load_nccl() {
     LOADSYM(AllReduce, "ncclAllReduce");
     LOADSYM(GroupStart, "ncclGroupStart");
     LOADSYM(GroupEnd, "ncclGroupEnd");
+    LOADSYM(Send, "ncclSend");
+    LOADSYM(Recv, "ncclRecv");
 #undef LOADSYM
     g_nccl.ok = true;
     return true;
@@ -93,7 +98,7 @@ struct ellpack_ctx_s {
     int32_t* d_bw = nullptr;                  // bandwidth probe
     LaunchCfg last_cfg{};
     struct Host {
-        int32_t bw[4];
+        int32_t bw[6];
         int32_t status[2];
         unsigned long long keys[2];
         double sums[8];
@@ -107,6 +112,7 @@ struct ellpack_ctx_s {
     int64_t ident_n = 0;
     Buf hx_val, hx_col, hx_nnz, hy_val, hy_col, hy_nnz;  // host-path device copies
     Buf bt, bt_nbin, bp;
+    Buf halo;  // all ranks' referenced row ranges (halo exchange)
     Buf it[3][3];  // SP2 iterate buffers (val, col, nnz) x 3 slots                         // bank-balanced copy of B (fast path)
     // ring sizing cache: (hB, G, mode) -> (S, rows resident per SM)
     int64_t ring_key = -1;
@@ -226,12 +232,12 @@ int reduce_status(ellpack_ctx c) {
 int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
     p.ncols = n;
     const bool has_old = p.old_mode != 0;
-    CK(cudaMemsetAsync(c->d_bw, 0, 4 * sizeof(int32_t), c->stream));
+    CK(cudaMemsetAsync(c->d_bw, 0, 6 * sizeof(int32_t), c->stream));
     const KMat none{nullptr, nullptr, nullptr, 0};
     CK(launch_bandwidth(p.alpha != 0.0 ? p.A : none, p.B, has_old ? p.Old : none,
                         has_old ? 3 : 2, p.row_begin, p.row_end, n, c->d_bw, c->stream));
     c->launches++;
-    CK(cudaMemcpyAsync(c->h->bw, c->d_bw, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->h->bw, c->d_bw, 6 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     const int64_t hB = c->h->bw[1];
     const int64_t hprod = p.alpha != 0.0 ? (int64_t)c->h->bw[0] + hB : 0;
@@ -294,7 +300,11 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
         const int wt = 64 * (groups < 1 ? 1 : groups);
         RK(grow(c, c->bt, (size_t)12 * n * wt));
         RK(grow(c, c->bt_nbin, sizeof(int32_t) * (size_t)n));
-        CK(launch_balance(p.B, n, wt, p.S, (unsigned char*)c->bt.p, (int32_t*)c->bt_nbin.p, c->num_sms,
+        // only the B rows this launch's A rows reference (a rank's block plus its halo; rows a halo
+        // exchange did not deliver are never read)
+        const int64_t k0 = std::max<int64_t>(0, (int64_t)INT_MAX - c->h->bw[4]);
+        const int64_t k1 = std::min<int64_t>(n, (int64_t)c->h->bw[5]);
+        CK(launch_balance(p.B, k0, k1, wt, p.S, (unsigned char*)c->bt.p, (int32_t*)c->bt_nbin.p, c->num_sms,
                           c->stream));
         c->launches++;
         p.bt = (const unsigned char*)c->bt.p;
@@ -412,6 +422,50 @@ int allgather_desc(ellpack_ctx c, const ellpack_desc* m) {
     return ELLPACK_OK;
 }
 
+// Band-aware halo exchange (§8f-f1): this rank's rows of `a` reference B rows [lo, hi]; the
+// ranges of all ranks are all-gathered (16 bytes each), then every rank sends the part of its own
+// block of `b` each peer reads and receives the parts of the peers' blocks it reads (NCCL
+// point-to-point in one group; the plan is ellpack_halo_plan, identical on both sides of a pair).
+int halo_desc(ellpack_ctx c, const ellpack_desc* a, ellpack_desc* b) {
+    if (!c->comm) return ELLPACK_OK;
+    const int64_t n = b->n;
+    int64_t r0, r1;
+    rows_of(c, n, &r0, &r1);
+    const int P = c->nranks;
+    RK(grow(c, c->halo, sizeof(long long) * 2 * (size_t)P));
+    long long* d_need = (long long*)c->halo.p;
+    long long* mine = d_need + 2 * c->rank;
+    const long long init[2] = {LLONG_MAX, -1};
+    CK(cudaMemcpyAsync(mine, init, sizeof init, cudaMemcpyHostToDevice, c->stream));
+    CK(launch_col_range(kmat(a), r0, r1, mine, c->stream));
+    c->launches++;
+    NK(g_nccl.AllGather(mine, d_need, 2, ncclInt64, c->comm, c->stream));
+    std::vector<long long> need(2 * (size_t)P);
+    CK(cudaMemcpyAsync(need.data(), d_need, sizeof(long long) * 2 * P, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<int64_t> needl(need.begin(), need.end()), snd(3 * (size_t)P), rcv(3 * (size_t)P);
+    int32_t ns = 0, nr = 0;
+    RK(ellpack_halo_plan(n, P, c->rank, r1 - r0, needl.data(), &ns, snd.data(), &nr, rcv.data()));
+    const size_t w = (size_t)b->w;
+    NK(g_nccl.GroupStart());
+    for (int q = 0; q < ns; ++q) {
+        const int peer = (int)snd[3 * q];
+        const size_t s0 = (size_t)snd[3 * q + 1], cnt = (size_t)(snd[3 * q + 2] - snd[3 * q + 1]);
+        NK(g_nccl.Send(b->val + s0 * w, cnt * w, ncclFloat64, peer, c->comm, c->stream));
+        NK(g_nccl.Send(b->col + s0 * w, cnt * w, ncclInt32, peer, c->comm, c->stream));
+        NK(g_nccl.Send(b->nnz + s0, cnt, ncclInt32, peer, c->comm, c->stream));
+    }
+    for (int q = 0; q < nr; ++q) {
+        const int peer = (int)rcv[3 * q];
+        const size_t t0 = (size_t)rcv[3 * q + 1], cnt = (size_t)(rcv[3 * q + 2] - rcv[3 * q + 1]);
+        NK(g_nccl.Recv(b->val + t0 * w, cnt * w, ncclFloat64, peer, c->comm, c->stream));
+        NK(g_nccl.Recv(b->col + t0 * w, cnt * w, ncclInt32, peer, c->comm, c->stream));
+        NK(g_nccl.Recv(b->nnz + t0, cnt, ncclInt32, peer, c->comm, c->stream));
+    }
+    NK(g_nccl.GroupEnd());
+    return ELLPACK_OK;
+}
+
 }  // namespace
 
 // =========================================================================== ABI
@@ -473,7 +527,7 @@ int ellpack_ctx_destroy(ellpack_ctx c) {
     Buf* bufs[] = {&c->rows[0], &c->rows[1], &c->rows[2], &c->rows[3], &c->partials,
                    &c->stash_val, &c->stash_col, &c->ident_val, &c->ident_col, &c->ident_nnz,
                    &c->hx_val, &c->hx_col, &c->hx_nnz, &c->hy_val, &c->hy_col, &c->hy_nnz,
-                   &c->bt, &c->bt_nbin, &c->bp};
+                   &c->bt, &c->bt_nbin, &c->bp, &c->halo};
     for (auto& sl : c->it)
         for (Buf& b : sl) release(c, b);
     for (Buf* b : bufs) release(c, *b);
@@ -758,6 +812,38 @@ int ellpack_allgather_rows(ellpack_ctx c, ellpack_desc* m) {
     return allgather_desc(c, m);
 }
 
+int ellpack_halo_plan(int64_t n, int nranks, int rank, int64_t per, const int64_t* need, int32_t* n_send,
+                      int64_t* send, int32_t* n_recv, int64_t* recv) {
+    if (n < 0 || nranks < 1 || rank < 0 || rank >= nranks || per < 1 || !need || !n_send || !send || !n_recv ||
+        !recv)
+        return ELLPACK_ERR_ARG;
+    // block q = [q per, min(n, (q + 1) per)); need[2q..2q+1] = rank q's referenced rows (inclusive)
+    auto blk0 = [&](int q) { return std::min<int64_t>(n, (int64_t)q * per); };
+    auto blk1 = [&](int q) { return std::min<int64_t>(n, (int64_t)(q + 1) * per); };
+    int32_t ns = 0, nr = 0;
+    for (int q = 0; q < nranks; ++q) {
+        if (q == rank) continue;
+        const int64_t s0 = std::max(blk0(rank), std::max<int64_t>(0, need[2 * q]));
+        const int64_t s1 = std::min(blk1(rank), need[2 * q + 1] + 1);
+        if (s0 < s1) { send[3 * ns] = q; send[3 * ns + 1] = s0; send[3 * ns + 2] = s1; ++ns; }
+        const int64_t t0 = std::max(blk0(q), std::max<int64_t>(0, need[2 * rank]));
+        const int64_t t1 = std::min(blk1(q), need[2 * rank + 1] + 1);
+        if (t0 < t1) { recv[3 * nr] = q; recv[3 * nr + 1] = t0; recv[3 * nr + 2] = t1; ++nr; }
+    }
+    *n_send = ns;
+    *n_recv = nr;
+    return ELLPACK_OK;
+}
+
+int ellpack_halo_rows(ellpack_ctx c, const ellpack_desc* a, ellpack_desc* b) {
+    if (!c) return ELLPACK_ERR_ARG;
+    RK(check_desc(a));
+    RK(check_desc(b));
+    if (a->n != b->n) return ELLPACK_ERR_DIM;
+    CK(cudaSetDevice(c->device));
+    return halo_desc(c, a, b);
+}
+
 int ellpack_nccl_unique_id(uint8_t id[128]) {
     if (!id) return ELLPACK_ERR_ARG;
     if (!load_nccl()) return ELLPACK_ERR_NCCL;
@@ -822,6 +908,9 @@ int dm_alloc(ellpack_ctx c, DevMatrix& m, int64_t n, int32_t w) {
     m.d.val = (double*)b[0].p;
     m.d.col = (int32_t*)b[1].p;
     m.d.nnz = (int32_t*)b[2].p;
+    // rows are reinterpreted at the new width: empty them (with a halo exchange, rows outside a
+    // rank's block and halo are never written and must read as valid rows)
+    CK(cudaMemsetAsync(m.d.nnz, 0, sizeof(int32_t) * (size_t)n, c->stream));
     m.owned = true;
     return ELLPACK_OK;
 }
@@ -936,7 +1025,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     CK(launch_copy_rows(kmat(&T.d), kout(&X.d), r0, r1, c->d_status, c->stream));
     c->launches++;
     dm_free(c, T);
-    if ((rc = allgather_desc(c, &X.d))) { cleanup(); return rc; }
+    if ((rc = halo_desc(c, &X.d, &X.d))) { cleanup(); return rc; }  // rows X0's rows reference
     double trX;
     if ((rc = ellpack_trace(c, &X.d, &trX))) { cleanup(); return rc; }
     // trace-closest rule (SP2_RULE_TRACE_CLOSEST): T2 of X0 here, of X_{n+1} after step n
@@ -1076,7 +1165,8 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             iters[it].frob2 = t2;
         }
         if (closest) t2 = c->h->sums[3];
-        if ((rc = allgather_desc(c, &Y.d))) { status = rc; break; }
+        // the next step reads only the rows of X_{n+1} its rows reference (band-aware halo, f1)
+        if ((rc = halo_desc(c, &Y.d, &Y.d))) { status = rc; break; }
         std::swap(X, Y);
         wx = wy;
         trX = trY;
@@ -1094,6 +1184,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     R.trD = trX;
     if (status == ELLPACK_OK) {
         R.stop_reason = stop;
+        RK(allgather_desc(c, &X.d));  // D is replicated: every block of the final iterate
         CK(cudaMemsetAsync(c->d_status, 0, 8, c->stream));
         CK(launch_copy_rows(kmat(&X.d), kout(dout), 0, n, c->d_status, c->stream));
         c->launches++;

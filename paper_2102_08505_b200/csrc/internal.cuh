@@ -81,9 +81,11 @@ cudaError_t launch_row_op(const RowOpParams& p, const LaunchCfg& cfg, cudaStream
 size_t row_op_warp_smem(int S, bool has_old, bool fast);
 // bank-balanced copy of B for the fast path (wt = 64 G >= 16 ceil(nnz/16) for every row)
 // (S: the ring size of the launch that consumes it; slots are precomputed as 8 (j mod S))
-cudaError_t launch_balance(KMat b, int64_t n, int wt, int S, unsigned char* bt, int32_t* bt_nbin, int num_sms,
-                           cudaStream_t s);
-// out[0..2] = max half-bandwidth of a (rows r0..r1), b (all rows), c (rows r0..r1); out[3] = max nnz of b
+// (rows k0 <= k < k1 only: the B rows the launch's A rows reference)
+cudaError_t launch_balance(KMat b, int64_t k0, int64_t k1, int wt, int S, unsigned char* bt, int32_t* bt_nbin,
+                           int num_sms, cudaStream_t s);
+// out[0..2] = max half-bandwidth of a (rows r0..r1), b (all rows), c (rows r0..r1); out[3] = max nnz of b;
+// A's rows r0..r1 reference B rows [INT_MAX - out[4], out[5] - 1] (out[0..5] zeroed by the caller)
 cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64_t r1, int64_t n,
                              int32_t* out, cudaStream_t s);
 
@@ -103,6 +105,9 @@ cudaError_t launch_identity(int64_t n, KOut id, cudaStream_t s);
 cudaError_t launch_copy_rows(KMat src, KOut dst, int64_t row_begin, int64_t row_end,
                              int32_t* status, cudaStream_t s);
 cudaError_t launch_breakpoints(KMat b, int64_t n, int S, int np, int32_t* bp, int num_sms, cudaStream_t s);
+// out[0] = min first column, out[1] = max last column of a's rows r0..r1 (caller initialises
+// out to {INT64_MAX, -1})
+cudaError_t launch_col_range(KMat a, int64_t r0, int64_t r1, long long* out, cudaStream_t s);
 cudaError_t launch_products(KMat a, const int32_t* nnz_b, int64_t r0, int64_t r1, unsigned long long* out,
                             cudaStream_t s);
 cudaError_t launch_max_nnz(const int32_t* nnz, int64_t row_begin, int64_t row_end,

@@ -10,6 +10,7 @@
 //  * Gershgorin bounds (§8c-c8): thread per row, sequential in slot
 //    order; min/max are exact, so any combine order gives the same bits.
 //  * fnorm_diff rows: warp per row, binary search of the partner row.
+#include <climits>
 #include "internal.cuh"
 
 namespace ell {
@@ -182,6 +183,34 @@ cudaError_t launch_sumsq_rows(KMat a, int64_t r0, int64_t r1, double* out, cudaS
     const int64_t rows = r1 - r0;
     if (rows <= 0) return cudaSuccess;
     sumsq_rows_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(a, r0, r1, out);
+    return cudaGetLastError();
+}
+
+__global__ void col_range_kernel(KMat a, int64_t r0, int64_t r1, long long* out) {
+    const int64_t i = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    long long lo = LLONG_MAX, hi = -1;
+    if (i < r1) {
+        const int nz = a.nnz[i];
+        if (nz > 0) {
+            lo = a.col[(size_t)i * a.w];
+            hi = a.col[(size_t)i * a.w + nz - 1];
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(FULL, lo, o));
+        hi = max(hi, __shfl_xor_sync(FULL, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (lo != LLONG_MAX) atomicMin(out, lo);
+        if (hi >= 0) atomicMax(out + 1, hi);
+    }
+}
+
+cudaError_t launch_col_range(KMat a, int64_t r0, int64_t r1, long long* out, cudaStream_t s) {
+    const int64_t rows = r1 - r0;
+    if (rows <= 0) return cudaSuccess;
+    col_range_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(a, r0, r1, out);
     return cudaGetLastError();
 }
 

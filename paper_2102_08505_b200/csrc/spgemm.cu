@@ -179,7 +179,7 @@ __host__ __device__ inline size_t warp_smem_bytes(int S, bool has_old, bool fast
 //      run the same LDS / DFMA / STS.
 // Record of row k (12 * 64 G bytes): int32 slot8[64 G] (= 8 * slot) then f64 val[64 G].
 // bt_nbin[k] = NB: group g holds entries iff NB > 4 g.
-__global__ void balance_kernel(KMat b, int64_t n, int wt, int S, unsigned char* __restrict__ bt,
+__global__ void balance_kernel(KMat b, int64_t k0, int64_t k1, int wt, int S, unsigned char* __restrict__ bt,
                                int32_t* __restrict__ bt_nbin) {
     __shared__ int hist_s[8][16];        // per warp: entries per residue (256-thread blocks)
     __shared__ unsigned bmask_s[8][16];  // per warp and bin: residues of its real entries
@@ -195,7 +195,7 @@ __global__ void balance_kernel(KMat b, int64_t n, int wt, int S, unsigned char* 
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const double invS = 1.0 / (double)S;
-    for (int64_t k = w0; k < n; k += nw) {
+    for (int64_t k = k0 + w0; k < k1; k += nw) {
         const int nb = b.nnz[k];  // <= 256 on the fast path (8 chunks)
         // bins: every bin of the 64-entry groups a step loads anyway (4 ceil(nb / 64), not
         // ceil(nb / 16)), so the entries of a residue class spread over more bins: fewer
@@ -287,11 +287,13 @@ __global__ void balance_kernel(KMat b, int64_t n, int wt, int S, unsigned char* 
     }
 }
 
-cudaError_t launch_balance(KMat b, int64_t n, int wt, int S, unsigned char* bt, int32_t* bt_nbin, int num_sms,
-                           cudaStream_t s) {
-    const int64_t blocks_needed = (n + 7) / 8;
+cudaError_t launch_balance(KMat b, int64_t k0, int64_t k1, int wt, int S, unsigned char* bt, int32_t* bt_nbin,
+                           int num_sms, cudaStream_t s) {
+    if (k1 <= k0) return cudaSuccess;
+    const int64_t blocks_needed = (k1 - k0 + 7) / 8;
     const int64_t cap = (int64_t)num_sms * 8;
-    balance_kernel<<<(unsigned)(blocks_needed < cap ? blocks_needed : cap), 256, 0, s>>>(b, n, wt, S, bt, bt_nbin);
+    balance_kernel<<<(unsigned)(blocks_needed < cap ? blocks_needed : cap), 256, 0, s>>>(b, k0, k1, wt, S, bt,
+                                                                                         bt_nbin);
     return cudaGetLastError();
 }
 
@@ -1194,10 +1196,13 @@ __global__ void __launch_bounds__(128, 1) row_general_kernel(const RowOpParams p
     flush_status(p, lane, my_max_kept, my_ovf);
 }
 
-// Half-bandwidth probe: out[m] = max over rows of max(i - col[i][0], col[i][nnz-1] - i).
+// Half-bandwidth probe: out[m] = max over rows of max(i - col[i][0], col[i][nnz-1] - i);
+// out[3] = max nnz of b; the B rows the A rows [r0, r1) reference are [INT_MAX - out[4], out[5] - 1]
+// (zero-initialised maxima of INT_MAX - first column and last column + 1).
 __global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int64_t r0, int64_t r1, int64_t n, int32_t* out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int bw[3] = {0, 0, 0};
+    int reach[2] = {0, 0};
     const KMat* ms[3] = {&a, &b, &c};
     if (i < n) {
 #pragma unroll
@@ -1210,13 +1215,14 @@ __global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int64_t r0, int64_t r1,
             if (nz > 0) {
                 const int f = x.col[(size_t)i * x.w], l = x.col[(size_t)i * x.w + nz - 1];
                 bw[m] = max(max((int)(i - f), (int)(l - i)), 0);
+                if (m == 0) { reach[0] = INT_MAX - f; reach[1] = l + 1; }
             }
         }
     }
     int nzb = (i < n) ? b.nnz[i] : 0;
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        int v = m < 3 ? bw[m] : nzb;
+    for (int m = 0; m < 6; ++m) {
+        int v = m < 3 ? bw[m] : (m == 3 ? nzb : reach[m - 4]);
 #pragma unroll
         for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
         if ((threadIdx.x & 31) == 0 && v > 0) atomicMax(out + m, v);

@@ -466,6 +466,13 @@ def test_row_block_partition_is_bitwise_invariant(ellpack_lib, nranks):
     full.close()
 
 
+def test_halo_rows_without_communicator_is_a_no_op(ctx):
+    X = synth.cfg5(4096, 32)
+    x = up(X)
+    ctx.halo_rows(x)
+    assert same_bits(x.to_host(), X)
+
+
 def test_host_buffer_e2e_path(ctx):
     X = synth.cfg1()
     r, Y = ora_x2(X, 256, 1e-5)

@@ -108,6 +108,91 @@ def _worker(rank, ws, port, n, m, tau):
     dist.destroy_process_group()
 
 
+def _halo_worker(rank, ws, port, n, m, tau):
+    """§8f-f1: each rank holds only its own block of X; the library's halo plan
+    (ellpack_halo_plan, the function ellpack_halo_rows runs) moves exactly the rows its own rows
+    reference; the rank's X^2 rows computed from that partial X are bitwise the full result."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(ws),
+                      LOCAL_RANK=str(rank))
+    sys.path.insert(0, ROOT)
+    import oracle
+    import synth
+    import paper_2102_08505_b200 as eb
+    from paper_2102_08505_b200 import multirank as mr
+
+    oracle.set_threads(1)
+    dist = mr.init_process_group("gloo")
+    r0, r1 = mr.rank_rows(n, ws, rank)
+    per = r1 - r0
+    X = synth.cfg5(n, m)
+    # this rank's view: own block only
+    Xr = synth.Ell.empty(n, X.w)
+    Xr.val[r0:r1], Xr.col[r0:r1], Xr.nnz[r0:r1] = X.val[r0:r1], X.col[r0:r1], X.nnz[r0:r1]
+    own = [i for i in range(r0, r1) if X.nnz[i] > 0]
+    need = (min(int(X.col[i, 0]) for i in own), max(int(X.col[i, X.nnz[i] - 1]) for i in own))
+    needs = [None] * ws
+    dist.all_gather_object(needs, need)
+    sends, recvs = eb.halo_plan(n, ws, rank, per, needs)
+    # every referenced row is either own or received, and nothing else is received
+    got = set(range(r0, r1))
+    for _, t0, t1 in recvs:
+        got |= set(range(t0, t1))
+    assert set(range(need[0], need[1] + 1)) <= got
+    assert all(need[0] <= t0 and t1 <= need[1] + 1 for _, t0, t1 in recvs)
+    # the sends of every rank are the receives of their peers (plans agree pairwise)
+    all_s, all_r = [None] * ws, [None] * ws
+    dist.all_gather_object(all_s, sends)
+    dist.all_gather_object(all_r, recvs)
+    for p_ in range(ws):
+        for q, s0, s1 in all_s[p_]:
+            assert (p_, s0, s1) in all_r[q]
+    reqs = []
+    for q, s0, s1 in sends:
+        for name in ("val", "col", "nnz"):
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(getattr(Xr, name)[s0:s1])), q))
+    bufs = []
+    for q, t0, t1 in recvs:
+        for name in ("val", "col", "nnz"):
+            b = torch.from_numpy(np.ascontiguousarray(getattr(Xr, name)[t0:t1]).copy())
+            bufs.append((name, t0, t1, b))
+            reqs.append(dist.irecv(b, q))
+    for r in reqs:
+        r.wait()
+    for name, t0, t1, b in bufs:
+        getattr(Xr, name)[t0:t1] = b.numpy()
+    # own rows of X^2 from the partial view == the full computation
+    A = synth.Ell.empty(n, X.w)
+    A.val[r0:r1], A.col[r0:r1], A.nnz[r0:r1] = X.val[r0:r1], X.col[r0:r1], X.nnz[r0:r1]
+    full = synth.Ell.empty(n, n)
+    part = synth.Ell.empty(n, n)
+    oracle.multiply(A, X, full, 1.0, 0.0, tau)
+    oracle.multiply(A, Xr, part, 1.0, 0.0, tau)
+    assert np.array_equal(part.nnz[r0:r1], full.nnz[r0:r1])
+    for i in range(r0, r1):
+        k = int(full.nnz[i])
+        assert np.array_equal(part.col[i, :k], full.col[i, :k])
+        assert np.array_equal(part.val[i, :k].view(np.uint64), full.val[i, :k].view(np.uint64))
+    # the halo moved less than the all-gather would have
+    moved = sum(t1 - t0 for _, t0, t1 in recvs)
+    assert moved <= n - per
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws,n,m", [(2, 2048, 32), (4, 4096, 16), (4, 2048, 64)])
+def test_halo_exchange_plan_gloo(ws, n, m):
+    tmp.spawn(_halo_worker, args=(ws, _free_port(), n, m, 1e-5), nprocs=ws, join=True)
+
+
+def test_halo_plan_rejects_bad_arguments():
+    sys.path.insert(0, ROOT)
+    import paper_2102_08505_b200 as eb
+    with pytest.raises(eb.EllpackError):
+        eb.halo_plan(1024, 2, 2, 512, [(0, 1), (0, 1)])  # rank out of range
+    s, r = eb.halo_plan(1024, 2, 0, 512, [(0, 100), (900, 1023)])  # disjoint ranges: nothing moves
+    assert s == [] and r == []
+
+
 @pytest.mark.parametrize("n,m", [(2048, 64), (4096, 32)])
 def test_row_partition_protocol_gloo_ws2(n, m):
     tmp.spawn(_worker, args=(2, _free_port(), n, m, 1e-5), nprocs=2, join=True)
