@@ -1085,7 +1085,10 @@ __global__ void __launch_bounds__(32, 8) row_fast_kernel(const RowOpParams p) {
 // split at window boundaries by precomputed breakpoints (rows wider than any ring that fits
 // shared memory, B rows > 256 entries: the densifying SP2 iterates).
 template <int MODE>
-__global__ void __launch_bounds__(128, 1) row_general_kernel(const RowOpParams p) {
+#ifndef ELL_GEN_MINB
+#define ELL_GEN_MINB 1  // general kernel: min resident 128-thread CTAs per SM (register cap)
+#endif
+__global__ void __launch_bounds__(128, ELL_GEN_MINB) row_general_kernel(const RowOpParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;

@@ -30,7 +30,8 @@ for v in sys.argv[1:]:
     for spec in sp2.split():  # "C" or "C:K" (K = SP2 window)
         c, _, k = spec.partition(":")
         o = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "sp2", "--sp2-cfg", c,
-                            "--steps", "2", "--warmup", "1"] + (["--sp2-iters", k] if k else []),
+                            "--steps", "2", "--warmup", "1"] + (["--sp2-iters", k] if k else [])
+                           + (["--general-window", os.environ["GW"]] if os.environ.get("GW") else []),
                            capture_output=True, text=True, cwd=ROOT).stdout
         line = o.strip().splitlines()[-1] if o.strip() else "?"
         try:
