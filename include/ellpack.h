@@ -104,9 +104,15 @@ int ellpack_ctx_set_stream(ellpack_ctx ctx, void* stream);
  *                          0 = off (default). Only builds with -DELL_ABLATE=1 accept a
  *                          nonzero mask (ELLPACK_ERR_ARG otherwise).
  *  ELLPACK_OPT_GENERAL_WINDOW  window (doubles, multiple of 32) of the general path that
- *                          wide rows (dense SP2 iterates) use; 0 = automatic (1024). */
+ *                          wide rows (dense SP2 iterates) use; 0 = automatic (1024).
+ *  ELLPACK_OPT_VALIDATE    nonzero: every entry point first checks its input operands
+ *                          for canonical form on the device (0 <= nnz <= w; columns in
+ *                          [0, N), strictly ascending; values finite; §8c-c1) and returns
+ *                          ELLPACK_ERR_ARG on a violation (one extra kernel and one
+ *                          synchronising read-back per operand set). 0 = inputs trusted
+ *                          (default). */
 enum { ELLPACK_OPT_WINDOW = 1, ELLPACK_OPT_WARPS = 2, ELLPACK_OPT_SP2_WIDTH0 = 3, ELLPACK_OPT_PROFILE = 4,
-       ELLPACK_OPT_ABLATE = 5, ELLPACK_OPT_GENERAL_WINDOW = 6 };
+       ELLPACK_OPT_ABLATE = 5, ELLPACK_OPT_GENERAL_WINDOW = 6, ELLPACK_OPT_VALIDATE = 7 };
 int ellpack_ctx_set_option(ellpack_ctx ctx, int key, int64_t value);
 
 /* Accumulated device time (ms, CUDA events on the ctx stream) and launch count of

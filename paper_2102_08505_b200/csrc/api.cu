@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <chrono>
 #include <climits>
+#include <initializer_list>
 #include <cstdio>
 #include <vector>
 #include <cmath>
@@ -89,7 +90,7 @@ struct ellpack_ctx_s {
     int device = 0;
     cudaStream_t stream = nullptr;
     int num_sms = 148;
-    int window_opt = 0, warps_opt = 0, sp2_width0 = 0, ablate = 0, general_s = 0;
+    int window_opt = 0, warps_opt = 0, sp2_width0 = 0, ablate = 0, general_s = 0, validate = 0;
     int64_t launches = 0;
     // small device/pinned blocks
     int32_t* d_status = nullptr;              // [0] ovf rows, [1] max kept
@@ -113,6 +114,7 @@ struct ellpack_ctx_s {
     Buf hx_val, hx_col, hx_nnz, hy_val, hy_col, hy_nnz;  // host-path device copies
     Buf bt, bt_nbin, bp;
     Buf halo;  // all ranks' referenced row ranges (halo exchange)
+    Buf vflag; // ELLPACK_OPT_VALIDATE violation flag
     Buf it[3][3];  // SP2 iterate buffers (val, col, nnz) x 3 slots                         // bank-balanced copy of B (fast path)
     // ring sizing cache: (hB, G, mode) -> (S, rows resident per SM)
     int64_t ring_key = -1;
@@ -184,6 +186,23 @@ int check_desc(const ellpack_desc* d) {
 }
 
 bool valid_tau(double t) { return t >= 0.0 && std::isfinite(t); }
+
+// ELLPACK_OPT_VALIDATE: canonical-form check of input operands on the device (one thread per
+// row, one synchronising read-back); ARG on any violation. Off: inputs are trusted (§8b).
+int validate_inputs(ellpack_ctx c, std::initializer_list<const ellpack_desc*> ds) {
+    if (!c->validate) return ELLPACK_OK;
+    RK(grow(c, c->vflag, sizeof(int32_t)));
+    int32_t* flag = (int32_t*)c->vflag.p;
+    CK(cudaMemsetAsync(flag, 0, sizeof(int32_t), c->stream));
+    for (const ellpack_desc* d : ds) {
+        CK(launch_validate(KMat{d->val, d->col, d->nnz, d->w}, d->n, flag, c->stream));
+        c->launches++;
+    }
+    int32_t bad = 0;
+    CK(cudaMemcpyAsync(&bad, flag, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return bad ? ELLPACK_ERR_ARG : ELLPACK_OK;
+}
 
 KMat kmat(const ellpack_desc* d) { return KMat{d->val, d->col, d->nnz, d->w}; }
 KOut kout(const ellpack_desc* d) { return KOut{d->val, d->col, d->nnz, d->w}; }
@@ -527,7 +546,7 @@ int ellpack_ctx_destroy(ellpack_ctx c) {
     Buf* bufs[] = {&c->rows[0], &c->rows[1], &c->rows[2], &c->rows[3], &c->partials,
                    &c->stash_val, &c->stash_col, &c->ident_val, &c->ident_col, &c->ident_nnz,
                    &c->hx_val, &c->hx_col, &c->hx_nnz, &c->hy_val, &c->hy_col, &c->hy_nnz,
-                   &c->bt, &c->bt_nbin, &c->bp, &c->halo};
+                   &c->bt, &c->bt_nbin, &c->bp, &c->halo, &c->vflag};
     for (auto& sl : c->it)
         for (Buf& b : sl) release(c, b);
     for (Buf* b : bufs) release(c, *b);
@@ -553,6 +572,7 @@ int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
     if (!c || v < 0) return ELLPACK_ERR_ARG;
     switch (key) {
         case ELLPACK_OPT_WINDOW: c->window_opt = (int)v; return ELLPACK_OK;
+        case ELLPACK_OPT_VALIDATE: c->validate = v != 0; return ELLPACK_OK;
         case ELLPACK_OPT_WARPS: c->warps_opt = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_SP2_WIDTH0: c->sp2_width0 = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_ABLATE:
@@ -642,6 +662,7 @@ int ellpack_multiply(ellpack_ctx c, const ellpack_desc* a, const ellpack_desc* b
     if (!valid_tau(tau) || !std::isfinite(alpha) || !std::isfinite(beta)) return ELLPACK_ERR_ARG;
     if (same(cm, a) || same(cm, b)) return ELLPACK_ERR_ARG;
     CK(cudaSetDevice(c->device));
+    if (beta != 0.0) RK(validate_inputs(c, {a, b, cm})); else RK(validate_inputs(c, {a, b}));
     RowOpParams p = base_params(c, a->n);
     p.A = kmat(a);
     p.B = kmat(b);
@@ -669,6 +690,7 @@ int ellpack_multiply_x2(ellpack_ctx c, const ellpack_desc* x, ellpack_desc* x2, 
     if (!valid_tau(tau)) return ELLPACK_ERR_ARG;
     if (same(x, x2)) return ELLPACK_ERR_ARG;
     CK(cudaSetDevice(c->device));
+    RK(validate_inputs(c, {x}));
     const int64_t n = x->n;
     RK(grow(c, c->rows[0], sizeof(double) * n));
     RK(grow(c, c->rows[1], sizeof(double) * n));
@@ -722,6 +744,8 @@ int ellpack_add(ellpack_ctx c, ellpack_desc* a, const ellpack_desc* b, double al
     if (!valid_tau(tau) || !std::isfinite(alpha) || !std::isfinite(beta)) return ELLPACK_ERR_ARG;
     const bool ident = a->val == b->val && a->col == b->col && a->nnz == b->nnz && a->w == b->w;
     if (!ident && same(a, b)) return ELLPACK_ERR_ARG;  // partial aliasing
+    CK(cudaSetDevice(c->device));
+    RK(validate_inputs(c, {a, b}));
     return add_via_identity(c, a, kmat(b), ident, alpha, beta, tau);
 }
 
@@ -730,6 +754,7 @@ int ellpack_scale_add_identity(ellpack_ctx c, ellpack_desc* a, double alpha, dou
     RK(check_desc(a));
     if (!valid_tau(tau) || !std::isfinite(alpha) || !std::isfinite(beta)) return ELLPACK_ERR_ARG;
     CK(cudaSetDevice(c->device));
+    RK(validate_inputs(c, {a}));
     RK(ensure_identity(c, a->n));
     return add_via_identity(c, a, identity(c), false, alpha, beta, tau);
 }
@@ -742,6 +767,7 @@ int ellpack_trace(ellpack_ctx c, const ellpack_desc* a, double* out) {
     if (!c || !out) return ELLPACK_ERR_ARG;
     RK(check_desc(a));
     CK(cudaSetDevice(c->device));
+    RK(validate_inputs(c, {a}));
     const int64_t n = a->n;
     RK(grow(c, c->rows[0], sizeof(double) * n));
     int64_t r0, r1;
@@ -762,6 +788,7 @@ int ellpack_fnorm_diff(ellpack_ctx c, const ellpack_desc* a, const ellpack_desc*
     RK(check_desc(b));
     if (a->n != b->n) return ELLPACK_ERR_DIM;
     CK(cudaSetDevice(c->device));
+    RK(validate_inputs(c, {a, b}));
     const int64_t n = a->n;
     RK(grow(c, c->rows[0], sizeof(double) * n));
     int64_t r0, r1;
@@ -803,6 +830,7 @@ int ellpack_gershgorin(ellpack_ctx c, const ellpack_desc* h, double* emin, doubl
     if (!c || !emin || !emax) return ELLPACK_ERR_ARG;
     RK(check_desc(h));
     CK(cudaSetDevice(c->device));
+    RK(validate_inputs(c, {h}));
     return gershgorin_impl(c, h, emin, emax);
 }
 
@@ -975,6 +1003,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     if (!valid_tau(o.threshold) || o.max_iter < 1) return ELLPACK_ERR_ARG;
     if (o.branch_rule != SP2_RULE_TRACE_SIGN && o.branch_rule != SP2_RULE_TRACE_CLOSEST) return ELLPACK_ERR_ARG;
     CK(cudaSetDevice(c->device));
+    RK(validate_inputs(c, {h}));
     sp2_iter_rec* iters = rep ? rep->iters : nullptr;
     sp2_report R;
     memset(&R, 0, sizeof R);

@@ -101,6 +101,7 @@ cudaError_t launch_gershgorin(KMat h, int64_t row_begin, int64_t row_end,
 cudaError_t launch_fnorm_rows(KMat a, KMat b, int64_t row_begin, int64_t row_end, double* out,
                               cudaStream_t s);
 cudaError_t launch_sumsq_rows(KMat a, int64_t row_begin, int64_t row_end, double* out, cudaStream_t s);
+cudaError_t launch_validate(KMat a, int64_t n, int32_t* bad, cudaStream_t s);
 cudaError_t launch_identity(int64_t n, KOut id, cudaStream_t s);
 cudaError_t launch_copy_rows(KMat src, KOut dst, int64_t row_begin, int64_t row_end,
                              int32_t* status, cudaStream_t s);

@@ -214,6 +214,31 @@ cudaError_t launch_col_range(KMat a, int64_t r0, int64_t r1, long long* out, cud
     return cudaGetLastError();
 }
 
+// Canonical-form check (D1, §8c-c1): 0 <= nnz <= w, columns in [0, n) strictly ascending, values
+// finite. Thread per row; any violation sets *bad (ELLPACK_OPT_VALIDATE).
+__global__ void validate_kernel(KMat a, int64_t n, int32_t* bad) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int nz = a.nnz[i];
+    bool ok = nz >= 0 && nz <= a.w;
+    if (ok) {
+        const int32_t* c = a.col + (size_t)i * a.w;
+        const double* v = a.val + (size_t)i * a.w;
+        int prev = -1;
+        for (int p = 0; p < nz && ok; ++p) {
+            const int j = c[p];
+            ok = j > prev && (int64_t)j < n && isfinite(v[p]);
+            prev = j;
+        }
+    }
+    if (!ok) atomicOr(bad, 1);
+}
+
+cudaError_t launch_validate(KMat a, int64_t n, int32_t* bad, cudaStream_t s) {
+    validate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, n, bad);
+    return cudaGetLastError();
+}
+
 __global__ void identity_kernel(int64_t n, KOut id) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;

@@ -466,6 +466,57 @@ def test_row_block_partition_is_bitwise_invariant(ellpack_lib, nranks):
     full.close()
 
 
+def _corrupt(X, kind):
+    Y = X.copy()
+    i = int(np.argmax(Y.nnz))  # a row with >= 2 entries
+    if kind == "unsorted":
+        Y.col[i, 0], Y.col[i, 1] = Y.col[i, 1], Y.col[i, 0]
+    elif kind == "duplicate":
+        Y.col[i, 1] = Y.col[i, 0]
+    elif kind == "col_range":
+        Y.col[i, Y.nnz[i] - 1] = Y.n
+    elif kind == "negative_col":
+        Y.col[i, 0] = -1
+    elif kind == "nnz_range":
+        Y.nnz[i] = Y.w + 2
+    elif kind == "nan":
+        Y.val[i, 0] = float("nan")
+    return Y
+
+
+@pytest.mark.parametrize("kind", ["unsorted", "duplicate", "col_range", "negative_col", "nnz_range", "nan"])
+def test_validate_option_rejects_non_canonical_inputs(ellpack_lib, kind):
+    """ELLPACK_OPT_VALIDATE (§8b: inputs must be canonical D1, checked on request): every entry point
+    returns ARG for a non-canonical operand and still computes bitwise for canonical ones."""
+    E = ellpack_lib
+    ctx = E.Context(0)
+    ctx.set_option(E.OPT_VALIDATE, 1)
+    X = synth.cfg1()
+    Y = synth.Ell.empty(X.n, 256)
+    r = oracle.x2(X, Y, 1e-5)
+    y = E.Mat.empty(X.n, 256)
+    st, tx, tx2 = ctx.multiply_x2(up(X), y, 1e-5)
+    assert st == E.OK and (tx, tx2) == (r.trace_x, r.trace_x2) and same_bits(y.to_host(), Y)
+    bad = up(_corrupt(X, kind))
+    good = up(X)
+    calls = [
+        lambda: ctx.multiply_x2(bad, E.Mat.empty(X.n, 256), 1e-5, ok=()),
+        lambda: ctx.multiply(bad, good, E.Mat.empty(X.n, 256), 1.0, 0.0, 1e-5, ok=()),
+        lambda: ctx.multiply(good, bad, E.Mat.empty(X.n, 256), 1.0, 0.0, 1e-5, ok=()),
+        lambda: ctx.add(up(X, w=64), bad, 1.0, 1.0, 0.0, ok=()),
+        lambda: ctx.add_identity(bad, 1.0, 0.0, ok=()),
+        lambda: ctx.trace(bad),
+        lambda: ctx.fnorm_diff(good, bad),
+        lambda: ctx.gershgorin(bad),
+        lambda: ctx.sp2_run(bad, X.n // 2, 1e-8, E.Mat.empty(X.n, X.n), ok=()),
+    ]
+    for k, call in enumerate(calls):
+        with pytest.raises(E.EllpackError) as ei:
+            call()
+        assert ei.value.status == E.ERR_ARG, (kind, k)
+    ctx.close()
+
+
 def test_halo_rows_without_communicator_is_a_no_op(ctx):
     X = synth.cfg5(4096, 32)
     x = up(X)
