@@ -517,6 +517,34 @@ def test_validate_option_rejects_non_canonical_inputs(ellpack_lib, kind):
     ctx.close()
 
 
+def test_nccl_single_rank_communicator_paths(ellpack_lib):
+    """The NCCL code paths on one GPU (a 1-rank communicator): status all-reduce, trace-partial
+    all-gather, halo exchange (col-range kernel + range all-gather + an empty plan), SP2 with
+    halo exchanges and the final all-gather -- all bitwise equal to the oracle."""
+    import torch  # noqa: F401  (loads torch's libnccl.so.2 for the library's dlopen)
+    E = ellpack_lib
+    ctx = E.Context(0)
+    uid = E.Context.nccl_unique_id()
+    n = 1024
+    ctx.attach_nccl(1, 0, uid, 0, n)
+    X = synth.cfg5(n, 32)
+    Y = synth.Ell.empty(n, 512)
+    r = oracle.x2(X, Y, 1e-5)
+    x = up(X)
+    ctx.halo_rows(x)
+    assert same_bits(x.to_host(), X)
+    y = E.Mat.empty(n, 512)
+    st, tx, tx2 = ctx.multiply_x2(x, y, 1e-5)
+    assert st == E.OK and (tx, tx2) == (r.trace_x, r.trace_x2) and same_bits(y.to_host(), Y)
+    H = synth.sym_banded(n, 32, 6, 12, 1, -1.0, 1.0, 0, 4.0, 0.0, 3)
+    o = oracle.sp2(H, n // 2, 1e-10, oracle.SP2Opts(threshold=1e-7, max_iter=100), d_width=n)
+    d = E.Mat.empty(n, n)
+    g = ctx.sp2_run(up(H), n // 2, 1e-10, d, threshold=1e-7, max_iter=100)
+    _compare_sp2(g, o)
+    assert same_bits(d.to_host(), o.D)
+    ctx.close()
+
+
 def test_halo_rows_without_communicator_is_a_no_op(ctx):
     X = synth.cfg5(4096, 32)
     x = up(X)
