@@ -725,17 +725,20 @@ __device__ __forceinline__ void ring_emit_block(const RowOpParams& p, const Warp
     kept = before;
 }
 
-// Emit [F, Fto) (multiples of 32), four chunks at a time where possible; advances F, baseF.
+#ifndef ELL_EMIT_NCH
+#define ELL_EMIT_NCH 4  // ring emission: 32-column chunks per block (<= 4: a block wraps at most once)
+#endif
+// Emit [F, Fto) (multiples of 32), ELL_EMIT_NCH chunks at a time where possible; advances F, baseF.
 template <int MODE, bool A1>
 __device__ __forceinline__ void ring_emit_range_t(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
                                                   int& F, int& baseF, int Fto, const int32_t* o_col,
                                                   const double* o_val, int nOld, int& old_cur,
                                                   double* __restrict__ crow_v, int32_t* __restrict__ crow_c,
                                                   int& kept, double& ds, double& dc, double& nrm) {
-    while (p.S >= 256 && F + 128 <= Fto) {  // a 128-column block wraps at most once
-        ring_emit_block<MODE, 4, A1>(p, w, lane, i, F, baseF, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept,
-                                     ds, dc, nrm);
-        F += 128;
+    while (p.S >= 256 && F + 32 * ELL_EMIT_NCH <= Fto) {  // a block of <= 128 columns wraps at most once
+        ring_emit_block<MODE, ELL_EMIT_NCH, A1>(p, w, lane, i, F, baseF, o_col, o_val, nOld, old_cur, crow_v,
+                                                crow_c, kept, ds, dc, nrm);
+        F += 32 * ELL_EMIT_NCH;
         while (F - baseF >= p.S) baseF += p.S;
     }
     while (F < Fto) {
