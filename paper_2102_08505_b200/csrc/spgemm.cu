@@ -42,7 +42,7 @@ constexpr int kStage = 64;  // general path: A-row entries staged per piece (64:
 #define ELL_SEG_U 4  // general path: gathers per lane per round
 #endif
 #ifndef ELL_STAGE_F
-#define ELL_STAGE_F 128  // fast path: stage entries (16 B each); 128 measured best vs 64, 96
+#define ELL_STAGE_F 128  // fast path: stage entries (16 B each); 128 measured best vs 64, 96, 160, 192, 256
 #endif
 constexpr int kStageF = ELL_STAGE_F;
 #ifndef ELL_ABLATE
