@@ -1,0 +1,75 @@
+#!/usr/bin/env python
+"""Full SP2 runs to the stop rule on the GPU (BASELINE configs[2] / [3], or a model Hamiltonian),
+checked with the north star's SP2 invariants instead of the oracle (which would take hours at
+these sizes): idempotency ||D^2 - D||_F, tr D vs nocc, commutation ||DH - HD||_F / ||H||_F.
+The invariants use torch FP64 dense GEMMs on the GPU (cuBLAS; a checker, not the product path).
+
+    python tools/sp2_full.py --cfg 3 [--max-iter 100]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+
+def dense(m, n, device):
+    """Dense FP64 copy of a device ELLPACK matrix (checker only)."""
+    import torch
+    D = torch.zeros((n, n), dtype=torch.float64, device=device)
+    w = m.val.shape[1]
+    mask = torch.arange(w, device=device)[None, :] < m.nnz.long()[:, None]
+    rows = torch.arange(n, device=device)[:, None].expand(n, w)[mask]
+    D[rows, m.col.long()[mask]] = m.val[mask]
+    return D
+
+
+def main():
+    import torch
+    import paper_2102_08505_b200 as eb
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cfg", type=int, default=3, choices=[3, 4])
+    ap.add_argument("--model", default="")
+    ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--max-iter", type=int, default=100)
+    a = ap.parse_args()
+    if a.model:
+        H = synth.model_hamiltonian(a.n, a.model, tau_store=1e-5)
+        cf = dict(nocc=a.n // 2, tol=1e-8, threshold=1e-5)
+        name = f"{a.model} N={a.n}"
+    else:
+        H, cf = (synth.cfg3(), synth.CFG3) if a.cfg == 3 else (synth.cfg4(), synth.CFG4)
+        name = f"cfg{a.cfg} N={H.n}"
+    n = H.n
+    ctx = eb.Context(0)
+    h = eb.Mat.from_host(H)
+    d = eb.Mat.empty(n, n + (n & 1))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = ctx.sp2_run(h, cf["nocc"], cf["tol"], d, threshold=cf["threshold"], max_iter=a.max_iter)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    dev = torch.device("cuda", 0)
+    Dd = dense(d, n, dev)
+    Hd = dense(h, n, dev)
+    idem = torch.linalg.norm(Dd @ Dd - Dd).item()
+    comm = (torch.linalg.norm(Dd @ Hd - Hd @ Dd) / torch.linalg.norm(Hd)).item()
+    tr = torch.trace(Dd).item()
+    prods = sum(it["products"] for it in r.iters)
+    print(json.dumps({
+        "workload": f"{name} SP2 tau={cf['threshold']} tol={cf['tol']} max_iter={a.max_iter} GROW",
+        "status": r.status, "stop": r.stop, "iterations": r.iterations, "seconds": dt,
+        "iterations_per_s": r.iterations / dt, "gflops": 2.0 * prods / dt / 1e9, "final_width": r.final_width,
+        "regrows": r.regrows, "trD": r.trD, "nocc": cf["nocc"], "trace_dense": tr,
+        "idempotency_fro": idem, "commutator_rel": comm, "phases_s": r.phases,
+        "e_last": [it["e"] for it in r.iters[-3:]], "widths": [it["width"] for it in r.iters]}), flush=True)
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()
