@@ -217,6 +217,51 @@ def test_fast_path_wide_rows_bitwise(ctx, case, alpha, beta, tau):
         assert ctx.overflow_info() == (lit.overflow_rows, lit.required_width)
 
 
+def _fuzz_cases(count=24, seed=2102):
+    rng = np.random.default_rng(seed)
+    out = []
+    for t in range(count):
+        n = int(rng.choice([1, 7, 31, 32, 33, 100, 257, 1000, 2049, 3000]))
+        w = int(rng.choice([2, 8, 32, 64, 96, 128, 200, 256, 300]))
+        kmax = int(min(w, max(1, rng.integers(1, w + 1))))
+        kmin = int(rng.integers(0, kmax + 1))
+        band = int(rng.choice([1, 4, 50, 300, 5000]))
+        pe = float(rng.choice([0.0, 0.1, 0.5]))
+        ab = [(1.0, 0.0, 0.0), (0.75, -1.5, 1e-3), (-1.0, 2.0, 1e-6), (0.0, 1.0, 0.0), (2.0, 0.5, 0.5)][t % 5]
+        out.append((t, n, w, kmin, kmax, band, pe) + ab)
+    # the general path for sure: B rows over 256 entries; a half-bandwidth beyond any ring
+    out += [(count, 1500, 300, 257, 300, 2000, 0.0, 1.0, 0.0, 1e-6),
+            (count + 1, 2500, 300, 200, 300, 1500, 0.05, 0.75, -1.5, 1e-3),
+            (count + 2, 8000, 32, 16, 32, 8000, 0.0, 1.0, 0.0, 0.0),
+            (count + 3, 8000, 32, 8, 32, 8000, 0.1, -1.0, 2.0, 1e-6)]
+    return out
+
+
+@pytest.mark.parametrize("case", _fuzz_cases(), ids=lambda c: f"t{c[0]}n{c[1]}w{c[2]}")
+def test_random_multiply_fuzz_bitwise(ctx, case):
+    """Seeded random shapes across both paths (ring and general: B rows up to 300 entries,
+    half-bandwidths up to 5000), ragged/empty rows and the alpha/beta/tau corners; the output
+    width is the oracle's required width, and the literal width's overflow report must match."""
+    t, n, w, kmin, kmax, band, pe, alpha, beta, tau = case
+    w += w & 1
+    A = synth.random_sparse(n, w, kmin, kmax, band, pe, 1.0, seed=1000 + 3 * t)
+    B = synth.random_sparse(n, w, kmin, kmax, band, pe, 1.0, seed=1001 + 3 * t)
+    C0 = synth.random_sparse(n, w, kmin, kmax, band, pe, 1.0, seed=1002 + 3 * t)
+    lit = oracle.multiply(A, B, C0.copy(), alpha, beta, tau)
+    wo = max(w, ((lit.required_width + 31) // 32) * 32)
+    wo += wo & 1
+    Co = C0.widened(wo).copy()
+    r = oracle.multiply(A, B, Co, alpha, beta, tau)
+    assert r.status == oracle.OK
+    g = up(C0.widened(wo))
+    assert ctx.multiply(up(A), up(B), g, alpha, beta, tau) == eb().OK
+    assert same_bits(g.to_host(), Co)
+    if lit.status != oracle.OK:
+        g2 = up(C0)
+        assert ctx.multiply(up(A), up(B), g2, alpha, beta, tau) == eb().ERR_OVERFLOW
+        assert ctx.overflow_info() == (lit.overflow_rows, lit.required_width)
+
+
 @pytest.mark.parametrize("window", [32, 64, 256])
 @pytest.mark.parametrize("beta", [0.0, 0.5])
 def test_multipass_window_and_stash_bitwise(ellpack_lib, window, beta):
