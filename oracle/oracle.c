@@ -547,8 +547,9 @@ int oracle_sp2(const omat* H, int64_t nocc, double tol, const osp2_opts* o, omat
     R.emin = emin; R.emax = emax;
     if (!(Dl > 0.0) || !isfinite(Dl)) { if (rep) *rep = R; return O_BOUNDS; }
     double alpha = -1.0 / Dl, beta = emax / Dl;
-    int32_t maxw = o->max_width > 0 ? o->max_width : (int32_t)n;
-    int32_t w = o->initial_width > 0 ? o->initial_width : H->w;
+    /* widths are even (reading R20: the ABI's ELLPACK widths are even, 16-byte slot pairs) */
+    int32_t maxw = ((o->max_width > 0 ? o->max_width : (int32_t)n) + 1) & ~1;
+    int32_t w = ((o->initial_width > 0 ? o->initial_width : H->w) + 1) & ~1;
     /* X0 = drop(alpha*H + beta*I) computed at width H.w + 1 (always enough: a row of H
      * plus its diagonal); its max kept count decides FAIL / GROW against the width w. */
     omat T, X, Y;
