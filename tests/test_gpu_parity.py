@@ -358,6 +358,48 @@ def test_add_family_trace_fnorm_gershgorin(ctx):
     assert abs(f_g - f_o) <= 1e-12 * f_o
 
 
+@pytest.mark.parametrize("seed", range(8))
+def test_glue_ops_fuzz_bitwise(ctx, seed):
+    """Seeded random shapes for the SP2 glue (§8a-a6, §8c-c6..c8): add, add_identity,
+    scale_add_identity (incl. OVERFLOW reports), trace, Gershgorin; bitwise vs the oracle."""
+    rng = np.random.default_rng(7000 + seed)
+    n = int(rng.choice([1, 5, 33, 256, 257, 1500, 4099]))
+    w = int(rng.choice([2, 4, 16, 40, 64, 130]))
+    kmax = int(rng.integers(0, w + 1))
+    kmin = int(rng.integers(0, kmax + 1))
+    band = int(rng.choice([1, 3, 60, 5000]))
+    pe = float(rng.choice([0.0, 0.2]))
+    A = synth.random_sparse(n, w, kmin, kmax, band, pe, float(rng.choice([1e-3, 1.0, 50.0])), seed=seed * 3 + 1)
+    B = synth.random_sparse(n, w, kmin, kmax, band, pe, 1.0, seed=seed * 3 + 2)
+    alpha, beta = float(rng.normal()), float(rng.normal())
+    tau = float(rng.choice([0.0, 1e-6, 1e-2, 0.5]))
+    wo = int(rng.choice([w, w + 2, 2 * w]))
+    for op in ("add", "add_identity", "scale_add_identity"):
+        Ao = A.widened(wo)
+        if op == "add":
+            r = oracle.add(Ao, B, alpha, beta, tau)
+            g = up(A, w=wo)
+            st = ctx.add(g, up(B), alpha, beta, tau)
+        elif op == "add_identity":
+            r = oracle.add_identity(Ao, beta, tau)
+            g = up(A, w=wo)
+            st = ctx.add_identity(g, beta, tau)
+        else:
+            r = oracle.scale_add_identity(Ao, alpha, beta, tau)
+            g = up(A, w=wo)
+            st = ctx.scale_add_identity(g, alpha, beta, tau)
+        if r.status == oracle.OK:
+            assert st == eb().OK, op
+            assert same_bits(g.to_host(), Ao), op
+        else:
+            assert st == eb().ERR_OVERFLOW, op
+            assert ctx.overflow_info() == (r.overflow_rows, r.required_width), op
+    assert same_bits_scalar(ctx.trace(up(A)), oracle.trace(A))
+    lo, hi = ctx.gershgorin(up(A))
+    olo, ohi = oracle.gershgorin(A)
+    assert same_bits_scalar(lo, olo) and same_bits_scalar(hi, ohi)
+
+
 @pytest.mark.parametrize("case", load_golden("hand_vectors.json") + load_golden("spec_examples.json"),
                          ids=lambda c: c["id"])
 def test_golden_vectors_on_gpu(ctx, case):
