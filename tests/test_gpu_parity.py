@@ -358,6 +358,30 @@ def test_add_family_trace_fnorm_gershgorin(ctx):
     assert abs(f_g - f_o) <= 1e-12 * f_o
 
 
+@pytest.mark.parametrize("seed", range(10))
+def test_x2_fuzz_bitwise(ctx, seed):
+    """Seeded random (non-symmetric) X for the x2 entry point: output, tr X and tr X^2 bitwise
+    (both paths: B rows up to 300 entries, half-bandwidths up to beyond any ring)."""
+    rng = np.random.default_rng(9100 + seed)
+    n = int(rng.choice([1, 2, 63, 300, 1025, 4000, 9000]))
+    w = int(rng.choice([2, 8, 32, 128, 256, 300]))
+    kmax = int(rng.integers(1, w + 1))
+    kmin = int(rng.integers(0, kmax + 1))
+    band = int(rng.choice([2, 20, 700, 9000]))
+    X = synth.random_sparse(n, w, kmin, kmax, band, float(rng.choice([0.0, 0.3])), 1.0, seed=seed + 40)
+    tau = float(rng.choice([0.0, 1e-5, 1e-1]))
+    lit = oracle.x2(X, synth.Ell.empty(n, w), tau)
+    wo = max(2, ((lit.required_width + 31) // 32) * 32)
+    Y = synth.Ell.empty(n, wo)
+    r = oracle.x2(X, Y, tau)
+    assert r.status == oracle.OK
+    y = eb().Mat.empty(n, wo)
+    st, tx, tx2 = ctx.multiply_x2(up(X), y, tau)
+    assert st == eb().OK
+    assert same_bits_scalar(tx, r.trace_x) and same_bits_scalar(tx2, r.trace_x2)
+    assert same_bits(y.to_host(), Y)
+
+
 @pytest.mark.parametrize("seed", range(8))
 def test_glue_ops_fuzz_bitwise(ctx, seed):
     """Seeded random shapes for the SP2 glue (§8a-a6, §8c-c6..c8): add, add_identity,
