@@ -9,4 +9,5 @@ timeout 900 python bench.py --workload sp2 --sp2-cfg 3 --steps 3 --warmup 1 > gp
 timeout 900 python bench.py --workload sp2 --sp2-cfg 4 --sp2-iters 6 --steps 2 --warmup 1 > gpurun_out/bench_sp2_cfg4.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:row_fast -s 1 -c 1 -o gpurun_out/x2_full python tools/prof_one.py --n 262144 --m 256 --reps 2 > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:row_general -s 4 -c 1 -o gpurun_out/sp2_general python bench.py --workload sp2 --sp2-cfg 4 --sp2-iters 6 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_general.log 2>&1
 echo done
