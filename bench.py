@@ -56,6 +56,11 @@ def ncu_traffic(workload: str):
     return None
 
 
+def ncu_l2_hit(workload: str):
+    """L2 hit rates (all sectors / reads) of the same capture (north star (4): HBM GB/s and L2 hit rate)."""
+    return ncu_traffic(f"{workload}_l2_hit_pct")
+
+
 class ClockSampler:
     """SM clocks + throttle reasons sampled DURING the timed region: NVML every 10 ms (the timed
     region of a default run is ~0.1 s), nvidia-smi every 0.2 s if NVML is unavailable."""
@@ -332,6 +337,7 @@ def run_ours(args):
             "hbm_gbs_algorithmic": Bc / (ms_step * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
+                         "l2_hit_pct": ncu_l2_hit(f"x2_n{n}_m{args.m}"),
                          "kernel": "ell::row_fast_kernel", "kernel_ms_avg": kern_avg,
                          "algorithmic_bytes_per_launch": bytes_launch},
             "cpu_baseline": cpu,
