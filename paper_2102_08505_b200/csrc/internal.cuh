@@ -59,6 +59,7 @@ struct RowOpParams {
     double* normsq;   // sum over the union of (s_ij - old_ij)^2   (old_mode != 0)
     int32_t* status;  // [0] overflow rows, [1] max kept count
     unsigned long long* row_ticket;  // fast kernel: dynamic row counter (zeroed before each launch)
+    int32_t row_chunk;               // fast kernel: consecutive rows per ticket (4; 1 for small launches)
     // per-warp global scratch: in-place rows are copied aside (stash) before they are rewritten
     double* st_val;
     int32_t* st_col;

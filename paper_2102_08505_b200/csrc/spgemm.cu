@@ -1028,10 +1028,6 @@ __device__ __forceinline__ void flush_status(const RowOpParams& p, int lane, int
     }
 }
 
-#ifndef ELL_ROW_CHUNK
-#define ELL_ROW_CHUNK 4
-#endif
-constexpr int kRowChunk = ELL_ROW_CHUNK;  // fast kernel: rows per ticket
 
 // Next ticket (relative to row_begin) for this warp: lane 0 takes it, all lanes get it.
 __device__ __forceinline__ int64_t next_row(const RowOpParams& p, int lane) {
@@ -1053,11 +1049,13 @@ __global__ void __launch_bounds__(32, 8) row_fast_kernel(const RowOpParams p) {
     int32_t my_max_kept = 0, my_ovf = 0;
     // Rows are handed out dynamically (one atomic per row): 6 resident warps share 4 schedulers
     // unevenly (2, 2, 1, 1), so a static stride would leave the lone warps idle at the tail.
-    // Tickets hand out chunks of kRowChunk consecutive rows (fewer atomics on the critical path,
+    // Tickets hand out chunks of p.row_chunk consecutive rows (fewer atomics on the critical path,
     // neighbouring rows share B records in L2).
-    for (int64_t i0 = p.row_begin + kRowChunk * next_row(p, lane); i0 < p.row_end;
-         i0 = p.row_begin + kRowChunk * next_row(p, lane))
-    for (int64_t i = i0; i < i0 + kRowChunk && i < p.row_end; ++i) {
+    // (p.row_chunk: 4, or 1 when a launch has < 64 rows per warp so the tail stays short)
+    const int chunk = p.row_chunk;
+    for (int64_t i0 = p.row_begin + chunk * next_row(p, lane); i0 < p.row_end;
+         i0 = p.row_begin + chunk * next_row(p, lane))
+    for (int64_t i = i0; i < i0 + chunk && i < p.row_end; ++i) {
         RowIO r = row_io<MODE>(p, i);
         const double dA = p.diag_a ? stored_diag_a(r, lane, i) : 0.0;
         if (p.stash_a || p.stash_old) {
