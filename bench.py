@@ -375,6 +375,8 @@ def run_sp2(args):
     ctx = eb.Context(dev)
     if args.general_window:
         ctx.set_option(eb.OPT_GENERAL_WINDOW, args.general_window)
+    if args.no_sp2_symmetric:
+        ctx.set_option(eb.OPT_SP2_SYMMETRIC, 0)
     if args.sp2_model:
         # the paper's own gapped SP2 workloads, run to the stop rule
         H = synth.model_hamiltonian(args.sp2_n, args.sp2_model, tau_store=1e-5)
@@ -466,6 +468,8 @@ def main():
                     help="SP2 on the paper's model Hamiltonian instead of cfg3/cfg4")
     ap.add_argument("--sp2-n", type=int, default=16384)
     ap.add_argument("--general-window", type=int, default=0, help="general-path window (0 = auto)")
+    ap.add_argument("--no-sp2-symmetric", action="store_true",
+                    help="SP2: compute whole rows even when H is symmetric (A/B of §8f-f4 ii)")
     args = ap.parse_args()
     if args.workload == "sp2":
         if args.impl == "reference":

@@ -110,9 +110,16 @@ int ellpack_ctx_set_stream(ellpack_ctx ctx, void* stream);
  *                          [0, N), strictly ascending; values finite; §8c-c1) and returns
  *                          ELLPACK_ERR_ARG on a violation (one extra kernel and one
  *                          synchronising read-back per operand set). 0 = inputs trusted
- *                          (default). */
+ *                          (default).
+ *  ELLPACK_OPT_SP2_SYMMETRIC  1 (default): sp2_run on one rank with the GROW policy checks H for
+ *                          bitwise symmetry; if symmetric, every SP2 step that runs on the general
+ *                          (wide-row) path computes only the upper triangle of X_{n+1} (columns
+ *                          j >= i) and mirrors it (§8f-f4 ii; X_n symmetric => X_n^2 bitwise
+ *                          symmetric, P4), about half the products. Results are bitwise those of
+ *                          the full computation. 0: always compute whole rows. */
 enum { ELLPACK_OPT_WINDOW = 1, ELLPACK_OPT_WARPS = 2, ELLPACK_OPT_SP2_WIDTH0 = 3, ELLPACK_OPT_PROFILE = 4,
-       ELLPACK_OPT_ABLATE = 5, ELLPACK_OPT_GENERAL_WINDOW = 6, ELLPACK_OPT_VALIDATE = 7 };
+       ELLPACK_OPT_ABLATE = 5, ELLPACK_OPT_GENERAL_WINDOW = 6, ELLPACK_OPT_VALIDATE = 7,
+       ELLPACK_OPT_SP2_SYMMETRIC = 8 };
 int ellpack_ctx_set_option(ellpack_ctx ctx, int key, int64_t value);
 
 /* Accumulated device time (ms, CUDA events on the ctx stream) and launch count of

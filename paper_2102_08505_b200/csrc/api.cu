@@ -91,6 +91,8 @@ struct ellpack_ctx_s {
     cudaStream_t stream = nullptr;
     int num_sms = 148;
     int window_opt = 0, warps_opt = 0, sp2_width0 = 0, ablate = 0, general_s = 0, validate = 0;
+    int sp2_sym = 1;     // ELLPACK_OPT_SP2_SYMMETRIC
+    int last_upper = 0;  // the last row op computed the upper triangle only
     int64_t launches = 0;
     // small device/pinned blocks
     int32_t* d_status = nullptr;              // [0] ovf rows, [1] max kept
@@ -100,6 +102,7 @@ struct ellpack_ctx_s {
     LaunchCfg last_cfg{};
     struct Host {
         int32_t bw[6];
+        int32_t status_u[2];
         int32_t status[2];
         unsigned long long keys[2];
         double sums[8];
@@ -115,7 +118,8 @@ struct ellpack_ctx_s {
     Buf bt, bt_nbin, bp;
     Buf halo;  // all ranks' referenced row ranges (halo exchange)
     Buf vflag; // ELLPACK_OPT_VALIDATE violation flag
-    Buf it[3][3];  // SP2 iterate buffers (val, col, nnz) x 3 slots                         // bank-balanced copy of B (fast path)
+    Buf symaux; // symmetric SP2 step: [0] H asymmetric flag, [1] U reach, [2..3] U status
+    Buf it[4][3];  // SP2 iterate buffers (val, col, nnz) x 3 slots                         // bank-balanced copy of B (fast path)
     // ring sizing cache: (hB, G, mode) -> (S, rows resident per SM)
     int64_t ring_key = -1;
     int ring_S = 0;
@@ -313,6 +317,17 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
     LaunchCfg cfg;
     CK(plan_row_op(p, (int)S, groups, c->warps_opt, c->num_sms, &cfg));
     p.S = cfg.S;
+    // symmetric SP2 step (f4 ii): a general-path launch computes only the upper triangle, into
+    // C_upper; the ring path computes whole rows
+    c->last_upper = 0;
+    if (p.upper) {
+        if (p.fast) {
+            p.upper = 0;
+        } else {
+            p.C = p.C_upper;
+            c->last_upper = 1;
+        }
+    }
     if (p.fast) {
         // bank-balanced copy of B with ring slots precomputed for this S (all N rows: B is the
         // full operand on every rank)
@@ -552,7 +567,7 @@ int ellpack_ctx_destroy(ellpack_ctx c) {
     Buf* bufs[] = {&c->rows[0], &c->rows[1], &c->rows[2], &c->rows[3], &c->partials,
                    &c->stash_val, &c->stash_col, &c->ident_val, &c->ident_col, &c->ident_nnz,
                    &c->hx_val, &c->hx_col, &c->hx_nnz, &c->hy_val, &c->hy_col, &c->hy_nnz,
-                   &c->bt, &c->bt_nbin, &c->bp, &c->halo, &c->vflag};
+                   &c->bt, &c->bt_nbin, &c->bp, &c->halo, &c->vflag, &c->symaux};
     for (auto& sl : c->it)
         for (Buf& b : sl) release(c, b);
     for (Buf* b : bufs) release(c, *b);
@@ -579,6 +594,7 @@ int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
     switch (key) {
         case ELLPACK_OPT_WINDOW: c->window_opt = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_VALIDATE: c->validate = v != 0; return ELLPACK_OK;
+        case ELLPACK_OPT_SP2_SYMMETRIC: c->sp2_sym = v != 0; return ELLPACK_OK;
         case ELLPACK_OPT_WARPS: c->warps_opt = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_SP2_WIDTH0: c->sp2_width0 = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_ABLATE:
@@ -1032,13 +1048,29 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     int32_t w = c->sp2_width0 > 0 ? c->sp2_width0 : (o.initial_width > 0 ? o.initial_width : h->w);
     w = (w + 1) & ~1;
     const double t_read_end = now_s();
-    DevMatrix X, Y, T;
+    DevMatrix X, Y, T, U;
     X.slot = 0;
     Y.slot = 1;
     T.slot = 2;
+    U.slot = 3;  // symmetric step: the upper triangle of X_{n+1}
     int status = ELLPACK_OK;
     int32_t req = 0;
-    auto cleanup = [&]() { dm_free(c, X); dm_free(c, Y); dm_free(c, T); };
+    auto cleanup = [&]() { dm_free(c, X); dm_free(c, Y); dm_free(c, T); dm_free(c, U); };
+    // Symmetric step (§8f-f4 ii): with H bitwise symmetric every iterate is (P4), so general-path
+    // steps compute only the upper triangle and mirror it. Single rank, GROW policy (FAIL needs the
+    // exact overflow row count of a step, which a truncated upper triangle cannot give).
+    bool sym = false, sym_off = false;
+    if (c->sp2_sym && !c->comm && o.on_overflow == SP2_GROW) {
+        RK(grow(c, c->symaux, 4 * sizeof(int32_t)));
+        int32_t* aux = (int32_t*)c->symaux.p;
+        CK(cudaMemsetAsync(aux, 0, sizeof(int32_t), c->stream));
+        CK(launch_sym_check(kmat(h), n, aux, c->stream));
+        c->launches++;
+        int32_t asym = 1;
+        CK(cudaMemcpyAsync(&asym, aux, sizeof asym, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        sym = asym == 0;
+    }
     int rc = sp2_make_x0(c, h, alpha0, beta0, o.threshold, T, &req);
     if (rc) { cleanup(); return rc; }
     if (req > w) {
@@ -1133,8 +1165,28 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             p.diag_s = (double*)c->rows[0].p;
             p.diag_c = (double*)c->rows[1].p;
             p.normsq = (double*)c->rows[2].p;
+            if (sym && !sym_off) {
+                if (!U.owned || U.d.w < Y.d.w) {
+                    if ((rc = dm_alloc(c, U, n, Y.d.w))) { status = rc; break; }
+                }
+                p.upper = 1;  // taken only if the general path runs (enqueue_row_op)
+                p.C_upper = kout(&U.d);
+            }
             cudaEventRecord(c->ev[0], c->stream);
             if ((rc = enqueue_row_op(c, p, n))) { status = rc; break; }
+            const bool upper = c->last_upper != 0;
+            if (upper) {
+                // U's status aside, then X_{n+1} row i = L_i || U_i with the step's status
+                int32_t* aux = (int32_t*)c->symaux.p;
+                CK(cudaMemcpyAsync(aux + 2, c->d_status, 2 * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream));
+                CK(cudaMemcpyAsync(c->h->status_u, aux + 2, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+                CK(cudaMemsetAsync(c->d_status, 0, 2 * sizeof(int32_t), c->stream));
+                CK(cudaMemsetAsync(aux + 1, 0, sizeof(int32_t), c->stream));
+                CK(launch_upper_reach(kmat(&U.d), r0, r1, aux + 1, c->stream));
+                CK(launch_sym_assemble(kmat(&U.d), kmat(&X.d), kout(&Y.d), r0, r1, aux + 1, p.diag_s, p.normsq,
+                                       c->d_status, c->num_sms, c->stream));
+                c->launches += 2;
+            }
             cudaEventRecord(c->ev[1], c->stream);
             if ((rc = reduce_status(c))) { status = rc; break; }
             if (closest) {
@@ -1152,6 +1204,20 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             cudaEventElapsedTime(&ms2, c->ev[1], c->ev[2]);
             t_x2 += ms1 * 1e-3;
             t_norm += ms2 * 1e-3;
+            if (upper && c->h->status_u[0] > 0) {
+                // the upper triangle overflowed its buffer (so does X_{n+1}): the step's counts are
+                // not exact -- grow the physical width (or, at the ceiling, take the full path) and
+                // redo the step before any logical decision
+                if (wcap >= maxw) {
+                    sym_off = true;
+                } else {
+                    const int64_t want = round_up32((int64_t)c->h->status_u[1] * 4);
+                    wcap = (int32_t)std::min<int64_t>(maxw, std::max<int64_t>(want, (int64_t)wcap * 2));
+                    if ((rc = dm_alloc(c, Y, n, wcap))) { status = rc; break; }
+                }
+                redo = true;
+                continue;
+            }
             kept_max = c->h->status[1];
             if (kept_max > wy) {
                 // the logical width grows (the oracle's regrow)

@@ -60,6 +60,8 @@ struct RowOpParams {
     int32_t* status;  // [0] overflow rows, [1] max kept count
     unsigned long long* row_ticket;  // fast kernel: dynamic row counter (zeroed before each launch)
     int32_t row_chunk;               // fast kernel: consecutive rows per ticket (4; 1 for small launches)
+    int32_t upper;                   // general kernel: columns j >= i only (symmetric SP2 step, f4 ii)
+    KOut C_upper;                    // upper-triangle output when the general path takes `upper`
     // per-warp global scratch: in-place rows are copied aside (stash) before they are rewritten
     double* st_val;
     int32_t* st_col;
@@ -89,6 +91,15 @@ cudaError_t launch_balance(KMat b, int64_t k0, int64_t k1, int wt, int S, unsign
 // A's rows r0..r1 reference B rows [INT_MAX - out[4], out[5] - 1] (out[0..5] zeroed by the caller)
 cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64_t r1, int64_t n,
                              int32_t* out, cudaStream_t s);
+
+// symmetric SP2 step (f4 ii): is h bitwise symmetric (ok[0] stays 0); reach of U's rows
+cudaError_t launch_sym_check(KMat h, int64_t n, int32_t* bad, cudaStream_t s);
+cudaError_t launch_upper_reach(KMat u, int64_t r0, int64_t r1, int32_t* reach, cudaStream_t s);
+// row i of Y = L_i (column i of the rows j < i of U, ascending j) followed by U_i; status as the
+// row kernel (rows over Y.w, max kept); normsq (nullable): upper-triangle norm -> full norm
+cudaError_t launch_sym_assemble(KMat u, KMat x, KOut y, int64_t r0, int64_t r1, const int32_t* reach,
+                                const double* diag_s, double* normsq, int32_t* status, int num_sms,
+                                cudaStream_t s);
 
 // reduce.cu
 cudaError_t launch_block_partials(const double* const* arrays, int narr, int64_t row_begin,

@@ -1127,7 +1127,9 @@ __global__ void __launch_bounds__(128, ELL_GEN_MINB) row_general_kernel(const Ro
                 lo = min(lo, o_col[0]);
                 hi = max(hi, o_col[nOld - 1]);
             }
-            lo = warp_min(lo) & ~1;  // even window start (16-byte slot pairs)
+            lo = warp_min(lo);
+            if (p.upper) lo = max(lo, (int)i);  // symmetric step: columns j >= i only
+            lo &= ~1;  // even window start (16-byte slot pairs)
             hi = warp_max(hi);
             if (hi >= lo) {
                 const bool multi = hi / S > lo / S;  // more than one aligned window
@@ -1147,6 +1149,14 @@ __global__ void __launch_bounds__(128, ELL_GEN_MINB) row_general_kernel(const Ro
                 }
                 __syncwarp();
                 int old_cur = 0;
+                if (MODE != 0 && p.upper) {  // Old entries below the diagonal belong to L_i
+                    int lo_o = 0, hi_o = nOld;
+                    while (lo_o < hi_o) {
+                        const int mid = (lo_o + hi_o) >> 1;
+                        if (o_col[mid] < (int)i) lo_o = mid + 1; else hi_o = mid;
+                    }
+                    old_cur = lo_o;
+                }
                 const int np = p.bp_np;
                 for (int pass = lo / S; pass <= hi / S; ++pass) {
                     const int c0 = pass * S;
@@ -1165,6 +1175,16 @@ __global__ void __launch_bounds__(128, ELL_GEN_MINB) row_general_kernel(const Ro
                                 const int32_t* bpk = p.bp + (size_t)k * np + pass;
                                 sb = __ldg(bpk);
                                 se = __ldg(bpk + 1);
+                                if (p.upper && c0 <= (int)i && (int64_t)i < (int64_t)c0 + S) {
+                                    // first entry of B row k with column >= i
+                                    const int32_t* bck = p.B.col + (size_t)k * p.B.w;
+                                    int lo_b = sb, hi_b = se;
+                                    while (lo_b < hi_b) {
+                                        const int mid = (lo_b + hi_b) >> 1;
+                                        if (__ldg(bck + mid) < (int)i) lo_b = mid + 1; else hi_b = mid;
+                                    }
+                                    sb = lo_b;
+                                }
                             }
                             const bool ne = se > sb;
                             const unsigned m = __ballot_sync(FULL, ne);
@@ -1237,6 +1257,138 @@ cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64
                              int32_t* out, cudaStream_t s) {
     (void)nmat;
     bandwidth_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, c, r0, r1, n, out);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ symmetric SP2 step (f4 ii)
+// S = X^2 of a bitwise-symmetric X is bitwise symmetric (each s_ji is the same fma chain over the
+// same products as s_ij, P4), and so is X_{n+1}. The row kernel then computes only U_i (columns
+// j >= i, upper = 1) and row i of X_{n+1} is L_i || U_i with L_i = column i of the rows j < i.
+
+// bad[0] = 1 unless every stored (i, j, v) has a stored (j, i) with identical bits.
+__global__ void sym_check_kernel(KMat h, int64_t n, int32_t* bad) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int nz = h.nnz[i];
+    bool ok = true;
+    for (int q = 0; q < nz && ok; ++q) {
+        const int j = h.col[(size_t)i * h.w + q];
+        const int32_t* cj = h.col + (size_t)j * h.w;
+        int lo = 0, hi = h.nnz[j];
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (cj[mid] < (int)i) lo = mid + 1; else hi = mid;
+        }
+        ok = lo < h.nnz[j] && cj[lo] == (int)i &&
+             __double_as_longlong(h.val[(size_t)j * h.w + lo]) == __double_as_longlong(h.val[(size_t)i * h.w + q]);
+    }
+    if (!ok) atomicOr(bad, 1);
+}
+
+cudaError_t launch_sym_check(KMat h, int64_t n, int32_t* bad, cudaStream_t s) {
+    sym_check_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h, n, bad);
+    return cudaGetLastError();
+}
+
+// reach[0] = max over rows j of (last column of U_j) - j  (the L_i gather range)
+__global__ void upper_reach_kernel(KMat u, int64_t r0, int64_t r1, int32_t* reach) {
+    const int64_t j = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int v = 0;
+    if (j < r1) {
+        const int nz = u.nnz[j];
+        if (nz > 0) v = max(0, (int)(u.col[(size_t)j * u.w + nz - 1] - j));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+    if ((threadIdx.x & 31) == 0 && v > 0) atomicMax(reach, v);
+}
+
+cudaError_t launch_upper_reach(KMat u, int64_t r0, int64_t r1, int32_t* reach, cudaStream_t s) {
+    const int64_t rows = r1 - r0;
+    if (rows <= 0) return cudaSuccess;
+    upper_reach_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(u, r0, r1, reach);
+    return cudaGetLastError();
+}
+
+// Warp per row i: L_i by testing the candidate rows j in [i - reach, i) 32 at a time (binary search
+// of column i in U_j; a ballot keeps ascending j), then U_i; status and the full Frobenius term.
+__global__ void __launch_bounds__(256) sym_assemble_kernel(KMat u, KMat x, KOut y, int64_t r0, int64_t r1,
+                                                           const int32_t* reach_p, const double* diag_s,
+                                                           double* normsq, int32_t* status) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int reach = *reach_p;
+    int32_t my_max = 0, my_ovf = 0;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = r0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < r1; i += nw) {
+        double* yv = y.val + (size_t)i * y.w;
+        int32_t* yc = y.col + (size_t)i * y.w;
+        int kept = 0;
+        const int64_t j0 = i - reach > 0 ? i - reach : 0;
+        for (int64_t jb = j0; jb < i; jb += 32) {
+            const int64_t j = jb + lane;
+            bool found = false;
+            double v = 0.0;
+            if (j < i) {
+                const int nz = u.nnz[j];
+                const int32_t* cj = u.col + (size_t)j * u.w;
+                if (nz > 0 && cj[nz - 1] >= (int)i) {
+                    int lo = 0, hi = nz;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (cj[mid] < (int)i) lo = mid + 1; else hi = mid;
+                    }
+                    if (cj[lo] == (int)i) { found = true; v = u.val[(size_t)j * u.w + lo]; }
+                }
+            }
+            const unsigned m = __ballot_sync(FULL, found);
+            const int pos = kept + __popc(m & lt);
+            if (found && pos < y.w) { yv[pos] = v; yc[pos] = (int32_t)j; }
+            kept += __popc(m);
+        }
+        const int nu = u.nnz[i];
+        for (int q = lane; q < nu; q += 32) {
+            const int pos = kept + q;
+            if (pos < y.w) {
+                yv[pos] = u.val[(size_t)i * u.w + q];
+                yc[pos] = u.col[(size_t)i * u.w + q];
+            }
+        }
+        kept += nu;
+        if (lane == 0) {
+            y.nnz[i] = kept < y.w ? kept : y.w;
+            if (normsq) {
+                // upper norm counted (s - x)^2 once for j > i and once for j = i: full = 2 up - diag
+                const int nx = x.nnz[i];
+                const int32_t* cx = x.col + (size_t)i * x.w;
+                int lo = 0, hi = nx;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (cx[mid] < (int)i) lo = mid + 1; else hi = mid;
+                }
+                const double xd = (lo < nx && cx[lo] == (int)i) ? x.val[(size_t)i * x.w + lo] : 0.0;
+                const double d = __dsub_rn(diag_s[i], xd);
+                normsq[i] = __fma_rn(2.0, normsq[i], -__dmul_rn(d, d));
+            }
+        }
+        my_max = max(my_max, kept);
+        if (kept > y.w) ++my_ovf;
+    }
+    if (lane == 0) {
+        if (my_ovf) atomicAdd(status, my_ovf);
+        if (my_max) atomicMax(status + 1, my_max);
+    }
+}
+
+cudaError_t launch_sym_assemble(KMat u, KMat x, KOut y, int64_t r0, int64_t r1, const int32_t* reach,
+                                const double* diag_s, double* normsq, int32_t* status, int num_sms,
+                                cudaStream_t s) {
+    const int64_t rows = r1 - r0;
+    if (rows <= 0) return cudaSuccess;
+    const int64_t blocks = (rows + 7) / 8;
+    const int64_t cap = (int64_t)num_sms * 8;
+    sym_assemble_kernel<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, s>>>(u, x, y, r0, r1, reach, diag_s,
+                                                                                normsq, status);
     return cudaGetLastError();
 }
 
