@@ -26,7 +26,9 @@ def main():
     ap.add_argument("--warps", nargs="+", type=int, default=[0])
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--ablate", nargs="+", type=int, default=[0],
-                    help="timing-only ablations (results wrong): 1 no row stores, 2 no accumulate")
+                    help="timing-only ablations (results wrong; needs a -DELL_ABLATE=1 build, e.g. "
+                         "tools/variants.py ELL_ABLATE=1): 1 no row stores, 2 no accumulate, 4 no gathers, "
+                         "8 no emission")
     args = ap.parse_args()
     eb.build()
     for sz in args.sizes:
