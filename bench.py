@@ -146,6 +146,27 @@ def x2_bytes(nnz_x: int, nnz_c: int, n: int) -> int:
     return 12 * (nnz_x + nnz_c) + 8 * n
 
 
+def lsu_floor(X, P: int, nnz_c: int, sm_mhz, num_sms: int = 148) -> dict:
+    """The ring kernel's L1/LSU data-pipe floor: one 128-byte wavefront per
+    SM-cycle; per product a 64-bit LDS + STS on the ring (4 wavefronts per 32 lanes) and a 12-byte
+    B record gather; per output-span column one read-and-clear (2 per 32); per kept entry 12 bytes
+    stored. Conflict-free, unpadded counts: the floor a perfect schedule would meet."""
+    nnz = X.nnz.astype(np.int64)
+    live = nnz > 0
+    rows = np.flatnonzero(live)
+    first = X.col[rows, 0].astype(np.int64)
+    last = X.col[rows, nnz[rows] - 1].astype(np.int64)
+    hB = int(max((rows - first).max(initial=0), (last - rows).max(initial=0)))
+    lo = np.maximum(0, first - hB) & ~31
+    hi = (np.minimum(X.n - 1, last + hB) + 32) & ~31
+    cols = int((hi - lo).sum())
+    wf = P * (4 / 32 + 12 / 128) + cols * (2 / 32) + nnz_c * (12 / 128)
+    if not sm_mhz:
+        return {"wavefronts": wf, "floor_ms": None}
+    return {"wavefronts": wf, "output_span_columns": cols, "sm_mhz": sm_mhz,
+            "floor_ms": wf / (num_sms * sm_mhz * 1e6) * 1e3}
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -324,6 +345,12 @@ def run_ours(args):
         dt = statistics.median([run() for _ in range(3)])
         cpu = {"value": 2.0 * Ps / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": desc}
 
+    clocks = clk.summary()
+    lsu_pipe = None
+    if ws == 1:
+        lsu_pipe = lsu_floor(X, P, nnz_c, clocks.get("sm_mhz"), torch.cuda.get_device_properties(dev).multi_processor_count)
+        if lsu_pipe.get("floor_ms"):
+            lsu_pipe["frac"] = lsu_pipe["floor_ms"] / kern_avg
     if rank == 0:
         line = {
             "metric": "ELLPACK X^2 multiply GFLOP/s", "value": gflops, "unit": "GFLOP/s", "n_gpus": ws,
@@ -339,11 +366,12 @@ def run_ours(args):
                          "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
                          "l2_hit_pct": ncu_l2_hit(f"x2_n{n}_m{args.m}"),
                          "kernel": "ell::row_fast_kernel", "kernel_ms_avg": kern_avg,
-                         "algorithmic_bytes_per_launch": bytes_launch},
+                         "algorithmic_bytes_per_launch": bytes_launch,
+                         "lsu_pipe": lsu_pipe},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
