@@ -424,11 +424,14 @@ __device__ __forceinline__ void accumulate_pipe(const RowOpParams& p, const Warp
     double v0[U], v1[U];
     double a0 = a, a1 = 0.0;
     auto load = [&](int (&j)[U], double (&v)[U]) {
+        // one 64-bit base per round; the U gathers use immediate offsets from it
+        const int32_t* __restrict__ cp = bcol + bo + q0 + lane;
+        const double* __restrict__ vp = bval + bo + q0 + lane;
+        const int rem = e - q0 - lane;  // entries left for this lane's slot 0
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int q = q0 + 32 * u + lane;
-            j[u] = q < e ? __ldg(bcol + bo + q) : -1;
-            v[u] = q < e ? __ldg(bval + bo + q) : 0.0;
+            j[u] = 32 * u < rem ? __ldg(cp + 32 * u) : -1;
+            v[u] = 32 * u < rem ? __ldg(vp + 32 * u) : 0.0;
         }
     };
     auto advance = [&]() -> bool {  // cursor to the next round; false past the last segment
