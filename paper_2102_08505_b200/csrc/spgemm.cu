@@ -34,7 +34,10 @@
 
 namespace ell {
 
-constexpr int kStage = 64;  // general path: A-row entries staged per piece (64: 20 warps/SM at S = 1024)
+#ifndef ELL_GEN_STAGE
+#define ELL_GEN_STAGE 64
+#endif
+constexpr int kStage = ELL_GEN_STAGE;  // general path: A-row entries staged per piece
 #ifndef ELL_SEG_PIPE
 #define ELL_SEG_PIPE 1  // general path: software-pipelined rounds (accumulate_pipe)
 #endif
