@@ -22,7 +22,9 @@
 //       ||S - Old||^2), reduced later in canonical order (reduce.cu).
 // With A = B = Old = X one launch is the fused SP2 step (BJ north_star (2)):
 // SQUARE = (alpha 1, old_mode 2), EXPAND = (alpha -1, beta 2, old_mode 1) since
-// fma(-1, s, 2x) = round(2x - s) exactly (2x is exact).
+// fma(-1, s, 2x) = round(2x - s) exactly (2x is exact). For a bitwise-symmetric X the general
+// kernel can compute only the columns j >= i of each row (p.upper, §8f-f4 ii); the
+// sym_assemble_kernel below then writes each row as its mirrored lower part followed by U_i.
 //
 // Template parameters: G (64-entry groups per B row), HB (steps per register half), MODE
 // (0: no Old operand; 1: Old operand; 2: Old operand + ||S - Old||^2 norm). Whether Old enters
