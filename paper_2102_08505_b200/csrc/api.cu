@@ -969,6 +969,18 @@ void dm_free(ellpack_ctx, DevMatrix& m) { m.owned = false; }
 
 int32_t round_up32(int64_t x) { return (int32_t)((x + 31) & ~int64_t(31)); }
 
+// Physical iterate width `want` (headroom), falling back to `need` when the headroom does not
+// fit in device memory (large N densifying iterates): NOMEM only if `need` does not fit either.
+int dm_alloc_headroom(ellpack_ctx c, DevMatrix& m, int64_t n, int32_t& want, int32_t need) {
+    int rc = dm_alloc(c, m, n, want);
+    if (rc == ELLPACK_ERR_NOMEM && need < want) {
+        cudaGetLastError();  // clear the failed allocation
+        want = need;
+        rc = dm_alloc(c, m, n, want);
+    }
+    return rc;
+}
+
 double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -1135,7 +1147,11 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             branch = (std::fabs(t2 - (double)nocc) < std::fabs((2.0 * trX - t2) - (double)nocc)) ? SP2_SQUARE
                                                                                                 : SP2_EXPAND;
         if (!Y.owned || Y.d.w < wy) {
-            if ((rc = dm_alloc(c, Y, n, wcap > wy ? wcap : wy))) { status = rc; break; }
+            {
+                int32_t want = wcap > wy ? wcap : wy;
+                if ((rc = dm_alloc_headroom(c, Y, n, want, wy))) { status = rc; break; }
+                if (want < wcap) wcap = want;
+            }
         }
         // scalar products of this X^2 (this rank's rows; summed over ranks below)
         CK(cudaMemsetAsync(c->d_keys + 2, 0, 8, c->stream));
@@ -1213,7 +1229,9 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
                 } else {
                     const int64_t want = round_up32((int64_t)c->h->status_u[1] * 4);
                     wcap = (int32_t)std::min<int64_t>(maxw, std::max<int64_t>(want, (int64_t)wcap * 2));
-                    if ((rc = dm_alloc(c, Y, n, wcap))) { status = rc; break; }
+                    const int32_t need = std::min<int32_t>(maxw, std::max<int32_t>(Y.d.w + 32,
+                                                                                   round_up32(c->h->status_u[1])));
+                    if ((rc = dm_alloc_headroom(c, Y, n, wcap, need))) { status = rc; break; }
                 }
                 redo = true;
                 continue;
@@ -1244,7 +1262,8 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
                 const int64_t want = round_up32((int64_t)kept_max * 4);
                 wcap = (int32_t)(want < maxw ? want : maxw);
                 if (wcap < wy) wcap = wy;
-                if ((rc = dm_alloc(c, Y, n, wcap))) { status = rc; break; }
+                const int32_t need = std::max<int32_t>(wy, std::min<int32_t>(maxw, round_up32(kept_max)));
+                if ((rc = dm_alloc_headroom(c, Y, n, wcap, need))) { status = rc; break; }
                 redo = true;
             }
         } while (redo);

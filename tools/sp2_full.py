@@ -48,18 +48,21 @@ def main():
     n = H.n
     ctx = eb.Context(0)
     h = eb.Mat.from_host(H)
-    d = eb.Mat.empty(n, n + (n & 1))
+    d = eb.Mat.empty(n, n + (n & 1) if n <= 20000 else 16384)  # D: OVERFLOW is reported if too narrow
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    r = ctx.sp2_run(h, cf["nocc"], cf["tol"], d, threshold=cf["threshold"], max_iter=a.max_iter)
+    r = ctx.sp2_run(h, cf["nocc"], cf["tol"], d, threshold=cf["threshold"], max_iter=a.max_iter,
+                    ok=(eb.OK, eb.ERR_NOCONV, eb.ERR_OVERFLOW))
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     dev = torch.device("cuda", 0)
-    Dd = dense(d, n, dev)
-    Hd = dense(h, n, dev)
-    idem = torch.linalg.norm(Dd @ Dd - Dd).item()
-    comm = (torch.linalg.norm(Dd @ Hd - Hd @ Dd) / torch.linalg.norm(Hd)).item()
-    tr = torch.trace(Dd).item()
+    idem = comm = tr = None
+    if n <= 20000:  # dense FP64 checks (N^2 doubles, N^3 GEMMs)
+        Dd = dense(d, n, dev)
+        Hd = dense(h, n, dev)
+        idem = torch.linalg.norm(Dd @ Dd - Dd).item()
+        comm = (torch.linalg.norm(Dd @ Hd - Hd @ Dd) / torch.linalg.norm(Hd)).item()
+        tr = torch.trace(Dd).item()
     prods = sum(it["products"] for it in r.iters)
     print(json.dumps({
         "workload": f"{name} SP2 tau={cf['threshold']} tol={cf['tol']} max_iter={a.max_iter} GROW",
