@@ -31,8 +31,11 @@
  *
  * Parity pins: see tests/test_oracle_*.py (dense brute force with exact
  * rational fma, numpy GEMM, closed forms, symmetry, eigh projector, dimer
- * closed form, hand vectors in tests/golden/). Functions without an external
- * pin are marked "parity unpinned" below; currently none.
+ * closed form, hand vectors in tests/golden/; the c6 single rounding and the
+ * c10 (vi) stop rule in tests/test_oracle_pins_c6_c10.py). tools/oracle_mutants.py
+ * applies plausible mistakes to this file and checks that a pin fails for each.
+ * Functions without an external pin are marked "parity unpinned" below;
+ * currently none.
  */
 #include <math.h>
 #include <stdint.h>
