@@ -116,10 +116,15 @@ int ellpack_ctx_set_stream(ellpack_ctx ctx, void* stream);
  *                          (wide-row) path computes only the upper triangle of X_{n+1} (columns
  *                          j >= i) and mirrors it (§8f-f4 ii; X_n symmetric => X_n^2 bitwise
  *                          symmetric, P4), about half the products. Results are bitwise those of
- *                          the full computation. 0: always compute whole rows. */
+ *                          the full computation. 0: always compute whole rows.
+ *  ELLPACK_OPT_SP2_MEM_CAP fault injection: sp2_run treats an iterate allocation as not fitting
+ *                          in device memory when the value arrays of its live iterates (X_n, X_{n+1},
+ *                          the symmetric step's upper triangle) would exceed this many bytes
+ *                          (exercises the fallback from the headroom width to the exact width and the
+ *                          symmetric step's whole-row fallback); 0 = off (default). */
 enum { ELLPACK_OPT_WINDOW = 1, ELLPACK_OPT_WARPS = 2, ELLPACK_OPT_SP2_WIDTH0 = 3, ELLPACK_OPT_PROFILE = 4,
        ELLPACK_OPT_ABLATE = 5, ELLPACK_OPT_GENERAL_WINDOW = 6, ELLPACK_OPT_VALIDATE = 7,
-       ELLPACK_OPT_SP2_SYMMETRIC = 8 };
+       ELLPACK_OPT_SP2_SYMMETRIC = 8, ELLPACK_OPT_SP2_MEM_CAP = 9 };
 int ellpack_ctx_set_option(ellpack_ctx ctx, int key, int64_t value);
 
 /* Accumulated device time (ms, CUDA events on the ctx stream) and launch count of
@@ -128,6 +133,10 @@ int ellpack_ctx_kernel_time(ellpack_ctx ctx, double* row_kernel_ms, int64_t* row
 
 /* Number of kernels this context launched since creation (evidence counter). */
 int64_t ellpack_ctx_kernel_launches(ellpack_ctx ctx);
+
+/* Number of blocking host synchronisations of the context stream since creation (evidence
+ * counter for the SP2 control path: sp2_run waits once per iteration). */
+int64_t ellpack_ctx_host_syncs(ellpack_ctx ctx);
 
 /* --------------------------------------------------------------- storage */
 
@@ -188,7 +197,9 @@ int ellpack_fnorm_diff(ellpack_ctx ctx, const ellpack_desc* a, const ellpack_des
 int ellpack_gershgorin(ellpack_ctx ctx, const ellpack_desc* h, double* emin, double* emax);
 
 /* Details of the last ELLPACK_ERR_OVERFLOW returned on this context
- * (required width = max kept count over rows; overflow rows = #rows kept > w). */
+ * (required width = max kept count over rows; overflow rows = #rows kept > w, exact, also
+ * for sp2_run's FAIL at X0 (rows of X0 over the initial width) and inside the loop (rows of
+ * X_{n+1} over the current width), §8c-c4). */
 int ellpack_overflow_info(ellpack_ctx ctx, int64_t* overflow_rows, int32_t* required_width);
 
 /* ------------------------------------------------------------------ SP2 */
@@ -277,8 +288,12 @@ int ellpack_multiply_x2_host(ellpack_ctx ctx, int64_t n,
 /* NCCL bootstrap: rank 0 calls ellpack_nccl_unique_id and broadcasts the 128
  * bytes (e.g. torch.distributed.broadcast_object_list); every rank then calls
  * ellpack_ctx_attach_nccl (collective). Rows [row_begin,row_end) are this
- * rank's block; blocks must be contiguous, ascending with rank, cover [0,N) and
- * start on multiples of 256 (canonical trace blocks, §8c-c7/c12). */
+ * rank's block. The blocks of all ranks are all-gathered and checked: they must be
+ * contiguous, ascending with rank, EQUAL, a multiple of 256 rows each (canonical
+ * trace blocks and equal all-gather counts, §8c-c7/c12, reading R17) and cover
+ * [0, N) with N = nranks * block; otherwise every rank returns ELLPACK_ERR_ARG and
+ * no communicator is attached. Afterwards every operand of every call must have
+ * n == N (ELLPACK_ERR_DIM otherwise). Errors: ARG, NCCL, CUDA, STATE (already attached). */
 int ellpack_nccl_unique_id(uint8_t id[128]);
 int ellpack_ctx_attach_nccl(ellpack_ctx ctx, int nranks, int rank, const uint8_t id[128],
                             int64_t row_begin, int64_t row_end);

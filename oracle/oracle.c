@@ -568,7 +568,10 @@ int oracle_sp2(const omat* H, int64_t nocc, double tol, const osp2_opts* o, omat
     oracle_scale_add_identity(&T, alpha, beta, tau, &ovf, &req);
     if (req > w) {
         if (o->on_overflow == 0 || req > maxw) {
-            R.stop_reason = 3; R.overflow_rows = -1; R.required_width = req; R.fail_iter = -1;
+            /* c4: overflow_rows = #{i : kept_i > W} with W the width X0 was asked to fit */
+            int64_t over = 0;
+            for (int64_t i = 0; i < n; ++i) over += T.nnz[i] > w;
+            R.stop_reason = 3; R.overflow_rows = over; R.required_width = req; R.fail_iter = -1;
             mat_free(&T); if (rep) *rep = R; return O_OVERFLOW;
         }
         w = round_up32(req) < maxw ? round_up32(req) : maxw;

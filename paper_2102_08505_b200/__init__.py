@@ -28,6 +28,7 @@ _HDRS = [os.path.join(_HERE, "csrc", "internal.cuh"), os.path.join(_REPO, "inclu
 OK, ERR_ARG, ERR_DIM, ERR_OVERFLOW, ERR_BOUNDS, ERR_NOCONV, ERR_NOMEM, ERR_CUDA, ERR_NCCL, ERR_STATE = range(10)
 OPT_WINDOW, OPT_WARPS, OPT_SP2_WIDTH0, OPT_PROFILE, OPT_ABLATE, OPT_GENERAL_WINDOW, OPT_VALIDATE = 1, 2, 3, 4, 5, 6, 7
 OPT_SP2_SYMMETRIC = 8
+OPT_SP2_MEM_CAP = 9
 SP2_FAIL, SP2_GROW = 0, 1
 SP2_RULE_TRACE_SIGN, SP2_RULE_TRACE_CLOSEST = 0, 1
 STOP_NAMES = {0: "CONVERGED", 1: "STAGNATED", 2: "NOCONV", 3: "OVERFLOW"}
@@ -35,7 +36,7 @@ STOP_NAMES = {0: "CONVERGED", 1: "STAGNATED", 2: "NOCONV", 3: "OVERFLOW"}
 # Every symbol include/ellpack.h declares (checked by tests/test_abi.py).
 ABI_SYMBOLS = (
     "ellpack_ctx_create", "ellpack_ctx_destroy", "ellpack_ctx_set_stream", "ellpack_ctx_set_option",
-    "ellpack_ctx_kernel_launches", "ellpack_ctx_kernel_time", "ellpack_create", "ellpack_destroy", "ellpack_multiply",
+    "ellpack_ctx_kernel_launches", "ellpack_ctx_host_syncs", "ellpack_ctx_kernel_time", "ellpack_create", "ellpack_destroy", "ellpack_multiply",
     "ellpack_multiply_x2", "ellpack_add", "ellpack_add_identity", "ellpack_scale_add_identity",
     "ellpack_trace", "ellpack_fnorm_diff", "ellpack_gershgorin", "ellpack_overflow_info", "sp2_run",
     "sp2_opts_default", "ellpack_multiply_x2_host", "ellpack_nccl_unique_id", "ellpack_ctx_attach_nccl",
@@ -116,7 +117,7 @@ def lib() -> ctypes.CDLL:
         D = ctypes.POINTER(Desc)
         sig = {
             "ellpack_ctx_create": [i, P, P], "ellpack_ctx_destroy": [P], "ellpack_ctx_set_stream": [P, P],
-            "ellpack_ctx_set_option": [P, i, i64], "ellpack_ctx_kernel_launches": [P],
+            "ellpack_ctx_set_option": [P, i, i64], "ellpack_ctx_kernel_launches": [P], "ellpack_ctx_host_syncs": [P],
             "ellpack_ctx_kernel_time": [P, P, P],
             "ellpack_create": [P, i64, i32, D], "ellpack_destroy": [P, D],
             "ellpack_multiply": [P, D, D, D, d, d, d], "ellpack_multiply_x2": [P, D, D, d, P, P],
@@ -137,6 +138,7 @@ def lib() -> ctypes.CDLL:
             f.argtypes = args
             f.restype = ctypes.c_int
         L.ellpack_ctx_kernel_launches.restype = ctypes.c_int64
+        L.ellpack_ctx_host_syncs.restype = ctypes.c_int64
         L.ellpack_strerror.restype = ctypes.c_char_p
         L.sp2_opts_default.restype = None
         _lib = L
@@ -251,6 +253,10 @@ class Context:
 
     def kernel_launches(self) -> int:
         return int(lib().ellpack_ctx_kernel_launches(self._h))
+
+    def host_syncs(self) -> int:
+        """Blocking host synchronisations of the context stream so far (evidence counter)."""
+        return int(lib().ellpack_ctx_host_syncs(self._h))
 
     def kernel_time(self):
         """(accumulated row-kernel ms, launches) since OPT_PROFILE was set."""

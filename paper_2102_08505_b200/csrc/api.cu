@@ -94,16 +94,20 @@ struct ellpack_ctx_s {
     int sp2_sym = 1;     // ELLPACK_OPT_SP2_SYMMETRIC
     int last_upper = 0;  // the last row op computed the upper triangle only
     int64_t launches = 0;
+    int64_t host_syncs = 0;   // blocking stream synchronisations (evidence counter, f3)
+    int64_t sp2_mem_cap = 0;  // ELLPACK_OPT_SP2_MEM_CAP: max bytes of the live SP2 iterate value arrays
+    int64_t it_live[4] = {0, 0, 0, 0};  // value-array bytes of each live SP2 iterate slot
+    int sym_nomem = 0;        // the symmetric step's U buffer did not fit (whole rows instead)
     // small device/pinned blocks
     int32_t* d_status = nullptr;              // [0] ovf rows, [1] max kept
     unsigned long long* d_keys = nullptr;     // gershgorin min/max keys; [2] SP2 product count
     double* d_sums = nullptr;                 // final sums (<= 8)
-    int32_t* d_bw = nullptr;                  // bandwidth probe
+    int32_t* d_bw = nullptr;                  // bandwidth probe [0..5]; [8] agreed width (comm)
     LaunchCfg last_cfg{};
     struct Host {
         int32_t bw[6];
         int32_t status_u[2];
-        int32_t status[2];
+        int32_t status[4];
         unsigned long long keys[2];
         double sums[8];
         int32_t imax;
@@ -119,7 +123,8 @@ struct ellpack_ctx_s {
     Buf halo;  // all ranks' referenced row ranges (halo exchange)
     Buf vflag; // ELLPACK_OPT_VALIDATE violation flag
     Buf symaux; // symmetric SP2 step: [0] H asymmetric flag, [1] U reach, [2..3] U status
-    Buf it[4][3];  // SP2 iterate buffers (val, col, nnz) x 3 slots                         // bank-balanced copy of B (fast path)
+    Buf it[4][3];  // SP2 iterate buffers (val, col, nnz) x 4 slots
+    int32_t* h_reach = nullptr;  // pinned: every rank's probe reach (2 per rank), fetched with a step
     // ring sizing cache: (hB, G, mode) -> (S, rows resident per SM)
     int64_t ring_key = -1;
     int ring_S = 0;
@@ -129,6 +134,7 @@ struct ellpack_ctx_s {
     int32_t last_req = 0;
     // row partition
     int64_t row_begin = 0, row_end = -1;
+    int64_t comm_n = 0;  // with a communicator: N of every operand (ranks' equal blocks cover [0, N))
     int nranks = 1, rank = 0;
     ncclComm_t comm = nullptr;
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -160,6 +166,18 @@ int from_cuda(cudaError_t e) {
     do {                                       \
         if ((x) != ncclSuccess) return ELLPACK_ERR_NCCL; \
     } while (0)
+
+// every blocking wait on the context stream goes through here (counted: ellpack_ctx_host_syncs)
+int host_sync(ellpack_ctx c) {
+    c->host_syncs++;
+    CK(cudaStreamSynchronize(c->stream));
+    return ELLPACK_OK;
+}
+
+// With a communicator every operand must be the N x N matrix the ranks' blocks partition.
+int check_comm_n(ellpack_ctx c, int64_t n) {
+    return (c->comm && n != c->comm_n) ? ELLPACK_ERR_DIM : ELLPACK_OK;
+}
 
 int grow(ellpack_ctx c, Buf& b, size_t bytes) {
     if (b.bytes >= bytes) return ELLPACK_OK;
@@ -204,7 +222,7 @@ int validate_inputs(ellpack_ctx c, std::initializer_list<const ellpack_desc*> ds
     }
     int32_t bad = 0;
     CK(cudaMemcpyAsync(&bad, flag, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    RK(host_sync(c));
     return bad ? ELLPACK_ERR_ARG : ELLPACK_OK;
 }
 
@@ -247,26 +265,48 @@ int reduce_status(ellpack_ctx c) {
     return ELLPACK_OK;
 }
 
-// Enqueue one row op (kernel + scratch management). Status is left in d_status.
-// The launch geometry comes from a bandwidth probe (one tiny kernel + a 12-byte read-back):
-// with half-bandwidths hA, hB, hOld every row's products and Old entries lie within
-// i +- h, h = max(hA + hB, hOld), so a row-centred window of S >= 2h + 1 doubles holds the
-// whole row ("fast path", no span pre-pass). Wider rows use the multi-pass general path.
-int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
-    p.ncols = n;
+// Bandwidth probe of a row op, enqueued only (d_bw[0..5], see launch_bandwidth). With a
+// communicator each rank probes its own rows of every operand and the maxima (half-bandwidths,
+// max nnz of B) are all-reduced, so every rank plans the same launch from the global values even
+// when it holds only its block + halo of B; the reach (d_bw[4..5]) stays per rank.
+int enqueue_probe(ellpack_ctx c, const RowOpParams& p, int64_t n) {
     const bool has_old = p.old_mode != 0;
     CK(cudaMemsetAsync(c->d_bw, 0, 6 * sizeof(int32_t), c->stream));
     const KMat none{nullptr, nullptr, nullptr, 0};
-    CK(launch_bandwidth(p.alpha != 0.0 ? p.A : none, p.B, has_old ? p.Old : none,
-                        has_old ? 3 : 2, p.row_begin, p.row_end, n, c->d_bw, c->stream));
+    const int64_t b0 = c->comm ? p.row_begin : 0, b1 = c->comm ? p.row_end : n;
+    CK(launch_bandwidth(p.alpha != 0.0 ? p.A : none, p.B, has_old ? p.Old : none, p.row_begin, p.row_end,
+                        b0, b1, n, c->d_bw, c->stream));
     c->launches++;
-    CK(cudaMemcpyAsync(c->h->bw, c->d_bw, 6 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    const int64_t hB = c->h->bw[1];
-    const int64_t hprod = p.alpha != 0.0 ? (int64_t)c->h->bw[0] + hB : 0;
-    const int64_t h = has_old ? (hprod > c->h->bw[2] ? hprod : c->h->bw[2]) : hprod;
+    if (c->comm) NK(g_nccl.AllReduce(c->d_bw, c->d_bw, 4, ncclInt32, ncclMax, c->comm, c->stream));
+    return ELLPACK_OK;
+}
+
+// Enqueue one row op (kernel + scratch management). Status is left in d_status.
+// The launch geometry comes from a bandwidth probe (one tiny kernel + a 24-byte read-back, or
+// `bw`: the probe values of these operands already on the host, e.g. fetched by the previous SP2
+// step with its status -- then nothing here waits on the device): with half-bandwidths hA, hB,
+// hOld every row's products and Old entries lie within i +- h, h = max(hA + hB, hOld), so a
+// ring of S >= 2 hB + 33 doubles holds the live part of every row ("fast path", progressive
+// emission). Wider rows use the multi-pass general path.
+// alloc_upper (nullable): called when a launch takes the symmetric (upper-triangle) route, to
+// provide p.C_upper; a NOMEM there falls back to whole rows (c->sym_nomem = 1).
+int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw = nullptr,
+                   int (*alloc_upper)(ellpack_ctx, void*, KOut*) = nullptr, void* alloc_arg = nullptr) {
+    p.ncols = n;
+    const bool has_old = p.old_mode != 0;
+    if (!bw) {
+        RK(enqueue_probe(c, p, n));
+        CK(cudaMemcpyAsync(c->h->bw, c->d_bw, 6 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        RK(host_sync(c));
+        bw = c->h->bw;
+    }
+    int32_t bwv[6];
+    memcpy(bwv, bw, sizeof bwv);
+    const int64_t hB = bwv[1];
+    const int64_t hprod = p.alpha != 0.0 ? (int64_t)bwv[0] + hB : 0;
+    const int64_t h = has_old ? (hprod > bwv[2] ? hprod : bwv[2]) : hprod;
     const int64_t nr = (n + 31) & ~int64_t(31);
-    const int maxnb = p.alpha != 0.0 ? c->h->bw[3] : 0;
+    const int maxnb = p.alpha != 0.0 ? bwv[3] : 0;
     const int groups = maxnb <= 64 ? 1 : (maxnb + 63) / 64;
     p.hB = (int32_t)hB;
     p.ablate = c->ablate;
@@ -320,12 +360,20 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
     // symmetric SP2 step (f4 ii): a general-path launch computes only the upper triangle, into
     // C_upper; the ring path computes whole rows
     c->last_upper = 0;
+    c->sym_nomem = 0;
     if (p.upper) {
-        if (p.fast) {
-            p.upper = 0;
-        } else {
+        int rc = (p.fast || !alloc_upper) ? ELLPACK_ERR_ARG : alloc_upper(c, alloc_arg, &p.C_upper);
+        if (rc == ELLPACK_OK) {
             p.C = p.C_upper;
             c->last_upper = 1;
+        } else {
+            p.upper = 0;
+            if (rc == ELLPACK_ERR_NOMEM) {
+                cudaGetLastError();
+                c->sym_nomem = 1;  // whole rows this time; the caller stops asking
+            } else if (!p.fast) {
+                return rc;
+            }
         }
     }
     if (p.fast) {
@@ -336,8 +384,8 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n) {
         RK(grow(c, c->bt_nbin, sizeof(int32_t) * (size_t)n));
         // only the B rows this launch's A rows reference (a rank's block plus its halo; rows a halo
         // exchange did not deliver are never read)
-        const int64_t k0 = std::max<int64_t>(0, (int64_t)INT_MAX - c->h->bw[4]);
-        const int64_t k1 = std::min<int64_t>(n, (int64_t)c->h->bw[5]);
+        const int64_t k0 = std::max<int64_t>(0, (int64_t)INT_MAX - bwv[4]);
+        const int64_t k1 = std::min<int64_t>(n, (int64_t)bwv[5]);
         CK(launch_balance(p.B, k0, k1, wt, p.S, (unsigned char*)c->bt.p, (int32_t*)c->bt_nbin.p, c->num_sms,
                           c->stream));
         c->launches++;
@@ -423,11 +471,19 @@ int enqueue_canonical(ellpack_ctx c, const double* const* arrays, int narr, int6
     return ELLPACK_OK;
 }
 
-int fetch(ellpack_ctx c, int nsums) {
+// One read-back: status, `nsums` canonical sums and, with probe, the bandwidth probe d_bw[0..5]
+// (+ every rank's reach with a communicator); then the one host synchronisation.
+int fetch(ellpack_ctx c, int nsums, bool probe = false) {
     CK(cudaMemcpyAsync(c->h->status, c->d_status, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
     if (nsums > 0)
         CK(cudaMemcpyAsync(c->h->sums, c->d_sums, nsums * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    if (probe) {
+        CK(cudaMemcpyAsync(c->h->bw, c->d_bw, 6 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        if (c->comm)
+            CK(cudaMemcpyAsync(c->h_reach, c->halo.p, 2 * sizeof(int32_t) * c->nranks, cudaMemcpyDeviceToHost,
+                               c->stream));
+    }
+    RK(host_sync(c));
     prof_collect(c);
     return ELLPACK_OK;
 }
@@ -466,26 +522,16 @@ int allgather_desc(ellpack_ctx c, const ellpack_desc* m) {
 // ranges of all ranks are all-gathered (16 bytes each), then every rank sends the part of its own
 // block of `b` each peer reads and receives the parts of the peers' blocks it reads (NCCL
 // point-to-point in one group; the plan is ellpack_halo_plan, identical on both sides of a pair).
-int halo_desc(ellpack_ctx c, const ellpack_desc* a, ellpack_desc* b) {
-    if (!c->comm) return ELLPACK_OK;
+// The send/recv half of the halo exchange, from every rank's referenced rows need[2q..2q+1]
+// (host values, inclusive; need[2q] > need[2q+1] = none). Enqueue only: no host wait.
+int halo_exec(ellpack_ctx c, ellpack_desc* b, const int64_t* need) {
     const int64_t n = b->n;
     int64_t r0, r1;
     rows_of(c, n, &r0, &r1);
     const int P = c->nranks;
-    RK(grow(c, c->halo, sizeof(long long) * 2 * (size_t)P));
-    long long* d_need = (long long*)c->halo.p;
-    long long* mine = d_need + 2 * c->rank;
-    const long long init[2] = {LLONG_MAX, -1};
-    CK(cudaMemcpyAsync(mine, init, sizeof init, cudaMemcpyHostToDevice, c->stream));
-    CK(launch_col_range(kmat(a), r0, r1, mine, c->stream));
-    c->launches++;
-    NK(g_nccl.AllGather(mine, d_need, 2, ncclInt64, c->comm, c->stream));
-    std::vector<long long> need(2 * (size_t)P);
-    CK(cudaMemcpyAsync(need.data(), d_need, sizeof(long long) * 2 * P, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    std::vector<int64_t> needl(need.begin(), need.end()), snd(3 * (size_t)P), rcv(3 * (size_t)P);
+    std::vector<int64_t> snd(3 * (size_t)P), rcv(3 * (size_t)P);
     int32_t ns = 0, nr = 0;
-    RK(ellpack_halo_plan(n, P, c->rank, r1 - r0, needl.data(), &ns, snd.data(), &nr, rcv.data()));
+    RK(ellpack_halo_plan(n, P, c->rank, r1 - r0, need, &ns, snd.data(), &nr, rcv.data()));
     const size_t w = (size_t)b->w;
     NK(g_nccl.GroupStart());
     for (int q = 0; q < ns; ++q) {
@@ -504,6 +550,27 @@ int halo_desc(ellpack_ctx c, const ellpack_desc* a, ellpack_desc* b) {
     }
     NK(g_nccl.GroupEnd());
     return ELLPACK_OK;
+}
+
+int halo_desc(ellpack_ctx c, const ellpack_desc* a, ellpack_desc* b) {
+    if (!c->comm) return ELLPACK_OK;
+    const int64_t n = b->n;
+    int64_t r0, r1;
+    rows_of(c, n, &r0, &r1);
+    const int P = c->nranks;
+    RK(grow(c, c->halo, sizeof(long long) * 2 * (size_t)P));
+    long long* d_need = (long long*)c->halo.p;
+    long long* mine = d_need + 2 * c->rank;
+    const long long init[2] = {LLONG_MAX, -1};
+    CK(cudaMemcpyAsync(mine, init, sizeof init, cudaMemcpyHostToDevice, c->stream));
+    CK(launch_col_range(kmat(a), r0, r1, mine, c->stream));
+    c->launches++;
+    NK(g_nccl.AllGather(mine, d_need, 2, ncclInt64, c->comm, c->stream));
+    std::vector<long long> need(2 * (size_t)P);
+    CK(cudaMemcpyAsync(need.data(), d_need, sizeof(long long) * 2 * P, cudaMemcpyDeviceToHost, c->stream));
+    RK(host_sync(c));
+    std::vector<int64_t> needl(need.begin(), need.end());
+    return halo_exec(c, b, needl.data());
 }
 
 }  // namespace
@@ -578,6 +645,7 @@ int ellpack_ctx_destroy(ellpack_ctx c) {
     cudaFree(c->d_sums);
     cudaFree(c->d_bw);
     if (c->h) cudaFreeHost(c->h);
+    if (c->h_reach) cudaFreeHost(c->h_reach);
     for (int k = 0; k < 6; ++k) if (c->ev[k]) cudaEventDestroy(c->ev[k]);
     delete c;
     return ELLPACK_OK;
@@ -597,6 +665,7 @@ int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
         case ELLPACK_OPT_SP2_SYMMETRIC: c->sp2_sym = v != 0; return ELLPACK_OK;
         case ELLPACK_OPT_WARPS: c->warps_opt = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_SP2_WIDTH0: c->sp2_width0 = (int)v; return ELLPACK_OK;
+        case ELLPACK_OPT_SP2_MEM_CAP: c->sp2_mem_cap = v; return ELLPACK_OK;
         case ELLPACK_OPT_ABLATE:
 #if defined(ELL_ABLATE) && ELL_ABLATE
             c->ablate = (int)v;
@@ -619,6 +688,8 @@ int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
 }
 
 int64_t ellpack_ctx_kernel_launches(ellpack_ctx c) { return c ? c->launches : -1; }
+
+int64_t ellpack_ctx_host_syncs(ellpack_ctx c) { return c ? c->host_syncs : -1; }
 
 int ellpack_ctx_kernel_time(ellpack_ctx c, double* ms, int64_t* launches) {
     if (!c) return ELLPACK_ERR_ARG;
@@ -681,6 +752,7 @@ int ellpack_multiply(ellpack_ctx c, const ellpack_desc* a, const ellpack_desc* b
     RK(check_desc(b));
     RK(check_desc(cm));
     if (a->n != b->n || a->n != cm->n) return ELLPACK_ERR_DIM;
+    RK(check_comm_n(c, a->n));
     if (!valid_tau(tau) || !std::isfinite(alpha) || !std::isfinite(beta)) return ELLPACK_ERR_ARG;
     if (same(cm, a) || same(cm, b)) return ELLPACK_ERR_ARG;
     CK(cudaSetDevice(c->device));
@@ -709,6 +781,7 @@ int ellpack_multiply_x2(ellpack_ctx c, const ellpack_desc* x, ellpack_desc* x2, 
     RK(check_desc(x));
     RK(check_desc(x2));
     if (x->n != x2->n) return ELLPACK_ERR_DIM;
+    RK(check_comm_n(c, x->n));
     if (!valid_tau(tau)) return ELLPACK_ERR_ARG;
     if (same(x, x2)) return ELLPACK_ERR_ARG;
     CK(cudaSetDevice(c->device));
@@ -738,6 +811,7 @@ int ellpack_multiply_x2(ellpack_ctx c, const ellpack_desc* x, ellpack_desc* x2, 
 
 static int add_via_identity(ellpack_ctx c, ellpack_desc* a, const KMat& old, bool old_is_a,
                             double alpha, double beta, double tau) {
+    RK(check_comm_n(c, a->n));
     CK(cudaSetDevice(c->device));
     RK(ensure_identity(c, a->n));
     RowOpParams p = base_params(c, a->n);
@@ -788,6 +862,7 @@ int ellpack_add_identity(ellpack_ctx c, ellpack_desc* a, double beta, double tau
 int ellpack_trace(ellpack_ctx c, const ellpack_desc* a, double* out) {
     if (!c || !out) return ELLPACK_ERR_ARG;
     RK(check_desc(a));
+    RK(check_comm_n(c, a->n));
     CK(cudaSetDevice(c->device));
     RK(validate_inputs(c, {a}));
     const int64_t n = a->n;
@@ -809,6 +884,7 @@ int ellpack_fnorm_diff(ellpack_ctx c, const ellpack_desc* a, const ellpack_desc*
     RK(check_desc(a));
     RK(check_desc(b));
     if (a->n != b->n) return ELLPACK_ERR_DIM;
+    RK(check_comm_n(c, a->n));
     CK(cudaSetDevice(c->device));
     RK(validate_inputs(c, {a, b}));
     const int64_t n = a->n;
@@ -842,7 +918,7 @@ static int gershgorin_impl(ellpack_ctx c, const ellpack_desc* h, double* emin, d
         NK(g_nccl.GroupEnd());
     }
     CK(cudaMemcpyAsync(c->h->keys, c->d_keys, 16, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    RK(host_sync(c));
     *emin = dkey_inv(c->h->keys[0]);
     *emax = dkey_inv(c->h->keys[1]);
     return ELLPACK_OK;
@@ -851,6 +927,7 @@ static int gershgorin_impl(ellpack_ctx c, const ellpack_desc* h, double* emin, d
 int ellpack_gershgorin(ellpack_ctx c, const ellpack_desc* h, double* emin, double* emax) {
     if (!c || !emin || !emax) return ELLPACK_ERR_ARG;
     RK(check_desc(h));
+    RK(check_comm_n(c, h->n));
     CK(cudaSetDevice(c->device));
     RK(validate_inputs(c, {h}));
     return gershgorin_impl(c, h, emin, emax);
@@ -859,6 +936,7 @@ int ellpack_gershgorin(ellpack_ctx c, const ellpack_desc* h, double* emin, doubl
 int ellpack_allgather_rows(ellpack_ctx c, ellpack_desc* m) {
     if (!c) return ELLPACK_ERR_ARG;
     RK(check_desc(m));
+    RK(check_comm_n(c, m->n));
     return allgather_desc(c, m);
 }
 
@@ -890,6 +968,7 @@ int ellpack_halo_rows(ellpack_ctx c, const ellpack_desc* a, ellpack_desc* b) {
     RK(check_desc(a));
     RK(check_desc(b));
     if (a->n != b->n) return ELLPACK_ERR_DIM;
+    RK(check_comm_n(c, a->n));
     CK(cudaSetDevice(c->device));
     return halo_desc(c, a, b);
 }
@@ -914,10 +993,41 @@ int ellpack_ctx_attach_nccl(ellpack_ctx c, int nranks, int rank, const uint8_t i
     ncclUniqueId u;
     memcpy(&u, id, 128);
     NK(g_nccl.CommInitRank(&c->comm, nranks, u, rank));
+    // Every rank's block, all-gathered (collective, so every rank takes the same decision): the
+    // blocks must be contiguous, ascending with rank, equal, multiples of 256 rows (canonical
+    // trace blocks and equal all-gather counts, §8c-c7/c12, reading R17) and cover [0, N).
+    long long* d_rng = nullptr;
+    std::vector<long long> rng(2 * (size_t)nranks);
+    const long long mine[2] = {(long long)row_begin, (long long)row_end};
+    cudaError_t e = cudaMalloc(&d_rng, sizeof(long long) * 2 * (nranks + 1));
+    if (!e) e = cudaMemcpyAsync(d_rng + 2 * nranks, mine, sizeof mine, cudaMemcpyHostToDevice, c->stream);
+    ncclResult_t ne = ncclSuccess;
+    if (!e) ne = g_nccl.AllGather(d_rng + 2 * nranks, d_rng, 2, ncclInt64, c->comm, c->stream);
+    if (!e && ne == ncclSuccess)
+        e = cudaMemcpyAsync(rng.data(), d_rng, sizeof(long long) * 2 * nranks, cudaMemcpyDeviceToHost, c->stream);
+    if (!e) { c->host_syncs++; e = cudaStreamSynchronize(c->stream); }
+    if (d_rng) cudaFree(d_rng);
+    int rc = e ? from_cuda(e) : (ne != ncclSuccess ? ELLPACK_ERR_NCCL : ELLPACK_OK);
+    const long long per = rng[1] - rng[0];
+    if (rc == ELLPACK_OK) {
+        bool ok = per > 0 && per % kTraceBlock == 0;
+        for (int q = 0; q < nranks && ok; ++q)
+            ok = rng[2 * q] == (long long)q * per && rng[2 * q + 1] == (long long)(q + 1) * per;
+        if (!ok) rc = ELLPACK_ERR_ARG;
+    }
+    if (rc != ELLPACK_OK) {
+        g_nccl.CommDestroy(c->comm);
+        c->comm = nullptr;
+        return rc;
+    }
     c->nranks = nranks;
     c->rank = rank;
     c->row_begin = row_begin;
     c->row_end = row_end;
+    c->comm_n = per * nranks;
+    if (c->h_reach) cudaFreeHost(c->h_reach);
+    c->h_reach = nullptr;
+    CK(cudaMallocHost(&c->h_reach, 2 * sizeof(int32_t) * nranks));
     return ELLPACK_OK;
 }
 
@@ -948,6 +1058,13 @@ struct DevMatrix {
 };
 
 int dm_alloc(ellpack_ctx c, DevMatrix& m, int64_t n, int32_t w) {
+    // ELLPACK_OPT_SP2_MEM_CAP (fault injection): the live iterates' value arrays above the cap
+    // "do not fit"
+    if (c->sp2_mem_cap > 0) {
+        int64_t live = (int64_t)sizeof(double) * n * w;
+        for (int q = 0; q < 4; ++q) live += q == m.slot ? 0 : c->it_live[q];
+        if (live > c->sp2_mem_cap) return ELLPACK_ERR_NOMEM;
+    }
     Buf* b = c->it[m.slot];
     RK(grow(c, b[0], sizeof(double) * (size_t)n * w));
     RK(grow(c, b[1], sizeof(int32_t) * (size_t)n * w));
@@ -962,27 +1079,87 @@ int dm_alloc(ellpack_ctx c, DevMatrix& m, int64_t n, int32_t w) {
     // rank's block and halo are never written and must read as valid rows)
     CK(cudaMemsetAsync(m.d.nnz, 0, sizeof(int32_t) * (size_t)n, c->stream));
     m.owned = true;
+    c->it_live[m.slot] = (int64_t)sizeof(double) * n * w;
     return ELLPACK_OK;
 }
 
-void dm_free(ellpack_ctx, DevMatrix& m) { m.owned = false; }
+void dm_free(ellpack_ctx c, DevMatrix& m) {
+    m.owned = false;
+    c->it_live[m.slot] = 0;
+}
+
+// give the slot's device memory back (grow() never shrinks: a failed retry must not keep a
+// partially grown, oversized value array)
+void dm_release(ellpack_ctx c, DevMatrix& m) {
+    for (Buf& b : c->it[m.slot]) release(c, b);
+    dm_free(c, m);
+}
 
 int32_t round_up32(int64_t x) { return (int32_t)((x + 31) & ~int64_t(31)); }
 
+// MIN over ranks of a width (0 = "did not fit" on some rank); identity without a communicator.
+int agree_width(ellpack_ctx c, int32_t mine, int32_t* out) {
+    if (!c->comm) { *out = mine; return ELLPACK_OK; }
+    int32_t* d = c->d_bw + 8;
+    c->h->imax = mine;
+    CK(cudaMemcpyAsync(d, &c->h->imax, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+    NK(g_nccl.AllReduce(d, d, 1, ncclInt32, ncclMin, c->comm, c->stream));
+    CK(cudaMemcpyAsync(&c->h->imax, d, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    RK(host_sync(c));
+    *out = c->h->imax;
+    return ELLPACK_OK;
+}
+
 // Physical iterate width `want` (headroom), falling back to `need` when the headroom does not
-// fit in device memory (large N densifying iterates): NOMEM only if `need` does not fit either.
+// fit in device memory (large N densifying iterates). The slot is released before the retry, so
+// the retry is not charged for a partial oversized allocation. With a communicator every rank
+// ends with the same physical width (MIN over ranks: the halo send/recv counts are cnt * w on
+// both sides) and a NOMEM on any rank is a NOMEM on every rank.
 int dm_alloc_headroom(ellpack_ctx c, DevMatrix& m, int64_t n, int32_t& want, int32_t need) {
     int rc = dm_alloc(c, m, n, want);
+    int32_t got = want;
     if (rc == ELLPACK_ERR_NOMEM && need < want) {
         cudaGetLastError();  // clear the failed allocation
-        want = need;
-        rc = dm_alloc(c, m, n, want);
+        dm_release(c, m);
+        rc = dm_alloc(c, m, n, need);
+        got = need;
     }
-    return rc;
+    if (rc == ELLPACK_ERR_NOMEM) {
+        cudaGetLastError();
+        got = 0;
+    } else if (rc != ELLPACK_OK) {
+        return rc;
+    }
+    int32_t agreed = got;
+    RK(agree_width(c, got, &agreed));
+    if (agreed <= 0) {
+        dm_release(c, m);
+        return ELLPACK_ERR_NOMEM;
+    }
+    m.d.w = agreed;  // a wider local buffer is viewed at the agreed (smaller) width
+    want = agreed;
+    return ELLPACK_OK;
 }
 
 double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// Exact number of (this rank's, then all-reduced) rows of m with more than w entries (the FAIL
+// report, §8c-c4: overflow_rows = #{i : kept_i > W}); m's stored counts must not be truncated
+// below w + 1 (physical width >= logical width). One kernel + one synchronising read-back.
+int count_rows_over(ellpack_ctx c, const ellpack_desc* m, int32_t w, int64_t* out) {
+    int64_t r0, r1;
+    rows_of(c, m->n, &r0, &r1);
+    int32_t* d = c->d_status + 2;
+    CK(cudaMemsetAsync(d, 0, sizeof(int32_t), c->stream));
+    CK(launch_count_over(m->nnz, r0, r1, w, d, c->stream));
+    c->launches++;
+    if (c->comm) NK(g_nccl.AllReduce(d, d, 1, ncclInt32, ncclSum, c->comm, c->stream));
+    CK(cudaMemcpyAsync(&c->h->imax, d, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    RK(host_sync(c));
+    *out = c->h->imax;
+    return ELLPACK_OK;
 }
 
 // X (width w) <- drop(alpha*H + beta*I) computed at a safe width first (H.w + 1),
@@ -1016,6 +1193,54 @@ int sp2_make_x0(ellpack_ctx c, const ellpack_desc* h, double alpha, double beta,
     return ELLPACK_OK;
 }
 
+// symmetric step: U (the upper triangle of X_{n+1}) is allocated only when a launch takes the
+// general path's upper route, at the physical width of the iterate it mirrors into
+struct UpperAlloc {
+    DevMatrix* U;
+    int64_t n;
+    int32_t w;
+};
+int alloc_upper(ellpack_ctx c, void* arg, KOut* out) {
+    UpperAlloc* a = (UpperAlloc*)arg;
+    if (!a->U->owned || a->U->d.w < a->w) {
+        int rc = dm_alloc(c, *a->U, a->n, a->w);
+        if (rc != ELLPACK_OK) {
+            if (rc == ELLPACK_ERR_NOMEM) { cudaGetLastError(); dm_release(c, *a->U); }
+            return rc;
+        }
+    }
+    *out = kout(&a->U->d);
+    return ELLPACK_OK;
+}
+
+// Probe of the next SP2 operand X (A = B = Old = X) enqueued right after the step that wrote it,
+// fetched with that step's status: the next step plans its launch with no read-back of its own.
+// With a communicator each rank's reach (the X rows its rows reference) is all-gathered too, so
+// the halo exchange of X needs no read-back either.
+int enqueue_next_probe(ellpack_ctx c, const ellpack_desc* x) {
+    RowOpParams q = base_params(c, x->n);
+    q.A = kmat(x);
+    q.B = kmat(x);
+    q.Old = kmat(x);
+    q.alpha = 1.0;
+    q.old_mode = 1;
+    RK(enqueue_probe(c, q, x->n));
+    if (c->comm) {
+        RK(grow(c, c->halo, sizeof(long long) * 2 * (size_t)c->nranks));
+        NK(g_nccl.AllGather(c->d_bw + 4, (int32_t*)c->halo.p, 2, ncclInt32, c->comm, c->stream));
+    }
+    return ELLPACK_OK;
+}
+
+// host copies of the prefetched probe (bw) and every rank's reach, as halo_exec's need ranges
+void take_probe(ellpack_ctx c, int32_t* bw, std::vector<int64_t>& need) {
+    memcpy(bw, c->h->bw, 6 * sizeof(int32_t));
+    for (int q = 0; c->comm && q < c->nranks; ++q) {
+        need[2 * q] = (int64_t)INT_MAX - c->h_reach[2 * q];
+        need[2 * q + 1] = (int64_t)c->h_reach[2 * q + 1] - 1;
+    }
+}
+
 }  // namespace
 
 int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, const sp2_opts* opts_in,
@@ -1025,6 +1250,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     RK(check_desc(dout));
     const int64_t n = h->n;
     if (dout->n != n) return ELLPACK_ERR_DIM;
+    RK(check_comm_n(c, n));
     if (nocc < 0 || nocc > n || !(tol >= 0.0)) return ELLPACK_ERR_ARG;
     {
         // a row block without a communicator cannot see the other rows of X_{n+1}
@@ -1080,16 +1306,19 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
         c->launches++;
         int32_t asym = 1;
         CK(cudaMemcpyAsync(&asym, aux, sizeof asym, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+        RK(host_sync(c));
         sym = asym == 0;
     }
     int rc = sp2_make_x0(c, h, alpha0, beta0, o.threshold, T, &req);
     if (rc) { cleanup(); return rc; }
     if (req > w) {
         if (o.on_overflow == SP2_FAIL || req > maxw) {
+            int64_t ovf = 0;
+            if ((rc = count_rows_over(c, &T.d, w, &ovf))) { cleanup(); return rc; }
             R.stop_reason = SP2_OVERFLOWED; R.required_width = req; R.fail_iter = -1;
-            R.overflow_rows = -1;
+            R.overflow_rows = ovf;
             c->last_req = req;
+            c->last_ovf_rows = ovf;
             cleanup();
             if (rep) *rep = R;
             return ELLPACK_ERR_OVERFLOW;
@@ -1120,9 +1349,18 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
         if ((rc = fetch(c, 1))) { cleanup(); return rc; }
         t2 = c->h->sums[0];
     }
+    // the probe of X0 (its halo rows are in place), for the first step's launch plan
+    int32_t bwX[6];
+    std::vector<int64_t> needX(2 * (size_t)c->nranks);
+    if ((rc = enqueue_next_probe(c, &X.d))) { cleanup(); return rc; }
+    if ((rc = fetch(c, 0, true))) { cleanup(); return rc; }
+    take_probe(c, bwX, needX);
     const double t_init_end = now_s();
 
     // ---- SP2 loop
+    // One host synchronisation per iteration: the step's status, traces, norm, product count,
+    // the probe of X_{n+1} and (with a communicator) every rank's reach arrive in one read-back;
+    // the next step's launch plan and halo exchange are computed from them without waiting.
     RK(grow(c, c->rows[0], sizeof(double) * n));
     RK(grow(c, c->rows[1], sizeof(double) * n));
     RK(grow(c, c->rows[2], sizeof(double) * n));
@@ -1141,17 +1379,16 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     int32_t wcap = o.on_overflow == SP2_FAIL ? w : (int32_t)std::min<int64_t>(maxw, round_up32((int64_t)w * 8));
     int stop = -1;
     int it;
+    UpperAlloc ua{&U, n, 0};
     for (it = 0; it < o.max_iter; ++it) {
         int branch = (trX > (double)nocc) ? SP2_SQUARE : SP2_EXPAND;
         if (closest)  // (same expression as the oracle: tie -> EXPAND)
             branch = (std::fabs(t2 - (double)nocc) < std::fabs((2.0 * trX - t2) - (double)nocc)) ? SP2_SQUARE
                                                                                                 : SP2_EXPAND;
         if (!Y.owned || Y.d.w < wy) {
-            {
-                int32_t want = wcap > wy ? wcap : wy;
-                if ((rc = dm_alloc_headroom(c, Y, n, want, wy))) { status = rc; break; }
-                if (want < wcap) wcap = want;
-            }
+            int32_t want = wcap > wy ? wcap : wy;
+            if ((rc = dm_alloc_headroom(c, Y, n, want, wy))) { status = rc; break; }
+            if (want < wcap) wcap = want;
         }
         // scalar products of this X^2 (this rank's rows; summed over ranks below)
         CK(cudaMemsetAsync(c->d_keys + 2, 0, 8, c->stream));
@@ -1181,15 +1418,11 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             p.diag_s = (double*)c->rows[0].p;
             p.diag_c = (double*)c->rows[1].p;
             p.normsq = (double*)c->rows[2].p;
-            if (sym && !sym_off) {
-                if (!U.owned || U.d.w < Y.d.w) {
-                    if ((rc = dm_alloc(c, U, n, Y.d.w))) { status = rc; break; }
-                }
-                p.upper = 1;  // taken only if the general path runs (enqueue_row_op)
-                p.C_upper = kout(&U.d);
-            }
+            p.upper = sym && !sym_off;  // taken only if the general path runs (enqueue_row_op)
+            ua.w = Y.d.w;
             cudaEventRecord(c->ev[0], c->stream);
-            if ((rc = enqueue_row_op(c, p, n))) { status = rc; break; }
+            if ((rc = enqueue_row_op(c, p, n, bwX, alloc_upper, &ua))) { status = rc; break; }
+            if (c->sym_nomem) sym_off = true;  // U did not fit: whole rows from now on
             const bool upper = c->last_upper != 0;
             if (upper) {
                 // U's status aside, then X_{n+1} row i = L_i || U_i with the step's status
@@ -1213,8 +1446,10 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             const double* arrs[4] = {p.diag_s, p.diag_c, p.normsq, (const double*)c->rows[3].p};
             const int narr = closest ? 4 : 3;
             if ((rc = enqueue_canonical(c, arrs, narr, n))) { status = rc; break; }
+            // the probe of X_{n+1} for the next step (its own rows; reaches all-gathered)
+            if ((rc = enqueue_next_probe(c, &Y.d))) { status = rc; break; }
             cudaEventRecord(c->ev[2], c->stream);
-            if ((rc = fetch(c, narr))) { status = rc; break; }
+            if ((rc = fetch(c, narr, true))) { status = rc; break; }
             float ms1 = 0.f, ms2 = 0.f;
             cudaEventElapsedTime(&ms1, c->ev[0], c->ev[1]);
             cudaEventElapsedTime(&ms2, c->ev[1], c->ev[2]);
@@ -1240,11 +1475,12 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             if (kept_max > wy) {
                 // the logical width grows (the oracle's regrow)
                 if (o.on_overflow == SP2_FAIL || kept_max > maxw) {
+                    // rows over the LOGICAL width wy (Y's counts are exact up to its physical
+                    // width >= wy, so the kernel counts rows over wy exactly)
+                    int64_t ovf = 0;
+                    if ((rc = count_rows_over(c, &Y.d, wy, &ovf))) { status = rc; break; }
                     R.stop_reason = SP2_OVERFLOWED;
-                    R.overflow_rows = 0;
-                    // rows over the logical width: exact count needs the full output when the
-                    // physical buffer overflowed too; the status word counts rows over Y.d.w
-                    R.overflow_rows = c->h->status[0] > 0 ? c->h->status[0] : -1;
+                    R.overflow_rows = ovf;
                     R.required_width = kept_max;
                     R.fail_iter = it;
                     c->last_ovf_rows = R.overflow_rows;
@@ -1285,8 +1521,10 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             iters[it].frob2 = t2;
         }
         if (closest) t2 = c->h->sums[3];
-        // the next step reads only the rows of X_{n+1} its rows reference (band-aware halo, f1)
-        if ((rc = halo_desc(c, &Y.d, &Y.d))) { status = rc; break; }
+        take_probe(c, bwX, needX);
+        // the next step reads only the rows of X_{n+1} its rows reference (band-aware halo, f1),
+        // planned from the reaches that arrived with this step's status
+        if (c->comm && (rc = halo_exec(c, &Y.d, needX.data()))) { status = rc; break; }
         std::swap(X, Y);
         wx = wy;
         trX = trY;
@@ -1319,6 +1557,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
         }
     }
     cleanup();
+    c->host_syncs++;
     cudaStreamSynchronize(c->stream);
     R.t_read_hamiltonian = t_read_end - t_start;
     R.t_init_misc = t_init_end - t_read_end;
@@ -1353,7 +1592,7 @@ int ellpack_multiply_x2_host(ellpack_ctx c, int64_t n, int32_t wx, const double*
     CK(cudaMemcpyAsync(yv, Y.val, cy * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(yc, Y.col, cy * 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(yn, Y.nnz, n * 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    RK(host_sync(c));
     if (rc == ELLPACK_OK) {
         if (trace_x) *trace_x = tx;
         if (trace_x2) *trace_x2 = tx2;

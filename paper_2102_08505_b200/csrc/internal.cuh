@@ -87,9 +87,10 @@ size_t row_op_warp_smem(int S, bool has_old, bool fast);
 // (rows k0 <= k < k1 only: the B rows the launch's A rows reference)
 cudaError_t launch_balance(KMat b, int64_t k0, int64_t k1, int wt, int S, unsigned char* bt, int32_t* bt_nbin,
                            int num_sms, cudaStream_t s);
-// out[0..2] = max half-bandwidth of a (rows r0..r1), b (all rows), c (rows r0..r1); out[3] = max nnz of b;
-// A's rows r0..r1 reference B rows [INT_MAX - out[4], out[5] - 1] (out[0..5] zeroed by the caller)
-cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64_t r1, int64_t n,
+// out[0..2] = max half-bandwidth of a (rows r0..r1), b (rows b0..b1), c (rows r0..r1); out[3] = max nnz
+// of b (rows b0..b1); A's rows r0..r1 reference B rows [INT_MAX - out[4], out[5] - 1] (out[0..5]
+// zeroed by the caller)
+cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int64_t r0, int64_t r1, int64_t b0, int64_t b1, int64_t n,
                              int32_t* out, cudaStream_t s);
 
 // symmetric SP2 step (f4 ii): is h bitwise symmetric (ok[0] stays 0); reach of U's rows
@@ -123,6 +124,8 @@ cudaError_t launch_breakpoints(KMat b, int64_t n, int S, int np, int32_t* bp, in
 cudaError_t launch_col_range(KMat a, int64_t r0, int64_t r1, long long* out, cudaStream_t s);
 cudaError_t launch_products(KMat a, const int32_t* nnz_b, int64_t r0, int64_t r1, unsigned long long* out,
                             cudaStream_t s);
+cudaError_t launch_count_over(const int32_t* nnz, int64_t r0, int64_t r1, int32_t w, int32_t* out,
+                              cudaStream_t s);
 cudaError_t launch_max_nnz(const int32_t* nnz, int64_t row_begin, int64_t row_end,
                            int32_t* out, cudaStream_t s);
 

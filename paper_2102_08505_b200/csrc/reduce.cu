@@ -287,6 +287,21 @@ __global__ void max_nnz_kernel(const int32_t* nnz, int64_t r0, int64_t r1, int32
     if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
 }
 
+// out[0] += #rows r in [r0, r1) with nnz[r] > w (the exact overflow-row count of a kept-count array)
+__global__ void count_over_kernel(const int32_t* nnz, int64_t r0, int64_t r1, int32_t w, int32_t* out) {
+    const int64_t i = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned m = __ballot_sync(FULL, i < r1 && nnz[i] > w);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(out, __popc(m));
+}
+
+cudaError_t launch_count_over(const int32_t* nnz, int64_t r0, int64_t r1, int32_t w, int32_t* out,
+                              cudaStream_t s) {
+    const int64_t rows = r1 - r0;
+    if (rows <= 0) return cudaSuccess;
+    count_over_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(nnz, r0, r1, w, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_max_nnz(const int32_t* nnz, int64_t r0, int64_t r1, int32_t* out, cudaStream_t s) {
     const int64_t rows = r1 - r0;
     if (rows <= 0) return cudaSuccess;

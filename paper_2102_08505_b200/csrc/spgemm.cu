@@ -1228,10 +1228,12 @@ __global__ void __launch_bounds__(128, ELL_GEN_MINB) row_general_kernel(const Ro
     flush_status(p, lane, my_max_kept, my_ovf);
 }
 
-// Half-bandwidth probe: out[m] = max over rows of max(i - col[i][0], col[i][nnz-1] - i);
-// out[3] = max nnz of b; the B rows the A rows [r0, r1) reference are [INT_MAX - out[4], out[5] - 1]
-// (zero-initialised maxima of INT_MAX - first column and last column + 1).
-__global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int64_t r0, int64_t r1, int64_t n, int32_t* out) {
+// Half-bandwidth probe: out[m] = max over rows of max(i - col[i][0], col[i][nnz-1] - i) (a and c
+// over rows [r0, r1), b over rows [b0, b1)); out[3] = max nnz of b over [b0, b1); the B rows the A
+// rows [r0, r1) reference are [INT_MAX - out[4], out[5] - 1] (zero-initialised maxima of
+// INT_MAX - first column and last column + 1).
+__global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int64_t r0, int64_t r1, int64_t b0, int64_t b1,
+                                 int64_t n, int32_t* out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int bw[3] = {0, 0, 0};
     int reach[2] = {0, 0};
@@ -1239,8 +1241,9 @@ __global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int64_t r0, int64_t r1,
     if (i < n) {
 #pragma unroll
         for (int m = 0; m < 3; ++m) {
-            // A and Old only matter on the computed rows; B on every row
+            // A and Old only matter on the computed rows; B on its probed rows
             if (m != 1 && (i < r0 || i >= r1)) continue;
+            if (m == 1 && (i < b0 || i >= b1)) continue;
             const KMat& x = *ms[m];
             if (x.nnz == nullptr) continue;
             const int nz = x.nnz[i];
@@ -1251,7 +1254,7 @@ __global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int64_t r0, int64_t r1,
             }
         }
     }
-    int nzb = (i < n) ? b.nnz[i] : 0;
+    int nzb = (i >= b0 && i < b1) ? b.nnz[i] : 0;
 #pragma unroll
     for (int m = 0; m < 6; ++m) {
         int v = m < 3 ? bw[m] : (m == 3 ? nzb : reach[m - 4]);
@@ -1261,10 +1264,9 @@ __global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int64_t r0, int64_t r1,
     }
 }
 
-cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int nmat, int64_t r0, int64_t r1, int64_t n,
+cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int64_t r0, int64_t r1, int64_t b0, int64_t b1, int64_t n,
                              int32_t* out, cudaStream_t s) {
-    (void)nmat;
-    bandwidth_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, c, r0, r1, n, out);
+    bandwidth_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, c, r0, r1, b0, b1, n, out);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,167 @@
+"""GPU parity for the round-2 pins and boundary checks (the sm_100a path through the C ABI vs the
+CPU oracle, bitwise):
+
+- c6 single rounding with non-dyadic alpha/beta and planted cancellations (add, scale_add_identity),
+  the fixtures of tests/test_oracle_pins_c6_c10.py;
+- the c10 (vi) stop-rule fixtures (STAGNATED exactly at n + 1 = min_iter with e_n = stag_gate);
+- FAIL at X0 reports the exact overflow-row count (§8c-c4) on both sides;
+- the iterate-memory fallbacks (headroom -> exact width; the symmetric step's U -> whole rows) give
+  the same bits (ELLPACK_OPT_SP2_MEM_CAP fault injection);
+- one host synchronisation per SP2 iteration (f3, first half) with bitwise-unchanged results;
+- ellpack_ctx_attach_nccl rejects row blocks that are not equal multiples of 256 (1-rank comm).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import from_dense
+from tests.helpers import same_bits
+from tests.test_gpu_parity import _compare_sp2, eb, up
+from tests.test_oracle_pins_c6_c10 import (_ALPHAS, _BETAS, _bits_equal, _brute_add, _ell,
+                                           _find_stagnation_fixture, _rows)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_c6_add_non_dyadic_gpu_bitwise(ctx, seed):
+    rng = np.random.default_rng(600 + seed)
+    n = int(rng.integers(10, 24)) * 7  # a few hundred rows: several warps, both paths' tails
+    Am = rng.random((n, n)) < 0.05
+    Bm = rng.random((n, n)) < 0.05
+    A = np.where(Am, rng.standard_normal((n, n)), 0.0)
+    B = np.where(Bm, rng.standard_normal((n, n)), 0.0)
+    alpha, beta = _ALPHAS[seed % 4], _BETAS[(seed // 4) % 4]
+    plant = Am & Bm & (rng.random((n, n)) < 0.5)
+    B = np.where(plant, -alpha * A / beta, B)
+    tau = [0.0, 1e-15, 1e-3][seed % 3]
+    w = int(2 * max((Am | Bm).sum(axis=1).max(), 1) + 2)
+    w += w & 1
+    Ao, Be = _ell(A, Am, w), _ell(B, Bm, w)
+    r = oracle.add(Ao, Be, alpha, beta, tau)
+    assert r.status == oracle.OK
+    if n <= 120:
+        assert _bits_equal(_rows(Ao), _brute_add(A, Am, B, Bm, alpha, beta, tau))
+    g = up(_ell(A, Am, w))
+    assert ctx.add(g, up(Be), alpha, beta, tau) == eb().OK
+    assert same_bits(g.to_host(), Ao)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_c6_scale_add_identity_cancellation_gpu_bitwise(ctx, seed):
+    rng = np.random.default_rng(700 + seed)
+    n = int(rng.integers(200, 900))
+    Am = rng.random((n, n)) < 0.02
+    Am = Am | Am.T
+    A = np.where(Am, rng.uniform(-2.0, 0.0, (n, n)), 0.0)
+    emin, emax = -6.38 + 0.1 * seed, 5.09 - 0.07 * seed
+    dl = emax - emin
+    alpha, beta = -1.0 / dl, emax / dl
+    diag = np.diag(A).copy()
+    for i in range(n):
+        if rng.random() < 0.5:
+            Am[i, i] = True
+            diag[i] = emax * (1.0 + rng.integers(-4, 5) * 2.0 ** -52)
+        elif rng.random() < 0.5:
+            Am[i, i] = False
+            diag[i] = 0.0
+    np.fill_diagonal(A, diag)
+    tau = [0.0, 1e-17, 1e-5][seed % 3]
+    w = int(Am.sum(axis=1).max() + 2)
+    w += w & 1
+    Ao = _ell(A, Am, w)
+    r = oracle.scale_add_identity(Ao, alpha, beta, tau)
+    assert r.status == oracle.OK
+    g = up(_ell(A, Am, w))
+    assert ctx.scale_add_identity(g, alpha, beta, tau) == eb().OK
+    assert same_bits(g.to_host(), Ao)
+
+
+@pytest.mark.parametrize("tau,nlev,seeds", [(0.0, 9, range(0, 400)), (1e-3, 12, range(400, 800)),
+                                              (0.0, 30, range(800, 1200))])
+def test_c10_stagnation_fixtures_gpu(ctx, tau, nlev, seeds):
+    """The stop iteration of each stop-rule fixture, on the GPU: STAGNATED at exactly n + 1."""
+    h, nocc, recs, n = _find_stagnation_fixture(tau, nlev, seeds)
+    gate = recs[n][3]
+    H = from_dense(np.diag(h), w=2)
+    for min_iter, g_ in ((n + 1, gate), (n + 2, gate), (n + 1, float(np.nextafter(gate, -np.inf)))):
+        o = oracle.sp2(H, nocc, 0.0, oracle.SP2Opts(threshold=tau, max_iter=60, min_iter=min_iter, stag_gate=g_),
+                       d_width=len(h) + (len(h) & 1))
+        d = eb().Mat.empty(len(h), len(h) + (len(h) & 1))
+        g = ctx.sp2_run(up(H), nocc, 0.0, d, threshold=tau, max_iter=60, min_iter=min_iter, stag_gate=g_)
+        _compare_sp2(g, o)
+        assert same_bits(d.to_host(), o.D)
+    assert o.iterations != n + 1  # (the last variant: gate one ulp below e_n)
+
+
+def test_sp2_fail_at_x0_overflow_rows_gpu(ctx):
+    H = synth.sym_banded(300, 40, 10, 30, 1, -1.0, 1.0, 0, 10.0, 0.0, 31)
+    o = oracle.sp2(H, 150, 1e-8, oracle.SP2Opts(threshold=0.0, on_overflow=0, initial_width=16), d_width=300)
+    assert o.status == oracle.OVERFLOW and o.fail_iter == -1 and o.overflow_rows > 0
+    d = eb().Mat.empty(300, 300)
+    g = ctx.sp2_run(up(H), 150, 1e-8, d, on_overflow=eb().SP2_FAIL, initial_width=16)
+    assert g.status == eb().ERR_OVERFLOW
+    assert (g.fail_iter, g.required_width, g.overflow_rows) == (o.fail_iter, o.required_width, o.overflow_rows)
+    assert ctx.overflow_info() == (o.overflow_rows, o.required_width)
+
+
+@pytest.mark.parametrize("slack", [8, 4096])
+def test_sp2_iterate_memory_fallbacks_bitwise(ellpack_lib, slack):
+    """ELLPACK_OPT_SP2_MEM_CAP = room for X_n and X_{n+1} at the final width (+ slack columns): the
+    x8 / x4 headroom widths "do not fit" (fallback to the exact width, slot released first) and,
+    with little slack, neither does the symmetric step's upper triangle (whole rows instead)."""
+    E = ellpack_lib
+    n = 1024
+    H = synth.sym_banded(n, 32, 6, 12, 1, -1.0, 1.0, 0, 4.0, 0.0, 6)
+    o = oracle.sp2(H, n // 2, 1e-10, oracle.SP2Opts(threshold=1e-6, max_iter=100), d_width=n)
+    assert o.final_width > 256  # the general path (and its symmetric route) runs
+    ctx = E.Context(0)
+    ctx.set_option(E.OPT_SP2_MEM_CAP, 8 * n * (2 * o.final_width + slack))
+    d = E.Mat.empty(n, n)
+    g = ctx.sp2_run(up(H), n // 2, 1e-10, d, threshold=1e-6, max_iter=100)
+    _compare_sp2(g, o)
+    assert same_bits(d.to_host(), o.D)
+    ctx.close()
+
+
+def test_sp2_one_host_sync_per_iteration(ellpack_lib):
+    """f3 (first half): every SP2 iteration waits on the device exactly once (the probe of X_{n+1}
+    travels with the step's status); two windows differ by exactly their iteration count."""
+    E = ellpack_lib
+    n = 2048
+    H = synth.sym_banded(n, 32, 6, 12, 1, -1.0, 1.0, 0, 4.0, 0.0, 3)
+    syncs = {}
+    for K in (4, 12):
+        ctx = E.Context(0)
+        ctx.set_option(E.OPT_SP2_SYMMETRIC, 0)
+        d = E.Mat.empty(n, n)
+        s0 = ctx.host_syncs()
+        # the initial width n: no physical regrow (which redoes a step) inside the window
+        g = ctx.sp2_run(up(H), n // 2, 0.0, d, threshold=1e-7, max_iter=K, min_iter=100, initial_width=n)
+        syncs[K] = ctx.host_syncs() - s0
+        assert g.iterations == K
+        o = oracle.sp2(H, n // 2, 0.0, oracle.SP2Opts(threshold=1e-7, max_iter=K, min_iter=100, initial_width=n),
+                       d_width=n)
+        _compare_sp2(g, o)
+        assert same_bits(d.to_host(), o.D)
+        ctx.close()
+    assert syncs[12] - syncs[4] == 8, syncs
+
+
+def test_attach_nccl_checks_row_blocks(ellpack_lib):
+    import torch  # noqa: F401  (torch's libnccl.so.2 for the library's dlopen)
+    E = ellpack_lib
+    uid = E.Context.nccl_unique_id()
+    ctx = E.Context(0)
+    with pytest.raises(E.EllpackError) as ei:
+        ctx.attach_nccl(1, 0, uid, 0, 1000)  # not a multiple of 256 rows
+    assert ei.value.status == E.ERR_ARG
+    ctx.close()
+    ctx = E.Context(0)
+    ctx.attach_nccl(1, 0, E.Context.nccl_unique_id(), 0, 1024)
+    X = synth.cfg5(2048, 32)
+    with pytest.raises(E.EllpackError) as ei:  # operands must be the N the blocks cover
+        ctx.multiply_x2(up(X), E.Mat.empty(2048, 1024), 1e-5)
+    assert ei.value.status == E.ERR_DIM
+    ctx.close()

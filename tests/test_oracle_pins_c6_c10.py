@@ -328,3 +328,33 @@ def test_c10_stop_precedence_and_gate():
     # max_iter exactly at n + 1 with the rule off (min_iter beyond): NOCONV with n + 1 iterations
     r = oracle.sp2(H, nocc, 0.0, oracle.SP2Opts(max_iter=n + 1, min_iter=100))
     assert (r.iterations, r.stop, r.status) == (n + 1, "NOCONV", oracle.NOCONV)
+
+
+# ------------------------------------------------- c4 at X0: the exact overflow-row count
+
+
+@pytest.mark.parametrize("seed,tau", [(31, 0.0), (32, 0.05)])
+def test_c4_sp2_fail_at_x0_counts_rows_over_the_width(seed, tau):
+    """SP2 with FAIL whose X0 = drop(alpha H + beta I) overflows the initial width: the report
+    carries required_width = max kept count and overflow_rows = #{i : kept_i > W} (§8c-c4), with
+    the kept counts of X0 computed here from the definition (c6 diagonal fma, c3 drop)."""
+    import synth
+    H = synth.sym_banded(300, 40, 10, 30, 1, -1.0, 1.0, 0, 10.0, 0.0, seed)
+    d = H.to_dense()
+    m = np.zeros_like(d, dtype=bool)
+    for i in range(H.n):
+        m[i, H.col[i, :H.nnz[i]]] = True
+    lo, hi = oracle.gershgorin(H)
+    alpha, beta = -1.0 / (hi - lo), hi / (hi - lo)
+    kept = np.zeros(H.n, int)
+    for i in range(H.n):
+        for j in np.nonzero(m[i])[0]:
+            if j != i:
+                kept[i] += abs(float(Fraction(alpha) * Fraction(float(d[i, j])))) > tau
+        a = float(d[i, i]) if m[i, i] else 0.0
+        kept[i] += abs(float(Fraction(alpha) * Fraction(a) + Fraction(beta))) > tau
+    w = int(np.percentile(kept, 60)) & ~1
+    r = oracle.sp2(H, 150, 1e-8, oracle.SP2Opts(threshold=tau, on_overflow=0, initial_width=w), d_width=300)
+    assert r.status == oracle.OVERFLOW and r.fail_iter == -1
+    assert r.required_width == kept.max()
+    assert r.overflow_rows == int((kept > w).sum()) > 0
