@@ -1,28 +1,35 @@
 #!/usr/bin/env python
-"""bench.py -- ELLPACK X^2 multiply on B200 (BASELINE.json metric), one JSON line.
+"""bench.py -- ELLPACK X^2 multiply + SP2 on B200 (BASELINE.json metric), one JSON line.
 
-Default workload (BASELINE.json configs[4], the largest single-GPU multiply, on
-which the north star's ">= 50% of HBM peak" target is stated):
+Headline (BASELINE.json configs[4], the largest single-GPU multiply, on which the north star's
+">= 50% of HBM peak" target is stated):
     cfg5: X^2 of a random banded symmetric X, N=262144, M=256, tau=1e-5, FP64.
-A "step" = one ellpack_multiply_x2 call (fused row kernel: window pre-pass,
-gather-accumulate, drop/compact/write, trace partials; canonical trace
-reduction; status read-back) -- SURVEY §8a rows a0..a4. With N>1 ranks a step
-is the band-aware halo exchange of X's rows (NCCL send/recv of exactly the rows
-the rank's own rows reference, §8f-f1; BJ north_star (3)) followed by the
+A "step" = one ellpack_multiply_x2 call (fused row kernel: window pre-pass, gather-accumulate,
+drop/compact/write, trace partials; canonical trace reduction; status read-back) -- SURVEY §8a
+rows a0..a4. With N > 1 ranks a step is the band-aware halo exchange of X's rows (NCCL send/recv
+of exactly the rows the rank's own rows reference, §8f-f1; BJ north_star (3)) followed by the
 multiply of the rank's own rows (strong scaling: total work fixed).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload x2|spgemm|sp2] [--n N --m M]
+The same line carries the rest of BASELINE.json's metric ("SP2 iterations/sec at 1/2/4/8") and the
+other configs' timings as sub-objects: "sp2" (cfg3 K = 10 and cfg4 K = 6 windows, SURVEY §8d "SP2
+protocol"), "cfg1" (us per ABI call, launch-latency bound) and "cfg2" (C = alpha A B + beta C).
 
---impl reference times the CPU oracle (oracle/, the reference arm of this tier)
-on the host cores, on a bounded row sample of the same workload.
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload x2|sp2] [--n N --m M] [--quick]
+
+--gpus N without a launcher re-executes itself under torch.distributed.run with N ranks (one per
+GPU); under a launcher WORLD_SIZE must equal N. --impl reference times the CPU oracle (oracle/, the
+reference arm of this tier) on the host cores, on a bounded row sample of the same workload (rank 0
+only under a launcher).
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -37,6 +44,12 @@ import numpy as np  # noqa: E402
 import synth  # noqa: E402
 
 HBM_FALLBACK_GBS = 6650.0
+TAU5 = 1e-5
+
+
+def workload_name(n: int, m: int, tau: float) -> str:
+    """The one workload string both arms print (the driver compares them)."""
+    return f"cfg5 X^2 N={n} M={m} tau={tau:g}"
 
 
 def peaks():
@@ -47,18 +60,35 @@ def peaks():
     return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(workload: str):
-    """dram bytes per launch of the row kernel from the committed ncu --set full capture."""
+def kernel_src_sha() -> str:
+    """Hash of the row-kernel source: an ncu capture is only quoted for the kernel it measured."""
+    h = hashlib.sha256()
+    for f in ("spgemm.cu", "internal.cuh"):
+        h.update(open(os.path.join(ROOT, "paper_2102_08505_b200", "csrc", f), "rb").read())
+    return h.hexdigest()[:16]
+
+
+def ncu_capture(key: str):
+    """DRAM bytes / L2 hit rates per launch of the row kernel from the committed ncu --set full
+    capture (profiles/ncu_traffic.json), or (None, why) when that capture is of another kernel
+    source than the one that just ran."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(p):
-        d = json.load(open(p))
-        return d.get(workload)
-    return None
+    if not os.path.exists(p):
+        return None, "no capture"
+    d = json.load(open(p)).get(key)
+    if not d:
+        return None, "no capture of this workload"
+    if d.get("src_sha") != kernel_src_sha():
+        return None, f"capture {d.get('source')} is of kernel source {d.get('src_sha')}, not the current one"
+    return d, d.get("source")
 
 
-def ncu_l2_hit(workload: str):
-    """L2 hit rates (all sectors / reads) of the same capture (north star (4): HBM GB/s and L2 hit rate)."""
-    return ncu_traffic(f"{workload}_l2_hit_pct")
+def microbench(name: str):
+    """Measured co-bound peaks (tools/microbench.cu on a B200, profiles/r02_microbench.json)."""
+    p = os.path.join(ROOT, "profiles", "r02_microbench.json")
+    if not os.path.exists(p):
+        return None
+    return json.load(open(p)).get(name)
 
 
 class ClockSampler:
@@ -136,6 +166,8 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
+
+
 def live_entries(e) -> int:
     return int(e.nnz.sum())
 
@@ -146,11 +178,12 @@ def x2_bytes(nnz_x: int, nnz_c: int, n: int) -> int:
     return 12 * (nnz_x + nnz_c) + 8 * n
 
 
-def lsu_floor(X, P: int, nnz_c: int, sm_mhz, num_sms: int = 148) -> dict:
+def lsu_floor(X, P: int, nnz_c: int, sm_mhz, num_sms: int = 148, slot_bytes: int = 4) -> dict:
     """The ring kernel's L1/LSU data-pipe floor: one 128-byte wavefront per
-    SM-cycle; per product a 64-bit LDS + STS on the ring (4 wavefronts per 32 lanes) and a 12-byte
-    B record gather; per output-span column one read-and-clear (2 per 32); per kept entry 12 bytes
-    stored. Conflict-free, unpadded counts: the floor a perfect schedule would meet."""
+    SM-cycle; per product a 64-bit LDS + STS on the ring (4 wavefronts per 32 lanes) and a
+    (8 + slot_bytes)-byte B record gather; per output-span column one read-and-clear (2 per 32);
+    per kept entry 12 bytes stored. Conflict-free, unpadded counts: the floor a perfect schedule
+    would meet."""
     nnz = X.nnz.astype(np.int64)
     live = nnz > 0
     rows = np.flatnonzero(live)
@@ -160,7 +193,7 @@ def lsu_floor(X, P: int, nnz_c: int, sm_mhz, num_sms: int = 148) -> dict:
     lo = np.maximum(0, first - hB) & ~31
     hi = (np.minimum(X.n - 1, last + hB) + 32) & ~31
     cols = int((hi - lo).sum())
-    wf = P * (4 / 32 + 12 / 128) + cols * (2 / 32) + nnz_c * (12 / 128)
+    wf = P * (4 / 32 + (8 + slot_bytes) / 128) + cols * (2 / 32) + nnz_c * (12 / 128)
     if not sm_mhz:
         return {"wavefronts": wf, "floor_ms": None}
     return {"wavefronts": wf, "output_span_columns": cols, "sm_mhz": sm_mhz,
@@ -174,11 +207,16 @@ def dist_env():
     return ws, rank, local
 
 
+def round_up32(x: int) -> int:
+    return ((x + 31) // 32) * 32
+
+
 # ---------------------------------------------------------------------------- oracle arm
 
 def oracle_sample(X, tau: float, budget_s: float):
     """Choose a bounded row sample of the X^2 workload for the oracle (as it stands): uniformly
-    sampled rows of X, grown until one oracle call takes about budget_s / 4 seconds.
+    sampled rows of X, grown until one oracle call takes about budget_s / 4 seconds. The sample's
+    output is stored at its required width (every kept entry is written, as in the GPU step).
     Returns (run, products, description, cores): run() executes the sample once (seconds)."""
     import oracle
     from synth import Ell
@@ -192,18 +230,22 @@ def oracle_sample(X, tau: float, budget_s: float):
         A.col[idx] = X.col[idx]
         A.nnz[idx] = X.nnz[idx]
         P = synth.products(A, X)
-        Y = Ell.empty(n, 8 * X.w if n > 8 * X.w else n + (n & 1))
+        t0 = time.perf_counter()
+        r = oracle.multiply(A, X, Ell.empty(n, 2), 1.0, 0.0, tau)  # sizing call: required width
+        dt = time.perf_counter() - t0
+        if dt > budget_s / 5 or rows >= n:
+            Y = Ell.empty(n, max(2, round_up32(r.required_width)))
 
-        def run(A=A, Y=Y):
-            t0 = time.perf_counter()
-            oracle.multiply(A, X, Y, 1.0, 0.0, tau)
-            return time.perf_counter() - t0
+            def run(A=A, Y=Y):
+                t0 = time.perf_counter()
+                rr = oracle.multiply(A, X, Y, 1.0, 0.0, tau)
+                assert rr.status == oracle.OK
+                return time.perf_counter() - t0
 
-        dt = run()
-        if dt > budget_s / 4 or rows >= n:
-            desc = f"{len(idx)} uniformly sampled rows of the same X^2 ({P} products per sample)"
+            desc = (f"{len(idx)} uniformly sampled rows of the same X^2 ({P} products per sample, output at "
+                    f"the sample's required width {Y.w})")
             return run, P, desc, oracle.num_threads()
-        rows = min(n, int(rows * max(2.0, (budget_s / 4) / max(dt, 1e-3))))
+        rows = min(n, int(rows * max(2.0, (budget_s / 5) / max(dt, 1e-3))))
 
 
 def run_reference(args):
@@ -211,7 +253,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     X = synth.cfg5(args.n, args.m)
-    run, P, desc, cores = oracle_sample(X, 1e-5, args.ref_budget)
+    run, P, desc, cores = oracle_sample(X, TAU5, args.ref_budget)
     for _ in range(args.warmup):
         run()
     times = [run() for _ in range(args.steps)]
@@ -220,9 +262,9 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "ELLPACK X^2 multiply GFLOP/s", "value": gflops, "unit": "GFLOP/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth.cfg5, seed 5)",
-        "config": {"workload": f"cfg5 X^2 N={args.n} M={args.m} tau=1e-5", "sample_products": P},
+        "config": {"workload": workload_name(args.n, args.m, TAU5), "sample_products": P},
         "cpu_baseline": {"value": gflops, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": desc},
         "e2e": {"value": gflops, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -232,9 +274,9 @@ def run_reference(args):
 
 # ----------------------------------------------------------------------------- GPU arm
 
-def run_ours(args):
+def _init(args):
+    """Process group (N > 1), device, context, NCCL communicator over the given rows."""
     import torch
-    import torch.distributed as dist
 
     import paper_2102_08505_b200 as eb
     from paper_2102_08505_b200 import multirank as mr
@@ -245,18 +287,174 @@ def run_ours(args):
         mr.init_process_group("nccl", device=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
-    dev = torch.cuda.current_device()
     eb.build()
+    return ws, rank, torch.cuda.current_device()
+
+
+def _comm_ctx(eb, mr, dev, ws, rank, n):
     ctx = eb.Context(dev)
+    if ws > 1:
+        uid = mr.broadcast_bytes(eb.Context.nccl_unique_id() if rank == 0 else None)
+        r0, r1 = mr.rank_rows(n, ws, rank)
+        ctx.attach_nccl(ws, rank, uid, r0, r1)
+    return ctx
+
+
+def check_ranks_bitwise(eb, mr, dev, ws, rank):
+    """N > 1: before timing, the rank's rows of a small cfg5 X^2 computed through the communicator
+    (halo exchange + own rows) must equal a one-rank computation bit for bit (§8c-c12)."""
+    import torch
+    import torch.distributed as dist
+    X = synth.cfg5(32768, 64)
+    solo = eb.Context(dev)
+    x1 = eb.Mat.from_host(X)
+    y1 = eb.Mat.empty(X.n, 832)
+    st1, tx1, tx21 = solo.multiply_x2(x1, y1, TAU5)
+    solo.close()
+    ctx = _comm_ctx(eb, mr, dev, ws, rank, X.n)
+    x = eb.Mat.from_host(X)
+    r0, r1 = mr.rank_rows(X.n, ws, rank)
+    keep = torch.zeros(X.n, dtype=torch.bool, device="cuda")
+    keep[r0:r1] = True
+    x.nnz.masked_fill_(~keep, 0)  # this rank holds only its own rows; the halo brings the rest
+    ctx.halo_rows(x)
+    y = eb.Mat.empty(X.n, 832)
+    st, tx, tx2 = ctx.multiply_x2(x, y, TAU5)
+    live = torch.arange(832, device="cuda")[None, :] < y1.nnz[r0:r1, None]
+    ok = (st == st1 == eb.OK and (tx, tx2) == (tx1, tx21) and torch.equal(y.nnz[r0:r1], y1.nnz[r0:r1])
+          and torch.equal(y.col[r0:r1][live], y1.col[r0:r1][live])
+          and torch.equal(y.val[r0:r1][live].view(torch.int64), y1.val[r0:r1][live].view(torch.int64)))
+    flag = torch.tensor([0 if ok else 1], device="cuda")
+    dist.all_reduce(flag)
+    ctx.close()
+    if int(flag.item()):
+        raise SystemExit(f"bench.py: P={ws} result differs from P=1 on cfg5 N=32768 M=64 (rank {rank}: ok={ok})")
+    return True
+
+
+def time_sp2(eb, mr, dev, ws, rank, cfg: int, K: int, steps: int, warmup: int):
+    """SP2 iterations/sec over a fixed K-iteration GROW window (SURVEY §8d "SP2 protocol"): one timed
+    call = one sp2_run of K iterations, CUDA events on the context stream, max over ranks."""
+    import torch
+    H, cf = (synth.cfg3(), synth.CFG3) if cfg == 3 else (synth.cfg4(), synth.CFG4)
+    n = H.n
+    ctx = _comm_ctx(eb, mr, dev, ws, rank, n)
+    h = eb.Mat.from_host(H)
+    d = eb.Mat.empty(n, min(n + (n & 1), 8192))
+    stream = torch.cuda.current_stream()
+    run = lambda: ctx.sp2_run(h, cf["nocc"], cf["tol"], d, threshold=cf["threshold"], max_iter=K)  # noqa: E731
+    for _ in range(max(1, warmup)):
+        r = run()
+    torch.cuda.synchronize()
+    s0, l0 = ctx.host_syncs(), ctx.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        r = run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if ws > 1:
+        ms = mr.max_over_ranks(ms, device="cuda")
+    syncs = (ctx.host_syncs() - s0) / steps
+    launches = (ctx.kernel_launches() - l0)
+    ctx.close()
+    P = sum(it["products"] for it in r.iters)
+    Pexec = sum(it["products_exec"] for it in r.iters)
+    rmw = microbench("smem_rmw_f64_random_peak")
+    rate = Pexec / (ms * 1e-3)
+    out = {"workload": f"cfg{cfg} SP2 N={n} tau={cf['threshold']:g} window K={K} GROW", "iterations": r.iterations,
+           "stop": r.stop, "final_width": r.final_width, "ms_per_window": ms, "iterations_per_s": r.iterations / (ms * 1e-3),
+           "products": P, "products_executed": Pexec,
+           "gflops_effective": 2.0 * P / (ms * 1e-3) / 1e9,
+           "gflops_executed": 2.0 * Pexec / (ms * 1e-3) / 1e9,
+           "host_syncs_per_iteration": syncs / max(r.iterations, 1), "gpu_launches": launches,
+           "roofline": {"bound": "smem_rmw", "achieved": rate / 1e9, "unit": "Gupd/s",
+                        "peak": rmw["Gupd_per_s"] if rmw else None,
+                        "frac": (rate / 1e9 / rmw["Gupd_per_s"]) if rmw else None,
+                        "peak_source": ("tools/microbench.cu random-address FP64 smem RMW, best occupancy "
+                                        "(profiles/r02_microbench.json)") if rmw else "not measured"},
+           "symmetric_step": ws == 1}
+    return out
+
+
+def time_cfg1(eb, dev, reps: int):
+    """cfg1 (N = 512): us per ellpack_multiply_x2 call (incl. its status read-back), host clock over
+    back-to-back calls, plus the device time of the same calls by CUDA events."""
+    import torch
+    X = synth.cfg1()
+    ctx = eb.Context(dev)
+    x = eb.Mat.from_host(X)
+    y = eb.Mat.empty(X.n, 256)
+    for _ in range(20):
+        assert ctx.multiply_x2(x, y, TAU5)[0] == eb.OK
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0, s0 = ctx.kernel_launches(), ctx.host_syncs()
+    e0.record()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        ctx.multiply_x2(x, y, TAU5)
+    dt = (time.perf_counter() - t0) / reps
+    e1.record()
+    torch.cuda.synchronize()
+    out = {"workload": "cfg1 X^2 N=512 M=32 tau=1e-05 (out width 256)", "us_per_call": dt * 1e6,
+           "device_us_per_call": e0.elapsed_time(e1) * 1e3 / reps, "calls": reps,
+           "gpu_launches_per_call": (ctx.kernel_launches() - l0) / reps,
+           "host_syncs_per_call": (ctx.host_syncs() - s0) / reps,
+           "gflops": 2.0 * synth.products(X, X) / dt / 1e9}
+    ctx.close()
+    return out
+
+
+def time_cfg2(eb, mr, dev, ws, rank, reps: int):
+    """cfg2: C <- drop(alpha A B + beta C) in place, N = 16384, M = 128, at the required width;
+    C_old is restored (outside the timed region) before every call."""
+    import torch
+    A, B, C = synth.cfg2()
+    cf = synth.CFG2
+    ctx = _comm_ctx(eb, mr, dev, ws, rank, A.n)
+    a, b = eb.Mat.from_host(A), eb.Mat.from_host(B)
+    c = eb.Mat.from_host(C)
+    st = ctx.multiply(a, b, c, cf["alpha"], cf["beta"], cf["threshold"])
+    assert st == eb.ERR_OVERFLOW
+    w = round_up32(ctx.overflow_info()[1])
+    c0 = eb.Mat.from_host(C, w=w)
+    c = eb.Mat.from_host(C, w=w)
+    ms = []
+    for k in range(reps + 3):
+        c.val.copy_(c0.val), c.col.copy_(c0.col), c.nnz.copy_(c0.nnz)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        assert ctx.multiply(a, b, c, cf["alpha"], cf["beta"], cf["threshold"]) == eb.OK
+        e1.record()
+        torch.cuda.synchronize()
+        if k >= 3:
+            ms.append(e0.elapsed_time(e1))
+    t = statistics.median(ms)
+    if ws > 1:
+        t = mr.max_over_ranks(t, device="cuda")
+    P = synth.products(A, B)
+    ctx.close()
+    return {"workload": f"cfg2 C=aAB+bC N=16384 M=128 a=1 b=0.5 tau=1e-06 (out width {w})", "ms_per_call": t,
+            "gflops": 2.0 * P / (t * 1e-3) / 1e9, "calls": reps}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2102_08505_b200 as eb
+    from paper_2102_08505_b200 import multirank as mr
+
+    ws, rank, dev = _init(args)
+    ranks_checked = check_ranks_bitwise(eb, mr, dev, ws, rank) if ws > 1 else None
+    ctx = _comm_ctx(eb, mr, dev, ws, rank, args.n)
     if args.window:
         ctx.set_option(eb.OPT_WINDOW, args.window)
     if args.warps:
         ctx.set_option(eb.OPT_WARPS, args.warps)
-    if ws > 1:
-        uid = mr.broadcast_bytes(eb.Context.nccl_unique_id() if rank == 0 else None)
-        r0, r1 = mr.rank_rows(args.n, ws, rank)
-        ctx.attach_nccl(ws, rank, uid, r0, r1)
-    tau = 1e-5
+    tau = TAU5
     X = synth.cfg5(args.n, args.m)
     n = X.n
     P = synth.products(X, X)
@@ -266,7 +464,7 @@ def run_ours(args):
     st, _, _ = ctx.multiply_x2(x, y, tau)
     assert st == eb.ERR_OVERFLOW
     _, req = ctx.overflow_info()
-    w_out = ((req + 31) // 32) * 32
+    w_out = round_up32(req)
     del y
     y = eb.Mat.empty(n, w_out)
     stream = torch.cuda.current_stream()
@@ -274,13 +472,13 @@ def run_ours(args):
     def step():
         if ws > 1:
             ctx.halo_rows(x)  # the rows of X this rank's rows reference (band-aware halo, §8f-f1)
-        s, tx, tx2 = ctx.multiply_x2(x, y, tau)
-        return s, tx, tx2
+        return ctx.multiply_x2(x, y, tau)
 
     for _ in range(max(3, args.warmup)):
         s, tx, tx2 = step()
         assert s == eb.OK
     nnz_c = int(y.nnz.sum().item())
+    launch = ctx.last_launch()
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -305,14 +503,17 @@ def run_ours(args):
     Bc = x2_bytes(live_entries(X), nnz_c, n)
     hbm_peak, peak_src = peaks()
     kern_avg = kern_ms / max(kern_n, 1)
-    rows_local = (n // ws)
-    bytes_launch = Bc * rows_local / n if ws > 1 else Bc
+    bytes_launch = Bc / ws  # equal row blocks: the rank's share of the compulsory bytes
     achieved = bytes_launch / (kern_avg * 1e-3) / 1e9
-    traffic = ncu_traffic(f"x2_n{n}_m{args.m}")
+    cap, cap_src = ncu_capture(f"x2_n{n}_m{args.m}")
+    kname = (f"ell::row_fast_kernel<G={launch['G']}> (ring S={launch['S']}, {launch['ctas_per_sm']} CTAs/SM)"
+             if launch["path"] == "ring" else "ell::row_general_kernel")
 
-    # ---- end to end through the host-buffer ABI call (H2D of X + kernels + D2H of X^2)
+    # ---- end to end through the host-buffer ABI call (H2D of X + kernels + D2H of the rank's X^2 rows)
     e2e = None
-    if not args.no_e2e and ws == 1:
+    del y
+    torch.cuda.empty_cache()
+    if not args.no_e2e:
         hx = {k: torch.from_numpy(getattr(X, k)).pin_memory() for k in ("val", "col", "nnz")}
         hy = {"val": torch.empty((n, w_out), dtype=torch.float64).pin_memory(),
               "col": torch.empty((n, w_out), dtype=torch.int32).pin_memory(),
@@ -324,19 +525,35 @@ def run_ours(args):
         for k in hx:
             setattr(hxo, k, hx[k])
             setattr(hyo, k, hy[k])
-        del y
-        torch.cuda.empty_cache()
         ctx.multiply_x2_host(hxo, hyo, tau)  # warm (allocates the device scratch)
         torch.cuda.synchronize()
         k_e2e = max(1, min(args.steps, 3))
+        if ws > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(k_e2e):
             ctx.multiply_x2_host(hxo, hyo, tau)
         dt = (time.perf_counter() - t0) / k_e2e
-        h2d = sum(t.numel() * t.element_size() for t in hx.values())
-        d2h = sum(t.numel() * t.element_size() for t in hy.values())
+        if ws > 1:
+            dt = mr.max_over_ranks(dt, device="cuda")
+        h2d = sum(t.numel() * t.element_size() for t in hx.values()) * ws
+        d2h = sum(t.numel() * t.element_size() for t in hy.values())  # every rank brings back its rows
         e2e = {"value": 2.0 * P / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3}
+               "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3,
+               "what": "ellpack_multiply_x2_host: pinned host X -> device, X^2, padded X^2 rows -> pinned host"}
+        del hx, hy, hxo, hyo
+    clocks = clk.summary()
+    ctx.close()
+    del x
+    torch.cuda.empty_cache()
+
+    # ---- the rest of the metric: SP2 windows, cfg1 latency, cfg2
+    sp2 = cfg1 = cfg2 = None
+    if not args.quick:
+        sp2 = {"cfg3": time_sp2(eb, mr, dev, ws, rank, 3, 10, 3, 1),
+               "cfg4": time_sp2(eb, mr, dev, ws, rank, 4, 6, 2, 1)}
+        cfg1 = time_cfg1(eb, dev, 300) if ws == 1 else {"skipped": "N=512 is not divisible into 256-row blocks (R17)"}
+        cfg2 = time_cfg2(eb, mr, dev, ws, rank, 10)
 
     # ---- CPU oracle beside it (rank 0, N=1 only, bounded sample)
     cpu = None
@@ -345,36 +562,38 @@ def run_ours(args):
         dt = statistics.median([run() for _ in range(3)])
         cpu = {"value": 2.0 * Ps / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": desc}
 
-    clocks = clk.summary()
     lsu_pipe = None
-    if ws == 1:
-        lsu_pipe = lsu_floor(X, P, nnz_c, clocks.get("sm_mhz"), torch.cuda.get_device_properties(dev).multi_processor_count)
+    if ws == 1 and launch["path"] == "ring":
+        lsu_pipe = lsu_floor(X, P, nnz_c, clocks.get("sm_mhz"), torch.cuda.get_device_properties(dev).multi_processor_count,
+                             slot_bytes=args.slot_bytes)
         if lsu_pipe.get("floor_ms"):
             lsu_pipe["frac"] = lsu_pipe["floor_ms"] / kern_avg
     if rank == 0:
         line = {
             "metric": "ELLPACK X^2 multiply GFLOP/s", "value": gflops, "unit": "GFLOP/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (synth.cfg5, seed 5; BASELINE configs[4] recipe, SURVEY §8d)",
-            "config": {"workload": f"cfg5 X^2 N={n} M={args.m} tau={tau}", "products": P,
+            "config": {"workload": workload_name(n, args.m, tau), "products": P,
                        "out_width": w_out, "nnz_x": live_entries(X), "nnz_x2": nnz_c,
                        "l2": "inputs larger than L2 (X 0.8 GB padded, X^2 16 GB)",
-                       "parallelism": f"row-blocks x{ws}" if ws > 1 else "1 GPU"},
+                       "parallelism": f"row-blocks x{ws} + band-aware halo" if ws > 1 else "1 GPU"},
             "hbm_gbs_algorithmic": Bc / (ms_step * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
-                         "l2_hit_pct": ncu_l2_hit(f"x2_n{n}_m{args.m}"),
-                         "kernel": "ell::row_fast_kernel", "kernel_ms_avg": kern_avg,
+                         "frac": achieved / hbm_peak, "traffic": (cap or {}).get("dram_bytes"),
+                         "traffic_source": cap_src, "peak_source": peak_src,
+                         "l2_hit_pct": (cap or {}).get("l2_hit_pct"),
+                         "kernel": kname, "launch": launch, "kernel_ms_avg": kern_avg,
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "lsu_pipe": lsu_pipe},
+            "sp2": sp2, "cfg1": cfg1, "cfg2": cfg2,
+            "ranks_bitwise_vs_1": ranks_checked,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
-    ctx.close()
     if ws > 1:
         dist.destroy_process_group()
     return 0
@@ -384,27 +603,15 @@ def run_ours(args):
 
 def run_sp2(args):
     """SP2 iterations/sec (BASELINE metric, second half) on cfg3 or cfg4 over a fixed window of K
-    iterations (GROW policy; the configs are gapless, SURVEY §8d "SP2 protocol"): one step = one
-    sp2_run call of K iterations, timed with CUDA events on the context stream; the CPU oracle
-    runs the same window beside it (rank 0, N = 1)."""
+    iterations, or on the paper's model Hamiltonian to the stop rule (GROW policy; SURVEY §8d "SP2
+    protocol"): one step = one sp2_run call, timed with CUDA events on the context stream; the CPU
+    oracle runs the same window beside it (rank 0, N = 1)."""
     import torch
 
     import paper_2102_08505_b200 as eb
     from paper_2102_08505_b200 import multirank as mr
 
-    ws, rank, local = mr.dist_env()
-    if ws > 1:
-        torch.cuda.set_device(local)
-        mr.init_process_group("nccl", device=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.cuda.current_device()
-    eb.build()
-    ctx = eb.Context(dev)
-    if args.general_window:
-        ctx.set_option(eb.OPT_GENERAL_WINDOW, args.general_window)
-    if args.no_sp2_symmetric:
-        ctx.set_option(eb.OPT_SP2_SYMMETRIC, 0)
+    ws, rank, dev = _init(args)
     if args.sp2_model:
         # the paper's own gapped SP2 workloads (P:L419-433, P:L495-497; SURVEY §8f f2), run to the stop rule
         H = synth.model_hamiltonian(args.sp2_n, args.sp2_model, tau_store=1e-5)
@@ -414,10 +621,11 @@ def run_sp2(args):
     else:
         H, cf = synth.cfg4(), synth.CFG4
     n = H.n
-    if ws > 1:
-        uid = mr.broadcast_bytes(eb.Context.nccl_unique_id() if rank == 0 else None)
-        r0, r1 = mr.rank_rows(n, ws, rank)
-        ctx.attach_nccl(ws, rank, uid, r0, r1)
+    ctx = _comm_ctx(eb, mr, dev, ws, rank, n)
+    if args.general_window:
+        ctx.set_option(eb.OPT_GENERAL_WINDOW, args.general_window)
+    if args.no_sp2_symmetric:
+        ctx.set_option(eb.OPT_SP2_SYMMETRIC, 0)
     K = args.sp2_iters
     h = eb.Mat.from_host(H)
     d = eb.Mat.empty(n, min(n + (n & 1), 8192))
@@ -428,11 +636,12 @@ def run_sp2(args):
 
     for _ in range(max(1, args.warmup)):
         r = step()
-    prods = sum(it.get("products", 0) for it in r.iters) if r.iters and "products" in r.iters[0] else None
+    prods = sum(it["products"] for it in r.iters)
+    pexec = sum(it["products_exec"] for it in r.iters)
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    launches0 = ctx.kernel_launches()
+    launches0, syncs0 = ctx.kernel_launches(), ctx.host_syncs()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev) as clk:
         e0.record(stream)
@@ -444,6 +653,7 @@ def run_sp2(args):
     if ws > 1:
         ms = mr.max_over_ranks(ms, device="cuda")
     its = r.iterations
+    syncs = (ctx.host_syncs() - syncs0) / args.steps
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         import oracle
@@ -453,6 +663,8 @@ def run_sp2(args):
         dt = time.perf_counter() - t0
         cpu = {"value": o.iterations / dt, "unit": "iterations/s", "cores": oracle.num_threads(), "kind": "oracle",
                "sample": f"the same {K}-iteration window (stop {o.stop}, width {o.final_width})"}
+    rmw = microbench("smem_rmw_f64_random_peak")
+    rate = pexec / (ms * 1e-3)
     if rank == 0:
         line = {
             "metric": "SP2 iterations/sec", "value": its / (ms * 1e-3), "unit": "iterations/s", "n_gpus": ws,
@@ -460,12 +672,17 @@ def run_sp2(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": (f"synthetic (synth.model_hamiltonian {args.sp2_model}, P:L419-433)" if args.sp2_model
                      else f"synthetic (synth.cfg{args.sp2_cfg}, SURVEY §8d)"),
-            "config": {"workload": (f"{args.sp2_model} SP2 N={n} tau={cf['threshold']} max_iter={K} GROW"
+            "config": {"workload": (f"{args.sp2_model} SP2 N={n} tau={cf['threshold']:g} max_iter={K} GROW"
                                     if args.sp2_model else
-                                    f"cfg{args.sp2_cfg} SP2 N={n} tau={cf['threshold']} window K={K} GROW"),
+                                    f"cfg{args.sp2_cfg} SP2 N={n} tau={cf['threshold']:g} window K={K} GROW"),
                        "iterations": its, "stop": r.stop, "final_width": r.final_width, "regrows": r.regrows,
-                       "products": prods, "gflops": (2.0 * prods / (ms * 1e-3) / 1e9) if prods else None,
-                       "phases_s": r.phases},
+                       "products": prods, "products_executed": pexec,
+                       "gflops_effective": 2.0 * prods / (ms * 1e-3) / 1e9,
+                       "gflops_executed": 2.0 * pexec / (ms * 1e-3) / 1e9,
+                       "host_syncs_per_iteration": syncs / max(its, 1), "phases_s": r.phases},
+            "roofline": {"bound": "smem_rmw", "achieved": rate / 1e9, "unit": "Gupd/s",
+                         "peak": rmw["Gupd_per_s"] if rmw else None,
+                         "frac": (rate / 1e9 / rmw["Gupd_per_s"]) if rmw else None},
             "cpu_baseline": cpu, "gpu_launches": ctx.kernel_launches() - launches0, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -473,6 +690,12 @@ def run_sp2(args):
     if ws > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def main():
@@ -487,9 +710,11 @@ def main():
     ap.add_argument("--warps", type=int, default=0, help="warps per CTA (0 = auto)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="headline only (no sp2 / cfg1 / cfg2 sub-objects)")
     ap.add_argument("--ref-budget", type=float, default=20.0, help="seconds of oracle work per sample")
+    ap.add_argument("--slot-bytes", type=int, default=4, help="B-record slot index bytes (LSU floor model)")
     ap.add_argument("--workload", default="x2", choices=["x2", "sp2"],
-                    help="x2: the headline cfg5 X^2 (default); sp2: SP2 iterations/sec on cfg3/cfg4")
+                    help="x2: the headline cfg5 X^2 line (default); sp2: one SP2 line on cfg3/cfg4/a model H")
     ap.add_argument("--sp2-cfg", type=int, default=3, choices=[3, 4])
     ap.add_argument("--sp2-iters", type=int, default=10, help="SP2 window (max_iter)")
     ap.add_argument("--sp2-model", default=None, choices=["metal", "semiconductor", "soft_matter"],
@@ -499,14 +724,29 @@ def main():
     ap.add_argument("--no-sp2-symmetric", action="store_true",
                     help="SP2: compute whole rows even when H is symmetric (A/B of §8f-f4 ii)")
     args = ap.parse_args()
-    if args.workload == "sp2":
-        if args.impl == "reference":
-            print(json.dumps({"impl": "reference", "unavailable": "--workload sp2 reports the oracle inline "
-                              "(cpu_baseline); the reference arm is the x2 workload"}))
-            return 0
-        return run_sp2(args)
+    if args.workload == "sp2" and args.impl == "reference":
+        print(json.dumps({"impl": "reference", "unavailable": "--workload sp2 reports the oracle inline "
+                          "(cpu_baseline); the reference arm is the x2 workload"}))
+        return 0
+    env_ws = os.environ.get("WORLD_SIZE")
+    if env_ws is None and args.gpus > 1:
+        # one process per GPU: re-execute under torch.distributed.run (rendezvous on 127.0.0.1)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+               *sys.argv[1:]]
+        return subprocess.call(cmd)
+    if env_ws is not None and int(env_ws) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_ws}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
+    import torch
+    if torch.cuda.device_count() < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but only {torch.cuda.device_count()} CUDA device(s) visible",
+              file=sys.stderr)
+        return 2
+    if args.workload == "sp2":
+        return run_sp2(args)
     return run_ours(args)
 
 

@@ -138,6 +138,13 @@ int64_t ellpack_ctx_kernel_launches(ellpack_ctx ctx);
  * counter for the SP2 control path: sp2_run waits once per iteration). */
 int64_t ellpack_ctx_host_syncs(ellpack_ctx ctx);
 
+/* Launch geometry of the last fused row-kernel launch on this context (what bench.py reports
+ * beside its roofline): out[0] path (1 ring fast path, 0 general path), out[1] G (64-entry B
+ * groups per step, fast path), out[2] S (ring / window doubles per row), out[3] warps per CTA,
+ * out[4] grid, out[5] dynamic shared memory bytes per CTA, out[6] resident CTAs per SM,
+ * out[7] B half-bandwidth of the probe. Errors: ARG. */
+int ellpack_ctx_last_launch(ellpack_ctx ctx, int32_t out[8]);
+
 /* --------------------------------------------------------------- storage */
 
 /* ellpack_create(N, M) (BJ north_star): allocate an N x M matrix on
@@ -237,6 +244,8 @@ typedef struct sp2_iter_rec {
     int32_t reserved;
     int64_t products;          /* scalar products of this X^2 (pattern count) */
     double frob2;              /* TRACE_CLOSEST: T2 of X_n that decided the branch; else 0 */
+    int64_t products_exec;     /* products the GPU executed for this step: = products, or about half
+                                  of them when the symmetric step (ELLPACK_OPT_SP2_SYMMETRIC) ran */
 } sp2_iter_rec;
 
 typedef struct sp2_report {
@@ -275,9 +284,10 @@ void sp2_opts_default(sp2_opts* opts);
 
 /* End-to-end X^2 through HOST memory (the bench's e2e leg): copies X (host
  * arrays, n x wx) to the device, runs ellpack_multiply_x2 into a device buffer of
- * width wx2, copies X2 back into the host arrays (n x wx2). Host arrays should be
- * pinned for full PCIe bandwidth. Device scratch is owned by the context and
- * reused across calls. Errors as ellpack_multiply_x2. */
+ * width wx2, copies X2 back into the host arrays (n x wx2) -- with a communicator
+ * only this rank's rows [row_begin, row_end) of X2 (X is copied whole: it is the B
+ * operand). Host arrays should be pinned for full PCIe bandwidth. Device scratch is
+ * owned by the context and reused across calls. Errors as ellpack_multiply_x2. */
 int ellpack_multiply_x2_host(ellpack_ctx ctx, int64_t n,
                              int32_t wx, const double* x_val, const int32_t* x_col, const int32_t* x_nnz,
                              int32_t wx2, double* x2_val, int32_t* x2_col, int32_t* x2_nnz,

@@ -36,7 +36,8 @@ STOP_NAMES = {0: "CONVERGED", 1: "STAGNATED", 2: "NOCONV", 3: "OVERFLOW"}
 # Every symbol include/ellpack.h declares (checked by tests/test_abi.py).
 ABI_SYMBOLS = (
     "ellpack_ctx_create", "ellpack_ctx_destroy", "ellpack_ctx_set_stream", "ellpack_ctx_set_option",
-    "ellpack_ctx_kernel_launches", "ellpack_ctx_host_syncs", "ellpack_ctx_kernel_time", "ellpack_create", "ellpack_destroy", "ellpack_multiply",
+    "ellpack_ctx_kernel_launches", "ellpack_ctx_host_syncs", "ellpack_ctx_last_launch", "ellpack_ctx_kernel_time",
+    "ellpack_create", "ellpack_destroy", "ellpack_multiply",
     "ellpack_multiply_x2", "ellpack_add", "ellpack_add_identity", "ellpack_scale_add_identity",
     "ellpack_trace", "ellpack_fnorm_diff", "ellpack_gershgorin", "ellpack_overflow_info", "sp2_run",
     "sp2_opts_default", "ellpack_multiply_x2_host", "ellpack_nccl_unique_id", "ellpack_ctx_attach_nccl",
@@ -89,7 +90,7 @@ class SP2IterRec(ctypes.Structure):
     _fields_ = [("trX", ctypes.c_double), ("trS", ctypes.c_double), ("e", ctypes.c_double),
                 ("fnorm", ctypes.c_double), ("branch", ctypes.c_int32), ("width", ctypes.c_int32),
                 ("required", ctypes.c_int32), ("reserved", ctypes.c_int32), ("products", ctypes.c_int64),
-                ("frob2", ctypes.c_double)]
+                ("frob2", ctypes.c_double), ("products_exec", ctypes.c_int64)]
 
 
 class SP2Report(ctypes.Structure):
@@ -117,7 +118,7 @@ def lib() -> ctypes.CDLL:
         D = ctypes.POINTER(Desc)
         sig = {
             "ellpack_ctx_create": [i, P, P], "ellpack_ctx_destroy": [P], "ellpack_ctx_set_stream": [P, P],
-            "ellpack_ctx_set_option": [P, i, i64], "ellpack_ctx_kernel_launches": [P], "ellpack_ctx_host_syncs": [P],
+            "ellpack_ctx_set_option": [P, i, i64], "ellpack_ctx_kernel_launches": [P], "ellpack_ctx_host_syncs": [P], "ellpack_ctx_last_launch": [P, P],
             "ellpack_ctx_kernel_time": [P, P, P],
             "ellpack_create": [P, i64, i32, D], "ellpack_destroy": [P, D],
             "ellpack_multiply": [P, D, D, D, d, d, d], "ellpack_multiply_x2": [P, D, D, d, P, P],
@@ -254,6 +255,13 @@ class Context:
     def kernel_launches(self) -> int:
         return int(lib().ellpack_ctx_kernel_launches(self._h))
 
+    def last_launch(self) -> dict:
+        """Geometry of the last row-kernel launch (ellpack_ctx_last_launch)."""
+        a = (ctypes.c_int32 * 8)()
+        _chk(lib().ellpack_ctx_last_launch(self._h, a), "ellpack_ctx_last_launch")
+        return dict(path="ring" if a[0] else "general", G=a[1], S=a[2], warps_per_cta=a[3], grid=a[4],
+                    smem_bytes=a[5], ctas_per_sm=a[6], hB=a[7])
+
     def host_syncs(self) -> int:
         """Blocking host synchronisations of the context stream so far (evidence counter)."""
         return int(lib().ellpack_ctx_host_syncs(self._h))
@@ -329,7 +337,8 @@ class Context:
         n_rec = min(rep.iterations, max_iter)
         iters = [dict(trX=recs[k].trX, trS=recs[k].trS, e=recs[k].e, fnorm=recs[k].fnorm,
                       branch="SQUARE" if recs[k].branch == 0 else "EXPAND", width=recs[k].width,
-                      required=recs[k].required, products=recs[k].products, frob2=recs[k].frob2)
+                      required=recs[k].required, products=recs[k].products, frob2=recs[k].frob2,
+                      products_exec=recs[k].products_exec)
                  for k in range(n_rec)]
         phases = dict(read_hamiltonian=rep.t_read_hamiltonian, init_misc=rep.t_init_misc,
                       sp2_loop_x2=rep.t_sp2_loop_x2, sp2_loop_norm=rep.t_sp2_loop_norm,

@@ -104,11 +104,13 @@ struct ellpack_ctx_s {
     double* d_sums = nullptr;                 // final sums (<= 8)
     int32_t* d_bw = nullptr;                  // bandwidth probe [0..5]; [8] agreed width (comm)
     LaunchCfg last_cfg{};
+    int32_t last_fast = 0, last_hB = 0;
+    bool last_step_general = false;
     struct Host {
         int32_t bw[6];
         int32_t status_u[2];
         int32_t status[4];
-        unsigned long long keys[2];
+        unsigned long long keys[4];
         double sums[8];
         int32_t imax;
     }* h = nullptr;
@@ -402,6 +404,8 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
         p.bp_np = np;
     }
     c->last_cfg = cfg;
+    c->last_fast = p.fast;
+    c->last_hB = (int32_t)hB;
     const int64_t total_warps = (int64_t)cfg.grid * cfg.warps_per_cta;
     const bool may_multi = n > cfg.S;
     p.st_val = nullptr;
@@ -690,6 +694,20 @@ int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
 int64_t ellpack_ctx_kernel_launches(ellpack_ctx c) { return c ? c->launches : -1; }
 
 int64_t ellpack_ctx_host_syncs(ellpack_ctx c) { return c ? c->host_syncs : -1; }
+
+int ellpack_ctx_last_launch(ellpack_ctx c, int32_t out[8]) {
+    if (!c || !out) return ELLPACK_ERR_ARG;
+    const LaunchCfg& g = c->last_cfg;
+    out[0] = c->last_fast;
+    out[1] = g.R;
+    out[2] = g.S;
+    out[3] = g.warps_per_cta;
+    out[4] = g.grid;
+    out[5] = (int32_t)g.smem;
+    out[6] = g.bps;
+    out[7] = c->last_hB;
+    return ELLPACK_OK;
+}
 
 int ellpack_ctx_kernel_time(ellpack_ctx c, double* ms, int64_t* launches) {
     if (!c) return ELLPACK_ERR_ARG;
@@ -1419,6 +1437,8 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             p.diag_c = (double*)c->rows[1].p;
             p.normsq = (double*)c->rows[2].p;
             p.upper = sym && !sym_off;  // taken only if the general path runs (enqueue_row_op)
+            CK(cudaMemsetAsync(c->d_keys + 4, 0, 8, c->stream));
+            p.exec_products = c->d_keys + 4;
             ua.w = Y.d.w;
             cudaEventRecord(c->ev[0], c->stream);
             if ((rc = enqueue_row_op(c, p, n, bwX, alloc_upper, &ua))) { status = rc; break; }
@@ -1436,6 +1456,10 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
                                        c->d_status, c->num_sms, c->stream));
                 c->launches += 2;
             }
+            if (c->comm)
+                NK(g_nccl.AllReduce(c->d_keys + 4, c->d_keys + 4, 1, ncclUint64, ncclSum, c->comm, c->stream));
+            CK(cudaMemcpyAsync(&c->h->keys[1], c->d_keys + 4, 8, cudaMemcpyDeviceToHost, c->stream));
+            c->last_step_general = !p.fast;
             cudaEventRecord(c->ev[1], c->stream);
             if ((rc = reduce_status(c))) { status = rc; break; }
             if (closest) {
@@ -1475,10 +1499,11 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             if (kept_max > wy) {
                 // the logical width grows (the oracle's regrow)
                 if (o.on_overflow == SP2_FAIL || kept_max > maxw) {
-                    // rows over the LOGICAL width wy (Y's counts are exact up to its physical
-                    // width >= wy, so the kernel counts rows over wy exactly)
-                    int64_t ovf = 0;
-                    if ((rc = count_rows_over(c, &Y.d, wy, &ovf))) { status = rc; break; }
+                    // rows over the LOGICAL width wy: the step's status counts rows over the
+                    // physical width; when that is wider, Y's stored counts min(kept, physical)
+                    // exceed wy exactly for the rows whose kept count does
+                    int64_t ovf = c->h->status[0];
+                    if (Y.d.w > wy && (rc = count_rows_over(c, &Y.d, wy, &ovf))) { status = rc; break; }
                     R.stop_reason = SP2_OVERFLOWED;
                     R.overflow_rows = ovf;
                     R.required_width = kept_max;
@@ -1519,6 +1544,8 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             iters[it].reserved = 0;
             iters[it].products = (int64_t)c->h->keys[0];  // landed with the status fetch
             iters[it].frob2 = t2;
+            // products executed: the general kernel counts them; the ring path runs all of them
+            iters[it].products_exec = c->last_step_general ? (int64_t)c->h->keys[1] : (int64_t)c->h->keys[0];
         }
         if (closest) t2 = c->h->sums[3];
         take_probe(c, bwX, needX);
@@ -1589,9 +1616,13 @@ int ellpack_multiply_x2_host(ellpack_ctx c, int64_t n, int32_t wx, const double*
     double tx = 0, tx2 = 0;
     int rc = ellpack_multiply_x2(c, &X, &Y, tau, &tx, &tx2);
     if (rc != ELLPACK_OK && rc != ELLPACK_ERR_OVERFLOW) return rc;
-    CK(cudaMemcpyAsync(yv, Y.val, cy * 8, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(yc, Y.col, cy * 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(yn, Y.nnz, n * 4, cudaMemcpyDeviceToHost, c->stream));
+    // this rank's rows of X^2 (all rows on one rank) come back
+    int64_t r0, r1;
+    rows_of(c, n, &r0, &r1);
+    const size_t o0 = (size_t)r0 * wx2, cr = (size_t)(r1 - r0) * wx2;
+    CK(cudaMemcpyAsync(yv + o0, Y.val + o0, cr * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(yc + o0, Y.col + o0, cr * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(yn + r0, Y.nnz + r0, (size_t)(r1 - r0) * 4, cudaMemcpyDeviceToHost, c->stream));
     RK(host_sync(c));
     if (rc == ELLPACK_OK) {
         if (trace_x) *trace_x = tx;

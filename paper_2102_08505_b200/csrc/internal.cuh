@@ -62,6 +62,8 @@ struct RowOpParams {
     int32_t row_chunk;               // fast kernel: consecutive rows per ticket (4; 1 for small launches)
     int32_t upper;                   // general kernel: columns j >= i only (symmetric SP2 step, f4 ii)
     KOut C_upper;                    // upper-triangle output when the general path takes `upper`
+    unsigned long long* exec_products;  // general kernel (nullable): += products it executes (B entries
+                                        // accumulated; the symmetric step's count, about P / 2)
     // per-warp global scratch: in-place rows are copied aside (stash) before they are rewritten
     double* st_val;
     int32_t* st_col;

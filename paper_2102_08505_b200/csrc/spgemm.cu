@@ -1106,6 +1106,7 @@ __global__ void __launch_bounds__(128, ELL_GEN_MINB) row_general_kernel(const Ro
     clear_window<MODE>(w, lane, S);
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
     int32_t my_max_kept = 0, my_ovf = 0;
+    unsigned long long my_exec = 0;  // products this lane staged (p.exec_products)
     for (int64_t i = p.row_begin + next_row(p, lane); i < p.row_end; i = p.row_begin + next_row(p, lane)) {
         RowIO r = row_io<MODE>(p, i);
         const double* a_val = r.a_val;
@@ -1195,6 +1196,7 @@ __global__ void __launch_bounds__(128, ELL_GEN_MINB) row_general_kernel(const Ro
                                 }
                             }
                             const bool ne = se > sb;
+                            if (ne) my_exec += (unsigned long long)(se - sb);
                             const unsigned m = __ballot_sync(FULL, ne);
                             if (ne) {
                                 const int t = ns + __popc(m & ((1u << lane) - 1u));
@@ -1226,6 +1228,11 @@ __global__ void __launch_bounds__(128, ELL_GEN_MINB) row_general_kernel(const Ro
         row_epilogue<MODE>(p, lane, i, kept, dA, ds, dc, nrm, my_max_kept, my_ovf);
     }
     flush_status(p, lane, my_max_kept, my_ovf);
+    if (p.exec_products) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) my_exec += __shfl_xor_sync(FULL, my_exec, o);
+        if (lane == 0 && my_exec) atomicAdd(p.exec_products, my_exec);
+    }
 }
 
 // Half-bandwidth probe: out[m] = max over rows of max(i - col[i][0], col[i][nnz-1] - i) (a and c

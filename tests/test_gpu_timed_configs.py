@@ -34,17 +34,18 @@ def test_cfg5_full_size_every_row_bitwise(ctx):
     y = eb().Mat.empty(X.n, w)
     st, tx, tx2 = ctx.multiply_x2(x, y, 1e-5)
     assert st == eb().OK
-    r = oracle.x2(X, Ell.empty(X.n, 2), 1e-5)  # traces + exact required width (output discarded)
-    assert r.status == oracle.OVERFLOW and r.required_width == req
-    assert (tx, tx2) == (r.trace_x, r.trace_x2)
     blk = 16384
+    ds = np.zeros(X.n)  # pre-drop diagonal of X^2, assembled from the blocks (tr X^2, R5)
+    kept_max = 0
     for r0 in range(0, X.n, blk):
         r1 = r0 + blk
         A = Ell.empty(X.n, X.w)  # X restricted to the block's rows (rows are independent)
         A.val[r0:r1], A.col[r0:r1], A.nnz[r0:r1] = X.val[r0:r1], X.col[r0:r1], X.nnz[r0:r1]
         Y = Ell.empty(X.n, w)
-        ro = oracle.multiply(A, X, Y, 1.0, 0.0, 1e-5)
+        ro = oracle.multiply(A, X, Y, 1.0, 0.0, 1e-5, want_diag=True)
         assert ro.status == oracle.OK
+        ds[r0:r1] = ro.diag_s[r0:r1]
+        kept_max = max(kept_max, ro.required_width)
         gn = y.nnz[r0:r1].cpu().numpy()
         assert np.array_equal(gn, Y.nnz[r0:r1]), r0
         gc = y.col[r0:r1].cpu().numpy()
@@ -53,6 +54,8 @@ def test_cfg5_full_size_every_row_bitwise(ctx):
         assert np.array_equal(gc[live], Y.col[r0:r1][live]), r0
         assert np.array_equal(gv[live].view(np.uint64), Y.val[r0:r1][live].view(np.uint64)), r0
         del A, Y, gc, gv
+    assert kept_max == req  # the literal-width call's required width is the oracle's max kept count
+    assert tx == oracle.trace(X) and tx2 == oracle.canonical_sum(ds)
     torch.cuda.synchronize()
 
 

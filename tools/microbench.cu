@@ -26,7 +26,9 @@ __global__ void gather12(const double* __restrict__ v, const int* __restrict__ c
     if (acc == 1234.5) out[0] = acc;
 }
 
-__global__ void smem_rmw(const int* __restrict__ idx, int nidx, int S, int reps, double* out) {
+// mode 0: random addresses (the accumulator of a sparse row: bank-pair collisions at random);
+// mode 1: 32 consecutive doubles per instruction (conflict-free: 2 wavefronts per 32 lanes)
+__global__ void smem_rmw(const int* __restrict__ idx, int nidx, int S, int reps, int mode, double* out) {
     extern __shared__ double win[];
     int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double* a = win + wid * S;
@@ -36,7 +38,7 @@ __global__ void smem_rmw(const int* __restrict__ idx, int nidx, int S, int reps,
     for (int r = 0; r < reps; ++r) {
         #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            int j = idx[base + (r * 4 + u) * 32 + lane] % S;
+            int j = mode ? (((r * 4 + u) * 32 + lane) & (S - 1)) : (idx[base + (r * 4 + u) * 32 + lane] % S);
             a[j] = __fma_rn(1.0000001, 0.5, a[j]);
         }
         __syncwarp();
@@ -90,17 +92,20 @@ int main() {
         int nidx = 1 << 22; int* h = new int[nidx]; uint64_t s = 99;
         for (int i = 0; i < nidx; ++i) { s = s * 6364136223846793005ull + 1442695040888963407ull; h[i] = (int)(s >> 33); }
         int* idx; CK(cudaMalloc(&idx, nidx * 4)); CK(cudaMemcpy(idx, h, nidx * 4, cudaMemcpyHostToDevice));
-        for (int S : {2048, 4096, 8192}) for (int wpc : {4}) {
+        for (int mode : {0, 1}) for (int S : {512, 1024, 2048, 4096}) for (int wpc : {1, 2, 4, 8}) {
             size_t smem = (size_t)wpc * S * 8;
+            if (smem > 227 * 1024) continue;
             cudaFuncSetAttribute(smem_rmw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             int bps = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, smem_rmw, wpc * 32, smem);
+            if (bps < 1) continue;
             int grid = sms * bps * 4, reps = 2048;
-            smem_rmw<<<grid, wpc * 32, smem>>>(idx, nidx, S, 16, out); CK(cudaDeviceSynchronize());
+            smem_rmw<<<grid, wpc * 32, smem>>>(idx, nidx, S, 16, mode, out); CK(cudaDeviceSynchronize());
             cudaEventRecord(e0);
-            smem_rmw<<<grid, wpc * 32, smem>>>(idx, nidx, S, reps, out);
+            smem_rmw<<<grid, wpc * 32, smem>>>(idx, nidx, S, reps, mode, out);
             cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
             double upd = (double)grid * wpc * 32 * 4 * reps;
-            printf("{\"bench\":\"smem_rmw_f64\",\"S\":%d,\"warps_per_sm\":%d,\"Gupd_per_s\":%.1f,\"ms\":%.3f}\n", S, bps * wpc, upd / ms / 1e6, ms);
+            printf("{\"bench\":\"smem_rmw_f64\",\"addresses\":\"%s\",\"S\":%d,\"warps_per_sm\":%d,\"Gupd_per_s\":%.1f,\"ms\":%.3f}\n",
+                   mode ? "conflict_free" : "random", S, bps * wpc, upd / ms / 1e6, ms);
         }
         cudaFree(idx); delete[] h;
     }
