@@ -78,6 +78,8 @@ def ncu_capture(key: str):
     d = json.load(open(p)).get(key)
     if not d:
         return None, "no capture of this workload"
+    if not isinstance(d, dict):
+        return None, "capture predates kernel-source hashing"
     if d.get("src_sha") != kernel_src_sha():
         return None, f"capture {d.get('source')} is of kernel source {d.get('src_sha')}, not the current one"
     return d, d.get("source")
@@ -506,8 +508,10 @@ def run_ours(args):
     bytes_launch = Bc / ws  # equal row blocks: the rank's share of the compulsory bytes
     achieved = bytes_launch / (kern_avg * 1e-3) / 1e9
     cap, cap_src = ncu_capture(f"x2_n{n}_m{args.m}")
-    kname = (f"ell::row_fast_kernel<G={launch['G']}> (ring S={launch['S']}, {launch['ctas_per_sm']} CTAs/SM)"
-             if launch["path"] == "ring" else "ell::row_general_kernel")
+    kname = {"split": f"ell::row_split_kernel<W={launch['warps_per_cta']},G={launch['G']}> (ring S={launch['S']}, "
+                      f"{launch['ctas_per_sm']} rows/SM)",
+             "ring": f"ell::row_fast_kernel<G={launch['G']}> (ring S={launch['S']}, {launch['ctas_per_sm']} CTAs/SM)",
+             "general": "ell::row_general_kernel"}[launch["path"]]
 
     # ---- end to end through the host-buffer ABI call (H2D of X + kernels + D2H of the rank's X^2 rows)
     e2e = None
@@ -563,9 +567,9 @@ def run_ours(args):
         cpu = {"value": 2.0 * Ps / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": desc}
 
     lsu_pipe = None
-    if ws == 1 and launch["path"] == "ring":
+    if ws == 1 and launch["path"] in ("ring", "split"):
         lsu_pipe = lsu_floor(X, P, nnz_c, clocks.get("sm_mhz"), torch.cuda.get_device_properties(dev).multi_processor_count,
-                             slot_bytes=args.slot_bytes)
+                             slot_bytes=2 if launch["path"] == "split" else 4)
         if lsu_pipe.get("floor_ms"):
             lsu_pipe["frac"] = lsu_pipe["floor_ms"] / kern_avg
     if rank == 0:
@@ -712,7 +716,6 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="headline only (no sp2 / cfg1 / cfg2 sub-objects)")
     ap.add_argument("--ref-budget", type=float, default=20.0, help="seconds of oracle work per sample")
-    ap.add_argument("--slot-bytes", type=int, default=4, help="B-record slot index bytes (LSU floor model)")
     ap.add_argument("--workload", default="x2", choices=["x2", "sp2"],
                     help="x2: the headline cfg5 X^2 line (default); sp2: one SP2 line on cfg3/cfg4/a model H")
     ap.add_argument("--sp2-cfg", type=int, default=3, choices=[3, 4])

@@ -121,10 +121,16 @@ int ellpack_ctx_set_stream(ellpack_ctx ctx, void* stream);
  *                          in device memory when the value arrays of its live iterates (X_n, X_{n+1},
  *                          the symmetric step's upper triangle) would exceed this many bytes
  *                          (exercises the fallback from the headroom width to the exact width and the
- *                          symmetric step's whole-row fallback); 0 = off (default). */
+ *                          symmetric step's whole-row fallback); 0 = off (default).
+ *  ELLPACK_OPT_RING_KERNEL which kernel runs rows on the ring (narrow-band) path: 0 = automatic
+ *                          (the split-row kernel with 1 warp per row whenever the output does not
+ *                          alias an input and the ring fits 16-bit offsets, else the legacy ring
+ *                          kernel), 1 = always the legacy ring kernel, 2 = the split-row kernel
+ *                          with 1 warp per row, 3 = with 2 warps per row. Results are bitwise the
+ *                          same for every choice (A/B experiments and tests). */
 enum { ELLPACK_OPT_WINDOW = 1, ELLPACK_OPT_WARPS = 2, ELLPACK_OPT_SP2_WIDTH0 = 3, ELLPACK_OPT_PROFILE = 4,
        ELLPACK_OPT_ABLATE = 5, ELLPACK_OPT_GENERAL_WINDOW = 6, ELLPACK_OPT_VALIDATE = 7,
-       ELLPACK_OPT_SP2_SYMMETRIC = 8, ELLPACK_OPT_SP2_MEM_CAP = 9 };
+       ELLPACK_OPT_SP2_SYMMETRIC = 8, ELLPACK_OPT_SP2_MEM_CAP = 9, ELLPACK_OPT_RING_KERNEL = 10 };
 int ellpack_ctx_set_option(ellpack_ctx ctx, int key, int64_t value);
 
 /* Accumulated device time (ms, CUDA events on the ctx stream) and launch count of
@@ -139,8 +145,9 @@ int64_t ellpack_ctx_kernel_launches(ellpack_ctx ctx);
 int64_t ellpack_ctx_host_syncs(ellpack_ctx ctx);
 
 /* Launch geometry of the last fused row-kernel launch on this context (what bench.py reports
- * beside its roofline): out[0] path (1 ring fast path, 0 general path), out[1] G (64-entry B
- * groups per step, fast path), out[2] S (ring / window doubles per row), out[3] warps per CTA,
+ * beside its roofline): out[0] path (2 split-row ring kernel, 1 one-warp ring kernel, 0 general
+ * path), out[1] G (64-entry B groups per step, ring paths), out[2] S (ring / window doubles per
+ * row), out[3] warps per CTA (split kernel: warps per row),
  * out[4] grid, out[5] dynamic shared memory bytes per CTA, out[6] resident CTAs per SM,
  * out[7] B half-bandwidth of the probe. Errors: ARG. */
 int ellpack_ctx_last_launch(ellpack_ctx ctx, int32_t out[8]);

@@ -22,13 +22,14 @@ from dataclasses import dataclass, field
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _REPO = os.path.dirname(_HERE)
 _LIB = os.environ.get("ELLPACK_LIB") or os.path.join(_HERE, "libellpack.so")
-_SRCS = [os.path.join(_HERE, "csrc", f) for f in ("spgemm.cu", "reduce.cu", "api.cu")]
-_HDRS = [os.path.join(_HERE, "csrc", "internal.cuh"), os.path.join(_REPO, "include", "ellpack.h")]
+_SRCS = [os.path.join(_HERE, "csrc", f) for f in ("spgemm.cu", "split.cu", "reduce.cu", "api.cu")]
+_HDRS = [os.path.join(_HERE, "csrc", f) for f in ("internal.cuh", "devutil.cuh")] + [os.path.join(_REPO, "include", "ellpack.h")]
 
 OK, ERR_ARG, ERR_DIM, ERR_OVERFLOW, ERR_BOUNDS, ERR_NOCONV, ERR_NOMEM, ERR_CUDA, ERR_NCCL, ERR_STATE = range(10)
 OPT_WINDOW, OPT_WARPS, OPT_SP2_WIDTH0, OPT_PROFILE, OPT_ABLATE, OPT_GENERAL_WINDOW, OPT_VALIDATE = 1, 2, 3, 4, 5, 6, 7
 OPT_SP2_SYMMETRIC = 8
 OPT_SP2_MEM_CAP = 9
+OPT_RING_KERNEL = 10
 SP2_FAIL, SP2_GROW = 0, 1
 SP2_RULE_TRACE_SIGN, SP2_RULE_TRACE_CLOSEST = 0, 1
 STOP_NAMES = {0: "CONVERGED", 1: "STAGNATED", 2: "NOCONV", 3: "OVERFLOW"}
@@ -57,13 +58,22 @@ def build(force: bool = False, verbose: bool = False, defines=()) -> str:
     stale = force or defines or not os.path.exists(_LIB) or any(
         os.path.getmtime(s) > os.path.getmtime(_LIB) for s in _SRCS + _HDRS)
     if stale:
+        import tempfile
         tmp = _LIB + f".tmp{os.getpid()}"
-        cmd = ["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-               "-Xcompiler", "-fPIC", "-shared", "-I" + os.path.join(_REPO, "include"),
-               "-I" + _nccl_include(), *[f"-D{d}" for d in defines], *_SRCS, "-o", tmp, "-ldl"]
+        flags = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+                 "-Xcompiler", "-fPIC", "-I" + os.path.join(_REPO, "include"), "-I" + _nccl_include(),
+                 *[f"-D{d}" for d in defines]]
         if verbose:
-            cmd.insert(1, "-Xptxas=-v")
-        subprocess.check_call(cmd, cwd=_HERE)
+            flags.insert(0, "-Xptxas=-v")
+        with tempfile.TemporaryDirectory(prefix="ellbuild_") as td:
+            # one nvcc per translation unit, in parallel, then one link
+            objs = [os.path.join(td, os.path.basename(src) + ".o") for src in _SRCS]
+            procs = [subprocess.Popen(["nvcc", *flags, "-c", src, "-o", o], cwd=_HERE) for src, o in zip(_SRCS, objs)]
+            rcs = [pr.wait() for pr in procs]
+            if any(rcs):
+                raise subprocess.CalledProcessError(max(rcs), "nvcc")
+            subprocess.check_call(["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp,
+                                   "-ldl"], cwd=_HERE)
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -259,7 +269,7 @@ class Context:
         """Geometry of the last row-kernel launch (ellpack_ctx_last_launch)."""
         a = (ctypes.c_int32 * 8)()
         _chk(lib().ellpack_ctx_last_launch(self._h, a), "ellpack_ctx_last_launch")
-        return dict(path="ring" if a[0] else "general", G=a[1], S=a[2], warps_per_cta=a[3], grid=a[4],
+        return dict(path={2: "split", 1: "ring", 0: "general"}[a[0]], G=a[1], S=a[2], warps_per_cta=a[3], grid=a[4],
                     smem_bytes=a[5], ctas_per_sm=a[6], hB=a[7])
 
     def host_syncs(self) -> int:

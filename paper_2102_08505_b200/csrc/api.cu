@@ -33,7 +33,9 @@ using namespace ell;
 // kFastWindowMax use the multi-pass general path with kGeneralWindow.
 constexpr int64_t kFastWindowMax = 12288;  // 96 KB + stage per warp
 constexpr int kFastMinRows = 4;            // ring path only with >= 4 rows resident per SM
-constexpr int64_t kGeneralWindow = 1024;  // measured best for cfg3/cfg4 SP2 (512..4096 swept)
+constexpr int64_t kGeneralWindow = 1024;
+constexpr int kProbe = 7;  // bandwidth-probe words (launch_bandwidth)
+constexpr int64_t kSplitRingMax = 8064;  // split kernel: ring slots (16-bit byte offsets incl. trash)  // measured best for cfg3/cfg4 SP2 (512..4096 swept)
 
 namespace {
 
@@ -104,10 +106,11 @@ struct ellpack_ctx_s {
     double* d_sums = nullptr;                 // final sums (<= 8)
     int32_t* d_bw = nullptr;                  // bandwidth probe [0..5]; [8] agreed width (comm)
     LaunchCfg last_cfg{};
-    int32_t last_fast = 0, last_hB = 0;
+    int32_t last_fast = 0, last_hB = 0, last_split = 0;
+    int ring_kernel = 0;  // ELLPACK_OPT_RING_KERNEL
     bool last_step_general = false;
     struct Host {
-        int32_t bw[6];
+        int32_t bw[8];
         int32_t status_u[2];
         int32_t status[4];
         unsigned long long keys[4];
@@ -267,19 +270,20 @@ int reduce_status(ellpack_ctx c) {
     return ELLPACK_OK;
 }
 
-// Bandwidth probe of a row op, enqueued only (d_bw[0..5], see launch_bandwidth). With a
+// Bandwidth probe of a row op, enqueued only (d_bw[0..kProbe), see launch_bandwidth). With a
 // communicator each rank probes its own rows of every operand and the maxima (half-bandwidths,
-// max nnz of B) are all-reduced, so every rank plans the same launch from the global values even
-// when it holds only its block + halo of B; the reach (d_bw[4..5]) stays per rank.
+// max nnz and max chunk-parity sub-row of B: d_bw[0..4]) are all-reduced, so every rank plans the
+// same launch from the global values even when it holds only its block + halo of B; the reach
+// (d_bw[5..6]) stays per rank.
 int enqueue_probe(ellpack_ctx c, const RowOpParams& p, int64_t n) {
     const bool has_old = p.old_mode != 0;
-    CK(cudaMemsetAsync(c->d_bw, 0, 6 * sizeof(int32_t), c->stream));
+    CK(cudaMemsetAsync(c->d_bw, 0, kProbe * sizeof(int32_t), c->stream));
     const KMat none{nullptr, nullptr, nullptr, 0};
     const int64_t b0 = c->comm ? p.row_begin : 0, b1 = c->comm ? p.row_end : n;
     CK(launch_bandwidth(p.alpha != 0.0 ? p.A : none, p.B, has_old ? p.Old : none, p.row_begin, p.row_end,
                         b0, b1, n, c->d_bw, c->stream));
     c->launches++;
-    if (c->comm) NK(g_nccl.AllReduce(c->d_bw, c->d_bw, 4, ncclInt32, ncclMax, c->comm, c->stream));
+    if (c->comm) NK(g_nccl.AllReduce(c->d_bw, c->d_bw, 5, ncclInt32, ncclMax, c->comm, c->stream));
     return ELLPACK_OK;
 }
 
@@ -298,11 +302,11 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
     const bool has_old = p.old_mode != 0;
     if (!bw) {
         RK(enqueue_probe(c, p, n));
-        CK(cudaMemcpyAsync(c->h->bw, c->d_bw, 6 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->h->bw, c->d_bw, kProbe * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
         RK(host_sync(c));
         bw = c->h->bw;
     }
-    int32_t bwv[6];
+    int32_t bwv[kProbe];
     memcpy(bwv, bw, sizeof bwv);
     const int64_t hB = bwv[1];
     const int64_t hprod = p.alpha != 0.0 ? (int64_t)bwv[0] + hB : 0;
@@ -316,7 +320,47 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
     int64_t ring = (2 * hB + 33 + 31) & ~int64_t(31);
     if (ring > nr) ring = nr < 32 ? 32 : nr;
     int64_t S;
-    if (c->window_opt > 0) {
+    // split-row ring kernel (split.cu): W warps per row, 128-column emission blocks, 16-bit slots:
+    // the default ring path whenever C does not alias an input (no stash) and the ring's byte
+    // offsets fit 16 bits (S + 16 <= 8192 slots)
+    int split_w = 0, split_g = 0;
+    LaunchCfg scfg{};
+    {
+        const int rk = c->ring_kernel;
+        const int64_t sring = (2 * hB + 129 + 127) & ~int64_t(127);
+        const bool stash = p.stash_a || p.stash_old;
+        if (c->window_opt == 0 && rk != 1 && !stash && groups <= 4 && sring <= kSplitRingMax) {
+            const int W = rk == 3 ? 2 : 1;  // automatic: one warp per row (measured faster)
+            const int maxsub = p.alpha != 0.0 ? bwv[4] : 0;
+            const int G = W == 1 ? (groups < 1 ? 1 : groups) : std::max(1, (maxsub + 63) / 64);
+            const int mode = !has_old ? 0 : (p.normsq ? 2 : 1);
+            const int64_t key = (((sring * 8 + G) * 4 + mode) * 4 + W) * 2 + 1;
+            if (key != c->ring_key) {
+                LaunchCfg t;
+                CK(plan_split(p, (int)sring, W, G, c->num_sms, &t));
+                c->ring_ok = t.bps >= kFastMinRows;  // rows in flight per SM
+                int64_t grown = sring;
+                // slack: emission every few halves instead of every half, at the same rows per SM
+                for (int64_t s2 = sring + 128; s2 <= sring + 512 && s2 <= kSplitRingMax; s2 += 128) {
+                    LaunchCfg u;
+                    if (plan_split(p, (int)s2, W, G, c->num_sms, &u) != cudaSuccess) break;
+                    if (u.bps < t.bps) break;
+                    grown = s2;
+                }
+                c->ring_key = key;
+                c->ring_S = (int)grown;
+            }
+            if (c->ring_ok) {
+                split_w = W;
+                split_g = G;
+                CK(plan_split(p, c->ring_S, W, G, c->num_sms, &scfg));
+            }
+        }
+    }
+    if (split_w) {
+        p.fast = 1;
+        S = scfg.S;
+    } else if (c->window_opt > 0) {
         // forced general path (tests): multi-pass windows of window_opt doubles
         S = c->window_opt;
         p.fast = 0;
@@ -325,7 +369,7 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
         // emission run in 4-chunk blocks every few steps instead of one chunk per step.
         p.fast = 1;
         const int mode = !has_old ? 0 : (p.normsq ? 2 : 1);
-        const int64_t key = ((ring * 8 + groups) * 4 + mode) * 64 + c->warps_opt;
+        const int64_t key = (((ring * 8 + groups) * 4 + mode) * 64 + c->warps_opt) * 2;
         if (key != c->ring_key) {
             LaunchCfg t;
             CK(plan_row_op(p, (int)ring, groups, c->warps_opt, c->num_sms, &t));
@@ -354,10 +398,14 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
         p.fast = 0;
     }
     (void)h;
-    if (S > nr) S = nr;
-    if (S < 32) S = 32;
     LaunchCfg cfg;
-    CK(plan_row_op(p, (int)S, groups, c->warps_opt, c->num_sms, &cfg));
+    if (split_w) {
+        cfg = scfg;
+    } else {
+        if (S > nr) S = nr;
+        if (S < 32) S = 32;
+        CK(plan_row_op(p, (int)S, groups, c->warps_opt, c->num_sms, &cfg));
+    }
     p.S = cfg.S;
     // symmetric SP2 step (f4 ii): a general-path launch computes only the upper triangle, into
     // C_upper; the ring path computes whole rows
@@ -378,7 +426,19 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
             }
         }
     }
-    if (p.fast) {
+    if (split_w) {
+        // per-owner bank-balanced copy of B, 16-bit ring byte offsets for this S
+        const int64_t k0 = std::max<int64_t>(0, (int64_t)INT_MAX - bwv[5]);
+        const int64_t k1 = std::min<int64_t>(n, (int64_t)bwv[6]);
+        RK(grow(c, c->bt, (size_t)640 * split_g * split_w * n));
+        RK(grow(c, c->bt_nbin, sizeof(int32_t) * (size_t)split_w * n));
+        CK(launch_balance_split(p.B, k0, k1, split_w, split_g, p.S, (unsigned char*)c->bt.p,
+                                (int32_t*)c->bt_nbin.p, c->num_sms, c->stream));
+        c->launches++;
+        p.bt = (const unsigned char*)c->bt.p;
+        p.bt_nbin = (const int32_t*)c->bt_nbin.p;
+        p.bt_w = 64 * split_g;
+    } else if (p.fast) {
         // bank-balanced copy of B with ring slots precomputed for this S (all N rows: B is the
         // full operand on every rank)
         const int wt = 64 * (groups < 1 ? 1 : groups);
@@ -386,8 +446,8 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
         RK(grow(c, c->bt_nbin, sizeof(int32_t) * (size_t)n));
         // only the B rows this launch's A rows reference (a rank's block plus its halo; rows a halo
         // exchange did not deliver are never read)
-        const int64_t k0 = std::max<int64_t>(0, (int64_t)INT_MAX - bwv[4]);
-        const int64_t k1 = std::min<int64_t>(n, (int64_t)bwv[5]);
+        const int64_t k0 = std::max<int64_t>(0, (int64_t)INT_MAX - bwv[5]);
+        const int64_t k1 = std::min<int64_t>(n, (int64_t)bwv[6]);
         CK(launch_balance(p.B, k0, k1, wt, p.S, (unsigned char*)c->bt.p, (int32_t*)c->bt_nbin.p, c->num_sms,
                           c->stream));
         c->launches++;
@@ -405,6 +465,7 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
     }
     c->last_cfg = cfg;
     c->last_fast = p.fast;
+    c->last_split = split_w;
     c->last_hB = (int32_t)hB;
     const int64_t total_warps = (int64_t)cfg.grid * cfg.warps_per_cta;
     const bool may_multi = n > cfg.S;
@@ -427,11 +488,13 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
         // rows per ticket: 4 (fewer atomics, neighbouring rows share B records in L2) unless the
         // launch has fewer than 64 rows per resident warp, where one-row tickets keep the tail short
         const int64_t rows = p.row_end - p.row_begin;
-        p.row_chunk = rows >= 64 * total_warps ? 4 : 1;
+        const int64_t in_flight = split_w ? (int64_t)cfg.grid : total_warps;  // rows being worked on
+        p.row_chunk = rows >= 64 * in_flight ? 4 : 1;
     }
     CK(cudaMemsetAsync(p.row_ticket, 0, 8, c->stream));
     if (c->profile) CK(cudaEventRecord(c->ev[4], c->stream));
-    CK(launch_row_op(p, cfg, c->stream));
+    if (split_w) CK(launch_split(p, cfg, c->stream));
+    else CK(launch_row_op(p, cfg, c->stream));
     if (c->profile) {
         CK(cudaEventRecord(c->ev[5], c->stream));
         c->prof_pending = true;
@@ -482,7 +545,7 @@ int fetch(ellpack_ctx c, int nsums, bool probe = false) {
     if (nsums > 0)
         CK(cudaMemcpyAsync(c->h->sums, c->d_sums, nsums * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     if (probe) {
-        CK(cudaMemcpyAsync(c->h->bw, c->d_bw, 6 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->h->bw, c->d_bw, kProbe * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
         if (c->comm)
             CK(cudaMemcpyAsync(c->h_reach, c->halo.p, 2 * sizeof(int32_t) * c->nranks, cudaMemcpyDeviceToHost,
                                c->stream));
@@ -670,6 +733,11 @@ int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
         case ELLPACK_OPT_WARPS: c->warps_opt = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_SP2_WIDTH0: c->sp2_width0 = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_SP2_MEM_CAP: c->sp2_mem_cap = v; return ELLPACK_OK;
+        case ELLPACK_OPT_RING_KERNEL:
+            if (v > 3) return ELLPACK_ERR_ARG;
+            c->ring_kernel = (int)v;
+            c->ring_key = -1;
+            return ELLPACK_OK;
         case ELLPACK_OPT_ABLATE:
 #if defined(ELL_ABLATE) && ELL_ABLATE
             c->ablate = (int)v;
@@ -706,6 +774,7 @@ int ellpack_ctx_last_launch(ellpack_ctx c, int32_t out[8]) {
     out[5] = (int32_t)g.smem;
     out[6] = g.bps;
     out[7] = c->last_hB;
+    out[0] = c->last_split ? 2 : c->last_fast;  // 2: split-row ring kernel (out[3] = W warps per row)
     return ELLPACK_OK;
 }
 
@@ -1245,14 +1314,14 @@ int enqueue_next_probe(ellpack_ctx c, const ellpack_desc* x) {
     RK(enqueue_probe(c, q, x->n));
     if (c->comm) {
         RK(grow(c, c->halo, sizeof(long long) * 2 * (size_t)c->nranks));
-        NK(g_nccl.AllGather(c->d_bw + 4, (int32_t*)c->halo.p, 2, ncclInt32, c->comm, c->stream));
+        NK(g_nccl.AllGather(c->d_bw + 5, (int32_t*)c->halo.p, 2, ncclInt32, c->comm, c->stream));
     }
     return ELLPACK_OK;
 }
 
 // host copies of the prefetched probe (bw) and every rank's reach, as halo_exec's need ranges
 void take_probe(ellpack_ctx c, int32_t* bw, std::vector<int64_t>& need) {
-    memcpy(bw, c->h->bw, 6 * sizeof(int32_t));
+    memcpy(bw, c->h->bw, kProbe * sizeof(int32_t));
     for (int q = 0; c->comm && q < c->nranks; ++q) {
         need[2 * q] = (int64_t)INT_MAX - c->h_reach[2 * q];
         need[2 * q + 1] = (int64_t)c->h_reach[2 * q + 1] - 1;
@@ -1368,7 +1437,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
         t2 = c->h->sums[0];
     }
     // the probe of X0 (its halo rows are in place), for the first step's launch plan
-    int32_t bwX[6];
+    int32_t bwX[kProbe];
     std::vector<int64_t> needX(2 * (size_t)c->nranks);
     if ((rc = enqueue_next_probe(c, &X.d))) { cleanup(); return rc; }
     if ((rc = fetch(c, 0, true))) { cleanup(); return rc; }

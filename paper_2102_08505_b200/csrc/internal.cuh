@@ -90,10 +90,17 @@ size_t row_op_warp_smem(int S, bool has_old, bool fast);
 cudaError_t launch_balance(KMat b, int64_t k0, int64_t k1, int wt, int S, unsigned char* bt, int32_t* bt_nbin,
                            int num_sms, cudaStream_t s);
 // out[0..2] = max half-bandwidth of a (rows r0..r1), b (rows b0..b1), c (rows r0..r1); out[3] = max nnz
-// of b (rows b0..b1); A's rows r0..r1 reference B rows [INT_MAX - out[4], out[5] - 1] (out[0..5]
-// zeroed by the caller)
+// of b (rows b0..b1); out[4] = max chunk-parity half of those B rows; A's rows r0..r1 reference B rows
+// [INT_MAX - out[5], out[6] - 1] (out[0..6] zeroed by the caller)
 cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int64_t r0, int64_t r1, int64_t b0, int64_t b1, int64_t n,
                              int32_t* out, cudaStream_t s);
+
+// split.cu: the split-row ring kernel (W warps per row, 16-bit balanced sub-records)
+cudaError_t plan_split(const RowOpParams& p, int S, int W, int G, int num_sms, LaunchCfg* cfg);
+cudaError_t launch_split(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s);
+size_t split_row_smem(int S, int W, bool has_old);
+cudaError_t launch_balance_split(KMat b, int64_t k0, int64_t k1, int W, int G, int S, unsigned char* bt,
+                                 int32_t* bt_nbin, int num_sms, cudaStream_t s);
 
 // symmetric SP2 step (f4 ii): is h bitwise symmetric (ok[0] stays 0); reach of U's rows
 cudaError_t launch_sym_check(KMat h, int64_t n, int32_t* bad, cudaStream_t s);

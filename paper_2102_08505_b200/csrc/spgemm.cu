@@ -31,6 +31,7 @@
 // the value (beta*old, p.old_mode == 1) or only the union (p.old_mode == 2) is a runtime,
 // warp-uniform choice.
 #include "internal.cuh"
+#include "devutil.cuh"
 #include <climits>
 #include <type_traits>
 
@@ -62,63 +63,6 @@ constexpr int kStageF = ELL_STAGE_F;
 #define ELL_G3_HB 2  // fast path, 3 groups per step: steps per register half
 #endif
 
-__device__ __forceinline__ int warp_min(int v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(FULL, v, o));
-    return v;
-}
-__device__ __forceinline__ int warp_max(int v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
-    return v;
-}
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, o));
-    return v;
-}
-
-// 32-bit shared-window accesses (no generic->shared conversion per access)
-__device__ __forceinline__ double lds64(uint32_t a) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ void sts64(uint32_t a, double v) {
-    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
-}
-__device__ __forceinline__ void lds128(uint32_t a, double& x, double& y) {
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a) : "memory");
-}
-__device__ __forceinline__ void sts128(uint32_t a, double x, double y) {
-    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x), "d"(y) : "memory");
-}
-__device__ __forceinline__ uint32_t lds8(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
-    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t lds16u(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ void sts16u(uint32_t a, uint32_t v) {
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-
-// Branch-free predicated store of one output entry (value + column).
-__device__ __forceinline__ void st_entry(bool pred, double* pv, int32_t* pc, double x, int32_t c) {
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t"
-        "@q st.global.cs.f64 [%1], %2;\n\t@q st.global.cs.b32 [%3], %4;\n\t}" ::"r"((int)pred),
-        "l"(pv), "d"(x), "l"(pc), "r"(c)
-        : "memory");
-}
-
 // Per-warp shared layout: acc[S + 2] f64 | stage: boff[kStage] i64, aa[kStage] f64,
 // anb[kStage] i32, ast[kStage] i32, ak[kStage] i32 | flags[S] u8 (MODE != 0 only)
 struct WarpSmem {
@@ -135,14 +79,6 @@ __device__ __forceinline__ long long stg_boff(const WarpSmem& w, int t) {
     return v;
 }
 __device__ __forceinline__ double stg_aa(const WarpSmem& w, int t) { return lds64(w.stg + 8u * (kStage + t)); }
-__device__ __forceinline__ int lds32i(uint32_t a) {
-    int v;
-    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ void sts32i(uint32_t a, int v) {
-    asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
 __device__ __forceinline__ uint32_t stg_anb_a(const WarpSmem& w, int t) { return w.stg + 16u * kStage + 4u * t; }
 __device__ __forceinline__ uint32_t stg_ast_a(const WarpSmem& w, int t) { return w.stg + 20u * kStage + 4u * t; }
 __device__ __forceinline__ uint32_t stg_ak_a(const WarpSmem& w, int t) { return w.stg + 24u * kStage + 4u * t; }
@@ -309,59 +245,6 @@ __device__ __forceinline__ void stage_fast_get(const WarpSmem& w, int t, double&
     a = __longlong_as_double((long long)x);
     k = (int)(uint32_t)y;
     nb = (int)(y >> 32);
-}
-
-// Gathers of the balanced B copy: read-only, no L1 allocation (each is used once per SM), L2
-// evict_last (every record is re-read by the ~2 hB rows around it while the output stream,
-// written with .cs, passes through L2).
-__device__ __forceinline__ uint64_t l2_evict_last_policy() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-// predicated forms with an immediate byte offset: the address is formed once per B row
-template <int OFF>
-__device__ __forceinline__ void ldg_keep_i2_if(bool pr, const void* p, uint64_t pol, int2& v) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
-                 "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%3+%5], %4;\n\t}"
-                 : "+r"(v.x), "+r"(v.y) : "r"((int)pr), "l"(p), "l"(pol), "n"(OFF));
-}
-template <int OFF>
-__device__ __forceinline__ void ldg_keep_d2_if(bool pr, const void* p, uint64_t pol, double2& v) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
-                 "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%3+%5], %4;\n\t}"
-                 : "+d"(v.x), "+d"(v.y) : "r"((int)pr), "l"(p), "l"(pol), "n"(OFF));
-}
-__device__ __forceinline__ int2 ldg_keep_i2(const void* p, uint64_t pol) {
-    int2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
-                 : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ double2 ldg_keep_d2(const void* p, uint64_t pol) {
-    double2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-                 : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
-    return v;
-}
-
-// read-and-clear of an accumulator slot: shared 64-bit atomic exchange with +0.0
-__device__ __forceinline__ double lds64_clear(uint32_t a) {
-    unsigned long long v;
-    asm volatile("atom.shared.exch.b64 %0, [%1], 0;" : "=l"(v) : "r"(a) : "memory");
-    return __longlong_as_double((long long)v);
-}
-
-// predicated shared accesses (padding lanes issue no request and cost no wavefront)
-__device__ __forceinline__ double lds64_if(bool pr, uint32_t a) {
-    double v;  // undefined when !pr (the predicated store discards the result)
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t@q ld.shared.f64 %0, [%2];\n\t}"
-                 : "=d"(v) : "r"((int)pr), "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ void sts64_if(bool pr, uint32_t a, double v) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.shared.f64 [%1], %2;\n\t}"
-                 ::"r"((int)pr), "r"(a), "d"(v) : "memory");
 }
 
 // ------------------------------------------------------------------------- general path
@@ -669,11 +552,6 @@ __device__ __forceinline__ void ring_merge_old(const RowOpParams& p, const WarpS
 // (NCH independent ballots) and write; the slots (and flags) are cleared. One slot per lane
 // per chunk, so each chunk's kept entries are ONE contiguous run written by one store
 // instruction per array (fully coalesced). A1: alpha == 1 (no scaling of product-only slots).
-__device__ __forceinline__ uint64_t opaque_u64(uint64_t x) {
-    asm volatile("mov.b64 %0, %0;" : "+l"(x));  // keeps the row base a plain 64-bit register
-    return x;
-}
-
 template <int MODE, int NCH, bool A1>
 __device__ __forceinline__ void ring_emit_block(const RowOpParams& p, const WarpSmem& w, int lane, int64_t i,
                                                 int F, int baseF, const int32_t* o_col, const double* o_val,
@@ -1236,8 +1114,9 @@ __global__ void __launch_bounds__(128, ELL_GEN_MINB) row_general_kernel(const Ro
 }
 
 // Half-bandwidth probe: out[m] = max over rows of max(i - col[i][0], col[i][nnz-1] - i) (a and c
-// over rows [r0, r1), b over rows [b0, b1)); out[3] = max nnz of b over [b0, b1); the B rows the A
-// rows [r0, r1) reference are [INT_MAX - out[4], out[5] - 1] (zero-initialised maxima of
+// over rows [r0, r1), b over rows [b0, b1)); out[3] = max nnz of b over [b0, b1); out[4] = max over
+// those B rows of the larger chunk-parity half (the split kernel's sub-rows, W = 2); the B rows the
+// A rows [r0, r1) reference are [INT_MAX - out[5], out[6] - 1] (zero-initialised maxima of
 // INT_MAX - first column and last column + 1).
 __global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int64_t r0, int64_t r1, int64_t b0, int64_t b1,
                                  int64_t n, int32_t* out) {
@@ -1262,9 +1141,17 @@ __global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int64_t r0, int64_t r1,
         }
     }
     int nzb = (i >= b0 && i < b1) ? b.nnz[i] : 0;
+    // the larger chunk-parity half of the B row (split kernel, W = 2: columns j with (j >> 5) & 1)
+    int sub = nzb;
+    if (nzb > 64 && nzb <= 256) {
+        const int32_t* bc = b.col + (size_t)i * b.w;
+        int odd = 0;
+        for (int q = 0; q < nzb; ++q) odd += (bc[q] >> 5) & 1;
+        sub = max(odd, nzb - odd);
+    }
 #pragma unroll
-    for (int m = 0; m < 6; ++m) {
-        int v = m < 3 ? bw[m] : (m == 3 ? nzb : reach[m - 4]);
+    for (int m = 0; m < 7; ++m) {
+        int v = m < 3 ? bw[m] : (m == 3 ? nzb : (m == 4 ? sub : reach[m - 5]));
 #pragma unroll
         for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
         if ((threadIdx.x & 31) == 0 && v > 0) atomicMax(out + m, v);

@@ -1,0 +1,625 @@
+// split.cu — the split-row ring kernel of libellpack (sm_100a, FP64 CUDA cores): W warps per
+// output row (BJ north_star (1): "a warp or small CTA owns each output row").
+//
+// Same method as the ring path of spgemm.cu (readings R3, R5, R12):
+// row i's products lie in columns [k - hB, k + hB] for the k of A_i in ascending order; column j
+// accumulates in ring slot j mod S as the fma chain s <- fma(a_ik, b_kj, s) in ascending k; every
+// column below the sweep's floor is final and is combined with Old, dropped (|c| > tau kept),
+// compacted and written ("progressive emission"). What differs is who does the work:
+//
+//  * Column ownership. The row's CTA has W warps; 32-column chunk c = j >> 5 belongs to warp
+//    c mod W. Every warp walks ALL k of A_i in ascending order but applies only the entries of
+//    B row k in its own chunks, so each output entry is still one fma chain in ascending k, in one
+//    warp (bitwise the oracle's), and no two warps ever touch the same ring slot (S is a multiple
+//    of 32 W). The per-step work of a row is split W ways while the ring (the row's shared-memory
+//    footprint) stays one ring: W times the warps per SM at the same shared memory, which is what
+//    the accumulator needs (tools/microbench.cu: random FP64 smem read-modify-write 311 Gupd/s at
+//    6 warps/SM vs 570 at 12 and 690 at 24, profiles/r02_microbench.json).
+//  * Emission in 128-column blocks (S a multiple of 128, blocks 128-aligned: a block never wraps).
+//    Warp w emits its NCH = 4 / W chunks of the block; the kept counts of the block's 4 chunks are
+//    exchanged through shared memory (one named barrier per block), so every warp knows where its
+//    runs go in the output row and the row stays one contiguous ascending run.
+//  * B is read from a per-owner bank-balanced copy with 16-bit ring slots: B row k, owner w is a
+//    record of 64 G entries (uint16 byte offset 8 (j mod S) | f64 value), 10 bytes per product
+//    gathered instead of 12.
+//
+// Template parameters: W (warps per row: 1, 2), G (64-entry groups per sub-record step), HB
+// (steps per register half), MODE (0: no Old; 1: Old operand; 2: Old + ||S - Old||^2).
+#include "internal.cuh"
+#include "devutil.cuh"
+
+#include <climits>
+#include <type_traits>
+
+namespace ell {
+
+constexpr int kSplitStage = 64;  // A-row steps staged per warp (16 B each)
+constexpr int kSplitTrash = 16;  // trash slots S .. S + 15 (one per bank pair) for padding lanes
+
+__host__ __device__ inline size_t split_smem_bytes(int S, int W, bool has_old) {
+    // acc[S + 16] f64 | stage[W][kSplitStage] 16 B | xcnt[2][4] i32 | rowq[2] i64 | nrm[W] f64 | flags[S] u8
+    return (size_t)(S + kSplitTrash) * 8 + (size_t)W * kSplitStage * 16 + 32 + 16 + (size_t)W * 8 +
+           (has_old ? (size_t)S : 0);
+}
+
+// ------------------------------------------------------------------ per-owner balanced B
+
+// Record of B row k, owner w (chunk parity for W = 2): bt + (k W + w) * 640 G bytes:
+//   uint16 slot8[64 G]: byte offset 8 (j mod S) of the entry's ring slot (padding: 8 (S + r), a
+//   trash slot whose bank pair r no real entry of the same half-instruction uses), then
+//   f64 val[64 G] at byte 128 G. bt_nbin[k W + w] = NB = 4 ceil(n_w / 64) used bins.
+// Within a sub-record the entries are ranked by residue j mod 16 (bank pair) and dealt
+// round-robin over the NB half-instruction bins (as balance_kernel in spgemm.cu): bin b is half
+// (b >> 1) & 1 of group b >> 2, parity b & 1; position m in the bin -> slot
+// 64 (b >> 2) + 2 (16 ((b >> 1) & 1) + m) + (b & 1). One lane's two slots of a group are adjacent:
+// one 4-byte index load and one 16-byte value load per lane per group.
+template <int W>
+__global__ void __launch_bounds__(128) balance_split_kernel(KMat b, int64_t k0, int64_t k1, int G, int S,
+                                                            unsigned char* __restrict__ bt,
+                                                            int32_t* __restrict__ bt_nbin) {
+    static_assert(W == 1 || W == 2, "W");
+    __shared__ int hist_s[4][32];                             // per warp: entries per (owner, residue)
+    __shared__ unsigned bmask_s[4][W][16];                    // per warp, owner, bin: bank pairs used
+    __shared__ __align__(16) unsigned char rec_s[4][W][2560];  // per warp, owner: u16[256] | f64[256]
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    int* hist = hist_s[wi];
+    const size_t rs = (size_t)640 * G;
+    const double invS = 1.0 / (double)S;
+    for (int64_t k = k0 + (int64_t)blockIdx.x * 4 + wi; k < k1; k += (int64_t)gridDim.x * 4) {
+        const int nb = b.nnz[k];  // <= 256 on the ring path
+        const int32_t* __restrict__ bc = b.col + (size_t)k * b.w;
+        const double* __restrict__ bv = b.val + (size_t)k * b.w;
+        hist[lane] = 0;
+        if (lane < W * 16) bmask_s[wi][lane >> 4][lane & 15] = 0u;
+        __syncwarp();
+        int jr[8], rk[8];
+        double vr[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int q = 32 * c + lane;
+            jr[c] = q < nb ? __ldg(bc + q) : -1;
+            vr[c] = q < nb ? __ldg(bv + q) : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            rk[c] = 0;
+            if (32 * c < nb) {  // warp-uniform
+                const int key = jr[c] >= 0 ? ((((jr[c] >> 5) & (W - 1)) << 4) | (jr[c] & 15)) : 64 + lane;
+                const unsigned m = __match_any_sync(FULL, key);
+                const int leader = __ffs(m) - 1;
+                int base = 0;
+                if (lane == leader && jr[c] >= 0) base = atomicAdd(&hist[key], __popc(m));
+                base = __shfl_sync(FULL, base, leader);
+                rk[c] = base + __popc(m & lt);
+            }
+        }
+        __syncwarp();
+        // exclusive prefix over the residues of each owner (16-lane segments); owner totals
+        const int h = hist[lane];
+        int pre = h;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, pre, o);
+            if ((lane & 15) >= o) pre += y;
+        }
+        const int n0 = __shfl_sync(FULL, pre, 15);
+        const int n1 = W > 1 ? __shfl_sync(FULL, pre, 31) : 0;
+        pre -= h;
+        if (lane < W) bt_nbin[k * W + lane] = 4 * (((lane ? n1 : n0) + 63) >> 6);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            if (32 * c < nb) {
+                const int j = jr[c];
+                const int key = j >= 0 ? ((((j >> 5) & (W - 1)) << 4) | (j & 15)) : 0;
+                const int e = __shfl_sync(FULL, pre, key) + rk[c];
+                if (j >= 0) {
+                    const int own = key >> 4;
+                    const int NB = 4 * (((own ? n1 : n0) + 63) >> 6);
+                    const int pos = e / NB;
+                    const int bin = e - pos * NB;
+                    const int sl = 64 * (bin >> 2) + 2 * (16 * ((bin >> 1) & 1) + pos) + (bin & 1);
+                    int qs = __double2int_rz((double)j * invS);
+                    int js = j - qs * S;
+                    js += js < 0 ? S : 0;
+                    js -= js >= S ? S : 0;
+                    reinterpret_cast<uint16_t*>(rec_s[wi][own])[sl] = (uint16_t)(8 * js);
+                    reinterpret_cast<double*>(rec_s[wi][own] + 512)[sl] = vr[c];
+                    atomicOr(&bmask_s[wi][own][bin], 1u << (js & 15));
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int own = 0; own < W; ++own) {
+            const int n = own ? n1 : n0;
+            const int NB = 4 * ((n + 63) >> 6);
+            uint16_t* so = reinterpret_cast<uint16_t*>(rec_s[wi][own]);
+            double* sv = reinterpret_cast<double*>(rec_s[wi][own] + 512);
+            for (int t = lane; t < NB * 16; t += 32) {
+                const int bb = t >> 4, m = t & 15;
+                const int fill = (n - bb + NB - 1) / NB;
+                if (m >= fill) {
+                    const int sl = 64 * (bb >> 2) + 2 * (16 * ((bb >> 1) & 1) + m) + (bb & 1);
+                    unsigned f = ~bmask_s[wi][own][bb] & 0xffffu;
+                    for (int q = m - fill; q > 0; --q) f &= f - 1u;
+                    so[sl] = (uint16_t)(8 * (S + ((__ffs(f) - 1 - S) & 15)));
+                    sv[sl] = 0.0;
+                }
+            }
+            __syncwarp();
+            // used groups (NB / 4) leave in coalesced 16-byte stores
+            unsigned char* dst = bt + ((size_t)k * W + own) * rs;
+            const int groups = NB >> 2;
+            for (int t = lane; t < groups * 8; t += 32)  // 128 B of indices per group
+                reinterpret_cast<int4*>(dst)[t] = reinterpret_cast<const int4*>(so)[t];
+            for (int t = lane; t < groups * 32; t += 32)  // 512 B of values per group
+                reinterpret_cast<int4*>(dst + 128 * G)[t] = reinterpret_cast<const int4*>(sv)[t];
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_balance_split(KMat b, int64_t k0, int64_t k1, int W, int G, int S, unsigned char* bt,
+                                 int32_t* bt_nbin, int num_sms, cudaStream_t s) {
+    if (k1 <= k0) return cudaSuccess;
+    const int64_t blocks_needed = (k1 - k0 + 3) / 4;
+    const int64_t cap = (int64_t)num_sms * 12;
+    const unsigned grid = (unsigned)(blocks_needed < cap ? blocks_needed : cap);
+    if (W == 2) balance_split_kernel<2><<<grid, 128, 0, s>>>(b, k0, k1, G, S, bt, bt_nbin);
+    else balance_split_kernel<1><<<grid, 128, 0, s>>>(b, k0, k1, G, S, bt, bt_nbin);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------ the row kernel
+
+template <int OFF>
+__device__ __forceinline__ void ldg_keep_u32_if(bool pr, const void* p, uint64_t pol, uint32_t& v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
+                 "@q ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%2+%4], %3;\n\t}"
+                 : "+r"(v) : "r"((int)pr), "l"(p), "l"(pol), "n"(OFF));
+}
+
+__device__ __forceinline__ void bar_cta(int nthreads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+template <int W>
+struct SplitSmem {
+    uint32_t acc, stg, xcnt, rowq, nrmx, flg;
+};
+
+// Kernel state of the row in flight (every warp holds the same values except the per-warp
+// diagonal / norm partials).
+struct SplitRow {
+    int64_t i;
+    int F;       // first unemitted column (multiple of 128)
+    int sF;      // ring slot of F (F mod S)
+    int kept;    // entries kept so far (all warps agree)
+    int old_cur; // Old-row cursor (entries with column < F merged or skipped)
+    int xbuf;    // exchange buffer parity: alternates every block, across rows too (consecutive
+                 // blocks of consecutive rows have no other barrier between them)
+    double ds, dc, nrm;
+};
+
+// Merge this warp's Old entries with columns < Fe into the ring (see ring_merge_old, spgemm.cu).
+template <int W, int MODE>
+__device__ __forceinline__ void split_merge_old(const RowOpParams& p, const SplitSmem<W>& sm, int lane, int wid,
+                                                int Fe, int F, int sF, const int32_t* o_col, const double* o_val,
+                                                int nOld, int& old_cur, double& nrm) {
+    while (old_cur < nOld) {
+        const int q = old_cur + lane;
+        const bool v = q < nOld;
+        const int jo = v ? o_col[q] : INT_MAX;
+        const bool inr = jo < Fe;
+        if (inr && ((jo >> 5) & (W - 1)) == wid) {
+            const double x = o_val[q];
+            const uint32_t off = (uint32_t)(sF + (jo - F));  // jo in [F, Fe): the block never wraps
+            const uint32_t sa = sm.acc + 8u * off;
+            const double sv = lds64(sa);
+            if (MODE == 2) {
+                const double df = __dsub_rn(sv, x);
+                nrm = __fma_rn(df, df, nrm);
+            }
+            const double tt = (p.old_mode == 1) ? __dmul_rn(p.beta, x) : 0.0;
+            sts64(sa, __fma_rn(p.alpha, sv, tt));
+            sts8(sm.flg + off, 1u);
+        }
+        const int n = __popc(__ballot_sync(FULL, inr));
+        old_cur += n;
+        if (n < 32) break;
+    }
+    __syncwarp();
+}
+
+// Emit blocks [R.F, Fto) (multiples of 128): per block, this warp's NCH chunks are read and
+// cleared, combined, dropped and ballot-compacted; the block's four chunk counts are exchanged
+// (W > 1) and each warp writes its runs at their place in the row.
+template <int W, int MODE, bool A1>
+__device__ __forceinline__ void split_emit(const RowOpParams& p, const SplitSmem<W>& sm, int lane, int wid,
+                                           SplitRow& R, int Fto, const int32_t* o_col, const double* o_val,
+                                           int nOld, double* __restrict__ crow_v, int32_t* __restrict__ crow_c) {
+    constexpr int NCH = 4 / W;
+    const int S = p.S;
+    const double tau = p.tau;
+    const unsigned lt = (1u << lane) - 1u;
+    const int cw = p.C.w;
+    const uint64_t bv = opaque_u64((uint64_t)crow_v), bc = opaque_u64((uint64_t)crow_c);
+    while (R.F < Fto) {
+        const int F = R.F, sF = R.sF;
+        // the pre-combine diagonal s_ii (tr X^2 pre-drop, R5): read before the Old merge
+        if ((int64_t)F <= R.i && R.i < (int64_t)F + 128 && (((int)R.i >> 5) & (W - 1)) == wid &&
+            lane == ((int)R.i & 31))
+            R.ds = lds64(sm.acc + 8u * (uint32_t)(sF + (int)(R.i - F)));
+        if (MODE != 0)
+            split_merge_old<W, MODE>(p, sm, lane, wid, F + 128, F, sF, o_col, o_val, nOld, R.old_cur, R.nrm);
+        double x[NCH];
+        unsigned m[NCH];
+#pragma unroll
+        for (int t = 0; t < NCH; ++t) {
+            const int q = wid + W * t;
+            const uint32_t off = (uint32_t)(sF + 32 * q + lane);
+            const double v = lds64_clear(sm.acc + 8u * off);
+            bool flagged = false;
+            if (MODE != 0) {
+                flagged = lds8(sm.flg + off) != 0;
+                sts8(sm.flg + off, 0u);
+            }
+            x[t] = v;
+            if (!flagged) {
+                if (!A1) x[t] = __dmul_rn(p.alpha, v);
+                if (MODE == 2) R.nrm = __fma_rn(v, v, R.nrm);
+            }
+            m[t] = __ballot_sync(FULL, fabs(x[t]) > tau);
+        }
+        int cnt[4];
+        if (W == 1) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) cnt[t] = __popc(m[t]);
+        } else {
+            const uint32_t xb = sm.xcnt + 16u * (uint32_t)R.xbuf;
+            if (lane == 0) {
+#pragma unroll
+                for (int t = 0; t < NCH; ++t) sts32i(xb + 4u * (uint32_t)(wid + W * t), __popc(m[t]));
+            }
+            bar_cta(32 * W);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cnt[q] = lds32i(xb + 4u * q);
+            R.xbuf ^= 1;
+        }
+        const bool room = R.kept + 128 <= cw;
+#pragma unroll
+        for (int t = 0; t < NCH; ++t) {
+            const int q = wid + W * t;
+            int before = R.kept;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) before += u < q ? cnt[u] : 0;
+            const bool keep = (m[t] >> lane) & 1u;
+            const uint32_t pos = (uint32_t)before + (uint32_t)__popc(m[t] & lt);
+            const int col = F + 32 * q + lane;
+            st_entry(keep && (room || pos < (uint32_t)cw), reinterpret_cast<double*>(bv + 8ull * pos),
+                     reinterpret_cast<int32_t*>(bc + 4ull * pos), x[t], col);
+            if (MODE != 0 && (int64_t)col == R.i) R.dc = keep ? x[t] : 0.0;
+            if (MODE == 0 && p.diag_c && (int64_t)col == R.i) R.dc = keep ? x[t] : 0.0;
+        }
+        R.kept += cnt[0] + cnt[1] + cnt[2] + cnt[3];
+        R.F = F + 128;
+        R.sF = sF + 128 == S ? 0 : sF + 128;
+    }
+}
+
+template <int W, int MODE>
+__device__ __forceinline__ void split_emit_to(const RowOpParams& p, const SplitSmem<W>& sm, int lane, int wid,
+                                              SplitRow& R, int Fto, const int32_t* o_col, const double* o_val,
+                                              int nOld, double* __restrict__ crow_v, int32_t* __restrict__ crow_c) {
+    if (p.alpha == 1.0) split_emit<W, MODE, true>(p, sm, lane, wid, R, Fto, o_col, o_val, nOld, crow_v, crow_c);
+    else split_emit<W, MODE, false>(p, sm, lane, wid, R, Fto, o_col, o_val, nOld, crow_v, crow_c);
+}
+
+// One output row, warp `wid` of W: the ring sweep of row_ring (spgemm.cu) over this warp's
+// sub-records, register bursts of HB steps in a two-half register ring (a half touches its own
+// burst, emits if the sweep would wrap onto unemitted columns, issues the next half's burst,
+// then runs its steps branch-free).
+template <int W, int G, int HB, int MODE>
+__device__ __forceinline__ void row_split(const RowOpParams& p, const SplitSmem<W>& sm, int lane, int wid,
+                                          SplitRow& R, const int32_t* a_col, const double* a_val, int nA,
+                                          const int32_t* o_col, const double* o_val, int nOld,
+                                          double* __restrict__ crow_v, int32_t* __restrict__ crow_c) {
+    constexpr int kPiece = kSplitStage - 2 * HB + 1;  // real steps per piece
+    constexpr int RS = 640 * G;                        // sub-record bytes
+    const int S = p.S;
+    const int hB = p.hB;
+    const int ncols = (int)p.ncols;
+    int lo_col = INT_MAX, hi_col = -1;
+    if (nA > 0) {
+        lo_col = max(0, a_col[0] - hB);
+        hi_col = min(ncols - 1, a_col[nA - 1] + hB);
+    }
+    if (MODE != 0 && nOld > 0) {
+        lo_col = min(lo_col, o_col[0]);
+        hi_col = max(hi_col, o_col[nOld - 1]);
+    }
+    if (hi_col < lo_col) return;
+    R.F = lo_col & ~127;
+    R.sF = R.F % S;
+    const int Fend = (hi_col + 128) & ~127;
+    const uint32_t acc = sm.acc;
+    const uint32_t stg = sm.stg;
+    const unsigned char* __restrict__ btl = p.bt + (size_t)wid * RS;  // this warp's sub-record of row 0
+    const uint64_t pol = l2_evict_last_policy();
+
+    uint32_t ro[2][HB][G];
+    double2 rv[2][HB][G];
+    // step metadata (a_ik, k, NB of this warp's sub-record), re-read from the stage where used
+    auto get = [&](int t, double& a, int& k, int& nb) {
+        unsigned long long x, y;
+        asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(stg + 16u * t) : "memory");
+        a = __longlong_as_double((long long)x);
+        k = (int)(uint32_t)y;
+        nb = (int)(y >> 32);
+    };
+    auto burst = [&](auto Xc, int h) {
+        constexpr int X = decltype(Xc)::value;
+#pragma unroll
+        for (int e = 0; e < HB; ++e) {
+            double a_u;
+            int k_u, nb;
+            get(h * HB + e, a_u, k_u, nb);
+            const unsigned char* __restrict__ rp = btl + (size_t)(uint32_t)k_u * (W * RS);
+            const unsigned char* __restrict__ sp = rp + 4 * lane;
+            const unsigned char* __restrict__ vp = rp + 16 * lane;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                if (g == 0) { ldg_keep_u32_if<0>(nb > 0, sp, pol, ro[X][e][0]); ldg_keep_d2_if<128 * G>(nb > 0, vp, pol, rv[X][e][0]); }
+                if (g == 1) { ldg_keep_u32_if<128>(nb > 4, sp, pol, ro[X][e][1]); ldg_keep_d2_if<128 * G + 512>(nb > 4, vp, pol, rv[X][e][1]); }
+                if (g == 2) { ldg_keep_u32_if<256>(nb > 8, sp, pol, ro[X][e][2]); ldg_keep_d2_if<128 * G + 1024>(nb > 8, vp, pol, rv[X][e][2]); }
+                if (g == 3) { ldg_keep_u32_if<384>(nb > 12, sp, pol, ro[X][e][3]); ldg_keep_d2_if<128 * G + 1536>(nb > 12, vp, pol, rv[X][e][3]); }
+            }
+        }
+    };
+    auto step = [&](int X, int e, double a, int nb) {
+        double old[G][2];
+        bool gl[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            gl[g] = nb > 4 * g;
+            old[g][0] = lds64_if(gl[g], acc + (ro[X][e][g] & 0xffffu));
+            old[g][1] = lds64_if(gl[g], acc + (ro[X][e][g] >> 16));
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            sts64_if(gl[g], acc + (ro[X][e][g] & 0xffffu), __fma_rn(a, rv[X][e][g].x, old[g][0]));
+            sts64_if(gl[g], acc + (ro[X][e][g] >> 16), __fma_rn(a, rv[X][e][g].y, old[g][1]));
+        }
+        __syncwarp();
+    };
+    auto half = [&](auto Xc, int h) {
+        constexpr int X = decltype(Xc)::value;
+        double a_[HB];
+        int k_[HB], nb_[HB];
+#pragma unroll
+        for (int e = 0; e < HB; ++e) get(h * HB + e, a_[e], k_[e], nb_[e]);
+        if (nb_[0] > 0) sts32i(acc + 8u * (uint32_t)S, (int)ro[X][0][0]);  // touch: waits for this burst
+        const int kf = k_[0], kl = k_[HB - 1];
+        if (kf + hB >= R.F + S) split_emit_to<W, MODE>(p, sm, lane, wid, R, (kf - hB) & ~127, o_col, o_val, nOld,
+                                                       crow_v, crow_c);
+        __syncwarp();
+        burst(std::integral_constant<int, X ^ 1>{}, h + 1);
+        if (kl + hB < R.F + S) {
+#pragma unroll
+            for (int e = 0; e < HB; ++e) step(X, e, a_[e], nb_[e]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < HB; ++e) {
+                const int kt = k_[e];
+                if (kt + hB >= R.F + S)
+                    split_emit_to<W, MODE>(p, sm, lane, wid, R, (kt - hB) & ~127, o_col, o_val, nOld, crow_v, crow_c);
+                step(X, e, a_[e], nb_[e]);
+            }
+        }
+    };
+    for (int p0 = 0; p0 < nA; p0 += kPiece) {
+        const int cnt = min(kPiece, nA - p0);
+        const int nh = (cnt + HB - 1) / HB;
+        for (int q = lane; q < (nh + 1) * HB; q += 32) {
+            int k, nb;
+            double a;
+            if (q < cnt) {
+                k = a_col[p0 + q];
+                nb = __ldg(p.bt_nbin + (size_t)k * W + wid);
+                a = a_val[p0 + q];
+            } else {
+                k = a_col[p0 + cnt - 1];
+                nb = 0;
+                a = 0.0;
+            }
+            const unsigned long long knb = (unsigned long long)(uint32_t)k | ((unsigned long long)(uint32_t)nb << 32);
+            asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(stg + 16u * q), "l"(__double_as_longlong(a)),
+                         "l"(knb) : "memory");
+        }
+        __syncwarp();
+        burst(std::integral_constant<int, 0>{}, 0);
+        for (int h = 0; h < nh; h += 2) {
+            half(std::integral_constant<int, 0>{}, h);
+            if (h + 1 < nh) half(std::integral_constant<int, 1>{}, h + 1);
+        }
+    }
+    split_emit_to<W, MODE>(p, sm, lane, wid, R, Fend, o_col, o_val, nOld, crow_v, crow_c);
+}
+
+template <int W, int G, int HB, int MODE>
+__global__ void __launch_bounds__(32 * W, 6) row_split_kernel(const RowOpParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int S = p.S;
+    SplitSmem<W> sm;
+    sm.acc = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    sm.stg = sm.acc + (uint32_t)((S + kSplitTrash) * 8) + (uint32_t)(wid * kSplitStage * 16);
+    sm.xcnt = sm.acc + (uint32_t)((S + kSplitTrash) * 8 + W * kSplitStage * 16);
+    sm.rowq = sm.xcnt + 32u;
+    sm.nrmx = sm.rowq + 16u;
+    sm.flg = sm.nrmx + 8u * W;
+    for (int jj = 2 * (int)threadIdx.x; jj < S + kSplitTrash; jj += 64 * W) sts128(sm.acc + 8u * jj, 0.0, 0.0);
+    if (MODE != 0)
+        for (int jj = 4 * (int)threadIdx.x; jj < S; jj += 128 * W) sts32i(sm.flg + jj, 0);
+    __syncthreads();
+    int32_t my_max_kept = 0, my_ovf = 0;
+    int xbuf = 0;
+    const int chunk = p.row_chunk;
+    for (int it = 0;; ++it) {
+        const uint32_t rq = sm.rowq + 8u * (uint32_t)(it & 1);  // double-buffered row ticket
+        if (threadIdx.x == 0) {
+            const unsigned long long t = atomicAdd(p.row_ticket, 1ull);
+            asm volatile("st.shared.s64 [%0], %1;" ::"r"(rq), "l"((long long)(p.row_begin + chunk * (int64_t)t))
+                         : "memory");
+        }
+        __syncthreads();
+        long long i0;
+        asm volatile("ld.shared.s64 %0, [%1];" : "=l"(i0) : "r"(rq) : "memory");
+        if (i0 >= p.row_end) break;
+        for (int64_t i = i0; i < i0 + chunk && i < p.row_end; ++i) {
+            const double* a_val = p.A.val + (size_t)i * p.A.w;
+            const int32_t* a_col = p.A.col + (size_t)i * p.A.w;
+            const int nA = (p.alpha != 0.0) ? p.A.nnz[i] : 0;
+            const double* o_val = nullptr;
+            const int32_t* o_col = nullptr;
+            int nOld = 0;
+            if (MODE != 0) {
+                o_val = p.Old.val + (size_t)i * p.Old.w;
+                o_col = p.Old.col + (size_t)i * p.Old.w;
+                nOld = p.Old.nnz[i];
+            }
+            double* crow_v = p.C.val + (size_t)i * p.C.w;
+            int32_t* crow_c = p.C.col + (size_t)i * p.C.w;
+            SplitRow R;
+            R.i = i;
+            R.kept = 0;
+            R.old_cur = 0;
+            R.xbuf = xbuf;
+            R.ds = R.dc = R.nrm = 0.0;
+            double dA = 0.0;
+            if (p.diag_a && wid == 0) {
+                bool has = false;
+                for (int q = lane; q < nA; q += 32)
+                    if (a_col[q] == (int)i) { dA = a_val[q]; has = true; }
+                const unsigned mm = __ballot_sync(FULL, has);
+                dA = mm ? __shfl_sync(FULL, dA, __ffs(mm) - 1) : 0.0;
+            }
+            row_split<W, G, HB, MODE>(p, sm, lane, wid, R, a_col, a_val, nA, o_col, o_val, nOld, crow_v, crow_c);
+            xbuf = R.xbuf;
+            // epilogue: the diagonal values live in the owning warp's lane (x + 0 = x exactly)
+            const double ds = warp_sum(R.ds), dc = warp_sum(R.dc);
+            const bool owner = (((int)i >> 5) & (W - 1)) == wid;
+            if (owner && lane == 0) {
+                if (p.diag_c) p.diag_c[i] = dc;
+                if (p.diag_s) p.diag_s[i] = ds;
+            }
+            if (MODE == 2 && p.normsq) {
+                const double nr = warp_sum(R.nrm);
+                if (W == 1) {
+                    if (lane == 0) p.normsq[i] = nr;
+                } else {
+                    if (lane == 0) sts64(sm.nrmx + 8u * wid, nr);
+                    bar_cta(32 * W);
+                    if (wid == 0 && lane == 0) {
+                        double t = 0.0;
+#pragma unroll
+                        for (int q = 0; q < W; ++q) t = __dadd_rn(t, lds64(sm.nrmx + 8u * q));
+                        p.normsq[i] = t;
+                    }
+                    bar_cta(32 * W);
+                }
+            }
+            if (wid == 0) {
+                if (lane == 0) {
+                    p.C.nnz[i] = R.kept < p.C.w ? R.kept : p.C.w;
+                    if (p.diag_a) p.diag_a[i] = dA;
+                }
+                my_max_kept = max(my_max_kept, R.kept);
+                if (R.kept > p.C.w) ++my_ovf;
+            }
+        }
+    }
+    if (wid == 0 && lane == 0) {
+        if (my_ovf) atomicAdd(p.status + 0, my_ovf);
+        if (my_max_kept) atomicMax(p.status + 1, my_max_kept);
+    }
+}
+
+// -------------------------------------------------------------------------- dispatch
+
+template <typename K>
+static cudaError_t split_prep(K kern, int threads, size_t smem, int* bps) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, kern, threads, smem);
+}
+
+template <int W, int MODE, typename Fn>
+static void split_dispatch(int G, Fn f) {
+    // steps per register half: deep bursts for one warp per row (255 registers); W = 2 runs 6
+    // two-warp CTAs per SM, 168 registers per thread
+    switch (G) {
+        case 1: f(row_split_kernel<W, 1, W == 1 ? 4 : 3, MODE>); break;
+        case 2: f(row_split_kernel<W, 2, W == 1 ? 3 : 2, MODE>); break;
+        case 3: f(row_split_kernel<W, 3, W == 1 ? 2 : 1, MODE>); break;
+        default: f(row_split_kernel<W, 4, W == 1 ? 2 : 1, MODE>); break;
+    }
+}
+
+template <int W, int MODE>
+static cudaError_t split_prep_wm(int G, size_t smem, int* bps) {
+    cudaError_t e = cudaSuccess;
+    split_dispatch<W, MODE>(G, [&](auto k) { e = split_prep(k, 32 * W, smem, bps); });
+    return e;
+}
+
+template <int W, int MODE>
+static void split_launch_wm(int G, const RowOpParams& p, int grid, size_t smem, cudaStream_t s) {
+    split_dispatch<W, MODE>(G, [&](auto k) { k<<<grid, 32 * W, smem, s>>>(p); });
+}
+
+static int split_mode_of(const RowOpParams& p) { return p.old_mode == 0 ? 0 : (p.normsq ? 2 : 1); }
+
+size_t split_row_smem(int S, int W, bool has_old) { return split_smem_bytes(S, W, has_old); }
+
+cudaError_t plan_split(const RowOpParams& p, int S, int W, int G, int num_sms, LaunchCfg* cfg) {
+    if (S % 128 || W < 1 || W > 2 || G < 1 || G > 4) return cudaErrorInvalidValue;
+    const size_t smem = split_smem_bytes(S, W, p.old_mode != 0);
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    int bps = 0;
+    const int mode = split_mode_of(p);
+    cudaError_t e;
+    if (W == 2) e = mode == 0 ? split_prep_wm<2, 0>(G, smem, &bps) : mode == 1 ? split_prep_wm<2, 1>(G, smem, &bps)
+                                                                          : split_prep_wm<2, 2>(G, smem, &bps);
+    else e = mode == 0 ? split_prep_wm<1, 0>(G, smem, &bps) : mode == 1 ? split_prep_wm<1, 1>(G, smem, &bps)
+                                                                      : split_prep_wm<1, 2>(G, smem, &bps);
+    if (e) return e;
+    if (bps < 1) return cudaErrorInvalidConfiguration;
+    cfg->S = S;
+    cfg->R = G;
+    cfg->warps_per_cta = W;
+    cfg->smem = smem;
+    cfg->bps = bps;
+    const int64_t rows = p.row_end - p.row_begin;
+    const int64_t full = (int64_t)bps * num_sms;
+    cfg->grid = (int)(rows < full ? (rows > 0 ? rows : 1) : full);
+    return cudaSuccess;
+}
+
+cudaError_t launch_split(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s) {
+    const int mode = split_mode_of(p);
+    const int G = cfg.R;
+    if (cfg.warps_per_cta == 2) {
+        if (mode == 0) split_launch_wm<2, 0>(G, p, cfg.grid, cfg.smem, s);
+        else if (mode == 1) split_launch_wm<2, 1>(G, p, cfg.grid, cfg.smem, s);
+        else split_launch_wm<2, 2>(G, p, cfg.grid, cfg.smem, s);
+    } else {
+        if (mode == 0) split_launch_wm<1, 0>(G, p, cfg.grid, cfg.smem, s);
+        else if (mode == 1) split_launch_wm<1, 1>(G, p, cfg.grid, cfg.smem, s);
+        else split_launch_wm<1, 2>(G, p, cfg.grid, cfg.smem, s);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace ell

@@ -19,12 +19,15 @@ ap.add_argument("--m", type=int, default=64)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--window", type=int, default=0)
 ap.add_argument("--ablate", type=int, default=0)
+ap.add_argument("--ring-kernel", type=int, default=0)
 a = ap.parse_args()
 X = synth.cfg5(a.n, a.m)
 x = eb.Mat.from_host(X)
 ctx = eb.Context(0)
 if a.window:
     ctx.set_option(eb.OPT_WINDOW, a.window)
+if a.ring_kernel:
+    ctx.set_option(eb.OPT_RING_KERNEL, a.ring_kernel)
 if a.ablate:
     ctx.set_option(eb.OPT_ABLATE, a.ablate)
 y = eb.Mat.empty(a.n, a.m)
