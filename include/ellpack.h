@@ -127,10 +127,18 @@ int ellpack_ctx_set_stream(ellpack_ctx ctx, void* stream);
  *                          alias an input and the ring fits 16-bit offsets, else the legacy ring
  *                          kernel), 1 = always the legacy ring kernel, 2 = the split-row kernel
  *                          with 1 warp per row, 3 = with 2 warps per row. Results are bitwise the
- *                          same for every choice (A/B experiments and tests). */
+ *                          same for every choice (A/B experiments and tests).
+ *  ELLPACK_OPT_SP2_DEVICE_LOOP  0 (default) = automatic: on one rank, for N <= 8192, sp2_run runs its
+ *                          loop as ONE launch of a CUDA graph with a conditional WHILE node (branch,
+ *                          stop and width rules decided on the device): no host
+ *                          synchronisation per iteration; both iterates at the physical width
+ *                          max_width, every step on the general path. 1 = always the host loop
+ *                          (one synchronisation per iteration), 2 = the device loop whenever it
+ *                          applies (one rank). Results are bitwise the same either way. */
 enum { ELLPACK_OPT_WINDOW = 1, ELLPACK_OPT_WARPS = 2, ELLPACK_OPT_SP2_WIDTH0 = 3, ELLPACK_OPT_PROFILE = 4,
        ELLPACK_OPT_ABLATE = 5, ELLPACK_OPT_GENERAL_WINDOW = 6, ELLPACK_OPT_VALIDATE = 7,
-       ELLPACK_OPT_SP2_SYMMETRIC = 8, ELLPACK_OPT_SP2_MEM_CAP = 9, ELLPACK_OPT_RING_KERNEL = 10 };
+       ELLPACK_OPT_SP2_SYMMETRIC = 8, ELLPACK_OPT_SP2_MEM_CAP = 9, ELLPACK_OPT_RING_KERNEL = 10,
+       ELLPACK_OPT_SP2_DEVICE_LOOP = 11 };
 int ellpack_ctx_set_option(ellpack_ctx ctx, int key, int64_t value);
 
 /* Accumulated device time (ms, CUDA events on the ctx stream) and launch count of

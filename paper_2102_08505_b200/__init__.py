@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _REPO = os.path.dirname(_HERE)
 _LIB = os.environ.get("ELLPACK_LIB") or os.path.join(_HERE, "libellpack.so")
-_SRCS = [os.path.join(_HERE, "csrc", f) for f in ("spgemm.cu", "split.cu", "reduce.cu", "api.cu")]
+_SRCS = [os.path.join(_HERE, "csrc", f) for f in ("spgemm.cu", "split.cu", "reduce.cu", "sp2_graph.cu", "api.cu")]
 _HDRS = [os.path.join(_HERE, "csrc", f) for f in ("internal.cuh", "devutil.cuh")] + [os.path.join(_REPO, "include", "ellpack.h")]
 
 OK, ERR_ARG, ERR_DIM, ERR_OVERFLOW, ERR_BOUNDS, ERR_NOCONV, ERR_NOMEM, ERR_CUDA, ERR_NCCL, ERR_STATE = range(10)
@@ -30,6 +30,7 @@ OPT_WINDOW, OPT_WARPS, OPT_SP2_WIDTH0, OPT_PROFILE, OPT_ABLATE, OPT_GENERAL_WIND
 OPT_SP2_SYMMETRIC = 8
 OPT_SP2_MEM_CAP = 9
 OPT_RING_KERNEL = 10
+OPT_SP2_DEVICE_LOOP = 11
 SP2_FAIL, SP2_GROW = 0, 1
 SP2_RULE_TRACE_SIGN, SP2_RULE_TRACE_CLOSEST = 0, 1
 STOP_NAMES = {0: "CONVERGED", 1: "STAGNATED", 2: "NOCONV", 3: "OVERFLOW"}

@@ -108,6 +108,12 @@ struct ellpack_ctx_s {
     LaunchCfg last_cfg{};
     int32_t last_fast = 0, last_hB = 0, last_split = 0;
     int ring_kernel = 0;  // ELLPACK_OPT_RING_KERNEL
+    int sp2_loop = 0;     // ELLPACK_OPT_SP2_DEVICE_LOOP
+    int force_general_s = 0;  // device SP2 loop: every row op on the general path with this window
+    Buf sp2dev, sp2rec;       // device SP2 loop: control block, iteration records
+    cudaGraphExec_t sp2_exec = nullptr;  // device SP2 loop: the instantiated graph and what it captured
+    uint64_t sp2_exec_key = 0;
+    int sp2_exec_launches = 0;
     bool last_step_general = false;
     struct Host {
         int32_t bw[8];
@@ -329,7 +335,8 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
         const int rk = c->ring_kernel;
         const int64_t sring = (2 * hB + 129 + 127) & ~int64_t(127);
         const bool stash = p.stash_a || p.stash_old;
-        if (c->window_opt == 0 && rk != 1 && !stash && groups <= 4 && sring <= kSplitRingMax) {
+        if (c->window_opt == 0 && c->force_general_s == 0 && rk != 1 && !stash && groups <= 4 &&
+            sring <= kSplitRingMax) {
             const int W = rk == 3 ? 2 : 1;  // automatic: one warp per row (measured faster)
             const int maxsub = p.alpha != 0.0 ? bwv[4] : 0;
             const int G = W == 1 ? (groups < 1 ? 1 : groups) : std::max(1, (maxsub + 63) / 64);
@@ -360,9 +367,9 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
     if (split_w) {
         p.fast = 1;
         S = scfg.S;
-    } else if (c->window_opt > 0) {
-        // forced general path (tests): multi-pass windows of window_opt doubles
-        S = c->window_opt;
+    } else if (c->window_opt > 0 || c->force_general_s > 0) {
+        // forced general path (tests; the device SP2 loop): multi-pass windows
+        S = c->window_opt > 0 ? c->window_opt : c->force_general_s;
         p.fast = 0;
     } else if (ring <= kFastWindowMax && groups <= 4) {
         // Grow the ring by slack while the rows resident per SM stay the same: slack lets the
@@ -701,7 +708,8 @@ int ellpack_ctx_destroy(ellpack_ctx c) {
     Buf* bufs[] = {&c->rows[0], &c->rows[1], &c->rows[2], &c->rows[3], &c->partials,
                    &c->stash_val, &c->stash_col, &c->ident_val, &c->ident_col, &c->ident_nnz,
                    &c->hx_val, &c->hx_col, &c->hx_nnz, &c->hy_val, &c->hy_col, &c->hy_nnz,
-                   &c->bt, &c->bt_nbin, &c->bp, &c->halo, &c->vflag, &c->symaux};
+                   &c->bt, &c->bt_nbin, &c->bp, &c->halo, &c->vflag, &c->symaux, &c->sp2dev, &c->sp2rec};
+    if (c->sp2_exec) cudaGraphExecDestroy(c->sp2_exec);
     for (auto& sl : c->it)
         for (Buf& b : sl) release(c, b);
     for (Buf* b : bufs) release(c, *b);
@@ -733,6 +741,10 @@ int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
         case ELLPACK_OPT_WARPS: c->warps_opt = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_SP2_WIDTH0: c->sp2_width0 = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_SP2_MEM_CAP: c->sp2_mem_cap = v; return ELLPACK_OK;
+        case ELLPACK_OPT_SP2_DEVICE_LOOP:
+            if (v > 2) return ELLPACK_ERR_ARG;
+            c->sp2_loop = (int)v;
+            return ELLPACK_OK;
         case ELLPACK_OPT_RING_KERNEL:
             if (v > 3) return ELLPACK_ERR_ARG;
             c->ring_kernel = (int)v;
@@ -1328,6 +1340,192 @@ void take_probe(ellpack_ctx c, int32_t* bw, std::vector<int64_t>& need) {
     }
 }
 
+
+// ---------------------------------------------------------------- device-resident SP2 loop
+
+constexpr int64_t kDevLoopMaxN = 8192;         // automatic: the device loop for N up to this
+constexpr int kDevLoopWindow = 1024;           // its general-path window (every iterate width)
+
+// The device loop keeps both iterates at the physical width max_width (no regrow inside the
+// graph), single rank, and the automatic choice takes it for small N only: there the host
+// synchronisation and the launch sequence are the iteration's cost.
+bool use_device_loop(ellpack_ctx c, int64_t n, int32_t maxw) {
+    if (c->comm || c->sp2_loop == 1) return false;
+    const double bytes = 2.0 * 12.0 * (double)n * (double)maxw;
+    if (c->sp2_loop == 2) return bytes <= 64e9;
+    return n <= kDevLoopMaxN && bytes <= 4e9;
+}
+
+uint64_t mix64(uint64_t h, uint64_t v) {
+    h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    return h;
+}
+
+// SP2 iterations as ONE launch of a CUDA graph: a WHILE node whose body is one iteration
+// (products, breakpoints, the fused step on the general path with (alpha, beta, old_mode) from the
+// control block, [T2], canonical sums, rows over the logical width, the control kernel, X <- Y).
+// The host waits once, after the loop. X (width maxw) holds X0 on entry and the final iterate on
+// exit. Fills the report fields the host loop fills and returns an ellpack status.
+int sp2_device_loop(ellpack_ctx c, const sp2_opts& o, int64_t n, int64_t nocc, double tol, int32_t w, int32_t maxw,
+                    bool closest, double& trX, double t2, DevMatrix& X, DevMatrix& Y, sp2_report& R,
+                    sp2_iter_rec* iters, int32_t& wx, int& stop, int& it, double& t_loop) {
+    // iterates at the physical width maxw
+    if (X.d.w < maxw) {
+        RK(dm_alloc(c, Y, n, maxw));
+        CK(cudaMemsetAsync(c->d_status, 0, 8, c->stream));
+        CK(launch_copy_rows(kmat(&X.d), kout(&Y.d), 0, n, c->d_status, c->stream));
+        c->launches++;
+        std::swap(X, Y);
+    }
+    if (!Y.owned || Y.d.w < maxw) RK(dm_alloc(c, Y, n, maxw));
+    // workspace the captured launches use, grown before capture (no allocation inside the graph)
+    const int S = (int)std::min<int64_t>(kDevLoopWindow, (n + 31) & ~int64_t(31));
+    const int np = (int)((n + S - 1) / S) + 1;
+    RK(grow(c, c->bp, sizeof(int32_t) * (size_t)n * np));
+    for (int a = 0; a < 4; ++a) RK(grow(c, c->rows[a], sizeof(double) * n));
+    RK(grow(c, c->partials, sizeof(double) * 4 * (size_t)((n + kTraceBlock - 1) / kTraceBlock)));
+    RK(grow(c, c->sp2dev, sizeof(Sp2Dev)));
+    RK(grow(c, c->sp2rec, sizeof(sp2_iter_rec) * (size_t)o.max_iter));
+    Sp2Dev* dev = (Sp2Dev*)c->sp2dev.p;
+    Sp2Dev hd;
+    memset(&hd, 0, sizeof hd);
+    hd.tol = tol;
+    hd.stag_gate = o.stag_gate;
+    hd.nocc = (double)nocc;
+    hd.min_iter = o.min_iter;
+    hd.max_iter = o.max_iter;
+    hd.on_overflow = o.on_overflow;
+    hd.closest = closest;
+    hd.maxw = maxw;
+    int branch = (trX > (double)nocc) ? SP2_SQUARE : SP2_EXPAND;
+    if (closest)
+        branch = (std::fabs(t2 - (double)nocc) < std::fabs((2.0 * trX - t2) - (double)nocc)) ? SP2_SQUARE : SP2_EXPAND;
+    hd.branch = branch;
+    hd.dyn[0] = branch == SP2_SQUARE ? 1.0 : -1.0;
+    hd.dyn[1] = branch == SP2_SQUARE ? 0.0 : 2.0;
+    hd.dyn[2] = branch == SP2_SQUARE ? 2.0 : 1.0;
+    hd.trX = trX;
+    hd.t2 = t2;
+    hd.e2 = hd.e1 = NAN;
+    hd.stop = -1;
+    hd.wy = w;
+    CK(cudaMemcpyAsync(dev, &hd, sizeof hd, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->d_status + 2, 0, sizeof(int32_t), c->stream));
+    CK(cudaMemsetAsync(c->d_keys + 2, 0, 8, c->stream));
+
+    // the graph: rebuilt only when something it captured changed
+    uint64_t key = 0x5350320ull;
+    for (uint64_t v : {(uint64_t)(uintptr_t)X.d.val, (uint64_t)(uintptr_t)Y.d.val, (uint64_t)(uintptr_t)c->bp.p,
+                       (uint64_t)(uintptr_t)c->rows[0].p, (uint64_t)(uintptr_t)c->rows[3].p,
+                       (uint64_t)(uintptr_t)c->partials.p, (uint64_t)(uintptr_t)c->sp2dev.p,
+                       (uint64_t)(uintptr_t)c->sp2rec.p, (uint64_t)(uintptr_t)c->stream, (uint64_t)n,
+                       (uint64_t)maxw, (uint64_t)closest, (uint64_t)S})
+        key = mix64(key, v);
+    uint64_t tb;
+    memcpy(&tb, &o.threshold, 8);
+    key = mix64(key, tb);
+    if (!c->sp2_exec || c->sp2_exec_key != key) {
+        if (c->sp2_exec) { cudaGraphExecDestroy(c->sp2_exec); c->sp2_exec = nullptr; }
+        cudaGraph_t g = nullptr;
+        CK(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle cond;
+        cudaError_t e = cudaGraphConditionalHandleCreate(&cond, g, 1u, cudaGraphCondAssignDefault);
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = cond;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t wnode;
+        if (!e) e = cudaGraphAddNode(&wnode, g, nullptr, 0, &cp);
+        cudaStream_t cs = nullptr;
+        if (!e) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+        int rc = ELLPACK_OK;
+        int64_t l0 = c->launches;
+        if (!e) e = cudaStreamBeginCaptureToGraph(cs, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                  cudaStreamCaptureModeRelaxed);
+        if (!e) {
+            cudaStream_t saved = c->stream;
+            const bool prof = c->profile;
+            c->stream = cs;
+            c->profile = false;
+            c->force_general_s = S;
+            do {
+                if ((e = launch_products(kmat(&X.d), X.d.nnz, 0, n, c->d_keys + 2, cs))) break;
+                c->launches++;
+                RowOpParams p = base_params(c, n);
+                p.A = kmat(&X.d);
+                p.B = kmat(&X.d);
+                p.Old = kmat(&X.d);
+                p.C = kout(&Y.d);
+                p.tau = o.threshold;
+                p.alpha = 1.0;     // placeholders for the planner: the kernel reads p.dyn
+                p.old_mode = 2;
+                p.dyn = dev->dyn;
+                p.diag_s = (double*)c->rows[0].p;
+                p.diag_c = (double*)c->rows[1].p;
+                p.normsq = (double*)c->rows[2].p;
+                int32_t bw0[kProbe] = {0, 0, 0, 0, 0, 0, 0};
+                if ((rc = enqueue_row_op(c, p, n, bw0))) break;
+                if (closest) {
+                    if ((e = launch_sumsq_rows(kmat(&Y.d), 0, n, (double*)c->rows[3].p, cs))) break;
+                    c->launches++;
+                }
+                const double* arrs[4] = {p.diag_s, p.diag_c, p.normsq, (const double*)c->rows[3].p};
+                if ((rc = enqueue_canonical(c, arrs, closest ? 4 : 3, n))) break;
+                if ((e = launch_count_over_dev(Y.d.nnz, n, dev, c->d_status + 2, cs))) break;
+                if ((e = launch_sp2_ctl(dev, c->d_sums, c->d_status, c->d_status + 2, c->d_keys + 2, c->sp2rec.p,
+                                        (unsigned long long)cond, cs)))
+                    break;
+                if ((e = launch_copy_rows(kmat(&Y.d), kout(&X.d), 0, n, c->d_status + 4, cs))) break;
+                c->launches += 3;
+            } while (false);
+            c->stream = saved;
+            c->profile = prof;
+            c->force_general_s = 0;
+            cudaGraph_t body_out = nullptr;
+            cudaError_t e2 = cudaStreamEndCapture(cs, &body_out);
+            if (!e) e = e2;
+        }
+        c->sp2_exec_launches = (int)(c->launches - l0);
+        c->launches = l0;
+        if (!e && rc == ELLPACK_OK) e = cudaGraphInstantiate(&c->sp2_exec, g, 0);
+        if (cs) cudaStreamDestroy(cs);
+        cudaGraphDestroy(g);
+        if (rc != ELLPACK_OK) return rc;
+        CK(e);
+        c->sp2_exec_key = key;
+    }
+    cudaEventRecord(c->ev[0], c->stream);
+    CK(cudaGraphLaunch(c->sp2_exec, c->stream));
+    cudaEventRecord(c->ev[1], c->stream);
+    CK(cudaMemcpyAsync(&hd, dev, sizeof hd, cudaMemcpyDeviceToHost, c->stream));
+    RK(host_sync(c));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    t_loop = ms * 1e-3;
+    it = hd.it;
+    c->launches += (int64_t)c->sp2_exec_launches * (hd.it + (hd.stop == SP2_OVERFLOWED ? 1 : 0));
+    if (iters && hd.it > 0) {
+        CK(cudaMemcpyAsync(iters, c->sp2rec.p, sizeof(sp2_iter_rec) * (size_t)hd.it, cudaMemcpyDeviceToHost,
+                           c->stream));
+        RK(host_sync(c));
+    }
+    trX = hd.trX;
+    wx = hd.wy;
+    R.regrows += hd.regrows;
+    if (hd.stop == SP2_OVERFLOWED) {
+        R.stop_reason = SP2_OVERFLOWED;
+        R.overflow_rows = hd.overflow_rows;
+        R.required_width = hd.required;
+        R.fail_iter = hd.fail_iter;
+        c->last_ovf_rows = hd.overflow_rows;
+        c->last_req = hd.required;
+        return ELLPACK_ERR_OVERFLOW;
+    }
+    stop = hd.stop;
+    return ELLPACK_OK;
+}
+
 }  // namespace
 
 int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, const sp2_opts* opts_in,
@@ -1467,6 +1665,16 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     int stop = -1;
     int it;
     UpperAlloc ua{&U, n, 0};
+    const bool dev_loop = use_device_loop(c, n, maxw);
+    if (dev_loop) {
+        // (§8f-f3) the whole loop as one graph launch: zero host synchronisations per iteration
+        double t_loop = 0.0;
+        it = 0;
+        rc = sp2_device_loop(c, o, n, nocc, tol, w, maxw, closest, trX, t2, X, Y, R, iters, wx, stop, it, t_loop);
+        if (rc) status = rc;
+        t_x2 = t_loop;
+    }
+    if (!dev_loop)
     for (it = 0; it < o.max_iter; ++it) {
         int branch = (trX > (double)nocc) ? SP2_SQUARE : SP2_EXPAND;
         if (closest)  // (same expression as the oracle: tie -> EXPAND)

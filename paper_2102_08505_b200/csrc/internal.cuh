@@ -62,6 +62,8 @@ struct RowOpParams {
     int32_t row_chunk;               // fast kernel: consecutive rows per ticket (4; 1 for small launches)
     int32_t upper;                   // general kernel: columns j >= i only (symmetric SP2 step, f4 ii)
     KOut C_upper;                    // upper-triangle output when the general path takes `upper`
+    const double* dyn;                  // general kernel (nullable): (alpha, beta, old_mode) read from
+                                        // device memory (device-resident SP2 loop, f3)
     unsigned long long* exec_products;  // general kernel (nullable): += products it executes (B entries
                                         // accumulated; the symmetric step's count, about P / 2)
     // per-warp global scratch: in-place rows are copied aside (stash) before they are rewritten
@@ -94,6 +96,29 @@ cudaError_t launch_balance(KMat b, int64_t k0, int64_t k1, int wt, int S, unsign
 // [INT_MAX - out[5], out[6] - 1] (out[0..6] zeroed by the caller)
 cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int64_t r0, int64_t r1, int64_t b0, int64_t b1, int64_t n,
                              int32_t* out, cudaStream_t s);
+
+// sp2_graph.cu: device-resident SP2 control (§8f-f3). The loop state lives in device memory; a
+// one-thread control kernel at the end of every captured iteration applies the stop rule, the
+// GROW/FAIL width rule and the branch rule (the host loop's decisions, same expressions), records
+// the iteration, writes (alpha, beta, old_mode) of the next step for row_general_dyn_kernel and
+// sets the condition of the graph's WHILE node.
+struct Sp2Dev {
+    // constants (host)
+    double tol, stag_gate, nocc;
+    int32_t min_iter, max_iter, on_overflow, closest, maxw, pad0;
+    // state
+    double dyn[3];  // alpha, beta, old_mode of the next step
+    double trX, t2, e2, e1;  // tr X_n, T2 of X_n (trace-closest rule), e_{n-2}, e_{n-1}
+    int32_t it, stop, wy, regrows, fail_iter, required, branch, pad1;
+    int64_t overflow_rows;
+};
+// count rows of [0, n) with nnz > dev->wy into *out (the FAIL report over the logical width)
+cudaError_t launch_count_over_dev(const int32_t* nnz, int64_t n, const Sp2Dev* dev, int32_t* out, cudaStream_t s);
+// one thread: the loop's decisions after a step (sums: trS, trX_{n+1}, ||S - X||^2 [, T2 of X_{n+1}];
+// status[1]: max kept; ovf: rows over the logical width; prod: products of the step); also zeroes
+// ovf and prod for the next iteration. rec: the caller's sp2_iter_rec array (device).
+cudaError_t launch_sp2_ctl(Sp2Dev* dev, const double* sums, const int32_t* status, int32_t* ovf,
+                           unsigned long long* prod, void* rec, unsigned long long cond_handle, cudaStream_t s);
 
 // split.cu: the split-row ring kernel (W warps per row, 16-bit balanced sub-records)
 cudaError_t plan_split(const RowOpParams& p, int S, int W, int G, int num_sms, LaunchCfg* cfg);

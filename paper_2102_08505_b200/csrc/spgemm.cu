@@ -971,12 +971,11 @@ __global__ void __launch_bounds__(32, 8) row_fast_kernel(const RowOpParams p) {
 // General kernel: span pre-pass + one pass per S-aligned window the row touches; B rows are
 // split at window boundaries by precomputed breakpoints (rows wider than any ring that fits
 // shared memory, B rows > 256 entries: the densifying SP2 iterates).
-template <int MODE>
 #ifndef ELL_GEN_MINB
 #define ELL_GEN_MINB 1  // general kernel: min resident 128-thread CTAs per SM (register cap)
 #endif
-__global__ void __launch_bounds__(128, ELL_GEN_MINB) row_general_kernel(const RowOpParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+template <int MODE>
+__device__ __forceinline__ void row_general_body(const RowOpParams& p, unsigned char* smem_raw) {
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int S = p.S;
@@ -1111,6 +1110,26 @@ __global__ void __launch_bounds__(128, ELL_GEN_MINB) row_general_kernel(const Ro
         for (int o = 16; o; o >>= 1) my_exec += __shfl_xor_sync(FULL, my_exec, o);
         if (lane == 0 && my_exec) atomicAdd(p.exec_products, my_exec);
     }
+}
+
+
+template <int MODE>
+__global__ void __launch_bounds__(128, ELL_GEN_MINB) row_general_kernel(const RowOpParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    row_general_body<MODE>(p, smem_raw);
+}
+
+// The same kernel with (alpha, beta, old_mode) read from device memory (p.dyn): the SP2 step of
+// the device-resident loop (§8f-f3), whose branch is decided on the device between launches of
+// one captured CUDA graph.
+template <int MODE>
+__global__ void __launch_bounds__(128, ELL_GEN_MINB) row_general_dyn_kernel(const RowOpParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RowOpParams q = p;
+    q.alpha = p.dyn[0];
+    q.beta = p.dyn[1];
+    q.old_mode = (int)p.dyn[2];
+    row_general_body<MODE>(q, smem_raw);
 }
 
 // Half-bandwidth probe: out[m] = max over rows of max(i - col[i][0], col[i][nnz-1] - i) (a and c
@@ -1311,7 +1330,10 @@ static cudaError_t prep_kernel(K kern, const LaunchCfg& cfg, int* bps) {
 template <int MODE>
 static cudaError_t prep_mode(const LaunchCfg& cfg, int* bps) {
     switch (cfg.R) {
-        case 0: return prep_kernel(row_general_kernel<MODE>, cfg, bps);
+        case 0: {
+            cudaError_t e = prep_kernel(row_general_dyn_kernel<MODE>, cfg, bps);
+            return e ? e : prep_kernel(row_general_kernel<MODE>, cfg, bps);
+        }
         case 1: return prep_kernel(row_fast_kernel<1, 4, MODE>, cfg, bps);
         case 2: return prep_kernel(row_fast_kernel<2, 3, MODE>, cfg, bps);
         case 3: return prep_kernel(row_fast_kernel<3, ELL_G3_HB, MODE>, cfg, bps);
@@ -1323,7 +1345,10 @@ template <int MODE>
 static void launch_mode(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s) {
     dim3 block(cfg.warps_per_cta * 32), grid(cfg.grid);
     switch (cfg.R) {
-        case 0: row_general_kernel<MODE><<<grid, block, cfg.smem, s>>>(p); break;
+        case 0:
+            if (p.dyn) row_general_dyn_kernel<MODE><<<grid, block, cfg.smem, s>>>(p);
+            else row_general_kernel<MODE><<<grid, block, cfg.smem, s>>>(p);
+            break;
         case 1: row_fast_kernel<1, 4, MODE><<<grid, block, cfg.smem, s>>>(p); break;
         case 2: row_fast_kernel<2, 3, MODE><<<grid, block, cfg.smem, s>>>(p); break;
         case 3: row_fast_kernel<3, ELL_G3_HB, MODE><<<grid, block, cfg.smem, s>>>(p); break;

@@ -117,6 +117,7 @@ def test_sp2_iterate_memory_fallbacks_bitwise(ellpack_lib, slack):
     o = oracle.sp2(H, n // 2, 1e-10, oracle.SP2Opts(threshold=1e-6, max_iter=100), d_width=n)
     assert o.final_width > 256  # the general path (and its symmetric route) runs
     ctx = E.Context(0)
+    ctx.set_option(E.OPT_SP2_DEVICE_LOOP, 1)  # headroom widths and the symmetric step: the host loop
     ctx.set_option(E.OPT_SP2_MEM_CAP, 8 * n * (2 * o.final_width + slack))
     d = E.Mat.empty(n, n)
     g = ctx.sp2_run(up(H), n // 2, 1e-10, d, threshold=1e-6, max_iter=100)
@@ -134,6 +135,7 @@ def test_sp2_one_host_sync_per_iteration(ellpack_lib):
     syncs = {}
     for K in (4, 12):
         ctx = E.Context(0)
+        ctx.set_option(E.OPT_SP2_DEVICE_LOOP, 1)  # the host loop: one synchronisation per iteration
         ctx.set_option(E.OPT_SP2_SYMMETRIC, 0)
         d = E.Mat.empty(n, n)
         s0 = ctx.host_syncs()
@@ -165,3 +167,70 @@ def test_attach_nccl_checks_row_blocks(ellpack_lib):
         ctx.multiply_x2(up(X), E.Mat.empty(2048, 1024), 1e-5)
     assert ei.value.status == E.ERR_DIM
     ctx.close()
+
+
+# ---------------------------------------------- f3: the device-resident SP2 loop (CUDA graph)
+
+DEVLOOP = [
+    # (n, m, partners, band, seed, tau, rule, width0, nocc_frac, on_overflow)
+    (512, 32, 6, 12, 2, 0.0, 0, 0, 0.5, 1),
+    (600, 64, 10, 100, 14, 1e-4, 1, 0, 0.5, 1),
+    (513, 32, 8, 64, 13, 1e-4, 0, 16, 0.7, 1),
+    (1024, 32, 6, 12, 6, 1e-6, 0, 8, 0.5, 1),
+    (2048, 32, 6, 12, 3, 1e-7, 1, 0, 0.5, 1),
+    (300, 40, 10, 30, 31, 0.0, 0, 64, 0.5, 0),   # FAIL inside the loop: exact report
+]
+
+
+@pytest.mark.parametrize("case", DEVLOOP, ids=lambda c: f"n{c[0]}tau{c[5]}r{c[6]}f{c[9]}")
+def test_sp2_device_loop_bitwise(ellpack_lib, case):
+    """§8f-f3: the loop as one CUDA-graph launch (branch, stop and width rules on the device) is
+    bitwise the oracle and the host loop, report included, with a constant number of host
+    synchronisations per run (none per iteration)."""
+    E = ellpack_lib
+    n, m, partners, band, seed, tau, rule, w0, frac, onov = case
+    H = synth.sym_banded(n, m, partners, band, 1, -1.0, 1.0, 0, band / 4.0, 0.0, seed)
+    nocc = int(frac * n)
+    o = oracle.sp2(H, nocc, 1e-9, oracle.SP2Opts(threshold=tau, max_iter=100, branch_rule=rule, initial_width=w0,
+                                                 on_overflow=onov), d_width=n + (n & 1))
+    res = {}
+    for loop in (2, 1):
+        ctx = E.Context(0)
+        ctx.set_option(E.OPT_SP2_DEVICE_LOOP, loop)
+        ctx.set_option(E.OPT_SP2_SYMMETRIC, 0)
+        if w0:
+            ctx.set_option(E.OPT_SP2_WIDTH0, w0)
+        d = E.Mat.empty(n, n + (n & 1))
+        s0 = ctx.host_syncs()
+        g = ctx.sp2_run(up(H), nocc, 1e-9, d, threshold=tau, max_iter=100, branch_rule=rule, on_overflow=onov)
+        res[loop] = (g, ctx.host_syncs() - s0, d.to_host())
+        assert g.status == o.status
+        if o.status == oracle.OVERFLOW:
+            assert (g.fail_iter, g.required_width, g.overflow_rows) == (o.fail_iter, o.required_width, o.overflow_rows)
+        else:
+            _compare_sp2(g, o)
+            assert same_bits(res[loop][2], o.D)
+        ctx.close()
+    if o.status != oracle.OVERFLOW:
+        assert res[1][1] >= res[2][1] + o.iterations - 2  # the host loop waits once per iteration
+
+
+def test_sp2_device_loop_syncs_do_not_grow_with_iterations(ellpack_lib):
+    E = ellpack_lib
+    n = 1024
+    H = synth.sym_banded(n, 32, 6, 12, 1, -1.0, 1.0, 0, 4.0, 0.0, 3)
+    syncs = {}
+    for K in (4, 16):
+        ctx = E.Context(0)
+        ctx.set_option(E.OPT_SP2_DEVICE_LOOP, 2)
+        d = E.Mat.empty(n, n)
+        ctx.sp2_run(up(H), n // 2, 0.0, d, threshold=1e-7, max_iter=K, min_iter=100)  # graph built
+        s0 = ctx.host_syncs()
+        g = ctx.sp2_run(up(H), n // 2, 0.0, d, threshold=1e-7, max_iter=K, min_iter=100)
+        syncs[K] = ctx.host_syncs() - s0
+        assert g.iterations == K
+        o = oracle.sp2(H, n // 2, 0.0, oracle.SP2Opts(threshold=1e-7, max_iter=K, min_iter=100), d_width=n)
+        _compare_sp2(g, o)
+        assert same_bits(d.to_host(), o.D)
+        ctx.close()
+    assert syncs[16] == syncs[4], syncs
