@@ -380,6 +380,39 @@ def time_sp2(eb, mr, dev, ws, rank, cfg: int, K: int, steps: int, warmup: int):
     return out
 
 
+def time_sp2_small(eb, dev, reps: int):
+    """SP2 on a cfg1-sized H (BASELINE configs[0]'s matrix, N = 512, as the Hamiltonian; nocc = N/2,
+    tau = 1e-5, tol = 1e-8, to the stop rule): us per iteration with the host loop (one host
+    synchronisation per iteration) and with the device-resident loop (one CUDA-graph launch per run,
+    SURVEY §8f-f3), the same bits either way."""
+    import torch
+    H = synth.cfg1()
+    n = H.n
+    out = {"workload": "SP2 on cfg1's X as H: N=512 nocc=256 tau=1e-05 tol=1e-08, to the stop rule"}
+    ref = None
+    for name, loop in (("host_loop", 1), ("device_loop", 2)):
+        ctx = eb.Context(dev)
+        ctx.set_option(eb.OPT_SP2_DEVICE_LOOP, loop)
+        h = eb.Mat.from_host(H)
+        d = eb.Mat.empty(n, n)
+        run = lambda: ctx.sp2_run(h, n // 2, 1e-8, d, threshold=1e-5, max_iter=100)  # noqa: E731
+        for _ in range(3):
+            r = run()
+        torch.cuda.synchronize()
+        s0 = ctx.host_syncs()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            r = run()
+        dt = (time.perf_counter() - t0) / reps
+        out[name] = {"us_per_iteration": dt * 1e6 / r.iterations, "us_per_run": dt * 1e6, "iterations": r.iterations,
+                     "stop": r.stop, "host_syncs_per_run": (ctx.host_syncs() - s0) / reps}
+        key = (r.iterations, r.trD, tuple(it["e"] for it in r.iters))
+        out[name]["same_as_host_loop"] = None if ref is None else key == ref
+        ref = ref or key
+        ctx.close()
+    return out
+
+
 def time_cfg1(eb, dev, reps: int):
     """cfg1 (N = 512): us per ellpack_multiply_x2 call (incl. its status read-back), host clock over
     back-to-back calls, plus the device time of the same calls by CUDA events."""
@@ -508,7 +541,9 @@ def run_ours(args):
     bytes_launch = Bc / ws  # equal row blocks: the rank's share of the compulsory bytes
     achieved = bytes_launch / (kern_avg * 1e-3) / 1e9
     cap, cap_src = ncu_capture(f"x2_n{n}_m{args.m}")
-    kname = {"split": f"ell::row_split_kernel<W={launch['warps_per_cta']},G={launch['G']}> (ring S={launch['S']}, "
+    kname = {"ws": f"ell::row_ws_kernel<G={launch['G']}> (accumulator + emitter warps, ring S={launch['S']}, "
+                   f"{launch['ctas_per_sm']} rows/SM)",
+             "split": f"ell::row_split_kernel<W={launch['warps_per_cta']},G={launch['G']}> (ring S={launch['S']}, "
                       f"{launch['ctas_per_sm']} rows/SM)",
              "ring": f"ell::row_fast_kernel<G={launch['G']}> (ring S={launch['S']}, {launch['ctas_per_sm']} CTAs/SM)",
              "general": "ell::row_general_kernel"}[launch["path"]]
@@ -556,6 +591,8 @@ def run_ours(args):
     if not args.quick:
         sp2 = {"cfg3": time_sp2(eb, mr, dev, ws, rank, 3, 10, 3, 1),
                "cfg4": time_sp2(eb, mr, dev, ws, rank, 4, 6, 2, 1)}
+        if ws == 1:
+            sp2["cfg1_sized"] = time_sp2_small(eb, dev, 20)
         cfg1 = time_cfg1(eb, dev, 300) if ws == 1 else {"skipped": "N=512 is not divisible into 256-row blocks (R17)"}
         cfg2 = time_cfg2(eb, mr, dev, ws, rank, 10)
 
@@ -567,9 +604,9 @@ def run_ours(args):
         cpu = {"value": 2.0 * Ps / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": desc}
 
     lsu_pipe = None
-    if ws == 1 and launch["path"] in ("ring", "split"):
+    if ws == 1 and launch["path"] in ("ring", "split", "ws"):
         lsu_pipe = lsu_floor(X, P, nnz_c, clocks.get("sm_mhz"), torch.cuda.get_device_properties(dev).multi_processor_count,
-                             slot_bytes=2 if launch["path"] == "split" else 4)
+                             slot_bytes=2 if launch["path"] in ("split", "ws") else 4)
         if lsu_pipe.get("floor_ms"):
             lsu_pipe["frac"] = lsu_pipe["floor_ms"] / kern_avg
     if rank == 0:

@@ -270,7 +270,8 @@ class Context:
         """Geometry of the last row-kernel launch (ellpack_ctx_last_launch)."""
         a = (ctypes.c_int32 * 8)()
         _chk(lib().ellpack_ctx_last_launch(self._h, a), "ellpack_ctx_last_launch")
-        return dict(path={2: "split", 1: "ring", 0: "general"}[a[0]], G=a[1], S=a[2], warps_per_cta=a[3], grid=a[4],
+        return dict(path={3: "ws", 2: "split", 1: "ring", 0: "general"}[a[0]], G=a[1], S=a[2], warps_per_cta=a[3],
+                    grid=a[4],
                     smem_bytes=a[5], ctas_per_sm=a[6], hB=a[7])
 
     def host_syncs(self) -> int:

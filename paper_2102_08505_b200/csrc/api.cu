@@ -337,20 +337,24 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
         const bool stash = p.stash_a || p.stash_old;
         if (c->window_opt == 0 && c->force_general_s == 0 && rk != 1 && !stash && groups <= 4 &&
             sring <= kSplitRingMax) {
-            const int W = rk == 3 ? 2 : 1;  // automatic: one warp per row (measured faster)
+            // W = 0: the warp-specialized kernel (accumulator + emitter warps, W = 1 records)
+            const int W = rk == 3 ? 2 : (rk == 4 ? 0 : 1);  // automatic: one warp per row
             const int maxsub = p.alpha != 0.0 ? bwv[4] : 0;
-            const int G = W == 1 ? (groups < 1 ? 1 : groups) : std::max(1, (maxsub + 63) / 64);
+            const int G = W != 2 ? (groups < 1 ? 1 : groups) : std::max(1, (maxsub + 63) / 64);
             const int mode = !has_old ? 0 : (p.normsq ? 2 : 1);
             const int64_t key = (((sring * 8 + G) * 4 + mode) * 4 + W) * 2 + 1;
+            auto plan = [&](int64_t S_, LaunchCfg* t_) {
+                return W == 0 ? plan_ws(p, (int)S_, G, c->num_sms, t_) : plan_split(p, (int)S_, W, G, c->num_sms, t_);
+            };
             if (key != c->ring_key) {
                 LaunchCfg t;
-                CK(plan_split(p, (int)sring, W, G, c->num_sms, &t));
+                CK(plan(sring, &t));
                 c->ring_ok = t.bps >= kFastMinRows;  // rows in flight per SM
                 int64_t grown = sring;
                 // slack: emission every few halves instead of every half, at the same rows per SM
                 for (int64_t s2 = sring + 128; s2 <= sring + 512 && s2 <= kSplitRingMax; s2 += 128) {
                     LaunchCfg u;
-                    if (plan_split(p, (int)s2, W, G, c->num_sms, &u) != cudaSuccess) break;
+                    if (plan(s2, &u) != cudaSuccess) break;
                     if (u.bps < t.bps) break;
                     grown = s2;
                 }
@@ -358,9 +362,9 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
                 c->ring_S = (int)grown;
             }
             if (c->ring_ok) {
-                split_w = W;
+                split_w = W == 0 ? -1 : W;
                 split_g = G;
-                CK(plan_split(p, c->ring_S, W, G, c->num_sms, &scfg));
+                CK(plan(c->ring_S, &scfg));
             }
         }
     }
@@ -435,11 +439,12 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
     }
     if (split_w) {
         // per-owner bank-balanced copy of B, 16-bit ring byte offsets for this S
+        const int rw = split_w < 0 ? 1 : split_w;  // records per B row
         const int64_t k0 = std::max<int64_t>(0, (int64_t)INT_MAX - bwv[5]);
         const int64_t k1 = std::min<int64_t>(n, (int64_t)bwv[6]);
-        RK(grow(c, c->bt, (size_t)640 * split_g * split_w * n));
-        RK(grow(c, c->bt_nbin, sizeof(int32_t) * (size_t)split_w * n));
-        CK(launch_balance_split(p.B, k0, k1, split_w, split_g, p.S, (unsigned char*)c->bt.p,
+        RK(grow(c, c->bt, (size_t)640 * split_g * rw * n));
+        RK(grow(c, c->bt_nbin, sizeof(int32_t) * (size_t)rw * n));
+        CK(launch_balance_split(p.B, k0, k1, rw, split_g, p.S, (unsigned char*)c->bt.p,
                                 (int32_t*)c->bt_nbin.p, c->num_sms, c->stream));
         c->launches++;
         p.bt = (const unsigned char*)c->bt.p;
@@ -500,7 +505,8 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
     }
     CK(cudaMemsetAsync(p.row_ticket, 0, 8, c->stream));
     if (c->profile) CK(cudaEventRecord(c->ev[4], c->stream));
-    if (split_w) CK(launch_split(p, cfg, c->stream));
+    if (split_w < 0) CK(launch_ws(p, cfg, c->stream));
+    else if (split_w) CK(launch_split(p, cfg, c->stream));
     else CK(launch_row_op(p, cfg, c->stream));
     if (c->profile) {
         CK(cudaEventRecord(c->ev[5], c->stream));
@@ -746,7 +752,7 @@ int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
             c->sp2_loop = (int)v;
             return ELLPACK_OK;
         case ELLPACK_OPT_RING_KERNEL:
-            if (v > 3) return ELLPACK_ERR_ARG;
+            if (v > 4) return ELLPACK_ERR_ARG;
             c->ring_kernel = (int)v;
             c->ring_key = -1;
             return ELLPACK_OK;
@@ -786,7 +792,8 @@ int ellpack_ctx_last_launch(ellpack_ctx c, int32_t out[8]) {
     out[5] = (int32_t)g.smem;
     out[6] = g.bps;
     out[7] = c->last_hB;
-    out[0] = c->last_split ? 2 : c->last_fast;  // 2: split-row ring kernel (out[3] = W warps per row)
+    // 3: warp-specialized ring kernel, 2: split-row ring kernel (out[3] = W warps per row)
+    out[0] = c->last_split < 0 ? 3 : (c->last_split ? 2 : c->last_fast);
     return ELLPACK_OK;
 }
 

@@ -124,6 +124,9 @@ cudaError_t launch_sp2_ctl(Sp2Dev* dev, const double* sums, const int32_t* statu
 cudaError_t plan_split(const RowOpParams& p, int S, int W, int G, int num_sms, LaunchCfg* cfg);
 cudaError_t launch_split(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s);
 size_t split_row_smem(int S, int W, bool has_old);
+// the warp-specialized ring kernel (accumulator warp + emitter warp per row, W = 1 records)
+cudaError_t plan_ws(const RowOpParams& p, int S, int G, int num_sms, LaunchCfg* cfg);
+cudaError_t launch_ws(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s);
 cudaError_t launch_balance_split(KMat b, int64_t k0, int64_t k1, int W, int G, int S, unsigned char* bt,
                                  int32_t* bt_nbin, int num_sms, cudaStream_t s);
 

@@ -546,6 +546,427 @@ __global__ void __launch_bounds__(32 * W, 6) row_split_kernel(const RowOpParams 
     }
 }
 
+// ------------------------------------------------------- warp-specialized ring kernel (WS)
+//
+// One CTA per output row in flight, two warps: the ACCUMULATOR warp walks A_i and applies every
+// B row to the ring (one warp per row: the full 123-entry records keep the bank balance of the
+// one-warp kernel), the EMITTER warp turns finished 128-column blocks into output (combine with
+// Old, drop, compact, write) and clears them. Emission -- half of the one-warp kernel's
+// instructions -- then overlaps accumulation instead of interrupting it.
+//
+// The ring's NB = S / 128 regions (block b of the row lives in region b mod NB) are handed over
+// with mbarriers: the accumulator arrives on full[r] when block b is final (every later k has
+// k - hB >= 128 (b + 1)), the emitter arrives on empty[r] after emitting it. Before touching
+// block b the accumulator waits until the block that last used region r was emitted. Blocks are
+// acquired, released and emitted in ascending order (across rows too), so with the live window
+// of a step (33 blocks for hB = 2048) below NB every wait is on a block already released: no
+// deadlock. Row headers (row, first block, end block) travel through a 4-entry queue with its own
+// full/empty mbarriers; a header with row -1 ends the emitter.
+constexpr int kWsStage = 64;
+constexpr int kWsHQ = 4;
+
+__host__ __device__ inline size_t ws_smem_bytes(int S, bool has_old) {
+    // acc[S + 16] f64 | stage[kWsStage] 16 B | full[NB], empty[NB] u64 | hq[4] 16 B | hfull[4], hempty[4] u64
+    // | flags[S] u8
+    const int NB = S / 128;
+    return (size_t)(S + kSplitTrash) * 8 + (size_t)kWsStage * 16 + (size_t)NB * 16 + kWsHQ * 16 + kWsHQ * 16 +
+           (has_old ? (size_t)S : 0);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(a), "r"(parity) : "memory");
+}
+
+struct WsSmem {
+    uint32_t acc, stg, full, empty, hq, hfull, hempty, flg;
+    int NB;
+};
+
+// Emitter: one block [F, F + 128) of row i (ring slots sF ..), Old merged first.
+template <int MODE, bool A1>
+__device__ __forceinline__ void ws_emit_block(const RowOpParams& p, const WsSmem& sm, int lane, int64_t i, int F,
+                                              int sF, const int32_t* o_col, const double* o_val, int nOld,
+                                              int& old_cur, double* __restrict__ crow_v, int32_t* __restrict__ crow_c,
+                                              int& kept, double& ds, double& dc, double& nrm) {
+    const double tau = p.tau;
+    const unsigned lt = (1u << lane) - 1u;
+    const int cw = p.C.w;
+    if ((int64_t)F <= i && i < (int64_t)F + 128 && lane == ((int)i & 31))
+        ds = lds64(sm.acc + 8u * (uint32_t)(sF + (int)(i - F)));
+    if (MODE != 0) {
+        SplitSmem<1> s1;
+        s1.acc = sm.acc;
+        s1.flg = sm.flg;
+        split_merge_old<1, MODE>(p, s1, lane, 0, F + 128, F, sF, o_col, o_val, nOld, old_cur, nrm);
+    }
+    double x[4];
+    unsigned m[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t off = (uint32_t)(sF + 32 * q + lane);
+        const double v = lds64_clear(sm.acc + 8u * off);
+        bool flagged = false;
+        if (MODE != 0) {
+            flagged = lds8(sm.flg + off) != 0;
+            sts8(sm.flg + off, 0u);
+        }
+        x[q] = v;
+        if (!flagged) {
+            if (!A1) x[q] = __dmul_rn(p.alpha, v);
+            if (MODE == 2) nrm = __fma_rn(v, v, nrm);
+        }
+        m[q] = __ballot_sync(FULL, fabs(x[q]) > tau);
+    }
+    const bool room = kept + 128 <= cw;
+    const uint64_t bv = opaque_u64((uint64_t)crow_v), bc = opaque_u64((uint64_t)crow_c);
+    int before = kept;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const bool keep = (m[q] >> lane) & 1u;
+        const uint32_t pos = (uint32_t)before + (uint32_t)__popc(m[q] & lt);
+        const int col = F + 32 * q + lane;
+        st_entry(keep && (room || pos < (uint32_t)cw), reinterpret_cast<double*>(bv + 8ull * pos),
+                 reinterpret_cast<int32_t*>(bc + 4ull * pos), x[q], col);
+        if ((int64_t)col == i) dc = keep ? x[q] : 0.0;
+        before += __popc(m[q]);
+    }
+    kept = before;
+}
+
+template <int MODE>
+__device__ __forceinline__ void ws_emitter(const RowOpParams& p, const WsSmem& sm, int lane) {
+    const int S = p.S;
+    uint64_t e_par = 0;  // per region: parity of the next full-phase to wait for
+    int32_t my_max_kept = 0, my_ovf = 0;
+    for (int q = 0;; ++q) {
+        const int h = q % kWsHQ;
+        mbar_wait(sm.hfull + 8u * h, (uint32_t)((q / kWsHQ) & 1));
+        long long i;
+        int F0, Fend;
+        asm volatile("ld.shared.s64 %0, [%1];" : "=l"(i) : "r"(sm.hq + 16u * h) : "memory");
+        F0 = lds32i(sm.hq + 16u * h + 8u);
+        Fend = lds32i(sm.hq + 16u * h + 12u);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(sm.hempty + 8u * h);
+        if (i < 0) break;
+        const double* o_val = nullptr;
+        const int32_t* o_col = nullptr;
+        int nOld = 0;
+        if (MODE != 0) {
+            o_val = p.Old.val + (size_t)i * p.Old.w;
+            o_col = p.Old.col + (size_t)i * p.Old.w;
+            nOld = p.Old.nnz[i];
+        }
+        double* crow_v = p.C.val + (size_t)i * p.C.w;
+        int32_t* crow_c = p.C.col + (size_t)i * p.C.w;
+        int kept = 0, old_cur = 0;
+        double ds = 0.0, dc = 0.0, nrm = 0.0;
+        for (int F = F0; F < Fend; F += 128) {
+            const int b = F >> 7;
+            const int r = b % sm.NB;
+            mbar_wait(sm.full + 8u * r, (uint32_t)((e_par >> r) & 1u));
+            e_par ^= 1ull << r;
+            const int sF = r * 128;  // F mod S (S = 128 NB)
+            if (p.alpha == 1.0)
+                ws_emit_block<MODE, true>(p, sm, lane, i, F, sF, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept,
+                                          ds, dc, nrm);
+            else
+                ws_emit_block<MODE, false>(p, sm, lane, i, F, sF, o_col, o_val, nOld, old_cur, crow_v, crow_c, kept,
+                                           ds, dc, nrm);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(sm.empty + 8u * r);
+        }
+        (void)S;
+        ds = warp_sum(ds);
+        dc = warp_sum(dc);
+        if (MODE == 2 && p.normsq) nrm = warp_sum(nrm);
+        if (lane == 0) {
+            p.C.nnz[i] = kept < p.C.w ? kept : p.C.w;
+            if (p.diag_c) p.diag_c[i] = dc;
+            if (p.diag_s) p.diag_s[i] = ds;
+            if (MODE == 2 && p.normsq) p.normsq[i] = nrm;
+        }
+        if (p.diag_a) {
+            const double* a_val = p.A.val + (size_t)i * p.A.w;
+            const int32_t* a_col = p.A.col + (size_t)i * p.A.w;
+            const int nA = (p.alpha != 0.0) ? p.A.nnz[i] : 0;
+            double dA = 0.0;
+            bool has = false;
+            for (int t = lane; t < nA; t += 32)
+                if (a_col[t] == (int)i) { dA = a_val[t]; has = true; }
+            const unsigned mm = __ballot_sync(FULL, has);
+            dA = mm ? __shfl_sync(FULL, dA, __ffs(mm) - 1) : 0.0;
+            if (lane == 0) p.diag_a[i] = dA;
+        }
+        my_max_kept = max(my_max_kept, kept);
+        if (kept > p.C.w) ++my_ovf;
+    }
+    if (lane == 0) {
+        if (my_ovf) atomicAdd(p.status + 0, my_ovf);
+        if (my_max_kept) atomicMax(p.status + 1, my_max_kept);
+    }
+}
+
+// Accumulator: the ring sweep of row_split (W = 1) without emission; blocks are acquired before
+// the steps that may touch them and released once final.
+template <int G, int HB>
+struct WsAcc {
+    const RowOpParams& p;
+    const WsSmem& sm;
+    int lane;
+    uint64_t used = 0, par = 0;  // per region: used before, parity of the next empty-phase to wait for
+    int acq = -1;                // highest acquired block
+    int rel = 0;                 // next block to release
+    int endb = 0;                // one past the row's last block
+    __device__ WsAcc(const RowOpParams& p_, const WsSmem& sm_, int lane_) : p(p_), sm(sm_), lane(lane_) {}
+    __device__ __forceinline__ void acquire_to(int b) {
+        if (b >= endb) b = endb - 1;
+        while (acq < b) {
+            ++acq;
+            const int r = acq % sm.NB;
+            if ((used >> r) & 1ull) {
+                mbar_wait(sm.empty + 8u * r, (uint32_t)((par >> r) & 1ull));
+                par ^= 1ull << r;
+            } else {
+                used |= 1ull << r;
+            }
+        }
+    }
+    __device__ __forceinline__ void release_below(int b) {  // every block < b is final
+        if (b > endb) b = endb;
+        if (rel >= b) return;
+        acquire_to(b - 1);  // (blocks no product touched are still handed over: zeroed, owned)
+        __syncwarp();
+        if (lane == 0)
+            for (int q = rel; q < b; ++q) mbar_arrive(sm.full + 8u * (uint32_t)(q % sm.NB));
+        rel = b;
+    }
+};
+
+template <int G, int HB>
+__device__ __forceinline__ void ws_accumulate_row(const RowOpParams& p, WsAcc<G, HB>& A, int lane,
+                                                  const int32_t* a_col, const double* a_val, int nA, int F0) {
+    constexpr int kPiece = kWsStage - 2 * HB + 1;
+    constexpr int RS = 640 * G;
+    const int hB = p.hB;
+    const WsSmem& sm = A.sm;
+    const uint32_t acc = sm.acc, stg = sm.stg;
+    const unsigned char* __restrict__ btl = p.bt;
+    const uint64_t pol = l2_evict_last_policy();
+    const int NB = sm.NB;
+    uint32_t ro[2][HB][G];
+    double2 rv[2][HB][G];
+    auto get = [&](int t, double& a, int& k, int& nb) {
+        unsigned long long x, y;
+        asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(stg + 16u * t) : "memory");
+        a = __longlong_as_double((long long)x);
+        k = (int)(uint32_t)y;
+        nb = (int)(y >> 32);
+    };
+    auto burst = [&](auto Xc, int h) {
+        constexpr int X = decltype(Xc)::value;
+#pragma unroll
+        for (int e = 0; e < HB; ++e) {
+            double a_u;
+            int k_u, nb;
+            get(h * HB + e, a_u, k_u, nb);
+            const unsigned char* __restrict__ rp = btl + (size_t)(uint32_t)k_u * RS;
+            const unsigned char* __restrict__ sp = rp + 4 * lane;
+            const unsigned char* __restrict__ vp = rp + 16 * lane;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                if (g == 0) { ldg_keep_u32_if<0>(nb > 0, sp, pol, ro[X][e][0]); ldg_keep_d2_if<128 * G>(nb > 0, vp, pol, rv[X][e][0]); }
+                if (g == 1) { ldg_keep_u32_if<128>(nb > 4, sp, pol, ro[X][e][1]); ldg_keep_d2_if<128 * G + 512>(nb > 4, vp, pol, rv[X][e][1]); }
+                if (g == 2) { ldg_keep_u32_if<256>(nb > 8, sp, pol, ro[X][e][2]); ldg_keep_d2_if<128 * G + 1024>(nb > 8, vp, pol, rv[X][e][2]); }
+                if (g == 3) { ldg_keep_u32_if<384>(nb > 12, sp, pol, ro[X][e][3]); ldg_keep_d2_if<128 * G + 1536>(nb > 12, vp, pol, rv[X][e][3]); }
+            }
+        }
+    };
+    auto step = [&](int X, int e, double a, int nb) {
+        double old[G][2];
+        bool gl[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            gl[g] = nb > 4 * g;
+            old[g][0] = lds64_if(gl[g], acc + (ro[X][e][g] & 0xffffu));
+            old[g][1] = lds64_if(gl[g], acc + (ro[X][e][g] >> 16));
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            sts64_if(gl[g], acc + (ro[X][e][g] & 0xffffu), __fma_rn(a, rv[X][e][g].x, old[g][0]));
+            sts64_if(gl[g], acc + (ro[X][e][g] >> 16), __fma_rn(a, rv[X][e][g].y, old[g][1]));
+        }
+        __syncwarp();
+    };
+    // floor((k - hB) / 128) for k - hB possibly negative: blocks below it are final before step k
+    auto fin = [&](int k) { return (k - hB) >= 0 ? ((k - hB) >> 7) : -1; };
+    auto half = [&](auto Xc, int h) {
+        constexpr int X = decltype(Xc)::value;
+        double a_[HB];
+        int k_[HB], nb_[HB];
+#pragma unroll
+        for (int e = 0; e < HB; ++e) get(h * HB + e, a_[e], k_[e], nb_[e]);
+        if (nb_[0] > 0) sts32i(acc + 8u * (uint32_t)p.S, (int)ro[X][0][0]);  // touch: waits for this burst
+        const int kf = k_[0], kl = k_[HB - 1];
+        A.release_below(fin(kf));
+        const int top = (kl + hB) >> 7;
+        __syncwarp();
+        burst(std::integral_constant<int, X ^ 1>{}, h + 1);
+        if (top < A.rel + NB) {
+            A.acquire_to(top);
+#pragma unroll
+            for (int e = 0; e < HB; ++e) step(X, e, a_[e], nb_[e]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < HB; ++e) {
+                A.release_below(fin(k_[e]));
+                A.acquire_to((k_[e] + hB) >> 7);
+                step(X, e, a_[e], nb_[e]);
+            }
+        }
+    };
+    for (int p0 = 0; p0 < nA; p0 += kPiece) {
+        const int cnt = min(kPiece, nA - p0);
+        const int nh = (cnt + HB - 1) / HB;
+        for (int q = lane; q < (nh + 1) * HB; q += 32) {
+            int k, nb;
+            double a;
+            if (q < cnt) {
+                k = a_col[p0 + q];
+                nb = __ldg(p.bt_nbin + k);
+                a = a_val[p0 + q];
+            } else {
+                k = a_col[p0 + cnt - 1];
+                nb = 0;
+                a = 0.0;
+            }
+            const unsigned long long knb = (unsigned long long)(uint32_t)k | ((unsigned long long)(uint32_t)nb << 32);
+            asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(stg + 16u * q), "l"(__double_as_longlong(a)),
+                         "l"(knb) : "memory");
+        }
+        __syncwarp();
+        burst(std::integral_constant<int, 0>{}, 0);
+        for (int h = 0; h < nh; h += 2) {
+            half(std::integral_constant<int, 0>{}, h);
+            if (h + 1 < nh) half(std::integral_constant<int, 1>{}, h + 1);
+        }
+    }
+    (void)F0;
+}
+
+// next ticket of row_chunk rows (lane 0 takes it, the warp gets it)
+__device__ __forceinline__ int64_t ws_next_row(const RowOpParams& p, int lane) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(p.row_ticket, 1ull);
+    return (int64_t)__shfl_sync(FULL, t, 0);
+}
+
+template <int G, int HB, int MODE>
+__global__ void __launch_bounds__(64, 6) row_ws_kernel(const RowOpParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int S = p.S;
+    WsSmem sm;
+    sm.NB = S / 128;
+    sm.acc = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    sm.stg = sm.acc + (uint32_t)((S + kSplitTrash) * 8);
+    sm.full = sm.stg + (uint32_t)(kWsStage * 16);
+    sm.empty = sm.full + 8u * (uint32_t)sm.NB;
+    sm.hq = sm.empty + 8u * (uint32_t)sm.NB;
+    sm.hfull = sm.hq + 16u * kWsHQ;
+    sm.hempty = sm.hfull + 8u * kWsHQ;
+    sm.flg = sm.hempty + 8u * kWsHQ;
+    for (int jj = 2 * (int)threadIdx.x; jj < S + kSplitTrash; jj += 128) sts128(sm.acc + 8u * jj, 0.0, 0.0);
+    if (MODE != 0)
+        for (int jj = 4 * (int)threadIdx.x; jj < S; jj += 256) sts32i(sm.flg + jj, 0);
+    if (threadIdx.x == 0) {
+        for (int r = 0; r < sm.NB; ++r) {
+            mbar_init(sm.full + 8u * r, 1);
+            mbar_init(sm.empty + 8u * r, 1);
+        }
+        for (int h = 0; h < kWsHQ; ++h) {
+            mbar_init(sm.hfull + 8u * h, 1);
+            mbar_init(sm.hempty + 8u * h, 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (wid == 1) {
+        ws_emitter<MODE>(p, sm, lane);
+        return;
+    }
+    // accumulator warp
+    WsAcc<G, HB> A(p, sm, lane);
+    const int hB = p.hB;
+    const int ncols = (int)p.ncols;
+    const int chunk = p.row_chunk;
+    int q = 0;  // headers sent
+    auto send = [&](long long i, int F0, int Fend) {
+        const int h = q % kWsHQ;
+        if (q >= kWsHQ) mbar_wait(sm.hempty + 8u * h, (uint32_t)(((q / kWsHQ) - 1) & 1));
+        if (lane == 0) {
+            asm volatile("st.shared.s64 [%0], %1;" ::"r"(sm.hq + 16u * h), "l"(i) : "memory");
+            sts32i(sm.hq + 16u * h + 8u, F0);
+            sts32i(sm.hq + 16u * h + 12u, Fend);
+            mbar_arrive(sm.hfull + 8u * h);
+        }
+        __syncwarp();
+        ++q;
+    };
+    for (int64_t i0 = p.row_begin + chunk * ws_next_row(p, lane); i0 < p.row_end;
+         i0 = p.row_begin + chunk * ws_next_row(p, lane)) {
+        for (int64_t i = i0; i < i0 + chunk && i < p.row_end; ++i) {
+            const double* a_val = p.A.val + (size_t)i * p.A.w;
+            const int32_t* a_col = p.A.col + (size_t)i * p.A.w;
+            const int nA = (p.alpha != 0.0) ? p.A.nnz[i] : 0;
+            int lo_col = INT_MAX, hi_col = -1;
+            if (nA > 0) {
+                lo_col = max(0, a_col[0] - hB);
+                hi_col = min(ncols - 1, a_col[nA - 1] + hB);
+            }
+            if (MODE != 0) {
+                const int nOld = p.Old.nnz[i];
+                if (nOld > 0) {
+                    const int32_t* o_col = p.Old.col + (size_t)i * p.Old.w;
+                    lo_col = min(lo_col, o_col[0]);
+                    hi_col = max(hi_col, o_col[nOld - 1]);
+                }
+            }
+            if (hi_col < lo_col) {
+                send(i, 0, 0);
+                continue;
+            }
+            const int F0 = lo_col & ~127, Fend = (hi_col + 128) & ~127;
+            send(i, F0, Fend);
+            A.acq = (F0 >> 7) - 1;
+            A.rel = F0 >> 7;
+            A.endb = Fend >> 7;
+            ws_accumulate_row<G, HB>(p, A, lane, a_col, a_val, nA, F0);
+            A.release_below(A.endb);
+        }
+    }
+    send(-1, 0, 0);
+}
+
+template <int MODE, typename Fn>
+static void ws_dispatch(int G, Fn f) {
+    switch (G) {
+        case 1: f(row_ws_kernel<1, 3, MODE>); break;
+        case 2: f(row_ws_kernel<2, 2, MODE>); break;
+        case 3: f(row_ws_kernel<3, 1, MODE>); break;
+        default: f(row_ws_kernel<4, 1, MODE>); break;
+    }
+}
+
 // -------------------------------------------------------------------------- dispatch
 
 template <typename K>
@@ -619,6 +1040,43 @@ cudaError_t launch_split(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_
         else if (mode == 1) split_launch_wm<1, 1>(G, p, cfg.grid, cfg.smem, s);
         else split_launch_wm<1, 2>(G, p, cfg.grid, cfg.smem, s);
     }
+    return cudaGetLastError();
+}
+
+template <int MODE>
+static cudaError_t ws_prep_m(int G, size_t smem, int* bps) {
+    cudaError_t e = cudaSuccess;
+    ws_dispatch<MODE>(G, [&](auto k) { e = split_prep(k, 64, smem, bps); });
+    return e;
+}
+
+cudaError_t plan_ws(const RowOpParams& p, int S, int G, int num_sms, LaunchCfg* cfg) {
+    if (S % 128 || S / 128 > 64 || G < 1 || G > 4) return cudaErrorInvalidValue;
+    const size_t smem = ws_smem_bytes(S, p.old_mode != 0);
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    int bps = 0;
+    const int mode = split_mode_of(p);
+    cudaError_t e = mode == 0 ? ws_prep_m<0>(G, smem, &bps) : mode == 1 ? ws_prep_m<1>(G, smem, &bps)
+                                                                    : ws_prep_m<2>(G, smem, &bps);
+    if (e) return e;
+    if (bps < 1) return cudaErrorInvalidConfiguration;
+    cfg->S = S;
+    cfg->R = G;
+    cfg->warps_per_cta = 2;
+    cfg->smem = smem;
+    cfg->bps = bps;
+    const int64_t rows = p.row_end - p.row_begin;
+    const int64_t full = (int64_t)bps * num_sms;
+    cfg->grid = (int)(rows < full ? (rows > 0 ? rows : 1) : full);
+    return cudaSuccess;
+}
+
+cudaError_t launch_ws(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s) {
+    const int mode = split_mode_of(p);
+    auto go = [&](auto k) { k<<<cfg.grid, 64, cfg.smem, s>>>(p); };
+    if (mode == 0) ws_dispatch<0>(cfg.R, go);
+    else if (mode == 1) ws_dispatch<1>(cfg.R, go);
+    else ws_dispatch<2>(cfg.R, go);
     return cudaGetLastError();
 }
 

@@ -12,10 +12,10 @@ from tests.test_gpu_parity import FAST, _compare_sp2, eb, up
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [1, 2, 3]
+KERNELS = [1, 2, 3, 4]
 
 
-@pytest.fixture(scope="module", params=KERNELS, ids=lambda k: {1: "legacy", 2: "split_w1", 3: "split_w2"}[k])
+@pytest.fixture(scope="module", params=KERNELS, ids=lambda k: {1: "legacy", 2: "split_w1", 3: "split_w2", 4: "ws"}[k])
 def kctx(request, ellpack_lib):
     c = ellpack_lib.Context(0)
     c.set_option(ellpack_lib.OPT_RING_KERNEL, request.param)
@@ -39,7 +39,7 @@ def test_ring_kernels_multiply_bitwise(kctx, case, alpha, beta, tau):
     g = up(C0.widened(wo))
     assert ctx.multiply(up(A), up(B), g, alpha, beta, tau) == eb().OK
     # in place with beta != 0 (C is also the Old operand, rows stashed): the legacy ring kernel
-    assert ctx.last_launch()["path"] == ("ring" if rk == 1 or beta != 0.0 else "split")
+    assert ctx.last_launch()["path"] == ("ring" if rk == 1 or beta != 0.0 else ("ws" if rk == 4 else "split"))
     assert same_bits(g.to_host(), Co)
     if lit.status != oracle.OK:
         g2 = up(C0.widened(w))
