@@ -6,9 +6,10 @@ Headline (BASELINE.json configs[4], the largest single-GPU multiply, on which th
     cfg5: X^2 of a random banded symmetric X, N=262144, M=256, tau=1e-5, FP64.
 A "step" = one ellpack_multiply_x2 call (fused row kernel: window pre-pass, gather-accumulate,
 drop/compact/write, trace partials; canonical trace reduction; status read-back) -- SURVEY §8a
-rows a0..a4. With N > 1 ranks a step is the band-aware halo exchange of X's rows (NCCL send/recv
-of exactly the rows the rank's own rows reference, §8f-f1; BJ north_star (3)) followed by the
-multiply of the rank's own rows (strong scaling: total work fixed).
+rows a0..a4. With N > 1 ranks a step is ellpack_multiply_x2_halo: the band-aware halo exchange of
+X's rows (NCCL send/recv of exactly the rows the rank's own rows reference, §8f-f1; BJ north_star
+(3)) on a second stream while the rank's interior rows are computed, then its boundary rows
+(strong scaling: total work fixed).
 
 The same line carries the rest of BASELINE.json's metric ("SP2 iterations/sec at 1/2/4/8") and the
 other configs' timings as sub-objects: "sp2" (cfg3 K = 10 and cfg4 K = 6 windows, SURVEY §8d "SP2
@@ -506,7 +507,9 @@ def run_ours(args):
 
     def step():
         if ws > 1:
-            ctx.halo_rows(x)  # the rows of X this rank's rows reference (band-aware halo, §8f-f1)
+            # the rows of X this rank's rows reference travel by NCCL on a second stream while the
+            # interior rows are computed (band-aware halo overlapped, §8f-f1)
+            return ctx.multiply_x2_halo(x, y, tau)
         return ctx.multiply_x2(x, y, tau)
 
     for _ in range(max(3, args.warmup)):

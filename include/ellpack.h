@@ -342,6 +342,23 @@ int ellpack_allgather_rows(ellpack_ctx ctx, ellpack_desc* m);
  * only the final iterate. */
 int ellpack_halo_rows(ellpack_ctx ctx, const ellpack_desc* a, ellpack_desc* b);
 
+/* X2 <- drop_tau(X*X) for this rank's rows when X holds only this rank's block valid (as an SP2
+ * iterate or a row-distributed input does): the band-aware halo of X (the rows of other ranks this
+ * rank's rows reference, ellpack_halo_rows) travels by NCCL on a second stream WHILE the interior
+ * rows -- rows i with [i - h, i + h] inside the rank's block, h the all-reduced half-bandwidth of
+ * X's rows -- are computed from the rank's own rows; the boundary rows follow once the halo is in
+ * (SURVEY §8f-f1 "exchange that halo ... while computing interior rows whose k's are all local").
+ * Traces and status as ellpack_multiply_x2; X's halo rows are received into X. Without a
+ * communicator nothing is exchanged (X must then hold every row the block references) and the
+ * rows are computed in the same interior / boundary launches. Errors as ellpack_multiply_x2. */
+int ellpack_multiply_x2_halo(ellpack_ctx ctx, ellpack_desc* x, ellpack_desc* x2, double threshold,
+                             double* trace_x, double* trace_x2);
+
+/* The row split of ellpack_multiply_x2_halo (host only): block [r0, r1), half-bandwidth h ->
+ * out[0..1] interior rows [i0, i1) = [min(r1, r0 + h), max(i0, r1 - h)), out[2..3] and out[4..5]
+ * the boundary rows [r0, i0) and [i1, r1). Errors: ARG. */
+int ellpack_row_split(int64_t r0, int64_t r1, int64_t h, int64_t out[6]);
+
 /* The halo plan (host only, no context; the same function both sides of every pair evaluate):
  * equal contiguous blocks of `per` rows (block q = [q per, min(n, (q+1) per))) and every rank's
  * referenced rows need[2q] .. need[2q+1] (inclusive; need[2q] > need[2q+1] = none). This rank

@@ -44,6 +44,7 @@ ABI_SYMBOLS = (
     "ellpack_trace", "ellpack_fnorm_diff", "ellpack_gershgorin", "ellpack_overflow_info", "sp2_run",
     "sp2_opts_default", "ellpack_multiply_x2_host", "ellpack_nccl_unique_id", "ellpack_ctx_attach_nccl",
     "ellpack_ctx_set_rows", "ellpack_allgather_rows", "ellpack_halo_rows", "ellpack_halo_plan",
+    "ellpack_multiply_x2_halo", "ellpack_row_split",
     "ellpack_strerror",
 )
 
@@ -143,6 +144,7 @@ def lib() -> ctypes.CDLL:
             "ellpack_nccl_unique_id": [P], "ellpack_ctx_attach_nccl": [P, i, i, P, i64, i64],
             "ellpack_ctx_set_rows": [P, i64, i64], "ellpack_allgather_rows": [P, D],
             "ellpack_halo_rows": [P, D, D], "ellpack_halo_plan": [i64, i32, i32, i64, P, P, P, P, P],
+            "ellpack_multiply_x2_halo": [P, D, D, d, P, P], "ellpack_row_split": [i64, i64, i64, P],
             "ellpack_strerror": [i],
         }
         for name, args in sig.items():
@@ -384,6 +386,13 @@ class Context:
         _chk(lib().ellpack_ctx_attach_nccl(self._h, nranks, rank, buf, row_begin, row_end),
              "ellpack_ctx_attach_nccl")
 
+    def multiply_x2_halo(self, x: Mat, x2: Mat, threshold: float, ok=(OK, ERR_OVERFLOW)):
+        """X^2 of this rank's rows with the halo exchange of X overlapped with the interior rows (f1)."""
+        tx, tx2 = ctypes.c_double(math.nan), ctypes.c_double(math.nan)
+        st = _chk(lib().ellpack_multiply_x2_halo(self._h, x.ref(), x2.ref(), threshold, ctypes.byref(tx),
+                                                 ctypes.byref(tx2)), "ellpack_multiply_x2_halo", ok)
+        return st, tx.value, tx2.value
+
     def allgather_rows(self, m: Mat):
         _chk(lib().ellpack_allgather_rows(self._h, m.ref()), "ellpack_allgather_rows")
 
@@ -404,6 +413,13 @@ def halo_plan(n: int, nranks: int, rank: int, per: int, need):
                                  ctypes.byref(nr), rcv.ctypes.data), "ellpack_halo_plan")
     return ([tuple(int(x) for x in snd[3 * k:3 * k + 3]) for k in range(ns.value)],
             [tuple(int(x) for x in rcv[3 * k:3 * k + 3]) for k in range(nr.value)])
+
+
+def row_split(r0: int, r1: int, h: int):
+    """ellpack_row_split (host only): (interior, lower boundary, upper boundary) row ranges."""
+    out = (ctypes.c_int64 * 6)()
+    _chk(lib().ellpack_row_split(r0, r1, h, out), "ellpack_row_split")
+    return (out[0], out[1]), (out[2], out[3]), (out[4], out[5])
 
 
 def row_partition(n: int, nranks: int, align: int = 256):

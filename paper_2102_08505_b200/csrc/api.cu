@@ -15,6 +15,7 @@
 
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only: ranges are no-ops unless a profiler is attached
 
 #include <algorithm>
 #include <chrono>
@@ -58,6 +59,7 @@ struct NcclApi {
     ncclResult_t (*GroupEnd)() = nullptr;
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
 };
 
 NcclApi g_nccl;
@@ -81,6 +83,7 @@ bool load_nccl() {
     LOADSYM(GroupEnd, "ncclGroupEnd");
     LOADSYM(Send, "ncclSend");
     LOADSYM(Recv, "ncclRecv");
+    LOADSYM(CommGetAsyncError, "ncclCommGetAsyncError");
 #undef LOADSYM
     g_nccl.ok = true;
     return true;
@@ -151,6 +154,10 @@ struct ellpack_ctx_s {
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     // row-kernel profiling (ELLPACK_OPT_PROFILE)
     bool profile = false, prof_pending = false;
+    int prof_n = 0;                                    // row-kernel launches awaiting collection
+    cudaEvent_t pev[4][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+    cudaStream_t side = nullptr;                       // halo exchange beside the interior rows (f1)
+    cudaEvent_t sev[2] = {nullptr, nullptr};
     double prof_ms = 0.0;
     int64_t prof_launches = 0;
 };
@@ -182,8 +189,20 @@ int from_cuda(cudaError_t e) {
 int host_sync(ellpack_ctx c) {
     c->host_syncs++;
     CK(cudaStreamSynchronize(c->stream));
+    if (c->comm) {
+        // a failed or aborted communicator (peer lost, network error) surfaces here, not as a hang
+        ncclResult_t ae = ncclSuccess;
+        if (g_nccl.CommGetAsyncError(c->comm, &ae) != ncclSuccess || ae != ncclSuccess) return ELLPACK_ERR_NCCL;
+    }
     return ELLPACK_OK;
 }
+
+// NVTX range over a scope (the paper's phase names), visible in nsys / ncu timelines
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    void next(const char* name) { nvtxRangePop(); nvtxRangePushA(name); }  // the next phase
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 // With a communicator every operand must be the N x N matrix the ranks' blocks partition.
 int check_comm_n(ellpack_ctx c, int64_t n) {
@@ -302,8 +321,18 @@ int enqueue_probe(ellpack_ctx c, const RowOpParams& p, int64_t n) {
 // emission). Wider rows use the multi-pass general path.
 // alloc_upper (nullable): called when a launch takes the symmetric (upper-triangle) route, to
 // provide p.C_upper; a NOMEM there falls back to whole rows (c->sym_nomem = 1).
+// Per-launch extras of a row op split into several launches (the halo-overlapped multiply, f1):
+// which B rows the balance pass prepares (nbal ranges [k0, k1); default: every row the launch's A
+// rows reference) and whether the status block accumulates over the previous launch.
+struct RowOpExtra {
+    int nbal = -1;
+    int64_t bal[4] = {0, 0, 0, 0};
+    bool keep_status = false;
+};
+
 int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw = nullptr,
-                   int (*alloc_upper)(ellpack_ctx, void*, KOut*) = nullptr, void* alloc_arg = nullptr) {
+                   int (*alloc_upper)(ellpack_ctx, void*, KOut*) = nullptr, void* alloc_arg = nullptr,
+                   const RowOpExtra* ex = nullptr) {
     p.ncols = n;
     const bool has_old = p.old_mode != 0;
     if (!bw) {
@@ -444,9 +473,14 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
         const int64_t k1 = std::min<int64_t>(n, (int64_t)bwv[6]);
         RK(grow(c, c->bt, (size_t)640 * split_g * rw * n));
         RK(grow(c, c->bt_nbin, sizeof(int32_t) * (size_t)rw * n));
-        CK(launch_balance_split(p.B, k0, k1, rw, split_g, p.S, (unsigned char*)c->bt.p,
-                                (int32_t*)c->bt_nbin.p, c->num_sms, c->stream));
-        c->launches++;
+        const int nbal = ex && ex->nbal >= 0 ? ex->nbal : 1;
+        for (int q = 0; q < nbal; ++q) {
+            const int64_t b0 = ex && ex->nbal >= 0 ? ex->bal[2 * q] : k0;
+            const int64_t b1 = ex && ex->nbal >= 0 ? ex->bal[2 * q + 1] : k1;
+            CK(launch_balance_split(p.B, b0, b1, rw, split_g, p.S, (unsigned char*)c->bt.p,
+                                    (int32_t*)c->bt_nbin.p, c->num_sms, c->stream));
+            c->launches++;
+        }
         p.bt = (const unsigned char*)c->bt.p;
         p.bt_nbin = (const int32_t*)c->bt_nbin.p;
         p.bt_w = 64 * split_g;
@@ -460,9 +494,14 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
         // exchange did not deliver are never read)
         const int64_t k0 = std::max<int64_t>(0, (int64_t)INT_MAX - bwv[5]);
         const int64_t k1 = std::min<int64_t>(n, (int64_t)bwv[6]);
-        CK(launch_balance(p.B, k0, k1, wt, p.S, (unsigned char*)c->bt.p, (int32_t*)c->bt_nbin.p, c->num_sms,
-                          c->stream));
-        c->launches++;
+        const int nbal = ex && ex->nbal >= 0 ? ex->nbal : 1;
+        for (int q = 0; q < nbal; ++q) {
+            const int64_t b0 = ex && ex->nbal >= 0 ? ex->bal[2 * q] : k0;
+            const int64_t b1 = ex && ex->nbal >= 0 ? ex->bal[2 * q + 1] : k1;
+            CK(launch_balance(p.B, b0, b1, wt, p.S, (unsigned char*)c->bt.p, (int32_t*)c->bt_nbin.p,
+                              c->num_sms, c->stream));
+            c->launches++;
+        }
         p.bt = (const unsigned char*)c->bt.p;
         p.bt_nbin = (const int32_t*)c->bt_nbin.p;
         p.bt_w = wt;
@@ -494,7 +533,7 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
         }
     }
     p.status = c->d_status;
-    CK(cudaMemsetAsync(c->d_status, 0, 2 * sizeof(int32_t), c->stream));
+    if (!(ex && ex->keep_status)) CK(cudaMemsetAsync(c->d_status, 0, 2 * sizeof(int32_t), c->stream));
     p.row_ticket = c->d_keys + 3;  // d_keys[3]: the fast kernel's row counter
     {
         // rows per ticket: 4 (fewer atomics, neighbouring rows share B records in L2) unless the
@@ -504,12 +543,14 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
         p.row_chunk = rows >= 64 * in_flight ? 4 : 1;
     }
     CK(cudaMemsetAsync(p.row_ticket, 0, 8, c->stream));
-    if (c->profile) CK(cudaEventRecord(c->ev[4], c->stream));
+    const int pk = c->prof_n < 4 ? c->prof_n : 3;
+    if (c->profile) CK(cudaEventRecord(c->pev[pk][0], c->stream));
     if (split_w < 0) CK(launch_ws(p, cfg, c->stream));
     else if (split_w) CK(launch_split(p, cfg, c->stream));
     else CK(launch_row_op(p, cfg, c->stream));
     if (c->profile) {
-        CK(cudaEventRecord(c->ev[5], c->stream));
+        CK(cudaEventRecord(c->pev[pk][1], c->stream));
+        c->prof_n = pk + 1;
         c->prof_pending = true;
     }
     c->launches++;
@@ -520,9 +561,12 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
 void prof_collect(ellpack_ctx c) {
     if (!c->prof_pending) return;
     float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]) == cudaSuccess) {
-        c->prof_ms += ms;
-        c->prof_launches++;
+    for (int q = 0; q < c->prof_n; ++q) {
+        if (cudaEventElapsedTime(&ms, c->pev[q][0], c->pev[q][1]) == cudaSuccess) c->prof_ms += ms;
+    }
+    c->prof_n = 0;
+    {
+        c->prof_launches++;  // one multiply (its row-kernel launches summed)
     }
     c->prof_pending = false;
 }
@@ -703,6 +747,10 @@ int ellpack_ctx_create(int device, void* stream, ellpack_ctx* out) {
     if (!e) e = cudaMalloc(&c->d_bw, 64);
     if (!e) e = cudaMallocHost(&c->h, sizeof(ellpack_ctx_s::Host));
     for (int k = 0; k < 6 && !e; ++k) e = cudaEventCreate(&c->ev[k]);
+    for (int k = 0; k < 4 && !e; ++k) {
+        e = cudaEventCreate(&c->pev[k][0]);
+        if (!e) e = cudaEventCreate(&c->pev[k][1]);
+    }
     if (e) { ellpack_ctx_destroy(c); return from_cuda(e); }
     *out = c;
     return ELLPACK_OK;
@@ -728,6 +776,10 @@ int ellpack_ctx_destroy(ellpack_ctx c) {
     if (c->h) cudaFreeHost(c->h);
     if (c->h_reach) cudaFreeHost(c->h_reach);
     for (int k = 0; k < 6; ++k) if (c->ev[k]) cudaEventDestroy(c->ev[k]);
+    for (int k = 0; k < 4; ++k)
+        for (int q = 0; q < 2; ++q) if (c->pev[k][q]) cudaEventDestroy(c->pev[k][q]);
+    for (int q = 0; q < 2; ++q) if (c->sev[q]) cudaEventDestroy(c->sev[q]);
+    if (c->side) cudaStreamDestroy(c->side);
     delete c;
     return ELLPACK_OK;
 }
@@ -772,6 +824,7 @@ int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
             c->prof_ms = 0.0;
             c->prof_launches = 0;
             c->prof_pending = false;
+            c->prof_n = 0;
             return ELLPACK_OK;
         default: return ELLPACK_ERR_ARG;
     }
@@ -861,6 +914,7 @@ int ellpack_multiply(ellpack_ctx c, const ellpack_desc* a, const ellpack_desc* b
     RK(check_comm_n(c, a->n));
     if (!valid_tau(tau) || !std::isfinite(alpha) || !std::isfinite(beta)) return ELLPACK_ERR_ARG;
     if (same(cm, a) || same(cm, b)) return ELLPACK_ERR_ARG;
+    NvtxRange nv("ellpack_multiply");
     CK(cudaSetDevice(c->device));
     if (beta != 0.0) RK(validate_inputs(c, {a, b, cm})); else RK(validate_inputs(c, {a, b}));
     RowOpParams p = base_params(c, a->n);
@@ -890,6 +944,7 @@ int ellpack_multiply_x2(ellpack_ctx c, const ellpack_desc* x, ellpack_desc* x2, 
     RK(check_comm_n(c, x->n));
     if (!valid_tau(tau)) return ELLPACK_ERR_ARG;
     if (same(x, x2)) return ELLPACK_ERR_ARG;
+    NvtxRange nv("ellpack_multiply_x2 (SP2 Loop X2)");
     CK(cudaSetDevice(c->device));
     RK(validate_inputs(c, {x}));
     const int64_t n = x->n;
@@ -1564,6 +1619,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     const double t_start = now_s();
 
     // ---- Init Misc: bounds, X0, tr(X0)
+    NvtxRange phase("SP2 Init Misc");
     double emin = o.emin, emax = o.emax;
     if (std::isnan(emin) || std::isnan(emax)) RK(gershgorin_impl(c, h, &emin, &emax));
     R.emin = emin;
@@ -1648,6 +1704,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     if ((rc = fetch(c, 0, true))) { cleanup(); return rc; }
     take_probe(c, bwX, needX);
     const double t_init_end = now_s();
+    phase.next("SP2 Loop (X2 + Norm + Misc)");
 
     // ---- SP2 loop
     // One host synchronisation per iteration: the step's status, traces, norm, product count,
@@ -1848,6 +1905,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
         if (stop >= 0) { ++it; break; }
     }
     const double t_loop_end = now_s();
+    phase.next("SP2 final iterate");
     R.iterations = it;
     R.final_width = X.owned ? wx : 0;
     R.trD = trX;
@@ -1877,6 +1935,120 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     R.t_sp2_loop_misc = (t_loop_end - t_init_end) - t_x2 - t_norm;
     if (rep) *rep = R;
     return status;
+}
+
+int ellpack_row_split(int64_t r0, int64_t r1, int64_t h, int64_t out[6]) {
+    if (!out || r0 < 0 || r1 < r0 || h < 0) return ELLPACK_ERR_ARG;
+    const int64_t i0 = std::min(r1, r0 + h), i1 = std::max(i0, r1 - h);
+    out[0] = i0;  // interior [i0, i1): every column within [r0, r1)
+    out[1] = i1;
+    out[2] = r0;  // boundary [r0, i0) and [i1, r1)
+    out[3] = i0;
+    out[4] = i1;
+    out[5] = r1;
+    return ELLPACK_OK;
+}
+
+int ellpack_multiply_x2_halo(ellpack_ctx c, ellpack_desc* x, ellpack_desc* x2, double tau, double* trace_x,
+                             double* trace_x2) {
+    if (!c) return ELLPACK_ERR_ARG;
+    RK(check_desc(x));
+    RK(check_desc(x2));
+    if (x->n != x2->n) return ELLPACK_ERR_DIM;
+    RK(check_comm_n(c, x->n));
+    if (!valid_tau(tau)) return ELLPACK_ERR_ARG;
+    if (same(x, x2)) return ELLPACK_ERR_ARG;
+    NvtxRange nv("ellpack_multiply_x2_halo (halo || interior rows, then boundary rows)");
+    CK(cudaSetDevice(c->device));
+    RK(validate_inputs(c, {x}));
+    const int64_t n = x->n;
+    int64_t r0, r1;
+    rows_of(c, n, &r0, &r1);
+    RK(grow(c, c->rows[0], sizeof(double) * n));
+    RK(grow(c, c->rows[1], sizeof(double) * n));
+    // 1. the probe of this rank's rows (maxima all-reduced, reaches all-gathered): one read-back
+    RK(enqueue_next_probe(c, x));
+    RK(fetch(c, 0, true));
+    int32_t bwv[kProbe];
+    std::vector<int64_t> need(2 * (size_t)c->nranks);
+    take_probe(c, bwv, need);
+    int64_t sp[6];
+    RK(ellpack_row_split(r0, r1, bwv[0], sp));
+    const int64_t k0 = std::max<int64_t>(0, (int64_t)INT_MAX - bwv[5]);
+    const int64_t k1 = std::min<int64_t>(n, (int64_t)bwv[6]);
+    // 2. the band-aware halo on the side stream, beside the interior rows
+    if (c->comm) {
+        if (!c->side) {
+            CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&c->sev[0], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->sev[1], cudaEventDisableTiming));
+        }
+        CK(cudaEventRecord(c->sev[0], c->stream));
+        CK(cudaStreamWaitEvent(c->side, c->sev[0], 0));
+        cudaStream_t main = c->stream;
+        c->stream = c->side;
+        const int rc = halo_exec(c, x, need.data());
+        c->stream = main;
+        RK(rc);
+        CK(cudaEventRecord(c->sev[1], c->side));
+    }
+    RowOpParams p = base_params(c, n);
+    p.A = kmat(x);
+    p.B = kmat(x);
+    p.C = kout(x2);
+    p.alpha = 1.0;
+    p.tau = tau;
+    p.diag_a = (double*)c->rows[0].p;
+    p.diag_s = (double*)c->rows[1].p;
+    bool any = false;
+    // 3. interior rows: every B row they reference is this rank's own
+    if (sp[0] < sp[1]) {
+        RowOpParams q = p;
+        q.row_begin = sp[0];
+        q.row_end = sp[1];
+        RowOpExtra ex;
+        ex.nbal = 1;
+        ex.bal[0] = std::max(k0, r0);
+        ex.bal[1] = std::min(k1, r1);
+        RK(enqueue_row_op(c, q, n, bwv, nullptr, nullptr, &ex));
+        any = true;
+    }
+    // 4. boundary rows, once the halo rows are in
+    if (c->comm) CK(cudaStreamWaitEvent(c->stream, c->sev[1], 0));
+    for (int b = 0; b < 2; ++b) {
+        const int64_t b0 = sp[2 + 2 * b], b1 = sp[3 + 2 * b];
+        if (b0 >= b1) continue;
+        RowOpParams q = p;
+        q.row_begin = b0;
+        q.row_end = b1;
+        RowOpExtra ex;
+        ex.keep_status = any;
+        if (!any) {  // nothing balanced yet: every referenced row
+            ex.nbal = 1;
+            ex.bal[0] = k0;
+            ex.bal[1] = k1;
+        } else if (b == 0 || sp[2] >= sp[3]) {  // the halo rows, once
+            ex.nbal = 2;
+            ex.bal[0] = k0;
+            ex.bal[1] = std::max(k0, std::min(k1, r0));
+            ex.bal[2] = std::min(k1, std::max(k0, r1));
+            ex.bal[3] = k1;
+        } else {
+            ex.nbal = 0;
+        }
+        RK(enqueue_row_op(c, q, n, bwv, nullptr, nullptr, &ex));
+        any = true;
+    }
+    if (!any) CK(cudaMemsetAsync(c->d_status, 0, 2 * sizeof(int32_t), c->stream));
+    // 5. traces from this rank's rows (canonical partials all-gathered), status all-reduced
+    const double* arrs[2] = {p.diag_a, p.diag_s};
+    RK(enqueue_canonical(c, arrs, 2, n));
+    RK(reduce_status(c));
+    RK(fetch(c, 2));
+    RK(finish_status(c));
+    if (trace_x) *trace_x = c->h->sums[0];
+    if (trace_x2) *trace_x2 = c->h->sums[1];
+    return ELLPACK_OK;
 }
 
 int ellpack_multiply_x2_host(ellpack_ctx c, int64_t n, int32_t wx, const double* xv, const int32_t* xc,

@@ -33,7 +33,19 @@
 
 namespace ell {
 
-constexpr int kSplitStage = 64;  // A-row steps staged per warp (16 B each)
+#ifndef ELL_SPLIT_STAGE
+#define ELL_SPLIT_STAGE 64
+#endif
+#ifndef ELL_SPLIT_META
+#define ELL_SPLIT_META 1  // W = 1: the next half's step metadata read into registers one half ahead
+#endif
+#ifndef ELL_SPLIT_HB_G3
+#define ELL_SPLIT_HB_G3 2  // W = 1, G = 3: steps per register half
+#endif
+#ifndef ELL_SPLIT_HB_G2
+#define ELL_SPLIT_HB_G2 3
+#endif
+constexpr int kSplitStage = ELL_SPLIT_STAGE;  // A-row steps staged per warp (16 B each)
 constexpr int kSplitTrash = 16;  // trash slots S .. S + 15 (one per bank pair) for padding lanes
 
 __host__ __device__ inline size_t split_smem_bytes(int S, int W, bool has_old) {
@@ -350,7 +362,11 @@ __device__ __forceinline__ void row_split(const RowOpParams& p, const SplitSmem<
 
     uint32_t ro[2][HB][G];
     double2 rv[2][HB][G];
-    // step metadata (a_ik, k, NB of this warp's sub-record), re-read from the stage where used
+    // step metadata (a_ik, k, NB of this warp's sub-record): W = 1 keeps the next half's in
+    // registers, read one half ahead (ELL_SPLIT_META); W = 2 re-reads it from the stage where used
+    constexpr bool kMeta = ELL_SPLIT_META && W == 1;
+    double am[2][HB];
+    int km[2][HB], nbm[2][HB];
     auto get = [&](int t, double& a, int& k, int& nb) {
         unsigned long long x, y;
         asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(stg + 16u * t) : "memory");
@@ -358,13 +374,19 @@ __device__ __forceinline__ void row_split(const RowOpParams& p, const SplitSmem<
         k = (int)(uint32_t)y;
         nb = (int)(y >> 32);
     };
+    auto meta = [&](auto Xc, int h) {
+        constexpr int X = decltype(Xc)::value;
+#pragma unroll
+        for (int e = 0; e < HB; ++e) get(h * HB + e, am[X][e], km[X][e], nbm[X][e]);
+    };
     auto burst = [&](auto Xc, int h) {
         constexpr int X = decltype(Xc)::value;
 #pragma unroll
         for (int e = 0; e < HB; ++e) {
             double a_u;
             int k_u, nb;
-            get(h * HB + e, a_u, k_u, nb);
+            if (kMeta) { k_u = km[X][e]; nb = nbm[X][e]; }
+            else get(h * HB + e, a_u, k_u, nb);
             const unsigned char* __restrict__ rp = btl + (size_t)(uint32_t)k_u * (W * RS);
             const unsigned char* __restrict__ sp = rp + 4 * lane;
             const unsigned char* __restrict__ vp = rp + 16 * lane;
@@ -397,8 +419,14 @@ __device__ __forceinline__ void row_split(const RowOpParams& p, const SplitSmem<
         constexpr int X = decltype(Xc)::value;
         double a_[HB];
         int k_[HB], nb_[HB];
+        if (kMeta) {
 #pragma unroll
-        for (int e = 0; e < HB; ++e) get(h * HB + e, a_[e], k_[e], nb_[e]);
+            for (int e = 0; e < HB; ++e) { a_[e] = am[X][e]; k_[e] = km[X][e]; nb_[e] = nbm[X][e]; }
+            meta(std::integral_constant<int, X ^ 1>{}, h + 1);
+        } else {
+#pragma unroll
+            for (int e = 0; e < HB; ++e) get(h * HB + e, a_[e], k_[e], nb_[e]);
+        }
         if (nb_[0] > 0) sts32i(acc + 8u * (uint32_t)S, (int)ro[X][0][0]);  // touch: waits for this burst
         const int kf = k_[0], kl = k_[HB - 1];
         if (kf + hB >= R.F + S) split_emit_to<W, MODE>(p, sm, lane, wid, R, (kf - hB) & ~127, o_col, o_val, nOld,
@@ -438,6 +466,7 @@ __device__ __forceinline__ void row_split(const RowOpParams& p, const SplitSmem<
                          "l"(knb) : "memory");
         }
         __syncwarp();
+        if (kMeta) meta(std::integral_constant<int, 0>{}, 0);
         burst(std::integral_constant<int, 0>{}, 0);
         for (int h = 0; h < nh; h += 2) {
             half(std::integral_constant<int, 0>{}, h);
@@ -982,8 +1011,8 @@ static void split_dispatch(int G, Fn f) {
     // two-warp CTAs per SM, 168 registers per thread
     switch (G) {
         case 1: f(row_split_kernel<W, 1, W == 1 ? 4 : 3, MODE>); break;
-        case 2: f(row_split_kernel<W, 2, W == 1 ? 3 : 2, MODE>); break;
-        case 3: f(row_split_kernel<W, 3, W == 1 ? 2 : 1, MODE>); break;
+        case 2: f(row_split_kernel<W, 2, W == 1 ? ELL_SPLIT_HB_G2 : 2, MODE>); break;
+        case 3: f(row_split_kernel<W, 3, W == 1 ? ELL_SPLIT_HB_G3 : 1, MODE>); break;
         default: f(row_split_kernel<W, 4, W == 1 ? 2 : 1, MODE>); break;
     }
 }

@@ -234,3 +234,52 @@ def test_sp2_device_loop_syncs_do_not_grow_with_iterations(ellpack_lib):
         assert same_bits(d.to_host(), o.D)
         ctx.close()
     assert syncs[16] == syncs[4], syncs
+
+
+# --------------------------------------- f1: halo exchange overlapped with the interior rows
+
+@pytest.mark.parametrize("nranks", [1, 2, 4, 8])
+@pytest.mark.parametrize("m,kernel", [(64, 0), (256, 0), (64, 1)])
+def test_multiply_x2_halo_interior_boundary_bitwise(ellpack_lib, nranks, m, kernel):
+    """ellpack_multiply_x2_halo splits a rank's block into interior rows (computed while the halo
+    travels) and boundary rows (after it): emulated ranks (ellpack_ctx_set_rows) on one GPU, every
+    ring kernel, the union of the blocks bitwise the one-rank product (§8c-c12)."""
+    E = ellpack_lib
+    n = 32768
+    X = synth.cfg5(n, m)
+    w = {64: 864, 256: 5248}[m]
+    full = E.Context(0)
+    y1 = E.Mat.empty(n, w)
+    st, tx, tx2 = full.multiply_x2(up(X), y1, 1e-5)
+    assert st == E.OK
+    full.close()
+    x = up(X)
+    yp = E.Mat.empty(n, w)
+    for (r0, r1) in E.row_partition(n, nranks):
+        c = E.Context(0)
+        if kernel:
+            c.set_option(E.OPT_RING_KERNEL, kernel)
+        if nranks > 1:
+            c.set_rows(r0, r1)
+        st, tx_h, tx2_h = c.multiply_x2_halo(x, yp, 1e-5)
+        assert st == E.OK
+        if nranks == 1:
+            assert (tx_h, tx2_h) == (tx, tx2)
+        c.close()
+    assert same_bits(yp.to_host(), y1.to_host())
+
+
+def test_multiply_x2_halo_one_rank_communicator(ellpack_lib):
+    import torch  # noqa: F401
+    E = ellpack_lib
+    n = 4096
+    X = synth.cfg5(n, 64)
+    Y = synth.Ell.empty(n, 1024)
+    r = oracle.x2(X, Y, 1e-5)
+    ctx = E.Context(0)
+    ctx.attach_nccl(1, 0, E.Context.nccl_unique_id(), 0, n)
+    y = E.Mat.empty(n, 1024)
+    st, tx, tx2 = ctx.multiply_x2_halo(up(X), y, 1e-5)
+    assert st == E.OK and (tx, tx2) == (r.trace_x, r.trace_x2)
+    assert same_bits(y.to_host(), Y)
+    ctx.close()

@@ -184,6 +184,73 @@ def test_halo_exchange_plan_gloo(ws, n, m):
     tmp.spawn(_halo_worker, args=(ws, _free_port(), n, m, 1e-5), nprocs=ws, join=True)
 
 
+def _split_worker(rank, ws, port, n, m, tau):
+    """§8f-f1 overlap: the interior rows of a rank's block (ellpack_row_split with the all-reduced
+    half-bandwidth) reference only the rank's own rows, so they are computed BEFORE the halo arrives
+    from the own block alone; the boundary rows, computed after it, reference only own + received
+    rows; both phases reproduce the full result bit for bit and together cover the block."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(ws),
+                      LOCAL_RANK=str(rank))
+    sys.path.insert(0, ROOT)
+    import oracle
+    import synth
+    import paper_2102_08505_b200 as eb
+    from paper_2102_08505_b200 import multirank as mr
+
+    oracle.set_threads(1)
+    dist = mr.init_process_group("gloo")
+    r0, r1 = mr.rank_rows(n, ws, rank)
+    X = synth.cfg5(n, m)
+    rows = [i for i in range(r0, r1) if X.nnz[i] > 0]
+    h_mine = max(max(i - int(X.col[i, 0]), int(X.col[i, X.nnz[i] - 1]) - i) for i in rows)
+    h = int(mr.max_over_ranks(h_mine))
+    (i0, i1), (l0, l1), (u0, u1) = eb.row_split(r0, r1, h)
+    assert l0 == r0 and l1 == i0 and u0 == i1 and u1 == r1 and i0 <= i1
+    own = synth.Ell.empty(n, X.w)
+    own.val[r0:r1], own.col[r0:r1], own.nnz[r0:r1] = X.val[r0:r1], X.col[r0:r1], X.nnz[r0:r1]
+    for i in range(i0, i1):  # interior: every referenced row is the rank's own
+        k = int(X.nnz[i])
+        assert k == 0 or (r0 <= X.col[i, 0] and X.col[i, k - 1] < r1)
+    need = (min(int(X.col[i, 0]) for i in rows), max(int(X.col[i, X.nnz[i] - 1]) for i in rows))
+    needs = [None] * ws
+    dist.all_gather_object(needs, need)
+    _, recvs = eb.halo_plan(n, ws, rank, r1 - r0, needs)
+    have = set(range(r0, r1))
+    for _, t0, t1 in recvs:
+        have |= set(range(t0, t1))
+    halo = own.copy()
+    for _, t0, t1 in recvs:  # what the exchange delivers
+        halo.val[t0:t1], halo.col[t0:t1], halo.nnz[t0:t1] = X.val[t0:t1], X.col[t0:t1], X.nnz[t0:t1]
+
+    def rows_of_product(B, a, b):
+        A = synth.Ell.empty(n, X.w)
+        A.val[a:b], A.col[a:b], A.nnz[a:b] = X.val[a:b], X.col[a:b], X.nnz[a:b]
+        out = synth.Ell.empty(n, n)
+        oracle.multiply(A, B, out, 1.0, 0.0, tau)
+        return out
+
+    full = rows_of_product(X, r0, r1)
+    phase1 = rows_of_product(own, i0, i1)          # before the halo: own rows only
+    for a, b in ((l0, l1), (u0, u1)):
+        for i in range(a, b):                      # boundary rows: own + received suffice
+            k = int(X.nnz[i])
+            assert all(int(j) in have for j in X.col[i, :k])
+    phase2 = rows_of_product(halo, r0, r1)         # after it (boundary rows; interior too)
+    for i in range(r0, r1):
+        got = phase1 if i0 <= i < i1 else phase2
+        k = int(full.nnz[i])
+        assert got.nnz[i] == k
+        assert np.array_equal(got.col[i, :k], full.col[i, :k])
+        assert np.array_equal(got.val[i, :k].view(np.uint64), full.val[i, :k].view(np.uint64))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws,n,m", [(2, 4096, 32), (4, 4096, 16)])
+def test_interior_boundary_row_split_gloo(ws, n, m):
+    tmp.spawn(_split_worker, args=(ws, _free_port(), n, m, 1e-5), nprocs=ws, join=True)
+
+
 def test_halo_plan_rejects_bad_arguments():
     sys.path.insert(0, ROOT)
     import paper_2102_08505_b200 as eb
