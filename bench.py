@@ -64,7 +64,7 @@ def peaks():
 def kernel_src_sha() -> str:
     """Hash of the row-kernel source: an ncu capture is only quoted for the kernel it measured."""
     h = hashlib.sha256()
-    for f in ("spgemm.cu", "internal.cuh"):
+    for f in ("spgemm.cu", "split.cu", "internal.cuh", "devutil.cuh"):
         h.update(open(os.path.join(ROOT, "paper_2102_08505_b200", "csrc", f), "rb").read())
     return h.hexdigest()[:16]
 
@@ -381,15 +381,21 @@ def time_sp2(eb, mr, dev, ws, rank, cfg: int, K: int, steps: int, warmup: int):
     return out
 
 
-def time_sp2_small(eb, dev, reps: int):
-    """SP2 on a cfg1-sized H (BASELINE configs[0]'s matrix, N = 512, as the Hamiltonian; nocc = N/2,
-    tau = 1e-5, tol = 1e-8, to the stop rule): us per iteration with the host loop (one host
-    synchronisation per iteration) and with the device-resident loop (one CUDA-graph launch per run,
-    SURVEY §8f-f3), the same bits either way."""
+def time_sp2_small(eb, dev, reps: int, which: str = "cfg1"):
+    """SP2 on a cfg1-sized H, to the stop rule (nocc = N/2, tau = 1e-5, tol = 1e-8): us per iteration
+    with the host loop (one host synchronisation per iteration) and with the device-resident loop
+    (one CUDA-graph launch per run), the same bits either way. which = "cfg1":
+    BASELINE configs[0]'s matrix (N = 512) as H -- gapless, its iterates fill the 512 x 512 matrix, so
+    an iteration is a dense-ish 512^3 product; "soft_matter": the paper's gapped soft-matter model H
+    at N = 512, whose iterates stay sparse -- the launch-latency-bound case."""
     import torch
-    H = synth.cfg1()
+    if which == "cfg1":
+        H = synth.cfg1()
+        out = {"workload": "SP2 on cfg1's X as H: N=512 nocc=256 tau=1e-05 tol=1e-08, to the stop rule"}
+    else:
+        H = synth.model_hamiltonian(512, "soft_matter", tau_store=1e-5)
+        out = {"workload": "SP2 on the soft-matter model H: N=512 nocc=256 tau=1e-05 tol=1e-08, to the stop rule"}
     n = H.n
-    out = {"workload": "SP2 on cfg1's X as H: N=512 nocc=256 tau=1e-05 tol=1e-08, to the stop rule"}
     ref = None
     for name, loop in (("host_loop", 1), ("device_loop", 2)):
         ctx = eb.Context(dev)
@@ -595,7 +601,8 @@ def run_ours(args):
         sp2 = {"cfg3": time_sp2(eb, mr, dev, ws, rank, 3, 10, 3, 1),
                "cfg4": time_sp2(eb, mr, dev, ws, rank, 4, 6, 2, 1)}
         if ws == 1:
-            sp2["cfg1_sized"] = time_sp2_small(eb, dev, 20)
+            sp2["cfg1_sized"] = time_sp2_small(eb, dev, 20, "cfg1")
+            sp2["soft_matter_512"] = time_sp2_small(eb, dev, 50, "soft_matter")
         cfg1 = time_cfg1(eb, dev, 300) if ws == 1 else {"skipped": "N=512 is not divisible into 256-row blocks (R17)"}
         cfg2 = time_cfg2(eb, mr, dev, ws, rank, 10)
 

@@ -306,7 +306,7 @@ int enqueue_probe(ellpack_ctx c, const RowOpParams& p, int64_t n) {
     const KMat none{nullptr, nullptr, nullptr, 0};
     const int64_t b0 = c->comm ? p.row_begin : 0, b1 = c->comm ? p.row_end : n;
     CK(launch_bandwidth(p.alpha != 0.0 ? p.A : none, p.B, has_old ? p.Old : none, p.row_begin, p.row_end,
-                        b0, b1, n, c->d_bw, c->stream));
+                        b0, b1, n, c->ring_kernel == 3, c->d_bw, c->stream));
     c->launches++;
     if (c->comm) NK(g_nccl.AllReduce(c->d_bw, c->d_bw, 5, ncclInt32, ncclMax, c->comm, c->stream));
     return ELLPACK_OK;
@@ -695,6 +695,82 @@ int halo_desc(ellpack_ctx c, const ellpack_desc* a, ellpack_desc* b) {
     RK(host_sync(c));
     std::vector<int64_t> needl(need.begin(), need.end());
     return halo_exec(c, b, needl.data());
+}
+
+// The halo of `b` (need: every rank's referenced rows) sent and received on the side stream, after
+// everything already on the context stream; sev[1] marks its completion. With a communicator only.
+int start_halo(ellpack_ctx c, ellpack_desc* b, const int64_t* need) {
+    if (!c->side) {
+        CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->sev[0], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->sev[1], cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(c->sev[0], c->stream));
+    CK(cudaStreamWaitEvent(c->side, c->sev[0], 0));
+    cudaStream_t main = c->stream;
+    c->stream = c->side;
+    const int rc = halo_exec(c, b, need);
+    c->stream = main;
+    RK(rc);
+    CK(cudaEventRecord(c->sev[1], c->side));
+    return ELLPACK_OK;
+}
+
+// One row op over this rank's rows [r0, r1) in up to three launches (§8f-f1): the interior rows --
+// [r0 + h, r1 - h), h = the all-reduced half-bandwidth of A (bwv[0]), whose B rows are all the
+// rank's own -- first; then, once the halo started by start_halo is in (halo = true: the context
+// stream waits for sev[1]), the boundary rows [r0, r0 + h) and [r1 - h, r1). The balance pass of
+// the ring paths prepares the own B rows for the interior launch and the halo rows for the
+// boundary ones; the status block accumulates over the launches.
+int enqueue_row_op_split(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bwv, bool halo) {
+    const int64_t r0 = p.row_begin, r1 = p.row_end;
+    int64_t sp[6];
+    RK(ellpack_row_split(r0, r1, bwv[0], sp));
+    const int64_t k0 = std::max<int64_t>(0, (int64_t)INT_MAX - bwv[5]);
+    const int64_t k1 = std::min<int64_t>(n, (int64_t)bwv[6]);
+    bool any = false;
+    if (sp[0] < sp[1]) {
+        RowOpParams q = p;
+        q.row_begin = sp[0];
+        q.row_end = sp[1];
+        RowOpExtra ex;
+        ex.nbal = 1;
+        ex.bal[0] = std::max(k0, r0);
+        ex.bal[1] = std::max(ex.bal[0], std::min(k1, r1));
+        RK(enqueue_row_op(c, q, n, bwv, nullptr, nullptr, &ex));
+        p.fast = q.fast;
+        any = true;
+    }
+    if (halo) CK(cudaStreamWaitEvent(c->stream, c->sev[1], 0));
+    bool halo_balanced = false;
+    for (int b = 0; b < 2; ++b) {
+        const int64_t b0 = sp[2 + 2 * b], b1 = sp[3 + 2 * b];
+        if (b0 >= b1) continue;
+        RowOpParams q = p;
+        q.row_begin = b0;
+        q.row_end = b1;
+        RowOpExtra ex;
+        ex.keep_status = any;
+        if (!any) {  // nothing balanced yet: every referenced row
+            ex.nbal = 1;
+            ex.bal[0] = k0;
+            ex.bal[1] = k1;
+        } else if (!halo_balanced) {  // the halo rows, once
+            ex.nbal = 2;
+            ex.bal[0] = k0;
+            ex.bal[1] = std::max(k0, std::min(k1, r0));
+            ex.bal[2] = std::min(k1, std::max(k0, r1));
+            ex.bal[3] = k1;
+        } else {
+            ex.nbal = 0;
+        }
+        RK(enqueue_row_op(c, q, n, bwv, nullptr, nullptr, &ex));
+        p.fast = q.fast;
+        any = true;
+        halo_balanced = true;
+    }
+    if (!any) CK(cudaMemsetAsync(c->d_status, 0, 2 * sizeof(int32_t), c->stream));
+    return ELLPACK_OK;
 }
 
 }  // namespace
@@ -1729,6 +1805,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     int stop = -1;
     int it;
     UpperAlloc ua{&U, n, 0};
+    bool halo_pending = false;  // the halo of X_n travels on the side stream (communicator only)
     const bool dev_loop = use_device_loop(c, n, maxw);
     if (dev_loop) {
         // (§8f-f3) the whole loop as one graph launch: zero host synchronisations per iteration
@@ -1782,7 +1859,12 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             p.exec_products = c->d_keys + 4;
             ua.w = Y.d.w;
             cudaEventRecord(c->ev[0], c->stream);
-            if ((rc = enqueue_row_op(c, p, n, bwX, alloc_upper, &ua))) { status = rc; break; }
+            // with a communicator the halo of X_n (started after the previous step) is in flight:
+            // the interior rows run beside it, the boundary rows after it (§8f-f1)
+            if (c->comm) rc = enqueue_row_op_split(c, p, n, bwX, halo_pending);
+            else rc = enqueue_row_op(c, p, n, bwX, alloc_upper, &ua);
+            if (rc) { status = rc; break; }
+            halo_pending = false;
             if (c->sym_nomem) sym_off = true;  // U did not fit: whole rows from now on
             const bool upper = c->last_upper != 0;
             if (upper) {
@@ -1892,7 +1974,10 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
         take_probe(c, bwX, needX);
         // the next step reads only the rows of X_{n+1} its rows reference (band-aware halo, f1),
         // planned from the reaches that arrived with this step's status
-        if (c->comm && (rc = halo_exec(c, &Y.d, needX.data()))) { status = rc; break; }
+        if (c->comm) {
+            if ((rc = start_halo(c, &Y.d, needX.data()))) { status = rc; break; }
+            halo_pending = true;
+        }
         std::swap(X, Y);
         wx = wy;
         trX = trY;
@@ -1906,6 +1991,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     }
     const double t_loop_end = now_s();
     phase.next("SP2 final iterate");
+    if (halo_pending) CK(cudaStreamWaitEvent(c->stream, c->sev[1], 0));  // before D is assembled
     R.iterations = it;
     R.final_width = X.owned ? wx : 0;
     R.trD = trX;
@@ -1972,26 +2058,9 @@ int ellpack_multiply_x2_halo(ellpack_ctx c, ellpack_desc* x, ellpack_desc* x2, d
     int32_t bwv[kProbe];
     std::vector<int64_t> need(2 * (size_t)c->nranks);
     take_probe(c, bwv, need);
-    int64_t sp[6];
-    RK(ellpack_row_split(r0, r1, bwv[0], sp));
-    const int64_t k0 = std::max<int64_t>(0, (int64_t)INT_MAX - bwv[5]);
-    const int64_t k1 = std::min<int64_t>(n, (int64_t)bwv[6]);
     // 2. the band-aware halo on the side stream, beside the interior rows
-    if (c->comm) {
-        if (!c->side) {
-            CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
-            CK(cudaEventCreateWithFlags(&c->sev[0], cudaEventDisableTiming));
-            CK(cudaEventCreateWithFlags(&c->sev[1], cudaEventDisableTiming));
-        }
-        CK(cudaEventRecord(c->sev[0], c->stream));
-        CK(cudaStreamWaitEvent(c->side, c->sev[0], 0));
-        cudaStream_t main = c->stream;
-        c->stream = c->side;
-        const int rc = halo_exec(c, x, need.data());
-        c->stream = main;
-        RK(rc);
-        CK(cudaEventRecord(c->sev[1], c->side));
-    }
+    if (c->comm) RK(start_halo(c, x, need.data()));
+    // 3-4. interior rows now, boundary rows once the halo is in
     RowOpParams p = base_params(c, n);
     p.A = kmat(x);
     p.B = kmat(x);
@@ -2000,46 +2069,7 @@ int ellpack_multiply_x2_halo(ellpack_ctx c, ellpack_desc* x, ellpack_desc* x2, d
     p.tau = tau;
     p.diag_a = (double*)c->rows[0].p;
     p.diag_s = (double*)c->rows[1].p;
-    bool any = false;
-    // 3. interior rows: every B row they reference is this rank's own
-    if (sp[0] < sp[1]) {
-        RowOpParams q = p;
-        q.row_begin = sp[0];
-        q.row_end = sp[1];
-        RowOpExtra ex;
-        ex.nbal = 1;
-        ex.bal[0] = std::max(k0, r0);
-        ex.bal[1] = std::min(k1, r1);
-        RK(enqueue_row_op(c, q, n, bwv, nullptr, nullptr, &ex));
-        any = true;
-    }
-    // 4. boundary rows, once the halo rows are in
-    if (c->comm) CK(cudaStreamWaitEvent(c->stream, c->sev[1], 0));
-    for (int b = 0; b < 2; ++b) {
-        const int64_t b0 = sp[2 + 2 * b], b1 = sp[3 + 2 * b];
-        if (b0 >= b1) continue;
-        RowOpParams q = p;
-        q.row_begin = b0;
-        q.row_end = b1;
-        RowOpExtra ex;
-        ex.keep_status = any;
-        if (!any) {  // nothing balanced yet: every referenced row
-            ex.nbal = 1;
-            ex.bal[0] = k0;
-            ex.bal[1] = k1;
-        } else if (b == 0 || sp[2] >= sp[3]) {  // the halo rows, once
-            ex.nbal = 2;
-            ex.bal[0] = k0;
-            ex.bal[1] = std::max(k0, std::min(k1, r0));
-            ex.bal[2] = std::min(k1, std::max(k0, r1));
-            ex.bal[3] = k1;
-        } else {
-            ex.nbal = 0;
-        }
-        RK(enqueue_row_op(c, q, n, bwv, nullptr, nullptr, &ex));
-        any = true;
-    }
-    if (!any) CK(cudaMemsetAsync(c->d_status, 0, 2 * sizeof(int32_t), c->stream));
+    RK(enqueue_row_op_split(c, p, n, bwv, c->comm != nullptr));
     // 5. traces from this rank's rows (canonical partials all-gathered), status all-reduced
     const double* arrs[2] = {p.diag_a, p.diag_s};
     RK(enqueue_canonical(c, arrs, 2, n));

@@ -95,7 +95,7 @@ cudaError_t launch_balance(KMat b, int64_t k0, int64_t k1, int wt, int S, unsign
 // of b (rows b0..b1); out[4] = max chunk-parity half of those B rows; A's rows r0..r1 reference B rows
 // [INT_MAX - out[5], out[6] - 1] (out[0..6] zeroed by the caller)
 cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int64_t r0, int64_t r1, int64_t b0, int64_t b1, int64_t n,
-                             int32_t* out, cudaStream_t s);
+                             int count_sub, int32_t* out, cudaStream_t s);
 
 // sp2_graph.cu: device-resident SP2 control (§8f-f3). The loop state lives in device memory; a
 // one-thread control kernel at the end of every captured iteration applies the stop rule, the
@@ -165,6 +165,11 @@ cudaError_t launch_count_over(const int32_t* nnz, int64_t r0, int64_t r1, int32_
                               cudaStream_t s);
 cudaError_t launch_max_nnz(const int32_t* nnz, int64_t row_begin, int64_t row_end,
                            int32_t* out, cudaStream_t s);
+
+// Resident CTAs per SM of a kernel at (threads, dynamic smem), memoized per device: the first query
+// raises the kernel's dynamic-shared-memory limit as needed; later calls are a table lookup (the
+// runtime queries cost tens of microseconds, which a cfg1-sized call cannot afford).
+cudaError_t occupancy_cached(const void* kern, int threads, size_t smem, int* bps);
 
 // order-preserving double <-> u64 keys for exact atomic min/max
 __host__ __device__ inline unsigned long long dkey(double x) {

@@ -15,12 +15,23 @@
 
 namespace ell {
 
+// The sequential sum over the block partials (c7 second level), one array at a time: the whole CTA
+// stages the partials in shared memory (independent coalesced loads), then one thread adds them in
+// block order -- the dependent chain runs on shared-memory operands, not on global-load latency.
 __global__ void final_sums_kernel(const double* partials, int narr, int64_t nblocks, double* out) {
-    const int a = threadIdx.x;
-    if (a >= narr) return;
-    double s = 0.0;
-    for (int64_t b = 0; b < nblocks; ++b) s = __dadd_rn(s, partials[(size_t)a * nblocks + b]);
-    out[a] = s;
+    __shared__ double sp[2048];
+    for (int a = 0; a < narr; ++a) {
+        double s = 0.0;
+        for (int64_t b0 = 0; b0 < nblocks; b0 += 2048) {
+            const int cnt = (int)(nblocks - b0 < 2048 ? nblocks - b0 : 2048);
+            __syncthreads();
+            for (int t = threadIdx.x; t < cnt; t += blockDim.x) sp[t] = partials[(size_t)a * nblocks + b0 + t];
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (int t = 0; t < cnt; ++t) s = __dadd_rn(s, sp[t]);
+        }
+        if (threadIdx.x == 0) out[a] = s;
+    }
 }
 
 struct PtrPack { const double* p[8]; };
@@ -59,7 +70,7 @@ cudaError_t launch_block_partials(const double* const* arrays, int narr, int64_t
 
 cudaError_t launch_final_sums(const double* partials, int narr, int64_t nblocks, double* out,
                               cudaStream_t s) {
-    final_sums_kernel<<<1, 32, 0, s>>>(partials, narr, nblocks, out);
+    final_sums_kernel<<<1, 256, 0, s>>>(partials, narr, nblocks, out);
     return cudaGetLastError();
 }
 

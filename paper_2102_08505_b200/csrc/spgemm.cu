@@ -33,7 +33,10 @@
 #include "internal.cuh"
 #include "devutil.cuh"
 #include <climits>
+#include <mutex>
 #include <type_traits>
+#include <utility>
+#include <vector>
 
 namespace ell {
 
@@ -1134,11 +1137,12 @@ __global__ void __launch_bounds__(128, ELL_GEN_MINB) row_general_dyn_kernel(cons
 
 // Half-bandwidth probe: out[m] = max over rows of max(i - col[i][0], col[i][nnz-1] - i) (a and c
 // over rows [r0, r1), b over rows [b0, b1)); out[3] = max nnz of b over [b0, b1); out[4] = max over
-// those B rows of the larger chunk-parity half (the split kernel's sub-rows, W = 2); the B rows the
+// those B rows of the larger chunk-parity half (the split kernel's sub-rows, W = 2; counted only when
+// count_sub, else out[4] = out[3]); the B rows the
 // A rows [r0, r1) reference are [INT_MAX - out[5], out[6] - 1] (zero-initialised maxima of
 // INT_MAX - first column and last column + 1).
 __global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int64_t r0, int64_t r1, int64_t b0, int64_t b1,
-                                 int64_t n, int32_t* out) {
+                                 int64_t n, int count_sub, int32_t* out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int bw[3] = {0, 0, 0};
     int reach[2] = {0, 0};
@@ -1162,7 +1166,7 @@ __global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int64_t r0, int64_t r1,
     int nzb = (i >= b0 && i < b1) ? b.nnz[i] : 0;
     // the larger chunk-parity half of the B row (split kernel, W = 2: columns j with (j >> 5) & 1)
     int sub = nzb;
-    if (nzb > 64 && nzb <= 256) {
+    if (count_sub && nzb > 64 && nzb <= 256) {
         const int32_t* bc = b.col + (size_t)i * b.w;
         int odd = 0;
         for (int q = 0; q < nzb; ++q) odd += (bc[q] >> 5) & 1;
@@ -1178,8 +1182,8 @@ __global__ void bandwidth_kernel(KMat a, KMat b, KMat c, int64_t r0, int64_t r1,
 }
 
 cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int64_t r0, int64_t r1, int64_t b0, int64_t b1, int64_t n,
-                             int32_t* out, cudaStream_t s) {
-    bandwidth_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, c, r0, r1, b0, b1, n, out);
+                             int count_sub, int32_t* out, cudaStream_t s) {
+    bandwidth_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, c, r0, r1, b0, b1, n, count_sub, out);
     return cudaGetLastError();
 }
 
@@ -1322,9 +1326,7 @@ cudaError_t launch_sym_assemble(KMat u, KMat x, KOut y, int64_t r0, int64_t r1, 
 // cfg.R carries G; cfg.R == 0 selects the general kernel.
 template <typename K>
 static cudaError_t prep_kernel(K kern, const LaunchCfg& cfg, int* bps) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
-    if (e) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, kern, cfg.warps_per_cta * 32, cfg.smem);
+    return occupancy_cached((const void*)kern, cfg.warps_per_cta * 32, cfg.smem, bps);
 }
 
 template <int MODE>
@@ -1407,6 +1409,39 @@ cudaError_t launch_row_op(const RowOpParams& p, const LaunchCfg& cfg, cudaStream
     else if (mode == 1) launch_mode<1>(p, cfg, s);
     else launch_mode<2>(p, cfg, s);
     return cudaGetLastError();
+}
+
+cudaError_t occupancy_cached(const void* kern, int threads, size_t smem, int* bps) {
+    struct Ent {
+        const void* k;
+        int dev, threads;
+        size_t smem;
+        int bps;
+    };
+    static std::mutex mu;
+    static std::vector<Ent> tab;                        // (kernel, device, threads, smem) -> CTAs/SM
+    static std::vector<std::pair<const void*, int>> lim;  // (kernel, device) -> smem limit set (bytes)
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e) return e;
+    std::lock_guard<std::mutex> g(mu);
+    for (const Ent& t : tab)
+        if (t.k == kern && t.dev == dev && t.threads == threads && t.smem == smem) {
+            *bps = t.bps;
+            return cudaSuccess;
+        }
+    int have = -1;
+    for (auto& l : lim)
+        if (l.first == kern && (l.second >> 20) == dev) have = l.second & 0xfffff;
+    if (have < (int)smem) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e) return e;
+        lim.push_back({kern, (dev << 20) | (int)smem});
+    }
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, kern, threads, smem);
+    if (e) return e;
+    tab.push_back({kern, dev, threads, smem, *bps});
+    return cudaSuccess;
 }
 
 }  // namespace ell

@@ -37,7 +37,7 @@ namespace ell {
 #define ELL_SPLIT_STAGE 64
 #endif
 #ifndef ELL_SPLIT_META
-#define ELL_SPLIT_META 1  // W = 1: the next half's step metadata read into registers one half ahead
+#define ELL_SPLIT_META 0  // W = 1: the next half's step metadata read into registers one half ahead
 #endif
 #ifndef ELL_SPLIT_HB_G3
 #define ELL_SPLIT_HB_G3 2  // W = 1, G = 3: steps per register half
@@ -591,6 +591,9 @@ __global__ void __launch_bounds__(32 * W, 6) row_split_kernel(const RowOpParams 
 // of a step (33 blocks for hB = 2048) below NB every wait is on a block already released: no
 // deadlock. Row headers (row, first block, end block) travel through a 4-entry queue with its own
 // full/empty mbarriers; a header with row -1 ends the emitter.
+#ifndef ELL_WS_HB_G3
+#define ELL_WS_HB_G3 1
+#endif
 constexpr int kWsStage = 64;
 constexpr int kWsHQ = 4;
 
@@ -991,7 +994,7 @@ static void ws_dispatch(int G, Fn f) {
     switch (G) {
         case 1: f(row_ws_kernel<1, 3, MODE>); break;
         case 2: f(row_ws_kernel<2, 2, MODE>); break;
-        case 3: f(row_ws_kernel<3, 1, MODE>); break;
+        case 3: f(row_ws_kernel<3, ELL_WS_HB_G3, MODE>); break;
         default: f(row_ws_kernel<4, 1, MODE>); break;
     }
 }
@@ -1000,9 +1003,7 @@ static void ws_dispatch(int G, Fn f) {
 
 template <typename K>
 static cudaError_t split_prep(K kern, int threads, size_t smem, int* bps) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, kern, threads, smem);
+    return occupancy_cached((const void*)kern, threads, smem, bps);
 }
 
 template <int W, int MODE, typename Fn>
