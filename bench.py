@@ -420,6 +420,48 @@ def time_sp2_small(eb, dev, reps: int, which: str = "cfg1"):
     return out
 
 
+def time_sweep(eb, dev, reps: int):
+    """BASELINE configs[4]'s sweep, N in {32768, 131072, 262144} x M in {64, 128, 256} (one GPU): per
+    point the X^2 step time (CUDA events around the ABI call), the row kernel's time and its HBM
+    roofline fraction (compulsory bytes / kernel time / measured peak)."""
+    import torch
+    hbm_peak, _ = peaks()
+    out = []
+    for n in (32768, 131072, 262144):
+        for m in (64, 128, 256):
+            X = synth.cfg5(n, m)
+            ctx = eb.Context(dev)
+            x = eb.Mat.from_host(X)
+            y = eb.Mat.empty(n, m)
+            st, _, _ = ctx.multiply_x2(x, y, TAU5)
+            w = round_up32(ctx.overflow_info()[1]) if st == eb.ERR_OVERFLOW else m
+            del y
+            y = eb.Mat.empty(n, w)
+            for _ in range(2):
+                ctx.multiply_x2(x, y, TAU5)
+            torch.cuda.synchronize()
+            ctx.set_option(eb.OPT_PROFILE, 1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                ctx.multiply_x2(x, y, TAU5)
+            e1.record()
+            torch.cuda.synchronize()
+            kms, kn = ctx.kernel_time()
+            kms /= max(kn, 1)
+            ms = e0.elapsed_time(e1) / reps
+            P = synth.products(X, X)
+            Bc = x2_bytes(live_entries(X), int(y.nnz.sum().item()), n)
+            launch = ctx.last_launch()
+            out.append({"n": n, "m": m, "out_width": w, "ms_per_step": ms, "kernel_ms": kms,
+                        "gflops": 2.0 * P / (ms * 1e-3) / 1e9, "hbm_frac": Bc / (kms * 1e-3) / 1e9 / hbm_peak,
+                        "path": launch["path"], "G": launch["G"], "S": launch["S"], "rows_per_sm": launch["ctas_per_sm"]})
+            ctx.close()
+            del x, y
+            torch.cuda.empty_cache()
+    return out
+
+
 def time_cfg1(eb, dev, reps: int):
     """cfg1 (N = 512): us per ellpack_multiply_x2 call (incl. its status read-back), host clock over
     back-to-back calls, plus the device time of the same calls by CUDA events."""
@@ -596,7 +638,7 @@ def run_ours(args):
     torch.cuda.empty_cache()
 
     # ---- the rest of the metric: SP2 windows, cfg1 latency, cfg2
-    sp2 = cfg1 = cfg2 = None
+    sp2 = cfg1 = cfg2 = sweep = None
     if not args.quick:
         sp2 = {"cfg3": time_sp2(eb, mr, dev, ws, rank, 3, 10, 3, 1),
                "cfg4": time_sp2(eb, mr, dev, ws, rank, 4, 6, 2, 1)}
@@ -604,6 +646,7 @@ def run_ours(args):
             sp2["cfg1_sized"] = time_sp2_small(eb, dev, 20, "cfg1")
             sp2["soft_matter_512"] = time_sp2_small(eb, dev, 50, "soft_matter")
         cfg1 = time_cfg1(eb, dev, 300) if ws == 1 else {"skipped": "N=512 is not divisible into 256-row blocks (R17)"}
+        sweep = time_sweep(eb, dev, 5) if ws == 1 else None
         cfg2 = time_cfg2(eb, mr, dev, ws, rank, 10)
 
     # ---- CPU oracle beside it (rank 0, N=1 only, bounded sample)
@@ -637,7 +680,7 @@ def run_ours(args):
                          "kernel": kname, "launch": launch, "kernel_ms_avg": kern_avg,
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "lsu_pipe": lsu_pipe},
-            "sp2": sp2, "cfg1": cfg1, "cfg2": cfg2,
+            "sp2": sp2, "cfg1": cfg1, "cfg2": cfg2, "cfg5_sweep": sweep,
             "ranks_bitwise_vs_1": ranks_checked,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -36,19 +36,28 @@ __global__ void final_sums_kernel(const double* partials, int narr, int64_t nblo
 
 struct PtrPack { const double* p[8]; };
 
+// One 256-row block of one array per 32-thread group: the lanes stage the block's values in shared
+// memory with coalesced loads, then lane 0 adds them in row order (c7 first level: the dependent
+// chain runs on shared-memory operands, not on global-load latency).
 __global__ void block_partials_pack_kernel(PtrPack arrays, int narr, int64_t b0, int64_t b1,
                                            int64_t row_end, double* partials, int64_t nblocks_total) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ double sv[8][kTraceBlock];
+    const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + g;
     const int64_t nb = b1 - b0;
     if (t >= nb * narr) return;
     const int a = (int)(t / nb);
     const int64_t b = b0 + t % nb;
     const double* d = arrays.p[a];
     const int64_t r0 = b * kTraceBlock;
-    const int64_t r1 = min(r0 + kTraceBlock, row_end);
-    double s = 0.0;
-    for (int64_t r = r0; r < r1; ++r) s = __dadd_rn(s, d[r]);
-    partials[(size_t)a * nblocks_total + b] = s;
+    const int cnt = (int)(min(r0 + kTraceBlock, row_end) - r0);
+    for (int q = lane; q < cnt; q += 32) sv[g][q] = d[r0 + q];
+    __syncwarp();
+    if (lane == 0) {
+        double s = 0.0;
+        for (int q = 0; q < cnt; ++q) s = __dadd_rn(s, sv[g][q]);
+        partials[(size_t)a * nblocks_total + b] = s;
+    }
 }
 
 // partials layout: [narr][nblocks(n)], only blocks of [row_begin,row_end) written.
@@ -60,11 +69,9 @@ cudaError_t launch_block_partials(const double* const* arrays, int narr, int64_t
     const int64_t nbt = (n + kTraceBlock - 1) / kTraceBlock;
     const int64_t b0 = row_begin / kTraceBlock;
     const int64_t b1 = (row_end + kTraceBlock - 1) / kTraceBlock;
-    const int64_t work = (b1 - b0) * narr;
+    const int64_t work = (b1 - b0) * narr;  // (array, block) pairs, one warp each
     if (work <= 0) return cudaSuccess;
-    const int threads = 128;
-    block_partials_pack_kernel<<<(unsigned)((work + threads - 1) / threads), threads, 0, s>>>(
-        pk, narr, b0, b1, row_end, partials, nbt);
+    block_partials_pack_kernel<<<(unsigned)((work + 7) / 8), 256, 0, s>>>(pk, narr, b0, b1, row_end, partials, nbt);
     return cudaGetLastError();
 }
 
@@ -271,9 +278,14 @@ __global__ void copy_rows_kernel(KMat src, KOut dst, int64_t r0, int64_t r1, int
     const int n = src.nnz[i];
     const int m = n < dst.w ? n : dst.w;
     const size_t so = (size_t)i * src.w, d_o = (size_t)i * dst.w;
-    for (int q = lane; q < m; q += 32) {
-        dst.val[d_o + q] = src.val[so + q];
-        dst.col[d_o + q] = src.col[so + q];
+    // pairs of entries per lane (widths are even: 16-byte value pairs, 8-byte column pairs)
+    const double2* sv = reinterpret_cast<const double2*>(src.val + so);
+    const int2* sc = reinterpret_cast<const int2*>(src.col + so);
+    double2* dv = reinterpret_cast<double2*>(dst.val + d_o);
+    int2* dc = reinterpret_cast<int2*>(dst.col + d_o);
+    for (int q = lane; 2 * q < m; q += 32) {
+        dv[q] = sv[q];  // (a row's slot m of an odd count is padding: copying it is harmless)
+        dc[q] = sc[q];
     }
     if (lane == 0) {
         dst.nnz[i] = m;

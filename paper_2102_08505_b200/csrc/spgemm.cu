@@ -1192,13 +1192,15 @@ cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int64_t r0, int64_t r1, int
 // same products as s_ij, P4), and so is X_{n+1}. The row kernel then computes only U_i (columns
 // j >= i, upper = 1) and row i of X_{n+1} is L_i || U_i with L_i = column i of the rows j < i.
 
-// bad[0] = 1 unless every stored (i, j, v) has a stored (j, i) with identical bits.
+// bad[0] = 1 unless every stored (i, j, v) has a stored (j, i) with identical bits. Warp per row,
+// one entry per lane (the binary searches of a row run side by side).
 __global__ void sym_check_kernel(KMat h, int64_t n, int32_t* bad) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (i >= n) return;
     const int nz = h.nnz[i];
     bool ok = true;
-    for (int q = 0; q < nz && ok; ++q) {
+    for (int q = lane; q < nz && ok; q += 32) {
         const int j = h.col[(size_t)i * h.w + q];
         const int32_t* cj = h.col + (size_t)j * h.w;
         int lo = 0, hi = h.nnz[j];
@@ -1213,7 +1215,7 @@ __global__ void sym_check_kernel(KMat h, int64_t n, int32_t* bad) {
 }
 
 cudaError_t launch_sym_check(KMat h, int64_t n, int32_t* bad, cudaStream_t s) {
-    sym_check_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h, n, bad);
+    sym_check_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(h, n, bad);
     return cudaGetLastError();
 }
 

@@ -64,11 +64,18 @@ def main():
         comm = (torch.linalg.norm(Dd @ Hd - Hd @ Dd) / torch.linalg.norm(Hd)).item()
         tr = torch.trace(Dd).item()
     prods = sum(it["products"] for it in r.iters)
+    # D is stored at width d.w: when the final iterate is wider (N > 20000: D at 16384 columns), the
+    # run reports OVERFLOW for D only; the invariants are then not checked (no dense copy of D)
+    d_truncated = r.status == eb.ERR_OVERFLOW and r.required_width > d.w
+    checks = "dense FP64 invariants on D" if idem is not None else (
+        "not checked: N > 20000 (no dense copy)" + ("; D truncated" if d_truncated else ""))
     print(json.dumps({
         "workload": f"{name} SP2 tau={cf['threshold']} tol={cf['tol']} max_iter={a.max_iter} GROW",
         "status": r.status, "stop": r.stop, "iterations": r.iterations, "seconds": dt,
         "iterations_per_s": r.iterations / dt, "gflops": 2.0 * prods / dt / 1e9, "final_width": r.final_width,
         "regrows": r.regrows, "trD": r.trD, "nocc": cf["nocc"], "trace_dense": tr,
+        "d_width": d.w, "d_truncated": d_truncated, "required_width": r.required_width if d_truncated else None,
+        "invariants": checks,
         "idempotency_fro": idem, "commutator_rel": comm, "phases_s": r.phases,
         "e_last": [it["e"] for it in r.iters[-3:]], "widths": [it["width"] for it in r.iters]}), flush=True)
     ctx.close()
