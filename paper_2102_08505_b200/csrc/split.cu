@@ -45,6 +45,17 @@ namespace ell {
 #ifndef ELL_SPLIT_HB_G2
 #define ELL_SPLIT_HB_G2 3
 #endif
+#ifndef ELL_SPLIT_HB_G1
+#define ELL_SPLIT_HB_G1 4
+#endif
+// W = 1: minimum resident CTAs (rows) per SM the register allocation must allow, by groups per step
+// (narrow bands have small rings: registers, not shared memory, cap the rows per SM)
+#ifndef ELL_SPLIT_MINB_G1
+#define ELL_SPLIT_MINB_G1 6
+#endif
+#ifndef ELL_SPLIT_MINB_G2
+#define ELL_SPLIT_MINB_G2 6
+#endif
 constexpr int kSplitStage = ELL_SPLIT_STAGE;  // A-row steps staged per warp (16 B each)
 constexpr int kSplitTrash = 16;  // trash slots S .. S + 15 (one per bank pair) for padding lanes
 
@@ -477,7 +488,8 @@ __device__ __forceinline__ void row_split(const RowOpParams& p, const SplitSmem<
 }
 
 template <int W, int G, int HB, int MODE>
-__global__ void __launch_bounds__(32 * W, 6) row_split_kernel(const RowOpParams p) {
+__global__ void __launch_bounds__(32 * W, W == 1 && G == 1 ? ELL_SPLIT_MINB_G1 : (W == 1 && G == 2 ? ELL_SPLIT_MINB_G2 : 6))
+    row_split_kernel(const RowOpParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int S = p.S;
@@ -1011,7 +1023,7 @@ static void split_dispatch(int G, Fn f) {
     // steps per register half: deep bursts for one warp per row (255 registers); W = 2 runs 6
     // two-warp CTAs per SM, 168 registers per thread
     switch (G) {
-        case 1: f(row_split_kernel<W, 1, W == 1 ? 4 : 3, MODE>); break;
+        case 1: f(row_split_kernel<W, 1, W == 1 ? ELL_SPLIT_HB_G1 : 3, MODE>); break;
         case 2: f(row_split_kernel<W, 2, W == 1 ? ELL_SPLIT_HB_G2 : 2, MODE>); break;
         case 3: f(row_split_kernel<W, 3, W == 1 ? ELL_SPLIT_HB_G3 : 1, MODE>); break;
         default: f(row_split_kernel<W, 4, W == 1 ? 2 : 1, MODE>); break;
