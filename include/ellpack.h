@@ -111,7 +111,7 @@ int ellpack_ctx_set_stream(ellpack_ctx ctx, void* stream);
  *                          ELLPACK_ERR_ARG on a violation (one extra kernel and one
  *                          synchronising read-back per operand set). 0 = inputs trusted
  *                          (default).
- *  ELLPACK_OPT_SP2_SYMMETRIC  1 (default): sp2_run on one rank with the GROW policy checks H for
+ *  ELLPACK_OPT_SP2_SYMMETRIC  1 (default): sp2_run with the GROW policy (any number of ranks) checks H for
  *                          bitwise symmetry; if symmetric, every SP2 step that runs on the general
  *                          (wide-row) path computes only the upper triangle of X_{n+1} (columns
  *                          j >= i) and mirrors it (§8f-f4 ii; X_n symmetric => X_n^2 bitwise

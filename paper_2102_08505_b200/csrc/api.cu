@@ -36,6 +36,7 @@ constexpr int64_t kFastWindowMax = 12288;  // 96 KB + stage per warp
 constexpr int kFastMinRows = 4;            // ring path only with >= 4 rows resident per SM
 constexpr int64_t kGeneralWindow = 1024;
 constexpr int kProbe = 7;  // bandwidth-probe words (launch_bandwidth)
+constexpr int64_t kNoProbeN = 1024;  // up to this N a row op runs unprobed on one general-path window
 constexpr int64_t kSplitRingMax = 8064;  // split kernel: ring slots (16-bit byte offsets incl. trash)  // measured best for cfg3/cfg4 SP2 (512..4096 swept)
 
 namespace {
@@ -335,14 +336,18 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
                    const RowOpExtra* ex = nullptr) {
     p.ncols = n;
     const bool has_old = p.old_mode != 0;
-    if (!bw) {
+    // A small matrix (N <= kNoProbeN, one rank) needs no probe: one general-path window covers every
+    // column, so nothing depends on the bandwidths and the call waits on the device once, at the end
+    // (the cfg1-sized calls are launch- and synchronisation-bound).
+    int32_t bwv[kProbe] = {0, 0, 0, 0, 0, INT_MAX, (int32_t)std::min<int64_t>(n, INT_MAX)};
+    const bool no_probe = !bw && n <= kNoProbeN && !c->comm && c->window_opt == 0 && c->ring_kernel == 0;
+    if (!bw && !no_probe) {
         RK(enqueue_probe(c, p, n));
         CK(cudaMemcpyAsync(c->h->bw, c->d_bw, kProbe * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
         RK(host_sync(c));
         bw = c->h->bw;
     }
-    int32_t bwv[kProbe];
-    memcpy(bwv, bw, sizeof bwv);
+    if (bw) memcpy(bwv, bw, sizeof bwv);
     const int64_t hB = bwv[1];
     const int64_t hprod = p.alpha != 0.0 ? (int64_t)bwv[0] + hB : 0;
     const int64_t h = has_old ? (hprod > bwv[2] ? hprod : bwv[2]) : hprod;
@@ -364,7 +369,7 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
         const int rk = c->ring_kernel;
         const int64_t sring = (2 * hB + 129 + 127) & ~int64_t(127);
         const bool stash = p.stash_a || p.stash_old;
-        if (c->window_opt == 0 && c->force_general_s == 0 && rk != 1 && !stash && groups <= 4 &&
+        if (c->window_opt == 0 && c->force_general_s == 0 && !no_probe && rk != 1 && !stash && groups <= 4 &&
             sring <= kSplitRingMax) {
             // W = 0: the warp-specialized kernel (accumulator + emitter warps, W = 1 records)
             const int W = rk == 3 ? 2 : (rk == 4 ? 0 : 1);  // automatic: one warp per row
@@ -400,9 +405,9 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
     if (split_w) {
         p.fast = 1;
         S = scfg.S;
-    } else if (c->window_opt > 0 || c->force_general_s > 0) {
-        // forced general path (tests; the device SP2 loop): multi-pass windows
-        S = c->window_opt > 0 ? c->window_opt : c->force_general_s;
+    } else if (c->window_opt > 0 || c->force_general_s > 0 || no_probe) {
+        // forced general path (tests; the device SP2 loop; small matrices: one window of N columns)
+        S = c->window_opt > 0 ? c->window_opt : (no_probe ? nr : c->force_general_s);
         p.fast = 0;
     } else if (ring <= kFastWindowMax && groups <= 4) {
         // Grow the ring by slack while the rows resident per SM stay the same: slack lets the
@@ -722,7 +727,9 @@ int start_halo(ellpack_ctx c, ellpack_desc* b, const int64_t* need) {
 // stream waits for sev[1]), the boundary rows [r0, r0 + h) and [r1 - h, r1). The balance pass of
 // the ring paths prepares the own B rows for the interior launch and the halo rows for the
 // boundary ones; the status block accumulates over the launches.
-int enqueue_row_op_split(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bwv, bool halo) {
+int enqueue_row_op_split(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bwv, bool halo,
+                         int (*alloc_upper)(ellpack_ctx, void*, KOut*) = nullptr, void* alloc_arg = nullptr) {
+    bool upper = false;
     const int64_t r0 = p.row_begin, r1 = p.row_end;
     int64_t sp[6];
     RK(ellpack_row_split(r0, r1, bwv[0], sp));
@@ -737,8 +744,9 @@ int enqueue_row_op_split(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t
         ex.nbal = 1;
         ex.bal[0] = std::max(k0, r0);
         ex.bal[1] = std::max(ex.bal[0], std::min(k1, r1));
-        RK(enqueue_row_op(c, q, n, bwv, nullptr, nullptr, &ex));
+        RK(enqueue_row_op(c, q, n, bwv, alloc_upper, alloc_arg, &ex));
         p.fast = q.fast;
+        upper = upper || c->last_upper;
         any = true;
     }
     if (halo) CK(cudaStreamWaitEvent(c->stream, c->sev[1], 0));
@@ -764,12 +772,14 @@ int enqueue_row_op_split(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t
         } else {
             ex.nbal = 0;
         }
-        RK(enqueue_row_op(c, q, n, bwv, nullptr, nullptr, &ex));
+        RK(enqueue_row_op(c, q, n, bwv, alloc_upper, alloc_arg, &ex));
         p.fast = q.fast;
+        upper = upper || c->last_upper;
         any = true;
         halo_balanced = true;
     }
     if (!any) CK(cudaMemsetAsync(c->d_status, 0, 2 * sizeof(int32_t), c->stream));
+    c->last_upper = upper;  // every launch takes the same route (one plan)
     return ELLPACK_OK;
 }
 
@@ -1719,15 +1729,20 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     int32_t req = 0;
     auto cleanup = [&]() { dm_free(c, X); dm_free(c, Y); dm_free(c, T); dm_free(c, U); };
     // Symmetric step (§8f-f4 ii): with H bitwise symmetric every iterate is (P4), so general-path
-    // steps compute only the upper triangle and mirror it. Single rank, GROW policy (FAIL needs the
-    // exact overflow row count of a step, which a truncated upper triangle cannot give).
+    // steps compute only the upper triangle and mirror it. GROW policy (FAIL needs the exact
+    // overflow row count of a step, which a truncated upper triangle cannot give). With a
+    // communicator each rank checks its own rows (the flag is all-reduced) and the U rows of lower
+    // ranks its rows mirror arrive by a second halo.
     bool sym = false, sym_off = false;
-    if (c->sp2_sym && !c->comm && o.on_overflow == SP2_GROW) {
+    if (c->sp2_sym && o.on_overflow == SP2_GROW) {
         RK(grow(c, c->symaux, 4 * sizeof(int32_t)));
         int32_t* aux = (int32_t*)c->symaux.p;
+        int64_t q0, q1;
+        rows_of(c, n, &q0, &q1);
         CK(cudaMemsetAsync(aux, 0, sizeof(int32_t), c->stream));
-        CK(launch_sym_check(kmat(h), n, aux, c->stream));
+        CK(launch_sym_check(kmat(h), q0, q1, aux, c->stream));  // this rank's rows (H is replicated)
         c->launches++;
+        if (c->comm) NK(g_nccl.AllReduce(aux, aux, 1, ncclInt32, ncclMax, c->comm, c->stream));
         int32_t asym = 1;
         CK(cudaMemcpyAsync(&asym, aux, sizeof asym, cudaMemcpyDeviceToHost, c->stream));
         RK(host_sync(c));
@@ -1855,13 +1870,23 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             p.diag_c = (double*)c->rows[1].p;
             p.normsq = (double*)c->rows[2].p;
             p.upper = sym && !sym_off;  // taken only if the general path runs (enqueue_row_op)
+            if (p.upper && c->comm && (!U.owned || U.d.w != Y.d.w)) {
+                // every rank must take the upper route together: U at the agreed width, or none
+                int32_t want = Y.d.w;
+                if (dm_alloc_headroom(c, U, n, want, Y.d.w) != ELLPACK_OK || want != Y.d.w) {
+                    cudaGetLastError();
+                    dm_free(c, U);
+                    sym_off = true;
+                    p.upper = 0;
+                }
+            }
             CK(cudaMemsetAsync(c->d_keys + 4, 0, 8, c->stream));
             p.exec_products = c->d_keys + 4;
             ua.w = Y.d.w;
             cudaEventRecord(c->ev[0], c->stream);
             // with a communicator the halo of X_n (started after the previous step) is in flight:
             // the interior rows run beside it, the boundary rows after it (§8f-f1)
-            if (c->comm) rc = enqueue_row_op_split(c, p, n, bwX, halo_pending);
+            if (c->comm) rc = enqueue_row_op_split(c, p, n, bwX, halo_pending, alloc_upper, &ua);
             else rc = enqueue_row_op(c, p, n, bwX, alloc_upper, &ua);
             if (rc) { status = rc; break; }
             halo_pending = false;
@@ -1871,10 +1896,28 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
                 // U's status aside, then X_{n+1} row i = L_i || U_i with the step's status
                 int32_t* aux = (int32_t*)c->symaux.p;
                 CK(cudaMemcpyAsync(aux + 2, c->d_status, 2 * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream));
+                if (c->comm) {
+                    // every rank redoes an overflowed upper triangle together
+                    NK(g_nccl.GroupStart());
+                    NK(g_nccl.AllReduce(aux + 2, aux + 2, 1, ncclInt32, ncclSum, c->comm, c->stream));
+                    NK(g_nccl.AllReduce(aux + 3, aux + 3, 1, ncclInt32, ncclMax, c->comm, c->stream));
+                    NK(g_nccl.GroupEnd());
+                    // L_i needs column i of the U rows j in [i - reach, i); U_j ends by j + 2 h_X
+                    // (X_{n+1} lies within the band of X_n^2), so rank q reads the U rows
+                    // [r0_q - 2 h_X, r0_q) of lower ranks: a second, one-sided halo
+                    std::vector<int64_t> needU(2 * (size_t)c->nranks);
+                    const int64_t per = r1 - r0;
+                    for (int q = 0; q < c->nranks; ++q) {
+                        needU[2 * q] = std::max<int64_t>(0, (int64_t)q * per - 2 * (int64_t)bwX[0]);
+                        needU[2 * q + 1] = (int64_t)(q + 1) * per - 1;
+                    }
+                    if ((rc = halo_exec(c, &U.d, needU.data()))) { status = rc; break; }
+                }
                 CK(cudaMemcpyAsync(c->h->status_u, aux + 2, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
                 CK(cudaMemsetAsync(c->d_status, 0, 2 * sizeof(int32_t), c->stream));
                 CK(cudaMemsetAsync(aux + 1, 0, sizeof(int32_t), c->stream));
                 CK(launch_upper_reach(kmat(&U.d), r0, r1, aux + 1, c->stream));
+                if (c->comm) NK(g_nccl.AllReduce(aux + 1, aux + 1, 1, ncclInt32, ncclMax, c->comm, c->stream));
                 CK(launch_sym_assemble(kmat(&U.d), kmat(&X.d), kout(&Y.d), r0, r1, aux + 1, p.diag_s, p.normsq,
                                        c->d_status, c->num_sms, c->stream));
                 c->launches += 2;

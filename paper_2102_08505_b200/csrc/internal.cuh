@@ -131,7 +131,7 @@ cudaError_t launch_balance_split(KMat b, int64_t k0, int64_t k1, int W, int G, i
                                  int32_t* bt_nbin, int num_sms, cudaStream_t s);
 
 // symmetric SP2 step (f4 ii): is h bitwise symmetric (ok[0] stays 0); reach of U's rows
-cudaError_t launch_sym_check(KMat h, int64_t n, int32_t* bad, cudaStream_t s);
+cudaError_t launch_sym_check(KMat h, int64_t r0, int64_t r1, int32_t* bad, cudaStream_t s);
 cudaError_t launch_upper_reach(KMat u, int64_t r0, int64_t r1, int32_t* reach, cudaStream_t s);
 // row i of Y = L_i (column i of the rows j < i of U, ascending j) followed by U_i; status as the
 // row kernel (rows over Y.w, max kept); normsq (nullable): upper-triangle norm -> full norm

@@ -1194,10 +1194,10 @@ cudaError_t launch_bandwidth(KMat a, KMat b, KMat c, int64_t r0, int64_t r1, int
 
 // bad[0] = 1 unless every stored (i, j, v) has a stored (j, i) with identical bits. Warp per row,
 // one entry per lane (the binary searches of a row run side by side).
-__global__ void sym_check_kernel(KMat h, int64_t n, int32_t* bad) {
+__global__ void sym_check_kernel(KMat h, int64_t r0, int64_t r1, int32_t* bad) {
     const int lane = threadIdx.x & 31;
-    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (i >= n) return;
+    const int64_t i = r0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (i >= r1) return;
     const int nz = h.nnz[i];
     bool ok = true;
     for (int q = lane; q < nz && ok; q += 32) {
@@ -1214,8 +1214,9 @@ __global__ void sym_check_kernel(KMat h, int64_t n, int32_t* bad) {
     if (!ok) atomicOr(bad, 1);
 }
 
-cudaError_t launch_sym_check(KMat h, int64_t n, int32_t* bad, cudaStream_t s) {
-    sym_check_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(h, n, bad);
+cudaError_t launch_sym_check(KMat h, int64_t r0, int64_t r1, int32_t* bad, cudaStream_t s) {
+    if (r1 <= r0) return cudaSuccess;
+    sym_check_kernel<<<(unsigned)(((r1 - r0) * 32 + 255) / 256), 256, 0, s>>>(h, r0, r1, bad);
     return cudaGetLastError();
 }
 

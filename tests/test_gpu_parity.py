@@ -750,4 +750,6 @@ def test_kernel_launch_counter(ctx):
     before = ctx.kernel_launches()
     X = synth.cfg1()
     gpu_x2(ctx, X, 256, 1e-5)
-    assert ctx.kernel_launches() - before == 5  # bandwidth probe + balance pass + row kernel + block partials + final sums
+    # N = 512 <= 1024: no probe, one general-path window: breakpoints + row kernel + block partials + final sums
+    assert ctx.kernel_launches() - before == 4
+    assert ctx.last_launch()["path"] == "general"

@@ -283,3 +283,22 @@ def test_multiply_x2_halo_one_rank_communicator(ellpack_lib):
     assert st == E.OK and (tx, tx2) == (r.trace_x, r.trace_x2)
     assert same_bits(y.to_host(), Y)
     ctx.close()
+
+
+def test_sp2_symmetric_step_with_communicator(ellpack_lib):
+    """The symmetric step with a communicator (1-rank comm on this pool): the upper route runs (the
+    executed products are about half the pattern's), the U halo and the all-reduced reach are on the
+    path, and every iterate is bitwise the oracle's."""
+    import torch  # noqa: F401
+    E = ellpack_lib
+    n = 1024
+    H = synth.sym_banded(n, 32, 6, 12, 1, -1.0, 1.0, 0, 4.0, 0.0, 6)
+    o = oracle.sp2(H, n // 2, 1e-10, oracle.SP2Opts(threshold=1e-6, max_iter=100), d_width=n)
+    ctx = E.Context(0)
+    ctx.attach_nccl(1, 0, E.Context.nccl_unique_id(), 0, n)
+    d = E.Mat.empty(n, n)
+    g = ctx.sp2_run(up(H), n // 2, 1e-10, d, threshold=1e-6, max_iter=100)
+    _compare_sp2(g, o)
+    assert same_bits(d.to_host(), o.D)
+    assert any(it["products_exec"] < 0.75 * it["products"] for it in g.iters)  # the upper route ran
+    ctx.close()

@@ -246,6 +246,69 @@ def _split_worker(rank, ws, port, n, m, tau):
     dist.destroy_process_group()
 
 
+def _sym_halo_worker(rank, ws, port, n, m, tau):
+    """The symmetric SP2 step across ranks (§8f-f4 ii with a communicator): each rank computes the
+    upper triangle U of its own rows of Y = drop(X^2); the rows it mirrors (U rows of lower ranks) come
+    from the halo plan with need ranges [r0_q - 2 h_X, r1_q) -- X^2's band is at most twice X's --
+    and every row assembled as L_i || U_i from own + received U rows is the full row, bit for bit."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(ws),
+                      LOCAL_RANK=str(rank))
+    sys.path.insert(0, ROOT)
+    import oracle
+    import synth
+    import paper_2102_08505_b200 as eb
+    from paper_2102_08505_b200 import multirank as mr
+
+    oracle.set_threads(1)
+    dist = mr.init_process_group("gloo")
+    r0, r1 = mr.rank_rows(n, ws, rank)
+    per = r1 - r0
+    X = synth.cfg5(n, m)  # bitwise symmetric
+    rows = [i for i in range(r0, r1) if X.nnz[i] > 0]
+    h = int(mr.max_over_ranks(max(max(i - int(X.col[i, 0]), int(X.col[i, X.nnz[i] - 1]) - i) for i in rows)))
+    full = synth.Ell.empty(n, n)
+    oracle.x2(X, full, tau)  # every row (reference)
+    U = {}  # this rank's upper rows: (cols >= i, values)
+    for i in range(r0, r1):
+        k = int(full.nnz[i])
+        c, v = full.col[i, :k], full.val[i, :k]
+        U[i] = (c[c >= i].copy(), v[c >= i].copy())
+    need = [(max(0, q * per - 2 * h), (q + 1) * per - 1) for q in range(ws)]
+    sends, recvs = eb.halo_plan(n, ws, rank, per, need)
+    assert all(p_ < rank for p_, _, _ in recvs) and all(p_ > rank for p_, _, _ in sends)  # one-sided
+    got = {}
+    # exchange as objects (host test of the plan; the library moves the rows by NCCL send/recv)
+    box = [None] * ws
+    dist.all_gather_object(box, {"sends": sends, "U": {j: (U[j][0].tolist(), U[j][1].tolist())
+                                                     for q, s0, s1 in sends for j in range(s0, s1)}})
+    for p_ in range(ws):
+        for q, s0, s1 in box[p_]["sends"]:
+            if q == rank:
+                for j in range(s0, s1):
+                    c, v = box[p_]["U"][j]
+                    got[j] = (np.array(c, np.int32), np.array(v))
+    avail = dict(got)
+    avail.update(U)
+    for i in range(r0, r1):  # assemble L_i || U_i
+        L = [(j, avail[j][1][np.searchsorted(avail[j][0], i)]) for j in range(max(0, i - 2 * h), i)
+             if j in avail and np.searchsorted(avail[j][0], i) < len(avail[j][0])
+             and avail[j][0][np.searchsorted(avail[j][0], i)] == i]
+        cols = [j for j, _ in L] + U[i][0].tolist()
+        vals = np.array([v for _, v in L] + U[i][1].tolist())
+        k = int(full.nnz[i])
+        assert cols == full.col[i, :k].tolist(), i
+        assert np.array_equal(vals.view(np.uint64), full.val[i, :k].view(np.uint64)), i
+        # every row j whose U holds column i is available (own or received)
+        assert all(j in avail for j in range(max(0, i - 2 * h), i) if i in set(full.col[j, :full.nnz[j]].tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws,n,m", [(2, 2048, 32), (4, 4096, 16)])
+def test_symmetric_step_u_halo_gloo(ws, n, m):
+    tmp.spawn(_sym_halo_worker, args=(ws, _free_port(), n, m, 1e-5), nprocs=ws, join=True)
+
+
 @pytest.mark.parametrize("ws,n,m", [(2, 4096, 32), (4, 4096, 16)])
 def test_interior_boundary_row_split_gloo(ws, n, m):
     tmp.spawn(_split_worker, args=(ws, _free_port(), n, m, 1e-5), nprocs=ws, join=True)
