@@ -46,12 +46,12 @@ namespace ell {
 #define ELL_SPLIT_HB_G2 3
 #endif
 #ifndef ELL_SPLIT_HB_G1
-#define ELL_SPLIT_HB_G1 4
+#define ELL_SPLIT_HB_G1 2  // measured: 1.65 vs 1.93 ms at cfg5 M = 64 (12 vs 8 rows/SM)
 #endif
 // W = 1: minimum resident CTAs (rows) per SM the register allocation must allow, by groups per step
 // (narrow bands have small rings: registers, not shared memory, cap the rows per SM)
 #ifndef ELL_SPLIT_MINB_G1
-#define ELL_SPLIT_MINB_G1 6
+#define ELL_SPLIT_MINB_G1 12
 #endif
 #ifndef ELL_SPLIT_MINB_G2
 #define ELL_SPLIT_MINB_G2 6
