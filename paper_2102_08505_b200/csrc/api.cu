@@ -115,6 +115,12 @@ struct ellpack_ctx_s {
     int sp2_loop = 0;     // ELLPACK_OPT_SP2_DEVICE_LOOP
     int force_general_s = 0;  // device SP2 loop: every row op on the general path with this window
     Buf sp2dev, sp2rec;       // device SP2 loop: control block, iteration records
+    cudaGraphExec_t x2_exec = nullptr;   // small unprobed X^2: the captured launch sequence, replayed
+    uint64_t x2_exec_key = 0;
+    int x2_exec_launches = 0;
+    bool x2_exec_ok = false;             // cleared by every option change (the launch plan depends on them)
+    LaunchCfg x2_cfg{};                  // the captured call's launch record (ellpack_ctx_last_launch)
+    int x2_fast = 0, x2_split = 0, x2_hB = 0;
     cudaGraphExec_t sp2_exec = nullptr;  // device SP2 loop: the instantiated graph and what it captured
     uint64_t sp2_exec_key = 0;
     int sp2_exec_launches = 0;
@@ -196,6 +202,12 @@ int host_sync(ellpack_ctx c) {
         if (g_nccl.CommGetAsyncError(c->comm, &ae) != ncclSuccess || ae != ncclSuccess) return ELLPACK_ERR_NCCL;
     }
     return ELLPACK_OK;
+}
+
+// hash combine for the keys of cached CUDA graphs
+uint64_t mix64(uint64_t h, uint64_t v) {
+    h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    return h;
 }
 
 // NVTX range over a scope (the paper's phase names), visible in nsys / ncu timelines
@@ -510,6 +522,10 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
         p.bt = (const unsigned char*)c->bt.p;
         p.bt_nbin = (const int32_t*)c->bt_nbin.p;
         p.bt_w = wt;
+    } else if (p.S >= n) {
+        // one window covers every column: no breakpoints (the kernel takes whole B rows)
+        p.bp = nullptr;
+        p.bp_np = 0;
     } else {
         // breakpoints of B at the aligned window starts (general path)
         const int np = (int)((n + p.S - 1) / p.S) + 1;
@@ -581,6 +597,11 @@ int enqueue_canonical(ellpack_ctx c, const double* const* arrays, int narr, int6
     int64_t r0, r1;
     rows_of(c, n, &r0, &r1);
     const int64_t nb = (n + kTraceBlock - 1) / kTraceBlock;
+    if (!c->comm && nb * narr <= 16) {  // small: both levels in one launch
+        CK(launch_canonical_small(arrays, narr, n, c->d_sums, c->stream));
+        c->launches++;
+        return ELLPACK_OK;
+    }
     RK(grow(c, c->partials, sizeof(double) * (size_t)nb * narr));
     double* part = (double*)c->partials.p;
     CK(launch_block_partials(arrays, narr, r0, r1, n, part, c->stream));
@@ -602,10 +623,15 @@ int enqueue_canonical(ellpack_ctx c, const double* const* arrays, int narr, int6
 
 // One read-back: status, `nsums` canonical sums and, with probe, the bandwidth probe d_bw[0..5]
 // (+ every rank's reach with a communicator); then the one host synchronisation.
-int fetch(ellpack_ctx c, int nsums, bool probe = false) {
+int fetch_copies(ellpack_ctx c, int nsums) {
     CK(cudaMemcpyAsync(c->h->status, c->d_status, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
     if (nsums > 0)
         CK(cudaMemcpyAsync(c->h->sums, c->d_sums, nsums * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    return ELLPACK_OK;
+}
+
+int fetch(ellpack_ctx c, int nsums, bool probe = false) {
+    RK(fetch_copies(c, nsums));
     if (probe) {
         CK(cudaMemcpyAsync(c->h->bw, c->d_bw, kProbe * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
         if (c->comm)
@@ -850,6 +876,7 @@ int ellpack_ctx_destroy(ellpack_ctx c) {
                    &c->hx_val, &c->hx_col, &c->hx_nnz, &c->hy_val, &c->hy_col, &c->hy_nnz,
                    &c->bt, &c->bt_nbin, &c->bp, &c->halo, &c->vflag, &c->symaux, &c->sp2dev, &c->sp2rec};
     if (c->sp2_exec) cudaGraphExecDestroy(c->sp2_exec);
+    if (c->x2_exec) cudaGraphExecDestroy(c->x2_exec);
     for (auto& sl : c->it)
         for (Buf& b : sl) release(c, b);
     for (Buf* b : bufs) release(c, *b);
@@ -878,6 +905,7 @@ int ellpack_ctx_set_stream(ellpack_ctx c, void* stream) {
 
 int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
     if (!c || v < 0) return ELLPACK_ERR_ARG;
+    c->x2_exec_ok = false;
     switch (key) {
         case ELLPACK_OPT_WINDOW: c->window_opt = (int)v; return ELLPACK_OK;
         case ELLPACK_OPT_VALIDATE: c->validate = v != 0; return ELLPACK_OK;
@@ -1045,11 +1073,80 @@ int ellpack_multiply_x2(ellpack_ctx c, const ellpack_desc* x, ellpack_desc* x2, 
     p.tau = tau;
     p.diag_a = (double*)c->rows[0].p;
     p.diag_s = (double*)c->rows[1].p;
-    RK(enqueue_row_op(c, p, n));
-    const double* arrs[2] = {p.diag_a, p.diag_s};
-    RK(enqueue_canonical(c, arrs, 2, n));
-    RK(reduce_status(c));
-    RK(fetch(c, 2));
+    auto enqueue = [&]() -> int {
+        RK(enqueue_row_op(c, p, n));
+        const double* arrs[2] = {p.diag_a, p.diag_s};
+        RK(enqueue_canonical(c, arrs, 2, n));
+        return reduce_status(c);
+    };
+    // A small matrix runs unprobed on one general-path window: its launch sequence depends only on the
+    // shapes and pointers, so it is captured once as a CUDA graph and replayed (one launch instead of
+    // a breakpoints kernel, two memsets, the row kernel and two reduction kernels -- the cfg1-sized
+    // call is launch-latency bound)
+    const bool graphable = n <= kNoProbeN && !c->comm && c->window_opt == 0 && c->ring_kernel == 0 &&
+                           !c->profile && !c->validate && c->row_end < 0;
+    if (graphable) {
+        uint64_t key = 0x78325f67ull, tb;
+        memcpy(&tb, &tau, 8);
+        for (uint64_t v : {(uint64_t)(uintptr_t)x->val, (uint64_t)(uintptr_t)x->col, (uint64_t)(uintptr_t)x->nnz,
+                           (uint64_t)x->w, (uint64_t)(uintptr_t)x2->val, (uint64_t)(uintptr_t)x2->col,
+                           (uint64_t)(uintptr_t)x2->nnz, (uint64_t)x2->w, (uint64_t)n, tb,
+                           (uint64_t)(uintptr_t)c->rows[0].p, (uint64_t)(uintptr_t)c->rows[1].p,
+                           (uint64_t)(uintptr_t)c->partials.p, (uint64_t)(uintptr_t)c->bp.p})
+            key = mix64(key, v);
+        if (!c->x2_exec || !c->x2_exec_ok || c->x2_exec_key != key) {
+            if (c->x2_exec) { cudaGraphExecDestroy(c->x2_exec); c->x2_exec = nullptr; }
+            // grow the workspace outside the capture (the bp and partials buffers of this shape)
+            const int np = (int)((n + 31) / 32) + 1;  // any window S >= 32 the plan picks
+            RK(grow(c, c->bp, sizeof(int32_t) * (size_t)n * np));
+            RK(grow(c, c->partials, sizeof(double) * 2 * (size_t)((n + kTraceBlock - 1) / kTraceBlock)));
+            cudaStream_t cs = nullptr;
+            CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            cudaStream_t saved = c->stream;
+            const int64_t l0 = c->launches;
+            cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed);
+            int rc = ELLPACK_OK;
+            cudaGraph_t g = nullptr;
+            if (!e) {
+                c->stream = cs;
+                rc = enqueue();
+                if (rc == ELLPACK_OK) rc = fetch_copies(c, 2);  // the read-back copies are graph nodes too
+                c->stream = saved;
+                e = cudaStreamEndCapture(cs, &g);
+            }
+            c->x2_exec_launches = (int)(c->launches - l0);
+            c->launches = l0;
+            if (!e && rc == ELLPACK_OK) e = cudaGraphInstantiate(&c->x2_exec, g, 0);
+            if (g) cudaGraphDestroy(g);
+            cudaStreamDestroy(cs);
+            RK(rc);
+            CK(e);
+            // the key covers the buffers the capture saw (they may have grown inside it)
+            key = 0x78325f67ull;
+            for (uint64_t v : {(uint64_t)(uintptr_t)x->val, (uint64_t)(uintptr_t)x->col, (uint64_t)(uintptr_t)x->nnz,
+                               (uint64_t)x->w, (uint64_t)(uintptr_t)x2->val, (uint64_t)(uintptr_t)x2->col,
+                               (uint64_t)(uintptr_t)x2->nnz, (uint64_t)x2->w, (uint64_t)n, tb,
+                               (uint64_t)(uintptr_t)c->rows[0].p, (uint64_t)(uintptr_t)c->rows[1].p,
+                               (uint64_t)(uintptr_t)c->partials.p, (uint64_t)(uintptr_t)c->bp.p})
+                key = mix64(key, v);
+            c->x2_exec_key = key;
+            c->x2_exec_ok = true;
+            c->x2_cfg = c->last_cfg;
+            c->x2_fast = c->last_fast;
+            c->x2_split = c->last_split;
+            c->x2_hB = c->last_hB;
+        }
+        CK(cudaGraphLaunch(c->x2_exec, c->stream));
+        c->launches += c->x2_exec_launches;
+        c->last_cfg = c->x2_cfg;
+        c->last_fast = c->x2_fast;
+        c->last_split = c->x2_split;
+        c->last_hB = c->x2_hB;
+        RK(host_sync(c));
+    } else {
+        RK(enqueue());
+        RK(fetch(c, 2));
+    }
     RK(finish_status(c));
     if (trace_x) *trace_x = c->h->sums[0];
     if (trace_x2) *trace_x2 = c->h->sums[1];
@@ -1504,10 +1601,6 @@ bool use_device_loop(ellpack_ctx c, int64_t n, int32_t maxw) {
     return n <= kDevLoopMaxN && bytes <= 4e9;
 }
 
-uint64_t mix64(uint64_t h, uint64_t v) {
-    h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
-    return h;
-}
 
 // SP2 iterations as ONE launch of a CUDA graph: a WHILE node whose body is one iteration
 // (products, breakpoints, the fused step on the general path with (alpha, beta, old_mode) from the

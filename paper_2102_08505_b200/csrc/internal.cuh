@@ -142,6 +142,7 @@ cudaError_t launch_sym_assemble(KMat u, KMat x, KOut y, int64_t r0, int64_t r1, 
 // reduce.cu
 cudaError_t launch_block_partials(const double* const* arrays, int narr, int64_t row_begin,
                                   int64_t row_end, int64_t n, double* partials, cudaStream_t s);
+cudaError_t launch_canonical_small(const double* const* arrays, int narr, int64_t n, double* out, cudaStream_t s);
 cudaError_t launch_final_sums(const double* partials, int narr, int64_t nblocks, double* out,
                               cudaStream_t s);
 cudaError_t launch_stored_diag(KMat a, int64_t row_begin, int64_t row_end, double* out,

@@ -55,9 +55,48 @@ __global__ void block_partials_pack_kernel(PtrPack arrays, int narr, int64_t b0,
     __syncwarp();
     if (lane == 0) {
         double s = 0.0;
+#pragma unroll 8
         for (int q = 0; q < cnt; ++q) s = __dadd_rn(s, sv[g][q]);
         partials[(size_t)a * nblocks_total + b] = s;
     }
+}
+
+// Both levels in one CTA for a small matrix (narr * nblocks <= 16, one rank): warp t sums (array,
+// block) t as block_partials_pack_kernel does, then thread a adds array a's partials in block order
+// as final_sums_kernel does -- the same two sequential chains, one launch instead of two.
+__global__ void canonical_small_kernel(PtrPack arrays, int narr, int64_t n, double* out) {
+    __shared__ double sv[16][kTraceBlock];
+    __shared__ double sp[16];
+    const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nb = (int)((n + kTraceBlock - 1) / kTraceBlock);
+    if (g < narr * nb) {
+        const int a = g / nb, b = g % nb;
+        const double* d = arrays.p[a];
+        const int64_t r0 = (int64_t)b * kTraceBlock;
+        const int cnt = (int)(min(r0 + kTraceBlock, n) - r0);
+        for (int q = lane; q < cnt; q += 32) sv[g][q] = d[r0 + q];
+        __syncwarp();
+        if (lane == 0) {
+            double s = 0.0;
+#pragma unroll 8
+            for (int q = 0; q < cnt; ++q) s = __dadd_rn(s, sv[g][q]);
+            sp[g] = s;
+        }
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < narr) {
+        double s = 0.0;
+        for (int b = 0; b < nb; ++b) s = __dadd_rn(s, sp[threadIdx.x * nb + b]);
+        out[threadIdx.x] = s;
+    }
+}
+
+cudaError_t launch_canonical_small(const double* const* arrays, int narr, int64_t n, double* out, cudaStream_t s) {
+    if (narr < 1 || narr > 8 || narr * ((n + kTraceBlock - 1) / kTraceBlock) > 16) return cudaErrorInvalidValue;
+    PtrPack pk{};
+    for (int a = 0; a < narr; ++a) pk.p[a] = arrays[a];
+    canonical_small_kernel<<<1, 512, 0, s>>>(pk, narr, n, out);
+    return cudaGetLastError();
 }
 
 // partials layout: [narr][nblocks(n)], only blocks of [row_begin,row_end) written.

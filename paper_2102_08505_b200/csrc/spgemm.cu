@@ -1061,9 +1061,13 @@ __device__ __forceinline__ void row_general_body(const RowOpParams& p, unsigned 
                             int k = 0, sb = 0, se = 0;
                             if (q < cnt) {
                                 k = a_col[p0 + q];
-                                const int32_t* bpk = p.bp + (size_t)k * np + pass;
-                                sb = __ldg(bpk);
-                                se = __ldg(bpk + 1);
+                                if (p.bp) {
+                                    const int32_t* bpk = p.bp + (size_t)k * np + pass;
+                                    sb = __ldg(bpk);
+                                    se = __ldg(bpk + 1);
+                                } else {  // one window covers every column (S >= N): the whole B row
+                                    se = __ldg(p.B.nnz + k);
+                                }
                                 if (p.upper && c0 <= (int)i && (int64_t)i < (int64_t)c0 + S) {
                                     // first entry of B row k with column >= i
                                     const int32_t* bck = p.B.col + (size_t)k * p.B.w;

@@ -31,3 +31,19 @@ def test_sp2_reference_arm_is_explicit():
     assert out.returncode == 0
     d = json.loads(out.stdout.strip().splitlines()[-1])
     assert d["impl"] == "reference" and "unavailable" in d
+
+
+def test_gpus_flag_is_not_a_no_op():
+    """--gpus N must run N ranks or fail loudly: a WORLD_SIZE that disagrees is refused, and without a
+    launcher bench.py re-executes itself under torch.distributed.run, whose ranks refuse to run with
+    fewer GPUs than ranks (here: none) -- no JSON line claiming n_gpus = 1."""
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "0"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert out.returncode == 2 and "WORLD_SIZE" in out.stderr
+    assert not [l for l in out.stdout.splitlines() if l.startswith("{")]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "0",
+                          "--quick"], capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode != 0
+    assert not [l for l in out.stdout.splitlines() if l.startswith("{")]

@@ -302,3 +302,63 @@ def test_sp2_symmetric_step_with_communicator(ellpack_lib):
     assert same_bits(d.to_host(), o.D)
     assert any(it["products_exec"] < 0.75 * it["products"] for it in g.iters)  # the upper route ran
     ctx.close()
+
+
+def test_small_x2_graph_replay_bitwise(ellpack_lib):
+    """N <= 1024 X^2 is captured once as a CUDA graph and replayed: the replay reads the operands'
+    CURRENT contents (rewritten in place between calls), a new tau or a changed option re-captures,
+    an overflow is reported through the replay, and every call equals the oracle bitwise with one
+    host synchronisation."""
+    import torch
+    ctx = ellpack_lib.Context(0)
+    try:
+        n, w = 600, 24
+        Xs = [synth.random_sparse(n, w, 4, w, band=40, seed=900 + s) for s in range(3)]
+        x = up(Xs[0])
+        y = ellpack_lib.Mat.empty(n, 256)
+
+        def check(X, tau, w_out=256, y_=None, syncs=1):
+            y_ = y if y_ is None else y_
+            s0 = ctx.host_syncs()
+            st, tx, tx2 = ctx.multiply_x2(x, y_, tau)
+            assert ctx.host_syncs() - s0 == syncs
+            Y = oracle.Ell.empty(n, w_out)
+            r = oracle.x2(X, Y, tau)
+            assert st == r.status
+            if st == ellpack_lib.OK:
+                assert same_bits(y_.to_host(), Y)
+                assert np.float64(tx).view(np.uint64) == np.float64(r.trace_x).view(np.uint64)
+                assert np.float64(tx2).view(np.uint64) == np.float64(r.trace_x2).view(np.uint64)
+            else:
+                assert ctx.overflow_info() == (r.overflow_rows, r.required_width)
+            return st
+
+        for k in range(6):  # capture, replays, operands rewritten in place between replays
+            X = Xs[k % 3]
+            if k:
+                h = up(X)
+                x.val.copy_(h.val)
+                x.col.copy_(h.col)
+                x.nnz.copy_(h.nnz)
+                torch.cuda.synchronize()
+            assert check(X, 1e-5) == ellpack_lib.OK
+        assert ctx.last_launch()["path"] == "general"
+        l0 = ctx.kernel_launches()
+        check(Xs[2], 1e-5)
+        assert ctx.kernel_launches() - l0 == 2  # the captured kernels are counted on every replay
+        assert check(Xs[2], 0.0) == ellpack_lib.OK  # new tau: re-capture
+        wpc = ctx.last_launch()["warps_per_cta"]
+        ctx.set_option(ellpack_lib.OPT_WARPS, 1 if wpc != 1 else 2)  # any option change: re-capture
+        assert check(Xs[2], 1e-3) == ellpack_lib.OK
+        assert ctx.last_launch()["warps_per_cta"] == (1 if wpc != 1 else 2)
+        ctx.set_option(ellpack_lib.OPT_WINDOW, 64)  # a forced window: not graphed, still bitwise
+        assert check(Xs[2], 1e-3, syncs=2) == ellpack_lib.OK  # probed: the window is planned on the host
+        assert ctx.last_launch()["S"] == 64
+        ctx.set_option(ellpack_lib.OPT_WINDOW, 0)
+        assert check(Xs[2], 1e-3) == ellpack_lib.OK
+        assert ctx.last_launch()["S"] > 64
+        ys = ellpack_lib.Mat.empty(n, 8)  # too narrow: the overflow comes back through the replay
+        assert check(Xs[2], 1e-9, 8, ys) == ellpack_lib.ERR_OVERFLOW
+        assert check(Xs[2], 1e-9, 8, ys) == ellpack_lib.ERR_OVERFLOW
+    finally:
+        ctx.close()
