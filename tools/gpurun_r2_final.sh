@@ -9,4 +9,6 @@ timeout 1500 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.log 2>&1; 
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/ref.log 2>&1; echo "rc=$?" >> gpurun_out/ref.log
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --quick > gpurun_out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:row_split -s 1 -c 1 -o gpurun_out/x2_split_full python tools/prof_one.py --n 262144 --m 256 --reps 2 > gpurun_out/ncu_full.log 2>&1
-echo done
+echo done1
+timeout 900 ncu --metrics smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,gpu__time_duration.sum --clock-control none -k regex:row_split -c 3 --csv --log-file gpurun_out/dfma.csv python tools/prof_one.py --n 32768 --m 64 --reps 1 > gpurun_out/ncu_dfma.log 2>&1
+echo done2
