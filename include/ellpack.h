@@ -134,11 +134,23 @@ int ellpack_ctx_set_stream(ellpack_ctx ctx, void* stream);
  *                          synchronisation per iteration; both iterates at the physical width
  *                          max_width, every step on the general path. 1 = always the host loop
  *                          (one synchronisation per iteration), 2 = the device loop whenever it
- *                          applies (one rank). Results are bitwise the same either way. */
+ *                          applies (one rank). Results are bitwise the same either way.
+ *                          With the dense regime available (ELLPACK_OPT_DENSE 0), automatic picks
+ *                          the host loop, whose steps can switch to the dense GEMM.
+ *  ELLPACK_OPT_DENSE       the dense-regime step (one rank, N <= 32768): X_n is scattered into an
+ *                          N x N array and S = X_n^2 runs as a dense FP64 GEMM (k blocks empty on
+ *                          either side skipped; only the upper triangle of tiles when X_n is
+ *                          symmetric), then one warp per row combines, drops and compacts S into
+ *                          X_{n+1}. Every output is still one fma chain over k ascending -- the
+ *                          extra terms are exact zeros -- so results are bitwise those of the
+ *                          sparse kernels. 0 (default) = automatic: an SP2 step goes dense when
+ *                          N^3 < 16 x the estimated products of the step and 3 N^2 doubles fit in
+ *                          half the free device memory; 1 = never; 2 = always (every SP2 step on
+ *                          one rank and every ellpack_multiply_x2; tests). */
 enum { ELLPACK_OPT_WINDOW = 1, ELLPACK_OPT_WARPS = 2, ELLPACK_OPT_SP2_WIDTH0 = 3, ELLPACK_OPT_PROFILE = 4,
        ELLPACK_OPT_ABLATE = 5, ELLPACK_OPT_GENERAL_WINDOW = 6, ELLPACK_OPT_VALIDATE = 7,
        ELLPACK_OPT_SP2_SYMMETRIC = 8, ELLPACK_OPT_SP2_MEM_CAP = 9, ELLPACK_OPT_RING_KERNEL = 10,
-       ELLPACK_OPT_SP2_DEVICE_LOOP = 11 };
+       ELLPACK_OPT_SP2_DEVICE_LOOP = 11, ELLPACK_OPT_DENSE = 12 };
 int ellpack_ctx_set_option(ellpack_ctx ctx, int key, int64_t value);
 
 /* Accumulated device time (ms, CUDA events on the ctx stream) and launch count of
@@ -153,8 +165,8 @@ int64_t ellpack_ctx_kernel_launches(ellpack_ctx ctx);
 int64_t ellpack_ctx_host_syncs(ellpack_ctx ctx);
 
 /* Launch geometry of the last fused row-kernel launch on this context (what bench.py reports
- * beside its roofline): out[0] path (2 split-row ring kernel, 1 one-warp ring kernel, 0 general
- * path), out[1] G (64-entry B groups per step, ring paths), out[2] S (ring / window doubles per
+ * beside its roofline): out[0] path (4 dense regime -- out[1..7] then stale, 3 warp-specialized ring
+ * kernel, 2 split-row ring kernel, 1 one-warp ring kernel, 0 general path), out[1] G (64-entry B groups per step, ring paths), out[2] S (ring / window doubles per
  * row), out[3] warps per CTA (split kernel: warps per row),
  * out[4] grid, out[5] dynamic shared memory bytes per CTA, out[6] resident CTAs per SM,
  * out[7] B half-bandwidth of the probe. Errors: ARG. */
@@ -256,11 +268,12 @@ typedef struct sp2_iter_rec {
     int32_t branch;            /* SP2_SQUARE | SP2_EXPAND */
     int32_t width;             /* width of X_{n+1} */
     int32_t required;          /* max kept count of X_{n+1} */
-    int32_t reserved;
+    int32_t regime;            /* 0: the sparse row kernels; 1: the dense regime (ELLPACK_OPT_DENSE) */
     int64_t products;          /* scalar products of this X^2 (pattern count) */
     double frob2;              /* TRACE_CLOSEST: T2 of X_n that decided the branch; else 0 */
     int64_t products_exec;     /* products the GPU executed for this step: = products, or about half
-                                  of them when the symmetric step (ELLPACK_OPT_SP2_SYMMETRIC) ran */
+                                  of them when the symmetric step (ELLPACK_OPT_SP2_SYMMETRIC) ran;
+                                  dense regime: the FMAs of the GEMM's non-empty k blocks */
 } sp2_iter_rec;
 
 typedef struct sp2_report {

@@ -22,8 +22,9 @@ from dataclasses import dataclass, field
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _REPO = os.path.dirname(_HERE)
 _LIB = os.environ.get("ELLPACK_LIB") or os.path.join(_HERE, "libellpack.so")
-_SRCS = [os.path.join(_HERE, "csrc", f) for f in ("spgemm.cu", "split.cu", "reduce.cu", "sp2_graph.cu", "api.cu")]
-_HDRS = [os.path.join(_HERE, "csrc", f) for f in ("internal.cuh", "devutil.cuh")] + [os.path.join(_REPO, "include", "ellpack.h")]
+_SRCS = [os.path.join(_HERE, "csrc", f) for f in ("spgemm.cu", "split.cu", "reduce.cu", "sp2_graph.cu", "dense.cu",
+                                                          "api.cu")]
+_HDRS = [os.path.join(_HERE, "csrc", f) for f in ("internal.cuh", "devutil.cuh", "dense.cuh")] + [os.path.join(_REPO, "include", "ellpack.h")]
 
 OK, ERR_ARG, ERR_DIM, ERR_OVERFLOW, ERR_BOUNDS, ERR_NOCONV, ERR_NOMEM, ERR_CUDA, ERR_NCCL, ERR_STATE = range(10)
 OPT_WINDOW, OPT_WARPS, OPT_SP2_WIDTH0, OPT_PROFILE, OPT_ABLATE, OPT_GENERAL_WINDOW, OPT_VALIDATE = 1, 2, 3, 4, 5, 6, 7
@@ -31,6 +32,7 @@ OPT_SP2_SYMMETRIC = 8
 OPT_SP2_MEM_CAP = 9
 OPT_RING_KERNEL = 10
 OPT_SP2_DEVICE_LOOP = 11
+OPT_DENSE = 12
 SP2_FAIL, SP2_GROW = 0, 1
 SP2_RULE_TRACE_SIGN, SP2_RULE_TRACE_CLOSEST = 0, 1
 STOP_NAMES = {0: "CONVERGED", 1: "STAGNATED", 2: "NOCONV", 3: "OVERFLOW"}
@@ -101,7 +103,7 @@ class SP2Opts(ctypes.Structure):
 class SP2IterRec(ctypes.Structure):
     _fields_ = [("trX", ctypes.c_double), ("trS", ctypes.c_double), ("e", ctypes.c_double),
                 ("fnorm", ctypes.c_double), ("branch", ctypes.c_int32), ("width", ctypes.c_int32),
-                ("required", ctypes.c_int32), ("reserved", ctypes.c_int32), ("products", ctypes.c_int64),
+                ("required", ctypes.c_int32), ("regime", ctypes.c_int32), ("products", ctypes.c_int64),
                 ("frob2", ctypes.c_double), ("products_exec", ctypes.c_int64)]
 
 
@@ -272,7 +274,7 @@ class Context:
         """Geometry of the last row-kernel launch (ellpack_ctx_last_launch)."""
         a = (ctypes.c_int32 * 8)()
         _chk(lib().ellpack_ctx_last_launch(self._h, a), "ellpack_ctx_last_launch")
-        return dict(path={3: "ws", 2: "split", 1: "ring", 0: "general"}[a[0]], G=a[1], S=a[2], warps_per_cta=a[3],
+        return dict(path={4: "dense", 3: "ws", 2: "split", 1: "ring", 0: "general"}[a[0]], G=a[1], S=a[2], warps_per_cta=a[3],
                     grid=a[4],
                     smem_bytes=a[5], ctas_per_sm=a[6], hB=a[7])
 
@@ -352,7 +354,8 @@ class Context:
         iters = [dict(trX=recs[k].trX, trS=recs[k].trS, e=recs[k].e, fnorm=recs[k].fnorm,
                       branch="SQUARE" if recs[k].branch == 0 else "EXPAND", width=recs[k].width,
                       required=recs[k].required, products=recs[k].products, frob2=recs[k].frob2,
-                      products_exec=recs[k].products_exec)
+                      products_exec=recs[k].products_exec,
+                      regime="dense" if recs[k].regime == 1 else "sparse")
                  for k in range(n_rec)]
         phases = dict(read_hamiltonian=rep.t_read_hamiltonian, init_misc=rep.t_init_misc,
                       sp2_loop_x2=rep.t_sp2_loop_x2, sp2_loop_norm=rep.t_sp2_loop_norm,

@@ -11,6 +11,7 @@
 // A x I reproduces a exactly (fma(a, 1, +0) = a), so add/identity share the
 // kernel's single-rounding combine instead of a second code path.
 #include "internal.cuh"
+#include "dense.cuh"
 #include "../../include/ellpack.h"
 
 #include <dlfcn.h>
@@ -125,6 +126,10 @@ struct ellpack_ctx_s {
     uint64_t sp2_exec_key = 0;
     int sp2_exec_launches = 0;
     bool last_step_general = false;
+    int dense_opt = 0;     // ELLPACK_OPT_DENSE
+    Buf dense[3];          // dense regime: X (or B), X^T (non-symmetric A), S -- np x np doubles each
+    Buf dflags;            // dense regime: k-block occupancy of the left and right operands
+    int last_dense = 0;    // the last SP2 step / X^2 ran in the dense regime
     struct Host {
         int32_t bw[8];
         int32_t status_u[2];
@@ -347,6 +352,7 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
                    int (*alloc_upper)(ellpack_ctx, void*, KOut*) = nullptr, void* alloc_arg = nullptr,
                    const RowOpExtra* ex = nullptr) {
     p.ncols = n;
+    c->last_dense = 0;
     const bool has_old = p.old_mode != 0;
     // A small matrix (N <= kNoProbeN, one rank) needs no probe: one general-path window covers every
     // column, so nothing depends on the bandwidths and the call waits on the device once, at the end
@@ -621,6 +627,71 @@ int enqueue_canonical(ellpack_ctx c, const double* const* arrays, int narr, int6
     return ELLPACK_OK;
 }
 
+// ---- dense regime (dense.cu): S = A B as a dense FP64 GEMM, then the row epilogue
+constexpr int64_t kDenseMaxN = 32768;
+constexpr double kDenseRatio = 16.0;  // dense when N^3 < kDenseRatio x products (measured rates ~25x)
+
+int64_t dense_np(int64_t n) { return (n + kDenseTile - 1) / kDenseTile * kDenseTile; }
+
+// can this context run a dense step of dimension n (buffers for `bufs` np x np arrays)?
+bool dense_fits(ellpack_ctx c, int64_t n, int bufs) {
+    if (c->comm || c->dense_opt == 1 || n > kDenseMaxN || n <= 0) return false;
+    const int64_t np = dense_np(n);
+    const double need = (double)bufs * 8.0 * (double)np * (double)np;
+    double have = 0.0;
+    for (int b = 0; b < bufs; ++b) have += (double)c->dense[b].bytes;
+    if (need <= have) return true;
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return false; }
+    return need - have <= 0.5 * (double)fr;
+}
+
+// p as for enqueue_row_op (A, B, Old, C, alpha, beta, old_mode, tau, diagonals, norm, exec_products);
+// C must not alias A, B or Old; Old (when old_mode != 0) must be B. sym: A = B and bitwise
+// symmetric (one dense array, half the tiles).
+int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym) {
+    if (p.old_mode != 0 && (p.Old.val != p.B.val || p.Old.col != p.B.col || p.Old.nnz != p.B.nnz))
+        return ELLPACK_ERR_ARG;
+    p.ncols = n;
+    const int64_t np = dense_np(n);
+    const size_t bytes = sizeof(double) * (size_t)np * (size_t)np;
+    const int64_t T = np / kDenseTile, KB = np / kDenseK;
+    RK(grow(c, c->dense[0], bytes));
+    RK(grow(c, c->dense[2], bytes));
+    if (!sym) RK(grow(c, c->dense[1], bytes));
+    const size_t fbytes = 2 * (size_t)T * KB;
+    RK(grow(c, c->dflags, fbytes));
+    unsigned char* fa = (unsigned char*)c->dflags.p;
+    unsigned char* fb = fa + (size_t)T * KB;
+    double* D = (double*)c->dense[0].p;                    // B (row-major)
+    double* Dt = sym ? D : (double*)c->dense[1].p;         // A transposed
+    double* S = (double*)c->dense[2].p;
+    CK(cudaMemsetAsync(c->dflags.p, 0, fbytes, c->stream));
+    CK(cudaMemsetAsync(D, 0, bytes, c->stream));
+    if (!sym) CK(cudaMemsetAsync(Dt, 0, bytes, c->stream));
+    if (sym) {
+        CK(launch_densify(p.B, n, (int)np, false, D, fa, fb, c->stream));
+        c->launches++;
+    } else {
+        CK(launch_densify(p.A, n, (int)np, true, Dt, fa, nullptr, c->stream));
+        CK(launch_densify(p.B, n, (int)np, false, D, nullptr, fb, c->stream));
+        c->launches += 2;
+    }
+    CK(launch_dense_gemm(Dt, D, (int)np, sym, fa, fb, S, p.exec_products, c->num_sms, c->stream));
+    c->launches++;
+    p.status = c->d_status;
+    CK(cudaMemsetAsync(c->d_status, 0, 2 * sizeof(int32_t), c->stream));
+    // stored a_ii of A: the diagonal of either dense copy of A
+    const double* dA = sym ? D : Dt;
+    // Old must be B (the SP2 step: Old = X = B), whose dense copy D the emission reads
+    CK(launch_dense_emit(S, (int)np, p, dA, p.old_mode != 0 ? D : nullptr, c->num_sms, c->stream));
+    c->launches++;
+    c->last_upper = 0;
+    c->last_dense = 1;
+    p.fast = 0;
+    return ELLPACK_OK;
+}
+
 // One read-back: status, `nsums` canonical sums and, with probe, the bandwidth probe d_bw[0..5]
 // (+ every rank's reach with a communicator); then the one host synchronisation.
 int fetch_copies(ellpack_ctx c, int nsums) {
@@ -874,7 +945,8 @@ int ellpack_ctx_destroy(ellpack_ctx c) {
     Buf* bufs[] = {&c->rows[0], &c->rows[1], &c->rows[2], &c->rows[3], &c->partials,
                    &c->stash_val, &c->stash_col, &c->ident_val, &c->ident_col, &c->ident_nnz,
                    &c->hx_val, &c->hx_col, &c->hx_nnz, &c->hy_val, &c->hy_col, &c->hy_nnz,
-                   &c->bt, &c->bt_nbin, &c->bp, &c->halo, &c->vflag, &c->symaux, &c->sp2dev, &c->sp2rec};
+                   &c->bt, &c->bt_nbin, &c->bp, &c->halo, &c->vflag, &c->symaux, &c->sp2dev, &c->sp2rec,
+                   &c->dense[0], &c->dense[1], &c->dense[2], &c->dflags};
     if (c->sp2_exec) cudaGraphExecDestroy(c->sp2_exec);
     if (c->x2_exec) cudaGraphExecDestroy(c->x2_exec);
     for (auto& sl : c->it)
@@ -916,6 +988,10 @@ int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
         case ELLPACK_OPT_SP2_DEVICE_LOOP:
             if (v > 2) return ELLPACK_ERR_ARG;
             c->sp2_loop = (int)v;
+            return ELLPACK_OK;
+        case ELLPACK_OPT_DENSE:
+            if (v > 2) return ELLPACK_ERR_ARG;
+            c->dense_opt = (int)v;
             return ELLPACK_OK;
         case ELLPACK_OPT_RING_KERNEL:
             if (v > 4) return ELLPACK_ERR_ARG;
@@ -961,6 +1037,7 @@ int ellpack_ctx_last_launch(ellpack_ctx c, int32_t out[8]) {
     out[7] = c->last_hB;
     // 3: warp-specialized ring kernel, 2: split-row ring kernel (out[3] = W warps per row)
     out[0] = c->last_split < 0 ? 3 : (c->last_split ? 2 : c->last_fast);
+    if (c->last_dense) out[0] = 4;  // dense regime (dense.cu): out[1..7] describe no row kernel
     return ELLPACK_OK;
 }
 
@@ -1073,8 +1150,23 @@ int ellpack_multiply_x2(ellpack_ctx c, const ellpack_desc* x, ellpack_desc* x2, 
     p.tau = tau;
     p.diag_a = (double*)c->rows[0].p;
     p.diag_s = (double*)c->rows[1].p;
+    // forced dense regime (ELLPACK_OPT_DENSE 2): X's symmetry decides one or two dense copies
+    int dense_sym = -1;
+    if (c->dense_opt == 2 && dense_fits(c, n, 3)) {
+        RK(grow(c, c->symaux, 4 * sizeof(int32_t)));
+        int32_t* aux = (int32_t*)c->symaux.p;
+        CK(cudaMemsetAsync(aux, 0, sizeof(int32_t), c->stream));
+        CK(launch_sym_check(kmat(x), 0, n, aux, c->stream));
+        c->launches++;
+        int32_t asym = 1;
+        CK(cudaMemcpyAsync(&asym, aux, sizeof asym, cudaMemcpyDeviceToHost, c->stream));
+        RK(host_sync(c));
+        dense_sym = asym == 0 ? 1 : 0;
+    }
+    c->last_dense = 0;
     auto enqueue = [&]() -> int {
-        RK(enqueue_row_op(c, p, n));
+        if (dense_sym >= 0) RK(enqueue_dense_op(c, p, n, dense_sym == 1));
+        else RK(enqueue_row_op(c, p, n));
         const double* arrs[2] = {p.diag_a, p.diag_s};
         RK(enqueue_canonical(c, arrs, 2, n));
         return reduce_status(c);
@@ -1083,7 +1175,7 @@ int ellpack_multiply_x2(ellpack_ctx c, const ellpack_desc* x, ellpack_desc* x2, 
     // shapes and pointers, so it is captured once as a CUDA graph and replayed (one launch instead of
     // a breakpoints kernel, two memsets, the row kernel and two reduction kernels -- the cfg1-sized
     // call is launch-latency bound)
-    const bool graphable = n <= kNoProbeN && !c->comm && c->window_opt == 0 && c->ring_kernel == 0 &&
+    const bool graphable = dense_sym < 0 && n <= kNoProbeN && !c->comm && c->window_opt == 0 && c->ring_kernel == 0 &&
                            !c->profile && !c->validate && c->row_end < 0;
     if (graphable) {
         uint64_t key = 0x78325f67ull, tb;
@@ -1594,10 +1686,22 @@ constexpr int kDevLoopWindow = 1024;           // its general-path window (every
 // The device loop keeps both iterates at the physical width max_width (no regrow inside the
 // graph), single rank, and the automatic choice takes it for small N only: there the host
 // synchronisation and the launch sequence are the iteration's cost.
-bool use_device_loop(ellpack_ctx c, int64_t n, int32_t maxw) {
+constexpr int64_t kDevLoopDenseN = 1024;  // the device loop's steps are all dense up to this N
+
+// the device loop's steps run dense: forced, or small N where a dense step costs about as much as a
+// narrow sparse one (N = 512: 31 us GEMM) and the run is bound by per-iteration host work
+bool device_loop_dense(ellpack_ctx c, int64_t n, bool sym) {
+    if (c->dense_opt == 1 || !dense_fits(c, n, sym ? 2 : 3)) return false;
+    return c->dense_opt == 2 || n <= kDevLoopDenseN;
+}
+
+bool use_device_loop(ellpack_ctx c, int64_t n, int32_t maxw, bool sym) {
     if (c->comm || c->sp2_loop == 1) return false;
     const double bytes = 2.0 * 12.0 * (double)n * (double)maxw;
     if (c->sp2_loop == 2) return bytes <= 64e9;
+    // automatic. With the dense regime available: the device loop when all its steps go dense, else
+    // the host loop, whose steps switch to dense as the iterates fill in
+    if (c->dense_opt != 1 && n <= kDenseMaxN) return device_loop_dense(c, n, sym) && bytes <= 4e9;
     return n <= kDevLoopMaxN && bytes <= 4e9;
 }
 
@@ -1608,8 +1712,10 @@ bool use_device_loop(ellpack_ctx c, int64_t n, int32_t maxw) {
 // The host waits once, after the loop. X (width maxw) holds X0 on entry and the final iterate on
 // exit. Fills the report fields the host loop fills and returns an ellpack status.
 int sp2_device_loop(ellpack_ctx c, const sp2_opts& o, int64_t n, int64_t nocc, double tol, int32_t w, int32_t maxw,
-                    bool closest, double& trX, double t2, DevMatrix& X, DevMatrix& Y, sp2_report& R,
+                    bool closest, bool sym, double& trX, double t2, DevMatrix& X, DevMatrix& Y, sp2_report& R,
                     sp2_iter_rec* iters, int32_t& wx, int& stop, int& it, double& t_loop) {
+    // every step dense (dense.cu) or every step on the general path
+    const bool dense = device_loop_dense(c, n, sym);
     // iterates at the physical width maxw
     if (X.d.w < maxw) {
         RK(dm_alloc(c, Y, n, maxw));
@@ -1627,6 +1733,14 @@ int sp2_device_loop(ellpack_ctx c, const sp2_opts& o, int64_t n, int64_t nocc, d
     RK(grow(c, c->partials, sizeof(double) * 4 * (size_t)((n + kTraceBlock - 1) / kTraceBlock)));
     RK(grow(c, c->sp2dev, sizeof(Sp2Dev)));
     RK(grow(c, c->sp2rec, sizeof(sp2_iter_rec) * (size_t)o.max_iter));
+    if (dense) {
+        const int64_t np = dense_np(n);
+        const size_t bytes = sizeof(double) * (size_t)np * (size_t)np;
+        RK(grow(c, c->dense[0], bytes));
+        RK(grow(c, c->dense[2], bytes));
+        if (!sym) RK(grow(c, c->dense[1], bytes));
+        RK(grow(c, c->dflags, 2 * (size_t)(np / kDenseTile) * (size_t)(np / kDenseK)));
+    }
     Sp2Dev* dev = (Sp2Dev*)c->sp2dev.p;
     Sp2Dev hd;
     memset(&hd, 0, sizeof hd);
@@ -1638,6 +1752,7 @@ int sp2_device_loop(ellpack_ctx c, const sp2_opts& o, int64_t n, int64_t nocc, d
     hd.on_overflow = o.on_overflow;
     hd.closest = closest;
     hd.maxw = maxw;
+    hd.pad0 = dense ? 1 : 0;  // recorded as each iteration's regime
     int branch = (trX > (double)nocc) ? SP2_SQUARE : SP2_EXPAND;
     if (closest)
         branch = (std::fabs(t2 - (double)nocc) < std::fabs((2.0 * trX - t2) - (double)nocc)) ? SP2_SQUARE : SP2_EXPAND;
@@ -1660,7 +1775,9 @@ int sp2_device_loop(ellpack_ctx c, const sp2_opts& o, int64_t n, int64_t nocc, d
                        (uint64_t)(uintptr_t)c->rows[0].p, (uint64_t)(uintptr_t)c->rows[3].p,
                        (uint64_t)(uintptr_t)c->partials.p, (uint64_t)(uintptr_t)c->sp2dev.p,
                        (uint64_t)(uintptr_t)c->sp2rec.p, (uint64_t)(uintptr_t)c->stream, (uint64_t)n,
-                       (uint64_t)maxw, (uint64_t)closest, (uint64_t)S})
+                       (uint64_t)maxw, (uint64_t)closest, (uint64_t)S, (uint64_t)dense, (uint64_t)sym,
+                       (uint64_t)(uintptr_t)c->dense[0].p, (uint64_t)(uintptr_t)c->dense[1].p,
+                       (uint64_t)(uintptr_t)c->dense[2].p, (uint64_t)(uintptr_t)c->dflags.p})
         key = mix64(key, v);
     uint64_t tb;
     memcpy(&tb, &o.threshold, 8);
@@ -1706,7 +1823,9 @@ int sp2_device_loop(ellpack_ctx c, const sp2_opts& o, int64_t n, int64_t nocc, d
                 p.diag_c = (double*)c->rows[1].p;
                 p.normsq = (double*)c->rows[2].p;
                 int32_t bw0[kProbe] = {0, 0, 0, 0, 0, 0, 0};
-                if ((rc = enqueue_row_op(c, p, n, bw0))) break;
+                if (dense) rc = enqueue_dense_op(c, p, n, sym);
+                else rc = enqueue_row_op(c, p, n, bw0);
+                if (rc) break;
                 if (closest) {
                     if ((e = launch_sumsq_rows(kmat(&Y.d), 0, n, (double*)c->rows[3].p, cs))) break;
                     c->launches++;
@@ -1912,14 +2031,16 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     int32_t wcap = o.on_overflow == SP2_FAIL ? w : (int32_t)std::min<int64_t>(maxw, round_up32((int64_t)w * 8));
     int stop = -1;
     int it;
+    double p_prev = 0.0, p_prev2 = 0.0;  // products of the last two steps (dense-regime decision)
     UpperAlloc ua{&U, n, 0};
     bool halo_pending = false;  // the halo of X_n travels on the side stream (communicator only)
-    const bool dev_loop = use_device_loop(c, n, maxw);
+    const bool dev_loop = use_device_loop(c, n, maxw, sym);
     if (dev_loop) {
         // (§8f-f3) the whole loop as one graph launch: zero host synchronisations per iteration
         double t_loop = 0.0;
         it = 0;
-        rc = sp2_device_loop(c, o, n, nocc, tol, w, maxw, closest, trX, t2, X, Y, R, iters, wx, stop, it, t_loop);
+        rc = sp2_device_loop(c, o, n, nocc, tol, w, maxw, closest, sym, trX, t2, X, Y, R, iters, wx, stop, it,
+                             t_loop);
         if (rc) status = rc;
         t_x2 = t_loop;
     }
@@ -1947,6 +2068,18 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             // read back with the step's status/sums (same stream, no extra synchronisation)
             CK(cudaMemcpyAsync(&c->h->keys[0], c->d_keys + 2, 8, cudaMemcpyDeviceToHost, c->stream));
         }
+        // the dense regime (dense.cu) for this step: forced, or N^3 below kDenseRatio x the products
+        // estimated from the last two steps (fill grows monotonically in the densifying phase)
+        bool dense_step = false;
+        if (!c->comm && c->dense_opt != 1 && dense_fits(c, n, sym ? 2 : 3)) {
+            if (c->dense_opt == 2) {
+                dense_step = true;
+            } else if (p_prev > 0.0) {
+                const double g = p_prev2 > 0.0 ? std::min(4.0, std::max(1.0, p_prev / p_prev2)) : 1.0;
+                dense_step = (double)n * (double)n * (double)n < kDenseRatio * p_prev * g;
+            }
+        }
+        c->last_dense = 0;
         bool redo;
         int32_t kept_max = 0;
         do {
@@ -1962,7 +2095,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             p.diag_s = (double*)c->rows[0].p;
             p.diag_c = (double*)c->rows[1].p;
             p.normsq = (double*)c->rows[2].p;
-            p.upper = sym && !sym_off;  // taken only if the general path runs (enqueue_row_op)
+            p.upper = sym && !sym_off && !dense_step;  // taken only if the general path runs (enqueue_row_op)
             if (p.upper && c->comm && (!U.owned || U.d.w != Y.d.w)) {
                 // every rank must take the upper route together: U at the agreed width, or none
                 int32_t want = Y.d.w;
@@ -1979,7 +2112,8 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             cudaEventRecord(c->ev[0], c->stream);
             // with a communicator the halo of X_n (started after the previous step) is in flight:
             // the interior rows run beside it, the boundary rows after it (§8f-f1)
-            if (c->comm) rc = enqueue_row_op_split(c, p, n, bwX, halo_pending, alloc_upper, &ua);
+            if (dense_step) rc = enqueue_dense_op(c, p, n, sym);
+            else if (c->comm) rc = enqueue_row_op_split(c, p, n, bwX, halo_pending, alloc_upper, &ua);
             else rc = enqueue_row_op(c, p, n, bwX, alloc_upper, &ua);
             if (rc) { status = rc; break; }
             halo_pending = false;
@@ -2100,13 +2234,15 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             iters[it].branch = branch;
             iters[it].width = wy;
             iters[it].required = kept_max;
-            iters[it].reserved = 0;
+            iters[it].regime = c->last_dense;
             iters[it].products = (int64_t)c->h->keys[0];  // landed with the status fetch
             iters[it].frob2 = t2;
             // products executed: the general kernel counts them; the ring path runs all of them
             iters[it].products_exec = c->last_step_general ? (int64_t)c->h->keys[1] : (int64_t)c->h->keys[0];
         }
         if (closest) t2 = c->h->sums[3];
+        p_prev2 = p_prev;
+        p_prev = (double)c->h->keys[0];
         take_probe(c, bwX, needX);
         // the next step reads only the rows of X_{n+1} its rows reference (band-aware halo, f1),
         // planned from the reaches that arrived with this step's status

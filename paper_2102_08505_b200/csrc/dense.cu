@@ -1,0 +1,334 @@
+// dense.cu — dense-regime X^2 / SP2 step of libellpack (sm_100a, FP64 CUDA cores).
+//
+// Three kernels (dense.cuh states the exactness argument):
+//  * densify_kernel: a warp per ELLPACK row scatters its entries into a zeroed np x np array and
+//    marks the 128 x 16 / 16 x 128 blocks they fall in (the GEMM skips k blocks that are empty on
+//    either side: banded iterates keep most of them empty until late in the run);
+//  * dense_gemm_kernel: 128 x 128 tile per CTA, 256 threads with 8 x 8 outputs each, a 4-stage
+//    cp.async pipeline of 16-row k blocks, k strictly ascending through the stages and inside each
+//    -- every output is the fma chain s <- fma(a_ik, b_kj, s) in ascending k, which is the sparse
+//    kernels' chain plus exact-zero terms. No tensor cores: tcgen05 has no FP64 kind, and DMMA's
+//    internal summation order is not the chain's;
+//  * dense_emit_kernel: a warp per output row walks the dense row (and the dense copy of Old) in
+//    128-column steps, combines / drops / compacts as split_emit (split.cu) does, and writes the
+//    ELLPACK row, its diagonals, its norm partial and the overflow status.
+#include "dense.cuh"
+#include "devutil.cuh"
+
+#include <climits>
+
+namespace ell {
+
+// ------------------------------------------------------------------------------ densify
+
+__global__ void __launch_bounds__(256) densify_kernel(KMat a, int64_t n, int np, int transpose, double* __restrict__ D,
+                                                      unsigned char* __restrict__ fa, unsigned char* __restrict__ fb) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int KB = np / kDenseK, T = np / kDenseTile;
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+        const int nnz = a.nnz[i];
+        const int32_t* c = a.col + (size_t)i * a.w;
+        const double* v = a.val + (size_t)i * a.w;
+        for (int q = lane; q < nnz; q += 32) {
+            const int j = c[q];
+            const double x = v[q];
+            if (transpose) D[(size_t)j * np + i] = x;
+            else D[(size_t)i * np + j] = x;
+            if (fa) fa[(size_t)(i / kDenseTile) * KB + j / kDenseK] = 1;
+            if (fb) fb[(size_t)(i / kDenseK) * T + j / kDenseTile] = 1;
+        }
+    }
+}
+
+cudaError_t launch_densify(KMat a, int64_t n, int np, bool transpose, double* D, unsigned char* fa,
+                           unsigned char* fb, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t blocks = (n + 7) / 8;
+    densify_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, s>>>(a, n, np, transpose ? 1 : 0, D,
+                                                                                   fa, fb);
+    return cudaGetLastError();
+}
+
+// --------------------------------------------------------------------------------- GEMM
+
+constexpr int kDenseStages = 4;
+
+template <int BM>
+__host__ __device__ constexpr int stage_bytes() { return (kDenseK * BM + kDenseK * kDenseTile) * 8; }  // At block + B block
+
+size_t dense_gemm_smem(int np) { return (size_t)kDenseStages * stage_bytes<128>() + sizeof(int) * (size_t)(np / kDenseK); }
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void stg128(double* p, double x, double y) {
+    asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(x), "d"(y) : "memory");
+}
+
+// A BM x 128 tile of S per CTA, 16 TY threads: thread (ty, tx) = (tid / 16, tid % 16) owns rows
+// 2 TY g + 2 ty + r (g < RM / 2, r < 2) and columns 32 h + 2 tx + c (h < 4, c < 2). Its A and B
+// fragments are 16-byte shared loads that a warp (two ty, sixteen tx) serves in 1 (A: two
+// broadcast addresses) and 2 (B: 256 contiguous bytes) wavefronts.
+//   BM = 128, TY = 16: 8 x 8 per thread, the large-N kernel (SYM: tiles bi <= bj, each also stored
+//                      transposed);
+//   BM = 16,  TY = 8:  2 x 8 per thread, 128 threads: small N, where 128-row tiles leave most SMs idle.
+template <int BM, int TY, bool SYM>
+__global__ void __launch_bounds__(16 * TY, BM == 128 ? 1 : 4)
+    dense_gemm_kernel(const double* __restrict__ At, const double* __restrict__ B, int np,
+                      const unsigned char* __restrict__ fa, const unsigned char* __restrict__ fb,
+                      double* __restrict__ S, unsigned long long* exec) {
+    static_assert(!SYM || BM == kDenseTile, "symmetric tiles are square");
+    constexpr int NT = 16 * TY, NW = NT / 32, RM = BM / TY, SB = stage_bytes<BM>();
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int wcnt[NW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tx = tid & 15, ty = tid >> 4;
+    const int T = np / kDenseTile, KB = np / kDenseK;
+    int bi, bj;  // bi: BM-row block, bj: 128-column block
+    if (SYM) {
+        int t = blockIdx.x;
+        bi = 0;
+        while (t >= T - bi) { t -= T - bi; ++bi; }
+        bj = bi + t;
+    } else {
+        bi = blockIdx.x / T;
+        bj = blockIdx.x % T;
+    }
+    const int bf = bi * BM / kDenseTile;  // the 128-row flag block of this tile's rows
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+    int* list = reinterpret_cast<int*>(smem + kDenseStages * SB);
+    // the k blocks with an entry on both sides, ascending
+    int nact = 0;
+    for (int k0 = 0; k0 < KB; k0 += NT) {
+        const int kb = k0 + tid;
+        const bool act = kb < KB && (!fa || fa[(size_t)bf * KB + kb]) && (!fb || fb[(size_t)kb * T + bj]);
+        const unsigned m = __ballot_sync(FULL, act);
+        if (lane == 0) wcnt[warp] = __popc(m);
+        __syncthreads();
+        int off = nact, tot = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            off += w < warp ? wcnt[w] : 0;
+            tot += wcnt[w];
+        }
+        if (act) list[off + __popc(m & ((1u << lane) - 1u))] = kb;
+        __syncthreads();
+        nact += tot;
+    }
+    const double* a0 = At + (size_t)bi * BM;
+    const double* b0 = B + (size_t)bj * kDenseTile;
+    auto load_stage = [&](int st, int kb) {
+        const uint32_t sa = sbase + (uint32_t)(st * SB), sb = sa + (uint32_t)(kDenseK * BM * 8);
+        const size_t r0 = (size_t)kb * kDenseK;
+        constexpr int CA = kDenseK * BM / 2, CB = kDenseK * kDenseTile / 2;  // 16-byte chunks
+#pragma unroll
+        for (int u = 0; u < (CA + NT - 1) / NT; ++u) {
+            const int c = tid + NT * u;
+            if (CA % NT == 0 || c < CA) {
+                const int r = c / (BM / 2), q = c % (BM / 2);
+                cp_async16(sa + (uint32_t)(r * BM * 8 + q * 16), a0 + (r0 + r) * np + 2 * q);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < CB / NT; ++u) {
+            const int c = tid + NT * u;
+            const int r = c >> 6, q = c & 63;
+            cp_async16(sb + (uint32_t)(r * 1024 + q * 16), b0 + (r0 + r) * np + 2 * q);
+        }
+    };
+    double acc[RM][8];
+#pragma unroll
+    for (int r = 0; r < RM; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[r][c] = 0.0;
+#pragma unroll
+    for (int st = 0; st < kDenseStages - 1; ++st) {
+        if (st < nact) load_stage(st, list[st]);
+        cp_async_commit();
+    }
+    for (int t = 0; t < nact; ++t) {
+        cp_async_wait<kDenseStages - 2>();
+        __syncthreads();  // stage t landed for every thread; stage t - 1 is free
+        {
+            const int tn = t + kDenseStages - 1;
+            if (tn < nact) load_stage(tn % kDenseStages, list[tn]);
+            cp_async_commit();
+        }
+        const uint32_t sa = sbase + (uint32_t)((t % kDenseStages) * SB), sb = sa + (uint32_t)(kDenseK * BM * 8);
+#pragma unroll
+        for (int k = 0; k < kDenseK; ++k) {
+            double a[RM], b[8];
+#pragma unroll
+            for (int g = 0; g < RM / 2; ++g)
+                lds128(sa + (uint32_t)((k * BM + 2 * TY * g + 2 * ty) * 8), a[2 * g], a[2 * g + 1]);
+#pragma unroll
+            for (int h = 0; h < 4; ++h) lds128(sb + (uint32_t)(k * 1024 + (32 * h + 2 * tx) * 8), b[2 * h], b[2 * h + 1]);
+#pragma unroll
+            for (int r = 0; r < RM; ++r)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc[r][c] = __fma_rn(a[r], b[c], acc[r][c]);
+        }
+    }
+    cp_async_wait<0>();
+    // tile (bi, bj), and for SYM off the diagonal its transpose at (bj, bi)
+#pragma unroll
+    for (int g = 0; g < RM / 2; ++g)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            double* row = S + (size_t)(bi * BM + 2 * TY * g + 2 * ty + r) * np + bj * kDenseTile;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) stg128(row + 32 * h + 2 * tx, acc[2 * g + r][2 * h], acc[2 * g + r][2 * h + 1]);
+        }
+    if (SYM && bi != bj) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                double* row = S + (size_t)(bj * kDenseTile + 32 * h + 2 * tx + c) * np + bi * BM;
+#pragma unroll
+                for (int g = 0; g < RM / 2; ++g)
+                    stg128(row + 2 * TY * g + 2 * ty, acc[2 * g][2 * h + c], acc[2 * g + 1][2 * h + c]);
+            }
+    }
+    if (exec && tid == 0 && nact)
+        atomicAdd(exec, (unsigned long long)nact * kDenseK * BM * kDenseTile);
+}
+
+template <int BM, int TY, bool SYM>
+cudaError_t launch_gemm_t(unsigned grid, const double* At, const double* B, int np, const unsigned char* fa,
+                          const unsigned char* fb, double* S, unsigned long long* exec, cudaStream_t s) {
+    static int attr = 0;  // dynamic shared memory opted in so far (per instantiation)
+    const size_t smem = (size_t)kDenseStages * stage_bytes<BM>() + sizeof(int) * (size_t)(np / kDenseK);
+    if (smem > 48 * 1024 && attr < (int)smem) {
+        cudaError_t e = cudaFuncSetAttribute(dense_gemm_kernel<BM, TY, SYM>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e) return e;
+        attr = (int)smem;
+    }
+    dense_gemm_kernel<BM, TY, SYM><<<grid, 16 * TY, smem, s>>>(At, B, np, fa, fb, S, exec);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_gemm(const double* At, const double* B, int np, bool sym, const unsigned char* fa,
+                              const unsigned char* fb, double* S, unsigned long long* exec, int num_sms,
+                              cudaStream_t s) {
+    if (np <= 0 || np % kDenseTile) return cudaErrorInvalidValue;
+    const int T = np / kDenseTile;
+    const int tiles = sym ? T * (T + 1) / 2 : T * T;
+    // 128-row tiles while they fill most of the SMs; below that 16-row tiles (8x the CTAs)
+    if (tiles >= (num_sms * 4) / 5) {
+        if (sym) return launch_gemm_t<128, 16, true>((unsigned)tiles, At, B, np, fa, fb, S, exec, s);
+        return launch_gemm_t<128, 16, false>((unsigned)tiles, At, B, np, fa, fb, S, exec, s);
+    }
+    return launch_gemm_t<16, 8, false>((unsigned)(8 * T * T), At, B, np, fa, fb, S, exec, s);
+}
+
+// ---------------------------------------------------------------------------- emission
+
+// MODE as the row kernels: 0 no Old operand; 1 Old operand; 2 Old operand and the norm
+// ||S - Old||^2. p.old_mode (runtime): 1 Old enters the value (beta old), 2 only the union and the
+// norm (SP2 SQUARE). The Old row is read from its dense copy dOld: a column absent from Old reads
+// x = +0, and with x = +0 the row kernels' formula for a column OUTSIDE Old (c = alpha s, norm term
+// s^2) and the one for a column INSIDE Old (c = fma(alpha, s, beta x or +0), norm term (s - x)^2)
+// agree on everything kept or summed (they can differ only in the sign of a zero c, which is
+// dropped) -- so no merge of the Old row is needed. A warp per row, 128 columns (four 32-column
+// chunks, column j on lane j mod 32) per iteration with the loads of all four issued first.
+template <int MODE>
+__global__ void __launch_bounds__(256) dense_emit_kernel(const double* __restrict__ S, int np, const RowOpParams p,
+                                                         const double* __restrict__ dA,
+                                                         const double* __restrict__ dOld) {
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int n = (int)p.ncols;
+    const int cw = p.C.w;
+    const double tau = p.tau;
+    // (alpha, beta, old_mode) from device memory in the device-resident SP2 loop (p.dyn)
+    const double alpha = p.dyn ? p.dyn[0] : p.alpha, beta = p.dyn ? p.dyn[1] : p.beta;
+    const int old_mode = p.dyn ? (int)p.dyn[2] : p.old_mode;
+    const bool a1 = alpha == 1.0, o1 = old_mode == 1;
+    int32_t my_max = 0, my_ovf = 0;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t i = p.row_begin + (int64_t)blockIdx.x * (blockDim.x >> 5) + wi; i < p.row_end; i += nw) {
+        const double* srow = S + (size_t)i * np;
+        const double* xrow = MODE != 0 ? dOld + (size_t)i * np : nullptr;
+        double* cv = p.C.val + (size_t)i * cw;
+        int32_t* cc = p.C.col + (size_t)i * cw;
+        int kept = 0;
+        double ds = 0.0, dc = 0.0, nrm = 0.0;
+        for (int j0 = 0; j0 < n; j0 += 128) {
+            double sv[4], xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = j0 + 32 * u + lane;
+                sv[u] = j < n ? __ldcs(srow + j) : 0.0;  // S is read once: streaming
+                xv[u] = (MODE != 0 && j < n) ? xrow[j] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = j0 + 32 * u + lane;
+                const double s = sv[u];
+                double c;
+                if (MODE != 0) {
+                    c = __fma_rn(alpha, s, o1 ? __dmul_rn(beta, xv[u]) : 0.0);
+                    if (MODE == 2) {
+                        const double df = __dsub_rn(s, xv[u]);
+                        nrm = __fma_rn(df, df, nrm);
+                    }
+                } else {
+                    c = a1 ? s : __dmul_rn(alpha, s);
+                }
+                const bool keep = j < n && fabs(c) > tau;
+                const unsigned km = __ballot_sync(FULL, keep);
+                const int pos = kept + __popc(km & lt);
+                if (keep && pos < cw) {
+                    cv[pos] = c;
+                    cc[pos] = j;
+                }
+                if ((int64_t)j == i) {
+                    ds = s;
+                    dc = keep ? c : 0.0;
+                }
+                kept += __popc(km);
+            }
+        }
+        // the diagonal values live in lane i mod 32
+        const int owner = (int)(i & 31);
+        ds = __shfl_sync(FULL, ds, owner);
+        dc = __shfl_sync(FULL, dc, owner);
+        if (MODE == 2) nrm = warp_sum(nrm);
+        if (lane == 0) {
+            p.C.nnz[i] = kept < cw ? kept : cw;
+            if (p.diag_s) p.diag_s[i] = ds;
+            if (p.diag_c) p.diag_c[i] = dc;
+            if (p.diag_a) p.diag_a[i] = dA[(size_t)i * np + i];
+            if (MODE == 2) p.normsq[i] = nrm;
+        }
+        my_max = max(my_max, kept);
+        if (kept > cw) ++my_ovf;
+    }
+    if (lane == 0) {
+        if (my_ovf) atomicAdd(p.status + 0, my_ovf);
+        if (my_max) atomicMax(p.status + 1, my_max);
+    }
+}
+
+cudaError_t launch_dense_emit(const double* S, int np, const RowOpParams& p, const double* dA, const double* dOld,
+                              int num_sms, cudaStream_t s) {
+    const int64_t rows = p.row_end - p.row_begin;
+    if (rows <= 0) return cudaSuccess;
+    if (p.old_mode != 0 && !dOld) return cudaErrorInvalidValue;
+    int64_t blocks = (rows + 7) / 8;
+    if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+    const int mode = p.old_mode == 0 ? 0 : (p.normsq ? 2 : 1);  // as the row kernels' MODE
+    if (mode == 0) dense_emit_kernel<0><<<(unsigned)blocks, 256, 0, s>>>(S, np, p, dA, dOld);
+    else if (mode == 1) dense_emit_kernel<1><<<(unsigned)blocks, 256, 0, s>>>(S, np, p, dA, dOld);
+    else dense_emit_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(S, np, p, dA, dOld);
+    return cudaGetLastError();
+}
+
+}  // namespace ell

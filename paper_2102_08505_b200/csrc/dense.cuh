@@ -1,0 +1,40 @@
+// dense.cuh — the dense-regime step of libellpack: when an SP2 iterate has filled in (cfg3 reaches
+// width 12096 of N = 12288 by iteration 45, profiles/r01_sp2_full_cfg3.json), the sparse row kernels
+// pay a shared-memory read-modify-write per product for work a dense FP64 GEMM does from registers.
+// The product is the same bit for bit: every output entry is still ONE fma chain over k ascending,
+// and the chain's extra terms are exact zeros (fma(a, +-0, s) == s for s != -0; an accumulator that
+// starts at +0 never becomes -0 under round-to-nearest), so the values, the pattern (|c| > tau drops
+// every structural zero) and the traces equal the oracle's (readings R3, R5, R12).
+#pragma once
+#include "internal.cuh"
+
+namespace ell {
+
+constexpr int kDenseTile = 128;  // rows and columns of S per CTA
+constexpr int kDenseK = 16;      // k rows per pipeline stage
+
+// D (np x np doubles, zeroed by the caller) <- the stored entries of rows [0, n) of a:
+// D[i][j] = a_ij, or D[j][i] = a_ij with transpose. Occupancy flags (nullable, zeroed by the caller):
+// fa[(i / 128) * (np / 16) + j / 16] = 1 (a as the left operand: (m-block, k-block)),
+// fb[(i / 16) * (np / 128) + j / 128] = 1 (a as the right operand: (k-block, n-block)).
+cudaError_t launch_densify(KMat a, int64_t n, int np, bool transpose, double* D, unsigned char* fa,
+                           unsigned char* fb, cudaStream_t s);
+
+// S = A B over the k blocks whose flags are both set (nullable flags: every block), k ascending:
+// At is A transposed (At[k][m] = a_mk); sym: A B is symmetric (A = B = B^T), only tiles bi <= bj are
+// computed and each is also stored transposed. exec (nullable) += FMAs executed.
+// Tiles of 128 rows x 128 columns while they fill most SMs, else 16 x 128 (small N).
+cudaError_t launch_dense_gemm(const double* At, const double* B, int np, bool sym, const unsigned char* fa,
+                              const unsigned char* fb, double* S, unsigned long long* exec, int num_sms,
+                              cudaStream_t s);
+
+// Rows [p.row_begin, p.row_end) of C from the dense S (row stride np): combine with Old (p.old_mode),
+// drop, compact, write, diagonals, norm and status as the row kernels do (RowOpParams).
+// dA (row stride np; read only with p.diag_a): a dense copy of A whose diagonal is the stored a_ii;
+// dOld (row stride np; required when p.old_mode != 0): the dense copy of Old.
+cudaError_t launch_dense_emit(const double* S, int np, const RowOpParams& p, const double* dA, const double* dOld,
+                              int num_sms, cudaStream_t s);
+
+size_t dense_gemm_smem(int np);
+
+}  // namespace ell

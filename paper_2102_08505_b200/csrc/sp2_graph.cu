@@ -58,7 +58,7 @@ __global__ void sp2_ctl_kernel(Sp2Dev* dev, const double* sums, const int32_t* s
     r.branch = d.branch;
     r.width = d.wy;
     r.required = kept;
-    r.reserved = 0;
+    r.regime = dev->pad0;  // pad0: the regime of every step of this loop (1 dense), set by the host
     r.products = products;
     r.frob2 = d.closest ? d.t2 : 0.0;
     r.products_exec = products;

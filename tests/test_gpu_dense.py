@@ -1,0 +1,134 @@
+"""GPU parity of the dense regime (csrc/dense.cu, ELLPACK_OPT_DENSE): the X^2 / SP2 step as a dense
+FP64 GEMM over the scattered operand, then the row epilogue. Every output entry is the same ascending-k
+fma chain as the oracle's plus exact-zero terms, so the comparison is bitwise (values, patterns,
+traces, overflow counts, SP2 branches and stop iterations), on symmetric operands (one dense copy,
+upper-triangle tiles mirrored) and non-symmetric ones (A^T and B copies, every tile), at sizes that
+are not multiples of the 128 tile."""
+import pytest
+
+import oracle
+import synth
+from tests.helpers import same_bits
+from tests.test_gpu_parity import _compare_sp2, gpu_x2, ora_x2, same_bits_scalar, up
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx(E, dense=2, loop=1, sym=1):
+    c = E.Context(0)
+    c.set_option(E.OPT_DENSE, dense)
+    c.set_option(E.OPT_SP2_DEVICE_LOOP, loop)
+    c.set_option(E.OPT_SP2_SYMMETRIC, sym)
+    return c
+
+
+def _sym(n, seed):
+    return synth.sym_banded(n, 32, 6, 12, 1, -1.0, 1.0, 0, 4.0, 0.0, seed)
+
+
+@pytest.mark.parametrize("kind,n,tau", [("sym", 200, 0.0), ("sym", 517, 1e-5), ("sym", 1000, 1e-7),
+                                        ("nonsym", 130, 0.0), ("nonsym", 300, 1e-4), ("nonsym", 645, 1e-6),
+                                        ("cfg1", 512, 1e-5)])
+def test_x2_dense_forced_bitwise(ellpack_lib, kind, n, tau):
+    E = ellpack_lib
+    if kind == "sym":
+        X = _sym(n, n)
+    elif kind == "cfg1":
+        X = synth.cfg1()
+    else:
+        X = synth.random_sparse(n, 40, 0, 40, band=n // 3, p_empty=0.05, seed=n)
+    wo = n + (n & 1)  # ELLPACK widths are even
+    r, Y = ora_x2(X, wo, tau)
+    c = _ctx(E)
+    try:
+        st, Yg, tx, tx2 = gpu_x2(c, X, wo, tau)
+        assert c.last_launch()["path"] == "dense"
+        assert st == r.status == E.OK
+        assert same_bits(Yg, Y)
+        assert same_bits_scalar(tx, r.trace_x) and same_bits_scalar(tx2, r.trace_x2)
+        # overflow through the dense epilogue: exact rows over the width and required width
+        w = max(2, (r.required_width // 2) & ~1)
+        r2, _ = ora_x2(X, w, tau)
+        st2, _, _, _ = gpu_x2(c, X, w, tau)
+        assert st2 == r2.status == E.ERR_OVERFLOW
+        assert c.overflow_info() == (r2.overflow_rows, r2.required_width)
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("n,seed,tau,sym", [(300, 2, 0.0, 1), (517, 5, 1e-6, 1), (517, 5, 1e-6, 0),
+                                            (700, 9, 1e-5, 1)])
+def test_sp2_dense_forced_bitwise(ellpack_lib, n, seed, tau, sym):
+    """Every SP2 step dense (ELLPACK_OPT_DENSE 2): bitwise the oracle's run; with the symmetric
+    option off the GEMM takes the non-symmetric route (A^T copy, all tiles)."""
+    E = ellpack_lib
+    H = _sym(n, seed)
+    wd = n + (n & 1)
+    o = oracle.sp2(H, n // 2, 1e-10, oracle.SP2Opts(threshold=tau, max_iter=100), d_width=wd)
+    c = _ctx(E, dense=2, sym=sym)
+    try:
+        d = E.Mat.empty(n, wd)
+        g = c.sp2_run(up(H), n // 2, 1e-10, d, threshold=tau, max_iter=100)
+        _compare_sp2(g, o)
+        assert same_bits(d.to_host(), o.D)
+        assert all(it["regime"] == "dense" for it in g.iters)
+        T = (n + 127) // 128
+        for it in g.iters:  # FMAs of the non-empty k blocks of the computed tiles
+            assert it["products_exec"] % (16 * 128 * 128) == 0
+            assert 0 < it["products_exec"] <= T * T * (T * 8) * 16 * 128 * 128
+    finally:
+        c.close()
+
+
+def test_sp2_dense_auto_switches_mid_run(ellpack_lib):
+    """Automatic regime on the host loop: the early, narrow iterates run on the sparse kernels, the
+    filled-in ones on the dense GEMM -- one run, bitwise the oracle's."""
+    E = ellpack_lib
+    H = synth.cfg1()
+    n = H.n
+    o = oracle.sp2(H, n // 2, 1e-8, oracle.SP2Opts(threshold=1e-5, max_iter=100), d_width=n)
+    c = _ctx(E, dense=0, loop=1)
+    try:
+        d = E.Mat.empty(n, n)
+        g = c.sp2_run(up(H), n // 2, 1e-8, d, threshold=1e-5, max_iter=100)
+        _compare_sp2(g, o)
+        assert same_bits(d.to_host(), o.D)
+        regimes = [it["regime"] for it in g.iters]
+        assert regimes[0] == "sparse" and "dense" in regimes
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("n,sym", [(512, 1), (300, 0), (1000, 1)])
+def test_sp2_device_loop_dense_bitwise(ellpack_lib, n, sym):
+    """The automatic choice for N <= 1024: the device-resident loop (one graph launch) with every
+    step dense, (alpha, beta, old_mode) read from device memory by the epilogue; bitwise."""
+    E = ellpack_lib
+    H = synth.cfg1() if n == 512 else _sym(n, 4)
+    wd = n + (n & 1)
+    o = oracle.sp2(H, n // 2, 1e-8, oracle.SP2Opts(threshold=1e-5, max_iter=100), d_width=wd)
+    c = _ctx(E, dense=0, loop=0, sym=sym)
+    try:
+        d = E.Mat.empty(n, wd)
+        s0 = c.host_syncs()
+        g = c.sp2_run(up(H), n // 2, 1e-8, d, threshold=1e-5, max_iter=100)
+        assert c.host_syncs() - s0 < 20  # the device loop: a fixed number, not one per iteration
+        _compare_sp2(g, o)
+        assert same_bits(d.to_host(), o.D)
+        assert all(it["regime"] == "dense" for it in g.iters)
+    finally:
+        c.close()
+
+
+def test_dense_off_keeps_sparse_kernels(ellpack_lib):
+    E = ellpack_lib
+    X = _sym(400, 1)
+    c = _ctx(E, dense=1)
+    try:
+        st, _, _, _ = gpu_x2(c, X, 400, 1e-5)
+        assert st == E.OK and c.last_launch()["path"] != "dense"
+        d = E.Mat.empty(400, 400)
+        g = c.sp2_run(up(X), 200, 1e-10, d, threshold=1e-6, max_iter=100)
+        assert all(it["regime"] == "sparse" for it in g.iters)
+    finally:
+        c.close()

@@ -604,6 +604,7 @@ def test_sp2_symmetric_step_vs_whole_rows(ellpack_lib, n, seed, tau, width0):
     for sym in (1, 0):
         ctx = E.Context(0)
         ctx.set_option(E.OPT_SP2_DEVICE_LOOP, 1)  # the symmetric step belongs to the host loop
+        ctx.set_option(E.OPT_DENSE, 1)  # the sparse kernels' symmetric route (the dense GEMM has its own)
         ctx.set_option(E.OPT_SP2_SYMMETRIC, sym)
         if width0:
             ctx.set_option(E.OPT_SP2_WIDTH0, width0)

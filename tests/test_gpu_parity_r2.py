@@ -118,6 +118,7 @@ def test_sp2_iterate_memory_fallbacks_bitwise(ellpack_lib, slack):
     assert o.final_width > 256  # the general path (and its symmetric route) runs
     ctx = E.Context(0)
     ctx.set_option(E.OPT_SP2_DEVICE_LOOP, 1)  # headroom widths and the symmetric step: the host loop
+    ctx.set_option(E.OPT_DENSE, 1)  # the sparse kernels' U buffer fallback
     ctx.set_option(E.OPT_SP2_MEM_CAP, 8 * n * (2 * o.final_width + slack))
     d = E.Mat.empty(n, n)
     g = ctx.sp2_run(up(H), n // 2, 1e-10, d, threshold=1e-6, max_iter=100)
