@@ -381,6 +381,82 @@ def time_sp2(eb, mr, dev, ws, rank, cfg: int, K: int, steps: int, warmup: int):
     return out
 
 
+def time_sp2_full(eb, dev, cfg: int = 3, max_iter: int = 100):
+    """BASELINE configs[2] as named: SP2 on cfg3 to the stop rule (GROW, max_iter 100), one GPU, the
+    automatic regime -- sparse row kernels while the iterates are narrow, the dense GEMM once they fill
+    in (ELLPACK_OPT_DENSE 0). One warm-up run of 30 iterations (workspace, dense buffers), then one
+    timed run, CUDA events on the context stream."""
+    import torch
+    H, cf = synth.cfg3(), synth.CFG3
+    n = H.n
+    ctx = eb.Context(dev)
+    h = eb.Mat.from_host(H)
+    d = eb.Mat.empty(n, n + (n & 1))
+    ctx.sp2_run(h, cf["nocc"], cf["tol"], d, threshold=cf["threshold"], max_iter=30)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0 = ctx.host_syncs()
+    e0.record(stream)
+    r = ctx.sp2_run(h, cf["nocc"], cf["tol"], d, threshold=cf["threshold"], max_iter=max_iter)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    sec = e0.elapsed_time(e1) * 1e-3
+    syncs = ctx.host_syncs() - s0
+    ctx.close()
+    dense = [it for it in r.iters if it["regime"] == "dense"]
+    return {"workload": f"cfg3 SP2 N={n} tau={cf['threshold']:g} tol={cf['tol']:g} to the stop rule "
+                        f"(max_iter {max_iter}), GROW, automatic regime",
+            "iterations": r.iterations, "stop": r.stop, "final_width": r.final_width, "seconds": sec,
+            "iterations_per_s": r.iterations / sec, "host_syncs_per_iteration": syncs / max(r.iterations, 1),
+            "regimes": "".join("D" if it["regime"] == "dense" else "s" for it in r.iters),
+            "dense_iterations": len(dense), "products": sum(it["products"] for it in r.iters),
+            "dense_fmas_executed": sum(it["products_exec"] for it in dense),
+            "sparse_products_executed": sum(it["products_exec"] for it in r.iters if it["regime"] != "dense"),
+            "round1_seconds": 51.18, "round1_source": "profiles/r01_sp2_full_cfg3.json (sparse kernels only)"}
+
+
+def time_dense_gemm(eb, dev, n: int = 8192, reps: int = 5):
+    """The dense regime's GEMM (csrc/dense.cu) on its own: X^2 of a filled, bitwise-symmetric N x N
+    matrix (seeded N(0, 0.01)), ELLPACK_OPT_DENSE 2: symmetric tiles (T (T + 1) / 2 of 128 x 128,
+    every k block non-empty), the GEMM's device time by CUDA events around its launch
+    (ELLPACK_OPT_PROFILE), against the measured FP64 FMA peak (profiles/r02_microbench.json)."""
+    import numpy as np
+    import torch
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal((n, n)) * 0.01
+    a = (a + a.T) * 0.5
+    X = synth.Ell(val=np.ascontiguousarray(a), col=np.tile(np.arange(n, dtype=np.int32), (n, 1)),
+                  nnz=np.full(n, n, dtype=np.int32))
+    del a
+    ctx = eb.Context(dev)
+    ctx.set_option(eb.OPT_DENSE, 2)
+    x = eb.Mat.from_host(X)
+    y = eb.Mat.empty(n, n)
+    for _ in range(2):
+        ctx.multiply_x2(x, y, 0.0)
+    torch.cuda.synchronize()
+    ctx.set_option(eb.OPT_DENSE, 2)
+    ctx.set_option(eb.OPT_PROFILE, 1)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        st, _, _ = ctx.multiply_x2(x, y, 0.0)
+    dt = (time.perf_counter() - t0) / reps
+    kms, kn = ctx.kernel_time()
+    path = ctx.last_launch()["path"]
+    ctx.close()
+    T = n // 128
+    fmas = T * (T + 1) // 2 * 128 * 128 * n
+    tf = 2.0 * fmas / (kms / kn * 1e-3) / 1e12
+    mb = microbench("fp64_fma")
+    return {"workload": f"X^2 of a filled symmetric N={n} matrix, dense regime forced (symmetric tiles)",
+            "status": st, "path": path, "ms_per_call": dt * 1e3, "gemm_ms": kms / kn, "fmas": fmas,
+            "roofline": {"bound": "fp64", "achieved": tf, "unit": "TFLOP/s",
+                         "peak": mb["TFLOPs"] if mb else None, "frac": tf / mb["TFLOPs"] if mb else None,
+                         "peak_source": "tools/microbench.cu FP64 FMA throughput (profiles/r02_microbench.json)"},
+            "full_product_equivalent_tflops": 2.0 * n ** 3 / (kms / kn * 1e-3) / 1e12}
+
+
 def time_sp2_small(eb, dev, reps: int, which: str = "cfg1"):
     """SP2 on a cfg1-sized H, to the stop rule (nocc = N/2, tau = 1e-5, tol = 1e-8): us per iteration
     with the host loop (one host synchronisation per iteration) and with the device-resident loop
@@ -397,9 +473,12 @@ def time_sp2_small(eb, dev, reps: int, which: str = "cfg1"):
         out = {"workload": "SP2 on the soft-matter model H: N=512 nocc=256 tau=1e-05 tol=1e-08, to the stop rule"}
     n = H.n
     ref = None
-    for name, loop in (("host_loop", 1), ("device_loop", 2)):
+    # automatic regime (dense GEMM steps once filled: the host loop switches per step, the device loop
+    # runs every step dense at N <= 1024), and the device loop on the sparse kernels only (round 2's first)
+    for name, loop, dense in (("host_loop", 1, 0), ("device_loop", 2, 0), ("device_loop_sparse_only", 2, 1)):
         ctx = eb.Context(dev)
         ctx.set_option(eb.OPT_SP2_DEVICE_LOOP, loop)
+        ctx.set_option(eb.OPT_DENSE, dense)
         h = eb.Mat.from_host(H)
         d = eb.Mat.empty(n, n)
         run = lambda: ctx.sp2_run(h, n // 2, 1e-8, d, threshold=1e-5, max_iter=100)  # noqa: E731
@@ -412,7 +491,8 @@ def time_sp2_small(eb, dev, reps: int, which: str = "cfg1"):
             r = run()
         dt = (time.perf_counter() - t0) / reps
         out[name] = {"us_per_iteration": dt * 1e6 / r.iterations, "us_per_run": dt * 1e6, "iterations": r.iterations,
-                     "stop": r.stop, "host_syncs_per_run": (ctx.host_syncs() - s0) / reps}
+                     "stop": r.stop, "host_syncs_per_run": (ctx.host_syncs() - s0) / reps,
+                     "dense_iterations": sum(it["regime"] == "dense" for it in r.iters)}
         key = (r.iterations, r.trD, tuple(it["e"] for it in r.iters))
         out[name]["same_as_host_loop"] = None if ref is None else key == ref
         ref = ref or key
@@ -638,15 +718,17 @@ def run_ours(args):
     torch.cuda.empty_cache()
 
     # ---- the rest of the metric: SP2 windows, cfg1 latency, cfg2
-    sp2 = cfg1 = cfg2 = sweep = None
+    sp2 = cfg1 = cfg2 = sweep = dense_gemm = None
     if not args.quick:
         sp2 = {"cfg3": time_sp2(eb, mr, dev, ws, rank, 3, 10, 3, 1),
                "cfg4": time_sp2(eb, mr, dev, ws, rank, 4, 6, 2, 1)}
         if ws == 1:
+            sp2["cfg3_full"] = time_sp2_full(eb, dev)
             sp2["cfg1_sized"] = time_sp2_small(eb, dev, 20, "cfg1")
             sp2["soft_matter_512"] = time_sp2_small(eb, dev, 50, "soft_matter")
         cfg1 = time_cfg1(eb, dev, 300) if ws == 1 else {"skipped": "N=512 is not divisible into 256-row blocks (R17)"}
         sweep = time_sweep(eb, dev, 5) if ws == 1 else None
+        dense_gemm = time_dense_gemm(eb, dev) if ws == 1 else None
         cfg2 = time_cfg2(eb, mr, dev, ws, rank, 10)
 
     # ---- CPU oracle beside it (rank 0, N=1 only, bounded sample)
@@ -680,7 +762,7 @@ def run_ours(args):
                          "kernel": kname, "launch": launch, "kernel_ms_avg": kern_avg,
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "lsu_pipe": lsu_pipe},
-            "sp2": sp2, "cfg1": cfg1, "cfg2": cfg2, "cfg5_sweep": sweep,
+            "sp2": sp2, "cfg1": cfg1, "cfg2": cfg2, "cfg5_sweep": sweep, "dense_gemm": dense_gemm,
             "ranks_bitwise_vs_1": ranks_checked,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -94,10 +94,10 @@ int ellpack_ctx_set_stream(ellpack_ctx ctx, void* stream);
  *  ELLPACK_OPT_WARPS       warps (rows in flight) per CTA (0 = automatic).
  *  ELLPACK_OPT_SP2_WIDTH0  fault injection: sp2_run starts its iterates at this
  *                          width (exercises GROW), 0 = off.
- *  ELLPACK_OPT_PROFILE     1 = bracket every launch of the fused row kernel with
- *                          CUDA events on the context stream and accumulate its
- *                          device time (ellpack_ctx_kernel_time); setting it
- *                          resets the accumulators. 0 = off (default).
+ *  ELLPACK_OPT_PROFILE     1 = bracket every launch of the fused row kernel (in the dense
+ *                          regime: of the dense GEMM) with CUDA events on the context
+ *                          stream and accumulate its device time (ellpack_ctx_kernel_time);
+ *                          setting it resets the accumulators. 0 = off (default).
  *  ELLPACK_OPT_ABLATE      timing experiments only, results are WRONG when set (bit mask):
  *                          1 = the ring kernel skips its output-row stores, 2 = its
  *                          accumulator updates, 4 = its B gathers, 8 = its emission.

@@ -677,7 +677,15 @@ int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym) {
         CK(launch_densify(p.B, n, (int)np, false, D, nullptr, fb, c->stream));
         c->launches += 2;
     }
+    // ELLPACK_OPT_PROFILE: the GEMM is this op's "row kernel" (ellpack_ctx_kernel_time)
+    const int pk = c->prof_n < 4 ? c->prof_n : 3;
+    if (c->profile) CK(cudaEventRecord(c->pev[pk][0], c->stream));
     CK(launch_dense_gemm(Dt, D, (int)np, sym, fa, fb, S, p.exec_products, c->num_sms, c->stream));
+    if (c->profile) {
+        CK(cudaEventRecord(c->pev[pk][1], c->stream));
+        c->prof_n = pk + 1;
+        c->prof_pending = true;
+    }
     c->launches++;
     p.status = c->d_status;
     CK(cudaMemsetAsync(c->d_status, 0, 2 * sizeof(int32_t), c->stream));

@@ -26,9 +26,11 @@ def _sym(n, seed):
     return synth.sym_banded(n, 32, 6, 12, 1, -1.0, 1.0, 0, 4.0, 0.0, seed)
 
 
+# 128-row tiles from 118 tiles on (sym: N >= 1793, otherwise N >= 1281), 16-row tiles below
 @pytest.mark.parametrize("kind,n,tau", [("sym", 200, 0.0), ("sym", 517, 1e-5), ("sym", 1000, 1e-7),
                                         ("nonsym", 130, 0.0), ("nonsym", 300, 1e-4), ("nonsym", 645, 1e-6),
-                                        ("cfg1", 512, 1e-5)])
+                                        ("cfg1", 512, 1e-5), ("sym", 2000, 1e-6), ("sym", 1921, 0.0),
+                                        ("nonsym", 1500, 1e-6), ("nonsym", 1283, 0.0)])
 def test_x2_dense_forced_bitwise(ellpack_lib, kind, n, tau):
     E = ellpack_lib
     if kind == "sym":
@@ -36,7 +38,7 @@ def test_x2_dense_forced_bitwise(ellpack_lib, kind, n, tau):
     elif kind == "cfg1":
         X = synth.cfg1()
     else:
-        X = synth.random_sparse(n, 40, 0, 40, band=n // 3, p_empty=0.05, seed=n)
+        X = synth.random_sparse(n, 40, 0, 40, band=n // 3 if n < 1000 else None, p_empty=0.05, seed=n)
     wo = n + (n & 1)  # ELLPACK widths are even
     r, Y = ora_x2(X, wo, tau)
     c = _ctx(E)
@@ -57,18 +59,19 @@ def test_x2_dense_forced_bitwise(ellpack_lib, kind, n, tau):
 
 
 @pytest.mark.parametrize("n,seed,tau,sym", [(300, 2, 0.0, 1), (517, 5, 1e-6, 1), (517, 5, 1e-6, 0),
-                                            (700, 9, 1e-5, 1)])
+                                            (700, 9, 1e-5, 1), (1900, 3, 1e-6, 1), (1300, 4, 1e-6, 0)])
 def test_sp2_dense_forced_bitwise(ellpack_lib, n, seed, tau, sym):
     """Every SP2 step dense (ELLPACK_OPT_DENSE 2): bitwise the oracle's run; with the symmetric
     option off the GEMM takes the non-symmetric route (A^T copy, all tiles)."""
     E = ellpack_lib
     H = _sym(n, seed)
     wd = n + (n & 1)
-    o = oracle.sp2(H, n // 2, 1e-10, oracle.SP2Opts(threshold=tau, max_iter=100), d_width=wd)
+    K = 100 if n < 1000 else 8  # large N: a window of the run (the oracle's steps grow as N w^2)
+    o = oracle.sp2(H, n // 2, 1e-10, oracle.SP2Opts(threshold=tau, max_iter=K), d_width=wd)
     c = _ctx(E, dense=2, sym=sym)
     try:
         d = E.Mat.empty(n, wd)
-        g = c.sp2_run(up(H), n // 2, 1e-10, d, threshold=tau, max_iter=100)
+        g = c.sp2_run(up(H), n // 2, 1e-10, d, threshold=tau, max_iter=K)
         _compare_sp2(g, o)
         assert same_bits(d.to_host(), o.D)
         assert all(it["regime"] == "dense" for it in g.iters)
