@@ -52,7 +52,13 @@ cudaError_t launch_densify(KMat a, int64_t n, int np, bool transpose, double* D,
 
 // --------------------------------------------------------------------------------- GEMM
 
-constexpr int kDenseStages = 4;
+#ifndef ELL_DENSE_STAGES
+#define ELL_DENSE_STAGES 4  // cp.async pipeline depth (k blocks in flight)
+#endif
+#ifndef ELL_DENSE_TY
+#define ELL_DENSE_TY 16  // large tiles: 16 TY threads, 128 / TY rows x 8 columns each
+#endif
+constexpr int kDenseStages = ELL_DENSE_STAGES;
 
 template <int BM>
 __host__ __device__ constexpr int stage_bytes() { return (kDenseK * BM + kDenseK * kDenseTile) * 8; }  // At block + B block
@@ -66,6 +72,27 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+#ifndef ELL_DENSE_TMA
+#define ELL_DENSE_TMA 1  // stages arrive by bulk copies on an mbarrier (1) or by per-thread cp.async (0)
+#endif
+__device__ __forceinline__ void dmbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void dmbar_expect(uint32_t a, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void dmbar_wait(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tDWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra DWAIT_%=;\n\t}" ::"r"(a), "r"(parity) : "memory");
+}
+// one contiguous global -> shared bulk copy (the TMA engine), completing `bytes` on the mbarrier
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+
 __device__ __forceinline__ void stg128(double* p, double x, double y) {
     asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(x), "d"(y) : "memory");
 }
@@ -78,7 +105,7 @@ __device__ __forceinline__ void stg128(double* p, double x, double y) {
 //                      transposed);
 //   BM = 16,  TY = 8:  2 x 8 per thread, 128 threads: small N, where 128-row tiles leave most SMs idle.
 template <int BM, int TY, bool SYM>
-__global__ void __launch_bounds__(16 * TY, BM == 128 ? 1 : 4)
+__global__ void __launch_bounds__(16 * TY, BM == 128 ? (TY == 8 ? 2 : 1) : 4)
     dense_gemm_kernel(const double* __restrict__ At, const double* __restrict__ B, int np,
                       const unsigned char* __restrict__ fa, const unsigned char* __restrict__ fb,
                       double* __restrict__ S, unsigned long long* exec) {
@@ -102,6 +129,16 @@ __global__ void __launch_bounds__(16 * TY, BM == 128 ? 1 : 4)
     const int bf = bi * BM / kDenseTile;  // the 128-row flag block of this tile's rows
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
     int* list = reinterpret_cast<int*>(smem + kDenseStages * SB);
+#if ELL_DENSE_TMA
+    __shared__ __align__(8) unsigned long long fullbar[kDenseStages];
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(fullbar);
+    if (tid == 0) {
+#pragma unroll
+        for (int st = 0; st < kDenseStages; ++st) dmbar_init(bar0 + 8u * st, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // (the first __syncthreads of the k-block scan below publishes the initialised barriers)
+#endif
     // the k blocks with an entry on both sides, ascending
     int nact = 0;
     for (int k0 = 0; k0 < KB; k0 += NT) {
@@ -122,6 +159,21 @@ __global__ void __launch_bounds__(16 * TY, BM == 128 ? 1 : 4)
     }
     const double* a0 = At + (size_t)bi * BM;
     const double* b0 = B + (size_t)bj * kDenseTile;
+#if ELL_DENSE_TMA
+    // warp 0: lane 0 arms the stage's barrier with its byte count, then 32 bulk copies (one k row of
+    // A^T or of B each) complete on it -- the stage's arrival is tracked by the barrier, not by the
+    // threads' scoreboards, so shared loads of the current stage never wait on the copies in flight
+    auto load_stage = [&](int st, int kb) {
+        const uint32_t sa = sbase + (uint32_t)(st * SB), sb = sa + (uint32_t)(kDenseK * BM * 8);
+        const uint32_t bar = bar0 + 8u * (uint32_t)st;
+        const size_t r0 = (size_t)kb * kDenseK;
+        if (lane == 0) dmbar_expect(bar, (uint32_t)SB);
+        __syncwarp();
+        const int r = lane & 15;
+        if (lane < 16) bulk_g2s(sa + (uint32_t)(r * BM * 8), a0 + (r0 + r) * np, (uint32_t)(BM * 8), bar);
+        else bulk_g2s(sb + (uint32_t)(r * 1024), b0 + (r0 + r) * np, 1024u, bar);
+    };
+#else
     auto load_stage = [&](int st, int kb) {
         const uint32_t sa = sbase + (uint32_t)(st * SB), sb = sa + (uint32_t)(kDenseK * BM * 8);
         const size_t r0 = (size_t)kb * kDenseK;
@@ -141,11 +193,26 @@ __global__ void __launch_bounds__(16 * TY, BM == 128 ? 1 : 4)
             cp_async16(sb + (uint32_t)(r * 1024 + q * 16), b0 + (r0 + r) * np + 2 * q);
         }
     };
+#endif
     double acc[RM][8];
 #pragma unroll
     for (int r = 0; r < RM; ++r)
 #pragma unroll
         for (int c = 0; c < 8; ++c) acc[r][c] = 0.0;
+#if ELL_DENSE_TMA
+    if (warp == 0) {
+#pragma unroll
+        for (int st = 0; st < kDenseStages - 1; ++st)
+            if (st < nact) load_stage(st, list[st]);
+    }
+    for (int t = 0; t < nact; ++t) {
+        __syncthreads();  // every thread is done with stage t - 1: its slot takes stage t + S - 1
+        {
+            const int tn = t + kDenseStages - 1;
+            if (warp == 0 && tn < nact) load_stage(tn % kDenseStages, list[tn]);
+        }
+        dmbar_wait(bar0 + 8u * (uint32_t)(t % kDenseStages), (uint32_t)((t / kDenseStages) & 1));
+#else
 #pragma unroll
     for (int st = 0; st < kDenseStages - 1; ++st) {
         if (st < nact) load_stage(st, list[st]);
@@ -159,6 +226,7 @@ __global__ void __launch_bounds__(16 * TY, BM == 128 ? 1 : 4)
             if (tn < nact) load_stage(tn % kDenseStages, list[tn]);
             cp_async_commit();
         }
+#endif
         const uint32_t sa = sbase + (uint32_t)((t % kDenseStages) * SB), sb = sa + (uint32_t)(kDenseK * BM * 8);
 #pragma unroll
         for (int k = 0; k < kDenseK; ++k) {
@@ -174,7 +242,9 @@ __global__ void __launch_bounds__(16 * TY, BM == 128 ? 1 : 4)
                 for (int c = 0; c < 8; ++c) acc[r][c] = __fma_rn(a[r], b[c], acc[r][c]);
         }
     }
+#if !ELL_DENSE_TMA
     cp_async_wait<0>();
+#endif
     // tile (bi, bj), and for SYM off the diagonal its transpose at (bj, bi)
 #pragma unroll
     for (int g = 0; g < RM / 2; ++g)
@@ -222,8 +292,8 @@ cudaError_t launch_dense_gemm(const double* At, const double* B, int np, bool sy
     const int tiles = sym ? T * (T + 1) / 2 : T * T;
     // 128-row tiles while they fill most of the SMs; below that 16-row tiles (8x the CTAs)
     if (tiles >= (num_sms * 4) / 5) {
-        if (sym) return launch_gemm_t<128, 16, true>((unsigned)tiles, At, B, np, fa, fb, S, exec, s);
-        return launch_gemm_t<128, 16, false>((unsigned)tiles, At, B, np, fa, fb, S, exec, s);
+        if (sym) return launch_gemm_t<128, ELL_DENSE_TY, true>((unsigned)tiles, At, B, np, fa, fb, S, exec, s);
+        return launch_gemm_t<128, ELL_DENSE_TY, false>((unsigned)tiles, At, B, np, fa, fb, S, exec, s);
     }
     return launch_gemm_t<16, 8, false>((unsigned)(8 * T * T), At, B, np, fa, fb, S, exec, s);
 }
