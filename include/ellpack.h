@@ -274,6 +274,8 @@ typedef struct sp2_iter_rec {
     int64_t products_exec;     /* products the GPU executed for this step: = products, or about half
                                   of them when the symmetric step (ELLPACK_OPT_SP2_SYMMETRIC) ran;
                                   dense regime: the FMAs of the GEMM's non-empty k blocks */
+    double step_ms;            /* host loop: device time of the step (X^2 + combine, CUDA events on the
+                                  ctx stream); device loop: NaN (the loop is one graph launch) */
 } sp2_iter_rec;
 
 typedef struct sp2_report {

@@ -104,7 +104,7 @@ class SP2IterRec(ctypes.Structure):
     _fields_ = [("trX", ctypes.c_double), ("trS", ctypes.c_double), ("e", ctypes.c_double),
                 ("fnorm", ctypes.c_double), ("branch", ctypes.c_int32), ("width", ctypes.c_int32),
                 ("required", ctypes.c_int32), ("regime", ctypes.c_int32), ("products", ctypes.c_int64),
-                ("frob2", ctypes.c_double), ("products_exec", ctypes.c_int64)]
+                ("frob2", ctypes.c_double), ("products_exec", ctypes.c_int64), ("step_ms", ctypes.c_double)]
 
 
 class SP2Report(ctypes.Structure):
@@ -355,7 +355,7 @@ class Context:
                       branch="SQUARE" if recs[k].branch == 0 else "EXPAND", width=recs[k].width,
                       required=recs[k].required, products=recs[k].products, frob2=recs[k].frob2,
                       products_exec=recs[k].products_exec,
-                      regime="dense" if recs[k].regime == 1 else "sparse")
+                      regime="dense" if recs[k].regime == 1 else "sparse", step_ms=recs[k].step_ms)
                  for k in range(n_rec)]
         phases = dict(read_hamiltonian=rep.t_read_hamiltonian, init_misc=rep.t_init_misc,
                       sp2_loop_x2=rep.t_sp2_loop_x2, sp2_loop_norm=rep.t_sp2_loop_norm,

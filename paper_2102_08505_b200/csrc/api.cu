@@ -629,7 +629,6 @@ int enqueue_canonical(ellpack_ctx c, const double* const* arrays, int narr, int6
 
 // ---- dense regime (dense.cu): S = A B as a dense FP64 GEMM, then the row epilogue
 constexpr int64_t kDenseMaxN = 32768;
-constexpr double kDenseRatio = 16.0;  // dense when N^3 < kDenseRatio x products (measured rates ~25x)
 
 int64_t dense_np(int64_t n) { return (n + kDenseTile - 1) / kDenseTile * kDenseTile; }
 
@@ -644,6 +643,29 @@ bool dense_fits(ellpack_ctx c, int64_t n, int bufs) {
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return false; }
     return need - have <= 0.5 * (double)fr;
+}
+
+// FMAs the symmetric dense GEMM runs on X^2 for X of half-bandwidth h (every 128 x 16 block within
+// the band counted as occupied: an upper bound of the flags' count), the model the regime choice
+// times with the measured dense rate.
+double dense_band_fmas(int64_t n, int64_t h, bool sym) {
+    const int64_t np = dense_np(n), T = np / kDenseTile;
+    double blocks = 0.0;
+    for (int64_t bi = 0; bi < T; ++bi) {
+        const int64_t rlo = std::max<int64_t>(0, bi * kDenseTile - h);
+        const int64_t rhi = std::min<int64_t>(n - 1, bi * kDenseTile + kDenseTile - 1 + h);
+        for (int64_t bj = sym ? bi : 0; bj < T; ++bj) {
+            const int64_t clo = std::max<int64_t>(0, bj * kDenseTile - h);
+            const int64_t chi = std::min<int64_t>(n - 1, bj * kDenseTile + kDenseTile - 1 + h);
+            const int64_t lo = std::max(rlo, clo), hi = std::min(rhi, chi);
+            if (lo > hi) {
+                if (bj * kDenseTile > bi * kDenseTile + 2 * h + kDenseTile) break;  // past the band
+                continue;
+            }
+            blocks += (double)(hi / kDenseK - lo / kDenseK + 1);
+        }
+    }
+    return blocks * kDenseK * kDenseTile * kDenseTile;
 }
 
 // p as for enqueue_row_op (A, B, Old, C, alpha, beta, old_mode, tau, diagonals, norm, exec_products);
@@ -2040,6 +2062,9 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     int stop = -1;
     int it;
     double p_prev = 0.0, p_prev2 = 0.0;  // products of the last two steps (dense-regime decision)
+    // measured rates of the two regimes (pattern products / s of a sparse step; dense_band_fmas / s of
+    // a dense step), seeded with cfg3's (tools/dense_switch.py, profiles/r02_dense_switch_cfg3.log)
+    double rate_sparse = 1.2e12, rate_dense = 1.0e13;
     UpperAlloc ua{&U, n, 0};
     bool halo_pending = false;  // the halo of X_n travels on the side stream (communicator only)
     const bool dev_loop = use_device_loop(c, n, maxw, sym);
@@ -2076,20 +2101,28 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             // read back with the step's status/sums (same stream, no extra synchronisation)
             CK(cudaMemcpyAsync(&c->h->keys[0], c->d_keys + 2, 8, cudaMemcpyDeviceToHost, c->stream));
         }
-        // the dense regime (dense.cu) for this step: forced, or N^3 below kDenseRatio x the products
-        // estimated from the last two steps (fill grows monotonically in the densifying phase)
+        // the regime of this step (dense.cu or the sparse kernels): forced, or the one whose predicted
+        // time is lower. Sparse: the products P of the step (the last step's, times its growth) at the
+        // pattern-product rate the last sparse step achieved. Dense: the GEMM's FMAs over the k blocks
+        // inside X_n's band (dense_band_fmas: every 128 x 16 block within the probe's half-bandwidth
+        // counted as occupied) at the rate the last dense step achieved on that count.
         bool dense_step = false;
+        double w_dense = 0.0, p_est = 0.0;
         if (!c->comm && c->dense_opt != 1 && dense_fits(c, n, sym ? 2 : 3)) {
+            w_dense = dense_band_fmas(n, std::max(bwX[0], bwX[1]), sym);
             if (c->dense_opt == 2) {
                 dense_step = true;
             } else if (p_prev > 0.0) {
-                const double g = p_prev2 > 0.0 ? std::min(4.0, std::max(1.0, p_prev / p_prev2)) : 1.0;
-                dense_step = (double)n * (double)n * (double)n < kDenseRatio * p_prev * g;
+                // (growth per step <= 2: cfg3's early steps grow 1.5-1.9x once past X0)
+                const double g = p_prev2 > 0.0 ? std::min(2.0, std::max(1.0, p_prev / p_prev2)) : 1.0;
+                p_est = p_prev * g;
+                dense_step = w_dense / rate_dense < 0.85 * p_est / rate_sparse;
             }
         }
         c->last_dense = 0;
         bool redo;
         int32_t kept_max = 0;
+        double step_ms = 0.0;
         do {
             redo = false;
             RowOpParams p = base_params(c, n);
@@ -2180,6 +2213,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             cudaEventElapsedTime(&ms2, c->ev[1], c->ev[2]);
             t_x2 += ms1 * 1e-3;
             t_norm += ms2 * 1e-3;
+            step_ms = ms1;
             if (upper && c->h->status_u[0] > 0) {
                 // the upper triangle overflowed its buffer (so does X_{n+1}): the step's counts are
                 // not exact -- grow the physical width (or, at the ceiling, take the full path) and
@@ -2247,10 +2281,19 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             iters[it].frob2 = t2;
             // products executed: the general kernel counts them; the ring path runs all of them
             iters[it].products_exec = c->last_step_general ? (int64_t)c->h->keys[1] : (int64_t)c->h->keys[0];
+            iters[it].step_ms = step_ms;
         }
         if (closest) t2 = c->h->sums[3];
         p_prev2 = p_prev;
         p_prev = (double)c->h->keys[0];
+        // the rates the next regime choice predicts with (device time of this step)
+        if (step_ms >= 1.0) {  // steps long enough for their rate to carry over
+            if (c->last_dense) {
+                if (w_dense > 0.0) rate_dense = w_dense / (step_ms * 1e-3);
+            } else if (p_prev > 0.0) {
+                rate_sparse = p_prev / (step_ms * 1e-3);
+            }
+        }
         take_probe(c, bwX, needX);
         // the next step reads only the rows of X_{n+1} its rows reference (band-aware halo, f1),
         // planned from the reaches that arrived with this step's status

@@ -7,6 +7,7 @@
 // (reading R6/R19 branch rules, c10 (iv) GROW/FAIL, c10 (vi) stop rule), so the iterates, traces,
 // branches and the stop iteration are bitwise those of the host loop and of the oracle.
 #include "internal.cuh"
+#include <math_constants.h>
 #include "../../include/ellpack.h"
 
 #include <cmath>
@@ -62,6 +63,7 @@ __global__ void sp2_ctl_kernel(Sp2Dev* dev, const double* sums, const int32_t* s
     r.products = products;
     r.frob2 = d.closest ? d.t2 : 0.0;
     r.products_exec = products;
+    r.step_ms = CUDART_NAN;  // one graph launch: no per-iteration timing
     if (d.closest) d.t2 = sums[3];
     d.trX = trY;
     int stop = -1;
