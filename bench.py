@@ -363,21 +363,44 @@ def time_sp2(eb, mr, dev, ws, rank, cfg: int, K: int, steps: int, warmup: int):
     launches = (ctx.kernel_launches() - l0)
     ctx.close()
     P = sum(it["products"] for it in r.iters)
-    Pexec = sum(it["products_exec"] for it in r.iters)
-    rmw = microbench("smem_rmw_f64_random_peak")
-    rate = Pexec / (ms * 1e-3)
     out = {"workload": f"cfg{cfg} SP2 N={n} tau={cf['threshold']:g} window K={K} GROW", "iterations": r.iterations,
            "stop": r.stop, "final_width": r.final_width, "ms_per_window": ms, "iterations_per_s": r.iterations / (ms * 1e-3),
-           "products": P, "products_executed": Pexec,
-           "gflops_effective": 2.0 * P / (ms * 1e-3) / 1e9,
-           "gflops_executed": 2.0 * Pexec / (ms * 1e-3) / 1e9,
+           "products": P, "gflops_effective": 2.0 * P / (ms * 1e-3) / 1e9,
            "host_syncs_per_iteration": syncs / max(r.iterations, 1), "gpu_launches": launches,
-           "roofline": {"bound": "smem_rmw", "achieved": rate / 1e9, "unit": "Gupd/s",
-                        "peak": rmw["Gupd_per_s"] if rmw else None,
-                        "frac": (rate / 1e9 / rmw["Gupd_per_s"]) if rmw else None,
-                        "peak_source": ("tools/microbench.cu random-address FP64 smem RMW, best occupancy "
-                                        "(profiles/r02_microbench.json)") if rmw else "not measured"},
-           "symmetric_step": ws == 1}
+           "symmetric_step": True,
+           "regimes": "".join("D" if it["regime"] == "dense" else "s" for it in r.iters)}
+    out.update(sp2_rooflines(r.iters))
+    return out
+
+
+def sp2_rooflines(iters):
+    """Per-regime rooflines of an SP2 run from its per-step device times (sp2_iter_rec.step_ms): the
+    sparse steps' executed products against the measured random FP64 shared-RMW peak (the
+    accumulator's bound), the dense steps' GEMM FMAs against the measured FP64 FMA peak; "roofline"
+    is the regime that took more of the time."""
+    rmw, fma = microbench("smem_rmw_f64_random_peak"), microbench("fp64_fma")
+    sp = [it for it in iters if it["regime"] != "dense"]
+    de = [it for it in iters if it["regime"] == "dense"]
+    sp_ms = sum(it["step_ms"] for it in sp)
+    de_ms = sum(it["step_ms"] for it in de)
+    out = {"products_executed": sum(it["products_exec"] for it in sp), "dense_fmas_executed":
+           sum(it["products_exec"] for it in de), "sparse_step_ms": sp_ms, "dense_step_ms": de_ms}
+    r_s = r_d = None
+    if sp and sp_ms > 0:
+        a = out["products_executed"] / (sp_ms * 1e-3) / 1e9
+        r_s = {"bound": "smem_rmw", "achieved": a, "unit": "Gupd/s", "peak": rmw["Gupd_per_s"] if rmw else None,
+               "frac": a / rmw["Gupd_per_s"] if rmw else None, "steps": len(sp),
+               "peak_source": "tools/microbench.cu random-address FP64 smem RMW, best occupancy "
+                              "(profiles/r02_microbench.json)"}
+    if de and de_ms > 0:
+        a = 2.0 * out["dense_fmas_executed"] / (de_ms * 1e-3) / 1e12
+        r_d = {"bound": "fp64", "achieved": a, "unit": "TFLOP/s", "peak": fma["TFLOPs"] if fma else None,
+               "frac": a / fma["TFLOPs"] if fma else None, "steps": len(de),
+               "note": "step time includes densify and epilogue; FMAs of the occupied k blocks",
+               "peak_source": "tools/microbench.cu FP64 FMA throughput (profiles/r02_microbench.json)"}
+    out["roofline_sparse_steps"] = r_s
+    out["roofline_dense_steps"] = r_d
+    out["roofline"] = r_d if (r_d and de_ms >= sp_ms) else r_s
     return out
 
 
@@ -405,15 +428,15 @@ def time_sp2_full(eb, dev, cfg: int = 3, max_iter: int = 100):
     syncs = ctx.host_syncs() - s0
     ctx.close()
     dense = [it for it in r.iters if it["regime"] == "dense"]
-    return {"workload": f"cfg3 SP2 N={n} tau={cf['threshold']:g} tol={cf['tol']:g} to the stop rule "
-                        f"(max_iter {max_iter}), GROW, automatic regime",
-            "iterations": r.iterations, "stop": r.stop, "final_width": r.final_width, "seconds": sec,
-            "iterations_per_s": r.iterations / sec, "host_syncs_per_iteration": syncs / max(r.iterations, 1),
-            "regimes": "".join("D" if it["regime"] == "dense" else "s" for it in r.iters),
-            "dense_iterations": len(dense), "products": sum(it["products"] for it in r.iters),
-            "dense_fmas_executed": sum(it["products_exec"] for it in dense),
-            "sparse_products_executed": sum(it["products_exec"] for it in r.iters if it["regime"] != "dense"),
-            "round1_seconds": 51.18, "round1_source": "profiles/r01_sp2_full_cfg3.json (sparse kernels only)"}
+    out = {"workload": f"cfg3 SP2 N={n} tau={cf['threshold']:g} tol={cf['tol']:g} to the stop rule "
+                       f"(max_iter {max_iter}), GROW, automatic regime",
+           "iterations": r.iterations, "stop": r.stop, "final_width": r.final_width, "seconds": sec,
+           "iterations_per_s": r.iterations / sec, "host_syncs_per_iteration": syncs / max(r.iterations, 1),
+           "regimes": "".join("D" if it["regime"] == "dense" else "s" for it in r.iters),
+           "dense_iterations": len(dense), "products": sum(it["products"] for it in r.iters),
+           "round1_seconds": 51.18, "round1_source": "profiles/r01_sp2_full_cfg3.json (sparse kernels only)"}
+    out.update(sp2_rooflines(r.iters))
+    return out
 
 
 def time_dense_gemm(eb, dev, n: int = 8192, reps: int = 5):
@@ -802,6 +825,7 @@ def run_sp2(args):
         ctx.set_option(eb.OPT_GENERAL_WINDOW, args.general_window)
     if args.no_sp2_symmetric:
         ctx.set_option(eb.OPT_SP2_SYMMETRIC, 0)
+    ctx.set_option(eb.OPT_DENSE, args.dense)
     K = args.sp2_iters
     h = eb.Mat.from_host(H)
     d = eb.Mat.empty(n, min(n + (n & 1), 8192))
@@ -813,7 +837,6 @@ def run_sp2(args):
     for _ in range(max(1, args.warmup)):
         r = step()
     prods = sum(it["products"] for it in r.iters)
-    pexec = sum(it["products_exec"] for it in r.iters)
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -839,8 +862,7 @@ def run_sp2(args):
         dt = time.perf_counter() - t0
         cpu = {"value": o.iterations / dt, "unit": "iterations/s", "cores": oracle.num_threads(), "kind": "oracle",
                "sample": f"the same {K}-iteration window (stop {o.stop}, width {o.final_width})"}
-    rmw = microbench("smem_rmw_f64_random_peak")
-    rate = pexec / (ms * 1e-3)
+    roof = sp2_rooflines(r.iters)
     if rank == 0:
         line = {
             "metric": "SP2 iterations/sec", "value": its / (ms * 1e-3), "unit": "iterations/s", "n_gpus": ws,
@@ -852,13 +874,11 @@ def run_sp2(args):
                                     if args.sp2_model else
                                     f"cfg{args.sp2_cfg} SP2 N={n} tau={cf['threshold']:g} window K={K} GROW"),
                        "iterations": its, "stop": r.stop, "final_width": r.final_width, "regrows": r.regrows,
-                       "products": prods, "products_executed": pexec,
-                       "gflops_effective": 2.0 * prods / (ms * 1e-3) / 1e9,
-                       "gflops_executed": 2.0 * pexec / (ms * 1e-3) / 1e9,
+                       "products": prods, "gflops_effective": 2.0 * prods / (ms * 1e-3) / 1e9,
+                       "regimes": "".join("D" if it["regime"] == "dense" else "s" for it in r.iters),
                        "host_syncs_per_iteration": syncs / max(its, 1), "phases_s": r.phases},
-            "roofline": {"bound": "smem_rmw", "achieved": rate / 1e9, "unit": "Gupd/s",
-                         "peak": rmw["Gupd_per_s"] if rmw else None,
-                         "frac": (rate / 1e9 / rmw["Gupd_per_s"]) if rmw else None},
+            "roofline": roof["roofline"], "roofline_sparse_steps": roof["roofline_sparse_steps"],
+            "roofline_dense_steps": roof["roofline_dense_steps"],
             "cpu_baseline": cpu, "gpu_launches": ctx.kernel_launches() - launches0, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -896,6 +916,8 @@ def main():
                     help="SP2 on the paper's model Hamiltonian instead of cfg3/cfg4")
     ap.add_argument("--sp2-n", type=int, default=16384)
     ap.add_argument("--general-window", type=int, default=0, help="general-path window (0 = auto)")
+    ap.add_argument("--dense", type=int, default=0, choices=(0, 1, 2),
+                    help="SP2 workload: ELLPACK_OPT_DENSE (0 automatic regime, 1 sparse kernels only, 2 every step dense)")
     ap.add_argument("--no-sp2-symmetric", action="store_true",
                     help="SP2: compute whole rows even when H is symmetric (A/B of §8f-f4 ii)")
     args = ap.parse_args()

@@ -130,6 +130,7 @@ struct ellpack_ctx_s {
     Buf dense[3];          // dense regime: X (or B), X^T (non-symmetric A), S -- np x np doubles each
     Buf dflags;            // dense regime: k-block occupancy of the left and right operands
     int last_dense = 0;    // the last SP2 step / X^2 ran in the dense regime
+    int64_t dense_clean_np = 0;  // dense[0] is zero outside the blocks dflags' fa marks (for this N_p)
     struct Host {
         int32_t bw[8];
         int32_t status_u[2];
@@ -636,13 +637,19 @@ int64_t dense_np(int64_t n) { return (n + kDenseTile - 1) / kDenseTile * kDenseT
 bool dense_fits(ellpack_ctx c, int64_t n, int bufs) {
     if (c->comm || c->dense_opt == 1 || n > kDenseMaxN || n <= 0) return false;
     const int64_t np = dense_np(n);
-    const double need = (double)bufs * 8.0 * (double)np * (double)np;
-    double have = 0.0;
-    for (int b = 0; b < bufs; ++b) have += (double)c->dense[b].bytes;
-    if (need <= have) return true;
+    const double one = 8.0 * (double)np * (double)np;
+    // the arrays this step uses (dense[0] X or B, dense[2] S, dense[1] A^T when not symmetric) that
+    // are not already large enough: only then ask the driver for free memory (cudaMemGetInfo costs
+    // milliseconds)
+    double need = 0.0;
+    for (int b : {0, 2, 1}) {
+        if (b == 1 && bufs < 3) break;
+        if ((double)c->dense[b].bytes < one) need += one;
+    }
+    if (need == 0.0) return true;
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return false; }
-    return need - have <= 0.5 * (double)fr;
+    return need <= 0.5 * (double)fr;
 }
 
 // FMAs the symmetric dense GEMM runs on X^2 for X of half-bandwidth h (every 128 x 16 block within
@@ -672,24 +679,38 @@ double dense_band_fmas(int64_t n, int64_t h, bool sym) {
 // C must not alias A, B or Old; Old (when old_mode != 0) must be B. sym: A = B and bitwise
 // symmetric (one dense array, half the tiles).
 int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym) {
+    // the dense regime computes X X (A = B; Old, when present, is X too)
+    if (p.A.val != p.B.val || p.A.col != p.B.col || p.A.nnz != p.B.nnz) return ELLPACK_ERR_ARG;
     if (p.old_mode != 0 && (p.Old.val != p.B.val || p.Old.col != p.B.col || p.Old.nnz != p.B.nnz))
         return ELLPACK_ERR_ARG;
     p.ncols = n;
     const int64_t np = dense_np(n);
     const size_t bytes = sizeof(double) * (size_t)np * (size_t)np;
     const int64_t T = np / kDenseTile, KB = np / kDenseK;
+    const void* d0 = c->dense[0].p;
+    const void* f0 = c->dflags.p;
     RK(grow(c, c->dense[0], bytes));
     RK(grow(c, c->dense[2], bytes));
     if (!sym) RK(grow(c, c->dense[1], bytes));
-    const size_t fbytes = 2 * (size_t)T * KB;
-    RK(grow(c, c->dflags, fbytes));
+    const size_t fbytes = 2 * (size_t)T * KB;                      // fa | fb
+    const size_t tbytes = (size_t)(np / 16) * T;                    // tw (16-row tiles at most)
+    RK(grow(c, c->dflags, fbytes + tbytes));
+    if (c->dense[0].p != d0 || c->dflags.p != f0) c->dense_clean_np = 0;  // reallocated: contents unknown
     unsigned char* fa = (unsigned char*)c->dflags.p;
     unsigned char* fb = fa + (size_t)T * KB;
-    double* D = (double*)c->dense[0].p;                    // B (row-major)
-    double* Dt = sym ? D : (double*)c->dense[1].p;         // A transposed
+    unsigned char* tw = fa + fbytes;
+    double* D = (double*)c->dense[0].p;                    // X (row-major): B, Old
+    double* Dt = sym ? D : (double*)c->dense[1].p;         // X^T: A
     double* S = (double*)c->dense[2].p;
+    // D is zero outside the blocks fa flags (the last densify's) when dense_clean_np == np: clearing
+    // those costs the previous iterate's band instead of N^2
+    if (c->dense_clean_np == np) {
+        CK(launch_dense_clear(D, (int)np, fa, c->num_sms, c->stream));
+        c->launches++;
+    } else {
+        CK(cudaMemsetAsync(D, 0, bytes, c->stream));
+    }
     CK(cudaMemsetAsync(c->dflags.p, 0, fbytes, c->stream));
-    CK(cudaMemsetAsync(D, 0, bytes, c->stream));
     if (!sym) CK(cudaMemsetAsync(Dt, 0, bytes, c->stream));
     if (sym) {
         CK(launch_densify(p.B, n, (int)np, false, D, fa, fb, c->stream));
@@ -699,10 +720,11 @@ int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym) {
         CK(launch_densify(p.B, n, (int)np, false, D, nullptr, fb, c->stream));
         c->launches += 2;
     }
+    c->dense_clean_np = np;  // D = X, nonzero only in fa's blocks (A = B = X)
     // ELLPACK_OPT_PROFILE: the GEMM is this op's "row kernel" (ellpack_ctx_kernel_time)
     const int pk = c->prof_n < 4 ? c->prof_n : 3;
     if (c->profile) CK(cudaEventRecord(c->pev[pk][0], c->stream));
-    CK(launch_dense_gemm(Dt, D, (int)np, sym, fa, fb, S, p.exec_products, c->num_sms, c->stream));
+    CK(launch_dense_gemm(Dt, D, (int)np, sym, fa, fb, S, tw, p.exec_products, c->num_sms, c->stream));
     if (c->profile) {
         CK(cudaEventRecord(c->pev[pk][1], c->stream));
         c->prof_n = pk + 1;
@@ -711,10 +733,10 @@ int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym) {
     c->launches++;
     p.status = c->d_status;
     CK(cudaMemsetAsync(c->d_status, 0, 2 * sizeof(int32_t), c->stream));
-    // stored a_ii of A: the diagonal of either dense copy of A
+    // stored a_ii of A: the diagonal of either dense copy of A; Old = X: its dense copy D and flags fa
     const double* dA = sym ? D : Dt;
-    // Old must be B (the SP2 step: Old = X = B), whose dense copy D the emission reads
-    CK(launch_dense_emit(S, (int)np, p, dA, p.old_mode != 0 ? D : nullptr, c->num_sms, c->stream));
+    CK(launch_dense_emit(S, (int)np, p, dA, p.old_mode != 0 ? D : nullptr, tw,
+                         dense_tile_rows((int)np, sym, c->num_sms), fa, c->num_sms, c->stream));
     c->launches++;
     c->last_upper = 0;
     c->last_dense = 1;
@@ -1769,7 +1791,12 @@ int sp2_device_loop(ellpack_ctx c, const sp2_opts& o, int64_t n, int64_t nocc, d
         RK(grow(c, c->dense[0], bytes));
         RK(grow(c, c->dense[2], bytes));
         if (!sym) RK(grow(c, c->dense[1], bytes));
-        RK(grow(c, c->dflags, 2 * (size_t)(np / kDenseTile) * (size_t)(np / kDenseK)));
+        RK(grow(c, c->dflags, 2 * (size_t)(np / kDenseTile) * (size_t)(np / kDenseK) +
+                                  (size_t)(np / 16) * (size_t)(np / kDenseTile)));
+        // the captured steps clear D by the previous step's flags: start from D = 0, flags = 0
+        CK(cudaMemsetAsync(c->dense[0].p, 0, bytes, c->stream));
+        CK(cudaMemsetAsync(c->dflags.p, 0, c->dflags.bytes, c->stream));
+        c->dense_clean_np = np;
     }
     Sp2Dev* dev = (Sp2Dev*)c->sp2dev.p;
     Sp2Dev hd;

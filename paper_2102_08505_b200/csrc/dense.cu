@@ -108,7 +108,7 @@ template <int BM, int TY, bool SYM>
 __global__ void __launch_bounds__(16 * TY, BM == 128 ? (TY == 8 ? 2 : 1) : 4)
     dense_gemm_kernel(const double* __restrict__ At, const double* __restrict__ B, int np,
                       const unsigned char* __restrict__ fa, const unsigned char* __restrict__ fb,
-                      double* __restrict__ S, unsigned long long* exec) {
+                      double* __restrict__ S, unsigned char* __restrict__ tw, unsigned long long* exec) {
     static_assert(!SYM || BM == kDenseTile, "symmetric tiles are square");
     constexpr int NT = 16 * TY, NW = NT / 32, RM = BM / TY, SB = stage_bytes<BM>();
     extern __shared__ __align__(16) unsigned char smem[];
@@ -245,7 +245,13 @@ __global__ void __launch_bounds__(16 * TY, BM == 128 ? (TY == 8 ? 2 : 1) : 4)
 #if !ELL_DENSE_TMA
     cp_async_wait<0>();
 #endif
-    // tile (bi, bj), and for SYM off the diagonal its transpose at (bj, bi)
+    // tile (bi, bj), and for SYM off the diagonal its transpose at (bj, bi). A tile with no occupied k
+    // block is exactly zero: it is not stored, its tw flag tells the epilogue to read zeros instead
+    if (tid == 0) {
+        tw[(size_t)bi * T + bj] = nact > 0;
+        if (SYM && bi != bj) tw[(size_t)bj * T + bi] = nact > 0;
+    }
+    if (nact == 0) return;
 #pragma unroll
     for (int g = 0; g < RM / 2; ++g)
 #pragma unroll
@@ -271,7 +277,8 @@ __global__ void __launch_bounds__(16 * TY, BM == 128 ? (TY == 8 ? 2 : 1) : 4)
 
 template <int BM, int TY, bool SYM>
 cudaError_t launch_gemm_t(unsigned grid, const double* At, const double* B, int np, const unsigned char* fa,
-                          const unsigned char* fb, double* S, unsigned long long* exec, cudaStream_t s) {
+                          const unsigned char* fb, double* S, unsigned char* tw, unsigned long long* exec,
+                          cudaStream_t s) {
     static int attr = 0;  // dynamic shared memory opted in so far (per instantiation)
     const size_t smem = (size_t)kDenseStages * stage_bytes<BM>() + sizeof(int) * (size_t)(np / kDenseK);
     if (smem > 48 * 1024 && attr < (int)smem) {
@@ -280,22 +287,51 @@ cudaError_t launch_gemm_t(unsigned grid, const double* At, const double* B, int 
         if (e) return e;
         attr = (int)smem;
     }
-    dense_gemm_kernel<BM, TY, SYM><<<grid, 16 * TY, smem, s>>>(At, B, np, fa, fb, S, exec);
+    dense_gemm_kernel<BM, TY, SYM><<<grid, 16 * TY, smem, s>>>(At, B, np, fa, fb, S, tw, exec);
     return cudaGetLastError();
 }
 
-cudaError_t launch_dense_gemm(const double* At, const double* B, int np, bool sym, const unsigned char* fa,
-                              const unsigned char* fb, double* S, unsigned long long* exec, int num_sms,
-                              cudaStream_t s) {
-    if (np <= 0 || np % kDenseTile) return cudaErrorInvalidValue;
+int dense_tile_rows(int np, bool sym, int num_sms) {
     const int T = np / kDenseTile;
     const int tiles = sym ? T * (T + 1) / 2 : T * T;
     // 128-row tiles while they fill most of the SMs; below that 16-row tiles (8x the CTAs)
-    if (tiles >= (num_sms * 4) / 5) {
-        if (sym) return launch_gemm_t<128, ELL_DENSE_TY, true>((unsigned)tiles, At, B, np, fa, fb, S, exec, s);
-        return launch_gemm_t<128, ELL_DENSE_TY, false>((unsigned)tiles, At, B, np, fa, fb, S, exec, s);
+    return tiles >= (num_sms * 4) / 5 ? 128 : 16;
+}
+
+cudaError_t launch_dense_gemm(const double* At, const double* B, int np, bool sym, const unsigned char* fa,
+                              const unsigned char* fb, double* S, unsigned char* tw, unsigned long long* exec,
+                              int num_sms, cudaStream_t s) {
+    if (np <= 0 || np % kDenseTile) return cudaErrorInvalidValue;
+    const int T = np / kDenseTile;
+    if (dense_tile_rows(np, sym, num_sms) == 128) {
+        if (sym)
+            return launch_gemm_t<128, ELL_DENSE_TY, true>((unsigned)(T * (T + 1) / 2), At, B, np, fa, fb, S, tw, exec, s);
+        return launch_gemm_t<128, ELL_DENSE_TY, false>((unsigned)(T * T), At, B, np, fa, fb, S, tw, exec, s);
     }
-    return launch_gemm_t<16, 8, false>((unsigned)(8 * T * T), At, B, np, fa, fb, S, exec, s);
+    return launch_gemm_t<16, 8, false>((unsigned)(8 * T * T), At, B, np, fa, fb, S, tw, exec, s);
+}
+
+// Zero the 128 x 16 blocks of D that fa flags (D holds nonzeros only there): the dense array returns
+// to all-zero at the cost of the previous iterate's band instead of N^2. A warp per block.
+__global__ void __launch_bounds__(256) dense_clear_kernel(double* __restrict__ D, int np,
+                                                          const unsigned char* __restrict__ fa) {
+    const int lane = threadIdx.x & 31;
+    const int KB = np / kDenseK;
+    const int64_t nblk = (int64_t)(np / kDenseTile) * KB;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nblk; b += nw) {
+        if (!fa[b]) continue;
+        const int64_t bi = b / KB, kb = b % KB;
+        double* base = D + (size_t)bi * kDenseTile * np + (size_t)kb * kDenseK;
+        // 128 rows x 16 doubles: 1024 16-byte stores, 32 per lane (8 lanes per row)
+#pragma unroll 4
+        for (int q = lane; q < 1024; q += 32) stg128(base + (size_t)(q >> 3) * np + 2 * (q & 7), 0.0, 0.0);
+    }
+}
+
+cudaError_t launch_dense_clear(double* D, int np, const unsigned char* fa, int num_sms, cudaStream_t s) {
+    dense_clear_kernel<<<(unsigned)(num_sms * 8), 256, 0, s>>>(D, np, fa);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------- emission
@@ -311,7 +347,9 @@ cudaError_t launch_dense_gemm(const double* At, const double* B, int np, bool sy
 template <int MODE>
 __global__ void __launch_bounds__(256) dense_emit_kernel(const double* __restrict__ S, int np, const RowOpParams p,
                                                          const double* __restrict__ dA,
-                                                         const double* __restrict__ dOld) {
+                                                         const double* __restrict__ dOld,
+                                                         const unsigned char* __restrict__ tw, int tw_rows,
+                                                         const unsigned char* __restrict__ fold) {
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const int n = (int)p.ncols;
@@ -330,13 +368,21 @@ __global__ void __launch_bounds__(256) dense_emit_kernel(const double* __restric
         int32_t* cc = p.C.col + (size_t)i * cw;
         int kept = 0;
         double ds = 0.0, dc = 0.0, nrm = 0.0;
+        const int T = np / kDenseTile, KB = np / kDenseK;
+        const unsigned char* twr = tw + (size_t)(i / tw_rows) * T;
+        const unsigned char* fr = MODE != 0 ? fold + (size_t)(i / kDenseTile) * KB : nullptr;
         for (int j0 = 0; j0 < n; j0 += 128) {
+            // the tile of S was not stored (exactly zero) / the Old row has no entry in these 128
+            // columns (its 8 occupancy flags): read zeros; both -> nothing to emit or sum here
+            const bool s_ok = twr[j0 >> 7] != 0;
+            const bool x_ok = MODE != 0 && *reinterpret_cast<const unsigned long long*>(fr + (j0 >> 4)) != 0ull;
+            if (!s_ok && !x_ok) continue;
             double sv[4], xv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int j = j0 + 32 * u + lane;
-                sv[u] = j < n ? __ldcs(srow + j) : 0.0;  // S is read once: streaming
-                xv[u] = (MODE != 0 && j < n) ? xrow[j] : 0.0;
+                sv[u] = (s_ok && j < n) ? __ldcs(srow + j) : 0.0;  // S is read once: streaming
+                xv[u] = (x_ok && j < n) ? xrow[j] : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -388,16 +434,17 @@ __global__ void __launch_bounds__(256) dense_emit_kernel(const double* __restric
 }
 
 cudaError_t launch_dense_emit(const double* S, int np, const RowOpParams& p, const double* dA, const double* dOld,
-                              int num_sms, cudaStream_t s) {
+                              const unsigned char* tw, int tw_rows, const unsigned char* fold, int num_sms,
+                              cudaStream_t s) {
     const int64_t rows = p.row_end - p.row_begin;
     if (rows <= 0) return cudaSuccess;
-    if (p.old_mode != 0 && !dOld) return cudaErrorInvalidValue;
+    if (p.old_mode != 0 && (!dOld || !fold)) return cudaErrorInvalidValue;
     int64_t blocks = (rows + 7) / 8;
     if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
     const int mode = p.old_mode == 0 ? 0 : (p.normsq ? 2 : 1);  // as the row kernels' MODE
-    if (mode == 0) dense_emit_kernel<0><<<(unsigned)blocks, 256, 0, s>>>(S, np, p, dA, dOld);
-    else if (mode == 1) dense_emit_kernel<1><<<(unsigned)blocks, 256, 0, s>>>(S, np, p, dA, dOld);
-    else dense_emit_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(S, np, p, dA, dOld);
+    if (mode == 0) dense_emit_kernel<0><<<(unsigned)blocks, 256, 0, s>>>(S, np, p, dA, dOld, tw, tw_rows, fold);
+    else if (mode == 1) dense_emit_kernel<1><<<(unsigned)blocks, 256, 0, s>>>(S, np, p, dA, dOld, tw, tw_rows, fold);
+    else dense_emit_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(S, np, p, dA, dOld, tw, tw_rows, fold);
     return cudaGetLastError();
 }
 

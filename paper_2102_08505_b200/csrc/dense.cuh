@@ -23,17 +23,26 @@ cudaError_t launch_densify(KMat a, int64_t n, int np, bool transpose, double* D,
 // S = A B over the k blocks whose flags are both set (nullable flags: every block), k ascending:
 // At is A transposed (At[k][m] = a_mk); sym: A B is symmetric (A = B = B^T), only tiles bi <= bj are
 // computed and each is also stored transposed. exec (nullable) += FMAs executed.
-// Tiles of 128 rows x 128 columns while they fill most SMs, else 16 x 128 (small N).
+// Tiles of dense_tile_rows(...) = 128 rows x 128 columns while they fill most SMs, else 16 x 128
+// (small N). A tile with no occupied k block is not stored: tw[(row / tile rows) * (np / 128) +
+// column / 128] = 0 for it, 1 for a stored tile (every entry written by the launch).
+int dense_tile_rows(int np, bool sym, int num_sms);
 cudaError_t launch_dense_gemm(const double* At, const double* B, int np, bool sym, const unsigned char* fa,
-                              const unsigned char* fb, double* S, unsigned long long* exec, int num_sms,
-                              cudaStream_t s);
+                              const unsigned char* fb, double* S, unsigned char* tw, unsigned long long* exec,
+                              int num_sms, cudaStream_t s);
+
+// D <- 0 given that D is zero outside the 128 x 16 blocks fa flags (the previous densify's).
+cudaError_t launch_dense_clear(double* D, int np, const unsigned char* fa, int num_sms, cudaStream_t s);
 
 // Rows [p.row_begin, p.row_end) of C from the dense S (row stride np): combine with Old (p.old_mode),
 // drop, compact, write, diagonals, norm and status as the row kernels do (RowOpParams).
 // dA (row stride np; read only with p.diag_a): a dense copy of A whose diagonal is the stored a_ii;
-// dOld (row stride np; required when p.old_mode != 0): the dense copy of Old.
+// dOld (row stride np; required when p.old_mode != 0): the dense copy of Old, zero outside the
+// 128 x 16 blocks its flags fold ([np/128][np/16], as launch_densify's fa) mark. S is read only where
+// tw (tile rows tw_rows) says the GEMM stored it.
 cudaError_t launch_dense_emit(const double* S, int np, const RowOpParams& p, const double* dA, const double* dOld,
-                              int num_sms, cudaStream_t s);
+                              const unsigned char* tw, int tw_rows, const unsigned char* fold, int num_sms,
+                              cudaStream_t s);
 
 size_t dense_gemm_smem(int np);
 
