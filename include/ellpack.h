@@ -136,17 +136,21 @@ int ellpack_ctx_set_stream(ellpack_ctx ctx, void* stream);
  *                          (one synchronisation per iteration), 2 = the device loop whenever it
  *                          applies (one rank). Results are bitwise the same either way.
  *                          With the dense regime available (ELLPACK_OPT_DENSE 0), automatic picks
- *                          the host loop, whose steps can switch to the dense GEMM.
- *  ELLPACK_OPT_DENSE       the dense-regime step (one rank, N <= 32768): X_n is scattered into an
- *                          N x N array and S = X_n^2 runs as a dense FP64 GEMM (k blocks empty on
- *                          either side skipped; only the upper triangle of tiles when X_n is
- *                          symmetric), then one warp per row combines, drops and compacts S into
+ *                          the device loop (every step dense) for N <= 1024 and otherwise the host
+ *                          loop, whose steps switch to the dense GEMM when it is predicted faster.
+ *  ELLPACK_OPT_DENSE       the dense-regime step (one rank, N <= 65536, X X only): X_n is scattered
+ *                          into an N x N array and S = X_n^2 runs as a dense FP64 GEMM (k blocks
+ *                          empty on either side skipped; only the upper triangle of tiles when X_n
+ *                          is symmetric), then one warp per row combines, drops and compacts S into
  *                          X_{n+1}. Every output is still one fma chain over k ascending -- the
  *                          extra terms are exact zeros -- so results are bitwise those of the
- *                          sparse kernels. 0 (default) = automatic: an SP2 step goes dense when
- *                          N^3 < 16 x the estimated products of the step and 3 N^2 doubles fit in
- *                          half the free device memory; 1 = never; 2 = always (every SP2 step on
- *                          one rank and every ellpack_multiply_x2; tests). */
+ *                          sparse kernels. 0 (default) = automatic: an SP2 step goes dense when its
+ *                          predicted time (FMAs of the k blocks inside X_n's band at the last dense
+ *                          step's rate) is below 0.85 x the sparse prediction (the step's estimated
+ *                          products at the last sparse step's rate), and the 2 (symmetric X) or 3
+ *                          N^2-double arrays fit in 60% of the free device memory; 1 = never;
+ *                          2 = always when they fit (every SP2 step on one rank and every
+ *                          ellpack_multiply_x2; tests). */
 enum { ELLPACK_OPT_WINDOW = 1, ELLPACK_OPT_WARPS = 2, ELLPACK_OPT_SP2_WIDTH0 = 3, ELLPACK_OPT_PROFILE = 4,
        ELLPACK_OPT_ABLATE = 5, ELLPACK_OPT_GENERAL_WINDOW = 6, ELLPACK_OPT_VALIDATE = 7,
        ELLPACK_OPT_SP2_SYMMETRIC = 8, ELLPACK_OPT_SP2_MEM_CAP = 9, ELLPACK_OPT_RING_KERNEL = 10,

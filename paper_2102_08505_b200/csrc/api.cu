@@ -129,8 +129,11 @@ struct ellpack_ctx_s {
     int dense_opt = 0;     // ELLPACK_OPT_DENSE
     Buf dense[3];          // dense regime: X (or B), X^T (non-symmetric A), S -- np x np doubles each
     Buf dflags;            // dense regime: k-block occupancy of the left and right operands
+    Buf docc;              // dense regime: occupancy bitsets of the next SP2 operand (exact GEMM work)
     int last_dense = 0;    // the last SP2 step / X^2 ran in the dense regime
     int64_t dense_clean_np = 0;  // dense[0] is zero outside the blocks dflags' fa marks (for this N_p)
+    int64_t dense_fit_key = -1;  // dense_fits: the cached free-memory answer (N_p, arrays)
+    bool dense_fit_ok = false;
     struct Host {
         int32_t bw[8];
         int32_t status_u[2];
@@ -629,7 +632,7 @@ int enqueue_canonical(ellpack_ctx c, const double* const* arrays, int narr, int6
 }
 
 // ---- dense regime (dense.cu): S = A B as a dense FP64 GEMM, then the row epilogue
-constexpr int64_t kDenseMaxN = 32768;
+constexpr int64_t kDenseMaxN = 65536;
 
 int64_t dense_np(int64_t n) { return (n + kDenseTile - 1) / kDenseTile * kDenseTile; }
 
@@ -647,9 +650,14 @@ bool dense_fits(ellpack_ctx c, int64_t n, int bufs) {
         if ((double)c->dense[b].bytes < one) need += one;
     }
     if (need == 0.0) return true;
+    // one driver query per (N_p, arrays) until the context's dense arrays change (sp2_run resets it)
+    const int64_t key = np * 4 + bufs;
+    if (c->dense_fit_key == key) return c->dense_fit_ok;
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return false; }
-    return need <= 0.5 * (double)fr;
+    c->dense_fit_key = key;
+    c->dense_fit_ok = need <= 0.6 * (double)fr;
+    return c->dense_fit_ok;
 }
 
 // FMAs the symmetric dense GEMM runs on X^2 for X of half-bandwidth h (every 128 x 16 block within
@@ -998,7 +1006,7 @@ int ellpack_ctx_destroy(ellpack_ctx c) {
                    &c->stash_val, &c->stash_col, &c->ident_val, &c->ident_col, &c->ident_nnz,
                    &c->hx_val, &c->hx_col, &c->hx_nnz, &c->hy_val, &c->hy_col, &c->hy_nnz,
                    &c->bt, &c->bt_nbin, &c->bp, &c->halo, &c->vflag, &c->symaux, &c->sp2dev, &c->sp2rec,
-                   &c->dense[0], &c->dense[1], &c->dense[2], &c->dflags};
+                   &c->dense[0], &c->dense[1], &c->dense[2], &c->dflags, &c->docc};
     if (c->sp2_exec) cudaGraphExecDestroy(c->sp2_exec);
     if (c->x2_exec) cudaGraphExecDestroy(c->x2_exec);
     for (auto& sl : c->it)
@@ -1962,6 +1970,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     }
     sp2_opts o;
     if (opts_in) o = *opts_in; else sp2_opts_default(&o);
+    c->dense_fit_key = -1;  // free memory is asked again once per run
     if (!valid_tau(o.threshold) || o.max_iter < 1) return ELLPACK_ERR_ARG;
     if (o.branch_rule != SP2_RULE_TRACE_SIGN && o.branch_rule != SP2_RULE_TRACE_CLOSEST) return ELLPACK_ERR_ARG;
     CK(cudaSetDevice(c->device));
@@ -2089,9 +2098,15 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     int stop = -1;
     int it;
     double p_prev = 0.0, p_prev2 = 0.0;  // products of the last two steps (dense-regime decision)
-    // measured rates of the two regimes (pattern products / s of a sparse step; dense_band_fmas / s of
-    // a dense step), seeded with cfg3's (tools/dense_switch.py, profiles/r02_dense_switch_cfg3.log)
-    double rate_sparse = 1.2e12, rate_dense = 1.0e13;
+    // measured rates of the two regimes (pattern products / s of a sparse step; GEMM FMAs / s of a
+    // dense step, densify and epilogue included), seeded below the long steps' rates of cfg3 and cfg4
+    // (tools/dense_switch.py, profiles/r02_dense_switch_*.log)
+    double rate_sparse = 5e11, rate_dense = 5e12;  // (dense: FMAs / s)
+    bool dense_tried = false;  // a dense step ran in this run (its rate replaced the seed)
+    // X_{n+1}'s exact dense work is measured after every step while the automatic regime may pick dense
+    // (symmetric X, one rank): w_next FMAs, 0 = not measured
+    const bool measure_work = sym && !c->comm && c->dense_opt == 0 && n <= kDenseMaxN;
+    double w_next = 0.0;
     UpperAlloc ua{&U, n, 0};
     bool halo_pending = false;  // the halo of X_n travels on the side stream (communicator only)
     const bool dev_loop = use_device_loop(c, n, maxw, sym);
@@ -2136,14 +2151,21 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
         bool dense_step = false;
         double w_dense = 0.0, p_est = 0.0;
         if (!c->comm && c->dense_opt != 1 && dense_fits(c, n, sym ? 2 : 3)) {
-            w_dense = dense_band_fmas(n, std::max(bwX[0], bwX[1]), sym);
+            // the GEMM's exact work when the last step measured X_n's block occupancy (symmetric X),
+            // else the band model
+            w_dense = w_next > 0.0 ? w_next : dense_band_fmas(n, std::max(bwX[0], bwX[1]), sym);
             if (c->dense_opt == 2) {
                 dense_step = true;
             } else if (p_prev > 0.0) {
                 // (growth per step <= 2: cfg3's early steps grow 1.5-1.9x once past X0)
                 const double g = p_prev2 > 0.0 ? std::min(2.0, std::max(1.0, p_prev / p_prev2)) : 1.0;
                 p_est = p_prev * g;
-                dense_step = w_dense / rate_dense < 0.85 * p_est / rate_sparse;
+                const double t_d = w_dense / rate_dense, t_s = p_est / rate_sparse;
+                dense_step = t_d < 0.85 * t_s;
+                // the band model counts every block inside the band as occupied: iterates with holes in
+                // their band (cfg4's lattice) run faster than it predicts, which only a measured dense
+                // step reveals -- one exploratory dense step per run when the prediction is close
+                if (!dense_step && !dense_tried && t_s > 5e-3 && t_d < 1.5 * t_s) dense_step = true;
             }
         }
         c->last_dense = 0;
@@ -2233,6 +2255,20 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             if ((rc = enqueue_canonical(c, arrs, narr, n))) { status = rc; break; }
             // the probe of X_{n+1} for the next step (its own rows; reaches all-gathered)
             if ((rc = enqueue_next_probe(c, &Y.d))) { status = rc; break; }
+            if (measure_work) {
+                // the next step's dense work, exactly: occupancy bitsets of X_{n+1}, then the occupied
+                // (tile, k block) pairs of the symmetric GEMM -- read back with this step's status
+                const int64_t np = dense_np(n);
+                const size_t fw = (size_t)(np / kDenseTile) * (size_t)((np / kDenseK + 63) / 64);
+                RK(grow(c, c->docc, fw * 8));
+                CK(cudaMemsetAsync(c->docc.p, 0, fw * 8, c->stream));
+                CK(cudaMemsetAsync(c->d_keys + 5, 0, 8, c->stream));
+                CK(launch_occupancy(kmat(&Y.d), n, (int)np, (unsigned long long*)c->docc.p, c->num_sms, c->stream));
+                CK(launch_dense_work((const unsigned long long*)c->docc.p, (int)np, c->d_keys + 5, c->num_sms,
+                                     c->stream));
+                c->launches += 2;
+                CK(cudaMemcpyAsync(&c->h->keys[2], c->d_keys + 5, 8, cudaMemcpyDeviceToHost, c->stream));
+            }
             cudaEventRecord(c->ev[2], c->stream);
             if ((rc = fetch(c, narr, true))) { status = rc; break; }
             float ms1 = 0.f, ms2 = 0.f;
@@ -2313,13 +2349,15 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
         if (closest) t2 = c->h->sums[3];
         p_prev2 = p_prev;
         p_prev = (double)c->h->keys[0];
+        if (measure_work) w_next = (double)c->h->keys[2] * kDenseK * kDenseTile * kDenseTile;
         // the rates the next regime choice predicts with (device time of this step)
-        if (step_ms >= 1.0) {  // steps long enough for their rate to carry over
-            if (c->last_dense) {
-                if (w_dense > 0.0) rate_dense = w_dense / (step_ms * 1e-3);
-            } else if (p_prev > 0.0) {
-                rate_sparse = p_prev / (step_ms * 1e-3);
-            }
+        // (only steps long enough for their rate to carry over: short sparse steps run far below the
+        // rate of the long ones -- cfg4's iteration 1 at 1.4e11 products/s, iteration 5 at 7.8e11)
+        if (c->last_dense && step_ms >= 1.0) {
+            dense_tried = true;
+            if (w_dense > 0.0) rate_dense = w_dense / (step_ms * 1e-3);
+        } else if (!c->last_dense && step_ms >= 10.0 && p_prev > 0.0) {
+            rate_sparse = p_prev / (step_ms * 1e-3);
         }
         take_probe(c, bwX, needX);
         // the next step reads only the rows of X_{n+1} its rows reference (band-aware halo, f1),

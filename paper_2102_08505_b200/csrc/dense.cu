@@ -334,6 +334,72 @@ cudaError_t launch_dense_clear(double* D, int np, const unsigned char* fa, int n
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------- dense work of X X
+
+// F[t][w] bit b = some entry of x in rows [128 t, 128 t + 128) and columns [16 (64 w + b), + 16):
+// the left operand's 128 x 16 occupancy as bitsets (for a symmetric x also the right operand's,
+// transposed). A warp per row; each lane ORs the bits of a contiguous piece of the (ascending) row
+// in a register and flushes one atomicOr per 64-bit word it touches.
+__global__ void __launch_bounds__(256) occupancy_kernel(KMat x, int64_t n, int kbw, unsigned long long* __restrict__ F) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+        const int nnz = x.nnz[i];
+        const int32_t* c = x.col + (size_t)i * x.w;
+        unsigned long long* row = F + (size_t)(i / kDenseTile) * kbw;
+        const int per = (nnz + 31) / 32;
+        const int q0 = lane * per, q1 = min(nnz, q0 + per);
+        int word = -1;
+        unsigned long long bits = 0ull;
+        for (int q = q0; q < q1; ++q) {
+            const int kb = c[q] / kDenseK;
+            if ((kb >> 6) != word) {
+                if (bits) atomicOr(row + word, bits);
+                word = kb >> 6;
+                bits = 0ull;
+            }
+            bits |= 1ull << (kb & 63);
+        }
+        if (bits) atomicOr(row + word, bits);
+    }
+}
+
+cudaError_t launch_occupancy(KMat x, int64_t n, int np, unsigned long long* F, int num_sms, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t blocks = (n + 7) / 8;
+    occupancy_kernel<<<(unsigned)(blocks < (int64_t)num_sms * 16 ? blocks : (int64_t)num_sms * 16), 256, 0, s>>>(
+        x, n, np / kDenseK / 64 + ((np / kDenseK) % 64 ? 1 : 0), F);
+    return cudaGetLastError();
+}
+
+// out += the occupied k blocks of every symmetric tile bi <= bj: popc(F[bi] & F[bj]) (x symmetric:
+// row block bj's occupancy is column tile bj's) -- the symmetric GEMM's work, exactly, in k blocks.
+__global__ void __launch_bounds__(256) dense_work_kernel(const unsigned long long* __restrict__ F, int T, int kbw,
+                                                         unsigned long long* out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t tiles = (int64_t)T * T;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    unsigned long long mine = 0ull;
+    for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < tiles; t += nw) {
+        const int bi = (int)(t / T), bj = (int)(t % T);
+        if (bj < bi) continue;
+        const unsigned long long* a = F + (size_t)bi * kbw;
+        const unsigned long long* b = F + (size_t)bj * kbw;
+        for (int w = lane; w < kbw; w += 32) mine += (unsigned long long)__popcll(a[w] & b[w]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(FULL, mine, o);
+    if (lane == 0 && mine) atomicAdd(out, mine);
+}
+
+cudaError_t launch_dense_work(const unsigned long long* F, int np, unsigned long long* out, int num_sms,
+                              cudaStream_t s) {
+    const int T = np / kDenseTile;
+    const int kbw = np / kDenseK / 64 + ((np / kDenseK) % 64 ? 1 : 0);
+    dense_work_kernel<<<(unsigned)(num_sms * 4), 256, 0, s>>>(F, T, kbw, out);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------- emission
 
 // MODE as the row kernels: 0 no Old operand; 1 Old operand; 2 Old operand and the norm

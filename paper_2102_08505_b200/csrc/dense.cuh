@@ -44,6 +44,13 @@ cudaError_t launch_dense_emit(const double* S, int np, const RowOpParams& p, con
                               const unsigned char* tw, int tw_rows, const unsigned char* fold, int num_sms,
                               cudaStream_t s);
 
+// The symmetric GEMM's exact work for a symmetric x (the next step's operand), without densifying
+// it: occupancy bitsets F ([np/128][ceil(np/16/64)] words, zeroed by the caller), then
+// out += the number of (tile bi <= bj, k block) pairs occupied on both sides.
+cudaError_t launch_occupancy(KMat x, int64_t n, int np, unsigned long long* F, int num_sms, cudaStream_t s);
+cudaError_t launch_dense_work(const unsigned long long* F, int np, unsigned long long* out, int num_sms,
+                              cudaStream_t s);
+
 size_t dense_gemm_smem(int np);
 
 }  // namespace ell

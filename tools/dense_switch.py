@@ -16,8 +16,8 @@ import synth  # noqa: E402
 eb.build()
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 40
 which = sys.argv[2] if len(sys.argv) > 2 else "cfg3"
-if which == "cfg3":
-    H, cf = synth.cfg3(), synth.CFG3
+if which in ("cfg3", "cfg4"):
+    H, cf = (synth.cfg3(), synth.CFG3) if which == "cfg3" else (synth.cfg4(), synth.CFG4)
     nocc, tol, tau = cf["nocc"], cf["tol"], cf["threshold"]
 else:
     H = synth.model_hamiltonian(int(which.split(":")[1]), which.split(":")[0], tau_store=1e-5)

@@ -1,6 +1,6 @@
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-timeout 1500 python -m pytest tests/test_gpu_dense.py tests/test_gpu_parity.py tests/test_gpu_parity_r2.py -q -x > gpurun_out/dense_tests.log 2>&1; echo "rc=$?" >> gpurun_out/dense_tests.log
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests.log
 timeout 900 python bench.py --workload sp2 --sp2-model soft_matter --sp2-n 16384 --sp2-iters 100 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/bench_sp2_soft.log 2>&1; echo "rc=$?" >> gpurun_out/bench_sp2_soft.log
 timeout 900 python tools/dense_switch.py 40 soft_matter:16384 > gpurun_out/dense_switch_soft.log 2>&1
 timeout 900 python tools/dense_switch.py 40 cfg3 > gpurun_out/dense_switch.log 2>&1
