@@ -134,6 +134,7 @@ struct ellpack_ctx_s {
     int64_t dense_clean_np = 0;  // dense[0] is zero outside the blocks dflags' fa marks (for this N_p)
     int64_t dense_fit_key = -1;  // dense_fits: the cached free-memory answer (N_p, arrays)
     bool dense_fit_ok = false;
+    bool dense_full_clear = false;  // the last dense step zeroed the whole array (one-time cost)
     struct Host {
         int32_t bw[8];
         int32_t status_u[2];
@@ -700,19 +701,23 @@ int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym) {
     RK(grow(c, c->dense[0], bytes));
     RK(grow(c, c->dense[2], bytes));
     if (!sym) RK(grow(c, c->dense[1], bytes));
-    const size_t fbytes = 2 * (size_t)T * KB;                      // fa | fb
+    const size_t fbytes = 2 * (size_t)T * KB;                      // fa | fb (bytes)
+    const size_t bbytes = 2 * (size_t)T * dense_kbw((int)np) * 8;   // Fa | Fb (bitsets)
     const size_t tbytes = (size_t)(np / 16) * T;                    // tw (16-row tiles at most)
-    RK(grow(c, c->dflags, fbytes + tbytes));
+    RK(grow(c, c->dflags, fbytes + bbytes + tbytes));
     if (c->dense[0].p != d0 || c->dflags.p != f0) c->dense_clean_np = 0;  // reallocated: contents unknown
     unsigned char* fa = (unsigned char*)c->dflags.p;
     unsigned char* fb = fa + (size_t)T * KB;
-    unsigned char* tw = fa + fbytes;
+    unsigned long long* Fa = (unsigned long long*)(fa + fbytes);
+    unsigned long long* Fb = Fa + (size_t)T * dense_kbw((int)np);
+    unsigned char* tw = fa + fbytes + bbytes;
     double* D = (double*)c->dense[0].p;                    // X (row-major): B, Old
     double* Dt = sym ? D : (double*)c->dense[1].p;         // X^T: A
     double* S = (double*)c->dense[2].p;
     // D is zero outside the blocks fa flags (the last densify's) when dense_clean_np == np: clearing
     // those costs the previous iterate's band instead of N^2
-    if (c->dense_clean_np == np) {
+    c->dense_full_clear = c->dense_clean_np != np;
+    if (!c->dense_full_clear) {
         CK(launch_dense_clear(D, (int)np, fa, c->num_sms, c->stream));
         c->launches++;
     } else {
@@ -729,10 +734,12 @@ int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym) {
         c->launches += 2;
     }
     c->dense_clean_np = np;  // D = X, nonzero only in fa's blocks (A = B = X)
+    CK(launch_pack_flags(fa, fb, (int)np, Fa, Fb, c->num_sms, c->stream));
+    c->launches++;
     // ELLPACK_OPT_PROFILE: the GEMM is this op's "row kernel" (ellpack_ctx_kernel_time)
     const int pk = c->prof_n < 4 ? c->prof_n : 3;
     if (c->profile) CK(cudaEventRecord(c->pev[pk][0], c->stream));
-    CK(launch_dense_gemm(Dt, D, (int)np, sym, fa, fb, S, tw, p.exec_products, c->num_sms, c->stream));
+    CK(launch_dense_gemm(Dt, D, (int)np, sym, Fa, Fb, S, tw, p.exec_products, c->num_sms, c->stream));
     if (c->profile) {
         CK(cudaEventRecord(c->pev[pk][1], c->stream));
         c->prof_n = pk + 1;
@@ -744,7 +751,7 @@ int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym) {
     // stored a_ii of A: the diagonal of either dense copy of A; Old = X: its dense copy D and flags fa
     const double* dA = sym ? D : Dt;
     CK(launch_dense_emit(S, (int)np, p, dA, p.old_mode != 0 ? D : nullptr, tw,
-                         dense_tile_rows((int)np, sym, c->num_sms), fa, c->num_sms, c->stream));
+                         dense_tile_rows((int)np, sym, c->num_sms), Fa, c->num_sms, c->stream));
     c->launches++;
     c->last_upper = 0;
     c->last_dense = 1;
@@ -1800,6 +1807,7 @@ int sp2_device_loop(ellpack_ctx c, const sp2_opts& o, int64_t n, int64_t nocc, d
         RK(grow(c, c->dense[2], bytes));
         if (!sym) RK(grow(c, c->dense[1], bytes));
         RK(grow(c, c->dflags, 2 * (size_t)(np / kDenseTile) * (size_t)(np / kDenseK) +
+                                  2 * (size_t)(np / kDenseTile) * dense_kbw((int)np) * 8 +
                                   (size_t)(np / 16) * (size_t)(np / kDenseTile)));
         // the captured steps clear D by the previous step's flags: start from D = 0, flags = 0
         CK(cudaMemsetAsync(c->dense[0].p, 0, bytes, c->stream));
@@ -2101,7 +2109,8 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     // measured rates of the two regimes (pattern products / s of a sparse step; GEMM FMAs / s of a
     // dense step, densify and epilogue included), seeded below the long steps' rates of cfg3 and cfg4
     // (tools/dense_switch.py, profiles/r02_dense_switch_*.log)
-    double rate_sparse = 5e11, rate_dense = 5e12;  // (dense: FMAs / s)
+    double rate_sparse = 5e11, rate_dense = 1e13;  // (dense: FMAs / s)
+    double rate_sparse_seen = 0.0;
     bool dense_tried = false;  // a dense step ran in this run (its rate replaced the seed)
     // X_{n+1}'s exact dense work is measured after every step while the automatic regime may pick dense
     // (symmetric X, one rank): w_next FMAs, 0 = not measured
@@ -2161,11 +2170,15 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
                 const double g = p_prev2 > 0.0 ? std::min(2.0, std::max(1.0, p_prev / p_prev2)) : 1.0;
                 p_est = p_prev * g;
                 const double t_d = w_dense / rate_dense, t_s = p_est / rate_sparse;
-                dense_step = t_d < 0.85 * t_s;
+                dense_step = t_d < (dense_tried ? 0.95 : 0.85) * t_s;  // (a measured dense rate: a thinner margin)
                 // the band model counts every block inside the band as occupied: iterates with holes in
                 // their band (cfg4's lattice) run faster than it predicts, which only a measured dense
                 // step reveals -- one exploratory dense step per run when the prediction is close
                 if (!dense_step && !dense_tried && t_s > 5e-3 && t_d < 1.5 * t_s) dense_step = true;
+                if (getenv("ELLPACK_DEBUG_REGIME"))
+                    fprintf(stderr, "[regime] it %d w %.3e (%s) rate_d %.3e t_d %.3f ms | P_est %.3e rate_s %.3e t_s %.3f ms -> %s\n",
+                            it, w_dense, w_next > 0.0 ? "exact" : "band", rate_dense, t_d * 1e3, p_est, rate_sparse,
+                            t_s * 1e3, dense_step ? "dense" : "sparse");
             }
         }
         c->last_dense = 0;
@@ -2353,11 +2366,14 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
         // the rates the next regime choice predicts with (device time of this step)
         // (only steps long enough for their rate to carry over: short sparse steps run far below the
         // rate of the long ones -- cfg4's iteration 1 at 1.4e11 products/s, iteration 5 at 7.8e11)
-        if (c->last_dense && step_ms >= 1.0) {
+        // (a dense step that zeroed the whole N_p^2 array -- the first of a context -- and a run's first
+        // step carry one-time costs; sparse steps grow more efficient with size: the best rate seen)
+        if (c->last_dense) {
             dense_tried = true;
-            if (w_dense > 0.0) rate_dense = w_dense / (step_ms * 1e-3);
-        } else if (!c->last_dense && step_ms >= 10.0 && p_prev > 0.0) {
-            rate_sparse = p_prev / (step_ms * 1e-3);
+            if (step_ms >= 1.0 && !c->dense_full_clear && w_dense > 0.0) rate_dense = w_dense / (step_ms * 1e-3);
+        } else if (it >= 1 && step_ms >= 10.0 && p_prev >= 1e10) {
+            rate_sparse_seen = std::max(rate_sparse_seen, p_prev / (step_ms * 1e-3));
+            rate_sparse = rate_sparse_seen;
         }
         take_probe(c, bwX, needX);
         // the next step reads only the rows of X_{n+1} its rows reference (band-aware halo, f1),

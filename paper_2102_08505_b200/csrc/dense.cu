@@ -50,6 +50,37 @@ cudaError_t launch_densify(KMat a, int64_t n, int np, bool transpose, double* D,
     return cudaGetLastError();
 }
 
+// Byte flags -> bitsets, one bitset of k blocks per 128-row block (Fa, from fa [T][KB]) and per
+// 128-column tile (Fb, from fb [KB][T]): the GEMM reads one 64-bit word per 64 k blocks instead of a
+// byte per k block (with a strided column of fb) -- at N = 65536 every tile's scan is 64 words.
+__global__ void __launch_bounds__(256) pack_flags_kernel(const unsigned char* __restrict__ fa,
+                                                         const unsigned char* __restrict__ fb, int T, int KB,
+                                                         int kbw, unsigned long long* __restrict__ Fa,
+                                                         unsigned long long* __restrict__ Fb) {
+    const int64_t total = (int64_t)T * kbw;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(t / kbw), w = (int)(t % kbw);
+        unsigned long long a = 0ull, b = 0ull;
+        for (int q = 0; q < 64; ++q) {
+            const int kb = 64 * w + q;
+            if (kb >= KB) break;
+            if (fa[(size_t)r * KB + kb]) a |= 1ull << q;
+            if (fb[(size_t)kb * T + r]) b |= 1ull << q;
+        }
+        Fa[t] = a;
+        Fb[t] = b;
+    }
+}
+
+cudaError_t launch_pack_flags(const unsigned char* fa, const unsigned char* fb, int np, unsigned long long* Fa,
+                              unsigned long long* Fb, int num_sms, cudaStream_t s) {
+    const int T = np / kDenseTile, KB = np / kDenseK, kbw = dense_kbw(np);
+    const int64_t total = (int64_t)T * kbw;
+    const int64_t blocks = (total + 255) / 256;
+    pack_flags_kernel<<<(unsigned)(blocks < num_sms * 4 ? blocks : num_sms * 4), 256, 0, s>>>(fa, fb, T, KB, kbw, Fa, Fb);
+    return cudaGetLastError();
+}
+
 // --------------------------------------------------------------------------------- GEMM
 
 #ifndef ELL_DENSE_STAGES
@@ -107,7 +138,7 @@ __device__ __forceinline__ void stg128(double* p, double x, double y) {
 template <int BM, int TY, bool SYM>
 __global__ void __launch_bounds__(16 * TY, BM == 128 ? (TY == 8 ? 2 : 1) : 4)
     dense_gemm_kernel(const double* __restrict__ At, const double* __restrict__ B, int np,
-                      const unsigned char* __restrict__ fa, const unsigned char* __restrict__ fb,
+                      const unsigned long long* __restrict__ Fa, const unsigned long long* __restrict__ Fb,
                       double* __restrict__ S, unsigned char* __restrict__ tw, unsigned long long* exec) {
     static_assert(!SYM || BM == kDenseTile, "symmetric tiles are square");
     constexpr int NT = 16 * TY, NW = NT / 32, RM = BM / TY, SB = stage_bytes<BM>();
@@ -139,24 +170,33 @@ __global__ void __launch_bounds__(16 * TY, BM == 128 ? (TY == 8 ? 2 : 1) : 4)
     }
     // (the first __syncthreads of the k-block scan below publishes the initialised barriers)
 #endif
-    // the k blocks with an entry on both sides, ascending
+    // the k blocks with an entry on both sides, ascending: one 64-bit word of each bitset per thread
+    const int kbw = dense_kbw(np);
     int nact = 0;
-    for (int k0 = 0; k0 < KB; k0 += NT) {
-        const int kb = k0 + tid;
-        const bool act = kb < KB && (!fa || fa[(size_t)bf * KB + kb]) && (!fb || fb[(size_t)kb * T + bj]);
-        const unsigned m = __ballot_sync(FULL, act);
-        if (lane == 0) wcnt[warp] = __popc(m);
+    for (int w0 = 0; w0 < kbw; w0 += NT) {
+        const int w = w0 + tid;
+        const unsigned long long m = w < kbw ? Fa[(size_t)bf * kbw + w] & Fb[(size_t)bj * kbw + w] : 0ull;
+        const int cnt = __popcll(m);
+        int incl = cnt;  // inclusive warp scan of the counts
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wcnt[warp] = incl;
         __syncthreads();
         int off = nact, tot = 0;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            off += w < warp ? wcnt[w] : 0;
-            tot += wcnt[w];
+        for (int q = 0; q < NW; ++q) {
+            off += q < warp ? wcnt[q] : 0;
+            tot += wcnt[q];
         }
-        if (act) list[off + __popc(m & ((1u << lane) - 1u))] = kb;
+        off += incl - cnt;
+        for (unsigned long long r = m; r; r &= r - 1) list[off++] = 64 * w + __ffsll((long long)r) - 1;
         __syncthreads();
         nact += tot;
     }
+    (void)KB;
     const double* a0 = At + (size_t)bi * BM;
     const double* b0 = B + (size_t)bj * kDenseTile;
 #if ELL_DENSE_TMA
@@ -276,8 +316,8 @@ __global__ void __launch_bounds__(16 * TY, BM == 128 ? (TY == 8 ? 2 : 1) : 4)
 }
 
 template <int BM, int TY, bool SYM>
-cudaError_t launch_gemm_t(unsigned grid, const double* At, const double* B, int np, const unsigned char* fa,
-                          const unsigned char* fb, double* S, unsigned char* tw, unsigned long long* exec,
+cudaError_t launch_gemm_t(unsigned grid, const double* At, const double* B, int np, const unsigned long long* fa,
+                          const unsigned long long* fb, double* S, unsigned char* tw, unsigned long long* exec,
                           cudaStream_t s) {
     static int attr = 0;  // dynamic shared memory opted in so far (per instantiation)
     const size_t smem = (size_t)kDenseStages * stage_bytes<BM>() + sizeof(int) * (size_t)(np / kDenseK);
@@ -298,8 +338,8 @@ int dense_tile_rows(int np, bool sym, int num_sms) {
     return tiles >= (num_sms * 4) / 5 ? 128 : 16;
 }
 
-cudaError_t launch_dense_gemm(const double* At, const double* B, int np, bool sym, const unsigned char* fa,
-                              const unsigned char* fb, double* S, unsigned char* tw, unsigned long long* exec,
+cudaError_t launch_dense_gemm(const double* At, const double* B, int np, bool sym, const unsigned long long* fa,
+                              const unsigned long long* fb, double* S, unsigned char* tw, unsigned long long* exec,
                               int num_sms, cudaStream_t s) {
     if (np <= 0 || np % kDenseTile) return cudaErrorInvalidValue;
     const int T = np / kDenseTile;
@@ -415,7 +455,7 @@ __global__ void __launch_bounds__(256) dense_emit_kernel(const double* __restric
                                                          const double* __restrict__ dA,
                                                          const double* __restrict__ dOld,
                                                          const unsigned char* __restrict__ tw, int tw_rows,
-                                                         const unsigned char* __restrict__ fold) {
+                                                         const unsigned long long* __restrict__ fold) {
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const int n = (int)p.ncols;
@@ -434,14 +474,14 @@ __global__ void __launch_bounds__(256) dense_emit_kernel(const double* __restric
         int32_t* cc = p.C.col + (size_t)i * cw;
         int kept = 0;
         double ds = 0.0, dc = 0.0, nrm = 0.0;
-        const int T = np / kDenseTile, KB = np / kDenseK;
+        const int T = np / kDenseTile;
         const unsigned char* twr = tw + (size_t)(i / tw_rows) * T;
-        const unsigned char* fr = MODE != 0 ? fold + (size_t)(i / kDenseTile) * KB : nullptr;
+        const unsigned long long* fr = MODE != 0 ? fold + (size_t)(i / kDenseTile) * dense_kbw(np) : nullptr;
         for (int j0 = 0; j0 < n; j0 += 128) {
             // the tile of S was not stored (exactly zero) / the Old row has no entry in these 128
             // columns (its 8 occupancy flags): read zeros; both -> nothing to emit or sum here
             const bool s_ok = twr[j0 >> 7] != 0;
-            const bool x_ok = MODE != 0 && *reinterpret_cast<const unsigned long long*>(fr + (j0 >> 4)) != 0ull;
+            const bool x_ok = MODE != 0 && ((fr[j0 >> 10] >> ((j0 >> 4) & 63)) & 0xffull) != 0ull;
             if (!s_ok && !x_ok) continue;
             double sv[4], xv[4];
 #pragma unroll
@@ -500,7 +540,7 @@ __global__ void __launch_bounds__(256) dense_emit_kernel(const double* __restric
 }
 
 cudaError_t launch_dense_emit(const double* S, int np, const RowOpParams& p, const double* dA, const double* dOld,
-                              const unsigned char* tw, int tw_rows, const unsigned char* fold, int num_sms,
+                              const unsigned char* tw, int tw_rows, const unsigned long long* fold, int num_sms,
                               cudaStream_t s) {
     const int64_t rows = p.row_end - p.row_begin;
     if (rows <= 0) return cudaSuccess;

@@ -13,6 +13,9 @@ namespace ell {
 constexpr int kDenseTile = 128;  // rows and columns of S per CTA
 constexpr int kDenseK = 16;      // k rows per pipeline stage
 
+// 64-bit words of one k-block bitset (np / 16 bits)
+__host__ __device__ inline int dense_kbw(int np) { return (np / kDenseK + 63) / 64; }
+
 // D (np x np doubles, zeroed by the caller) <- the stored entries of rows [0, n) of a:
 // D[i][j] = a_ij, or D[j][i] = a_ij with transpose. Occupancy flags (nullable, zeroed by the caller):
 // fa[(i / 128) * (np / 16) + j / 16] = 1 (a as the left operand: (m-block, k-block)),
@@ -23,12 +26,17 @@ cudaError_t launch_densify(KMat a, int64_t n, int np, bool transpose, double* D,
 // S = A B over the k blocks whose flags are both set (nullable flags: every block), k ascending:
 // At is A transposed (At[k][m] = a_mk); sym: A B is symmetric (A = B = B^T), only tiles bi <= bj are
 // computed and each is also stored transposed. exec (nullable) += FMAs executed.
+// fa, fb byte flags (as launch_densify's) -> bitsets Fa[T][kbw] (k blocks of each 128-row block) and
+// Fb[T][kbw] (k blocks of each 128-column tile), kbw = dense_kbw(np).
+cudaError_t launch_pack_flags(const unsigned char* fa, const unsigned char* fb, int np, unsigned long long* Fa,
+                              unsigned long long* Fb, int num_sms, cudaStream_t s);
+
 // Tiles of dense_tile_rows(...) = 128 rows x 128 columns while they fill most SMs, else 16 x 128
 // (small N). A tile with no occupied k block is not stored: tw[(row / tile rows) * (np / 128) +
 // column / 128] = 0 for it, 1 for a stored tile (every entry written by the launch).
 int dense_tile_rows(int np, bool sym, int num_sms);
-cudaError_t launch_dense_gemm(const double* At, const double* B, int np, bool sym, const unsigned char* fa,
-                              const unsigned char* fb, double* S, unsigned char* tw, unsigned long long* exec,
+cudaError_t launch_dense_gemm(const double* At, const double* B, int np, bool sym, const unsigned long long* Fa,
+                              const unsigned long long* Fb, double* S, unsigned char* tw, unsigned long long* exec,
                               int num_sms, cudaStream_t s);
 
 // D <- 0 given that D is zero outside the 128 x 16 blocks fa flags (the previous densify's).
@@ -38,10 +46,10 @@ cudaError_t launch_dense_clear(double* D, int np, const unsigned char* fa, int n
 // drop, compact, write, diagonals, norm and status as the row kernels do (RowOpParams).
 // dA (row stride np; read only with p.diag_a): a dense copy of A whose diagonal is the stored a_ii;
 // dOld (row stride np; required when p.old_mode != 0): the dense copy of Old, zero outside the
-// 128 x 16 blocks its flags fold ([np/128][np/16], as launch_densify's fa) mark. S is read only where
-// tw (tile rows tw_rows) says the GEMM stored it.
+// 128 x 16 blocks its bitsets fold (Fa of launch_pack_flags) mark. S is read only where tw (tile rows
+// tw_rows) says the GEMM stored it.
 cudaError_t launch_dense_emit(const double* S, int np, const RowOpParams& p, const double* dA, const double* dOld,
-                              const unsigned char* tw, int tw_rows, const unsigned char* fold, int num_sms,
+                              const unsigned char* tw, int tw_rows, const unsigned long long* fold, int num_sms,
                               cudaStream_t s);
 
 // The symmetric GEMM's exact work for a symmetric x (the next step's operand), without densifying
