@@ -135,3 +135,50 @@ def test_dense_off_keeps_sparse_kernels(ellpack_lib):
         assert all(it["regime"] == "sparse" for it in g.iters)
     finally:
         c.close()
+
+
+def test_cfg4_window_every_step_dense_bitwise(ellpack_lib):
+    """cfg4 (N = 65536 lattice, the bench's K = 6 window) with every step forced dense -- the
+    65536 x 65536 arrays, 128-row symmetric tiles with mostly-empty k blocks -- against the oracle."""
+    E = ellpack_lib
+    H, cf = synth.cfg4(), synth.CFG4
+    n, K = H.n, 6
+    dw = min(n, 8192)
+    o = oracle.sp2(H, cf["nocc"], cf["tol"], oracle.SP2Opts(threshold=cf["threshold"], max_iter=K), d_width=dw)
+    c = _ctx(E, dense=2, loop=1)
+    try:
+        d = E.Mat.empty(n, dw)
+        g = c.sp2_run(up(H), cf["nocc"], cf["tol"], d, threshold=cf["threshold"], max_iter=K)
+        assert all(it["regime"] == "dense" for it in g.iters)
+        _compare_sp2(g, o)
+        assert same_bits(d.to_host(), o.D)
+    finally:
+        c.close()
+
+
+def test_cfg3_dense_equals_sparse_through_the_fill(ellpack_lib):
+    """cfg3 at full size through the densifying phase (48 iterations: widths 448 -> ~12000, where the
+    oracle needs ~20 min per step): every step dense and every step on the sparse kernels (each
+    bitwise the oracle on the earlier windows) give the same bits -- iterate records, traces, D."""
+    E = ellpack_lib
+    H, cf = synth.cfg3(), synth.CFG3
+    n, K = H.n, 48
+    res = {}
+    for dense in (1, 2):
+        c = _ctx(E, dense=dense, loop=1)
+        try:
+            d = E.Mat.empty(n, n)
+            g = c.sp2_run(up(H), cf["nocc"], cf["tol"], d, threshold=cf["threshold"], max_iter=K)
+            assert all(it["regime"] == ("dense" if dense == 2 else "sparse") for it in g.iters)
+            res[dense] = (g, d.to_host())
+        finally:
+            c.close()
+    (gs, ds), (gd, dd) = res[1], res[2]
+    assert gs.iterations == gd.iterations == K and gs.stop == gd.stop
+    assert gs.final_width == gd.final_width and gs.final_width > 11000
+    for a, b in zip(gs.iters, gd.iters):
+        assert (a["branch"], a["width"], a["required"], a["products"]) == (b["branch"], b["width"], b["required"],
+                                                                          b["products"])
+        assert all(same_bits_scalar(a[k], b[k]) for k in ("trX", "trS", "e"))
+    assert same_bits_scalar(gs.trD, gd.trD)
+    assert same_bits(ds, dd)
