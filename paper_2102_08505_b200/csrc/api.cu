@@ -687,7 +687,8 @@ double dense_band_fmas(int64_t n, int64_t h, bool sym) {
 // p as for enqueue_row_op (A, B, Old, C, alpha, beta, old_mode, tau, diagonals, norm, exec_products);
 // C must not alias A, B or Old; Old (when old_mode != 0) must be B. sym: A = B and bitwise
 // symmetric (one dense array, half the tiles).
-int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym) {
+int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym, const int32_t* bwv = nullptr,
+                     bool halo = false) {
     // the dense regime computes X X (A = B; Old, when present, is X too)
     if (p.A.val != p.B.val || p.A.col != p.B.col || p.A.nnz != p.B.nnz) return ELLPACK_ERR_ARG;
     if (p.old_mode != 0 && (p.Old.val != p.B.val || p.Old.col != p.B.col || p.Old.nnz != p.B.nnz))
@@ -696,6 +697,16 @@ int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym) {
     const int64_t np = dense_np(n);
     const size_t bytes = sizeof(double) * (size_t)np * (size_t)np;
     const int64_t T = np / kDenseTile, KB = np / kDenseK;
+    // a rank's row block (communicator): S rows [r0, r1) from the X rows they reference -- its own
+    // and the halo rows [k0, k1) the probe's reach names (symmetric X: X^T = X, one dense copy)
+    const int64_t r0 = p.row_begin, r1 = p.row_end;
+    const bool part = r0 != 0 || r1 != n;
+    if (part && (!sym || r0 % kDenseTile || (r1 - r0) % kDenseTile)) return ELLPACK_ERR_ARG;
+    int64_t x0 = 0, x1 = n;  // rows of X densified (without a probe: every row is local)
+    if (part && bwv) {
+        x0 = std::min<int64_t>(r0, std::max<int64_t>(0, (int64_t)INT_MAX - bwv[5]));
+        x1 = std::max<int64_t>(r1, std::min<int64_t>(n, (int64_t)bwv[6]));
+    }
     const void* d0 = c->dense[0].p;
     const void* f0 = c->dflags.p;
     RK(grow(c, c->dense[0], bytes));
@@ -725,12 +736,13 @@ int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym) {
     }
     CK(cudaMemsetAsync(c->dflags.p, 0, fbytes, c->stream));
     if (!sym) CK(cudaMemsetAsync(Dt, 0, bytes, c->stream));
+    if (halo) CK(cudaStreamWaitEvent(c->stream, c->sev[1], 0));  // the halo rows of X_n have landed
     if (sym) {
-        CK(launch_densify(p.B, n, (int)np, false, D, fa, fb, c->stream));
+        CK(launch_densify(p.B, x0, x1, (int)np, false, D, fa, fb, c->stream));
         c->launches++;
     } else {
-        CK(launch_densify(p.A, n, (int)np, true, Dt, fa, nullptr, c->stream));
-        CK(launch_densify(p.B, n, (int)np, false, D, nullptr, fb, c->stream));
+        CK(launch_densify(p.A, 0, n, (int)np, true, Dt, fa, nullptr, c->stream));
+        CK(launch_densify(p.B, 0, n, (int)np, false, D, nullptr, fb, c->stream));
         c->launches += 2;
     }
     c->dense_clean_np = np;  // D = X, nonzero only in fa's blocks (A = B = X)
@@ -739,7 +751,10 @@ int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym) {
     // ELLPACK_OPT_PROFILE: the GEMM is this op's "row kernel" (ellpack_ctx_kernel_time)
     const int pk = c->prof_n < 4 ? c->prof_n : 3;
     if (c->profile) CK(cudaEventRecord(c->pev[pk][0], c->stream));
-    CK(launch_dense_gemm(Dt, D, (int)np, sym, Fa, Fb, S, tw, p.exec_products, c->num_sms, c->stream));
+    const bool sym_tiles = sym && !part;
+    const int64_t g0 = part ? r0 : 0, g1 = part ? r1 : np;
+    const int bm = dense_tile_rows((int)np, g1 - g0, sym_tiles, c->num_sms);
+    CK(launch_dense_gemm(Dt, D, (int)np, sym_tiles, Fa, Fb, S, tw, p.exec_products, g0, g1, bm, c->stream));
     if (c->profile) {
         CK(cudaEventRecord(c->pev[pk][1], c->stream));
         c->prof_n = pk + 1;
@@ -751,7 +766,7 @@ int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym) {
     // stored a_ii of A: the diagonal of either dense copy of A; Old = X: its dense copy D and flags fa
     const double* dA = sym ? D : Dt;
     CK(launch_dense_emit(S, (int)np, p, dA, p.old_mode != 0 ? D : nullptr, tw,
-                         dense_tile_rows((int)np, sym, c->num_sms), Fa, c->num_sms, c->stream));
+                         bm, Fa, c->num_sms, c->stream));
     c->launches++;
     c->last_upper = 0;
     c->last_dense = 1;
@@ -1229,6 +1244,8 @@ int ellpack_multiply_x2(ellpack_ctx c, const ellpack_desc* x, ellpack_desc* x2, 
         CK(cudaMemcpyAsync(&asym, aux, sizeof asym, cudaMemcpyDeviceToHost, c->stream));
         RK(host_sync(c));
         dense_sym = asym == 0 ? 1 : 0;
+        // a row block (ellpack_ctx_set_rows) runs dense only for a symmetric X (X^T = X: one copy)
+        if ((p.row_begin != 0 || p.row_end != n) && dense_sym != 1) dense_sym = -1;
     }
     c->last_dense = 0;
     auto enqueue = [&]() -> int {
@@ -2034,6 +2051,20 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
         RK(host_sync(c));
         sym = asym == 0;
     }
+    // the dense regime across ranks (symmetric X): every rank must take the same regime every step,
+    // so the choice uses only all-reduced inputs -- here the smallest free memory of any rank
+    bool dense_comm_ok = false, dense_comm_alloc = false;
+    if (c->comm && sym && c->dense_opt != 1 && n <= kDenseMaxN) {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); fr = 0; }
+        unsigned long long f64 = fr;
+        CK(cudaMemcpyAsync(c->d_keys + 6, &f64, 8, cudaMemcpyHostToDevice, c->stream));
+        NK(g_nccl.AllReduce(c->d_keys + 6, c->d_keys + 6, 1, ncclUint64, ncclMin, c->comm, c->stream));
+        CK(cudaMemcpyAsync(&f64, c->d_keys + 6, 8, cudaMemcpyDeviceToHost, c->stream));
+        RK(host_sync(c));
+        const double npd = (double)dense_np(n);
+        dense_comm_ok = 2.0 * 8.0 * npd * npd <= 0.6 * (double)f64;
+    }
     int rc = sp2_make_x0(c, h, alpha0, beta0, o.threshold, T, &req);
     if (rc) { cleanup(); return rc; }
     if (req > w) {
@@ -2159,7 +2190,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
         // counted as occupied) at the rate the last dense step achieved on that count.
         bool dense_step = false;
         double w_dense = 0.0, p_est = 0.0;
-        if (!c->comm && c->dense_opt != 1 && dense_fits(c, n, sym ? 2 : 3)) {
+        if (c->dense_opt != 1 && (c->comm ? dense_comm_ok : dense_fits(c, n, sym ? 2 : 3))) {
             // the GEMM's exact work when the last step measured X_n's block occupancy (symmetric X),
             // else the band model
             w_dense = w_next > 0.0 ? w_next : dense_band_fmas(n, std::max(bwX[0], bwX[1]), sym);
@@ -2179,6 +2210,27 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
                     fprintf(stderr, "[regime] it %d w %.3e (%s) rate_d %.3e t_d %.3f ms | P_est %.3e rate_s %.3e t_s %.3f ms -> %s\n",
                             it, w_dense, w_next > 0.0 ? "exact" : "band", rate_dense, t_d * 1e3, p_est, rate_sparse,
                             t_s * 1e3, dense_step ? "dense" : "sparse");
+            }
+        }
+        if (dense_step && c->comm && !dense_comm_alloc) {
+            // the first dense step of a run across ranks: every rank allocates, then all agree (MIN of
+            // the success flags) -- a rank that could not falls back with the others, never alone
+            dense_comm_alloc = true;
+            const int64_t np = dense_np(n);
+            const size_t bytes = sizeof(double) * (size_t)np * (size_t)np;
+            const size_t fl = 2 * (size_t)(np / kDenseTile) * (size_t)(np / kDenseK) +
+                              2 * (size_t)(np / kDenseTile) * dense_kbw((int)np) * 8 +
+                              (size_t)(np / 16) * (size_t)(np / kDenseTile);
+            unsigned long long okv = (grow(c, c->dense[0], bytes) == ELLPACK_OK && grow(c, c->dense[2], bytes) == ELLPACK_OK &&
+                                      grow(c, c->dflags, fl) == ELLPACK_OK) ? 1ull : 0ull;
+            cudaGetLastError();
+            CK(cudaMemcpyAsync(c->d_keys + 6, &okv, 8, cudaMemcpyHostToDevice, c->stream));
+            NK(g_nccl.AllReduce(c->d_keys + 6, c->d_keys + 6, 1, ncclUint64, ncclMin, c->comm, c->stream));
+            CK(cudaMemcpyAsync(&okv, c->d_keys + 6, 8, cudaMemcpyDeviceToHost, c->stream));
+            RK(host_sync(c));
+            if (!okv) {
+                dense_comm_ok = false;
+                dense_step = false;
             }
         }
         c->last_dense = 0;
@@ -2215,7 +2267,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             cudaEventRecord(c->ev[0], c->stream);
             // with a communicator the halo of X_n (started after the previous step) is in flight:
             // the interior rows run beside it, the boundary rows after it (§8f-f1)
-            if (dense_step) rc = enqueue_dense_op(c, p, n, sym);
+            if (dense_step) rc = enqueue_dense_op(c, p, n, sym, bwX, halo_pending);
             else if (c->comm) rc = enqueue_row_op_split(c, p, n, bwX, halo_pending, alloc_upper, &ua);
             else rc = enqueue_row_op(c, p, n, bwX, alloc_upper, &ua);
             if (rc) { status = rc; break; }
@@ -2368,10 +2420,13 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
         // rate of the long ones -- cfg4's iteration 1 at 1.4e11 products/s, iteration 5 at 7.8e11)
         // (a dense step that zeroed the whole N_p^2 array -- the first of a context -- and a run's first
         // step carry one-time costs; sparse steps grow more efficient with size: the best rate seen)
+        // (with a communicator the rates stay the seeds: a rank's own step time must not steer a choice
+        // every rank has to make alike)
         if (c->last_dense) {
             dense_tried = true;
-            if (step_ms >= 1.0 && !c->dense_full_clear && w_dense > 0.0) rate_dense = w_dense / (step_ms * 1e-3);
-        } else if (it >= 1 && step_ms >= 10.0 && p_prev >= 1e10) {
+            if (!c->comm && step_ms >= 1.0 && !c->dense_full_clear && w_dense > 0.0)
+                rate_dense = w_dense / (step_ms * 1e-3);
+        } else if (!c->comm && it >= 1 && step_ms >= 10.0 && p_prev >= 1e10) {
             rate_sparse_seen = std::max(rate_sparse_seen, p_prev / (step_ms * 1e-3));
             rate_sparse = rate_sparse_seen;
         }

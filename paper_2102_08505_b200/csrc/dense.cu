@@ -21,12 +21,13 @@ namespace ell {
 
 // ------------------------------------------------------------------------------ densify
 
-__global__ void __launch_bounds__(256) densify_kernel(KMat a, int64_t n, int np, int transpose, double* __restrict__ D,
-                                                      unsigned char* __restrict__ fa, unsigned char* __restrict__ fb) {
+__global__ void __launch_bounds__(256) densify_kernel(KMat a, int64_t i0, int64_t i1, int np, int transpose,
+                                                      double* __restrict__ D, unsigned char* __restrict__ fa,
+                                                      unsigned char* __restrict__ fb) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int KB = np / kDenseK, T = np / kDenseTile;
-    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+    for (int64_t i = i0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < i1; i += nw) {
         const int nnz = a.nnz[i];
         const int32_t* c = a.col + (size_t)i * a.w;
         const double* v = a.val + (size_t)i * a.w;
@@ -41,12 +42,12 @@ __global__ void __launch_bounds__(256) densify_kernel(KMat a, int64_t n, int np,
     }
 }
 
-cudaError_t launch_densify(KMat a, int64_t n, int np, bool transpose, double* D, unsigned char* fa,
+cudaError_t launch_densify(KMat a, int64_t i0, int64_t i1, int np, bool transpose, double* D, unsigned char* fa,
                            unsigned char* fb, cudaStream_t s) {
-    if (n <= 0) return cudaSuccess;
-    const int64_t blocks = (n + 7) / 8;
-    densify_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, s>>>(a, n, np, transpose ? 1 : 0, D,
-                                                                                   fa, fb);
+    if (i1 <= i0) return cudaSuccess;
+    const int64_t blocks = (i1 - i0 + 7) / 8;
+    densify_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, s>>>(a, i0, i1, np, transpose ? 1 : 0,
+                                                                                   D, fa, fb);
     return cudaGetLastError();
 }
 
@@ -139,7 +140,7 @@ template <int BM, int TY, bool SYM>
 __global__ void __launch_bounds__(16 * TY, BM == 128 ? (TY == 8 ? 2 : 1) : 4)
     dense_gemm_kernel(const double* __restrict__ At, const double* __restrict__ B, int np,
                       const unsigned long long* __restrict__ Fa, const unsigned long long* __restrict__ Fb,
-                      double* __restrict__ S, unsigned char* __restrict__ tw, unsigned long long* exec) {
+                      double* __restrict__ S, unsigned char* __restrict__ tw, unsigned long long* exec, int bi0) {
     static_assert(!SYM || BM == kDenseTile, "symmetric tiles are square");
     constexpr int NT = 16 * TY, NW = NT / 32, RM = BM / TY, SB = stage_bytes<BM>();
     extern __shared__ __align__(16) unsigned char smem[];
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(16 * TY, BM == 128 ? (TY == 8 ? 2 : 1) : 4)
         while (t >= T - bi) { t -= T - bi; ++bi; }
         bj = bi + t;
     } else {
-        bi = blockIdx.x / T;
+        bi = bi0 + (int)(blockIdx.x / T);  // a rank's rows start at row block bi0
         bj = blockIdx.x % T;
     }
     const int bf = bi * BM / kDenseTile;  // the 128-row flag block of this tile's rows
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(16 * TY, BM == 128 ? (TY == 8 ? 2 : 1) : 4)
 template <int BM, int TY, bool SYM>
 cudaError_t launch_gemm_t(unsigned grid, const double* At, const double* B, int np, const unsigned long long* fa,
                           const unsigned long long* fb, double* S, unsigned char* tw, unsigned long long* exec,
-                          cudaStream_t s) {
+                          int bi0, cudaStream_t s) {
     static int attr = 0;  // dynamic shared memory opted in so far (per instantiation)
     const size_t smem = (size_t)kDenseStages * stage_bytes<BM>() + sizeof(int) * (size_t)(np / kDenseK);
     if (smem > 48 * 1024 && attr < (int)smem) {
@@ -327,28 +328,32 @@ cudaError_t launch_gemm_t(unsigned grid, const double* At, const double* B, int 
         if (e) return e;
         attr = (int)smem;
     }
-    dense_gemm_kernel<BM, TY, SYM><<<grid, 16 * TY, smem, s>>>(At, B, np, fa, fb, S, tw, exec);
+    dense_gemm_kernel<BM, TY, SYM><<<grid, 16 * TY, smem, s>>>(At, B, np, fa, fb, S, tw, exec, bi0);
     return cudaGetLastError();
 }
 
-int dense_tile_rows(int np, bool sym, int num_sms) {
-    const int T = np / kDenseTile;
-    const int tiles = sym ? T * (T + 1) / 2 : T * T;
+int dense_tile_rows(int np, int64_t rows, bool sym, int num_sms) {
+    const int64_t T = np / kDenseTile, R = rows / kDenseTile;
+    const int64_t tiles = sym ? T * (T + 1) / 2 : R * T;
     // 128-row tiles while they fill most of the SMs; below that 16-row tiles (8x the CTAs)
     return tiles >= (num_sms * 4) / 5 ? 128 : 16;
 }
 
 cudaError_t launch_dense_gemm(const double* At, const double* B, int np, bool sym, const unsigned long long* fa,
                               const unsigned long long* fb, double* S, unsigned char* tw, unsigned long long* exec,
-                              int num_sms, cudaStream_t s) {
-    if (np <= 0 || np % kDenseTile) return cudaErrorInvalidValue;
+                              int64_t row0, int64_t row1, int bm, cudaStream_t s) {
+    if (np <= 0 || np % kDenseTile || row0 % kDenseTile || (row1 - row0) % kDenseTile || row1 <= row0)
+        return cudaErrorInvalidValue;
     const int T = np / kDenseTile;
-    if (dense_tile_rows(np, sym, num_sms) == 128) {
-        if (sym)
-            return launch_gemm_t<128, ELL_DENSE_TY, true>((unsigned)(T * (T + 1) / 2), At, B, np, fa, fb, S, tw, exec, s);
-        return launch_gemm_t<128, ELL_DENSE_TY, false>((unsigned)(T * T), At, B, np, fa, fb, S, tw, exec, s);
+    const int R = (int)((row1 - row0) / kDenseTile);
+    if (sym && (row0 != 0 || row1 != np)) return cudaErrorInvalidValue;  // symmetric tiles: all rows
+    if (bm == 128) {
+        if (sym) return launch_gemm_t<128, ELL_DENSE_TY, true>((unsigned)(T * (T + 1) / 2), At, B, np, fa, fb, S, tw,
+                                                               exec, 0, s);
+        return launch_gemm_t<128, ELL_DENSE_TY, false>((unsigned)(R * T), At, B, np, fa, fb, S, tw, exec,
+                                                       (int)(row0 / 128), s);
     }
-    return launch_gemm_t<16, 8, false>((unsigned)(8 * T * T), At, B, np, fa, fb, S, tw, exec, s);
+    return launch_gemm_t<16, 8, false>((unsigned)(8 * R * T), At, B, np, fa, fb, S, tw, exec, (int)(row0 / 16), s);
 }
 
 // Zero the 128 x 16 blocks of D that fa flags (D holds nonzeros only there): the dense array returns

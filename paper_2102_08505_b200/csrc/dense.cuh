@@ -16,11 +16,11 @@ constexpr int kDenseK = 16;      // k rows per pipeline stage
 // 64-bit words of one k-block bitset (np / 16 bits)
 __host__ __device__ inline int dense_kbw(int np) { return (np / kDenseK + 63) / 64; }
 
-// D (np x np doubles, zeroed by the caller) <- the stored entries of rows [0, n) of a:
+// D (np x np doubles, zeroed by the caller) <- the stored entries of rows [i0, i1) of a:
 // D[i][j] = a_ij, or D[j][i] = a_ij with transpose. Occupancy flags (nullable, zeroed by the caller):
 // fa[(i / 128) * (np / 16) + j / 16] = 1 (a as the left operand: (m-block, k-block)),
 // fb[(i / 16) * (np / 128) + j / 128] = 1 (a as the right operand: (k-block, n-block)).
-cudaError_t launch_densify(KMat a, int64_t n, int np, bool transpose, double* D, unsigned char* fa,
+cudaError_t launch_densify(KMat a, int64_t i0, int64_t i1, int np, bool transpose, double* D, unsigned char* fa,
                            unsigned char* fb, cudaStream_t s);
 
 // S = A B over the k blocks whose flags are both set (nullable flags: every block), k ascending:
@@ -31,13 +31,14 @@ cudaError_t launch_densify(KMat a, int64_t n, int np, bool transpose, double* D,
 cudaError_t launch_pack_flags(const unsigned char* fa, const unsigned char* fb, int np, unsigned long long* Fa,
                               unsigned long long* Fb, int num_sms, cudaStream_t s);
 
-// Tiles of dense_tile_rows(...) = 128 rows x 128 columns while they fill most SMs, else 16 x 128
-// (small N). A tile with no occupied k block is not stored: tw[(row / tile rows) * (np / 128) +
-// column / 128] = 0 for it, 1 for a stored tile (every entry written by the launch).
-int dense_tile_rows(int np, bool sym, int num_sms);
+// Rows [row0, row1) of S (multiples of 128; sym: all rows, tiles bi <= bj mirrored) in tiles of
+// bm = dense_tile_rows(np, rows, sym, SMs) rows x 128 columns: 128 while they fill most SMs, else 16
+// (small N). A tile with no occupied k block is not stored: tw[(row / bm) * (np / 128) + column / 128]
+// = 0 for it, 1 for a stored tile (every entry written by the launch).
+int dense_tile_rows(int np, int64_t rows, bool sym, int num_sms);
 cudaError_t launch_dense_gemm(const double* At, const double* B, int np, bool sym, const unsigned long long* Fa,
                               const unsigned long long* Fb, double* S, unsigned char* tw, unsigned long long* exec,
-                              int num_sms, cudaStream_t s);
+                              int64_t row0, int64_t row1, int bm, cudaStream_t s);
 
 // D <- 0 given that D is zero outside the 128 x 16 blocks fa flags (the previous densify's).
 cudaError_t launch_dense_clear(double* D, int np, const unsigned char* fa, int num_sms, cudaStream_t s);

@@ -297,12 +297,57 @@ def test_sp2_symmetric_step_with_communicator(ellpack_lib):
     o = oracle.sp2(H, n // 2, 1e-10, oracle.SP2Opts(threshold=1e-6, max_iter=100), d_width=n)
     ctx = E.Context(0)
     ctx.attach_nccl(1, 0, E.Context.nccl_unique_id(), 0, n)
+    ctx.set_option(E.OPT_DENSE, 1)  # the sparse kernels' symmetric route (the dense regime: below)
     d = E.Mat.empty(n, n)
     g = ctx.sp2_run(up(H), n // 2, 1e-10, d, threshold=1e-6, max_iter=100)
     _compare_sp2(g, o)
     assert same_bits(d.to_host(), o.D)
     assert any(it["products_exec"] < 0.75 * it["products"] for it in g.iters)  # the upper route ran
     ctx.close()
+
+
+@pytest.mark.parametrize("dense", [2, 0])
+def test_sp2_dense_with_communicator(ellpack_lib, dense):
+    """The dense regime with a communicator (1-rank comm): forced, and chosen automatically from
+    all-reduced inputs only (band model, fixed rates) -- bitwise the oracle."""
+    E = ellpack_lib
+    n = 1024
+    H = synth.sym_banded(n, 32, 6, 12, 1, -1.0, 1.0, 0, 4.0, 0.0, 6)
+    o = oracle.sp2(H, n // 2, 1e-10, oracle.SP2Opts(threshold=1e-6, max_iter=100), d_width=n)
+    ctx = E.Context(0)
+    ctx.attach_nccl(1, 0, E.Context.nccl_unique_id(), 0, n)
+    ctx.set_option(E.OPT_DENSE, dense)
+    d = E.Mat.empty(n, n)
+    g = ctx.sp2_run(up(H), n // 2, 1e-10, d, threshold=1e-6, max_iter=100)
+    _compare_sp2(g, o)
+    assert same_bits(d.to_host(), o.D)
+    regimes = [it["regime"] for it in g.iters]
+    assert (all(r == "dense" for r in regimes) if dense == 2 else "dense" in regimes)
+    ctx.close()
+
+
+@pytest.mark.parametrize("n,nranks", [(8192, 2), (8192, 4), (1024, 4)])
+def test_dense_row_blocks_bitwise(ellpack_lib, n, nranks):
+    """A rank's rows in the dense regime (ellpack_ctx_set_rows, emulated ranks): GEMM tiles of its
+    row blocks only (row offset; 128-row and 16-row tiles), X^T = X read from the one dense copy; the
+    union of the blocks equals the single-rank product bit for bit."""
+    E = ellpack_lib
+    X = synth.cfg5(n, 64)
+    wo = 1024
+    full = E.Context(0)
+    y1 = E.Mat.empty(n, wo)
+    assert full.multiply_x2(up(X), y1, 1e-5)[0] == E.OK
+    full.close()
+    yp = E.Mat.empty(n, wo)
+    x = up(X)
+    for (r0, r1) in E.row_partition(n, nranks):
+        c = E.Context(0)
+        c.set_option(E.OPT_DENSE, 2)
+        c.set_rows(r0, r1)
+        c.multiply_x2(x, yp, 1e-5)
+        assert c.last_launch()["path"] == "dense"
+        c.close()
+    assert same_bits(yp.to_host(), y1.to_host())
 
 
 def test_small_x2_graph_replay_bitwise(ellpack_lib):
