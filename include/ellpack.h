@@ -150,11 +150,15 @@ int ellpack_ctx_set_stream(ellpack_ctx ctx, void* stream);
  *                          products at the last sparse step's rate), and the 2 (symmetric X) or 3
  *                          N^2-double arrays fit in 60% of the free device memory; 1 = never;
  *                          2 = always when they fit (every SP2 step on one rank and every
- *                          ellpack_multiply_x2; tests). */
+ *                          ellpack_multiply_x2; tests).
+ *  ELLPACK_OPT_DENSE_KERNEL the dense GEMM's 128-row tiles: 0 (default) = on the FP64 MMA
+ *                          (mma.sync m8n8k4) when a per-device self-check confirms it computes the
+ *                          ascending fma chain bit for bit, else on FP64 FMAs; 1 = FP64 FMAs;
+ *                          2 = the FP64 MMA (tests). Results are bitwise the same either way. */
 enum { ELLPACK_OPT_WINDOW = 1, ELLPACK_OPT_WARPS = 2, ELLPACK_OPT_SP2_WIDTH0 = 3, ELLPACK_OPT_PROFILE = 4,
        ELLPACK_OPT_ABLATE = 5, ELLPACK_OPT_GENERAL_WINDOW = 6, ELLPACK_OPT_VALIDATE = 7,
        ELLPACK_OPT_SP2_SYMMETRIC = 8, ELLPACK_OPT_SP2_MEM_CAP = 9, ELLPACK_OPT_RING_KERNEL = 10,
-       ELLPACK_OPT_SP2_DEVICE_LOOP = 11, ELLPACK_OPT_DENSE = 12 };
+       ELLPACK_OPT_SP2_DEVICE_LOOP = 11, ELLPACK_OPT_DENSE = 12, ELLPACK_OPT_DENSE_KERNEL = 13 };
 int ellpack_ctx_set_option(ellpack_ctx ctx, int key, int64_t value);
 
 /* Accumulated device time (ms, CUDA events on the ctx stream) and launch count of

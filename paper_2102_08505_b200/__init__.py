@@ -33,6 +33,7 @@ OPT_SP2_MEM_CAP = 9
 OPT_RING_KERNEL = 10
 OPT_SP2_DEVICE_LOOP = 11
 OPT_DENSE = 12
+OPT_DENSE_KERNEL = 13
 SP2_FAIL, SP2_GROW = 0, 1
 SP2_RULE_TRACE_SIGN, SP2_RULE_TRACE_CLOSEST = 0, 1
 STOP_NAMES = {0: "CONVERGED", 1: "STAGNATED", 2: "NOCONV", 3: "OVERFLOW"}

@@ -127,6 +127,7 @@ struct ellpack_ctx_s {
     int sp2_exec_launches = 0;
     bool last_step_general = false;
     int dense_opt = 0;     // ELLPACK_OPT_DENSE
+    int dense_kernel = 0;  // ELLPACK_OPT_DENSE_KERNEL
     Buf dense[3];          // dense regime: X (or B), X^T (non-symmetric A), S -- np x np doubles each
     Buf dflags;            // dense regime: k-block occupancy of the left and right operands
     Buf docc;              // dense regime: occupancy bitsets of the next SP2 operand (exact GEMM work)
@@ -754,7 +755,8 @@ int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym, const i
     const bool sym_tiles = sym && !part;
     const int64_t g0 = part ? r0 : 0, g1 = part ? r1 : np;
     const int bm = dense_tile_rows((int)np, g1 - g0, sym_tiles, c->num_sms);
-    CK(launch_dense_gemm(Dt, D, (int)np, sym_tiles, Fa, Fb, S, tw, p.exec_products, g0, g1, bm, c->stream));
+    const bool mma = c->dense_kernel == 2 || (c->dense_kernel == 0 && dense_mma_ok(c->stream));
+    CK(launch_dense_gemm(Dt, D, (int)np, sym_tiles, Fa, Fb, S, tw, p.exec_products, g0, g1, bm, mma, c->stream));
     if (c->profile) {
         CK(cudaEventRecord(c->pev[pk][1], c->stream));
         c->prof_n = pk + 1;
@@ -1074,6 +1076,10 @@ int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
         case ELLPACK_OPT_DENSE:
             if (v > 2) return ELLPACK_ERR_ARG;
             c->dense_opt = (int)v;
+            return ELLPACK_OK;
+        case ELLPACK_OPT_DENSE_KERNEL:
+            if (v > 2) return ELLPACK_ERR_ARG;
+            c->dense_kernel = (int)v;
             return ELLPACK_OK;
         case ELLPACK_OPT_RING_KERNEL:
             if (v > 4) return ELLPACK_ERR_ARG;
@@ -1826,6 +1832,7 @@ int sp2_device_loop(ellpack_ctx c, const sp2_opts& o, int64_t n, int64_t nocc, d
         RK(grow(c, c->dflags, 2 * (size_t)(np / kDenseTile) * (size_t)(np / kDenseK) +
                                   2 * (size_t)(np / kDenseTile) * dense_kbw((int)np) * 8 +
                                   (size_t)(np / 16) * (size_t)(np / kDenseTile)));
+        (void)dense_mma_ok(c->stream);  // the once-per-device check synchronises: not inside the capture
         // the captured steps clear D by the previous step's flags: start from D = 0, flags = 0
         CK(cudaMemsetAsync(c->dense[0].p, 0, bytes, c->stream));
         CK(cudaMemsetAsync(c->dflags.p, 0, c->dflags.bytes, c->stream));

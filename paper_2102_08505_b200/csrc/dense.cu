@@ -339,14 +339,247 @@ int dense_tile_rows(int np, int64_t rows, bool sym, int num_sms) {
     return tiles >= (num_sms * 4) / 5 ? 128 : 16;
 }
 
+// ----------------------------------------------------------------- FP64 MMA variant (DMMA)
+//
+// The same tiles, k blocks and pipeline, with the 8 x 8 x 4 FP64 MMA (mma.sync.m8n8k4.f64) doing the
+// multiply-adds: one warp instruction = 256 of them, where the FMA kernel issues 8 (FP64 pipe 74 % busy,
+// bound by issue). Its use rests on reading R23: on sm_100a the MMA computes each output as the
+// ascending fma chain d = fma(a3, b3, fma(a2, b2, fma(a1, b1, fma(a0, b0, c)))) -- checked bit for
+// bit on 4.5e8 outputs including planted cancellations (tools/dmma_order.cu, profiles/r02_dmma_order.log)
+// and again on every device before first use (dense_mma_selfcheck); chained over the k blocks in
+// ascending order it is the sparse kernels' chain exactly.
+//
+// 8 warps as 2 x 4, each a 64 x 32 sub-tile = 8 x 4 MMA tiles (64 accumulators per lane). Stage rows
+// are padded to 132 doubles: the fragments (A: lane l reads row k0 + l % 4, column m0 + l / 4) then
+// hit 16 distinct bank pairs per half-warp.
+constexpr int kMmaPad = 132;  // padded stage row (doubles)
+constexpr int kMmaStage = 2 * kDenseK * kMmaPad * 8;  // At block + B block
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+template <bool SYM>
+__global__ void __launch_bounds__(256, 1)
+    dense_mma_kernel(const double* __restrict__ At, const double* __restrict__ B, int np,
+                     const unsigned long long* __restrict__ Fa, const unsigned long long* __restrict__ Fb,
+                     double* __restrict__ S, unsigned char* __restrict__ tw, unsigned long long* exec, int bi0) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int wcnt[8];
+    __shared__ __align__(8) unsigned long long fullbar[kDenseStages];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int T = np / kDenseTile;
+    int bi, bj;
+    if (SYM) {
+        int t = blockIdx.x;
+        bi = 0;
+        while (t >= T - bi) { t -= T - bi; ++bi; }
+        bj = bi + t;
+    } else {
+        bi = bi0 + (int)(blockIdx.x / T);
+        bj = blockIdx.x % T;
+    }
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+    int* list = reinterpret_cast<int*>(smem + kDenseStages * kMmaStage);
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(fullbar);
+    if (tid == 0) {
+#pragma unroll
+        for (int st = 0; st < kDenseStages; ++st) dmbar_init(bar0 + 8u * st, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    const int kbw = dense_kbw(np);
+    int nact = 0;
+    for (int w0 = 0; w0 < kbw; w0 += 256) {
+        const int w = w0 + tid;
+        const unsigned long long m = w < kbw ? Fa[(size_t)bi * kbw + w] & Fb[(size_t)bj * kbw + w] : 0ull;
+        const int cnt = __popcll(m);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wcnt[warp] = incl;
+        __syncthreads();
+        int off = nact, tot = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            off += q < warp ? wcnt[q] : 0;
+            tot += wcnt[q];
+        }
+        off += incl - cnt;
+        for (unsigned long long r = m; r; r &= r - 1) list[off++] = 64 * w + __ffsll((long long)r) - 1;
+        __syncthreads();
+        nact += tot;
+    }
+    const double* a0 = At + (size_t)bi * kDenseTile;
+    const double* b0 = B + (size_t)bj * kDenseTile;
+    auto load_stage = [&](int st, int kb) {  // warp 0: 32 bulk copies of one 1 KB row each
+        const uint32_t sa = sbase + (uint32_t)(st * kMmaStage), sb = sa + (uint32_t)(kMmaStage / 2);
+        const uint32_t bar = bar0 + 8u * (uint32_t)st;
+        const size_t r0 = (size_t)kb * kDenseK;
+        if (lane == 0) dmbar_expect(bar, 2u * kDenseK * kDenseTile * 8u);
+        __syncwarp();
+        const int r = lane & 15;
+        if (lane < 16) bulk_g2s(sa + (uint32_t)(r * kMmaPad * 8), a0 + (r0 + r) * np, 1024u, bar);
+        else bulk_g2s(sb + (uint32_t)(r * kMmaPad * 8), b0 + (r0 + r) * np, 1024u, bar);
+    };
+    const int wm = warp >> 2, wn = warp & 3;  // 64-row x 32-column sub-tile
+    const int fr = lane & 3, fc = lane >> 2;  // fragment: k offset, row / column offset
+    double acc[8][4][2];
+#pragma unroll
+    for (int mb = 0; mb < 8; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
+    if (warp == 0) {
+#pragma unroll
+        for (int st = 0; st < kDenseStages - 1; ++st)
+            if (st < nact) load_stage(st, list[st]);
+    }
+    for (int t = 0; t < nact; ++t) {
+        __syncthreads();  // every warp is done with stage t - 1: its slot takes stage t + S - 1
+        {
+            const int tn = t + kDenseStages - 1;
+            if (warp == 0 && tn < nact) load_stage(tn % kDenseStages, list[tn]);
+        }
+        dmbar_wait(bar0 + 8u * (uint32_t)(t % kDenseStages), (uint32_t)((t / kDenseStages) & 1));
+        const double* sa = reinterpret_cast<const double*>(smem + (t % kDenseStages) * kMmaStage);
+        const double* sb = sa + kDenseK * kMmaPad;
+#pragma unroll
+        for (int k4 = 0; k4 < kDenseK; k4 += 4) {  // k ascending: 4 per MMA, the MMAs in order
+            double a[8], b[4];
+            const double* ak = sa + (k4 + fr) * kMmaPad + wm * 64 + fc;
+            const double* bk = sb + (k4 + fr) * kMmaPad + wn * 32 + fc;
+#pragma unroll
+            for (int mb = 0; mb < 8; ++mb) a[mb] = ak[8 * mb];
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb) b[nb] = bk[8 * nb];
+#pragma unroll
+            for (int mb = 0; mb < 8; ++mb)
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb) dmma(acc[mb][nb][0], acc[mb][nb][1], a[mb], b[nb]);
+        }
+    }
+    if (tid == 0) {
+        tw[(size_t)bi * T + bj] = nact > 0;
+        if (SYM && bi != bj) tw[(size_t)bj * T + bi] = nact > 0;
+    }
+    if (nact == 0) return;
+    // accumulator (mb, nb, h): row wm 64 + 8 mb + lane / 4, column wn 32 + 8 nb + 2 (lane % 4) + h
+#pragma unroll
+    for (int mb = 0; mb < 8; ++mb) {
+        double* row = S + (size_t)(bi * kDenseTile + wm * 64 + 8 * mb + fc) * np + bj * kDenseTile + wn * 32 + 2 * fr;
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) stg128(row + 8 * nb, acc[mb][nb][0], acc[mb][nb][1]);
+    }
+    if (SYM && bi != bj) {
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                double* col = S + (size_t)(bj * kDenseTile + wn * 32 + 8 * nb + 2 * fr + h) * np + bi * kDenseTile +
+                              wm * 64 + fc;
+#pragma unroll
+                for (int mb = 0; mb < 8; ++mb) col[8 * mb] = acc[mb][nb][h];
+            }
+    }
+    if (exec && tid == 0)
+        atomicAdd(exec, (unsigned long long)nact * kDenseK * kDenseTile * kDenseTile);
+}
+
+// R23 on this device: MMA outputs vs the ascending fma chain on random, mixed-magnitude and planted-
+// cancellation inputs (the cases where other orders differ); bad[0] counts mismatches.
+__global__ void dense_mma_selfcheck_kernel(unsigned long long* bad) {
+    const int lane = threadIdx.x & 31;
+    uint64_t sd = 0x5eed0000ull + 7919ull * (blockIdx.x * 32 + lane);
+    auto rnd = [&](int mode) {
+        sd += 0x9e3779b97f4a7c15ull;
+        uint64_t z = sd;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        z ^= z >> 31;
+        const double u = (double)(z >> 11) * 0x1p-53 * 2.0 - 1.0;
+        return mode ? ldexp(u, (int)((z >> 3) % 60) - 30) : u;
+    };
+    __shared__ double A[8][4], Bm[4][8], C[8][8];
+    unsigned long long nb = 0;
+    for (int t = 0; t < 64; ++t) {
+        const int mode = t % 3;
+        A[lane >> 2][lane & 3] = rnd(mode);
+        Bm[lane >> 3][lane & 7] = rnd(mode);
+        for (int q = lane; q < 64; q += 32) C[q >> 3][q & 7] = rnd(mode);
+        __syncwarp();
+        if (mode == 2) {  // c = -(the products' sum), perturbed: the chain's rounding decides everything
+            for (int q = lane; q < 64; q += 32) {
+                const int i = q >> 3, j = q & 7;
+                double sum = 0.0;
+                for (int k = 0; k < 4; ++k) sum = __fma_rn(A[i][k], Bm[k][j], sum);
+                C[i][j] = -sum * (1.0 + ldexp((double)(q % 7 - 3), -50));
+            }
+            __syncwarp();
+        }
+        double d0 = C[lane >> 2][2 * (lane & 3)], d1 = C[lane >> 2][2 * (lane & 3) + 1];
+        dmma(d0, d1, A[lane >> 2][lane & 3], Bm[lane & 3][lane >> 2]);
+        for (int h = 0; h < 2; ++h) {
+            const int i = lane >> 2, j = 2 * (lane & 3) + h;
+            double ch = C[i][j];
+            for (int k = 0; k < 4; ++k) ch = __fma_rn(A[i][k], Bm[k][j], ch);
+            if (__double_as_longlong(h ? d1 : d0) != __double_as_longlong(ch)) ++nb;
+        }
+        __syncwarp();
+    }
+    if (nb) atomicAdd(bad, nb);
+}
+
+// 1: the MMA variant may run on this device (R23 holds here), 0: it may not. Checked once per device.
+int dense_mma_ok(cudaStream_t s) {
+    static int checked[64];
+    static int verdict[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+    if (checked[dev]) return verdict[dev];
+    unsigned long long* bad = nullptr;
+    unsigned long long h = 1;
+    if (cudaMallocAsync((void**)&bad, 8, s) == cudaSuccess && cudaMemsetAsync(bad, 0, 8, s) == cudaSuccess) {
+        dense_mma_selfcheck_kernel<<<148, 32, 0, s>>>(bad);
+        if (cudaMemcpyAsync(&h, bad, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+            h = 1;
+        cudaFreeAsync(bad, s);
+    }
+    cudaGetLastError();
+    checked[dev] = 1;
+    verdict[dev] = h == 0;
+    return verdict[dev];
+}
+
+template <bool SYM>
+cudaError_t launch_mma_t(unsigned grid, const double* At, const double* B, int np, const unsigned long long* fa,
+                         const unsigned long long* fb, double* S, unsigned char* tw, unsigned long long* exec, int bi0,
+                         cudaStream_t s) {
+    static int attr = 0;
+    const size_t smem = (size_t)kDenseStages * kMmaStage + sizeof(int) * (size_t)(np / kDenseK);
+    if (attr < (int)smem) {
+        cudaError_t e = cudaFuncSetAttribute(dense_mma_kernel<SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e) return e;
+        attr = (int)smem;
+    }
+    dense_mma_kernel<SYM><<<grid, 256, smem, s>>>(At, B, np, fa, fb, S, tw, exec, bi0);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_dense_gemm(const double* At, const double* B, int np, bool sym, const unsigned long long* fa,
                               const unsigned long long* fb, double* S, unsigned char* tw, unsigned long long* exec,
-                              int64_t row0, int64_t row1, int bm, cudaStream_t s) {
+                              int64_t row0, int64_t row1, int bm, bool mma, cudaStream_t s) {
     if (np <= 0 || np % kDenseTile || row0 % kDenseTile || (row1 - row0) % kDenseTile || row1 <= row0)
         return cudaErrorInvalidValue;
     const int T = np / kDenseTile;
     const int R = (int)((row1 - row0) / kDenseTile);
     if (sym && (row0 != 0 || row1 != np)) return cudaErrorInvalidValue;  // symmetric tiles: all rows
+    if (bm == 128 && mma) {
+        if (sym) return launch_mma_t<true>((unsigned)(T * (T + 1) / 2), At, B, np, fa, fb, S, tw, exec, 0, s);
+        return launch_mma_t<false>((unsigned)(R * T), At, B, np, fa, fb, S, tw, exec, (int)(row0 / 128), s);
+    }
     if (bm == 128) {
         if (sym) return launch_gemm_t<128, ELL_DENSE_TY, true>((unsigned)(T * (T + 1) / 2), At, B, np, fa, fb, S, tw,
                                                                exec, 0, s);

@@ -36,9 +36,14 @@ cudaError_t launch_pack_flags(const unsigned char* fa, const unsigned char* fb, 
 // (small N). A tile with no occupied k block is not stored: tw[(row / bm) * (np / 128) + column / 128]
 // = 0 for it, 1 for a stored tile (every entry written by the launch).
 int dense_tile_rows(int np, int64_t rows, bool sym, int num_sms);
+// mma: 128-row tiles on the FP64 MMA (mma.sync m8n8k4) instead of FP64 FMAs (reading R23; callers
+// pass dense_mma_ok()).
 cudaError_t launch_dense_gemm(const double* At, const double* B, int np, bool sym, const unsigned long long* Fa,
                               const unsigned long long* Fb, double* S, unsigned char* tw, unsigned long long* exec,
-                              int64_t row0, int64_t row1, int bm, cudaStream_t s);
+                              int64_t row0, int64_t row1, int bm, bool mma, cudaStream_t s);
+// 1 when the FP64 MMA computes the ascending fma chain bit for bit on this device (checked once per
+// device on adversarial inputs; reading R23), else 0.
+int dense_mma_ok(cudaStream_t s);
 
 // D <- 0 given that D is zero outside the 128 x 16 blocks fa flags (the previous densify's).
 cudaError_t launch_dense_clear(double* D, int np, const unsigned char* fa, int num_sms, cudaStream_t s);

@@ -21,6 +21,7 @@ for n in [int(v) for v in sys.argv[1:]] or [8192]:
                   nnz=np.full(n, n, dtype=np.int32))
     ctx = eb.Context(0)
     ctx.set_option(eb.OPT_DENSE, 2)
+    ctx.set_option(eb.OPT_DENSE_KERNEL, int(os.environ.get("DENSE_KERNEL", "0")))
     x = eb.Mat.from_host(X)
     y = eb.Mat.empty(n, n + (n & 1))
     for _ in range(2):
