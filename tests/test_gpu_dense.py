@@ -14,11 +14,12 @@ from tests.test_gpu_parity import _compare_sp2, gpu_x2, ora_x2, same_bits_scalar
 pytestmark = pytest.mark.gpu
 
 
-def _ctx(E, dense=2, loop=1, sym=1):
+def _ctx(E, dense=2, loop=1, sym=1, kernel=0):
     c = E.Context(0)
     c.set_option(E.OPT_DENSE, dense)
     c.set_option(E.OPT_SP2_DEVICE_LOOP, loop)
     c.set_option(E.OPT_SP2_SYMMETRIC, sym)
+    c.set_option(E.OPT_DENSE_KERNEL, kernel)
     return c
 
 
@@ -182,3 +183,38 @@ def test_cfg3_dense_equals_sparse_through_the_fill(ellpack_lib):
         assert all(same_bits_scalar(a[k], b[k]) for k in ("trX", "trS", "e"))
     assert same_bits_scalar(gs.trD, gd.trD)
     assert same_bits(ds, dd)
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kind,n,tau", [("sym", 2000, 1e-6), ("nonsym", 1500, 0.0)])
+def test_x2_dense_both_gemm_kernels_bitwise(ellpack_lib, kernel, kind, n, tau):
+    """The dense GEMM's two kernels for 128-row tiles -- FP64 FMAs (1) and the FP64 MMA (2, reading
+    R23) -- each bitwise the oracle."""
+    E = ellpack_lib
+    X = _sym(n, n) if kind == "sym" else synth.random_sparse(n, 40, 0, 40, band=None, p_empty=0.05, seed=n)
+    wo = n + (n & 1)
+    r, Y = ora_x2(X, wo, tau)
+    c = _ctx(E, kernel=kernel)
+    try:
+        st, Yg, tx, tx2 = gpu_x2(c, X, wo, tau)
+        assert c.last_launch()["path"] == "dense" and st == r.status == E.OK
+        assert same_bits(Yg, Y)
+        assert same_bits_scalar(tx, r.trace_x) and same_bits_scalar(tx2, r.trace_x2)
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_sp2_dense_both_gemm_kernels_bitwise(ellpack_lib, kernel):
+    E = ellpack_lib
+    n = 1900
+    H = _sym(n, 3)
+    o = oracle.sp2(H, n // 2, 1e-10, oracle.SP2Opts(threshold=1e-6, max_iter=8), d_width=n)
+    c = _ctx(E, dense=2, kernel=kernel)
+    try:
+        d = E.Mat.empty(n, n)
+        g = c.sp2_run(up(H), n // 2, 1e-10, d, threshold=1e-6, max_iter=8)
+        _compare_sp2(g, o)
+        assert same_bits(d.to_host(), o.D)
+    finally:
+        c.close()
