@@ -353,7 +353,14 @@ int dense_tile_rows(int np, int64_t rows, bool sym, int num_sms) {
 // are padded to 132 doubles: the fragments (A: lane l reads row k0 + l % 4, column m0 + l / 4) then
 // hit 16 distinct bank pairs per half-warp.
 constexpr int kMmaPad = 132;  // padded stage row (doubles)
-constexpr int kMmaStage = 2 * kDenseK * kMmaPad * 8;  // At block + B block
+#ifndef ELL_MMA_KPS
+#define ELL_MMA_KPS 3  // k blocks per pipeline stage (one barrier per stage; 3 x 2 stages measured best)
+#endif
+#ifndef ELL_MMA_STAGES
+#define ELL_MMA_STAGES 2
+#endif
+constexpr int kMmaKps = ELL_MMA_KPS, kMmaStages = ELL_MMA_STAGES;
+constexpr int kMmaStage = 2 * kMmaKps * kDenseK * kMmaPad * 8;  // At blocks + B blocks
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -367,7 +374,7 @@ __global__ void __launch_bounds__(256, 1)
                      double* __restrict__ S, unsigned char* __restrict__ tw, unsigned long long* exec, int bi0) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int wcnt[8];
-    __shared__ __align__(8) unsigned long long fullbar[kDenseStages];
+    __shared__ __align__(8) unsigned long long fullbar[kMmaStages];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int T = np / kDenseTile;
     int bi, bj;
@@ -381,11 +388,11 @@ __global__ void __launch_bounds__(256, 1)
         bj = blockIdx.x % T;
     }
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-    int* list = reinterpret_cast<int*>(smem + kDenseStages * kMmaStage);
+    int* list = reinterpret_cast<int*>(smem + kMmaStages * kMmaStage);
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(fullbar);
     if (tid == 0) {
 #pragma unroll
-        for (int st = 0; st < kDenseStages; ++st) dmbar_init(bar0 + 8u * st, 1);
+        for (int st = 0; st < kMmaStages; ++st) dmbar_init(bar0 + 8u * st, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     const int kbw = dense_kbw(np);
@@ -415,15 +422,20 @@ __global__ void __launch_bounds__(256, 1)
     }
     const double* a0 = At + (size_t)bi * kDenseTile;
     const double* b0 = B + (size_t)bj * kDenseTile;
-    auto load_stage = [&](int st, int kb) {  // warp 0: 32 bulk copies of one 1 KB row each
-        const uint32_t sa = sbase + (uint32_t)(st * kMmaStage), sb = sa + (uint32_t)(kMmaStage / 2);
-        const uint32_t bar = bar0 + 8u * (uint32_t)st;
-        const size_t r0 = (size_t)kb * kDenseK;
-        if (lane == 0) dmbar_expect(bar, 2u * kDenseK * kDenseTile * 8u);
+    const int nst = (nact + kMmaKps - 1) / kMmaKps;  // stages: kMmaKps listed k blocks each
+    auto load_stage = [&](int slot, int st) {  // warp 0: one 1 KB bulk copy per k row of A^T and of B
+        const uint32_t sa = sbase + (uint32_t)(slot * kMmaStage), sb = sa + (uint32_t)(kMmaStage / 2);
+        const uint32_t bar = bar0 + 8u * (uint32_t)slot;
+        const int ne = min(kMmaKps, nact - st * kMmaKps);
+        if (lane == 0) dmbar_expect(bar, (uint32_t)ne * 2u * kDenseK * kDenseTile * 8u);
         __syncwarp();
         const int r = lane & 15;
-        if (lane < 16) bulk_g2s(sa + (uint32_t)(r * kMmaPad * 8), a0 + (r0 + r) * np, 1024u, bar);
-        else bulk_g2s(sb + (uint32_t)(r * kMmaPad * 8), b0 + (r0 + r) * np, 1024u, bar);
+        for (int j = 0; j < ne; ++j) {
+            const size_t r0 = (size_t)list[st * kMmaKps + j] * kDenseK;
+            const uint32_t row = (uint32_t)((j * kDenseK + r) * kMmaPad * 8);
+            if (lane < 16) bulk_g2s(sa + row, a0 + (r0 + r) * np, 1024u, bar);
+            else bulk_g2s(sb + row, b0 + (r0 + r) * np, 1024u, bar);
+        }
     };
     const int wm = warp >> 2, wn = warp & 3;  // 64-row x 32-column sub-tile
     const int fr = lane & 3, fc = lane >> 2;  // fragment: k offset, row / column offset
@@ -434,20 +446,21 @@ __global__ void __launch_bounds__(256, 1)
         for (int nb = 0; nb < 4; ++nb) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
     if (warp == 0) {
 #pragma unroll
-        for (int st = 0; st < kDenseStages - 1; ++st)
-            if (st < nact) load_stage(st, list[st]);
+        for (int st = 0; st < kMmaStages - 1; ++st)
+            if (st < nst) load_stage(st, st);
     }
-    for (int t = 0; t < nact; ++t) {
+    for (int t = 0; t < nst; ++t) {
         __syncthreads();  // every warp is done with stage t - 1: its slot takes stage t + S - 1
         {
-            const int tn = t + kDenseStages - 1;
-            if (warp == 0 && tn < nact) load_stage(tn % kDenseStages, list[tn]);
+            const int tn = t + kMmaStages - 1;
+            if (warp == 0 && tn < nst) load_stage(tn % kMmaStages, tn);
         }
-        dmbar_wait(bar0 + 8u * (uint32_t)(t % kDenseStages), (uint32_t)((t / kDenseStages) & 1));
-        const double* sa = reinterpret_cast<const double*>(smem + (t % kDenseStages) * kMmaStage);
-        const double* sb = sa + kDenseK * kMmaPad;
-#pragma unroll
-        for (int k4 = 0; k4 < kDenseK; k4 += 4) {  // k ascending: 4 per MMA, the MMAs in order
+        dmbar_wait(bar0 + 8u * (uint32_t)(t % kMmaStages), (uint32_t)((t / kMmaStages) & 1));
+        const double* sa = reinterpret_cast<const double*>(smem + (t % kMmaStages) * kMmaStage);
+        const double* sb = sa + kMmaKps * kDenseK * kMmaPad;
+        const int krows = min(kMmaKps, nact - t * kMmaKps) * kDenseK;
+#pragma unroll 4
+        for (int k4 = 0; k4 < krows; k4 += 4) {  // k ascending: 4 per MMA, the MMAs in order
             double a[8], b[4];
             const double* ak = sa + (k4 + fr) * kMmaPad + wm * 64 + fc;
             const double* bk = sb + (k4 + fr) * kMmaPad + wn * 32 + fc;
@@ -558,7 +571,7 @@ cudaError_t launch_mma_t(unsigned grid, const double* At, const double* B, int n
                          const unsigned long long* fb, double* S, unsigned char* tw, unsigned long long* exec, int bi0,
                          cudaStream_t s) {
     static int attr = 0;
-    const size_t smem = (size_t)kDenseStages * kMmaStage + sizeof(int) * (size_t)(np / kDenseK);
+    const size_t smem = (size_t)kMmaStages * kMmaStage + sizeof(int) * (size_t)(np / kDenseK);
     if (attr < (int)smem) {
         cudaError_t e = cudaFuncSetAttribute(dense_mma_kernel<SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e) return e;

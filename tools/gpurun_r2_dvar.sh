@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 2400 python tools/variants_dense.py base ELL_DENSE_TMA=0 ELL_DENSE_TMA=1,ELL_DENSE_STAGES=3 ELL_DENSE_TMA=1,ELL_DENSE_STAGES=6 > gpurun_out/dense_variants.log 2>&1
+SIZES="8192 12288" timeout 2400 python tools/variants_dense.py base ELL_MMA_KPS=1,ELL_MMA_STAGES=4 ELL_MMA_KPS=2,ELL_MMA_STAGES=2 ELL_MMA_KPS=3,ELL_MMA_STAGES=2 > gpurun_out/dense_variants.log 2>&1
 echo done
