@@ -4,6 +4,7 @@ fma chain as the oracle's plus exact-zero terms, so the comparison is bitwise (v
 traces, overflow counts, SP2 branches and stop iterations), on symmetric operands (one dense copy,
 upper-triangle tiles mirrored) and non-symmetric ones (A^T and B copies, every tile), at sizes that
 are not multiples of the 128 tile."""
+import numpy as np
 import pytest
 
 import oracle
@@ -218,3 +219,24 @@ def test_sp2_dense_both_gemm_kernels_bitwise(ellpack_lib, kernel):
         assert same_bits(d.to_host(), o.D)
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("n", [1, 2, 127, 129])
+def test_x2_dense_degenerate_sizes(ellpack_lib, n):
+    """The dense regime at sizes around one 128 tile and on an all-empty operand (every tile empty:
+    nothing stored, nothing emitted, traces +0)."""
+    E = ellpack_lib
+    rng = np.random.default_rng(n)
+    dense = np.where(rng.random((n, n)) < 0.3, rng.standard_normal((n, n)), 0.0)
+    dense = (dense + dense.T) * 0.5
+    wo = n + (n & 1)
+    for X in (synth.from_dense(dense, w=wo), synth.from_dense(np.zeros((n, n)), w=wo)):
+        r, Y = ora_x2(X, wo, 0.0)
+        c = _ctx(E)
+        try:
+            st, Yg, tx, tx2 = gpu_x2(c, X, wo, 0.0)
+            assert c.last_launch()["path"] == "dense" and st == r.status == E.OK
+            assert same_bits(Yg, Y)
+            assert same_bits_scalar(tx, r.trace_x) and same_bits_scalar(tx2, r.trace_x2)
+        finally:
+            c.close()
