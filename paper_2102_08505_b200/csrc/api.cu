@@ -131,6 +131,7 @@ struct ellpack_ctx_s {
     Buf dense[3];          // dense regime: X (or B), X^T (non-symmetric A), S -- np x np doubles each
     Buf dflags;            // dense regime: k-block occupancy of the left and right operands
     Buf docc;              // dense regime: occupancy bitsets of the next SP2 operand (exact GEMM work)
+    Buf old_val, old_col, old_nnz;  // ellpack_multiply with beta != 0: the scratch copy of C_old
     int last_dense = 0;    // the last SP2 step / X^2 ran in the dense regime
     int64_t dense_clean_np = 0;  // dense[0] is zero outside the blocks dflags' fa marks (for this N_p)
     int64_t dense_fit_key = -1;  // dense_fits: the cached free-memory answer (N_p, arrays)
@@ -396,7 +397,8 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
         if (c->window_opt == 0 && c->force_general_s == 0 && !no_probe && rk != 1 && !stash && groups <= 4 &&
             sring <= kSplitRingMax) {
             // W = 0: the warp-specialized kernel (accumulator + emitter warps, W = 1 records)
-            const int W = rk == 3 ? 2 : (rk == 4 ? 0 : 1);  // automatic: one warp per row
+            // automatic: one warp per row; the warp-specialized experiment has no Old operand
+            const int W = rk == 3 ? 2 : ((rk == 4 && !has_old) ? 0 : 1);
             const int maxsub = p.alpha != 0.0 ? bwv[4] : 0;
             const int G = W != 2 ? (groups < 1 ? 1 : groups) : std::max(1, (maxsub + 63) / 64);
             const int mode = !has_old ? 0 : (p.normsq ? 2 : 1);
@@ -1030,7 +1032,8 @@ int ellpack_ctx_destroy(ellpack_ctx c) {
                    &c->stash_val, &c->stash_col, &c->ident_val, &c->ident_col, &c->ident_nnz,
                    &c->hx_val, &c->hx_col, &c->hx_nnz, &c->hy_val, &c->hy_col, &c->hy_nnz,
                    &c->bt, &c->bt_nbin, &c->bp, &c->halo, &c->vflag, &c->symaux, &c->sp2dev, &c->sp2rec,
-                   &c->dense[0], &c->dense[1], &c->dense[2], &c->dflags, &c->docc};
+                   &c->dense[0], &c->dense[1], &c->dense[2], &c->dflags, &c->docc,
+                   &c->old_val, &c->old_col, &c->old_nnz};
     if (c->sp2_exec) cudaGraphExecDestroy(c->sp2_exec);
     if (c->x2_exec) cudaGraphExecDestroy(c->x2_exec);
     for (auto& sl : c->it)
@@ -1205,8 +1208,18 @@ int ellpack_multiply(ellpack_ctx c, const ellpack_desc* a, const ellpack_desc* b
     p.tau = tau;
     if (beta != 0.0) {
         p.old_mode = 1;
-        p.Old = kmat(cm);
-        p.stash_old = 1;
+        // C_old is C itself (updated in place): its live entries go to a scratch copy first (one
+        // kernel, 12 B per live entry), so the row kernels read Old from memory the output never
+        // overwrites -- the split ring kernel then applies (it does not stash aliased rows)
+        const int64_t nn = a->n;
+        RK(grow(c, c->old_val, sizeof(double) * (size_t)nn * cm->w));
+        RK(grow(c, c->old_col, sizeof(int32_t) * (size_t)nn * cm->w));
+        RK(grow(c, c->old_nnz, sizeof(int32_t) * (size_t)nn));
+        KOut oc{(double*)c->old_val.p, (int32_t*)c->old_col.p, (int32_t*)c->old_nnz.p, cm->w};
+        CK(launch_copy_rows(kmat(cm), oc, p.row_begin, p.row_end, c->d_status + 4, c->stream));
+        c->launches++;
+        p.Old = KMat{oc.val, oc.col, oc.nnz, oc.w};
+        p.stash_old = 0;
     }
     RK(enqueue_row_op(c, p, a->n));
     RK(reduce_status(c));
