@@ -360,20 +360,25 @@ constexpr int kMmaPad = 132;  // padded stage row (doubles)
 #define ELL_MMA_STAGES 2
 #endif
 constexpr int kMmaKps = ELL_MMA_KPS, kMmaStages = ELL_MMA_STAGES;
-constexpr int kMmaStage = 2 * kMmaKps * kDenseK * kMmaPad * 8;  // At blocks + B blocks
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
-template <bool SYM>
-__global__ void __launch_bounds__(256, 1)
+template <int BM, bool SYM>
+__global__ void __launch_bounds__(BM == 128 ? 256 : 128, BM == 128 ? 1 : 4)
     dense_mma_kernel(const double* __restrict__ At, const double* __restrict__ B, int np,
                      const unsigned long long* __restrict__ Fa, const unsigned long long* __restrict__ Fb,
                      double* __restrict__ S, unsigned char* __restrict__ tw, unsigned long long* exec, int bi0) {
+    static_assert(!SYM || BM == kDenseTile, "symmetric tiles are square");
+    // BM = 128: 8 warps as 2 x 4 of 64 x 32; BM = 16: 4 warps of 16 x 32 (small N: 8x the CTAs)
+    constexpr int NW = BM == 128 ? 8 : 4, WM = BM == 128 ? 2 : 1, MB = BM / WM / 8;
+    constexpr int PA = BM + 4;  // padded A^T stage row: the fragments hit 16 bank pairs per half-warp
+    constexpr int SA = kMmaKps * kDenseK * PA, SB = kMmaKps * kDenseK * kMmaPad;  // doubles per stage part
+    constexpr int STG = (SA + SB) * 8;
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ int wcnt[8];
+    __shared__ int wcnt[NW];
     __shared__ __align__(8) unsigned long long fullbar[kMmaStages];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int T = np / kDenseTile;
@@ -388,7 +393,8 @@ __global__ void __launch_bounds__(256, 1)
         bj = blockIdx.x % T;
     }
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-    int* list = reinterpret_cast<int*>(smem + kMmaStages * kMmaStage);
+    int* list = reinterpret_cast<int*>(smem + kMmaStages * STG);
+    const int bf = bi * BM / kDenseTile;  // the 128-row flag block of this tile's rows
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(fullbar);
     if (tid == 0) {
 #pragma unroll
@@ -397,9 +403,9 @@ __global__ void __launch_bounds__(256, 1)
     }
     const int kbw = dense_kbw(np);
     int nact = 0;
-    for (int w0 = 0; w0 < kbw; w0 += 256) {
+    for (int w0 = 0; w0 < kbw; w0 += 32 * NW) {
         const int w = w0 + tid;
-        const unsigned long long m = w < kbw ? Fa[(size_t)bi * kbw + w] & Fb[(size_t)bj * kbw + w] : 0ull;
+        const unsigned long long m = w < kbw ? Fa[(size_t)bf * kbw + w] & Fb[(size_t)bj * kbw + w] : 0ull;
         const int cnt = __popcll(m);
         int incl = cnt;
 #pragma unroll
@@ -411,7 +417,7 @@ __global__ void __launch_bounds__(256, 1)
         __syncthreads();
         int off = nact, tot = 0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < NW; ++q) {
             off += q < warp ? wcnt[q] : 0;
             tot += wcnt[q];
         }
@@ -420,28 +426,27 @@ __global__ void __launch_bounds__(256, 1)
         __syncthreads();
         nact += tot;
     }
-    const double* a0 = At + (size_t)bi * kDenseTile;
+    const double* a0 = At + (size_t)bi * BM;
     const double* b0 = B + (size_t)bj * kDenseTile;
     const int nst = (nact + kMmaKps - 1) / kMmaKps;  // stages: kMmaKps listed k blocks each
-    auto load_stage = [&](int slot, int st) {  // warp 0: one 1 KB bulk copy per k row of A^T and of B
-        const uint32_t sa = sbase + (uint32_t)(slot * kMmaStage), sb = sa + (uint32_t)(kMmaStage / 2);
+    auto load_stage = [&](int slot, int st) {  // warp 0: one bulk copy per k row of A^T and of B
+        const uint32_t sa = sbase + (uint32_t)(slot * STG), sb = sa + (uint32_t)(SA * 8);
         const uint32_t bar = bar0 + 8u * (uint32_t)slot;
         const int ne = min(kMmaKps, nact - st * kMmaKps);
-        if (lane == 0) dmbar_expect(bar, (uint32_t)ne * 2u * kDenseK * kDenseTile * 8u);
+        if (lane == 0) dmbar_expect(bar, (uint32_t)ne * kDenseK * (BM + kDenseTile) * 8u);
         __syncwarp();
         const int r = lane & 15;
         for (int j = 0; j < ne; ++j) {
             const size_t r0 = (size_t)list[st * kMmaKps + j] * kDenseK;
-            const uint32_t row = (uint32_t)((j * kDenseK + r) * kMmaPad * 8);
-            if (lane < 16) bulk_g2s(sa + row, a0 + (r0 + r) * np, 1024u, bar);
-            else bulk_g2s(sb + row, b0 + (r0 + r) * np, 1024u, bar);
+            if (lane < 16) bulk_g2s(sa + (uint32_t)((j * kDenseK + r) * PA * 8), a0 + (r0 + r) * np, (uint32_t)(BM * 8), bar);
+            else bulk_g2s(sb + (uint32_t)((j * kDenseK + r) * kMmaPad * 8), b0 + (r0 + r) * np, 1024u, bar);
         }
     };
-    const int wm = warp >> 2, wn = warp & 3;  // 64-row x 32-column sub-tile
+    const int wm = warp >> 2, wn = warp & 3;  // (8 MB)-row x 32-column sub-tile
     const int fr = lane & 3, fc = lane >> 2;  // fragment: k offset, row / column offset
-    double acc[8][4][2];
+    double acc[MB][4][2];
 #pragma unroll
-    for (int mb = 0; mb < 8; ++mb)
+    for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
         for (int nb = 0; nb < 4; ++nb) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
     if (warp == 0) {
@@ -456,20 +461,20 @@ __global__ void __launch_bounds__(256, 1)
             if (warp == 0 && tn < nst) load_stage(tn % kMmaStages, tn);
         }
         dmbar_wait(bar0 + 8u * (uint32_t)(t % kMmaStages), (uint32_t)((t / kMmaStages) & 1));
-        const double* sa = reinterpret_cast<const double*>(smem + (t % kMmaStages) * kMmaStage);
-        const double* sb = sa + kMmaKps * kDenseK * kMmaPad;
+        const double* sa = reinterpret_cast<const double*>(smem + (t % kMmaStages) * STG);
+        const double* sb = sa + SA;
         const int krows = min(kMmaKps, nact - t * kMmaKps) * kDenseK;
 #pragma unroll 4
         for (int k4 = 0; k4 < krows; k4 += 4) {  // k ascending: 4 per MMA, the MMAs in order
-            double a[8], b[4];
-            const double* ak = sa + (k4 + fr) * kMmaPad + wm * 64 + fc;
+            double a[MB], b[4];
+            const double* ak = sa + (k4 + fr) * PA + wm * (8 * MB) + fc;
             const double* bk = sb + (k4 + fr) * kMmaPad + wn * 32 + fc;
 #pragma unroll
-            for (int mb = 0; mb < 8; ++mb) a[mb] = ak[8 * mb];
+            for (int mb = 0; mb < MB; ++mb) a[mb] = ak[8 * mb];
 #pragma unroll
             for (int nb = 0; nb < 4; ++nb) b[nb] = bk[8 * nb];
 #pragma unroll
-            for (int mb = 0; mb < 8; ++mb)
+            for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
                 for (int nb = 0; nb < 4; ++nb) dmma(acc[mb][nb][0], acc[mb][nb][1], a[mb], b[nb]);
         }
@@ -479,10 +484,10 @@ __global__ void __launch_bounds__(256, 1)
         if (SYM && bi != bj) tw[(size_t)bj * T + bi] = nact > 0;
     }
     if (nact == 0) return;
-    // accumulator (mb, nb, h): row wm 64 + 8 mb + lane / 4, column wn 32 + 8 nb + 2 (lane % 4) + h
+    // accumulator (mb, nb, h): row wm 8 MB + 8 mb + lane / 4, column wn 32 + 8 nb + 2 (lane % 4) + h
 #pragma unroll
-    for (int mb = 0; mb < 8; ++mb) {
-        double* row = S + (size_t)(bi * kDenseTile + wm * 64 + 8 * mb + fc) * np + bj * kDenseTile + wn * 32 + 2 * fr;
+    for (int mb = 0; mb < MB; ++mb) {
+        double* row = S + (size_t)(bi * BM + wm * (8 * MB) + 8 * mb + fc) * np + bj * kDenseTile + wn * 32 + 2 * fr;
 #pragma unroll
         for (int nb = 0; nb < 4; ++nb) stg128(row + 8 * nb, acc[mb][nb][0], acc[mb][nb][1]);
     }
@@ -491,14 +496,14 @@ __global__ void __launch_bounds__(256, 1)
         for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                double* col = S + (size_t)(bj * kDenseTile + wn * 32 + 8 * nb + 2 * fr + h) * np + bi * kDenseTile +
-                              wm * 64 + fc;
+                double* col = S + (size_t)(bj * kDenseTile + wn * 32 + 8 * nb + 2 * fr + h) * np + bi * BM +
+                              wm * (8 * MB) + fc;
 #pragma unroll
-                for (int mb = 0; mb < 8; ++mb) col[8 * mb] = acc[mb][nb][h];
+                for (int mb = 0; mb < MB; ++mb) col[8 * mb] = acc[mb][nb][h];
             }
     }
     if (exec && tid == 0)
-        atomicAdd(exec, (unsigned long long)nact * kDenseK * kDenseTile * kDenseTile);
+        atomicAdd(exec, (unsigned long long)nact * kDenseK * BM * kDenseTile);
 }
 
 // R23 on this device: MMA outputs vs the ascending fma chain on random, mixed-magnitude and planted-
@@ -566,18 +571,19 @@ int dense_mma_ok(cudaStream_t s) {
     return verdict[dev];
 }
 
-template <bool SYM>
+template <int BM, bool SYM>
 cudaError_t launch_mma_t(unsigned grid, const double* At, const double* B, int np, const unsigned long long* fa,
                          const unsigned long long* fb, double* S, unsigned char* tw, unsigned long long* exec, int bi0,
                          cudaStream_t s) {
     static int attr = 0;
-    const size_t smem = (size_t)kMmaStages * kMmaStage + sizeof(int) * (size_t)(np / kDenseK);
-    if (attr < (int)smem) {
-        cudaError_t e = cudaFuncSetAttribute(dense_mma_kernel<SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t stage = (size_t)kMmaKps * kDenseK * ((BM + 4) + kMmaPad) * 8;
+    const size_t smem = (size_t)kMmaStages * stage + sizeof(int) * (size_t)(np / kDenseK);
+    if (smem > 48 * 1024 && attr < (int)smem) {
+        cudaError_t e = cudaFuncSetAttribute(dense_mma_kernel<BM, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e) return e;
         attr = (int)smem;
     }
-    dense_mma_kernel<SYM><<<grid, 256, smem, s>>>(At, B, np, fa, fb, S, tw, exec, bi0);
+    dense_mma_kernel<BM, SYM><<<grid, BM == 128 ? 256 : 128, smem, s>>>(At, B, np, fa, fb, S, tw, exec, bi0);
     return cudaGetLastError();
 }
 
@@ -590,9 +596,11 @@ cudaError_t launch_dense_gemm(const double* At, const double* B, int np, bool sy
     const int R = (int)((row1 - row0) / kDenseTile);
     if (sym && (row0 != 0 || row1 != np)) return cudaErrorInvalidValue;  // symmetric tiles: all rows
     if (bm == 128 && mma) {
-        if (sym) return launch_mma_t<true>((unsigned)(T * (T + 1) / 2), At, B, np, fa, fb, S, tw, exec, 0, s);
-        return launch_mma_t<false>((unsigned)(R * T), At, B, np, fa, fb, S, tw, exec, (int)(row0 / 128), s);
+        if (sym) return launch_mma_t<128, true>((unsigned)(T * (T + 1) / 2), At, B, np, fa, fb, S, tw, exec, 0, s);
+        return launch_mma_t<128, false>((unsigned)(R * T), At, B, np, fa, fb, S, tw, exec, (int)(row0 / 128), s);
     }
+    // (16-row tiles stay on FP64 FMAs: the MMA variant measured slower there -- 0.36 vs 0.25 ms at
+    // N = 1024 -- with two fragments of A per four of B and 117 KB of stages per CTA)
     if (bm == 128) {
         if (sym) return launch_gemm_t<128, ELL_DENSE_TY, true>((unsigned)(T * (T + 1) / 2), At, B, np, fa, fb, S, tw,
                                                                exec, 0, s);
