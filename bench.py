@@ -12,7 +12,7 @@ X's rows (NCCL send/recv of exactly the rows the rank's own rows reference, §8f
 (strong scaling: total work fixed).
 
 The same line carries the rest of BASELINE.json's metric ("SP2 iterations/sec at 1/2/4/8") and the
-other configs' timings as sub-objects: "sp2" (cfg3 K = 10 and cfg4 K = 6 windows, SURVEY §8d "SP2
+other configs' timings as sub-objects: "sp2" (cfg3 K = 10 and cfg4 K = 10 windows, SURVEY §8d "SP2
 protocol"), "cfg1" (us per ABI call, launch-latency bound) and "cfg2" (C = alpha A B + beta C).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -744,7 +744,7 @@ def run_ours(args):
     sp2 = cfg1 = cfg2 = sweep = dense_gemm = None
     if not args.quick:
         sp2 = {"cfg3": time_sp2(eb, mr, dev, ws, rank, 3, 10, 3, 1),
-               "cfg4": time_sp2(eb, mr, dev, ws, rank, 4, 6, 2, 1)}
+               "cfg4": time_sp2(eb, mr, dev, ws, rank, 4, 10, 2, 1)}
         if ws == 1:
             sp2["cfg3_full"] = time_sp2_full(eb, dev)
             sp2["cfg1_sized"] = time_sp2_small(eb, dev, 20, "cfg1")

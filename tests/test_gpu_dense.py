@@ -240,3 +240,31 @@ def test_x2_dense_degenerate_sizes(ellpack_lib, n):
             assert same_bits_scalar(tx, r.trace_x) and same_bits_scalar(tx2, r.trace_x2)
         finally:
             c.close()
+
+
+def test_cfg4_bench_window_k10_regimes_agree(ellpack_lib):
+    """The cfg4 window bench.py times (K = 10, SURVEY §8d "SP2 protocol"): its iterations 6-9 are beyond
+    what the oracle finishes in a test (~10^12 products); the automatic regime (dense from iteration 3
+    on) equals the sparse kernels bit for bit there, and the first 6 iterations of either equal the
+    oracle (test_sp2_bench_window_bitwise, test_cfg4_window_every_step_dense_bitwise)."""
+    E = ellpack_lib
+    H, cf = synth.cfg4(), synth.CFG4
+    n, K = H.n, 10
+    dw = min(n, 8192)
+    res = {}
+    for dense in (0, 1):
+        c = _ctx(E, dense=dense, loop=0)
+        try:
+            d = E.Mat.empty(n, dw)
+            g = c.sp2_run(up(H), cf["nocc"], cf["tol"], d, threshold=cf["threshold"], max_iter=K)
+            res[dense] = (g, d.to_host())
+        finally:
+            c.close()
+    (ga, da), (gs, ds) = res[0], res[1]
+    assert "dense" in [it["regime"] for it in ga.iters]
+    assert ga.iterations == gs.iterations == K and ga.final_width == gs.final_width
+    for a, b in zip(ga.iters, gs.iters):
+        assert (a["branch"], a["width"], a["required"], a["products"]) == (b["branch"], b["width"], b["required"],
+                                                                          b["products"])
+        assert all(same_bits_scalar(a[k], b[k]) for k in ("trX", "trS", "e"))
+    assert same_bits(da, ds)

@@ -3,8 +3,8 @@
 
 - cfg5 X^2, N = 262144, M = 256 (the headline multiply): EVERY row, compared with the oracle in
   16384-row blocks (SURVEY §8d "compare in row blocks of 16384 rows"), plus tr X and tr X^2;
-- SP2 on cfg3 over the K = 10 window and on cfg4 over the K = 6 window that bench.py --workload sp2
-  times (GROW, symmetric step on), iterate by iterate;
+- SP2 on cfg3 over the K = 10 window bench.py times and on cfg4 over the first 6 iterations of its
+  K = 10 window (GROW, symmetric step on, automatic regime), iterate by iterate;
 - SP2 on the paper's soft-matter model Hamiltonian at N = 16384 to the stop rule (bench.py
   --workload sp2 --sp2-model soft_matter).
 All bitwise.
@@ -61,8 +61,9 @@ def test_cfg5_full_size_every_row_bitwise(ctx):
 
 @pytest.mark.parametrize("cfg,K", [(3, 10), (4, 6)])
 def test_sp2_bench_window_bitwise(ctx, cfg, K):
-    """The exact window bench.py --workload sp2 times (D of width min(N, 8192), GROW, default
-    symmetric step), iterate by iterate against the oracle."""
+    """The windows bench.py times (D of width min(N, 8192), GROW, default symmetric step, automatic
+    regime), iterate by iterate against the oracle: cfg3's whole K = 10 window; cfg4's first 6 of its
+    10 iterations (the rest: test_cfg4_bench_window_k10_regimes_agree)."""
     H, cf = (synth.cfg3(), synth.CFG3) if cfg == 3 else (synth.cfg4(), synth.CFG4)
     n = H.n
     dw = min(n + (n & 1), 8192)
