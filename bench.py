@@ -341,6 +341,7 @@ def time_sp2(eb, mr, dev, ws, rank, cfg: int, K: int, steps: int, warmup: int):
     import torch
     H, cf = (synth.cfg3(), synth.CFG3) if cfg == 3 else (synth.cfg4(), synth.CFG4)
     n = H.n
+    torch.cuda.empty_cache()  # (the dense regime's arrays are sized against the free memory)
     ctx = _comm_ctx(eb, mr, dev, ws, rank, n)
     h = eb.Mat.from_host(H)
     d = eb.Mat.empty(n, min(n + (n & 1), 8192))

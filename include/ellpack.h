@@ -121,7 +121,9 @@ int ellpack_ctx_set_stream(ellpack_ctx ctx, void* stream);
  *                          in device memory when the value arrays of its live iterates (X_n, X_{n+1},
  *                          the symmetric step's upper triangle) would exceed this many bytes
  *                          (exercises the fallback from the headroom width to the exact width and the
- *                          symmetric step's whole-row fallback); 0 = off (default).
+ *                          symmetric step's whole-row fallback); the dense regime's two N^2 arrays
+ *                          "do not fit" when they exceed it (the run falls back to the sparse
+ *                          kernels); 0 = off (default).
  *  ELLPACK_OPT_RING_KERNEL which kernel runs rows on the ring (narrow-band) path: 0 = automatic
  *                          (the split-row kernel with 1 warp per row whenever the output does not
  *                          alias an input and the ring fits 16-bit offsets, else the legacy ring

@@ -659,8 +659,20 @@ bool dense_fits(ellpack_ctx c, int64_t n, int bufs) {
     if (c->dense_fit_key == key) return c->dense_fit_ok;
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return false; }
+    if (need > 0.6 * (double)fr) {
+        // memory freed with cudaFreeAsync (an earlier context's dense arrays) stays in the device's
+        // default pool until trimmed: return it and ask again
+        cudaMemPool_t pool;
+        if (cudaStreamSynchronize(c->stream) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess &&
+            cudaMemPoolTrimTo(pool, 0) == cudaSuccess && cudaMemGetInfo(&fr, &tot) != cudaSuccess)
+            fr = 0;
+        cudaGetLastError();
+    }
     c->dense_fit_key = key;
     c->dense_fit_ok = need <= 0.6 * (double)fr;
+    if (getenv("ELLPACK_DEBUG_REGIME"))
+        fprintf(stderr, "[regime] dense arrays %.2f GB, free %.2f GB -> %s\n", need * 1e-9, (double)fr * 1e-9,
+                c->dense_fit_ok ? "fit" : "do not fit");
     return c->dense_fit_ok;
 }
 
@@ -710,6 +722,8 @@ int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym, const i
         x0 = std::min<int64_t>(r0, std::max<int64_t>(0, (int64_t)INT_MAX - bwv[5]));
         x1 = std::max<int64_t>(r1, std::min<int64_t>(n, (int64_t)bwv[6]));
     }
+    // ELLPACK_OPT_SP2_MEM_CAP fault injection: the dense arrays "do not fit" either
+    if (c->sp2_mem_cap > 0 && (int64_t)(2 * bytes) > c->sp2_mem_cap) return ELLPACK_ERR_NOMEM;
     const void* d0 = c->dense[0].p;
     const void* f0 = c->dflags.p;
     RK(grow(c, c->dense[0], bytes));
@@ -2163,6 +2177,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
     double rate_sparse = 5e11, rate_dense = 1e13;  // (dense: FMAs / s)
     double rate_sparse_seen = 0.0;
     bool dense_tried = false;  // a dense step ran in this run (its rate replaced the seed)
+    bool dense_off = false;    // the dense arrays could not be allocated: sparse kernels for the rest
     // X_{n+1}'s exact dense work is measured after every step while the automatic regime may pick dense
     // (symmetric X, one rank): w_next FMAs, 0 = not measured
     const bool measure_work = sym && !c->comm && c->dense_opt == 0 && n <= kDenseMaxN;
@@ -2210,7 +2225,7 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
         // counted as occupied) at the rate the last dense step achieved on that count.
         bool dense_step = false;
         double w_dense = 0.0, p_est = 0.0;
-        if (c->dense_opt != 1 && (c->comm ? dense_comm_ok : dense_fits(c, n, sym ? 2 : 3))) {
+        if (c->dense_opt != 1 && !dense_off && (c->comm ? dense_comm_ok : dense_fits(c, n, sym ? 2 : 3))) {
             // the GEMM's exact work when the last step measured X_n's block occupancy (symmetric X),
             // else the band model
             w_dense = w_next > 0.0 ? w_next : dense_band_fmas(n, std::max(bwX[0], bwX[1]), sym);
@@ -2287,9 +2302,28 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
             cudaEventRecord(c->ev[0], c->stream);
             // with a communicator the halo of X_n (started after the previous step) is in flight:
             // the interior rows run beside it, the boundary rows after it (§8f-f1)
-            if (dense_step) rc = enqueue_dense_op(c, p, n, sym, bwX, halo_pending);
-            else if (c->comm) rc = enqueue_row_op_split(c, p, n, bwX, halo_pending, alloc_upper, &ua);
-            else rc = enqueue_row_op(c, p, n, bwX, alloc_upper, &ua);
+            if (dense_step) {
+                rc = enqueue_dense_op(c, p, n, sym, bwX, halo_pending);
+                if (rc == ELLPACK_ERR_NOMEM && !c->comm) {
+                    // the dense arrays did not fit after all (fragmentation): this step and the rest of
+                    // the run on the sparse kernels (same bits). With a communicator the arrays were
+                    // allocated and agreed on before the first dense step.
+                    cudaGetLastError();
+                    release(c, c->dense[0]);
+                    release(c, c->dense[1]);
+                    release(c, c->dense[2]);
+                    c->dense_clean_np = 0;
+                    c->dense_fit_key = -2;  // (a key no (N_p, arrays) pair has: asks the driver again)
+                    dense_step = false;
+                    dense_off = true;
+                    c->last_dense = 0;
+                    rc = enqueue_row_op(c, p, n, bwX, alloc_upper, &ua);
+                }
+            } else if (c->comm) {
+                rc = enqueue_row_op_split(c, p, n, bwX, halo_pending, alloc_upper, &ua);
+            } else {
+                rc = enqueue_row_op(c, p, n, bwX, alloc_upper, &ua);
+            }
             if (rc) { status = rc; break; }
             halo_pending = false;
             if (c->sym_nomem) sym_off = true;  // U did not fit: whole rows from now on

@@ -247,10 +247,12 @@ def test_cfg4_bench_window_k10_regimes_agree(ellpack_lib):
     what the oracle finishes in a test (~10^12 products); the automatic regime (dense from iteration 3
     on) equals the sparse kernels bit for bit there, and the first 6 iterations of either equal the
     oracle (test_sp2_bench_window_bitwise, test_cfg4_window_every_step_dense_bitwise)."""
+    import torch
     E = ellpack_lib
     H, cf = synth.cfg4(), synth.CFG4
     n, K = H.n, 10
     dw = min(n, 8192)
+    torch.cuda.empty_cache()  # the two 34 GB dense arrays must fit in 60 % of the free memory
     res = {}
     for dense in (0, 1):
         c = _ctx(E, dense=dense, loop=0)
@@ -268,3 +270,22 @@ def test_cfg4_bench_window_k10_regimes_agree(ellpack_lib):
                                                                           b["products"])
         assert all(same_bits_scalar(a[k], b[k]) for k in ("trX", "trS", "e"))
     assert same_bits(da, ds)
+
+
+def test_sp2_dense_allocation_failure_falls_back(ellpack_lib):
+    """A dense step whose arrays cannot be allocated (ELLPACK_OPT_SP2_MEM_CAP fault injection) runs
+    on the sparse kernels instead, and so does the rest of the run: bitwise the oracle."""
+    E = ellpack_lib
+    n = 700
+    H = _sym(n, 9)
+    o = oracle.sp2(H, n // 2, 1e-10, oracle.SP2Opts(threshold=1e-5, max_iter=100), d_width=n)
+    c = _ctx(E, dense=2)
+    c.set_option(E.OPT_SP2_MEM_CAP, 8_600_000)  # below 2 x 768^2 doubles (9.4 MB); two 700-wide iterates fit
+    try:
+        d = E.Mat.empty(n, n)
+        g = c.sp2_run(up(H), n // 2, 1e-10, d, threshold=1e-5, max_iter=100)
+        _compare_sp2(g, o)
+        assert same_bits(d.to_host(), o.D)
+        assert all(it["regime"] == "sparse" for it in g.iters)
+    finally:
+        c.close()
