@@ -1054,6 +1054,12 @@ int ellpack_ctx_destroy(ellpack_ctx c) {
         for (Buf& b : sl) release(c, b);
     for (Buf* b : bufs) release(c, *b);
     cudaStreamSynchronize(c->stream);
+    {
+        // hand the freed workspace (up to two 34 GB dense arrays) back to the device, not to the pool
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+        cudaGetLastError();
+    }
     if (c->comm && g_nccl.ok) g_nccl.CommDestroy(c->comm);
     cudaFree(c->d_status);
     cudaFree(c->d_keys);
