@@ -16,6 +16,7 @@
 #include "devutil.cuh"
 
 #include <climits>
+#include <mutex>
 
 namespace ell {
 
@@ -320,13 +321,15 @@ template <int BM, int TY, bool SYM>
 cudaError_t launch_gemm_t(unsigned grid, const double* At, const double* B, int np, const unsigned long long* fa,
                           const unsigned long long* fb, double* S, unsigned char* tw, unsigned long long* exec,
                           int bi0, cudaStream_t s) {
-    static int attr = 0;  // dynamic shared memory opted in so far (per instantiation)
+    static int attr[64];  // dynamic shared memory opted in so far (per instantiation and device)
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
     const size_t smem = (size_t)kDenseStages * stage_bytes<BM>() + sizeof(int) * (size_t)(np / kDenseK);
-    if (smem > 48 * 1024 && attr < (int)smem) {
+    if (smem > 48 * 1024 && attr[dev] < (int)smem) {
         cudaError_t e = cudaFuncSetAttribute(dense_gemm_kernel<BM, TY, SYM>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e) return e;
-        attr = (int)smem;
+        attr[dev] = (int)smem;
     }
     dense_gemm_kernel<BM, TY, SYM><<<grid, 16 * TY, smem, s>>>(At, B, np, fa, fb, S, tw, exec, bi0);
     return cudaGetLastError();
@@ -552,10 +555,12 @@ __global__ void dense_mma_selfcheck_kernel(unsigned long long* bad) {
 
 // 1: the MMA variant may run on this device (R23 holds here), 0: it may not. Checked once per device.
 int dense_mma_ok(cudaStream_t s) {
+    static std::mutex mu;  // contexts of different host threads may ask at once
     static int checked[64];
     static int verdict[64];
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+    std::lock_guard<std::mutex> lock(mu);
     if (checked[dev]) return verdict[dev];
     unsigned long long* bad = nullptr;
     unsigned long long h = 1;
@@ -575,13 +580,15 @@ template <int BM, bool SYM>
 cudaError_t launch_mma_t(unsigned grid, const double* At, const double* B, int np, const unsigned long long* fa,
                          const unsigned long long* fb, double* S, unsigned char* tw, unsigned long long* exec, int bi0,
                          cudaStream_t s) {
-    static int attr = 0;
+    static int attr[64];  // per device
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
     const size_t stage = (size_t)kMmaKps * kDenseK * ((BM + 4) + kMmaPad) * 8;
     const size_t smem = (size_t)kMmaStages * stage + sizeof(int) * (size_t)(np / kDenseK);
-    if (smem > 48 * 1024 && attr < (int)smem) {
+    if (smem > 48 * 1024 && attr[dev] < (int)smem) {
         cudaError_t e = cudaFuncSetAttribute(dense_mma_kernel<BM, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e) return e;
-        attr = (int)smem;
+        attr[dev] = (int)smem;
     }
     dense_mma_kernel<BM, SYM><<<grid, BM == 128 ? 256 : 128, smem, s>>>(At, B, np, fa, fb, S, tw, exec, bi0);
     return cudaGetLastError();
