@@ -2234,7 +2234,8 @@ int sp2_run(ellpack_ctx c, const ellpack_desc* h, int64_t nocc, double tol, cons
         if (c->dense_opt != 1 && !dense_off && (c->comm ? dense_comm_ok : dense_fits(c, n, sym ? 2 : 3))) {
             // the GEMM's exact work when the last step measured X_n's block occupancy (symmetric X),
             // else the band model
-            w_dense = w_next > 0.0 ? w_next : dense_band_fmas(n, std::max(bwX[0], bwX[1]), sym);
+            // (across ranks every rank computes all tiles of its rows: no mirrored half)
+            w_dense = w_next > 0.0 ? w_next : dense_band_fmas(n, std::max(bwX[0], bwX[1]), sym && !c->comm);
             if (c->dense_opt == 2) {
                 dense_step = true;
             } else if (p_prev > 0.0) {
