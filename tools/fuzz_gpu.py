@@ -1,8 +1,10 @@
 #!/usr/bin/env python
 """Long randomized GPU-vs-oracle sweep (bitwise): multiply (both paths, in place / beta / alpha
-corners, literal-width overflow reports) and small SP2 runs (both branch rules, narrow GROW
-starts, symmetric step). A validation run, not part of the test suite:
-    python tools/fuzz_gpu.py --mult 400 --sp2 40
+corners, literal-width overflow reports), small SP2 runs (both branch rules, narrow GROW starts,
+symmetric step; regimes cycled: automatic, sparse only, every step dense on the host loop) and X^2 in the
+dense regime (symmetric / non-symmetric, both GEMM kernels, sizes 1..3000). A validation run, not part
+of the test suite:
+    python tools/fuzz_gpu.py --mult 400 --sp2 40 --x2dense 60
 """
 import argparse
 import os
@@ -36,6 +38,7 @@ def main():
     ap.add_argument("--mult", type=int, default=400)
     ap.add_argument("--sp2", type=int, default=40)
     ap.add_argument("--seed", type=int, default=77)
+    ap.add_argument("--x2dense", type=int, default=0)
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     ctx = eb.Context(0)
@@ -83,6 +86,10 @@ def main():
         c2 = eb.Context(0)
         if w0:
             c2.set_option(eb.OPT_SP2_WIDTH0, w0)
+        regime = t % 3  # 0 automatic, 1 sparse only, 2 every step dense (host loop)
+        c2.set_option(eb.OPT_DENSE, regime)
+        if regime == 2:
+            c2.set_option(eb.OPT_SP2_DEVICE_LOOP, 1)
         d = eb.Mat.empty(n, n + (n & 1))
         g = c2.sp2_run(eb.Mat.from_host(H), nocc, 1e-9, d, threshold=tau, max_iter=60, branch_rule=rule)
         ok = (g.status == o.status and g.iterations == o.iterations and g.final_width == o.final_width
@@ -92,11 +99,39 @@ def main():
         c2.close()
         if not ok:
             bad_s += 1
-            print("SP2 MISMATCH", t, (n, m, partners, band, tau, rule, w0, nocc), g.status, o.status,
+            print("SP2 MISMATCH", t, (n, m, partners, band, tau, rule, w0, nocc, regime), g.status, o.status,
                   g.iterations, o.iterations, g.final_width, o.final_width, flush=True)
     print(f"sp2: {a.sp2 - bad_s}/{a.sp2} bitwise", flush=True)
+    bad_d = 0
+    for t in range(a.x2dense):
+        n = int(rng.choice([1, 2, 3, 127, 128, 129, 255, 300, 511, 700, 1023, 1300, 1800, 2048, 2500, 3000]))
+        sym = bool(t % 2)
+        w = int(rng.choice([2, 8, 32, 64]))
+        tau = float(rng.choice([0.0, 1e-9, 1e-5, 1e-2]))
+        if sym:
+            X = synth.sym_banded(n, w, int(rng.integers(1, max(2, w // 3))), int(rng.choice([1, 16, 200, 5000])), 1,
+                                 -1.0, 1.0, 0, 8.0, 0.0, 900 + t)
+        else:
+            X = synth.random_sparse(n, w, 0, w, int(rng.choice([1, 16, 200, 5000])), 0.1, 1.0, seed=900 + t)
+        wo = n + (n & 1)
+        Y = synth.Ell.empty(n, wo)
+        r = oracle.x2(X, Y, tau)
+        c3 = eb.Context(0)
+        c3.set_option(eb.OPT_DENSE, 2)
+        kernel = int(rng.integers(0, 2))
+        c3.set_option(eb.OPT_DENSE_KERNEL, kernel)
+        y = eb.Mat.empty(n, wo)
+        st, tx, tx2 = c3.multiply_x2(eb.Mat.from_host(X), y, tau)
+        ok = (st == r.status and c3.last_launch()["path"] == "dense" and same(y.to_host(), Y)
+              and bits(tx, r.trace_x) and bits(tx2, r.trace_x2))
+        c3.close()
+        if not ok:
+            bad_d += 1
+            print("X2 DENSE MISMATCH", t, (n, sym, w, tau, kernel), st, r.status, flush=True)
+    if a.x2dense:
+        print(f"x2 dense: {a.x2dense - bad_d}/{a.x2dense} bitwise", flush=True)
     ctx.close()
-    return 1 if bad or bad_s else 0
+    return 1 if bad or bad_s or bad_d else 0
 
 
 if __name__ == "__main__":
