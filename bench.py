@@ -369,9 +369,21 @@ def time_sp2(eb, mr, dev, ws, rank, cfg: int, K: int, steps: int, warmup: int):
            "products": P, "gflops_effective": 2.0 * P / (ms * 1e-3) / 1e9,
            "host_syncs_per_iteration": syncs / max(r.iterations, 1), "gpu_launches": launches,
            "symmetric_step": True,
-           "regimes": "".join("D" if it["regime"] == "dense" else "s" for it in r.iters)}
+           "regimes": "".join("D" if it["regime"] == "dense" else "s" for it in r.iters),
+           "per_iteration": sp2_per_iteration(r.iters)}
     out.update(sp2_rooflines(r.iters))
     return out
+
+
+def sp2_per_iteration(iters):
+    """SURVEY §8d "SP2 protocol": per iteration the width, P_n, the step's device time, GFLOP/s, e_n,
+    the branch and the regime (compact arrays)."""
+    return {"width": [it["width"] for it in iters], "products": [it["products"] for it in iters],
+            "step_ms": [round(it["step_ms"], 4) if it["step_ms"] == it["step_ms"] else None for it in iters],
+            "gflops": [round(2.0 * it["products"] / (it["step_ms"] * 1e-3) / 1e9, 1)
+                       if it["step_ms"] == it["step_ms"] and it["step_ms"] > 0 else None for it in iters],
+            "e": [it["e"] for it in iters], "branch": "".join("S" if it["branch"] == "SQUARE" else "E" for it in iters),
+            "regime": "".join("D" if it["regime"] == "dense" else "s" for it in iters)}
 
 
 def sp2_rooflines(iters):
@@ -435,7 +447,8 @@ def time_sp2_full(eb, dev, cfg: int = 3, max_iter: int = 100):
            "iterations_per_s": r.iterations / sec, "host_syncs_per_iteration": syncs / max(r.iterations, 1),
            "regimes": "".join("D" if it["regime"] == "dense" else "s" for it in r.iters),
            "dense_iterations": len(dense), "products": sum(it["products"] for it in r.iters),
-           "round1_seconds": 51.18, "round1_source": "profiles/r01_sp2_full_cfg3.json (sparse kernels only)"}
+           "round1_seconds": 51.18, "round1_source": "profiles/r01_sp2_full_cfg3.json (sparse kernels only)",
+           "per_iteration": sp2_per_iteration(r.iters)}
     out.update(sp2_rooflines(r.iters))
     return out
 
@@ -877,7 +890,8 @@ def run_sp2(args):
                        "iterations": its, "stop": r.stop, "final_width": r.final_width, "regrows": r.regrows,
                        "products": prods, "gflops_effective": 2.0 * prods / (ms * 1e-3) / 1e9,
                        "regimes": "".join("D" if it["regime"] == "dense" else "s" for it in r.iters),
-                       "host_syncs_per_iteration": syncs / max(its, 1), "phases_s": r.phases},
+                       "host_syncs_per_iteration": syncs / max(its, 1), "phases_s": r.phases,
+                       "per_iteration": sp2_per_iteration(r.iters)},
             "roofline": roof["roofline"], "roofline_sparse_steps": roof["roofline_sparse_steps"],
             "roofline_dense_steps": roof["roofline_dense_steps"],
             "cpu_baseline": cpu, "gpu_launches": ctx.kernel_launches() - launches0, "clocks": clk.summary(),
