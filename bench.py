@@ -706,6 +706,13 @@ def run_ours(args):
     Bc = x2_bytes(live_entries(X), nnz_c, n)
     hbm_peak, peak_src = peaks()
     kern_avg = kern_ms / max(kern_n, 1)
+    # with N > 1 ranks, exchange-inclusive (the step: halo + every launch, max over ranks)
+    # and multiply-only (the row kernels alone, max over ranks) reported separately
+    multi = None
+    if ws > 1:
+        multi = {"exchange_inclusive_ms_per_step": ms_step,
+                 "row_kernels_ms_per_step_max_over_ranks": mr.max_over_ranks(kern_ms / args.steps, device="cuda"),
+                 "halo": "band-aware, ncclSend/ncclRecv on a second stream, overlapped with the interior rows"}
     bytes_launch = Bc / ws  # equal row blocks: the rank's share of the compulsory bytes
     achieved = bytes_launch / (kern_avg * 1e-3) / 1e9
     cap, cap_src = ncu_capture(f"x2_n{n}_m{args.m}")
@@ -800,6 +807,7 @@ def run_ours(args):
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "lsu_pipe": lsu_pipe},
             "sp2": sp2, "cfg1": cfg1, "cfg2": cfg2, "cfg5_sweep": sweep, "dense_gemm": dense_gemm,
+            "multi_gpu": multi,
             "ranks_bitwise_vs_1": ranks_checked,
             "cpu_baseline": cpu,
             "e2e": e2e,
