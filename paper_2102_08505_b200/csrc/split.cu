@@ -39,6 +39,12 @@ namespace ell {
 #ifndef ELL_SPLIT_META
 #define ELL_SPLIT_META 0  // W = 1: the next half's step metadata read into registers one half ahead
 #endif
+#ifndef ELL_SPLIT_LEAN_EMIT
+#define ELL_SPLIT_LEAN_EMIT 1  // W = 1: emission without per-block diagonal work (round 2)
+#endif
+#ifndef ELL_SPLIT_CLEAR_STS
+#define ELL_SPLIT_CLEAR_STS 0  // W = 1 lean emission: read + store zero instead of atom.exch
+#endif
 #ifndef ELL_SPLIT_HB_G3
 #define ELL_SPLIT_HB_G3 2  // W = 1, G = 3: steps per register half
 #endif
@@ -268,6 +274,64 @@ __device__ __forceinline__ void split_emit(const RowOpParams& p, const SplitSmem
     const unsigned lt = (1u << lane) - 1u;
     const int cw = p.C.w;
     const uint64_t bv = opaque_u64((uint64_t)crow_v), bc = opaque_u64((uint64_t)crow_c);
+    if constexpr (W == 1 && ELL_SPLIT_LEAN_EMIT) {
+        // One warp owns the whole block: the diagonal bookkeeping only in the block that holds
+        // column i (warp-uniform branch), the keep decision straight from the compare, one
+        // bounds compare per chunk (entries past the width are counted, not written).
+        const bool want_dc = MODE != 0 || p.diag_c != nullptr;
+        while (R.F < Fto) {
+            const int F = R.F, sF = R.sF;
+            const uint32_t di = (uint32_t)(R.i - (int64_t)F);
+            const bool dblk = di < 128u;
+            if (dblk && lane == (int)(di & 31u)) R.ds = lds64(sm.acc + 8u * (uint32_t)(sF + (int)di));
+            if (MODE != 0)
+                split_merge_old<W, MODE>(p, sm, lane, wid, F + 128, F, sF, o_col, o_val, nOld, R.old_cur, R.nrm);
+            double x[4];
+            bool kp[4];
+            unsigned m[4];
+            const uint32_t a0 = sm.acc + 8u * (uint32_t)(sF + lane);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint32_t off = (uint32_t)(sF + 32 * t + lane);
+                double v;
+                if (ELL_SPLIT_CLEAR_STS) {
+                    v = lds64(a0 + 256u * t);
+                    sts64(a0 + 256u * t, 0.0);
+                } else {
+                    v = lds64_clear(a0 + 256u * t);
+                }
+                bool flagged = false;
+                if (MODE != 0) {
+                    flagged = lds8(sm.flg + off) != 0;
+                    sts8(sm.flg + off, 0u);
+                }
+                x[t] = v;
+                if (!flagged) {
+                    if (!A1) x[t] = __dmul_rn(p.alpha, v);
+                    if (MODE == 2) R.nrm = __fma_rn(v, v, R.nrm);
+                }
+                kp[t] = fabs(x[t]) > tau;
+                m[t] = __ballot_sync(FULL, kp[t]);
+            }
+            uint32_t before = (uint32_t)R.kept;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint32_t pos = before + (uint32_t)__popc(m[t] & lt);
+                st_entry(kp[t] && pos < (uint32_t)cw, reinterpret_cast<double*>(bv + 8ull * pos),
+                         reinterpret_cast<int32_t*>(bc + 4ull * pos), x[t], F + 32 * t + lane);
+                before += (uint32_t)__popc(m[t]);
+            }
+            if (dblk && want_dc) {
+                const uint32_t tq = di >> 5;  // selects, not an indexed (local-memory) access
+                const double xs = tq == 0 ? x[0] : tq == 1 ? x[1] : tq == 2 ? x[2] : x[3];
+                const bool ks = tq == 0 ? kp[0] : tq == 1 ? kp[1] : tq == 2 ? kp[2] : kp[3];
+                if (lane == (int)(di & 31u)) R.dc = ks ? xs : 0.0;
+            }
+            R.kept = (int)before;
+            R.F = F + 128;
+            R.sF = sF + 128 == S ? 0 : sF + 128;
+        }
+    } else {
     while (R.F < Fto) {
         const int F = R.F, sF = R.sF;
         // the pre-combine diagonal s_ii (tr X^2 pre-drop, R5): read before the Old merge
@@ -328,6 +392,7 @@ __device__ __forceinline__ void split_emit(const RowOpParams& p, const SplitSmem
         R.kept += cnt[0] + cnt[1] + cnt[2] + cnt[3];
         R.F = F + 128;
         R.sF = sF + 128 == S ? 0 : sF + 128;
+    }
     }
 }
 
