@@ -16,25 +16,72 @@
 namespace ell {
 
 // The sequential sum over the block partials (c7 second level), one array at a time: the whole CTA
-// stages the partials in shared memory (independent coalesced loads), then one thread adds them in
-// block order -- the dependent chain runs on shared-memory operands, not on global-load latency.
-__global__ void final_sums_kernel(const double* partials, int narr, int64_t nblocks, double* out) {
+// stages the partials in shared memory (independent coalesced loads, all of a thread's loads issued
+// before its stores: a generic load may alias shared memory, so a load-store-load sequence would
+// wait out every load), then one thread adds them in block order -- the dependent chain runs on
+// shared-memory operands, not on global-load latency.
+__global__ void __launch_bounds__(256) final_sums_kernel(const double* __restrict__ partials, int narr,
+                                                         int64_t nblocks, double* out) {
     __shared__ double sp[2048];
     for (int a = 0; a < narr; ++a) {
         double s = 0.0;
         for (int64_t b0 = 0; b0 < nblocks; b0 += 2048) {
             const int cnt = (int)(nblocks - b0 < 2048 ? nblocks - b0 : 2048);
             __syncthreads();
-            for (int t = threadIdx.x; t < cnt; t += blockDim.x) sp[t] = partials[(size_t)a * nblocks + b0 + t];
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int t = (int)threadIdx.x + 256 * u;
+                v[u] = t < cnt ? __ldg(partials + (size_t)a * nblocks + b0 + t) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int t = (int)threadIdx.x + 256 * u;
+                if (t < cnt) sp[t] = v[u];
+            }
             __syncthreads();
-            if (threadIdx.x == 0)
+            if (threadIdx.x == 0) {
+#pragma unroll 16
                 for (int t = 0; t < cnt; ++t) s = __dadd_rn(s, sp[t]);
+            }
         }
         if (threadIdx.x == 0) out[a] = s;
     }
 }
 
 struct PtrPack { const double* p[8]; };
+
+// array a of the pack by selects (an indexed param array would be copied to local memory)
+__device__ __forceinline__ const double* pick_array(const PtrPack& pk, int a) {
+    const double* d = pk.p[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) d = a == q ? pk.p[q] : d;
+    return d;
+}
+
+// a 256-row block's values d[0, cnt) into shared sv by one warp: every load in flight before the
+// first store (see final_sums_kernel)
+__device__ __forceinline__ void stage_block(const double* __restrict__ d, int cnt, int lane, double* sv) {
+    double v[kTraceBlock / 32];
+#pragma unroll
+    for (int u = 0; u < kTraceBlock / 32; ++u) {
+        const int q = lane + 32 * u;
+        v[u] = q < cnt ? __ldg(d + q) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kTraceBlock / 32; ++u) {
+        const int q = lane + 32 * u;
+        if (q < cnt) sv[q] = v[u];
+    }
+}
+
+// lane 0: the block's values in row order (c7 first level)
+__device__ __forceinline__ double block_chain(const double* sv, int cnt) {
+    double s = 0.0;
+#pragma unroll 16
+    for (int q = 0; q < cnt; ++q) s = __dadd_rn(s, sv[q]);
+    return s;
+}
 
 // One 256-row block of one array per 32-thread group: the lanes stage the block's values in shared
 // memory with coalesced loads, then lane 0 adds them in row order (c7 first level: the dependent
@@ -48,17 +95,11 @@ __global__ void block_partials_pack_kernel(PtrPack arrays, int narr, int64_t b0,
     if (t >= nb * narr) return;
     const int a = (int)(t / nb);
     const int64_t b = b0 + t % nb;
-    const double* d = arrays.p[a];
     const int64_t r0 = b * kTraceBlock;
     const int cnt = (int)(min(r0 + kTraceBlock, row_end) - r0);
-    for (int q = lane; q < cnt; q += 32) sv[g][q] = d[r0 + q];
+    stage_block(pick_array(arrays, a) + r0, cnt, lane, sv[g]);
     __syncwarp();
-    if (lane == 0) {
-        double s = 0.0;
-#pragma unroll 8
-        for (int q = 0; q < cnt; ++q) s = __dadd_rn(s, sv[g][q]);
-        partials[(size_t)a * nblocks_total + b] = s;
-    }
+    if (lane == 0) partials[(size_t)a * nblocks_total + b] = block_chain(sv[g], cnt);
 }
 
 // Both levels in one CTA for a small matrix (narr * nblocks <= 16, one rank): warp t sums (array,
@@ -71,17 +112,11 @@ __global__ void canonical_small_kernel(PtrPack arrays, int narr, int64_t n, doub
     const int nb = (int)((n + kTraceBlock - 1) / kTraceBlock);
     if (g < narr * nb) {
         const int a = g / nb, b = g % nb;
-        const double* d = arrays.p[a];
         const int64_t r0 = (int64_t)b * kTraceBlock;
         const int cnt = (int)(min(r0 + kTraceBlock, n) - r0);
-        for (int q = lane; q < cnt; q += 32) sv[g][q] = d[r0 + q];
+        stage_block(pick_array(arrays, a) + r0, cnt, lane, sv[g]);
         __syncwarp();
-        if (lane == 0) {
-            double s = 0.0;
-#pragma unroll 8
-            for (int q = 0; q < cnt; ++q) s = __dadd_rn(s, sv[g][q]);
-            sp[g] = s;
-        }
+        if (lane == 0) sp[g] = block_chain(sv[g], cnt);
     }
     __syncthreads();
     if ((int)threadIdx.x < narr) {
