@@ -156,11 +156,17 @@ int ellpack_ctx_set_stream(ellpack_ctx ctx, void* stream);
  *  ELLPACK_OPT_DENSE_KERNEL the dense GEMM's 128-row tiles: 0 (default) = on the FP64 MMA
  *                          (mma.sync m8n8k4) when a per-device self-check confirms it computes the
  *                          ascending fma chain bit for bit, else on FP64 FMAs; 1 = FP64 FMAs;
- *                          2 = the FP64 MMA (tests). Results are bitwise the same either way. */
+ *                          2 = the FP64 MMA (tests). Results are bitwise the same either way.
+ *  ELLPACK_OPT_SMALL_KERNEL 0 (default) = ellpack_multiply_x2 on a small matrix (N <= 1024, one
+ *                          rank, input width <= 64) runs the small-matrix kernel: 16 B rows' gathers
+ *                          in flight per warp, status and the canonical trace sums finished by the
+ *                          last CTA, one launch; 1 = the general path (row kernel + trace-sum kernel).
+ *                          Results are bitwise the same either way. */
 enum { ELLPACK_OPT_WINDOW = 1, ELLPACK_OPT_WARPS = 2, ELLPACK_OPT_SP2_WIDTH0 = 3, ELLPACK_OPT_PROFILE = 4,
        ELLPACK_OPT_ABLATE = 5, ELLPACK_OPT_GENERAL_WINDOW = 6, ELLPACK_OPT_VALIDATE = 7,
        ELLPACK_OPT_SP2_SYMMETRIC = 8, ELLPACK_OPT_SP2_MEM_CAP = 9, ELLPACK_OPT_RING_KERNEL = 10,
-       ELLPACK_OPT_SP2_DEVICE_LOOP = 11, ELLPACK_OPT_DENSE = 12, ELLPACK_OPT_DENSE_KERNEL = 13 };
+       ELLPACK_OPT_SP2_DEVICE_LOOP = 11, ELLPACK_OPT_DENSE = 12, ELLPACK_OPT_DENSE_KERNEL = 13,
+       ELLPACK_OPT_SMALL_KERNEL = 14 };
 int ellpack_ctx_set_option(ellpack_ctx ctx, int key, int64_t value);
 
 /* Accumulated device time (ms, CUDA events on the ctx stream) and launch count of
@@ -175,7 +181,7 @@ int64_t ellpack_ctx_kernel_launches(ellpack_ctx ctx);
 int64_t ellpack_ctx_host_syncs(ellpack_ctx ctx);
 
 /* Launch geometry of the last fused row-kernel launch on this context (what bench.py reports
- * beside its roofline): out[0] path (4 dense regime -- out[1..7] then stale, 3 warp-specialized ring
+ * beside its roofline): out[0] path (5 the small-matrix kernel of ellpack_multiply_x2, 4 dense regime -- out[1..7] then stale, 3 warp-specialized ring
  * kernel, 2 split-row ring kernel, 1 one-warp ring kernel, 0 general path), out[1] G (64-entry B groups per step, ring paths), out[2] S (ring / window doubles per
  * row), out[3] warps per CTA (split kernel: warps per row),
  * out[4] grid, out[5] dynamic shared memory bytes per CTA, out[6] resident CTAs per SM,

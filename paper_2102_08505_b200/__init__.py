@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _REPO = os.path.dirname(_HERE)
 _LIB = os.environ.get("ELLPACK_LIB") or os.path.join(_HERE, "libellpack.so")
-_SRCS = [os.path.join(_HERE, "csrc", f) for f in ("spgemm.cu", "split.cu", "reduce.cu", "sp2_graph.cu", "dense.cu",
+_SRCS = [os.path.join(_HERE, "csrc", f) for f in ("spgemm.cu", "split.cu", "reduce.cu", "sp2_graph.cu", "dense.cu", "tiny.cu",
                                                           "api.cu")]
 _HDRS = [os.path.join(_HERE, "csrc", f) for f in ("internal.cuh", "devutil.cuh", "dense.cuh")] + [os.path.join(_REPO, "include", "ellpack.h")]
 
@@ -34,6 +34,7 @@ OPT_RING_KERNEL = 10
 OPT_SP2_DEVICE_LOOP = 11
 OPT_DENSE = 12
 OPT_DENSE_KERNEL = 13
+OPT_SMALL_KERNEL = 14
 SP2_FAIL, SP2_GROW = 0, 1
 SP2_RULE_TRACE_SIGN, SP2_RULE_TRACE_CLOSEST = 0, 1
 STOP_NAMES = {0: "CONVERGED", 1: "STAGNATED", 2: "NOCONV", 3: "OVERFLOW"}
@@ -275,7 +276,7 @@ class Context:
         """Geometry of the last row-kernel launch (ellpack_ctx_last_launch)."""
         a = (ctypes.c_int32 * 8)()
         _chk(lib().ellpack_ctx_last_launch(self._h, a), "ellpack_ctx_last_launch")
-        return dict(path={4: "dense", 3: "ws", 2: "split", 1: "ring", 0: "general"}[a[0]], G=a[1], S=a[2], warps_per_cta=a[3],
+        return dict(path={5: "small", 4: "dense", 3: "ws", 2: "split", 1: "ring", 0: "general"}[a[0]], G=a[1], S=a[2], warps_per_cta=a[3],
                     grid=a[4],
                     smem_bytes=a[5], ctas_per_sm=a[6], hB=a[7])
 

@@ -113,6 +113,7 @@ struct ellpack_ctx_s {
     LaunchCfg last_cfg{};
     int32_t last_fast = 0, last_hB = 0, last_split = 0;
     int ring_kernel = 0;  // ELLPACK_OPT_RING_KERNEL
+    int small_kernel = 0;  // ELLPACK_OPT_SMALL_KERNEL
     int sp2_loop = 0;     // ELLPACK_OPT_SP2_DEVICE_LOOP
     int force_general_s = 0;  // device SP2 loop: every row op on the general path with this window
     Buf sp2dev, sp2rec;       // device SP2 loop: control block, iteration records
@@ -121,7 +122,7 @@ struct ellpack_ctx_s {
     int x2_exec_launches = 0;
     bool x2_exec_ok = false;             // cleared by every option change (the launch plan depends on them)
     LaunchCfg x2_cfg{};                  // the captured call's launch record (ellpack_ctx_last_launch)
-    int x2_fast = 0, x2_split = 0, x2_hB = 0;
+    int x2_fast = 0, x2_split = 0, x2_hB = 0, x2_small = 0;
     cudaGraphExec_t sp2_exec = nullptr;  // device SP2 loop: the instantiated graph and what it captured
     uint64_t sp2_exec_key = 0;
     int sp2_exec_launches = 0;
@@ -133,6 +134,7 @@ struct ellpack_ctx_s {
     Buf docc;              // dense regime: occupancy bitsets of the next SP2 operand (exact GEMM work)
     Buf old_val, old_col, old_nnz;  // ellpack_multiply with beta != 0: the scratch copy of C_old
     int last_dense = 0;    // the last SP2 step / X^2 ran in the dense regime
+    int last_small = 0;    // the last X^2 ran the small-matrix kernel (tiny.cu)
     int64_t dense_clean_np = 0;  // dense[0] is zero outside the blocks dflags' fa marks (for this N_p)
     int64_t dense_fit_key = -1;  // dense_fits: the cached free-memory answer (N_p, arrays)
     bool dense_fit_ok = false;
@@ -145,6 +147,7 @@ struct ellpack_ctx_s {
         double sums[8];
         int32_t imax;
     }* h = nullptr;
+    Host* h_dev = nullptr;  // the same pinned block as the device addresses it (mapped; nullable)
     // workspace
     Buf rows[4];      // per-row double arrays
     Buf partials;     // canonical block partials
@@ -156,6 +159,7 @@ struct ellpack_ctx_s {
     Buf halo;  // all ranks' referenced row ranges (halo exchange)
     Buf vflag; // ELLPACK_OPT_VALIDATE violation flag
     Buf symaux; // symmetric SP2 step: [0] H asymmetric flag, [1] U reach, [2..3] U status
+    Buf tiny;   // small-matrix kernel (tiny.cu): [0] last-CTA counter (kept zero), [4..) 2 ints per CTA
     Buf it[4][3];  // SP2 iterate buffers (val, col, nnz) x 4 slots
     int32_t* h_reach = nullptr;  // pinned: every rank's probe reach (2 per rank), fetched with a step
     // ring sizing cache: (hB, G, mode) -> (S, rows resident per SM)
@@ -360,6 +364,7 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
                    const RowOpExtra* ex = nullptr) {
     p.ncols = n;
     c->last_dense = 0;
+    c->last_small = 0;
     const bool has_old = p.old_mode != 0;
     // A small matrix (N <= kNoProbeN, one rank) needs no probe: one general-path window covers every
     // column, so nothing depends on the bandwidths and the call waits on the device once, at the end
@@ -788,6 +793,7 @@ int enqueue_dense_op(ellpack_ctx c, RowOpParams& p, int64_t n, bool sym, const i
     c->launches++;
     c->last_upper = 0;
     c->last_dense = 1;
+    c->last_small = 0;
     p.fast = 0;
     return ELLPACK_OK;
 }
@@ -1029,6 +1035,12 @@ int ellpack_ctx_create(int device, void* stream, ellpack_ctx* out) {
     if (!e) e = cudaMalloc(&c->d_sums, 64);
     if (!e) e = cudaMalloc(&c->d_bw, 64);
     if (!e) e = cudaMallocHost(&c->h, sizeof(ellpack_ctx_s::Host));
+    if (!e) {  // the device's view of the pinned block: the small-matrix kernel writes its status and
+               // sums there directly (no read-back copies); null when the device cannot map it
+        void* hd = nullptr;
+        if (cudaHostGetDevicePointer(&hd, c->h, 0) == cudaSuccess) c->h_dev = (ellpack_ctx_s::Host*)hd;
+        cudaGetLastError();
+    }
     for (int k = 0; k < 6 && !e; ++k) e = cudaEventCreate(&c->ev[k]);
     for (int k = 0; k < 4 && !e; ++k) {
         e = cudaEventCreate(&c->pev[k][0]);
@@ -1045,7 +1057,7 @@ int ellpack_ctx_destroy(ellpack_ctx c) {
     Buf* bufs[] = {&c->rows[0], &c->rows[1], &c->rows[2], &c->rows[3], &c->partials,
                    &c->stash_val, &c->stash_col, &c->ident_val, &c->ident_col, &c->ident_nnz,
                    &c->hx_val, &c->hx_col, &c->hx_nnz, &c->hy_val, &c->hy_col, &c->hy_nnz,
-                   &c->bt, &c->bt_nbin, &c->bp, &c->halo, &c->vflag, &c->symaux, &c->sp2dev, &c->sp2rec,
+                   &c->bt, &c->bt_nbin, &c->bp, &c->halo, &c->vflag, &c->symaux, &c->sp2dev, &c->sp2rec, &c->tiny,
                    &c->dense[0], &c->dense[1], &c->dense[2], &c->dflags, &c->docc,
                    &c->old_val, &c->old_col, &c->old_nnz};
     if (c->sp2_exec) cudaGraphExecDestroy(c->sp2_exec);
@@ -1104,6 +1116,10 @@ int ellpack_ctx_set_option(ellpack_ctx c, int key, int64_t v) {
             if (v > 2) return ELLPACK_ERR_ARG;
             c->dense_kernel = (int)v;
             return ELLPACK_OK;
+        case ELLPACK_OPT_SMALL_KERNEL:
+            if (v > 1) return ELLPACK_ERR_ARG;
+            c->small_kernel = (int)v;
+            return ELLPACK_OK;
         case ELLPACK_OPT_RING_KERNEL:
             if (v > 4) return ELLPACK_ERR_ARG;
             c->ring_kernel = (int)v;
@@ -1149,6 +1165,7 @@ int ellpack_ctx_last_launch(ellpack_ctx c, int32_t out[8]) {
     // 3: warp-specialized ring kernel, 2: split-row ring kernel (out[3] = W warps per row)
     out[0] = c->last_split < 0 ? 3 : (c->last_split ? 2 : c->last_fast);
     if (c->last_dense) out[0] = 4;  // dense regime (dense.cu): out[1..7] describe no row kernel
+    if (c->last_small) out[0] = 5;  // small-matrix kernel (tiny.cu)
     return ELLPACK_OK;
 }
 
@@ -1287,7 +1304,36 @@ int ellpack_multiply_x2(ellpack_ctx c, const ellpack_desc* x, ellpack_desc* x2, 
         if ((p.row_begin != 0 || p.row_end != n) && dense_sym != 1) dense_sym = -1;
     }
     c->last_dense = 0;
+    // a small matrix on one rank: the small-matrix kernel (tiny.cu) -- one launch that also writes
+    // the status and the canonical sums of tr X, tr X^2
+    const bool tiny = dense_sym < 0 && n <= kNoProbeN && !c->comm && c->window_opt == 0 && c->ring_kernel == 0 &&
+                      c->small_kernel == 0 && !c->profile && tiny_eligible(p, n);
+    if (tiny) {
+        // counter + 2 ints per CTA, zeroed once here (the kernel leaves the counter zero); grown
+        // outside any graph capture
+        const size_t tb = 16 + 8 * (size_t)((n + 3) / 4);
+        if (c->tiny.bytes < tb) {
+            RK(grow(c, c->tiny, tb));
+            CK(cudaMemsetAsync(c->tiny.p, 0, c->tiny.bytes, c->stream));
+        }
+    }
     auto enqueue = [&]() -> int {
+        if (tiny) {
+            p.ncols = n;
+            p.status = c->d_status;  // written whole by the last CTA (no memset)
+            // status and sums straight into the pinned host block when it is mapped (the read-back
+            // copies are then not needed), else into the device status/sums
+            CK(launch_tiny(p, n, (unsigned int*)c->tiny.p, (int32_t*)((char*)c->tiny.p + 16),
+                           c->h_dev ? c->h_dev->status : c->d_status, c->h_dev ? c->h_dev->sums : c->d_sums,
+                           c->stream));
+            c->launches++;
+            c->last_cfg = LaunchCfg{(int)((n + 31) & ~int64_t(31)), 4, (int)((n + 3) / 4), tiny_smem(n), 0, 0};
+            c->last_fast = 0;
+            c->last_split = 0;
+            c->last_hB = 0;
+            c->last_small = 1;
+            return ELLPACK_OK;
+        }
         if (dense_sym >= 0) RK(enqueue_dense_op(c, p, n, dense_sym == 1));
         else RK(enqueue_row_op(c, p, n));
         const double* arrs[2] = {p.diag_a, p.diag_s};
@@ -1325,7 +1371,9 @@ int ellpack_multiply_x2(ellpack_ctx c, const ellpack_desc* x, ellpack_desc* x2, 
             if (!e) {
                 c->stream = cs;
                 rc = enqueue();
-                if (rc == ELLPACK_OK) rc = fetch_copies(c, 2);  // the read-back copies are graph nodes too
+                // the read-back copies are graph nodes too (none when the small-matrix kernel
+                // wrote to the mapped host block)
+                if (rc == ELLPACK_OK && !(tiny && c->h_dev)) rc = fetch_copies(c, 2);
                 c->stream = saved;
                 e = cudaStreamEndCapture(cs, &g);
             }
@@ -1350,6 +1398,7 @@ int ellpack_multiply_x2(ellpack_ctx c, const ellpack_desc* x, ellpack_desc* x2, 
             c->x2_fast = c->last_fast;
             c->x2_split = c->last_split;
             c->x2_hB = c->last_hB;
+            c->x2_small = c->last_small;
         }
         CK(cudaGraphLaunch(c->x2_exec, c->stream));
         c->launches += c->x2_exec_launches;
@@ -1357,10 +1406,12 @@ int ellpack_multiply_x2(ellpack_ctx c, const ellpack_desc* x, ellpack_desc* x2, 
         c->last_fast = c->x2_fast;
         c->last_split = c->x2_split;
         c->last_hB = c->x2_hB;
+        c->last_small = c->x2_small;
         RK(host_sync(c));
     } else {
         RK(enqueue());
-        RK(fetch(c, 2));
+        if (tiny && c->h_dev) RK(host_sync(c));
+        else RK(fetch(c, 2));
     }
     RK(finish_status(c));
     if (trace_x) *trace_x = c->h->sums[0];

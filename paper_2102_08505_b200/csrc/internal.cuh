@@ -120,6 +120,13 @@ cudaError_t launch_count_over_dev(const int32_t* nnz, int64_t n, const Sp2Dev* d
 cudaError_t launch_sp2_ctl(Sp2Dev* dev, const double* sums, const int32_t* status, int32_t* ovf,
                            unsigned long long* prod, void* rec, unsigned long long cond_handle, cudaStream_t s);
 
+// tiny.cu: the small-matrix kernel (N <= 1024, one rank, no Old operand, B rows <= 64 slots,
+// diag_a and diag_s set): rows, status and (sums != nullptr) the canonical sums of diag_a, diag_s
+bool tiny_eligible(const RowOpParams& p, int64_t n);
+size_t tiny_smem(int64_t n);
+cudaError_t launch_tiny(const RowOpParams& p, int64_t n, unsigned int* counter, int32_t* part, int32_t* status,
+                        double* sums, cudaStream_t s);
+
 // split.cu: the split-row ring kernel (W warps per row, 16-bit balanced sub-records)
 cudaError_t plan_split(const RowOpParams& p, int S, int W, int G, int num_sms, LaunchCfg* cfg);
 cudaError_t launch_split(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s);

@@ -751,7 +751,12 @@ def test_kernel_launch_counter(ctx):
     before = ctx.kernel_launches()
     X = synth.cfg1()
     gpu_x2(ctx, X, 256, 1e-5)
-    # N = 512 <= 1024: no probe, one general-path window covering every column (no breakpoints):
-    # the row kernel + the one-CTA canonical sums
+    # N = 512 <= 1024: no probe; the small-matrix kernel (rows, status and the canonical sums in
+    # one launch)
+    assert ctx.kernel_launches() - before == 1
+    assert ctx.last_launch()["path"] == "small"
+    ctx.set_option(eb().OPT_SMALL_KERNEL, 1)  # the general path: one window covering every column
+    before = ctx.kernel_launches()          # (no breakpoints), the row kernel + the one-CTA sums
+    gpu_x2(ctx, X, 256, 1e-5)
     assert ctx.kernel_launches() - before == 2
     assert ctx.last_launch()["path"] == "general"

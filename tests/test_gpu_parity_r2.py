@@ -357,6 +357,7 @@ def test_small_x2_graph_replay_bitwise(ellpack_lib):
     host synchronisation."""
     import torch
     ctx = ellpack_lib.Context(0)
+    ctx.set_option(ellpack_lib.OPT_SMALL_KERNEL, 1)  # the general path's graph (row kernel + sums)
     try:
         n, w = 600, 24
         Xs = [synth.random_sparse(n, w, 4, w, band=40, seed=900 + s) for s in range(3)]
@@ -408,3 +409,44 @@ def test_small_x2_graph_replay_bitwise(ellpack_lib):
         assert check(Xs[2], 1e-9, 8, ys) == ellpack_lib.ERR_OVERFLOW
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("n,w,kmin,band,p_empty,seed", [
+    (1, 4, 1, None, 0.0, 0), (7, 8, 0, None, 0.3, 1), (33, 16, 2, 8, 0.0, 2), (129, 32, 1, 40, 0.1, 3),
+    (256, 32, 32, None, 0.0, 4), (600, 24, 4, 40, 0.0, 5), (1000, 48, 8, 300, 0.05, 6),
+    (1024, 64, 60, None, 0.0, 7), (513, 40, 0, 64, 0.5, 8)])
+def test_small_kernel_bitwise(ellpack_lib, n, w, kmin, band, p_empty, seed):
+    """The small-matrix kernel (tiny.cu: N <= 1024, input width <= 64, the default for
+    ellpack_multiply_x2 there) against the oracle and against the general path
+    (ELLPACK_OPT_SMALL_KERNEL 1), bitwise: values, patterns, traces, literal-width overflow reports;
+    one launch and one host synchronisation per call, replayed from the captured graph."""
+    X = synth.random_sparse(n, w, kmin, w, band=band, p_empty=p_empty, seed=1700 + seed)
+    x = up(X)
+    outs = {}
+    for small in (0, 1):
+        ctx = ellpack_lib.Context(0)
+        try:
+            ctx.set_option(ellpack_lib.OPT_SMALL_KERNEL, small)
+            for tau, w_out in ((1e-5, min(n + (n & 1), 1024)), (0.0, min(n + (n & 1), 1024)), (1e-9, 4)):
+                y = ellpack_lib.Mat.empty(n, w_out)
+                Y = oracle.Ell.empty(n, w_out)
+                r = oracle.x2(X, Y, tau)
+                for rep in range(2):  # capture, then a replay
+                    l0, s0 = ctx.kernel_launches(), ctx.host_syncs()
+                    st, tx, tx2 = ctx.multiply_x2(x, y, tau)
+                    assert st == r.status
+                    assert ctx.host_syncs() - s0 == 1
+                    if small == 0:
+                        assert ctx.kernel_launches() - l0 == 1
+                    if st == ellpack_lib.OK:
+                        assert same_bits(y.to_host(), Y)
+                        assert np.float64(tx).view(np.uint64) == np.float64(r.trace_x).view(np.uint64)
+                        assert np.float64(tx2).view(np.uint64) == np.float64(r.trace_x2).view(np.uint64)
+                        outs.setdefault((tau, w_out), []).append((y.to_host(), tx, tx2))
+                    else:
+                        assert ctx.overflow_info() == (r.overflow_rows, r.required_width)
+        finally:
+            ctx.close()
+    for k, v in outs.items():  # both paths, every call: the same bits
+        for (a, ta, ta2) in v[1:]:
+            assert same_bits(a, v[0][0]) and (ta, ta2) == (v[0][1], v[0][2])
