@@ -182,11 +182,12 @@ def x2_bytes(nnz_x: int, nnz_c: int, n: int) -> int:
 
 
 def lsu_floor(X, P: int, nnz_c: int, sm_mhz, num_sms: int = 148, slot_bytes: int = 4) -> dict:
-    """The ring kernel's L1/LSU data-pipe floor: one 128-byte wavefront per
-    SM-cycle; per product a 64-bit LDS + STS on the ring (4 wavefronts per 32 lanes) and a
-    (8 + slot_bytes)-byte B record gather; per output-span column one read-and-clear (2 per 32);
-    per kept entry 12 bytes stored. Conflict-free, unpadded counts: the floor a perfect schedule
-    would meet."""
+    """The ring kernel's L1/LSU data-pipe floor, in SM-cycles: per product a 64-bit
+    LDS + STS on the ring -- a conflict-free 32-lane STS.64 takes 2 cycles, an LDS.64 1 (loads are
+    served at 256 B/clk: tools/bank_model.cu, profiles/r02_bank_model.log), so 3 cycles per 32
+    products -- and a (8 + slot_bytes)-byte B record gather (one 128-byte wavefront per cycle);
+    per output-span column one read-and-clear (2 per 32); per kept entry 12 bytes stored.
+    Conflict-free, unpadded counts: the floor a perfect schedule would meet."""
     nnz = X.nnz.astype(np.int64)
     live = nnz > 0
     rows = np.flatnonzero(live)
@@ -196,7 +197,7 @@ def lsu_floor(X, P: int, nnz_c: int, sm_mhz, num_sms: int = 148, slot_bytes: int
     lo = np.maximum(0, first - hB) & ~31
     hi = (np.minimum(X.n - 1, last + hB) + 32) & ~31
     cols = int((hi - lo).sum())
-    wf = P * (4 / 32 + (8 + slot_bytes) / 128) + cols * (2 / 32) + nnz_c * (12 / 128)
+    wf = P * (3 / 32 + (8 + slot_bytes) / 128) + cols * (2 / 32) + nnz_c * (12 / 128)
     if not sm_mhz:
         return {"wavefronts": wf, "floor_ms": None}
     return {"wavefronts": wf, "output_span_columns": cols, "sm_mhz": sm_mhz,
