@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--sp2", type=int, default=40)
     ap.add_argument("--seed", type=int, default=77)
     ap.add_argument("--x2dense", type=int, default=0)
+    ap.add_argument("--x2small", type=int, default=0, help="X^2 on the small-matrix kernel (N <= 1024)")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     ctx = eb.Context(0)
@@ -102,6 +103,32 @@ def main():
             print("SP2 MISMATCH", t, (n, m, partners, band, tau, rule, w0, nocc, regime), g.status, o.status,
                   g.iterations, o.iterations, g.final_width, o.final_width, flush=True)
     print(f"sp2: {a.sp2 - bad_s}/{a.sp2} bitwise", flush=True)
+    bad_t = 0
+    for t in range(a.x2small):  # X^2, N <= 1024, width <= 64: the small-matrix kernel (tiny.cu)
+        n = int(rng.integers(1, 1025))
+        w = int(rng.choice([2, 4, 8, 16, 30, 32, 34, 48, 64]))  # the ABI stores 16-byte slot pairs (R20)
+        kmax = int(rng.integers(1, w + 1))
+        kmin = int(rng.integers(0, kmax + 1))
+        band = int(rng.choice([1, 5, 40, 300, 2000]))
+        pe = float(rng.choice([0.0, 0.1, 0.6]))
+        tau = float(rng.choice([0.0, 1e-9, 1e-5, 1e-2, 10.0]))
+        X = synth.random_sparse(n, w, kmin, kmax, band, pe, float(rng.choice([1e-3, 1.0, 1e3])), seed=90000 + t)
+        lit = oracle.x2(X, oracle.Ell.empty(n, w), tau)
+        wo = max(2, ((lit.required_width + 31) // 32) * 32)
+        Y = oracle.Ell.empty(n, wo)
+        r = oracle.x2(X, Y, tau)
+        x = eb.Mat.from_host(X)
+        y = eb.Mat.empty(n, wo)
+        st, tx, tx2 = ctx.multiply_x2(x, y, tau)
+        ok = (st == eb.OK and r.status == oracle.OK and ctx.last_launch()["path"] == "small" and same(y.to_host(), Y)
+              and bits(tx, r.trace_x) and bits(tx2, r.trace_x2))
+        if lit.status != oracle.OK:
+            st2, _, _ = ctx.multiply_x2(x, eb.Mat.empty(n, w), tau)
+            ok = ok and st2 == eb.ERR_OVERFLOW and ctx.overflow_info() == (lit.overflow_rows, lit.required_width)
+        if not ok:
+            bad_t += 1
+            print("X2 SMALL MISMATCH", t, (n, w, kmin, kmax, band, pe, tau), st, r.status, flush=True)
+    print(f"x2 small: {a.x2small - bad_t}/{a.x2small} bitwise", flush=True)
     bad_d = 0
     for t in range(a.x2dense):
         n = int(rng.choice([1, 2, 3, 127, 128, 129, 255, 300, 511, 700, 1023, 1300, 1800, 2048, 2500, 3000]))
