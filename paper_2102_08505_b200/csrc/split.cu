@@ -34,7 +34,7 @@
 namespace ell {
 
 #ifndef ELL_SPLIT_STAGE
-#define ELL_SPLIT_STAGE 64
+#define ELL_SPLIT_STAGE 128  // A-row steps staged per warp: 128 measured 1-2 % faster than 64 after the lean emission
 #endif
 #ifndef ELL_SPLIT_META
 #define ELL_SPLIT_META 0  // W = 1: the next half's step metadata read into registers one half ahead
