@@ -130,7 +130,7 @@ cudaError_t launch_tiny(const RowOpParams& p, int64_t n, unsigned int* counter, 
 // split.cu: the split-row ring kernel (W warps per row, 16-bit balanced sub-records)
 cudaError_t plan_split(const RowOpParams& p, int S, int W, int G, int num_sms, LaunchCfg* cfg);
 cudaError_t launch_split(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s);
-size_t split_row_smem(int S, int W, bool has_old);
+size_t split_row_smem(int S, int W, bool has_old, int G);
 // the warp-specialized ring kernel (accumulator warp + emitter warp per row, W = 1 records)
 cudaError_t plan_ws(const RowOpParams& p, int S, int G, int num_sms, LaunchCfg* cfg);
 cudaError_t launch_ws(const RowOpParams& p, const LaunchCfg& cfg, cudaStream_t s);

@@ -62,12 +62,16 @@ namespace ell {
 #ifndef ELL_SPLIT_MINB_G2
 #define ELL_SPLIT_MINB_G2 6
 #endif
-constexpr int kSplitStage = ELL_SPLIT_STAGE;  // A-row steps staged per warp (16 B each)
+#ifndef ELL_SPLIT_STAGE_G3
+#define ELL_SPLIT_STAGE_G3 160  // G = 3 (cfg5 M = 256): one piece per row (<= 157 steps), 6 rows/SM kept
+#endif
+// A-row steps staged per warp (16 B each), by 64-entry groups per step
+__host__ __device__ constexpr int split_stage(int G) { return G >= 3 ? ELL_SPLIT_STAGE_G3 : ELL_SPLIT_STAGE; }
 constexpr int kSplitTrash = 16;  // trash slots S .. S + 15 (one per bank pair) for padding lanes
 
-__host__ __device__ inline size_t split_smem_bytes(int S, int W, bool has_old) {
-    // acc[S + 16] f64 | stage[W][kSplitStage] 16 B | xcnt[2][4] i32 | rowq[2] i64 | nrm[W] f64 | flags[S] u8
-    return (size_t)(S + kSplitTrash) * 8 + (size_t)W * kSplitStage * 16 + 32 + 16 + (size_t)W * 8 +
+__host__ __device__ inline size_t split_smem_bytes(int S, int W, bool has_old, int G) {
+    // acc[S + 16] f64 | stage[W][split_stage(G)] 16 B | xcnt[2][4] i32 | rowq[2] i64 | nrm[W] f64 | flags[S] u8
+    return (size_t)(S + kSplitTrash) * 8 + (size_t)W * split_stage(G) * 16 + 32 + 16 + (size_t)W * 8 +
            (has_old ? (size_t)S : 0);
 }
 
@@ -413,7 +417,7 @@ __device__ __forceinline__ void row_split(const RowOpParams& p, const SplitSmem<
                                           SplitRow& R, const int32_t* a_col, const double* a_val, int nA,
                                           const int32_t* o_col, const double* o_val, int nOld,
                                           double* __restrict__ crow_v, int32_t* __restrict__ crow_c) {
-    constexpr int kPiece = kSplitStage - 2 * HB + 1;  // real steps per piece
+    constexpr int kPiece = split_stage(G) - 2 * HB + 1;  // real steps per piece
     constexpr int RS = 640 * G;                        // sub-record bytes
     const int S = p.S;
     const int hB = p.hB;
@@ -560,8 +564,8 @@ __global__ void __launch_bounds__(32 * W, W == 1 && G == 1 ? ELL_SPLIT_MINB_G1 :
     const int S = p.S;
     SplitSmem<W> sm;
     sm.acc = (uint32_t)__cvta_generic_to_shared(smem_raw);
-    sm.stg = sm.acc + (uint32_t)((S + kSplitTrash) * 8) + (uint32_t)(wid * kSplitStage * 16);
-    sm.xcnt = sm.acc + (uint32_t)((S + kSplitTrash) * 8 + W * kSplitStage * 16);
+    sm.stg = sm.acc + (uint32_t)((S + kSplitTrash) * 8) + (uint32_t)(wid * split_stage(G) * 16);
+    sm.xcnt = sm.acc + (uint32_t)((S + kSplitTrash) * 8 + W * split_stage(G) * 16);
     sm.rowq = sm.xcnt + 32u;
     sm.nrmx = sm.rowq + 16u;
     sm.flg = sm.nrmx + 8u * W;
@@ -1109,11 +1113,11 @@ static void split_launch_wm(int G, const RowOpParams& p, int grid, size_t smem, 
 
 static int split_mode_of(const RowOpParams& p) { return p.old_mode == 0 ? 0 : (p.normsq ? 2 : 1); }
 
-size_t split_row_smem(int S, int W, bool has_old) { return split_smem_bytes(S, W, has_old); }
+size_t split_row_smem(int S, int W, bool has_old, int G) { return split_smem_bytes(S, W, has_old, G); }
 
 cudaError_t plan_split(const RowOpParams& p, int S, int W, int G, int num_sms, LaunchCfg* cfg) {
     if (S % 128 || W < 1 || W > 2 || G < 1 || G > 4) return cudaErrorInvalidValue;
-    const size_t smem = split_smem_bytes(S, W, p.old_mode != 0);
+    const size_t smem = split_smem_bytes(S, W, p.old_mode != 0, G);
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     int bps = 0;
     const int mode = split_mode_of(p);
