@@ -37,6 +37,9 @@ constexpr int64_t kFastWindowMax = 12288;  // 96 KB + stage per warp
 constexpr int kFastMinRows = 4;            // ring path only with >= 4 rows resident per SM
 constexpr int64_t kGeneralWindow = 1024;
 constexpr int kProbe = 7;  // bandwidth-probe words (launch_bandwidth)
+#ifndef ELL_ROW_CHUNK
+#define ELL_ROW_CHUNK 4  // rows per ticket of the ring kernels (large launches)
+#endif
 constexpr int64_t kNoProbeN = 1024;  // up to this N a row op runs unprobed on one general-path window
 constexpr int64_t kSplitRingMax = 8064;  // split kernel: ring slots (16-bit byte offsets incl. trash)  // measured best for cfg3/cfg4 SP2 (512..4096 swept)
 
@@ -580,7 +583,7 @@ int enqueue_row_op(ellpack_ctx c, RowOpParams& p, int64_t n, const int32_t* bw =
         // launch has fewer than 64 rows per resident warp, where one-row tickets keep the tail short
         const int64_t rows = p.row_end - p.row_begin;
         const int64_t in_flight = split_w ? (int64_t)cfg.grid : total_warps;  // rows being worked on
-        p.row_chunk = rows >= 64 * in_flight ? 4 : 1;
+        p.row_chunk = rows >= 64 * in_flight ? ELL_ROW_CHUNK : 1;
     }
     CK(cudaMemsetAsync(p.row_ticket, 0, 8, c->stream));
     const int pk = c->prof_n < 4 ? c->prof_n : 3;
