@@ -149,7 +149,9 @@ __global__ void __launch_bounds__(128) balance_split_kernel(KMat b, int64_t k0, 
                 if (j >= 0) {
                     const int own = key >> 4;
                     const int NB = 4 * (((own ? n1 : n0) + 63) >> 6);
-                    const int pos = e / NB;
+                    // e / NB for e < 256, NB <= 16 by a float reciprocal: (e + 1/2) / NB is at least
+                    // 1 / 32 from an integer, far above float rounding
+                    const int pos = __float2int_rz(((float)e + 0.5f) * __frcp_rn((float)NB));
                     const int bin = e - pos * NB;
                     const int sl = 64 * (bin >> 2) + 2 * (16 * ((bin >> 1) & 1) + pos) + (bin & 1);
                     int qs = __double2int_rz((double)j * invS);
@@ -167,16 +169,18 @@ __global__ void __launch_bounds__(128) balance_split_kernel(KMat b, int64_t k0, 
         for (int own = 0; own < W; ++own) {
             const int n = own ? n1 : n0;
             const int NB = 4 * ((n + 63) >> 6);
+            const int nq = n / NB, nr = n - nq * NB;  // bin bb holds nq + (bb < nr) real entries
             uint16_t* so = reinterpret_cast<uint16_t*>(rec_s[wi][own]);
             double* sv = reinterpret_cast<double*>(rec_s[wi][own] + 512);
             for (int t = lane; t < NB * 16; t += 32) {
                 const int bb = t >> 4, m = t & 15;
-                const int fill = (n - bb + NB - 1) / NB;
+                const int fill = nq + (bb < nr ? 1 : 0);
                 if (m >= fill) {
                     const int sl = 64 * (bb >> 2) + 2 * (16 * ((bb >> 1) & 1) + m) + (bb & 1);
-                    unsigned f = ~bmask_s[wi][own][bb] & 0xffffu;
-                    for (int q = m - fill; q > 0; --q) f &= f - 1u;
-                    so[sl] = (uint16_t)(8 * (S + ((__ffs(f) - 1 - S) & 15)));
+                    // the (m - fill)-th bank pair no real entry of the bin uses
+                    const unsigned f = ~bmask_s[wi][own][bb] & 0xffffu;
+                    const int r = (int)__fns(f, 0, m - fill + 1);
+                    so[sl] = (uint16_t)(8 * (S + ((r - S) & 15)));
                     sv[sl] = 0.0;
                 }
             }
