@@ -533,21 +533,31 @@ __device__ __forceinline__ void row_split(const RowOpParams& p, const SplitSmem<
     for (int p0 = 0; p0 < nA; p0 += kPiece) {
         const int cnt = min(kPiece, nA - p0);
         const int nh = (cnt + HB - 1) / HB;
-        for (int q = lane; q < (nh + 1) * HB; q += 32) {
-            int k, nb;
-            double a;
-            if (q < cnt) {
-                k = a_col[p0 + q];
-                nb = __ldg(p.bt_nbin + (size_t)k * W + wid);
-                a = a_val[p0 + q];
-            } else {
-                k = a_col[p0 + cnt - 1];
-                nb = 0;
-                a = 0.0;
+        // stage the piece (a_ik, k, NB(k)), null steps after it: every global load of the piece is
+        // issued before the first shared store (an asm store with a memory clobber would otherwise
+        // hold each lane's next loads behind it: ~5 dependent round trips per row)
+        constexpr int NI = (split_stage(G) + 31) / 32;
+        const int lim = (nh + 1) * HB;
+        const int kfill = __ldg(a_col + p0 + cnt - 1);
+        int kq[NI], nbq[NI];
+        double aq[NI];
+#pragma unroll
+        for (int u = 0; u < NI; ++u) {
+            const int q = lane + 32 * u;
+            kq[u] = q < cnt ? __ldg(a_col + p0 + q) : kfill;
+            aq[u] = q < cnt ? __ldg(a_val + p0 + q) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < NI; ++u) nbq[u] = lane + 32 * u < cnt ? __ldg(p.bt_nbin + (size_t)kq[u] * W + wid) : 0;
+#pragma unroll
+        for (int u = 0; u < NI; ++u) {
+            const int q = lane + 32 * u;
+            if (q < lim) {
+                const unsigned long long knb =
+                    (unsigned long long)(uint32_t)kq[u] | ((unsigned long long)(uint32_t)nbq[u] << 32);
+                asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(stg + 16u * q), "l"(__double_as_longlong(aq[u])),
+                             "l"(knb) : "memory");
             }
-            const unsigned long long knb = (unsigned long long)(uint32_t)k | ((unsigned long long)(uint32_t)nb << 32);
-            asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(stg + 16u * q), "l"(__double_as_longlong(a)),
-                         "l"(knb) : "memory");
         }
         __syncwarp();
         if (kMeta) meta(std::integral_constant<int, 0>{}, 0);
