@@ -42,6 +42,9 @@ namespace ell {
 #ifndef ELL_SPLIT_LEAN_EMIT
 #define ELL_SPLIT_LEAN_EMIT 1  // W = 1: emission without per-block diagonal work (round 2)
 #endif
+#ifndef ELL_SPLIT_EMITN
+#define ELL_SPLIT_EMITN 2  // W = 1, no Old, G >= 2: blocks emitted together when that many are pending
+#endif
 #ifndef ELL_SPLIT_CLEAR_STS
 #define ELL_SPLIT_CLEAR_STS 0  // W = 1 lean emission: read + store zero instead of atom.exch
 #endif
@@ -272,7 +275,7 @@ __device__ __forceinline__ void split_merge_old(const RowOpParams& p, const Spli
 // Emit blocks [R.F, Fto) (multiples of 128): per block, this warp's NCH chunks are read and
 // cleared, combined, dropped and ballot-compacted; the block's four chunk counts are exchanged
 // (W > 1) and each warp writes its runs at their place in the row.
-template <int W, int MODE, bool A1>
+template <int W, int MODE, bool A1, int NBK>
 __device__ __forceinline__ void split_emit(const RowOpParams& p, const SplitSmem<W>& sm, int lane, int wid,
                                            SplitRow& R, int Fto, const int32_t* o_col, const double* o_val,
                                            int nOld, double* __restrict__ crow_v, int32_t* __restrict__ crow_c) {
@@ -289,6 +292,39 @@ __device__ __forceinline__ void split_emit(const RowOpParams& p, const SplitSmem
         const bool want_dc = MODE != 0 || p.diag_c != nullptr;
         while (R.F < Fto) {
             const int F = R.F, sF = R.sF;
+            if (MODE == 0 && NBK > 1 && Fto - F >= 128 * NBK && (uint64_t)(R.i - (int64_t)F) >= 128u * NBK) {
+                // NBK blocks without the diagonal (the row's tail after its last k, runs of blocks):
+                // all 4 NBK read-and-clears in flight before the first compare, one latency chain
+                // instead of NBK (each block's stores would otherwise hold the next block's reads)
+                uint32_t bb[NBK];
+                int sFb = sF;
+#pragma unroll
+                for (int b = 0; b < NBK; ++b) {
+                    bb[b] = sm.acc + 8u * (uint32_t)(sFb + lane);
+                    sFb = sFb + 128 == S ? 0 : sFb + 128;
+                }
+                double x[4 * NBK];
+                unsigned m[4 * NBK];
+#pragma unroll
+                for (int t = 0; t < 4 * NBK; ++t) x[t] = lds64_clear(bb[t >> 2] + 256u * (uint32_t)(t & 3));
+#pragma unroll
+                for (int t = 0; t < 4 * NBK; ++t) {
+                    if (!A1) x[t] = __dmul_rn(p.alpha, x[t]);
+                    m[t] = __ballot_sync(FULL, fabs(x[t]) > tau);
+                }
+                uint32_t before = (uint32_t)R.kept;
+#pragma unroll
+                for (int t = 0; t < 4 * NBK; ++t) {
+                    const uint32_t pos = before + (uint32_t)__popc(m[t] & lt);
+                    st_entry(((m[t] >> lane) & 1u) && pos < (uint32_t)cw, reinterpret_cast<double*>(bv + 8ull * pos),
+                             reinterpret_cast<int32_t*>(bc + 4ull * pos), x[t], F + 32 * t + lane);
+                    before += (uint32_t)__popc(m[t]);
+                }
+                R.kept = (int)before;
+                R.F = F + 128 * NBK;
+                R.sF = sFb;
+                continue;
+            }
             const uint32_t di = (uint32_t)(R.i - (int64_t)F);
             const bool dblk = di < 128u;
             if (dblk && lane == (int)(di & 31u)) R.ds = lds64(sm.acc + 8u * (uint32_t)(sF + (int)di));
@@ -404,12 +440,12 @@ __device__ __forceinline__ void split_emit(const RowOpParams& p, const SplitSmem
     }
 }
 
-template <int W, int MODE>
+template <int W, int MODE, int NBK>
 __device__ __forceinline__ void split_emit_to(const RowOpParams& p, const SplitSmem<W>& sm, int lane, int wid,
                                               SplitRow& R, int Fto, const int32_t* o_col, const double* o_val,
                                               int nOld, double* __restrict__ crow_v, int32_t* __restrict__ crow_c) {
-    if (p.alpha == 1.0) split_emit<W, MODE, true>(p, sm, lane, wid, R, Fto, o_col, o_val, nOld, crow_v, crow_c);
-    else split_emit<W, MODE, false>(p, sm, lane, wid, R, Fto, o_col, o_val, nOld, crow_v, crow_c);
+    if (p.alpha == 1.0) split_emit<W, MODE, true, NBK>(p, sm, lane, wid, R, Fto, o_col, o_val, nOld, crow_v, crow_c);
+    else split_emit<W, MODE, false, NBK>(p, sm, lane, wid, R, Fto, o_col, o_val, nOld, crow_v, crow_c);
 }
 
 // One output row, warp `wid` of W: the ring sweep of row_ring (spgemm.cu) over this warp's
@@ -422,6 +458,9 @@ __device__ __forceinline__ void row_split(const RowOpParams& p, const SplitSmem<
                                           const int32_t* o_col, const double* o_val, int nOld,
                                           double* __restrict__ crow_v, int32_t* __restrict__ crow_c) {
     constexpr int kPiece = split_stage(G) - 2 * HB + 1;  // real steps per piece
+    // blocks emitted together in runs (no Old): G = 1 keeps one (the extra registers would cost it
+    // rows per SM: 16 -> 12 measured)
+    constexpr int kEmitBlocks = G >= 2 ? ELL_SPLIT_EMITN : 1;
     constexpr int RS = 640 * G;                        // sub-record bytes
     const int S = p.S;
     const int hB = p.hB;
@@ -513,7 +552,7 @@ __device__ __forceinline__ void row_split(const RowOpParams& p, const SplitSmem<
         }
         if (nb_[0] > 0) sts32i(acc + 8u * (uint32_t)S, (int)ro[X][0][0]);  // touch: waits for this burst
         const int kf = k_[0], kl = k_[HB - 1];
-        if (kf + hB >= R.F + S) split_emit_to<W, MODE>(p, sm, lane, wid, R, (kf - hB) & ~127, o_col, o_val, nOld,
+        if (kf + hB >= R.F + S) split_emit_to<W, MODE, kEmitBlocks>(p, sm, lane, wid, R, (kf - hB) & ~127, o_col, o_val, nOld,
                                                        crow_v, crow_c);
         __syncwarp();
         burst(std::integral_constant<int, X ^ 1>{}, h + 1);
@@ -525,7 +564,7 @@ __device__ __forceinline__ void row_split(const RowOpParams& p, const SplitSmem<
             for (int e = 0; e < HB; ++e) {
                 const int kt = k_[e];
                 if (kt + hB >= R.F + S)
-                    split_emit_to<W, MODE>(p, sm, lane, wid, R, (kt - hB) & ~127, o_col, o_val, nOld, crow_v, crow_c);
+                    split_emit_to<W, MODE, kEmitBlocks>(p, sm, lane, wid, R, (kt - hB) & ~127, o_col, o_val, nOld, crow_v, crow_c);
                 step(X, e, a_[e], nb_[e]);
             }
         }
@@ -567,7 +606,7 @@ __device__ __forceinline__ void row_split(const RowOpParams& p, const SplitSmem<
             if (h + 1 < nh) half(std::integral_constant<int, 1>{}, h + 1);
         }
     }
-    split_emit_to<W, MODE>(p, sm, lane, wid, R, Fend, o_col, o_val, nOld, crow_v, crow_c);
+    split_emit_to<W, MODE, kEmitBlocks>(p, sm, lane, wid, R, Fend, o_col, o_val, nOld, crow_v, crow_c);
 }
 
 template <int W, int G, int HB, int MODE>
