@@ -60,7 +60,7 @@ namespace ell {
 // W = 1: minimum resident CTAs (rows) per SM the register allocation must allow, by groups per step
 // (narrow bands have small rings: registers, not shared memory, cap the rows per SM)
 #ifndef ELL_SPLIT_MINB_G1
-#define ELL_SPLIT_MINB_G1 12
+#define ELL_SPLIT_MINB_G1 16  // 128 registers, no spill: 16 rows/SM at M = 64 (S = 1408)
 #endif
 #ifndef ELL_SPLIT_MINB_G2
 #define ELL_SPLIT_MINB_G2 6
@@ -452,11 +452,16 @@ __device__ __forceinline__ void split_emit_to(const RowOpParams& p, const SplitS
 // sub-records, register bursts of HB steps in a two-half register ring (a half touches its own
 // burst, emits if the sweep would wrap onto unemitted columns, issues the next half's burst,
 // then runs its steps branch-free).
+// c0 / c1: the first / last column of A_i when the caller already has them (c1 < 0: not known).
+// nxt_col / nxt_n: the next row of the caller's chunk (nxt_n <= 0: none): its first and last columns
+// are loaded into nxt_c0 / nxt_c1 before this row's tail emission, which hides their latency.
+// dA: the stored a_ii, read from the staged steps (p.diag_a set).
 template <int W, int G, int HB, int MODE>
 __device__ __forceinline__ void row_split(const RowOpParams& p, const SplitSmem<W>& sm, int lane, int wid,
                                           SplitRow& R, const int32_t* a_col, const double* a_val, int nA,
                                           const int32_t* o_col, const double* o_val, int nOld,
-                                          double* __restrict__ crow_v, int32_t* __restrict__ crow_c) {
+                                          double* __restrict__ crow_v, int32_t* __restrict__ crow_c, int c0, int c1,
+                                          const int32_t* nxt_col, int nxt_n, int& nxt_c0, int& nxt_c1, double& dA) {
     constexpr int kPiece = split_stage(G) - 2 * HB + 1;  // real steps per piece
     // blocks emitted together in runs (no Old): G = 1 keeps one (the extra registers would cost it
     // rows per SM: 16 -> 12 measured)
@@ -467,14 +472,27 @@ __device__ __forceinline__ void row_split(const RowOpParams& p, const SplitSmem<
     const int ncols = (int)p.ncols;
     int lo_col = INT_MAX, hi_col = -1;
     if (nA > 0) {
-        lo_col = max(0, a_col[0] - hB);
-        hi_col = min(ncols - 1, a_col[nA - 1] + hB);
+        if (c1 < 0) {
+            c0 = __ldg(a_col);
+            c1 = __ldg(a_col + nA - 1);
+        }
+        lo_col = max(0, c0 - hB);
+        hi_col = min(ncols - 1, c1 + hB);
     }
     if (MODE != 0 && nOld > 0) {
         lo_col = min(lo_col, o_col[0]);
         hi_col = max(hi_col, o_col[nOld - 1]);
     }
-    if (hi_col < lo_col) return;
+    double da = 0.0;  // this lane's a_ii candidate (one lane at most holds it)
+    bool has_da = false;
+    if (hi_col < lo_col) {
+        if (nxt_n > 0) {
+            nxt_c0 = __ldg(nxt_col);
+            nxt_c1 = __ldg(nxt_col + nxt_n - 1);
+        }
+        dA = 0.0;
+        return;
+    }
     R.F = lo_col & ~127;
     R.sF = R.F % S;
     const int Fend = (hi_col + 128) & ~127;
@@ -588,6 +606,11 @@ __device__ __forceinline__ void row_split(const RowOpParams& p, const SplitSmem<
         }
 #pragma unroll
         for (int u = 0; u < NI; ++u) nbq[u] = lane + 32 * u < cnt ? __ldg(p.bt_nbin + (size_t)kq[u] * W + wid) : 0;
+        if (p.diag_a) {
+#pragma unroll
+            for (int u = 0; u < NI; ++u)
+                if (lane + 32 * u < cnt && kq[u] == (int)R.i) { da = aq[u]; has_da = true; }
+        }
 #pragma unroll
         for (int u = 0; u < NI; ++u) {
             const int q = lane + 32 * u;
@@ -606,7 +629,13 @@ __device__ __forceinline__ void row_split(const RowOpParams& p, const SplitSmem<
             if (h + 1 < nh) half(std::integral_constant<int, 1>{}, h + 1);
         }
     }
+    if (nxt_n > 0) {  // in flight during the tail emission
+        nxt_c0 = __ldg(nxt_col);
+        nxt_c1 = __ldg(nxt_col + nxt_n - 1);
+    }
     split_emit_to<W, MODE, kEmitBlocks>(p, sm, lane, wid, R, Fend, o_col, o_val, nOld, crow_v, crow_c);
+    const unsigned mm = __ballot_sync(FULL, has_da);
+    dA = mm ? __shfl_sync(FULL, da, __ffs(mm) - 1) : 0.0;
 }
 
 template <int W, int G, int HB, int MODE>
@@ -640,10 +669,18 @@ __global__ void __launch_bounds__(32 * W, W == 1 && G == 1 ? ELL_SPLIT_MINB_G1 :
         long long i0;
         asm volatile("ld.shared.s64 %0, [%1];" : "=l"(i0) : "r"(rq) : "memory");
         if (i0 >= p.row_end) break;
-        for (int64_t i = i0; i < i0 + chunk && i < p.row_end; ++i) {
+        // rows of the chunk: the next row's count is loaded one row ahead, its first and last
+        // columns during this row's tail emission (row_split)
+        const int64_t iend = min((int64_t)i0 + chunk, p.row_end);
+        int nA_n = p.alpha != 0.0 ? __ldg(p.A.nnz + i0) : 0;
+        int c0_n = 0, c1_n = -1;
+        for (int64_t i = i0; i < iend; ++i) {
             const double* a_val = p.A.val + (size_t)i * p.A.w;
             const int32_t* a_col = p.A.col + (size_t)i * p.A.w;
-            const int nA = (p.alpha != 0.0) ? p.A.nnz[i] : 0;
+            const int nA = nA_n;
+            const int c0 = c0_n, c1 = c1_n;
+            nA_n = (p.alpha != 0.0 && i + 1 < iend) ? __ldg(p.A.nnz + i + 1) : 0;
+            c1_n = -1;
             const double* o_val = nullptr;
             const int32_t* o_col = nullptr;
             int nOld = 0;
@@ -661,14 +698,8 @@ __global__ void __launch_bounds__(32 * W, W == 1 && G == 1 ? ELL_SPLIT_MINB_G1 :
             R.xbuf = xbuf;
             R.ds = R.dc = R.nrm = 0.0;
             double dA = 0.0;
-            if (p.diag_a && wid == 0) {
-                bool has = false;
-                for (int q = lane; q < nA; q += 32)
-                    if (a_col[q] == (int)i) { dA = a_val[q]; has = true; }
-                const unsigned mm = __ballot_sync(FULL, has);
-                dA = mm ? __shfl_sync(FULL, dA, __ffs(mm) - 1) : 0.0;
-            }
-            row_split<W, G, HB, MODE>(p, sm, lane, wid, R, a_col, a_val, nA, o_col, o_val, nOld, crow_v, crow_c);
+            row_split<W, G, HB, MODE>(p, sm, lane, wid, R, a_col, a_val, nA, o_col, o_val, nOld, crow_v, crow_c, c0, c1,
+                                      p.A.col + (size_t)(i + 1) * p.A.w, nA_n, c0_n, c1_n, dA);
             xbuf = R.xbuf;
             // epilogue: the diagonal values live in the owning warp's lane (x + 0 = x exactly)
             const double ds = warp_sum(R.ds), dc = warp_sum(R.dc);
