@@ -65,6 +65,9 @@ namespace ell {
 #ifndef ELL_SPLIT_MINB_G2
 #define ELL_SPLIT_MINB_G2 6
 #endif
+#ifndef ELL_BAL_ATOMIC_RANK
+#define ELL_BAL_ATOMIC_RANK 1  // balance pass: class ranks by shared atomics, float j mod S
+#endif
 #ifndef ELL_SPLIT_STAGE_G3
 #define ELL_SPLIT_STAGE_G3 160  // G = 3 (cfg5 M = 256): one piece per row (<= 157 steps), 6 rows/SM kept
 #endif
@@ -98,10 +101,14 @@ __global__ void __launch_bounds__(128) balance_split_kernel(KMat b, int64_t k0, 
     __shared__ unsigned bmask_s[4][W][16];                    // per warp, owner, bin: bank pairs used
     __shared__ __align__(16) unsigned char rec_s[4][W][2560];  // per warp, owner: u16[256] | f64[256]
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-    const unsigned lt = (1u << lane) - 1u;
     int* hist = hist_s[wi];
     const size_t rs = (size_t)640 * G;
+#if ELL_BAL_ATOMIC_RANK
+    const float invSf = 1.0f / (float)S;
+#else
+    const unsigned lt = (1u << lane) - 1u;
     const double invS = 1.0 / (double)S;
+#endif
     for (int64_t k = k0 + (int64_t)blockIdx.x * 4 + wi; k < k1; k += (int64_t)gridDim.x * 4) {
         const int nb = b.nnz[k];  // <= 256 on the ring path
         const int32_t* __restrict__ bc = b.col + (size_t)k * b.w;
@@ -117,6 +124,14 @@ __global__ void __launch_bounds__(128) balance_split_kernel(KMat b, int64_t k0, 
             jr[c] = q < nb ? __ldg(bc + q) : -1;
             vr[c] = q < nb ? __ldg(bv + q) : 0.0;
         }
+#if ELL_BAL_ATOMIC_RANK
+        // rank within the (owner, residue) class straight from a shared atomic: no warp collective
+        // inside the (warp-uniform but unprovable) chunk guard. Any rank order within a class is a
+        // valid dealing: each output column's fma chain is fixed by the k order of the steps alone.
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            rk[c] = jr[c] >= 0 ? atomicAdd(&hist[(((jr[c] >> 5) & (W - 1)) << 4) | (jr[c] & 15)], 1) : 0;
+#else
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             rk[c] = 0;
@@ -130,6 +145,7 @@ __global__ void __launch_bounds__(128) balance_split_kernel(KMat b, int64_t k0, 
                 rk[c] = base + __popc(m & lt);
             }
         }
+#endif
         __syncwarp();
         // exclusive prefix over the residues of each owner (16-lane segments); owner totals
         const int h = hist[lane];
@@ -145,7 +161,7 @@ __global__ void __launch_bounds__(128) balance_split_kernel(KMat b, int64_t k0, 
         if (lane < W) bt_nbin[k * W + lane] = 4 * (((lane ? n1 : n0) + 63) >> 6);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-            if (32 * c < nb) {
+            if (ELL_BAL_ATOMIC_RANK || 32 * c < nb) {
                 const int j = jr[c];
                 const int key = j >= 0 ? ((((j >> 5) & (W - 1)) << 4) | (j & 15)) : 0;
                 const int e = __shfl_sync(FULL, pre, key) + rk[c];
@@ -157,7 +173,12 @@ __global__ void __launch_bounds__(128) balance_split_kernel(KMat b, int64_t k0, 
                     const int pos = __float2int_rz(((float)e + 0.5f) * __frcp_rn((float)NB));
                     const int bin = e - pos * NB;
                     const int sl = 64 * (bin >> 2) + 2 * (16 * ((bin >> 1) & 1) + pos) + (bin & 1);
+#if ELL_BAL_ATOMIC_RANK
+                    // j < 2^24 is exact in float; a quotient off by one is corrected below
+                    int qs = __float2int_rz(__int2float_rn(j) * invSf);
+#else
                     int qs = __double2int_rz((double)j * invS);
+#endif
                     int js = j - qs * S;
                     js += js < 0 ? S : 0;
                     js -= js >= S ? S : 0;
@@ -182,7 +203,20 @@ __global__ void __launch_bounds__(128) balance_split_kernel(KMat b, int64_t k0, 
                     const int sl = 64 * (bb >> 2) + 2 * (16 * ((bb >> 1) & 1) + m) + (bb & 1);
                     // the (m - fill)-th bank pair no real entry of the bin uses
                     const unsigned f = ~bmask_s[wi][own][bb] & 0xffffu;
+#if ELL_BAL_ATOMIC_RANK
+                    // the (m - fill)-th set bit of f by a 4-step popcount search (f has >= 16 - fill bits)
+                    int nth = m - fill, r = 0;
+                    unsigned x = f;
+                    int pc = __popc(x & 0xffu);
+                    if (nth >= pc) { nth -= pc; x >>= 8; r += 8; }
+                    pc = __popc(x & 0xfu);
+                    if (nth >= pc) { nth -= pc; x >>= 4; r += 4; }
+                    pc = __popc(x & 0x3u);
+                    if (nth >= pc) { nth -= pc; x >>= 2; r += 2; }
+                    r += (nth >= (int)(x & 1u)) ? 1 : 0;
+#else
                     const int r = (int)__fns(f, 0, m - fill + 1);
+#endif
                     so[sl] = (uint16_t)(8 * (S + ((r - S) & 15)));
                     sv[sl] = 0.0;
                 }
