@@ -92,11 +92,12 @@ __host__ __device__ inline size_t split_smem_bytes(int S, int W, bool has_old, i
 // (b >> 1) & 1 of group b >> 2, parity b & 1; position m in the bin -> slot
 // 64 (b >> 2) + 2 (16 ((b >> 1) & 1) + m) + (b & 1). One lane's two slots of a group are adjacent:
 // one 4-byte index load and one 16-byte value load per lane per group.
-template <int W>
+// NC 32-entry chunks per B row: 2G for W = 1 (nb <= 64 G), 8 for W = 2
+template <int W, int NC>
 __global__ void __launch_bounds__(128) balance_split_kernel(KMat b, int64_t k0, int64_t k1, int G, int S,
                                                             unsigned char* __restrict__ bt,
                                                             int32_t* __restrict__ bt_nbin) {
-    static_assert(W == 1 || W == 2, "W");
+    static_assert((W == 1 || W == 2) && NC >= 1 && NC <= 8, "W, NC");
     __shared__ int hist_s[4][32];                             // per warp: entries per (owner, residue)
     __shared__ unsigned bmask_s[4][W][16];                    // per warp, owner, bin: bank pairs used
     __shared__ __align__(16) unsigned char rec_s[4][W][2560];  // per warp, owner: u16[256] | f64[256]
@@ -116,10 +117,10 @@ __global__ void __launch_bounds__(128) balance_split_kernel(KMat b, int64_t k0, 
         hist[lane] = 0;
         if (lane < W * 16) bmask_s[wi][lane >> 4][lane & 15] = 0u;
         __syncwarp();
-        int jr[8], rk[8];
-        double vr[8];
+        int jr[NC], rk[NC];
+        double vr[NC];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < NC; ++c) {
             const int q = 32 * c + lane;
             jr[c] = q < nb ? __ldg(bc + q) : -1;
             vr[c] = q < nb ? __ldg(bv + q) : 0.0;
@@ -129,11 +130,11 @@ __global__ void __launch_bounds__(128) balance_split_kernel(KMat b, int64_t k0, 
         // inside the (warp-uniform but unprovable) chunk guard. Any rank order within a class is a
         // valid dealing: each output column's fma chain is fixed by the k order of the steps alone.
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
+        for (int c = 0; c < NC; ++c)
             rk[c] = jr[c] >= 0 ? atomicAdd(&hist[(((jr[c] >> 5) & (W - 1)) << 4) | (jr[c] & 15)], 1) : 0;
 #else
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < NC; ++c) {
             rk[c] = 0;
             if (32 * c < nb) {  // warp-uniform
                 const int key = jr[c] >= 0 ? ((((jr[c] >> 5) & (W - 1)) << 4) | (jr[c] & 15)) : 64 + lane;
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(128) balance_split_kernel(KMat b, int64_t k0, 
         pre -= h;
         if (lane < W) bt_nbin[k * W + lane] = 4 * (((lane ? n1 : n0) + 63) >> 6);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < NC; ++c) {
             if (ELL_BAL_ATOMIC_RANK || 32 * c < nb) {
                 const int j = jr[c];
                 const int key = j >= 0 ? ((((j >> 5) & (W - 1)) << 4) | (j & 15)) : 0;
@@ -240,8 +241,11 @@ cudaError_t launch_balance_split(KMat b, int64_t k0, int64_t k1, int W, int G, i
     const int64_t blocks_needed = (k1 - k0 + 3) / 4;
     const int64_t cap = (int64_t)num_sms * 12;
     const unsigned grid = (unsigned)(blocks_needed < cap ? blocks_needed : cap);
-    if (W == 2) balance_split_kernel<2><<<grid, 128, 0, s>>>(b, k0, k1, G, S, bt, bt_nbin);
-    else balance_split_kernel<1><<<grid, 128, 0, s>>>(b, k0, k1, G, S, bt, bt_nbin);
+    if (W == 2) balance_split_kernel<2, 8><<<grid, 128, 0, s>>>(b, k0, k1, G, S, bt, bt_nbin);
+    else if (G == 1) balance_split_kernel<1, 2><<<grid, 128, 0, s>>>(b, k0, k1, G, S, bt, bt_nbin);
+    else if (G == 2) balance_split_kernel<1, 4><<<grid, 128, 0, s>>>(b, k0, k1, G, S, bt, bt_nbin);
+    else if (G == 3) balance_split_kernel<1, 6><<<grid, 128, 0, s>>>(b, k0, k1, G, S, bt, bt_nbin);
+    else balance_split_kernel<1, 8><<<grid, 128, 0, s>>>(b, k0, k1, G, S, bt, bt_nbin);
     return cudaGetLastError();
 }
 
